@@ -1,0 +1,157 @@
+/*
+ * ck32_b200.h — the drop-in C ABI of the B200-native 32-bit RNS-CKKS hot path.
+ *
+ * Replaces the compute bodies behind the reference's C++ evaluator API
+ * (/root/reference/proj/include/ckks32/ckks.hpp, ntt.hpp, bconv.hpp,
+ * automorphism.hpp, poly.hpp).  Plain pointers and sizes only; no torch or
+ * C++ types.  Every entry point cites the reference interface it replaces.
+ *
+ * Data model (mirrors Polynomial, poly.hpp:74-119):
+ *   * a polynomial is `rows x n` uint32 residues, row-major, device memory;
+ *     rows [0, level) are the Q-prefix, then (when present) the alpha P rows;
+ *   * every value is CANONICAL in [0, q) — the reference's correct_lazy()
+ *     view of its signed lazy residues (modarith.hpp:39-43);
+ *   * evaluation-domain polynomials carry the Montgomery factor R = 2^32
+ *     exactly as the reference's (mont flag = true);
+ *   * a ciphertext at level l is `2 x l x n` (b rows then a rows,
+ *     ckks.hpp:61-66); batches of B ciphertexts are contiguous;
+ *   * an evaluation key is `D x 2 x (L+alpha) x n` (digit k: b_k rows then
+ *     a_k rows over the full PQ basis, global row order, ckks.hpp:79-84),
+ *     D = ceil(L / alpha).
+ * All compute calls are asynchronous on the given CUDA stream (NULL = legacy
+ * default stream).  A context is single-threaded like the reference's
+ * CkksContext (its caches are unsynchronised, ckks.hpp:141-144); use one
+ * context per host thread / device.
+ *
+ * Errors: every function returns a ck_status; ck_last_error() returns a
+ * thread-local message.  CK_INVALID_ARGUMENT maps to the reference's
+ * std::invalid_argument, CK_RUNTIME_ERROR to std::runtime_error.
+ */
+#ifndef CK32_B200_H
+#define CK32_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CK_OK = 0,
+  CK_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  CK_RUNTIME_ERROR = 2,    /* std::runtime_error / BasisExhausted */
+  CK_CUDA_ERROR = 3,
+} ck_status;
+
+typedef struct ck_context ck_context;
+typedef void* ck_stream; /* cudaStream_t */
+
+/* CkksParams subset that fixes the residue arithmetic (ckks.hpp:46-54). */
+typedef struct {
+  uint32_t n;          /* ring degree, power of two, 8 <= n <= 2^17 */
+  uint32_t l;          /* number of Q primes (even) */
+  uint32_t alpha;      /* number of P primes (= digit size) */
+  uint32_t delta_bits; /* scale bits used by generate_basis */
+  int32_t lazy_rescale;/* hmult: 0 merged ModDown+rescale, 1 lazy (ckks.cpp:822-863) */
+} ck_params;
+
+const char* ck_last_error(void);
+const char* ck_version(void);
+
+/* CkksContext::CkksContext (ckks.cpp:160-176): generate_basis (rns.cpp:63-117)
+ * + build_twiddles (ntt.cpp:100-135) + P mod q (ckks.cpp:171-175), uploaded to
+ * `device`.  primes == NULL generates the basis; otherwise l+alpha primes (Q then
+ * P, e.g. from deserialize_basis, rns.cpp:189-216) are used verbatim. */
+ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int device, ck_context** out);
+ck_status ck_context_destroy(ck_context* ctx);
+/* generate_basis (rns.cpp:63-117) on the host only: l Q primes then alpha P
+ * primes, identical to the reference's deterministic choice. */
+ck_status ck_generate_basis(uint32_t n, uint32_t l, uint32_t alpha, uint32_t delta_bits, uint32_t* primes_out);
+/* RnsBasis q_primes then p_primes (rns.hpp:23-40) */
+ck_status ck_context_primes(const ck_context* ctx, uint32_t* primes_out);
+/* OpCounters (ckks.hpp:34-44): modup, moddown, ntt, intt, keymult, bconv, rescale */
+ck_status ck_context_counters(const ck_context* ctx, uint64_t counters_out[7]);
+ck_status ck_context_reset_counters(ck_context* ctx);
+
+/* Device memory helpers for callers without their own allocator. */
+ck_status ck_malloc(ck_context* ctx, size_t bytes, void** dptr);
+ck_status ck_free(ck_context* ctx, void* dptr);
+ck_status ck_memcpy_h2d(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream);
+ck_status ck_memcpy_d2h(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream);
+ck_status ck_stream_sync(ck_context* ctx, ck_stream stream);
+
+/* ---- kernel-level entry points ------------------------------------------ */
+/* ntt_forward (ntt.cpp:288-299) over `rows` rows in place; gidx[i] = global
+ * prime index of row i (poly.hpp:103-106), host array.  Input coefficient
+ * domain (plain), output evaluation domain (Montgomery). */
+ck_status ck_ntt_forward(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
+                         ck_stream stream);
+/* intt_inverse (ntt.cpp:301-312) / NttPlan::inverse_row with the fused part-1
+ * epilogue (ntt.hpp:72-73): epilogue_mont[i] (host, canonical Montgomery form)
+ * or NULL. */
+ck_status ck_intt_inverse(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
+                          const uint32_t* epilogue_mont, ck_stream stream);
+/* make_bconv_table + bconv_part2 (bconv.cpp:13-46, 96-174): src is src_count
+ * contiguous canonical rows (coefficient domain), dst dst_count rows. */
+ck_status ck_bconv(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,
+                   uint32_t* dst_dev, uint32_t dst_count, const uint32_t* dst_gidx, ck_stream stream);
+/* apply_automorphism, evaluation domain (automorphism.cpp:76-100), rotation r */
+ck_status ck_automorphism(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t rows, int64_t r,
+                          ck_stream stream);
+/* ew_add / ew_sub / ew_mul over Q-prefix rows (poly.cpp:146-164) */
+ck_status ck_ew_add(ck_context* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t rows,
+                    ck_stream stream);
+ck_status ck_ew_sub(ck_context* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t rows,
+                    ck_stream stream);
+ck_status ck_ew_mul(ck_context* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t rows,
+                    ck_stream stream);
+
+/* ---- mechanisms (ckks.hpp:172-208) --------------------------------------- */
+/* mod_up (ckks.cpp:680-731): d = level rows -> hoist D(level) x (level+alpha) rows.
+ * Digit rows of each extension are the input rows (pass-through). */
+ck_status ck_mod_up(ck_context* ctx, uint32_t level, const uint32_t* d, uint32_t* hoist, ck_stream stream);
+/* key_mult (ckks.cpp:733-770): v = [v0; v1], each level+alpha rows. */
+ck_status ck_key_mult(ck_context* ctx, uint32_t level, const uint32_t* hoist, const uint32_t* evk, uint32_t* v,
+                      ck_stream stream);
+/* mod_down (ckks.cpp:772-776): v (level+alpha rows) -> level rows. */
+ck_status ck_mod_down(ck_context* ctx, uint32_t level, const uint32_t* v, uint32_t* out, ck_stream stream);
+/* key_switch (ckks.cpp:778-787): d (level rows) -> [c0; c1] (2 x level rows). */
+ck_status ck_key_switch(ck_context* ctx, uint32_t level, const uint32_t* d, const uint32_t* evk, uint32_t* out,
+                        ck_stream stream);
+/* rescale (ckks.cpp:789-802), batched: ct [B][2][level] -> out [B][2][level-2]. */
+ck_status ck_rescale(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, uint32_t* out,
+                     ck_stream stream);
+/* hmult (ckks.cpp:804-865), batched over B ciphertext pairs sharing one relin key:
+ * x, y [B][2][level] -> out [B][2][level-2] (merged) or [B][2][level] (lazy_rescale). */
+ck_status ck_hmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* x, const uint32_t* y,
+                   const uint32_t* relin_evk, uint32_t* out, ck_stream stream);
+/* hrot (ckks.cpp:890-897), batched over B ciphertexts sharing one rotation key. */
+ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, int64_t r,
+                  const uint32_t* rot_evk, uint32_t* out, ck_stream stream);
+/* hadd / padd / pmult element-wise parts (ckks.cpp:557-600), batched:
+ * ct [B][2][level]; pt [level] (shared by the batch). */
+ck_status ck_hadd(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* x, const uint32_t* y,
+                  uint32_t* out, ck_stream stream);
+ck_status ck_padd(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, const uint32_t* pt,
+                  uint32_t* out, ck_stream stream);
+ck_status ck_pmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, const uint32_t* pt,
+                   uint32_t* out, ck_stream stream);
+/* hoisted_rotations (ckks.cpp:899-925): one ModUp shared by `count` rotations;
+ * out [count][2][level]; evks[i] ignored (identity) when rots[i] == 0. */
+ck_status ck_hoisted_rotations(ck_context* ctx, uint32_t level, const uint32_t* ct, uint32_t count,
+                               const int64_t* rots, const uint32_t* const* evks, uint32_t* out, ck_stream stream);
+/* hoisted_rotate_accumulate (ckks.cpp:945-1012): sum_i pt_i * rot_{r_i}(ct) with
+ * one ModUp and one ModDown; pts[i] are P-extended (level+alpha rows). */
+ck_status ck_hoisted_rotate_accumulate(ck_context* ctx, uint32_t level, const uint32_t* ct, uint32_t count,
+                                       const int64_t* rots, const uint32_t* const* pts,
+                                       const uint32_t* const* evks, uint32_t* out, ck_stream stream);
+
+/* Number of this library's kernel launches issued since context creation
+ * (evidence for bench.py's gpu_launches). */
+uint64_t ck_launch_count(const ck_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CK32_B200_H */

@@ -1,0 +1,457 @@
+"""Python mirror of the reference evaluator API (ckks.hpp:102-219) over the
+B200 C-ABI (include/ck32_b200.h).
+
+Names, argument meaning, level/scale ledger and error behaviour follow the
+reference: ``std::invalid_argument`` becomes ``ValueError``.  Residues live on
+the GPU as int32 tensors holding canonical values in [0, q) (bit-identical to
+the reference's ``correct_lazy`` view); every compute call goes through the
+native library — there is no host fallback.
+
+Batching: any Ciphertext may carry a leading batch dimension
+(``data`` of shape ``[B, 2, level, n]``); hmult / hrot / rescale / hadd /
+padd / pmult process the whole batch in one launch sequence with the key
+streamed once.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+COEFFICIENT, EVALUATION = "coefficient", "evaluation"
+RELIN, ROTATION = "relin", "rotation"
+COUNTER_NAMES = ("modup", "moddown", "ntt", "intt", "keymult", "bconv", "rescale")  # ckks.hpp:34-44
+
+
+@dataclass
+class CkksParams:
+    """ckks.hpp:46-54 (hamming / sigma only matter for host-side key sampling)."""
+    n: int = 1 << 16
+    l: int = 54
+    alpha: int = 14
+    delta_bits: int = 48
+    hamming: int = 256
+    sigma: float = 3.2
+    lazy_rescale: bool = False
+
+
+def _ptr(t: torch.Tensor) -> int:
+    if not t.is_cuda:
+        raise ValueError("tensor must live on the GPU")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+class CkksContext:
+    """CkksContext (ckks.cpp:160-176): basis, twiddles and per-level tables
+    on one device."""
+
+    def __init__(self, params: CkksParams, device: int = 0, primes: Optional[Sequence[int]] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("ck32-b200 needs a CUDA device (no CPU fallback)")
+        self.params = params
+        self.device = torch.device("cuda", device)
+        p = nat.ck_params(params.n, params.l, params.alpha, params.delta_bits, int(params.lazy_rescale))
+        h = ctypes.c_void_p()
+        arr = nat.u32_array(primes) if primes is not None else None
+        with torch.cuda.device(self.device):
+            nat.call("ck_context_create", ctypes.byref(p), arr, device, ctypes.byref(h))
+        self._h = h
+        out = (ctypes.c_uint32 * (params.l + params.alpha))()
+        nat.call("ck_context_primes", h, out)
+        self.primes = np.array(list(out), dtype=np.uint32)
+        self.q_primes = self.primes[: params.l]
+        self.p_primes = self.primes[params.l:]
+
+    # ---------------------------------------------------------------- misc --
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n(self) -> int:
+        return self.params.n
+
+    @property
+    def slots(self) -> int:
+        return self.params.n // 2
+
+    def num_digits(self, level: int) -> int:
+        return (level + self.params.alpha - 1) // self.params.alpha
+
+    def default_scale(self) -> Fraction:
+        return Fraction(1 << self.params.delta_bits)
+
+    def stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def counters(self) -> dict:
+        out = (ctypes.c_uint64 * 7)()
+        nat.call("ck_context_counters", self._h, out)
+        return dict(zip(COUNTER_NAMES, list(out)))
+
+    def reset_counters(self) -> None:
+        nat.call("ck_context_reset_counters", self._h)
+
+    def launch_count(self) -> int:
+        return int(nat.lib().ck_launch_count(self._h))
+
+    def gidx(self, level: int, p_rows: int = 0) -> np.ndarray:
+        return np.concatenate([np.arange(level), self.params.l + np.arange(p_rows)]).astype(np.uint32)
+
+    def empty(self, *shape) -> torch.Tensor:
+        return torch.empty(shape, dtype=torch.int32, device=self.device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            torch.cuda.synchronize(self.device)
+            nat.call("ck_context_destroy", self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------- types --
+@dataclass
+class Polynomial:
+    """poly.hpp:74-119: rows x n residues, Q-prefix rows then P rows."""
+    data: torch.Tensor
+    q_count: int
+    p_count: int = 0
+    domain: str = EVALUATION
+    mont: bool = True
+
+    @property
+    def rows(self) -> int:
+        return self.q_count + self.p_count
+
+    def clone(self) -> "Polynomial":
+        return Polynomial(self.data.clone(), self.q_count, self.p_count, self.domain, self.mont)
+
+
+@dataclass
+class Plaintext:
+    poly: Polynomial
+    scale: Fraction
+    level: int
+
+
+@dataclass
+class Ciphertext:
+    """ckks.hpp:61-66; data is [2, level, n] (b, a) or [B, 2, level, n]."""
+    data: torch.Tensor
+    scale: Fraction
+    level: int
+    pending_rescale: bool = False
+
+    @property
+    def batched(self) -> bool:
+        return self.data.dim() == 4
+
+    @property
+    def batch(self) -> int:
+        return self.data.shape[0] if self.batched else 1
+
+    @property
+    def b(self) -> torch.Tensor:
+        return self.data[..., 0, :, :]
+
+    @property
+    def a(self) -> torch.Tensor:
+        return self.data[..., 1, :, :]
+
+
+@dataclass
+class EvaluationKey:
+    """ckks.hpp:79-84; data is [D, 2, L+alpha, n] over the full PQ basis."""
+    data: torch.Tensor
+    kind: str = RELIN
+    rotation: int = 0
+
+
+@dataclass
+class HoistState:
+    """ckks.hpp:88-91: D ModUp-extended digits over (level + alpha) rows."""
+    level: int
+    digits: torch.Tensor  # [D, level + alpha, n]
+
+
+# ------------------------------------------------------------------ checks --
+def _check_pair(ctx: CkksContext, ct: Ciphertext) -> None:  # ckks.cpp:122-129
+    shape = ct.data.shape[-3:]
+    if tuple(shape) != (2, ct.level, ctx.n):
+        raise ValueError("ciphertext level/shape mismatch")
+    if ct.level < 1 or ct.level > ctx.params.l:
+        raise ValueError("ciphertext level/shape mismatch")
+
+
+def _check_same_scale(a: Fraction, b: Fraction) -> None:  # ckks.cpp:131-136
+    if abs(a - b) * (1 << 40) > a:
+        raise ValueError("scale mismatch beyond tolerance")
+
+
+def _check_eval_mont(p: Polynomial, what: str) -> None:  # ckks.cpp:115-120
+    if p.domain != EVALUATION or not p.mont:
+        raise ValueError(f"{what}: expected evaluation-domain Montgomery form")
+
+
+def _flushed(ctx: CkksContext, ct: Ciphertext) -> Ciphertext:  # ckks.cpp:664-676
+    return rescale(ctx, ct) if ct.pending_rescale else ct
+
+
+def _qq(ctx: CkksContext, level: int) -> int:
+    return int(ctx.q_primes[level - 2]) * int(ctx.q_primes[level - 1])
+
+
+# ------------------------------------------------------- element-wise ops --
+def hadd(ctx: CkksContext, x: Ciphertext, y: Ciphertext) -> Ciphertext:  # ckks.cpp:557-571
+    _check_pair(ctx, x)
+    _check_pair(ctx, y)
+    if x.level != y.level:
+        raise ValueError("level mismatch")
+    if x.pending_rescale != y.pending_rescale:
+        raise ValueError("pending-rescale state mismatch")
+    _check_same_scale(x.scale, y.scale)
+    if x.data.shape != y.data.shape:
+        raise ValueError("batch mismatch")
+    out = torch.empty_like(x.data)
+    nat.call("ck_hadd", ctx.handle, x.level, x.batch, _ptr(x.data), _ptr(y.data), _ptr(out), ctx.stream())
+    return Ciphertext(out, x.scale, x.level, x.pending_rescale)
+
+
+def _pt_check(ctx, ct, pt, what):
+    _check_pair(ctx, ct)
+    _check_eval_mont(pt.poly, what)
+    if ct.level != pt.level or pt.poly.p_count != 0:
+        raise ValueError("level mismatch")
+
+
+def padd(ctx: CkksContext, ct: Ciphertext, pt: Plaintext) -> Ciphertext:  # ckks.cpp:573-584
+    _pt_check(ctx, ct, pt, "padd")
+    _check_same_scale(ct.scale, pt.scale)
+    out = torch.empty_like(ct.data)
+    nat.call("ck_padd", ctx.handle, ct.level, ct.batch, _ptr(ct.data), _ptr(pt.poly.data), _ptr(out), ctx.stream())
+    return Ciphertext(out, ct.scale, ct.level, ct.pending_rescale)
+
+
+def pmult(ctx: CkksContext, ct: Ciphertext, pt: Plaintext) -> Ciphertext:  # ckks.cpp:586-600
+    _pt_check(ctx, ct, pt, "pmult")
+    out = torch.empty_like(ct.data)
+    nat.call("ck_pmult", ctx.handle, ct.level, ct.batch, _ptr(ct.data), _ptr(pt.poly.data), _ptr(out), ctx.stream())
+    return Ciphertext(out, ct.scale * pt.scale, ct.level, ct.pending_rescale)
+
+
+# ------------------------------------------------------------- mechanisms --
+def rescale(ctx: CkksContext, ct: Ciphertext) -> Ciphertext:  # ckks.cpp:789-802
+    _check_pair(ctx, ct)
+    l = ct.level
+    if l < 4:
+        raise ValueError("level exhausted")
+    shape = list(ct.data.shape)
+    shape[-2] = l - 2
+    out = torch.empty(shape, dtype=torch.int32, device=ctx.device)
+    nat.call("ck_rescale", ctx.handle, l, ct.batch, _ptr(ct.data), _ptr(out), ctx.stream())
+    return Ciphertext(out, ct.scale / _qq(ctx, l), l - 2, False)
+
+
+def mod_up(ctx: CkksContext, d: Polynomial) -> HoistState:  # ckks.cpp:680-731
+    _check_eval_mont(d, "mod_up")
+    if d.p_count != 0:
+        raise ValueError("mod_up input must be Q-only")
+    l = d.q_count
+    out = ctx.empty(ctx.num_digits(l), l + ctx.params.alpha, ctx.n)
+    nat.call("ck_mod_up", ctx.handle, l, _ptr(d.data), _ptr(out), ctx.stream())
+    return HoistState(l, out)
+
+
+def key_mult(ctx: CkksContext, hoist: HoistState, evk: EvaluationKey) -> Tuple[Polynomial, Polynomial]:
+    """ckks.cpp:733-770"""
+    if evk.data.shape[0] < hoist.digits.shape[0]:
+        raise ValueError("evaluation key has too few digits")
+    l, a = hoist.level, ctx.params.alpha
+    v = ctx.empty(2, l + a, ctx.n)
+    nat.call("ck_key_mult", ctx.handle, l, _ptr(hoist.digits), _ptr(evk.data), _ptr(v), ctx.stream())
+    return Polynomial(v[0], l, a), Polynomial(v[1], l, a)
+
+
+def mod_down(ctx: CkksContext, v: Polynomial) -> Polynomial:  # ckks.cpp:772-776
+    if v.p_count != ctx.params.alpha:
+        raise ValueError("mod_down expects a P-extended polynomial")
+    out = ctx.empty(v.q_count, ctx.n)
+    nat.call("ck_mod_down", ctx.handle, v.q_count, _ptr(v.data.contiguous()), _ptr(out), ctx.stream())
+    return Polynomial(out, v.q_count, 0)
+
+
+def key_switch(ctx: CkksContext, d: Polynomial, evk: EvaluationKey) -> Tuple[Polynomial, Polynomial]:
+    """ckks.cpp:778-787"""
+    _check_eval_mont(d, "mod_up")
+    if d.p_count != 0:
+        raise ValueError("mod_up input must be Q-only")
+    l = d.q_count
+    out = ctx.empty(2, l, ctx.n)
+    nat.call("ck_key_switch", ctx.handle, l, _ptr(d.data), _ptr(evk.data), _ptr(out), ctx.stream())
+    return Polynomial(out[0], l), Polynomial(out[1], l)
+
+
+def hmult(ctx: CkksContext, x_in: Ciphertext, y_in: Ciphertext, relin: EvaluationKey) -> Ciphertext:
+    """ckks.cpp:804-865 (merged ModDown+rescale unless params.lazy_rescale)."""
+    if relin.kind != RELIN:
+        raise ValueError("hmult needs a relinearization key")
+    x, y = _flushed(ctx, x_in), _flushed(ctx, y_in)
+    _check_pair(ctx, x)
+    _check_pair(ctx, y)
+    if x.level != y.level:
+        raise ValueError("level mismatch")
+    l = x.level
+    if l < 4:
+        raise ValueError("level exhausted")
+    if x.data.shape != y.data.shape:
+        raise ValueError("batch mismatch")
+    lazy = ctx.params.lazy_rescale
+    shape = list(x.data.shape)
+    shape[-2] = l if lazy else l - 2
+    out = torch.empty(shape, dtype=torch.int32, device=ctx.device)
+    nat.call("ck_hmult", ctx.handle, l, x.batch, _ptr(x.data), _ptr(y.data), _ptr(relin.data), _ptr(out),
+             ctx.stream())
+    if lazy:
+        return Ciphertext(out, x.scale * y.scale, l, True)
+    return Ciphertext(out, x.scale * y.scale / _qq(ctx, l), l - 2, False)
+
+
+def hrot(ctx: CkksContext, ct_in: Ciphertext, r: int, evk: EvaluationKey) -> Ciphertext:  # ckks.cpp:890-897
+    ct = _flushed(ctx, ct_in)
+    _check_pair(ctx, ct)
+    if evk.kind != ROTATION or evk.rotation != r:
+        raise ValueError("rotation key mismatch")
+    out = torch.empty_like(ct.data)
+    nat.call("ck_hrot", ctx.handle, ct.level, ct.batch, _ptr(ct.data), int(r), _ptr(evk.data), _ptr(out),
+             ctx.stream())
+    return Ciphertext(out, ct.scale, ct.level, False)
+
+
+def hoisted_rotations(ctx: CkksContext, ct_in: Ciphertext, rotations: Sequence[int],
+                      evks: Sequence[Optional[EvaluationKey]]) -> List[Ciphertext]:
+    """ckks.cpp:899-925: one ModUp shared across rotations."""
+    if len(rotations) != len(evks):
+        raise ValueError("rotation/key count mismatch")
+    ct = _flushed(ctx, ct_in)
+    _check_pair(ctx, ct)
+    if ct.batched:
+        raise ValueError("hoisted rotations take one ciphertext")
+    for r, k in zip(rotations, evks):
+        if r != 0 and (k is None or k.kind != ROTATION or k.rotation != r):
+            raise ValueError("rotation key mismatch")
+    cnt = len(rotations)
+    out = ctx.empty(cnt, 2, ct.level, ctx.n)
+    rots = (ctypes.c_int64 * max(cnt, 1))(*[int(r) for r in rotations])
+    keys = (ctypes.c_void_p * max(cnt, 1))(*[(_ptr(k.data) if (k is not None and r != 0) else None)
+                                             for r, k in zip(rotations, evks)])
+    nat.call("ck_hoisted_rotations", ctx.handle, ct.level, _ptr(ct.data), cnt, rots, keys, _ptr(out), ctx.stream())
+    return [Ciphertext(out[i], ct.scale, ct.level, False) for i in range(cnt)]
+
+
+def hoisted_rotate_accumulate(ctx: CkksContext, ct_in: Ciphertext, rotations: Sequence[int],
+                              pts: Sequence[Plaintext], evks: Sequence[Optional[EvaluationKey]]) -> Ciphertext:
+    """ckks.cpp:945-1012: sum_k pt_k * rot_k(ct) with one ModUp and one ModDown."""
+    if not rotations or len(rotations) != len(pts) or len(rotations) != len(evks):
+        raise ValueError("rotation/plaintext/key count mismatch")
+    ct = _flushed(ctx, ct_in)
+    _check_pair(ctx, ct)
+    l, a = ct.level, ctx.params.alpha
+    for pt in pts:
+        _check_eval_mont(pt.poly, "hoisted accumulate")
+        if pt.level != l or pt.poly.p_count != a:
+            raise ValueError("plaintexts must be P-extended at the ciphertext level")
+        _check_same_scale(pts[0].scale, pt.scale)
+    for r, k in zip(rotations, evks):
+        if r != 0 and (k is None or k.kind != ROTATION or k.rotation != r):
+            raise ValueError("rotation key mismatch")
+    cnt = len(rotations)
+    out = ctx.empty(2, l, ctx.n)
+    rots = (ctypes.c_int64 * cnt)(*[int(r) for r in rotations])
+    pp = (ctypes.c_void_p * cnt)(*[_ptr(p.poly.data) for p in pts])
+    kp = (ctypes.c_void_p * cnt)(*[(_ptr(k.data) if (k is not None and r != 0) else None)
+                                   for r, k in zip(rotations, evks)])
+    nat.call("ck_hoisted_rotate_accumulate", ctx.handle, l, _ptr(ct.data), cnt, rots, pp, kp, _ptr(out),
+             ctx.stream())
+    return Ciphertext(out, ct.scale * pts[0].scale, l, False)
+
+
+# ----------------------------------------------------------- kernel level --
+def ntt_forward(ctx: CkksContext, p: Polynomial) -> Polynomial:  # ntt.cpp:288-299
+    if p.domain != COEFFICIENT:
+        raise ValueError("ntt_forward expects coefficient domain")
+    if p.mont:
+        raise ValueError("ntt_forward expects plain form (entry merge)")
+    g = nat.u32_array(ctx.gidx(p.q_count, p.p_count))
+    nat.call("ck_ntt_forward", ctx.handle, _ptr(p.data), p.rows, g, ctx.stream())
+    p.domain, p.mont = EVALUATION, True
+    return p
+
+
+def intt_inverse(ctx: CkksContext, p: Polynomial, epilogue_mont: Optional[Sequence[int]] = None) -> Polynomial:
+    """ntt.cpp:301-312 (+ the fused part-1 epilogue of NttPlan::inverse_row)."""
+    if p.domain != EVALUATION:
+        raise ValueError("intt_inverse expects evaluation domain")
+    if not p.mont:
+        raise ValueError("intt_inverse expects Montgomery form")
+    g = nat.u32_array(ctx.gidx(p.q_count, p.p_count))
+    e = nat.u32_array(epilogue_mont) if epilogue_mont is not None else None
+    nat.call("ck_intt_inverse", ctx.handle, _ptr(p.data), p.rows, g, e, ctx.stream())
+    p.domain, p.mont = COEFFICIENT, False
+    return p
+
+
+def bconv(ctx: CkksContext, src: torch.Tensor, src_gidx: Sequence[int], dst_gidx: Sequence[int]) -> torch.Tensor:
+    """make_bconv_table + bconv_part2 (bconv.cpp:13-46, 96-174)."""
+    out = ctx.empty(len(dst_gidx), ctx.n)
+    nat.call("ck_bconv", ctx.handle, _ptr(src), len(src_gidx), nat.u32_array(src_gidx), _ptr(out), len(dst_gidx),
+             nat.u32_array(dst_gidx), ctx.stream())
+    return out
+
+
+def apply_automorphism(ctx: CkksContext, p: Polynomial, r: int) -> Polynomial:  # automorphism.cpp:76-100
+    if p.domain != EVALUATION:
+        raise ValueError("only the evaluation-domain gather is implemented on the GPU")
+    out = torch.empty_like(p.data)
+    nat.call("ck_automorphism", ctx.handle, _ptr(p.data), _ptr(out), p.rows, int(r), ctx.stream())
+    return Polynomial(out, p.q_count, p.p_count, p.domain, p.mont)
+
+
+def ew_add(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:
+    return _ew(ctx, "ck_ew_add", a, b, a.mont)
+
+
+def ew_sub(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:
+    return _ew(ctx, "ck_ew_sub", a, b, a.mont)
+
+
+def ew_mul(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:
+    if not a.mont or not b.mont:
+        raise ValueError("ew_mul expects Montgomery-form operands")
+    return _ew(ctx, "ck_ew_mul", a, b, True)
+
+
+def _ew(ctx, fn, a: Polynomial, b: Polynomial, mont_out: bool) -> Polynomial:  # poly.cpp:138-164
+    if a.q_count != b.q_count or a.p_count != b.p_count:
+        raise ValueError("basis prefix mismatch")
+    if a.domain != b.domain:
+        raise ValueError("domain mismatch")
+    if a.mont != b.mont:
+        raise ValueError("Montgomery flag mismatch")
+    if a.p_count:
+        raise ValueError("element-wise kernels take Q-prefix polynomials")
+    out = torch.empty_like(a.data)
+    nat.call(fn, ctx.handle, _ptr(a.data), _ptr(b.data), _ptr(out), a.rows, ctx.stream())
+    return Polynomial(out, a.q_count, a.p_count, a.domain, mont_out)

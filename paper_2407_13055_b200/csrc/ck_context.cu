@@ -1,0 +1,1229 @@
+// Host runtime of ck32-b200: basis and table generation, per-level plans,
+// mechanism orchestration and the extern "C" ABI declared in
+// include/ck32_b200.h.
+//
+// Host-side table math restates the reference (rns.cpp:63-117 basis,
+// modarith.cpp:30-54 roots/Montgomery constants, ntt.cpp:100-135 twiddles,
+// bconv.cpp:13-46 conversion tables, ckks.cpp:188-265 per-level tables) with
+// machine-word modular arithmetic: (P/P_j) mod q is the product of the other
+// source primes reduced mod q, so no big integers are needed.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/ck32_b200.h"
+#include "ck_common.cuh"
+#include "ck_kernels.h"
+
+namespace ck {
+namespace {
+
+thread_local std::string g_err;
+
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------ modular math --
+uint64_t pow_mod(uint64_t b, uint64_t e, uint64_t m) {
+  unsigned __int128 acc = 1 % m;
+  b %= m;
+  while (e) {
+    if (e & 1) acc = acc * b % m;
+    b = (uint64_t)((unsigned __int128)b * b % m);
+    e >>= 1;
+  }
+  return (uint64_t)acc;
+}
+uint32_t mulm(uint32_t a, uint32_t b, uint32_t q) { return (uint32_t)((uint64_t)a * b % q); }
+uint32_t invm(uint32_t a, uint32_t q) { return (uint32_t)pow_mod(a, q - 2, q); }
+uint32_t shoup(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
+uint32_t r_mod(uint32_t q) { return (uint32_t)((1ull << 32) % q); }
+uint32_t to_mont(uint32_t a, uint32_t q) { return (uint32_t)(((uint64_t)a << 32) % q); }
+uint32_t bit_reverse(uint32_t x, uint32_t bits) {
+  uint32_t r = 0;
+  for (uint32_t i = 0; i < bits; ++i) r |= ((x >> i) & 1u) << (bits - 1 - i);
+  return r;
+}
+
+// Deterministic Miller-Rabin (modarith.cpp:7-28).
+bool is_prime(uint64_t v) {
+  static const uint64_t bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (v < 2) return false;
+  for (uint64_t p : bases)
+    if (v % p == 0) return v == p;
+  uint64_t d = v - 1;
+  int s = 0;
+  while ((d & 1) == 0) d >>= 1, ++s;
+  for (uint64_t a : bases) {
+    uint64_t x = pow_mod(a, d, v);
+    if (x == 1 || x == v - 1) continue;
+    bool composite = true;
+    for (int i = 1; i < s; ++i) {
+      x = (uint64_t)((unsigned __int128)x * x % v);
+      if (x == v - 1) {
+        composite = false;
+        break;
+      }
+    }
+    if (composite) return false;
+  }
+  return true;
+}
+
+// First g >= 2 whose (q-1)/2N power has order 2N (modarith.cpp:30-40): the
+// exact root choice fixes the evaluation-point order, so it is parity-critical.
+uint32_t find_root_2n(uint32_t q, uint32_t n) {
+  const uint64_t order = 2ull * n;
+  if ((q - 1) % order != 0) throw InvalidArgument("q not NTT-friendly for n");
+  const uint64_t cof = (q - 1) / order;
+  for (uint64_t g = 2; g < q; ++g) {
+    const uint64_t cand = pow_mod(g, cof, q);
+    if (pow_mod(cand, n, q) == q - 1) return (uint32_t)cand;
+  }
+  throw std::runtime_error("no primitive 2N-th root found");
+}
+
+// Largest primes = 1 mod 2n below `top`, descending (rns.cpp:10-20).
+std::vector<uint32_t> scan_down(uint64_t top, uint64_t two_n, size_t count, uint64_t stop_at = 0) {
+  std::vector<uint32_t> out;
+  uint64_t k = (top - 1) / two_n * two_n + 1;
+  if (k >= top) k -= two_n;
+  for (; k > two_n && k > stop_at && out.size() < count; k -= two_n)
+    if (is_prime(k)) out.push_back((uint32_t)k);
+  return out;
+}
+
+// generate_basis (rns.cpp:63-117): Q primes in delta groups, worst-matched
+// groups first; P primes the largest admissible below the cap.
+std::vector<uint32_t> generate_basis(uint32_t n, uint32_t l, uint32_t alpha, uint32_t db) {
+  if (n == 0 || (n & (n - 1)) != 0) throw InvalidArgument("n must be a power of two");
+  if (l == 0 || l % 2 != 0) throw InvalidArgument("l must be positive and even");
+  const uint64_t two_n = 2ull * n;
+  const uint64_t cap = std::min<uint64_t>(1ull << 29, (1ull << 32) / std::max<uint32_t>(alpha + 2, 3));
+  const uint64_t slots = cap > two_n ? (cap - two_n) / two_n : 0;
+  if (slots < l + alpha) throw std::runtime_error("prime window smaller than requested prime count");
+  auto p_list = scan_down(cap, two_n, alpha);
+  if (p_list.size() < alpha) throw std::runtime_error("too few auxiliary primes");
+  const uint64_t p_min = alpha ? p_list.back() : cap;
+  uint64_t q_top = std::min<uint64_t>(cap, (uint64_t)std::sqrt(std::ldexp(1.0, (int)db + 1)));
+  q_top = std::min(q_top, p_min);
+  auto cands = scan_down(q_top, two_n, l);
+  if (cands.size() < l) {
+    auto extra = scan_down(p_min, two_n, (size_t)-1, q_top - 1);
+    cands.insert(cands.end(), extra.begin(), extra.end());
+  }
+  std::sort(cands.begin(), cands.end());
+  cands.erase(std::unique(cands.begin(), cands.end()), cands.end());
+  if (cands.size() < l) throw std::runtime_error("too few main primes");
+  struct Group {
+    uint32_t a, b;
+    double lg() const { return std::log2((double)a) + std::log2((double)b); }
+  };
+  std::vector<Group> groups;
+  double lo = std::ldexp(1.0, (int)db - 1), hi = std::ldexp(1.0, (int)db + 1);
+  for (int widen = 0; groups.size() < l / 2 && widen <= 12; ++widen) {
+    size_t i = 0;
+    while (i < cands.size() && groups.size() < l / 2) {
+      const double a = (double)cands[i];
+      size_t j = cands.size() - 1;
+      while (j > i && a * (double)cands[j] >= hi) --j;
+      if (j > i && a * (double)cands[j] >= lo) {
+        groups.push_back({std::max(cands[i], cands[j]), std::min(cands[i], cands[j])});
+        cands.erase(cands.begin() + j);
+        cands.erase(cands.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+    lo /= 2;
+    hi *= 2;
+  }
+  if (groups.size() < l / 2) throw std::runtime_error("cannot form enough delta groups in the prime window");
+  std::stable_sort(groups.begin(), groups.end(), [&](const Group& x, const Group& y) {
+    return std::abs(x.lg() - db) > std::abs(y.lg() - db);
+  });
+  std::vector<uint32_t> primes;
+  for (const auto& g : groups) {
+    primes.push_back(g.a);
+    primes.push_back(g.b);
+  }
+  primes.insert(primes.end(), p_list.begin(), p_list.end());
+  return primes;
+}
+
+// ---------------------------------------------------------------- device blob
+// One cudaMalloc holding a plan's small tables (job lists, constants, maps).
+class Blob {
+ public:
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    const size_t off = (host_.size() + 15) / 16 * 16;
+    host_.resize(off + v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(host_.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+  void upload() {
+    if (dev_) cudaFree(dev_);
+    CK_CUDA(cudaMalloc(&dev_, std::max<size_t>(host_.size(), 16)));
+    CK_CUDA(cudaMemcpy(dev_, host_.data(), host_.size(), cudaMemcpyHostToDevice));
+  }
+  template <class T>
+  T* at(size_t off) const {
+    return reinterpret_cast<T*>(static_cast<char*>(dev_) + off);
+  }
+  ~Blob() {
+    if (dev_) cudaFree(dev_);
+  }
+
+ private:
+  std::vector<char> host_;
+  void* dev_ = nullptr;
+};
+
+struct NttPlan {  // one batched transform
+  Blob blob;
+  size_t jobs_off = 0, exits_off = 0;
+  int njobs = 0;
+};
+struct BconvPlan {
+  Blob blob;
+  size_t groups_off = 0, cmat_off = 0, row_off = 0, prime_off = 0;
+  int ngroups = 0, max_sc = 1;
+};
+// ModUp at one level: INTT(+part1) of the level rows, per-digit BConv, NTT.
+struct ModUpPlan {
+  uint32_t level = 0, D = 0;
+  NttPlan intt, ntt;
+  BconvPlan bc;
+  uint64_t ntt_rows = 0;
+};
+// drop_and_divide for npoly polynomials of (out_q + sc) rows each.
+struct SwitchPlan {
+  uint32_t out_q = 0, sc = 0, npoly = 0;
+  NttPlan intt, ntt;
+  BconvPlan bc;
+  Blob consts;  // div_inv_mont [out_q]
+};
+
+}  // namespace
+
+// ================================================================ context ==
+struct Context {
+  ck_params p{};
+  int device = 0;
+  uint32_t n = 0, logn = 0, L = 0, alpha = 0;
+  std::vector<uint32_t> primes;  // Q then P
+  std::vector<uint32_t> psi;
+  std::vector<PrimeDev> pdev_host;
+  PrimeDev* d_primes = nullptr;
+  uint2* d_fwd = nullptr;
+  uint2* d_inv = nullptr;
+  uint32_t* d_pmont = nullptr;  // P mod q_i (Montgomery), i < L
+  std::map<uint32_t, std::unique_ptr<ModUpPlan>> modup;
+  std::map<std::tuple<int, uint32_t, uint32_t>, std::unique_ptr<SwitchPlan>> switches;
+  std::map<int64_t, uint32_t*> rot_maps;
+  std::map<std::string, std::unique_ptr<NttPlan>> adhoc_ntt;
+  std::map<std::string, std::unique_ptr<BconvPlan>> adhoc_bc;
+  std::map<uint32_t, std::unique_ptr<Blob>> row_primes;  // (level+alpha)-row prime maps
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  uint64_t counters[7] = {0, 0, 0, 0, 0, 0, 0};  // modup moddown ntt intt keymult bconv rescale
+  std::atomic<uint64_t> launches{0};
+
+  ~Context() {
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
+    for (auto& kv : rot_maps) cudaFree(kv.second);
+    if (d_primes) cudaFree(d_primes);
+    if (d_fwd) cudaFree(d_fwd);
+    if (d_inv) cudaFree(d_inv);
+    if (d_pmont) cudaFree(d_pmont);
+    if (scratch) cudaFree(scratch);
+  }
+
+  uint32_t q(uint32_t g) const { return primes[g]; }
+  uint32_t gidx(uint32_t level, uint32_t row) const { return row < level ? row : L + (row - level); }
+  uint32_t digits(uint32_t level) const { return (level + alpha - 1) / alpha; }
+  size_t rowsz() const { return (size_t)n; }
+
+  void* scratch_get(size_t bytes) {
+    if (bytes > scratch_bytes) {
+      CK_CUDA(cudaDeviceSynchronize());
+      if (scratch) cudaFree(scratch);
+      scratch = nullptr;
+      const size_t want = bytes + bytes / 8;
+      CK_CUDA(cudaMalloc(&scratch, want));
+      scratch_bytes = want;
+    }
+    return scratch;
+  }
+
+  // Inverse exit constants for prime g with plain epilogue factor e (ntt.cpp:76-84).
+  ExitConst exit_const(uint32_t g, uint32_t e) const {
+    const uint32_t qq = q(g);
+    const uint32_t rinv = invm(r_mod(qq), qq);
+    const uint32_t ninv = invm(n % qq, qq);
+    const uint32_t psih_inv = invm((uint32_t)pow_mod(psi[g], n / 2, qq), qq);
+    const uint32_t cx = mulm(mulm(ninv, rinv, qq), e, qq);
+    const uint32_t cy = mulm(mulm(mulm(psih_inv, ninv, qq), rinv, qq), e, qq);
+    return make_uint4(cx, shoup(cx, qq), cy, shoup(cy, qq));
+  }
+
+  // make_bconv_table (bconv.cpp:13-46): (P/P_j) mod q_i in Montgomery form,
+  // and part1 = (P/P_j)^-1 mod p_j (plain; folded into the INTT exit).
+  void bconv_consts(const std::vector<uint32_t>& sg, const std::vector<uint32_t>& dg, std::vector<uint32_t>& cmat,
+                    std::vector<uint32_t>& part1) const {
+    part1.resize(sg.size());
+    for (size_t j = 0; j < sg.size(); ++j) {
+      const uint32_t pj = q(sg[j]);
+      uint32_t ph = 1 % pj;
+      for (size_t k = 0; k < sg.size(); ++k)
+        if (k != j) ph = mulm(ph, q(sg[k]) % pj, pj);
+      part1[j] = invm(ph, pj);
+    }
+    for (size_t i = 0; i < dg.size(); ++i) {
+      const uint32_t qi = q(dg[i]);
+      for (size_t j = 0; j < sg.size(); ++j) {
+        uint32_t ph = 1 % qi;
+        for (size_t k = 0; k < sg.size(); ++k)
+          if (k != j) ph = mulm(ph, q(sg[k]) % qi, qi);
+        cmat.push_back(to_mont(ph, qi));
+      }
+    }
+  }
+
+  void check_bconv_width(const std::vector<uint32_t>& sg) const {
+    // unsigned int64 accumulation is exact while sc * max(p) < 2^32 (the
+    // reference's cap makes (alpha+2) * p < 2^32, rns.cpp:69-72)
+    uint64_t pmax = 0;
+    for (uint32_t g : sg) pmax = std::max<uint64_t>(pmax, q(g));
+    if (sg.size() > 16 || (uint64_t)sg.size() * pmax >= (1ull << 32))
+      throw InvalidArgument("base-conversion source too wide");
+  }
+
+  const ModUpPlan& modup_plan(uint32_t level) {
+    auto it = modup.find(level);
+    if (it != modup.end()) return *it->second;
+    auto pl = std::make_unique<ModUpPlan>();
+    pl->level = level;
+    pl->D = digits(level);
+    const uint32_t rows = level + alpha;
+    std::vector<RowJob> ijobs, njobs;
+    std::vector<ExitConst> exits;
+    std::vector<BconvGroup> groups;
+    std::vector<uint32_t> cmat, drow;
+    std::vector<uint16_t> dprime;
+    int max_sc = 1;
+    for (uint32_t k = 0; k < pl->D; ++k) {  // modup_table (ckks.cpp:188-202)
+      const uint32_t b = k * alpha, e = std::min((k + 1) * alpha, level);
+      std::vector<uint32_t> sg, dg;
+      for (uint32_t j = b; j < e; ++j) sg.push_back(j);
+      for (uint32_t i = 0; i < rows; ++i)
+        if (i < b || i >= e) dg.push_back(gidx(level, i));
+      check_bconv_width(sg);
+      std::vector<uint32_t> part1;
+      BconvGroup G;
+      G.src_off = b;
+      G.sc = (uint32_t)sg.size();
+      G.dc = (uint32_t)dg.size();
+      G.cmat_off = (uint32_t)cmat.size();
+      G.map_off = (uint32_t)drow.size();
+      bconv_consts(sg, dg, cmat, part1);
+      max_sc = std::max<int>(max_sc, (int)sg.size());
+      for (uint32_t i = 0; i < rows; ++i)
+        if (i < b || i >= e) {
+          drow.push_back(k * rows + i);
+          dprime.push_back((uint16_t)gidx(level, i));
+          njobs.push_back({k * rows + i, k * rows + i, (uint16_t)gidx(level, i), 0});
+        }
+      groups.push_back(G);
+      for (uint32_t j = 0; j < sg.size(); ++j) {
+        ijobs.push_back({b + j, b + j, (uint16_t)(b + j), (uint16_t)exits.size()});
+        exits.push_back(exit_const(b + j, part1[j]));
+      }
+    }
+    pl->intt.jobs_off = pl->intt.blob.add(ijobs);
+    pl->intt.exits_off = pl->intt.blob.add(exits);
+    pl->intt.njobs = (int)ijobs.size();
+    pl->intt.blob.upload();
+    pl->ntt.jobs_off = pl->ntt.blob.add(njobs);
+    pl->ntt.njobs = (int)njobs.size();
+    pl->ntt.blob.upload();
+    pl->ntt_rows = njobs.size();
+    pl->bc.groups_off = pl->bc.blob.add(groups);
+    pl->bc.cmat_off = pl->bc.blob.add(cmat);
+    pl->bc.row_off = pl->bc.blob.add(drow);
+    pl->bc.prime_off = pl->bc.blob.add(dprime);
+    pl->bc.ngroups = (int)groups.size();
+    pl->bc.max_sc = max_sc;
+    pl->bc.blob.upload();
+    auto& ref = *pl;
+    modup[level] = std::move(pl);
+    return ref;
+  }
+
+  // kind 0 = ModDown (src P, out level), 1 = rescale (src 2 tail Q, out level-2),
+  // 2 = merged (src 2 tail Q + P, out level-2)  (ckks.cpp:206-258)
+  const SwitchPlan& switch_plan(int kind, uint32_t level, uint32_t npoly) {
+    auto key = std::make_tuple(kind, level, npoly);
+    auto it = switches.find(key);
+    if (it != switches.end()) return *it->second;
+    auto pl = std::make_unique<SwitchPlan>();
+    std::vector<uint32_t> sg;
+    uint32_t out_q = level;
+    if (kind == 0) {
+      for (uint32_t j = 0; j < alpha; ++j) sg.push_back(L + j);
+    } else {
+      if (level < 4) throw InvalidArgument("level exhausted");
+      out_q = level - 2;
+      sg = {level - 2, level - 1};
+      if (kind == 2)
+        for (uint32_t j = 0; j < alpha; ++j) sg.push_back(L + j);
+    }
+    check_bconv_width(sg);
+    const uint32_t sc = (uint32_t)sg.size();
+    pl->out_q = out_q;
+    pl->sc = sc;
+    pl->npoly = npoly;
+    std::vector<uint32_t> dg(out_q);
+    for (uint32_t i = 0; i < out_q; ++i) dg[i] = i;
+    std::vector<uint32_t> cmat, part1;
+    bconv_consts(sg, dg, cmat, part1);
+    std::vector<RowJob> ijobs, njobs;
+    std::vector<ExitConst> exits;
+    std::vector<BconvGroup> groups;
+    std::vector<uint32_t> drow;
+    std::vector<uint16_t> dprime;
+    for (uint32_t j = 0; j < sc; ++j) exits.push_back(exit_const(sg[j], part1[j]));
+    for (uint32_t p = 0; p < npoly; ++p) {
+      for (uint32_t j = 0; j < sc; ++j)
+        ijobs.push_back({p * (out_q + sc) + out_q + j, p * sc + j, (uint16_t)sg[j], (uint16_t)j});
+      BconvGroup G;
+      G.src_off = p * sc;
+      G.sc = sc;
+      G.dc = out_q;
+      G.cmat_off = 0;
+      G.map_off = (uint32_t)drow.size();
+      groups.push_back(G);
+      for (uint32_t i = 0; i < out_q; ++i) {
+        drow.push_back(p * out_q + i);
+        dprime.push_back((uint16_t)i);
+        njobs.push_back({p * out_q + i, p * out_q + i, (uint16_t)i, 0});
+      }
+    }
+    pl->intt.jobs_off = pl->intt.blob.add(ijobs);
+    pl->intt.exits_off = pl->intt.blob.add(exits);
+    pl->intt.njobs = (int)ijobs.size();
+    pl->intt.blob.upload();
+    pl->ntt.jobs_off = pl->ntt.blob.add(njobs);
+    pl->ntt.njobs = (int)njobs.size();
+    pl->ntt.blob.upload();
+    pl->bc.groups_off = pl->bc.blob.add(groups);
+    pl->bc.cmat_off = pl->bc.blob.add(cmat);
+    pl->bc.row_off = pl->bc.blob.add(drow);
+    pl->bc.prime_off = pl->bc.blob.add(dprime);
+    pl->bc.ngroups = (int)groups.size();
+    pl->bc.max_sc = (int)sc;
+    pl->bc.blob.upload();
+    // divisor = product of the source primes; one Montgomery inverse per row
+    std::vector<uint32_t> dinv(out_q);
+    for (uint32_t i = 0; i < out_q; ++i) {
+      uint32_t d = 1 % q(i);
+      for (uint32_t g : sg) d = mulm(d, q(g) % q(i), q(i));
+      dinv[i] = to_mont(invm(d, q(i)), q(i));
+    }
+    pl->consts.add(dinv);
+    pl->consts.upload();
+    auto& ref = *pl;
+    switches[key] = std::move(pl);
+    return ref;
+  }
+
+  const uint32_t* rotation_map(int64_t r) {  // AutomorphismMap::rotation (automorphism.cpp:11-69)
+    auto it = rot_maps.find(r);
+    if (it != rot_maps.end()) return it->second;
+    const int64_t half = (int64_t)n / 2;
+    int64_t e = (-r) % half;
+    if (e < 0) e += half;
+    uint64_t g = 1;
+    const uint64_t mod = 2ull * n;
+    for (int64_t i = 0; i < e; ++i) g = g * 5 % mod;
+    std::vector<uint32_t> src(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t bi = bit_reverse(i, logn);
+      const uint32_t phi = (uint32_t)((((2ull * bi + 1) * g) % mod - 1) / 2);
+      src[bit_reverse(phi, logn)] = i;
+    }
+    uint32_t* d = nullptr;
+    CK_CUDA(cudaMalloc(&d, n * sizeof(uint32_t)));
+    CK_CUDA(cudaMemcpy(d, src.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    rot_maps[r] = d;
+    return d;
+  }
+
+  // ------------------------------------------------------------- launches --
+  void run_ntt(const NttPlan& pl, bool inverse, int batch, const uint32_t* src, uint64_t src_bs, uint32_t* dst,
+               uint64_t dst_bs, int entry, cudaStream_t st) {
+    if (pl.njobs == 0 || batch == 0) return;
+    NttLaunch a;
+    a.jobs = pl.blob.at<RowJob>(pl.jobs_off);
+    a.njobs = pl.njobs;
+    a.batch = batch;
+    a.src = src;
+    a.src_bs = src_bs;
+    a.dst = dst;
+    a.dst_bs = dst_bs;
+    a.primes = d_primes;
+    a.tw = inverse ? d_inv : d_fwd;
+    a.exits = inverse ? pl.blob.at<ExitConst>(pl.exits_off) : nullptr;
+    a.entry = entry;
+    if (inverse)
+      ntt_inverse((int)logn, a, st);
+    else
+      ntt_forward((int)logn, a, st);
+    launches += 2;
+  }
+  void run_bconv(const BconvPlan& pl, int batch, const uint32_t* src, uint64_t src_bs, uint32_t* dst, uint64_t dst_bs,
+                 cudaStream_t st) {
+    if (batch == 0) return;
+    BconvLaunch a;
+    a.groups = pl.blob.at<BconvGroup>(pl.groups_off);
+    a.ngroups = pl.ngroups;
+    a.batch = batch;
+    a.max_sc = pl.max_sc;
+    a.src = src;
+    a.src_bs = src_bs;
+    a.dst = dst;
+    a.dst_bs = dst_bs;
+    a.cmat = pl.blob.at<uint32_t>(pl.cmat_off);
+    a.dst_row = pl.blob.at<uint32_t>(pl.row_off);
+    a.dst_prime = pl.blob.at<uint16_t>(pl.prime_off);
+    a.primes = d_primes;
+    bconv((int)n, a, st);
+    ++launches;
+  }
+
+  // ModUp (ckks.cpp:680-731) of B polynomials d (level rows, batch stride d_bs)
+  // into ext [B][D][level+alpha]; uses `is` [B][level] as INTT scratch.
+  // The digit rows of ext are NOT written: key_mult reads them from d.
+  void mod_up(uint32_t level, int B, const uint32_t* d, uint64_t d_bs, uint32_t* is, uint32_t* ext,
+              cudaStream_t st) {
+    const ModUpPlan& pl = modup_plan(level);
+    const uint64_t N = n;
+    run_ntt(pl.intt, true, B, d, d_bs, is, level * N, 0, st);
+    run_bconv(pl.bc, B, is, level * N, ext, (uint64_t)pl.D * (level + alpha) * N, st);
+    run_ntt(pl.ntt, false, B, ext, (uint64_t)pl.D * (level + alpha) * N, ext,
+            (uint64_t)pl.D * (level + alpha) * N, 1, st);
+    counters[0] += B;
+    counters[3] += (uint64_t)B * level;
+    counters[5] += (uint64_t)B * pl.D;
+    counters[2] += (uint64_t)B * pl.ntt_rows;
+  }
+
+  // key_mult (+ optional fold) into v [B][2][level+alpha]
+  void key_mult_v(uint32_t level, int B, const uint32_t* ext, const uint32_t* d, uint64_t d_bs, const uint32_t* evk,
+                  const uint32_t* fold, uint64_t fold_bs, uint32_t* v, cudaStream_t st) {
+    KeyMultLaunch a;
+    a.level = (int)level;
+    a.alpha = (int)alpha;
+    a.L = (int)L;
+    a.D = (int)digits(level);
+    a.batch = B;
+    a.ext = ext;
+    a.ext_bs = (uint64_t)a.D * (level + alpha) * n;
+    a.d = d;
+    a.d_bs = d_bs;
+    a.evk = evk;
+    a.fold = fold;
+    a.fold_bs = fold_bs;
+    a.p_mont = d_pmont;
+    a.v = v;
+    a.v_bs = 2ull * (level + alpha) * n;
+    a.primes = d_primes;
+    key_mult((int)n, a, st);
+    ++launches;
+    counters[4] += (uint64_t)B * a.D;
+  }
+
+  // drop_and_divide (ckks.cpp:611-655) for B x npoly polynomials v (out_q+sc
+  // rows each, poly stride, batch stride) into o [B][npoly][out_q]; ts scratch
+  // [B][npoly][sc]. If `combine_now` is false the caller fuses the combine.
+  void drop_divide(const SwitchPlan& pl, int B, const uint32_t* v, uint64_t v_bs, uint32_t* ts, uint32_t* o,
+                   bool combine_now, cudaStream_t st) {
+    const uint64_t N = n;
+    const uint64_t prow = pl.out_q + pl.sc;
+    run_ntt(pl.intt, true, B, v, v_bs, ts, (uint64_t)pl.npoly * pl.sc * N, 0, st);
+    run_bconv(pl.bc, B, ts, (uint64_t)pl.npoly * pl.sc * N, o, (uint64_t)pl.npoly * pl.out_q * N, st);
+    run_ntt(pl.ntt, false, B, o, (uint64_t)pl.npoly * pl.out_q * N, o, (uint64_t)pl.npoly * pl.out_q * N, 1, st);
+    if (combine_now) {
+      combine((int)n, (int)pl.out_q, (int)pl.npoly, B, v, prow * N, v_bs, o, pl.out_q * N,
+              (uint64_t)pl.npoly * pl.out_q * N, pl.consts.at<uint32_t>(0), d_primes, st);
+      ++launches;
+    }
+    counters[3] += (uint64_t)B * pl.npoly * pl.sc;
+    counters[5] += (uint64_t)B * pl.npoly;
+    counters[2] += (uint64_t)B * pl.npoly * pl.out_q;
+  }
+};
+
+namespace {
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+template <class F>
+ck_status guard(F&& f) {
+  try {
+    f();
+    return CK_OK;
+  } catch (const InvalidArgument& e) {
+    g_err = e.what();
+    return CK_INVALID_ARGUMENT;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return CK_INVALID_ARGUMENT;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return CK_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CK_RUNTIME_ERROR;
+  }
+}
+
+Context* C(ck_context* c) {
+  if (!c) throw InvalidArgument("null context");
+  return reinterpret_cast<Context*>(c);
+}
+cudaStream_t S(ck_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void check_level(const Context* c, uint32_t level, uint32_t min_level = 1) {
+  if (level < min_level || level > c->L) throw InvalidArgument("level out of range");
+}
+void check_ptr(const void* p) {
+  if (!p) throw InvalidArgument("null buffer");
+}
+
+}  // namespace
+}  // namespace ck
+
+using namespace ck;
+
+extern "C" {
+
+const char* ck_last_error(void) { return ck::g_err.c_str(); }
+const char* ck_version(void) { return "ck32-b200 0.1.0 (sm_100a)"; }
+
+ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int device, ck_context** out) {
+  return guard([&] {
+    if (!params || !out) throw InvalidArgument("null argument");
+    const ck_params& p = *params;
+    if (p.n < 8 || (p.n & (p.n - 1)) != 0 || p.n > (1u << 17))
+      throw InvalidArgument("ring degree must be a power of two in [8, 2^17]");
+    if (p.l < 2 || p.l % 2 != 0) throw InvalidArgument("level count must be even and >= 2");
+    if (p.alpha < 1) throw InvalidArgument("alpha must be positive");
+    if (p.l + p.alpha > (uint32_t)kMaxRows) throw InvalidArgument("too many primes");
+    auto c = std::make_unique<Context>();
+    c->p = p;
+    c->device = device;
+    c->n = p.n;
+    while ((1u << c->logn) < p.n) ++c->logn;
+    c->L = p.l;
+    c->alpha = p.alpha;
+    if (primes) {
+      c->primes.assign(primes, primes + p.l + p.alpha);
+      for (uint32_t q : c->primes)
+        if (q >= (1u << 29) || (q % (2 * p.n)) != 1 || !is_prime(q))
+          throw InvalidArgument("prime must be < 2^29, = 1 mod 2n");
+    } else {
+      c->primes = generate_basis(p.n, p.l, p.alpha, p.delta_bits);
+    }
+    CK_CUDA(cudaSetDevice(device));
+    const uint32_t np = p.l + p.alpha, n = p.n;
+    c->psi.resize(np);
+    c->pdev_host.resize(np);
+    std::vector<uint2> fwd((size_t)np * n), inv((size_t)np * n);
+#pragma omp parallel for schedule(dynamic)
+    for (int g = 0; g < (int)np; ++g) {  // build_twiddles (ntt.cpp:100-135), plain + Shoup
+      const uint32_t q = c->primes[g];
+      const uint32_t psi = find_root_2n(q, n);
+      c->psi[g] = psi;
+      const uint32_t psi_inv = invm(psi, q);
+      std::vector<uint32_t> pw(n), pwi(n);
+      pw[0] = pwi[0] = 1;
+      for (uint32_t k = 1; k < n; ++k) {
+        pw[k] = mulm(pw[k - 1], psi, q);
+        pwi[k] = mulm(pwi[k - 1], psi_inv, q);
+      }
+      uint2* F = fwd.data() + (size_t)g * n;
+      uint2* I = inv.data() + (size_t)g * n;
+      F[0] = I[0] = make_uint2(0, 0);
+      for (uint32_t i = 1; i < n; ++i) {
+        const uint32_t e = bit_reverse(i, c->logn);
+        F[i] = make_uint2(pw[e], shoup(pw[e], q));
+        I[i] = make_uint2(pwi[e], shoup(pwi[e], q));
+      }
+      PrimeDev& P = c->pdev_host[g];
+      P.q = q;
+      P.q2 = 2 * q;
+      uint32_t inv32 = q;
+      for (int i = 0; i < 5; ++i) inv32 *= 2u - q * inv32;  // modarith.cpp:47-49
+      P.qinv_neg = 0u - inv32;
+      P.r = r_mod(q);
+      P.r_sh = shoup(P.r, q);
+      P.w1r = mulm(pw[n / 2], P.r, q);
+      P.w1r_sh = shoup(P.w1r, q);
+      P.pad = 0;
+    }
+    CK_CUDA(cudaMalloc(&c->d_primes, np * sizeof(PrimeDev)));
+    CK_CUDA(cudaMemcpy(c->d_primes, c->pdev_host.data(), np * sizeof(PrimeDev), cudaMemcpyHostToDevice));
+    CK_CUDA(cudaMalloc(&c->d_fwd, fwd.size() * sizeof(uint2)));
+    CK_CUDA(cudaMemcpy(c->d_fwd, fwd.data(), fwd.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    CK_CUDA(cudaMalloc(&c->d_inv, inv.size() * sizeof(uint2)));
+    CK_CUDA(cudaMemcpy(c->d_inv, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    std::vector<uint32_t> pm(p.l);  // p_mont (ckks.cpp:171-175)
+    for (uint32_t i = 0; i < p.l; ++i) {
+      const uint32_t q = c->primes[i];
+      uint32_t prod = 1 % q;
+      for (uint32_t j = 0; j < p.alpha; ++j) prod = mulm(prod, c->primes[p.l + j] % q, q);
+      pm[i] = to_mont(prod, q);
+    }
+    CK_CUDA(cudaMalloc(&c->d_pmont, p.l * sizeof(uint32_t)));
+    CK_CUDA(cudaMemcpy(c->d_pmont, pm.data(), p.l * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    *out = reinterpret_cast<ck_context*>(c.release());
+  });
+}
+
+ck_status ck_generate_basis(uint32_t n, uint32_t l, uint32_t alpha, uint32_t delta_bits, uint32_t* primes_out) {
+  return guard([&] {
+    if (!primes_out) throw InvalidArgument("null argument");
+    const auto p = generate_basis(n, l, alpha, delta_bits);
+    std::copy(p.begin(), p.end(), primes_out);
+  });
+}
+
+ck_status ck_context_destroy(ck_context* ctx) {
+  return guard([&] { delete C(ctx); });
+}
+
+ck_status ck_context_primes(const ck_context* ctx, uint32_t* out) {
+  return guard([&] {
+    const Context* c = reinterpret_cast<const Context*>(ctx);
+    if (!c || !out) throw InvalidArgument("null argument");
+    std::copy(c->primes.begin(), c->primes.end(), out);
+  });
+}
+
+ck_status ck_context_counters(const ck_context* ctx, uint64_t out[7]) {
+  return guard([&] {
+    const Context* c = reinterpret_cast<const Context*>(ctx);
+    if (!c || !out) throw InvalidArgument("null argument");
+    std::copy(c->counters, c->counters + 7, out);
+  });
+}
+ck_status ck_context_reset_counters(ck_context* ctx) {
+  return guard([&] { std::fill(C(ctx)->counters, C(ctx)->counters + 7, 0); });
+}
+uint64_t ck_launch_count(const ck_context* ctx) {
+  return ctx ? reinterpret_cast<const Context*>(ctx)->launches.load() : 0;
+}
+
+ck_status ck_malloc(ck_context* ctx, size_t bytes, void** dptr) {
+  return guard([&] {
+    CK_CUDA(cudaSetDevice(C(ctx)->device));
+    CK_CUDA(cudaMalloc(dptr, std::max<size_t>(bytes, 16)));
+  });
+}
+ck_status ck_free(ck_context* ctx, void* dptr) {
+  return guard([&] {
+    CK_CUDA(cudaSetDevice(C(ctx)->device));
+    CK_CUDA(cudaFree(dptr));
+  });
+}
+ck_status ck_memcpy_h2d(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream) {
+  return guard([&] { CK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S(stream))); (void)ctx; });
+}
+ck_status ck_memcpy_d2h(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream) {
+  return guard([&] { CK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(stream))); (void)ctx; });
+}
+ck_status ck_stream_sync(ck_context* ctx, ck_stream stream) {
+  return guard([&] { CK_CUDA(cudaStreamSynchronize(S(stream))); (void)ctx; });
+}
+
+ck_status ck_ntt_forward(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, const uint32_t* gidx, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_ptr(rows_dev);
+    if (!gidx && rows) throw InvalidArgument("null prime index list");
+    std::string key = "F";
+    std::vector<RowJob> jobs;
+    for (uint32_t i = 0; i < rows; ++i) {
+      if (gidx[i] >= c->primes.size()) throw InvalidArgument("prime index out of range");
+      jobs.push_back({i, i, (uint16_t)gidx[i], 0});
+      key += std::to_string(gidx[i]) + ",";
+    }
+    auto& pl = c->adhoc_ntt[key];
+    if (!pl) {
+      pl = std::make_unique<NttPlan>();
+      pl->jobs_off = pl->blob.add(jobs);
+      pl->njobs = (int)jobs.size();
+      pl->blob.upload();
+    }
+    c->run_ntt(*pl, false, 1, rows_dev, 0, rows_dev, 0, 1, S(stream));
+    check_launch();
+    c->counters[2] += rows;
+  });
+}
+
+ck_status ck_intt_inverse(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
+                          const uint32_t* epilogue_mont, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_ptr(rows_dev);
+    if (!gidx && rows) throw InvalidArgument("null prime index list");
+    std::string key = "I";
+    std::vector<RowJob> jobs;
+    std::vector<ExitConst> exits;
+    for (uint32_t i = 0; i < rows; ++i) {
+      if (gidx[i] >= c->primes.size()) throw InvalidArgument("prime index out of range");
+      const uint32_t q = c->q(gidx[i]);
+      // epilogue given in Montgomery form (ntt.hpp:72-73): plain factor = e * R^-1
+      const uint32_t e = epilogue_mont ? mulm(epilogue_mont[i] % q, invm(r_mod(q), q), q) : 1u;
+      jobs.push_back({i, i, (uint16_t)gidx[i], (uint16_t)i});
+      exits.push_back(c->exit_const(gidx[i], e));
+      key += std::to_string(gidx[i]) + ":" + std::to_string(e) + ",";
+    }
+    auto& pl = c->adhoc_ntt[key];
+    if (!pl) {
+      pl = std::make_unique<NttPlan>();
+      pl->jobs_off = pl->blob.add(jobs);
+      pl->exits_off = pl->blob.add(exits);
+      pl->njobs = (int)jobs.size();
+      pl->blob.upload();
+    }
+    c->run_ntt(*pl, true, 1, rows_dev, 0, rows_dev, 0, 0, S(stream));
+    check_launch();
+    c->counters[3] += rows;
+  });
+}
+
+ck_status ck_bconv(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,
+                   uint32_t* dst_dev, uint32_t dst_count, const uint32_t* dst_gidx, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_ptr(src_dev);
+    check_ptr(dst_dev);
+    if (src_count == 0 || !src_gidx || !dst_gidx) throw InvalidArgument("empty conversion");
+    std::vector<uint32_t> sg(src_gidx, src_gidx + src_count), dg(dst_gidx, dst_gidx + dst_count);
+    for (uint32_t g : sg)
+      if (g >= c->primes.size()) throw InvalidArgument("prime index out of range");
+    for (uint32_t g : dg)
+      if (g >= c->primes.size()) throw InvalidArgument("prime index out of range");
+    c->check_bconv_width(sg);
+    std::string key;
+    for (uint32_t g : sg) key += std::to_string(g) + ",";
+    key += "|";
+    for (uint32_t g : dg) key += std::to_string(g) + ",";
+    auto& pl = c->adhoc_bc[key];
+    if (!pl) {
+      pl = std::make_unique<BconvPlan>();
+      std::vector<uint32_t> cmat, part1, drow(dst_count);
+      std::vector<uint16_t> dprime(dst_count);
+      c->bconv_consts(sg, dg, cmat, part1);
+      for (uint32_t i = 0; i < dst_count; ++i) {
+        drow[i] = i;
+        dprime[i] = (uint16_t)dg[i];
+      }
+      std::vector<BconvGroup> groups = {{0, src_count, dst_count, 0, 0}};
+      pl->groups_off = pl->blob.add(groups);
+      pl->cmat_off = pl->blob.add(cmat);
+      pl->row_off = pl->blob.add(drow);
+      pl->prime_off = pl->blob.add(dprime);
+      pl->ngroups = 1;
+      pl->max_sc = (int)src_count;
+      pl->blob.upload();
+    }
+    c->run_bconv(*pl, 1, src_dev, 0, dst_dev, 0, S(stream));
+    check_launch();
+    c->counters[5] += 1;
+  });
+}
+
+ck_status ck_automorphism(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t rows, int64_t r,
+                          ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_ptr(in_dev);
+    check_ptr(out_dev);
+    if (in_dev == out_dev) throw InvalidArgument("automorphism is out-of-place");
+    permute((int)c->n, (int)rows, 1, in_dev, 0, out_dev, 0, c->rotation_map(r), S(stream));
+    ++c->launches;
+    check_launch();
+  });
+}
+
+static ck_status ew(ck_context* ctx, int op, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t rows,
+                    ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_ptr(a);
+    check_ptr(b);
+    check_ptr(out);
+    if (rows > c->L) throw InvalidArgument("rows exceed the Q basis");
+    elementwise((int)c->n, (int)rows, 1, op, a, 0, b, 0, out, 0, nullptr, c->d_primes, S(stream));
+    ++c->launches;
+    check_launch();
+  });
+}
+ck_status ck_ew_add(ck_context* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t rows,
+                    ck_stream stream) {
+  return ew(ctx, 0, a, b, out, rows, stream);
+}
+ck_status ck_ew_sub(ck_context* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t rows,
+                    ck_stream stream) {
+  return ew(ctx, 1, a, b, out, rows, stream);
+}
+ck_status ck_ew_mul(ck_context* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t rows,
+                    ck_stream stream) {
+  return ew(ctx, 2, a, b, out, rows, stream);
+}
+
+ck_status ck_mod_up(ck_context* ctx, uint32_t level, const uint32_t* d, uint32_t* hoist, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(d);
+    check_ptr(hoist);
+    const uint64_t N = c->n;
+    const uint32_t D = c->digits(level), rows = level + c->alpha;
+    uint32_t* is = static_cast<uint32_t*>(c->scratch_get(level * N * 4));
+    c->mod_up(level, 1, d, 0, is, hoist, S(stream));
+    // the public HoistState carries the digit rows too (ckks.cpp:708-709)
+    for (uint32_t k = 0; k < D; ++k) {
+      const uint32_t b = k * c->alpha, e = std::min((k + 1) * c->alpha, level);
+      CK_CUDA(cudaMemcpyAsync(hoist + ((size_t)k * rows + b) * N, d + (size_t)b * N, (size_t)(e - b) * N * 4,
+                              cudaMemcpyDeviceToDevice, S(stream)));
+    }
+    check_launch();
+  });
+}
+
+ck_status ck_key_mult(ck_context* ctx, uint32_t level, const uint32_t* hoist, const uint32_t* evk, uint32_t* v,
+                      ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(hoist);
+    check_ptr(evk);
+    check_ptr(v);
+    // key_mult_v reads each digit's own (pass-through) rows from a compact
+    // level-row buffer; gather them out of the full HoistState first.
+    const uint32_t rows = level + c->alpha;
+    const uint64_t N = c->n;
+    uint32_t* dd = static_cast<uint32_t*>(c->scratch_get(level * N * 4));
+    const uint32_t D = c->digits(level);
+    for (uint32_t k = 0; k < D; ++k) {
+      const uint32_t b = k * c->alpha, e = std::min((k + 1) * c->alpha, level);
+      CK_CUDA(cudaMemcpyAsync(dd + (size_t)b * N, hoist + ((size_t)k * rows + b) * N, (size_t)(e - b) * N * 4,
+                              cudaMemcpyDeviceToDevice, S(stream)));
+    }
+    c->key_mult_v(level, 1, hoist, dd, 0, evk, nullptr, 0, v, S(stream));
+    check_launch();
+  });
+}
+
+ck_status ck_mod_down(ck_context* ctx, uint32_t level, const uint32_t* v, uint32_t* out, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(v);
+    check_ptr(out);
+    const SwitchPlan& pl = c->switch_plan(0, level, 1);
+    uint32_t* ts = static_cast<uint32_t*>(c->scratch_get((size_t)pl.sc * c->n * 4));
+    c->drop_divide(pl, 1, v, 0, ts, out, true, S(stream));
+    c->counters[1] += 1;
+    check_launch();
+  });
+}
+
+ck_status ck_key_switch(ck_context* ctx, uint32_t level, const uint32_t* d, const uint32_t* evk, uint32_t* out,
+                        ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(d);
+    check_ptr(evk);
+    check_ptr(out);
+    const uint64_t N = c->n;
+    const uint32_t D = c->digits(level), rows = level + c->alpha;
+    const SwitchPlan& pl = c->switch_plan(0, level, 2);
+    const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N;
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w) * 4));
+    uint32_t *is = base, *ext = is + is_w, *v = ext + ext_w, *ts = v + v_w;
+    c->mod_up(level, 1, d, 0, is, ext, S(stream));
+    c->key_mult_v(level, 1, ext, d, 0, evk, nullptr, 0, v, S(stream));
+    c->drop_divide(pl, 1, v, 0, ts, out, true, S(stream));
+    c->counters[1] += 1;
+    check_launch();
+  });
+}
+
+ck_status ck_rescale(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, uint32_t* out,
+                     ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level, 4);
+    check_ptr(ct);
+    check_ptr(out);
+    const SwitchPlan& pl = c->switch_plan(1, level, 2);
+    uint32_t* ts = static_cast<uint32_t*>(c->scratch_get((size_t)batch * 2 * pl.sc * c->n * 4));
+    c->drop_divide(pl, (int)batch, ct, 2ull * level * c->n, ts, out, true, S(stream));
+    c->counters[6] += batch;
+    check_launch();
+  });
+}
+
+ck_status ck_hmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* x, const uint32_t* y,
+                   const uint32_t* relin_evk, uint32_t* out, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level, 4);  // ckks.cpp:815
+    check_ptr(x);
+    check_ptr(y);
+    check_ptr(relin_evk);
+    check_ptr(out);
+    if (batch == 0) return;
+    const uint64_t N = c->n;
+    const int B = (int)batch;
+    const uint32_t D = c->digits(level), rows = level + c->alpha;
+    const bool lazy = c->p.lazy_rescale != 0;
+    const SwitchPlan& pl = lazy ? c->switch_plan(0, level, 2) : c->switch_plan(2, level, 2);
+    const size_t t01_w = 2ull * level * N, d2_w = level * N, is_w = level * N, ext_w = (size_t)D * rows * N,
+                 v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N, c_w = lazy ? 2ull * level * N : 0;
+    const size_t per = t01_w + d2_w + is_w + ext_w + v_w + ts_w + c_w;
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get(per * B * 4));
+    uint32_t* t01 = base;
+    uint32_t* d2 = t01 + t01_w * B;
+    uint32_t* is = d2 + d2_w * B;
+    uint32_t* ext = is + is_w * B;
+    uint32_t* v = ext + ext_w * B;
+    uint32_t* ts = v + v_w * B;
+    uint32_t* cc = ts + ts_w * B;
+    cudaStream_t st = S(stream);
+    tensor((int)N, (int)level, B, x, y, 2ull * level * N, t01, t01_w, d2, d2_w, c->d_primes, st);
+    ++c->launches;
+    c->mod_up(level, B, d2, d2_w, is, ext, st);
+    if (!lazy) {
+      c->key_mult_v(level, B, ext, d2, d2_w, relin_evk, t01, t01_w, v, st);  // fold P*d0/1 fused
+      c->drop_divide(pl, B, v, v_w, ts, out, true, st);
+    } else {
+      c->key_mult_v(level, B, ext, d2, d2_w, relin_evk, nullptr, 0, v, st);
+      c->drop_divide(pl, B, v, v_w, ts, cc, true, st);
+      // out.b = d0 + c0, out.a = d1 + c1 (ckks.cpp:857-858)
+      elementwise((int)N, (int)(2 * level), B, 0, t01, t01_w, cc, c_w, out, 2ull * level * N, nullptr,
+                  c->d_primes, st, (int)level);
+      ++c->launches;
+    }
+    c->counters[1] += B;
+    check_launch();
+  });
+}
+
+ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, int64_t r,
+                  const uint32_t* rot_evk, uint32_t* out, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(ct);
+    check_ptr(rot_evk);
+    check_ptr(out);
+    if (batch == 0) return;
+    if (ct == out) throw InvalidArgument("hrot is out-of-place");
+    const uint64_t N = c->n;
+    const int B = (int)batch;
+    const uint32_t D = c->digits(level), rows = level + c->alpha;
+    const SwitchPlan& pl = c->switch_plan(0, level, 2);
+    const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N,
+                 o_w = 2ull * level * N;
+    const size_t per = is_w + ext_w + v_w + ts_w + o_w;
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get(per * B * 4));
+    uint32_t* is = base;
+    uint32_t* ext = is + is_w * B;
+    uint32_t* v = ext + ext_w * B;
+    uint32_t* ts = v + v_w * B;
+    uint32_t* o = ts + ts_w * B;
+    cudaStream_t st = S(stream);
+    const uint64_t ct_bs = 2ull * level * N;
+    const uint32_t* a = ct + level * N;
+    c->mod_up(level, B, a, ct_bs, is, ext, st);
+    c->key_mult_v(level, B, ext, a, ct_bs, rot_evk, nullptr, 0, v, st);
+    c->drop_divide(pl, B, v, v_w, ts, o, false, st);
+    hrot_tail((int)N, (int)level, B, v, v_w, rows * N, o, o_w, level * N, ct, ct_bs, pl.consts.at<uint32_t>(0),
+              c->rotation_map(r), out, ct_bs, c->d_primes, st);
+    ++c->launches;
+    c->counters[1] += B;
+    check_launch();
+  });
+}
+
+static ck_status ct_ew(ck_context* ctx, int op, uint32_t level, uint32_t batch, const uint32_t* x, const uint32_t* y,
+                       bool y_is_pt, bool pt_only_b, uint32_t* out, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(x);
+    check_ptr(y);
+    check_ptr(out);
+    const uint64_t N = c->n, ct_bs = 2ull * level * N;
+    cudaStream_t st = S(stream);
+    if (!y_is_pt) {
+      elementwise((int)N, (int)(2 * level), (int)batch, op, x, ct_bs, y, ct_bs, out, ct_bs, nullptr, c->d_primes, st,
+                  (int)level);
+      ++c->launches;
+    } else {
+      elementwise((int)N, (int)level, (int)batch, op, x, ct_bs, y, 0, out, ct_bs, nullptr, c->d_primes, st);
+      ++c->launches;
+      if (pt_only_b) {  // padd: a copied (ckks.cpp:578)
+        CK_CUDA(cudaMemcpy2DAsync(out + level * N, ct_bs * 4, x + level * N, ct_bs * 4, level * N * 4, batch,
+                                  cudaMemcpyDeviceToDevice, st));
+      } else {
+        elementwise((int)N, (int)level, (int)batch, op, x + level * N, ct_bs, y, 0, out + level * N, ct_bs, nullptr,
+                    c->d_primes, st);
+        ++c->launches;
+      }
+    }
+    check_launch();
+  });
+}
+ck_status ck_hadd(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* x, const uint32_t* y,
+                  uint32_t* out, ck_stream stream) {
+  return ct_ew(ctx, 0, level, batch, x, y, false, false, out, stream);
+}
+ck_status ck_padd(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, const uint32_t* pt,
+                  uint32_t* out, ck_stream stream) {
+  return ct_ew(ctx, 0, level, batch, ct, pt, true, true, out, stream);
+}
+ck_status ck_pmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, const uint32_t* pt,
+                   uint32_t* out, ck_stream stream) {
+  return ct_ew(ctx, 2, level, batch, ct, pt, true, false, out, stream);
+}
+
+ck_status ck_hoisted_rotations(ck_context* ctx, uint32_t level, const uint32_t* ct, uint32_t count,
+                               const int64_t* rots, const uint32_t* const* evks, uint32_t* out, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(ct);
+    check_ptr(out);
+    if (count && (!rots || !evks)) throw InvalidArgument("rotation/key count mismatch");
+    const uint64_t N = c->n, ct_w = 2ull * level * N;
+    const uint32_t D = c->digits(level), rows = level + c->alpha;
+    const SwitchPlan& pl = c->switch_plan(0, level, 2);
+    const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N,
+                 o_w = 2ull * level * N;
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w + o_w) * 4));
+    uint32_t *is = base, *ext = is + is_w, *v = ext + ext_w, *ts = v + v_w, *o = ts + ts_w;
+    cudaStream_t st = S(stream);
+    const uint32_t* a = ct + level * N;
+    c->mod_up(level, 1, a, 0, is, ext, st);  // shared across all rotations
+    for (uint32_t i = 0; i < count; ++i) {
+      uint32_t* dst = out + i * ct_w;
+      if (rots[i] == 0) {
+        CK_CUDA(cudaMemcpyAsync(dst, ct, ct_w * 4, cudaMemcpyDeviceToDevice, st));
+        continue;
+      }
+      if (!evks[i]) throw InvalidArgument("missing rotation key");
+      c->key_mult_v(level, 1, ext, a, 0, evks[i], nullptr, 0, v, st);
+      c->drop_divide(pl, 1, v, 0, ts, o, false, st);
+      hrot_tail((int)N, (int)level, 1, v, 0, rows * N, o, 0, level * N, ct, 0, pl.consts.at<uint32_t>(0),
+                c->rotation_map(rots[i]), dst, 0, c->d_primes, st);
+      ++c->launches;
+      c->counters[1] += 1;
+    }
+    check_launch();
+  });
+}
+
+ck_status ck_hoisted_rotate_accumulate(ck_context* ctx, uint32_t level, const uint32_t* ct, uint32_t count,
+                                       const int64_t* rots, const uint32_t* const* pts,
+                                       const uint32_t* const* evks, uint32_t* out, ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(ct);
+    check_ptr(out);
+    if (count == 0 || !rots || !pts || !evks) throw InvalidArgument("rotation/plaintext/key count mismatch");
+    const uint64_t N = c->n;
+    const uint32_t D = c->digits(level), rows = level + c->alpha;
+    const SwitchPlan& pl = c->switch_plan(0, level, 2);
+    const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N,
+                 acc_w = 2ull * rows * N, o_w = 2ull * level * N;
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w + acc_w + o_w) * 4));
+    uint32_t *is = base, *ext = is + is_w, *v = ext + ext_w, *ts = v + v_w, *acc = ts + ts_w, *o = acc + acc_w;
+    cudaStream_t st = S(stream);
+    const uint32_t* b = ct;
+    const uint32_t* a = ct + level * N;
+    std::vector<uint16_t> rp(rows);
+    for (uint32_t i = 0; i < rows; ++i) rp[i] = (uint16_t)c->gidx(level, i);
+    // row->prime map for the (level + alpha)-row accumulators
+    auto& blob = c->row_primes[level];
+    if (!blob) {
+      blob = std::make_unique<Blob>();
+      blob->add(rp);
+      blob->upload();
+    }
+    const uint16_t* d_rp = blob->at<uint16_t>(0);
+    CK_CUDA(cudaMemsetAsync(acc, 0, acc_w * 4, st));
+    CK_CUDA(cudaMemsetAsync(out, 0, o_w * 4, st));
+    c->mod_up(level, 1, a, 0, is, ext, st);
+    bool used_pq = false;
+    for (uint32_t i = 0; i < count; ++i) {
+      check_ptr(pts[i]);
+      if (rots[i] == 0) {  // ckks.cpp:977-982
+        addmul((int)N, (int)level, 1, out, 0, b, 0, pts[i], 0, nullptr, c->d_primes, st);
+        addmul((int)N, (int)level, 1, out + level * N, 0, a, 0, pts[i], 0, nullptr, c->d_primes, st);
+        c->launches += 2;
+        continue;
+      }
+      if (!evks[i]) throw InvalidArgument("rotation key mismatch");
+      const uint32_t* map = c->rotation_map(rots[i]);
+      c->key_mult_v(level, 1, ext, a, 0, evks[i], nullptr, 0, v, st);
+      addmul_permuted((int)N, (int)rows, 1, acc, 0, v, 0, pts[i], 0, map, d_rp, c->d_primes, st);
+      addmul_permuted((int)N, (int)rows, 1, acc + rows * N, 0, v + rows * N, 0, pts[i], 0, map, d_rp, c->d_primes,
+                      st);
+      addmul_permuted((int)N, (int)level, 1, out, 0, b, 0, pts[i], 0, map, nullptr, c->d_primes, st);
+      c->launches += 3;
+      used_pq = true;
+    }
+    if (used_pq) {
+      c->drop_divide(pl, 1, acc, 0, ts, o, true, st);
+      elementwise((int)N, (int)(2 * level), 1, 0, out, 0, o, 0, out, 0, nullptr, c->d_primes, st, (int)level);
+      ++c->launches;
+      c->counters[1] += 1;
+    }
+    check_launch();
+  });
+}
+
+}  // extern "C"

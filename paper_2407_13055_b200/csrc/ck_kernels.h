@@ -1,0 +1,98 @@
+// Launch interface between the host runtime (ck_context.cu) and the kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ck_common.cuh"
+
+namespace ck {
+
+struct NttLaunch {
+  const RowJob* jobs = nullptr;  // device
+  int njobs = 0;
+  int batch = 1;
+  const uint32_t* src = nullptr;
+  uint64_t src_bs = 0;  // batch stride (words)
+  uint32_t* dst = nullptr;
+  uint64_t dst_bs = 0;
+  const PrimeDev* primes = nullptr;
+  const uint2* tw = nullptr;  // [prime][N] {w, w'}
+  const ExitConst* exits = nullptr;
+  int entry = 0;  // forward: multiply the input by R (reference entry merge)
+};
+void ntt_forward(int logn, const NttLaunch& a, cudaStream_t st);
+void ntt_inverse(int logn, const NttLaunch& a, cudaStream_t st);
+
+// One base-conversion group: src rows [src_off, src_off+sc) of the source
+// buffer, dc destination rows dst_row[map_off + i] (row offsets in the
+// destination buffer) with primes dst_prime[map_off + i], constants
+// cmat[cmat_off + i*sc + j] = ((P/P_j) mod q_i) * R mod q_i.
+struct BconvGroup {
+  uint32_t src_off, sc, dc, cmat_off, map_off;
+};
+struct BconvLaunch {
+  const BconvGroup* groups = nullptr;  // device
+  int ngroups = 0;
+  int batch = 1;
+  int max_sc = 1;  // max source rows over groups (template dispatch)
+  const uint32_t* src = nullptr;
+  uint64_t src_bs = 0;
+  uint32_t* dst = nullptr;
+  uint64_t dst_bs = 0;
+  const uint32_t* cmat = nullptr;
+  const uint32_t* dst_row = nullptr;
+  const uint16_t* dst_prime = nullptr;
+  const PrimeDev* primes = nullptr;
+};
+void bconv(int n, const BconvLaunch& a, cudaStream_t st);
+
+// tensor product of two ciphertexts (ckks.cpp:818-821): d0 = b b', d1 = b a' + a b', d2 = a a'
+void tensor(int n, int level, int batch, const uint32_t* x, const uint32_t* y, uint64_t ct_bs, uint32_t* d01,
+            uint64_t d01_bs, uint32_t* d2, uint64_t d2_bs, const PrimeDev* primes, cudaStream_t st);
+
+// KeyMult (ckks.cpp:733-770) with the ModUp pass-through rows read from `d`
+// and an optional fold v += P*d0/1 (ckks.cpp:831-842).
+struct KeyMultLaunch {
+  int level = 0, alpha = 0, L = 0, D = 0, batch = 1;
+  const uint32_t* ext = nullptr;  // [B][D][level+alpha][n]
+  uint64_t ext_bs = 0;
+  const uint32_t* d = nullptr;    // [B][level][n] ModUp input (pass-through rows)
+  uint64_t d_bs = 0;
+  const uint32_t* evk = nullptr;  // [D][2][L+alpha][n]
+  const uint32_t* fold = nullptr; // [B][2][level][n] (d0 then d1) or null
+  uint64_t fold_bs = 0;
+  const uint32_t* p_mont = nullptr;  // [level] P mod q_i in Montgomery form
+  uint32_t* v = nullptr;          // [B][2][level+alpha][n]
+  uint64_t v_bs = 0;
+  const PrimeDev* primes = nullptr;
+};
+void key_mult(int n, const KeyMultLaunch& a, cudaStream_t st);
+
+// drop-and-divide combine (ckks.cpp:643-651): o = (v - o) * div_inv (Montgomery)
+void combine(int n, int rows, int npoly, int batch, const uint32_t* v, uint64_t v_ps, uint64_t v_bs, uint32_t* o,
+             uint64_t o_ps, uint64_t o_bs, const uint32_t* div_inv_mont, const PrimeDev* primes, cudaStream_t st);
+
+// HRot tail (ckks.cpp:875-882): combine both halves, c0 += b, permute.
+void hrot_tail(int n, int level, int batch, const uint32_t* v, uint64_t v_bs, uint64_t v_ps, const uint32_t* o,
+               uint64_t o_bs, uint64_t o_ps, const uint32_t* b, uint64_t b_bs, const uint32_t* div_inv_mont,
+               const uint32_t* src_map, uint32_t* out, uint64_t out_bs, const PrimeDev* primes, cudaStream_t st);
+
+// element-wise (poly.cpp:146-205): op 0 add, 1 sub, 2 mul (Montgomery).
+// Row i uses prime row_prime[i] if given, else i % prime_mod (prime_mod = rows
+// of one polynomial when several polynomials are stacked; <= 0 means `rows`).
+void elementwise(int n, int rows, int batch, int op, const uint32_t* a, uint64_t a_bs, const uint32_t* b,
+                 uint64_t b_bs, uint32_t* o, uint64_t o_bs, const uint16_t* row_prime, const PrimeDev* primes,
+                 cudaStream_t st, int prime_mod = 0);
+// out[i][j] = in[i][src[j]] (automorphism.cpp:82-87)
+void permute(int n, int rows, int batch, const uint32_t* in, uint64_t in_bs, uint32_t* out, uint64_t out_bs,
+             const uint32_t* src_map, cudaStream_t st);
+// acc = acc + x*y (Montgomery), addmul_rows (ckks.cpp:930-941)
+void addmul(int n, int rows, int batch, uint32_t* acc, uint64_t acc_bs, const uint32_t* x, uint64_t x_bs,
+            const uint32_t* y, uint64_t y_bs, const uint16_t* row_prime, const PrimeDev* primes, cudaStream_t st);
+// permuted accumulate: acc[i][j] += x[i][src[j]] * y[i][j]
+void addmul_permuted(int n, int rows, int batch, uint32_t* acc, uint64_t acc_bs, const uint32_t* x, uint64_t x_bs,
+                     const uint32_t* y, uint64_t y_bs, const uint32_t* src_map, const uint16_t* row_prime,
+                     const PrimeDev* primes, cudaStream_t st);
+
+}  // namespace ck

@@ -1,0 +1,314 @@
+// Element-wise, base-conversion and key-switching kernels for sm_100a.
+//
+// All of these are HBM-bound integer kernels: every thread owns 4 adjacent
+// coefficients (one 128-bit load/store per row), grids cover (columns, rows,
+// batch), and per-row constants come from small device tables.  References:
+//   bconv_part2        bconv.cpp:96-174   (int64 delayed accumulation, one reduction)
+//   tensor             ckks.cpp:818-821
+//   key_mult (+fold)   ckks.cpp:733-770, ckks.cpp:831-842
+//   combine            ckks.cpp:643-651
+//   hrot tail          ckks.cpp:875-882 + apply_automorphism automorphism.cpp:76-100
+//   ew_*               poly.cpp:146-205;  addmul_rows ckks.cpp:930-941
+#include "ck_common.cuh"
+#include "ck_kernels.h"
+
+namespace ck {
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ uint4 ld4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ void st4(uint32_t* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+__device__ __forceinline__ uint32_t getc(const uint4& v, int k) {
+  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+
+// ------------------------------------------------------------------ bconv --
+template <int SC>
+__global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
+  __shared__ uint32_t cm[kMaxRows * SC];
+  const BconvGroup G = a.groups[blockIdx.y];
+  for (int e = threadIdx.x; e < G.dc * SC; e += kT) {
+    const int i = e / SC, j = e % SC;
+    cm[e] = j < (int)G.sc ? a.cmat[G.cmat_off + i * G.sc + j] : 0u;
+  }
+  __syncthreads();
+  const int x = (blockIdx.x * kT + threadIdx.x) * 4;
+  if (x >= n) return;
+  const uint32_t* src = a.src + blockIdx.z * a.src_bs + (size_t)G.src_off * n + x;
+  uint4 s[SC];
+#pragma unroll
+  for (int j = 0; j < SC; ++j) s[j] = j < (int)G.sc ? ld4(src + (size_t)j * n) : make_uint4(0, 0, 0, 0);
+  uint32_t* dst = a.dst + blockIdx.z * a.dst_bs + x;
+  for (int i = 0; i < (int)G.dc; ++i) {
+    uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+#pragma unroll
+    for (int j = 0; j < SC; ++j) {
+      const uint32_t c = cm[i * SC + j];
+      acc0 += (uint64_t)s[j].x * c;
+      acc1 += (uint64_t)s[j].y * c;
+      acc2 += (uint64_t)s[j].z * c;
+      acc3 += (uint64_t)s[j].w * c;
+    }
+    const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
+    uint4 r;
+    r.x = sub_if(mont_reduce64(acc0, P.q, P.qinv_neg), P.q);
+    r.y = sub_if(mont_reduce64(acc1, P.q, P.qinv_neg), P.q);
+    r.z = sub_if(mont_reduce64(acc2, P.q, P.qinv_neg), P.q);
+    r.w = sub_if(mont_reduce64(acc3, P.q, P.qinv_neg), P.q);
+    st4(dst + (size_t)a.dst_row[G.map_off + i] * n, r);
+  }
+}
+
+// ----------------------------------------------------------------- tensor --
+__global__ void __launch_bounds__(kT) k_tensor(int n, int level, const uint32_t* __restrict__ x,
+                                               const uint32_t* __restrict__ y, uint64_t ct_bs,
+                                               uint32_t* __restrict__ d01, uint64_t d01_bs,
+                                               uint32_t* __restrict__ d2, uint64_t d2_bs,
+                                               const PrimeDev* __restrict__ primes) {
+  const int xo = (blockIdx.x * kT + threadIdx.x) * 4;
+  if (xo >= n) return;
+  const int i = blockIdx.y, b = blockIdx.z;
+  const PrimeDev P = primes[i];
+  const size_t ro = (size_t)i * n + xo, ao = (size_t)(level + i) * n + xo;
+  const uint4 xb = ld4(x + b * ct_bs + ro), xa = ld4(x + b * ct_bs + ao);
+  const uint4 yb = ld4(y + b * ct_bs + ro), ya = ld4(y + b * ct_bs + ao);
+  uint4 o0, o1, o2;
+#define CK_T(c)                                                                              \
+  {                                                                                          \
+    const uint32_t bb = xb.c, ba = xa.c, cb = yb.c, ca = ya.c;                               \
+    o0.c = sub_if(mont_mul(bb, cb, P.q, P.qinv_neg), P.q);                                   \
+    o1.c = sub_if(mont_reduce64((uint64_t)bb * ca + (uint64_t)ba * cb, P.q, P.qinv_neg), P.q); \
+    o2.c = sub_if(mont_mul(ba, ca, P.q, P.qinv_neg), P.q);                                   \
+  }
+  CK_T(x) CK_T(y) CK_T(z) CK_T(w)
+#undef CK_T
+  st4(d01 + b * d01_bs + ro, o0);
+  st4(d01 + b * d01_bs + ao, o1);
+  st4(d2 + b * d2_bs + ro, o2);
+}
+
+// --------------------------------------------------------------- key_mult --
+__global__ void __launch_bounds__(kT) k_key_mult(KeyMultLaunch a, int n) {
+  const int xo = (blockIdx.x * kT + threadIdx.x) * 4;
+  if (xo >= n) return;
+  const int i = blockIdx.y, b = blockIdx.z;
+  const int rows = a.level + a.alpha;
+  const int g = i < a.level ? i : a.L + (i - a.level);  // global prime index (poly.hpp:103-106)
+  const PrimeDev P = a.primes[g];
+  const uint32_t LA = (uint32_t)(a.L + a.alpha);
+  uint64_t s0[4] = {0, 0, 0, 0}, s1[4] = {0, 0, 0, 0};
+  int terms = 0;
+  auto renorm = [&]() {  // keep the int64 sums below q*2^32 (acc value unchanged mod q, scaled back by R)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      s0[c] = shoup_mul(mont_reduce64(s0[c], P.q, P.qinv_neg), P.r, P.r_sh, P.q);
+      s1[c] = shoup_mul(mont_reduce64(s1[c], P.q, P.qinv_neg), P.r, P.r_sh, P.q);
+    }
+  };
+  for (int k = 0; k < a.D; ++k) {
+    const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+    const uint32_t* op = (i >= lo && i < hi) ? a.d + b * a.d_bs + (size_t)i * n + xo
+                                             : a.ext + b * a.ext_bs + ((size_t)k * rows + i) * n + xo;
+    const uint4 dv = ld4(op);
+    const uint4 eb = ld4(a.evk + (((size_t)k * 2 + 0) * LA + g) * n + xo);
+    const uint4 ea = ld4(a.evk + (((size_t)k * 2 + 1) * LA + g) * n + xo);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      s0[c] += (uint64_t)getc(dv, c) * getc(eb, c);
+      s1[c] += (uint64_t)getc(dv, c) * getc(ea, c);
+    }
+    if (++terms == 7) {
+      renorm();
+      terms = 1;
+    }
+  }
+  if (a.fold && i < a.level) {
+    const uint32_t pm = a.p_mont[i];
+    const uint4 f0 = ld4(a.fold + b * a.fold_bs + (size_t)i * n + xo);
+    const uint4 f1 = ld4(a.fold + b * a.fold_bs + (size_t)(a.level + i) * n + xo);
+    if (terms == 7) renorm();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      s0[c] += (uint64_t)getc(f0, c) * pm;
+      s1[c] += (uint64_t)getc(f1, c) * pm;
+    }
+  }
+  uint4 r0, r1;
+  r0.x = sub_if(mont_reduce64(s0[0], P.q, P.qinv_neg), P.q);
+  r0.y = sub_if(mont_reduce64(s0[1], P.q, P.qinv_neg), P.q);
+  r0.z = sub_if(mont_reduce64(s0[2], P.q, P.qinv_neg), P.q);
+  r0.w = sub_if(mont_reduce64(s0[3], P.q, P.qinv_neg), P.q);
+  r1.x = sub_if(mont_reduce64(s1[0], P.q, P.qinv_neg), P.q);
+  r1.y = sub_if(mont_reduce64(s1[1], P.q, P.qinv_neg), P.q);
+  r1.z = sub_if(mont_reduce64(s1[2], P.q, P.qinv_neg), P.q);
+  r1.w = sub_if(mont_reduce64(s1[3], P.q, P.qinv_neg), P.q);
+  st4(a.v + b * a.v_bs + (size_t)i * n + xo, r0);
+  st4(a.v + b * a.v_bs + (size_t)(rows + i) * n + xo, r1);
+}
+
+// ---------------------------------------------------------------- combine --
+__global__ void __launch_bounds__(kT) k_combine(int n, const uint32_t* __restrict__ v, uint64_t v_ps, uint64_t v_bs,
+                                                uint32_t* __restrict__ o, uint64_t o_ps, uint64_t o_bs,
+                                                const uint32_t* __restrict__ dinv, const PrimeDev* __restrict__ primes,
+                                                int npoly) {
+  const int xo = (blockIdx.x * kT + threadIdx.x) * 4;
+  if (xo >= n) return;
+  const int i = blockIdx.y;
+  const int b = blockIdx.z / npoly, p = blockIdx.z % npoly;
+  const PrimeDev P = primes[i];
+  const uint32_t di = dinv[i];
+  const uint32_t* vp = v + b * v_bs + p * v_ps + (size_t)i * n + xo;
+  uint32_t* op = o + b * o_bs + p * o_ps + (size_t)i * n + xo;
+  const uint4 vv = ld4(vp), ov = ld4(op);
+  uint4 r;
+  r.x = sub_if(mont_mul(vv.x - ov.x + P.q, di, P.q, P.qinv_neg), P.q);
+  r.y = sub_if(mont_mul(vv.y - ov.y + P.q, di, P.q, P.qinv_neg), P.q);
+  r.z = sub_if(mont_mul(vv.z - ov.z + P.q, di, P.q, P.qinv_neg), P.q);
+  r.w = sub_if(mont_mul(vv.w - ov.w + P.q, di, P.q, P.qinv_neg), P.q);
+  st4(op, r);
+}
+
+// -------------------------------------------------------------- hrot tail --
+__global__ void __launch_bounds__(kT) k_hrot_tail(int n, int level, const uint32_t* __restrict__ v, uint64_t v_bs,
+                                                  uint64_t v_ps, const uint32_t* __restrict__ o, uint64_t o_bs,
+                                                  uint64_t o_ps, const uint32_t* __restrict__ bb, uint64_t b_bs,
+                                                  const uint32_t* __restrict__ dinv, const uint32_t* __restrict__ src,
+                                                  uint32_t* __restrict__ out, uint64_t out_bs,
+                                                  const PrimeDev* __restrict__ primes) {
+  const int j = blockIdx.x * kT + threadIdx.x;
+  if (j >= n) return;
+  const int i = blockIdx.y, b = blockIdx.z;
+  const PrimeDev P = primes[i];
+  const uint32_t di = dinv[i];
+  const uint32_t s = __ldg(&src[j]);
+  const size_t r = (size_t)i * n + s;
+  const uint32_t* vb = v + b * v_bs;
+  const uint32_t* ob = o + b * o_bs;
+  uint32_t c0 = sub_if(mont_mul(vb[r] - ob[r] + P.q, di, P.q, P.qinv_neg), P.q);
+  c0 = sub_if(c0 + bb[b * b_bs + r], P.q);
+  const uint32_t c1 = sub_if(mont_mul(vb[v_ps + r] - ob[o_ps + r] + P.q, di, P.q, P.qinv_neg), P.q);
+  out[b * out_bs + (size_t)i * n + j] = c0;
+  out[b * out_bs + (size_t)(level + i) * n + j] = c1;
+}
+
+// ------------------------------------------------------------ elementwise --
+__global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_t* __restrict__ a, uint64_t a_bs,
+                                                    const uint32_t* __restrict__ bp, uint64_t b_bs,
+                                                    uint32_t* __restrict__ o, uint64_t o_bs,
+                                                    const uint16_t* __restrict__ row_prime,
+                                                    const PrimeDev* __restrict__ primes, int prime_mod) {
+  const int xo = (blockIdx.x * kT + threadIdx.x) * 4;
+  if (xo >= n) return;
+  const int i = blockIdx.y, b = blockIdx.z;
+  const PrimeDev P = primes[row_prime ? row_prime[i] : i % prime_mod];
+  const size_t r = (size_t)i * n + xo;
+  const uint4 x = ld4(a + b * a_bs + r), y = ld4(bp + b * b_bs + r);
+  uint4 z;
+  if (op == 0) {
+    z = make_uint4(sub_if(x.x + y.x, P.q), sub_if(x.y + y.y, P.q), sub_if(x.z + y.z, P.q), sub_if(x.w + y.w, P.q));
+  } else if (op == 1) {
+    z = make_uint4(sub_if(x.x - y.x + P.q, P.q), sub_if(x.y - y.y + P.q, P.q), sub_if(x.z - y.z + P.q, P.q),
+                   sub_if(x.w - y.w + P.q, P.q));
+  } else {
+    z = make_uint4(sub_if(mont_mul(x.x, y.x, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.y, y.y, P.q, P.qinv_neg), P.q),
+                   sub_if(mont_mul(x.z, y.z, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.w, y.w, P.q, P.qinv_neg), P.q));
+  }
+  st4(o + b * o_bs + r, z);
+}
+
+__global__ void __launch_bounds__(kT) k_permute(int n, const uint32_t* __restrict__ in, uint64_t in_bs,
+                                                uint32_t* __restrict__ out, uint64_t out_bs,
+                                                const uint32_t* __restrict__ src) {
+  const int j = blockIdx.x * kT + threadIdx.x;
+  if (j >= n) return;
+  const size_t r = (size_t)blockIdx.y * n;
+  out[blockIdx.z * out_bs + r + j] = in[blockIdx.z * in_bs + r + __ldg(&src[j])];
+}
+
+__global__ void __launch_bounds__(kT) k_addmul(int n, uint32_t* __restrict__ acc, uint64_t acc_bs,
+                                               const uint32_t* __restrict__ x, uint64_t x_bs,
+                                               const uint32_t* __restrict__ y, uint64_t y_bs,
+                                               const uint32_t* __restrict__ src, const uint16_t* __restrict__ row_prime,
+                                               const PrimeDev* __restrict__ primes) {
+  const int j = blockIdx.x * kT + threadIdx.x;
+  if (j >= n) return;
+  const int i = blockIdx.y, b = blockIdx.z;
+  const PrimeDev P = primes[row_prime ? row_prime[i] : i];
+  const size_t r = (size_t)i * n;
+  const uint32_t xs = x[b * x_bs + r + (src ? __ldg(&src[j]) : (uint32_t)j)];
+  const uint32_t ys = y[b * y_bs + r + j];
+  uint32_t* a = acc + b * acc_bs + r + j;
+  *a = sub_if(sub_if(*a + mont_mul(xs, ys, P.q, P.qinv_neg), P.q2), P.q);
+}
+
+inline unsigned cdiv(unsigned a, unsigned b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+void bconv(int n, const BconvLaunch& a, cudaStream_t st) {
+  dim3 grid(cdiv(n / 4, kT), a.ngroups, a.batch);
+  const int sc = a.max_sc;
+  const BconvLaunch b = a;
+  switch (sc) {
+#define CK_SC(S) case S: k_bconv<S><<<grid, kT, 0, st>>>(b, n); break;
+    CK_SC(1) CK_SC(2) CK_SC(3) CK_SC(4) CK_SC(5) CK_SC(6) CK_SC(7) CK_SC(8) CK_SC(9) CK_SC(10) CK_SC(11)
+    CK_SC(12) CK_SC(13) CK_SC(14) CK_SC(15) CK_SC(16)
+#undef CK_SC
+    default: break;
+  }
+}
+
+void tensor(int n, int level, int batch, const uint32_t* x, const uint32_t* y, uint64_t ct_bs, uint32_t* d01,
+            uint64_t d01_bs, uint32_t* d2, uint64_t d2_bs, const PrimeDev* primes, cudaStream_t st) {
+  dim3 grid(cdiv(n / 4, kT), level, batch);
+  k_tensor<<<grid, kT, 0, st>>>(n, level, x, y, ct_bs, d01, d01_bs, d2, d2_bs, primes);
+}
+
+void key_mult(int n, const KeyMultLaunch& a, cudaStream_t st) {
+  dim3 grid(cdiv(n / 4, kT), a.level + a.alpha, a.batch);
+  k_key_mult<<<grid, kT, 0, st>>>(a, n);
+}
+
+void combine(int n, int rows, int npoly, int batch, const uint32_t* v, uint64_t v_ps, uint64_t v_bs, uint32_t* o,
+             uint64_t o_ps, uint64_t o_bs, const uint32_t* div_inv_mont, const PrimeDev* primes, cudaStream_t st) {
+  dim3 grid(cdiv(n / 4, kT), rows, batch * npoly);
+  k_combine<<<grid, kT, 0, st>>>(n, v, v_ps, v_bs, o, o_ps, o_bs, div_inv_mont, primes, npoly);
+}
+
+void hrot_tail(int n, int level, int batch, const uint32_t* v, uint64_t v_bs, uint64_t v_ps, const uint32_t* o,
+               uint64_t o_bs, uint64_t o_ps, const uint32_t* b, uint64_t b_bs, const uint32_t* div_inv_mont,
+               const uint32_t* src_map, uint32_t* out, uint64_t out_bs, const PrimeDev* primes, cudaStream_t st) {
+  dim3 grid(cdiv(n, kT), level, batch);
+  k_hrot_tail<<<grid, kT, 0, st>>>(n, level, v, v_bs, v_ps, o, o_bs, o_ps, b, b_bs, div_inv_mont, src_map, out,
+                                   out_bs, primes);
+}
+
+void elementwise(int n, int rows, int batch, int op, const uint32_t* a, uint64_t a_bs, const uint32_t* b,
+                 uint64_t b_bs, uint32_t* o, uint64_t o_bs, const uint16_t* row_prime, const PrimeDev* primes,
+                 cudaStream_t st, int prime_mod) {
+  dim3 grid(cdiv(n / 4, kT), rows, batch);
+  k_elementwise<<<grid, kT, 0, st>>>(n, op, a, a_bs, b, b_bs, o, o_bs, row_prime, primes,
+                                     prime_mod > 0 ? prime_mod : rows);
+}
+
+void permute(int n, int rows, int batch, const uint32_t* in, uint64_t in_bs, uint32_t* out, uint64_t out_bs,
+             const uint32_t* src_map, cudaStream_t st) {
+  dim3 grid(cdiv(n, kT), rows, batch);
+  k_permute<<<grid, kT, 0, st>>>(n, in, in_bs, out, out_bs, src_map);
+}
+
+void addmul(int n, int rows, int batch, uint32_t* acc, uint64_t acc_bs, const uint32_t* x, uint64_t x_bs,
+            const uint32_t* y, uint64_t y_bs, const uint16_t* row_prime, const PrimeDev* primes, cudaStream_t st) {
+  dim3 grid(cdiv(n, kT), rows, batch);
+  k_addmul<<<grid, kT, 0, st>>>(n, acc, acc_bs, x, x_bs, y, y_bs, nullptr, row_prime, primes);
+}
+
+void addmul_permuted(int n, int rows, int batch, uint32_t* acc, uint64_t acc_bs, const uint32_t* x, uint64_t x_bs,
+                     const uint32_t* y, uint64_t y_bs, const uint32_t* src_map, const uint16_t* row_prime,
+                     const PrimeDev* primes, cudaStream_t st) {
+  dim3 grid(cdiv(n, kT), rows, batch);
+  k_addmul<<<grid, kT, 0, st>>>(n, acc, acc_bs, x, x_bs, y, y_bs, src_map, row_prime, primes);
+}
+
+}  // namespace ck

@@ -1,0 +1,310 @@
+"""GPU parity suite: every CUDA result is compared, canonical residue by
+residue, with (a) the reference's own fixtures / full-size hashes and (b) the
+C restatement oracle on seeded inputs.  Bit-exact is the only bar: all of
+this path is integer arithmetic."""
+from __future__ import annotations
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from golden_util import FULL, SMALL_DIRS, Fixture, full_cases, sha
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2407_13055_b200 import ckks  # noqa: E402
+from pyoracle import Oracle, Rng  # noqa: E402
+
+_CTX = {}
+
+
+def ctx_for(n, l, a, db=55, lazy=False):
+    key = (n, l, a, db, lazy)
+    if key not in _CTX:
+        _CTX[key] = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db, lazy_rescale=lazy))
+    return _CTX[key]
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x).astype(np.int32))).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().astype(np.uint32)
+
+
+def canon(O, rows, level, p_rows=0):
+    return O.canonical(rows, O.gidx(level, p_rows))
+
+
+def ct(data, level, scale=Fraction(1 << 55)):
+    return ckks.Ciphertext(dev(data), scale, level)
+
+
+# -------------------------------------------------------------- kernel level --
+@pytest.mark.parametrize("n", [8, 16, 64, 256, 1024, 4096, 32768, 65536, 131072])
+def test_ntt_roundtrip_and_oracle(n):
+    l, a = 4, 2
+    C = ctx_for(n, l, a, 48)
+    O = Oracle(n, l, a, 48)
+    rng = Rng(n)
+    g = O.gidx(l, a)
+    x = O.random_rows(rng, g)
+    p = ckks.Polynomial(dev(x), l, a, ckks.COEFFICIENT, False)
+    ckks.ntt_forward(C, p)
+    np.testing.assert_array_equal(host(p.data), canon(O, O.ntt_fwd(x, g), l, a))
+    ckks.intt_inverse(C, p)
+    np.testing.assert_array_equal(host(p.data), x.astype(np.uint32))
+
+
+@pytest.mark.parametrize("n", [256, 65536])
+def test_intt_fused_part1_epilogue(n):
+    l, a = 6, 3
+    C = ctx_for(n, l, a, 48)
+    O = Oracle(n, l, a, 48)
+    g = O.gidx(l)
+    x = O.random_rows(Rng(7), g)
+    epi_mont = [int(v) for v in O.bconv_part1(g)]  # part1 constants, Montgomery form (bconv.hpp:22-23)
+    p = ckks.Polynomial(dev(x), l, 0)
+    ckks.intt_inverse(C, p, epi_mont)
+    want = canon(O, O.intt(x, g, epi_mont), l)
+    np.testing.assert_array_equal(host(p.data), want)
+
+
+@pytest.mark.parametrize("n", [1024, 65536])
+@pytest.mark.parametrize("shape", [(8, 24), (10, 22), (2, 22), (1, 3), (16, 40)])
+def test_bconv_matches_oracle(n, shape):
+    sc, dc = shape
+    l, a = 40, 16
+    if sc == 16:
+        a = 16
+    C = ctx_for(n, l, a, 48)
+    O = Oracle(n, l, a, 48)
+    src_g = list(range(l - sc, l)) if sc <= 10 else [l + j for j in range(sc)]
+    dst_g = list(range(dc))
+    src = O.canonical(O.random_rows(Rng(sc * 100 + dc), np.array(src_g, np.uint32)), np.array(src_g, np.uint32))
+    got = ckks.bconv(C, dev(src), src_g, dst_g)
+    want = O.canonical(O.bconv(src.astype(np.int32), src_g, dst_g), np.array(dst_g, np.uint32))
+    np.testing.assert_array_equal(host(got), want)
+
+
+@pytest.mark.parametrize("r", [1, 3, -2, 1 << 14, 12345])
+def test_automorphism_and_group_law(r):
+    n, l, a = 65536, 4, 2
+    C = ctx_for(n, l, a, 48)
+    O = Oracle(n, l, a, 48)
+    x = O.random_rows(Rng(r & 0xFFFF), O.gidx(l))
+    p = ckks.Polynomial(dev(x), l)
+    got = host(ckks.apply_automorphism(C, p, r).data)
+    src = O.rotation_src_map(r)
+    np.testing.assert_array_equal(got, x[:, src].astype(np.uint32))
+    # rot_r then rot_-r is the identity (test_automorphism.cpp:29-39)
+    back = ckks.apply_automorphism(C, ckks.apply_automorphism(C, p, r), -r)
+    np.testing.assert_array_equal(host(back.data), x.astype(np.uint32))
+
+
+# --------------------------------------------------------- small fixtures ----
+@pytest.mark.parametrize("d", [pytest.param(d, id=d.name) for d in SMALL_DIRS])
+def test_mechanisms_equal_reference_fixtures(d):
+    fx = Fixture(d)
+    C = ctx_for(fx.n, fx.l, fx.alpha, fx.db)
+    np.testing.assert_array_equal(C.primes, fx.basis.primes)
+    l, a = fx.l, fx.alpha
+    u, v = fx.ct("ct_u"), fx.ct("ct_v")
+    cu = ckks.Ciphertext(dev(Fixture.ct_rows(u)), u.scale, l)
+    cv = ckks.Ciphertext(dev(Fixture.ct_rows(v)), v.scale, l)
+    relin = ckks.EvaluationKey(dev(fx.evk("evk_relin").stacked()), ckks.RELIN)
+    rot1 = ckks.EvaluationKey(dev(fx.evk("evk_rot1").stacked()), ckks.ROTATION, 1)
+    rot3 = ckks.EvaluationKey(dev(fx.evk("evk_rot3").stacked()), ckks.ROTATION, 3)
+
+    def eq(name, out):
+        ref = fx.ct(name)
+        assert out.level == ref.level, name
+        assert out.scale == ref.scale, name
+        assert out.pending_rescale == ref.pending_rescale, name
+        np.testing.assert_array_equal(host(out.data), Fixture.ct_rows(ref), err_msg=name)
+
+    eq("out_hmult", ckks.hmult(C, cu, cv, relin))
+    eq("out_hrot1", ckks.hrot(C, cu, 1, rot1))
+    eq("out_hrot3", ckks.hrot(C, cu, 3, rot3))
+    eq("out_rescale", ckks.rescale(C, cu))
+    eq("out_hadd", ckks.hadd(C, cu, cv))
+    pv = fx.poly("pt_v")
+    ptv = ckks.Plaintext(ckks.Polynomial(dev(pv.rows), l), Fraction(1 << fx.db), l)
+    eq("out_pmult", ckks.pmult(C, cu, ptv))
+    eq("out_padd", ckks.padd(C, cu, ptv))
+
+    d_a = ckks.Polynomial(dev(u.a.rows), l)
+    h = ckks.mod_up(C, d_a)
+    hh = host(h.digits)
+    for k in range(C.num_digits(l)):
+        np.testing.assert_array_equal(hh[k], fx.poly(f"out_modup_d{k}").rows)
+    v0, v1 = ckks.key_mult(C, h, relin)
+    np.testing.assert_array_equal(host(v0.data), fx.poly("out_keymult_v0").rows)
+    np.testing.assert_array_equal(host(v1.data), fx.poly("out_keymult_v1").rows)
+    np.testing.assert_array_equal(host(ckks.mod_down(C, v0).data), fx.poly("out_moddown_v0").rows)
+    c0, c1 = ckks.key_switch(C, d_a, relin)
+    np.testing.assert_array_equal(host(c0.data), fx.poly("out_keyswitch_c0").rows)
+    np.testing.assert_array_equal(host(c1.data), fx.poly("out_keyswitch_c1").rows)
+
+    hr = ckks.hoisted_rotations(C, cu, [1, 3], [rot1, rot3])
+    eq("out_hoisted_r1", hr[0])
+    eq("out_hoisted_r3", hr[1])
+    pts = [ckks.Plaintext(ckks.Polynomial(dev(fx.poly(f"pt_acc{i}").rows), l, a), Fraction(1 << fx.db), l)
+           for i in range(3)]
+    eq("out_hoisted_acc", ckks.hoisted_rotate_accumulate(C, cu, [0, 1, 3], pts, [None, rot1, rot3]))
+
+    coeff = fx.poly("in_ntt_coeff")
+    p = ckks.Polynomial(dev(coeff.rows), l, a, ckks.COEFFICIENT, False)
+    np.testing.assert_array_equal(host(ckks.ntt_forward(C, p).data), fx.poly("out_ntt_coeff").rows)
+    pb = ckks.Polynomial(dev(u.b.rows), l)
+    np.testing.assert_array_equal(host(ckks.intt_inverse(C, pb).data), fx.poly("out_intt_ctub").rows)
+
+    Cl = ctx_for(fx.n, fx.l, fx.alpha, fx.db, lazy=True)
+    eq("out_hmult_lazy", ckks.hmult(Cl, cu, cv, relin))
+
+
+# ---------------------------------------------------- full size (config 1/4) --
+FULL_IDS = [f"{c[0]}:{c[2]}@{c[3]}@{c[4]}" for c in full_cases()]
+
+
+@pytest.mark.parametrize("case", full_cases(), ids=FULL_IDS)
+def test_full_size_matches_reference_hash(case):
+    name, cfg, op, level, rot, h = case
+    n, l, a, db = cfg["n"], cfg["l"], cfg["alpha"], cfg["delta_bits"]
+    C = ctx_for(n, l, a, db, lazy=(op == "hmult_lazy"))
+    O = _oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(level, FULL["seed"])
+    x = ct(np.stack([xb, xa]), level)
+    y = ct(np.stack([yb, ya]), level)
+    kind = ckks.ROTATION if op == "hrot" else ckks.RELIN
+    K = ckks.EvaluationKey(dev(evk), kind, rot)
+    if op in ("hmult", "hmult_lazy"):
+        got = host(ckks.hmult(C, x, y, K).data)
+    elif op == "hrot":
+        got = host(ckks.hrot(C, x, rot, K).data)
+    elif op == "rescale":
+        got = host(ckks.rescale(C, x).data)
+    elif op == "key_switch":
+        c0, c1 = ckks.key_switch(C, ckks.Polynomial(dev(xa), level), K)
+        got = np.concatenate([host(c0.data), host(c1.data)])
+    elif op == "mod_up":
+        got = host(ckks.mod_up(C, ckks.Polynomial(dev(xa), level)).digits)
+    elif op == "ntt":
+        got = host(ckks.ntt_forward(C, ckks.Polynomial(dev(xb), level, 0, ckks.COEFFICIENT, False)).data)
+    elif op == "intt":
+        got = host(ckks.intt_inverse(C, ckks.Polynomial(dev(xb), level)).data)
+    else:
+        raise AssertionError(op)
+    assert sha(got) == h
+
+
+_OR = {}
+
+
+def _oracle(n, l, a, db):
+    if (n, l, a, db) not in _OR:
+        _OR[(n, l, a, db)] = Oracle(n, l, a, db)
+    return _OR[(n, l, a, db)]
+
+
+# ------------------------------------------------- oracle sweeps / batching --
+@pytest.mark.parametrize("level", [24, 23, 17, 9, 5, 4])
+def test_hmult_hrot_oracle_sweep_mid_size(level):
+    n, l, a, db = 4096, 24, 8, 55
+    C = ctx_for(n, l, a, db)
+    O = _oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(level, 99 + level)
+    x, y = ct(np.stack([xb, xa]), level), ct(np.stack([yb, ya]), level)
+    ob, oa = O.hmult(level, xb, xa, yb, ya, evk)
+    got = host(ckks.hmult(C, x, y, ckks.EvaluationKey(dev(evk))).data)
+    np.testing.assert_array_equal(got, np.stack([canon(O, ob, level - 2), canon(O, oa, level - 2)]))
+    for r in (1, -7, n // 4):
+        ob, oa = O.hrot(level, xb, xa, r, evk)
+        got = host(ckks.hrot(C, x, r, ckks.EvaluationKey(dev(evk), ckks.ROTATION, r)).data)
+        np.testing.assert_array_equal(got, np.stack([canon(O, ob, level), canon(O, oa, level)]))
+
+
+def test_batched_equals_unbatched():
+    n, l, a, db = 65536, 24, 8, 55
+    C = ctx_for(n, l, a, db)
+    O = _oracle(n, l, a, db)
+    B = 3
+    xs, ys = [], []
+    for b in range(B):
+        xb, xa, yb, ya, evk = O.synthetic(24, 500 + b)
+        xs.append(np.stack([xb, xa]))
+        ys.append(np.stack([yb, ya]))
+    K = ckks.EvaluationKey(dev(evk))
+    KR = ckks.EvaluationKey(K.data, ckks.ROTATION, 1)
+    X = ckks.Ciphertext(dev(np.stack(xs)), Fraction(1 << 55), 24)
+    Y = ckks.Ciphertext(dev(np.stack(ys)), Fraction(1 << 55), 24)
+    hm = host(ckks.hmult(C, X, Y, K).data)
+    hr = host(ckks.hrot(C, X, 1, KR).data)
+    for b in range(B):
+        one = host(ckks.hmult(C, ct(xs[b], 24), ct(ys[b], 24), K).data)
+        np.testing.assert_array_equal(hm[b], one)
+        one = host(ckks.hrot(C, ct(xs[b], 24), 1, KR).data)
+        np.testing.assert_array_equal(hr[b], one)
+
+
+def test_counters_follow_reference_profile():
+    # HMult at l=24: ntt 116, intt 44, bconv 5, keymult 3; HRot: ntt 120, intt 40
+    n, l, a, db = 1024, 24, 8, 55
+    C = ctx_for(n, l, a, db)
+    O = _oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(24, 1)
+    x, y = ct(np.stack([xb, xa]), 24), ct(np.stack([yb, ya]), 24)
+    C.reset_counters()
+    ckks.hmult(C, x, y, ckks.EvaluationKey(dev(evk)))
+    c = C.counters()
+    assert (c["modup"], c["moddown"], c["ntt"], c["intt"], c["keymult"], c["bconv"]) == (1, 1, 116, 44, 3, 5)
+    C.reset_counters()
+    ckks.hrot(C, x, 1, ckks.EvaluationKey(dev(evk), ckks.ROTATION, 1))
+    c = C.counters()
+    assert (c["modup"], c["moddown"], c["ntt"], c["intt"], c["keymult"], c["bconv"]) == (1, 1, 120, 40, 3, 5)
+
+
+def test_errors_mirror_reference():
+    n, l, a, db = 1024, 24, 8, 55
+    C = ctx_for(n, l, a, db)
+    O = _oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(4, 2)
+    x = ct(np.stack([xb, xa]), 4)
+    K = ckks.EvaluationKey(dev(evk))
+    with pytest.raises(ValueError):  # rotation key for hmult
+        ckks.hmult(C, x, x, ckks.EvaluationKey(K.data, ckks.ROTATION, 1))
+    with pytest.raises(ValueError):  # wrong rotation amount
+        ckks.hrot(C, x, 2, ckks.EvaluationKey(K.data, ckks.ROTATION, 1))
+    x2 = ct(np.stack([xb[:2], xa[:2]]), 2)
+    with pytest.raises(ValueError):  # level exhausted (ckks.cpp:815)
+        ckks.hmult(C, x2, x2, K)
+    with pytest.raises(ValueError):
+        ckks.rescale(C, x2)
+    bad = ckks.Ciphertext(x.data, x.scale * Fraction(1025, 1024), 4)
+    with pytest.raises(ValueError):  # scale mismatch beyond 2^-40 (ckks.cpp:131-136)
+        ckks.hadd(C, x, bad)
+    p = ckks.Polynomial(dev(xb), 4)
+    with pytest.raises(ValueError):  # domain discipline (ntt.cpp:290-292)
+        ckks.ntt_forward(C, p)
+    with pytest.raises(ValueError):
+        ckks.CkksContext(ckks.CkksParams(n=1000, l=4, alpha=2))
+
+
+def test_lazy_then_rescale_equals_merged_ledger():
+    # merged and lazy paths agree on level/scale after the deferred rescale (test_ckks.cpp:320-362)
+    n, l, a, db = 1024, 8, 2, 48
+    Cm, Cl = ctx_for(n, l, a, db), ctx_for(n, l, a, db, lazy=True)
+    O = _oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(8, 3)
+    s = Fraction(1 << 48)
+    x, y = ct(np.stack([xb, xa]), 8, s), ct(np.stack([yb, ya]), 8, s)
+    K = ckks.EvaluationKey(dev(evk))
+    pm = ckks.hmult(Cm, x, y, K)
+    pl = ckks.hmult(Cl, x, y, K)
+    assert pl.pending_rescale and pl.level == 8
+    pr = ckks.rescale(Cl, pl)
+    assert (pm.level, pm.scale) == (pr.level, pr.scale)
