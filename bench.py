@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RNS-CKKS hot path (BASELINE.json metric):
+HMult+relin and HRot throughput at N=2^16 (l=24, alpha=8, dnum=3).
+
+One step = one batch of B independent ciphertexts per GPU:
+    B x HMult+relinearize (merged ModDown+rescale, l=24 -> 22) and
+    B x HRot(r=1) (ModUp / KeyMult / ModDown / automorphism, l=24),
+inputs resident in HBM (`value`), and the same through the public API with
+the step's ciphertexts copied host->device from pinned memory and the results
+copied back (`e2e`).  Data-parallel over ranks (weak scaling, no collective in
+the step): `python -m torch.distributed.run --nproc-per-node N bench.py --gpus N`.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, built read-only from /root/reference) on the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from fractions import Fraction
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_RING, L, ALPHA, DB, LEVEL = 1 << 16, 24, 8, 55, 24
+METRIC = "HMult+relin & HRot ops/s at N=2^16 (l=24, alpha=8, dnum=3)"
+UNIT = "ops/s"
+LIMB = N_RING * 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=32, help="ciphertexts per GPU per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also report the HRot level sweep (config 2)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], "measured"
+    return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- CPU legs --
+def cpu_reference_times(reps: int, warmup: int):
+    """The reference's own mechanism benchmark (bench.cpp:332-389), all host cores."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from pyoracle import Reference
+
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    ref = Reference()
+    hm = ref.mechanism_bench("hmult", N_RING, L, ALPHA, DB, LEVEL, reps, warmup)
+    hr = ref.mechanism_bench("hrot", N_RING, L, ALPHA, DB, LEVEL, reps, warmup)
+    return hm, hr
+
+
+def cpu_baseline_leg():
+    try:
+        hm, hr = cpu_reference_times(reps=5, warmup=1)
+        per_pair = (hm["median_ns"] + hr["median_ns"]) * 1e-9
+        return {"value": round(2.0 / per_pair, 4), "unit": UNIT, "cores": hm["omp_threads"], "kind": "reference",
+                "sample": "reference bench::run_mechanism_bench hmult + hrot(r=1) at N=2^16 l=24 alpha=8, "
+                          "median of 5 reps each (1 ciphertext at a time, OpenMP inside the op)",
+                "hmult_ms": round(hm["median_ns"] / 1e6, 2), "hrot_ms": round(hr["median_ns"] / 1e6, 2),
+                "build": "reference sources -O3 as shipped (asserts live), Boost shim"}
+    except Exception as e:  # reference not built: fall back to the C restatement
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": f"{type(e).__name__}: {e}"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps, warm = max(args.steps, 1), max(args.warmup, 0)
+    hm, hr = cpu_reference_times(reps=steps, warmup=warm)
+    per_pair = (hm["median_ns"] + hr["median_ns"]) * 1e-9
+    v = 2.0 / per_pair
+    line = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": round(per_pair * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32 residues (u32 mod q < 2^29, int64 accum)",
+            "data": "synthetic (reference keygen/encrypt of random unit-disk slots, seed 42)",
+            "config": {"workload": "1 HMult+relin + 1 HRot(r=1) per step at N=2^16, l=24, alpha=8, dnum=3 "
+                                   "(reference CPU path, one ciphertext at a time)", "n": N_RING, "l": L,
+                       "alpha": ALPHA, "level": LEVEL},
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": hm["omp_threads"], "kind": "reference",
+                             "sample": f"median of {steps} reps of hmult and of hrot via bench::run_mechanism_bench"},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "hmult_ms": round(hm["median_ns"] / 1e6, 2), "hrot_ms": round(hr["median_ns"] / 1e6, 2)}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------- GPU leg ----
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_13055_b200 import ckks
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    B = args.batch
+    C = ckks.CkksContext(ckks.CkksParams(n=N_RING, l=L, alpha=ALPHA, delta_bits=DB), device=local)
+    q = torch.tensor(C.primes.astype(np.int64), device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    def rand_rows(shape_prefix, rows_q):  # uniform residues per row (synthetic)
+        u = torch.randint(0, 1 << 62, (*shape_prefix, len(rows_q), N_RING), device=dev, generator=gen,
+                          dtype=torch.int64)
+        return (u % q[rows_q].view(*([1] * len(shape_prefix)), -1, 1)).to(torch.int32).contiguous()
+
+    qrows = torch.arange(LEVEL, device=dev)
+    full = torch.cat([torch.arange(L, device=dev), L + torch.arange(ALPHA, device=dev)])
+    D = C.num_digits(L)
+    relin = ckks.EvaluationKey(rand_rows((D, 2), full), ckks.RELIN)
+    rot = ckks.EvaluationKey(rand_rows((D, 2), full), ckks.ROTATION, 1)
+    s = Fraction(1 << DB)
+    X = ckks.Ciphertext(rand_rows((B, 2), qrows), s, LEVEL)
+    Y = ckks.Ciphertext(rand_rows((B, 2), qrows), s, LEVEL)
+    st = torch.cuda.current_stream(dev)
+
+    def step():
+        o1 = ckks.hmult(C, X, Y, relin)
+        o2 = ckks.hrot(C, X, 1, rot)
+        return o1, o2
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- main timed region: inputs resident in HBM (B x 25 MB >> 126 MB L2)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps)]
+    l0 = C.launch_count()
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(st)
+        for k in range(args.steps):
+            ev[3 * k].record(st)
+            ckks.hmult(C, X, Y, relin)
+            ev[3 * k + 1].record(st)
+            ckks.hrot(C, X, 1, rot)
+            ev[3 * k + 2].record(st)
+        t_end.record(st)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = C.launch_count() - l0
+    ms = t_start.elapsed_time(t_end)
+    hm_ms = sum(ev[3 * k].elapsed_time(ev[3 * k + 1]) for k in range(args.steps))
+    hr_ms = sum(ev[3 * k + 1].elapsed_time(ev[3 * k + 2]) for k in range(args.steps))
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms, hm_ms, hr_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max, hm_ms, hr_ms = t.tolist()
+    ops_total = 2 * B * args.steps * world
+    value = ops_total / (ms_max / 1e3)
+
+    # ---- per-kernel-class breakdown (CUDA events around every launch group)
+    C.profile(True)
+    for _ in range(max(1, min(args.steps, 3))):
+        step()
+    prof = C.profile_read()
+    C.profile(False)
+    hbm, peak_kind = peaks()
+    tot_ms = sum(p["ms"] for p in prof) or 1.0
+    dom = max(prof, key=lambda p: p["ms"])
+    ntt = next(p for p in prof if p["name"] == "ntt_fwd")
+    kern = []
+    for p in prof:
+        if p["groups"]:
+            kern.append({"kernel": p["name"], "share": round(p["ms"] / tot_ms, 4),
+                         "GBps": round(p["bytes"] / (p["ms"] * 1e6), 1),
+                         "frac": round(p["bytes"] / (p["ms"] * 1e6) / hbm, 4)})
+
+    def roof(p):
+        ach = p["bytes"] / (p["ms"] * 1e6)
+        return {"kernel": p["name"], "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": None, "peak_kind": peak_kind,
+                "bytes_per_launch_group": round(p["bytes"] / max(p["groups"], 1)),
+                "avg_group_ms": round(p["ms"] / max(p["groups"], 1), 4)}
+
+    # ---- e2e: host ciphertexts in pinned memory, H2D + compute + D2H every step
+    e2e = None
+    if not args.no_e2e:
+        Be = B
+        hx = torch.empty((Be, 2, LEVEL, N_RING), dtype=torch.int32).pin_memory()
+        hy = torch.empty_like(hx).pin_memory()
+        hx.copy_(X.data[:Be].cpu())
+        hy.copy_(Y.data[:Be].cpu())
+        ho1 = torch.empty((Be, 2, LEVEL - 2, N_RING), dtype=torch.int32).pin_memory()
+        ho2 = torch.empty((Be, 2, LEVEL, N_RING), dtype=torch.int32).pin_memory()
+        dx = torch.empty_like(X.data[:Be])
+        dy = torch.empty_like(dx)
+
+        def e2e_step():
+            dx.copy_(hx, non_blocking=True)
+            dy.copy_(hy, non_blocking=True)
+            o1 = ckks.hmult(C, ckks.Ciphertext(dx, s, LEVEL), ckks.Ciphertext(dy, s, LEVEL), relin)
+            o2 = ckks.hrot(C, ckks.Ciphertext(dx, s, LEVEL), 1, rot)
+            ho1.copy_(o1.data, non_blocking=True)
+            ho2.copy_(o2.data, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        e_ms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = t.item()
+        e2e = {"value": round(2 * Be * args.steps * world / (e_ms / 1e3), 2), "unit": UNIT,
+               "h2d_bytes_per_step": int(hx.numel() * 4 * 2), "d2h_bytes_per_step": int((ho1.numel() + ho2.numel()) * 4),
+               "path": "ckks.hmult / ckks.hrot (C ABI) on ciphertexts copied from pinned host memory; results copied "
+                       "back each step"}
+
+    sweep = None
+    if args.sweep:
+        sweep = {}
+        for lv in range(LEVEL, 0, -2):
+            Xl = ckks.Ciphertext(X.data[:, :, :lv].contiguous(), s, lv)
+            ckks.hrot(C, Xl, 1, rot)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            for _ in range(3):
+                ckks.hrot(C, Xl, 1, rot)
+            b.record(st)
+            torch.cuda.synchronize(dev)
+            sweep[lv] = round(3 * B / (a.elapsed_time(b) / 1e3), 1)
+
+    if rank == 0:
+        cpu = None if args.no_cpu or world > 1 else cpu_baseline_leg()
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32 residues (u32 mod q < 2^29, int64 accum)",
+            "data": "synthetic uniform residues (ciphertexts and keys), random-init",
+            "config": {"workload": f"per GPU per step: {B} x HMult+relin (merged rescale, l=24->22) + {B} x HRot(r=1) "
+                                   f"at N=2^16, l=24, alpha=8, dnum=3 (configs[1]/[2] of BASELINE.json)",
+                       "n": N_RING, "l": L, "alpha": ALPHA, "level": LEVEL, "batch_per_gpu": B,
+                       "parallelism": f"dp{world} (independent ciphertexts, no collective)",
+                       "l2": "inputs larger than L2 (2 x B x 12 MiB ciphertext pairs per step); keys stay L2-resident"},
+            "hmult_ops_per_s": round(B * args.steps * world / (hm_ms / 1e3), 2),
+            "hrot_ops_per_s": round(B * args.steps * world / (hr_ms / 1e3), 2),
+            "roofline": roof(dom),
+            "roofline_ntt": roof(ntt),
+            "kernels": kern,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        if sweep:
+            line["hrot_level_sweep_ops_per_s"] = sweep
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -151,6 +151,22 @@ ck_status ck_hoisted_rotate_accumulate(ck_context* ctx, uint32_t level, const ui
  * (evidence for bench.py's gpu_launches). */
 uint64_t ck_launch_count(const ck_context* ctx);
 
+/* Per-kernel-class CUDA-event timing (no reference counterpart; the
+ * reference times whole mechanisms with steady_clock, bench.cpp:105-110).
+ * ck_profile(ctx, 1) clears and starts recording an event pair around every
+ * launch group; ck_profile_read synchronises and returns one entry per class
+ * (ntt_fwd, ntt_inv, bconv, key_mult, tensor, combine, hrot_tail) with the
+ * summed device time and the algorithmic bytes of SURVEY.md §8(d). */
+typedef struct {
+  char name[16];
+  uint64_t groups;   /* event-bracketed launch groups */
+  uint64_t launches; /* kernel launches inside them */
+  double ms;         /* summed event time */
+  double bytes;      /* summed algorithmic bytes (read + write once) */
+} ck_prof_stat;
+ck_status ck_profile(ck_context* ctx, int enable);
+ck_status ck_profile_read(ck_context* ctx, ck_prof_stat* out, uint32_t max_classes, uint32_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,11 @@ class CkCudaError(RuntimeError):
     pass
 
 
+class ck_prof_stat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 16), ("groups", ctypes.c_uint64), ("launches", ctypes.c_uint64),
+                ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
 class ck_params(ctypes.Structure):
     _fields_ = [("n", ctypes.c_uint32), ("l", ctypes.c_uint32), ("alpha", ctypes.c_uint32),
                 ("delta_bits", ctypes.c_uint32), ("lazy_rescale", ctypes.c_int32)]
@@ -43,6 +48,8 @@ _SIGS = {
     "ck_memcpy_h2d": [_vp, _vp, _vp, ctypes.c_size_t, _vp],
     "ck_memcpy_d2h": [_vp, _vp, _vp, ctypes.c_size_t, _vp],
     "ck_stream_sync": [_vp, _vp],
+    "ck_profile": [_vp, ctypes.c_int],
+    "ck_profile_read": [_vp, ctypes.POINTER(ck_prof_stat), _u32, ctypes.POINTER(ctypes.c_uint32)],
     "ck_ntt_forward": [_vp, _vp, _u32, _u32p, _vp],
     "ck_intt_inverse": [_vp, _vp, _u32, _u32p, _u32p, _vp],
     "ck_bconv": [_vp, _vp, _u32, _u32p, _vp, _u32, _u32p, _vp],

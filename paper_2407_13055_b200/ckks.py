@@ -100,6 +100,17 @@ class CkksContext:
     def reset_counters(self) -> None:
         nat.call("ck_context_reset_counters", self._h)
 
+    def profile(self, enable: bool = True) -> None:
+        """Start (clear) / stop per-kernel-class CUDA-event timing."""
+        nat.call("ck_profile", self._h, int(enable))
+
+    def profile_read(self) -> List[dict]:
+        buf = (nat.ck_prof_stat * 16)()
+        cnt = ctypes.c_uint32()
+        nat.call("ck_profile_read", self._h, buf, 16, ctypes.byref(cnt))
+        return [{"name": s.name.decode(), "groups": s.groups, "launches": s.launches, "ms": s.ms, "bytes": s.bytes}
+                for s in buf[: cnt.value]]
+
     def launch_count(self) -> int:
         return int(nat.lib().ck_launch_count(self._h))
 

@@ -208,6 +208,7 @@ struct BconvPlan {
   Blob blob;
   size_t groups_off = 0, cmat_off = 0, row_off = 0, prime_off = 0;
   int ngroups = 0, max_sc = 1;
+  uint64_t src_rows = 0, dst_rows = 0;  // algorithmic rows read / written per batch item
 };
 // ModUp at one level: INTT(+part1) of the level rows, per-digit BConv, NTT.
 struct ModUpPlan {
@@ -248,6 +249,51 @@ struct Context {
   size_t scratch_bytes = 0;
   uint64_t counters[7] = {0, 0, 0, 0, 0, 0, 0};  // modup moddown ntt intt keymult bconv rescale
   std::atomic<uint64_t> launches{0};
+
+  // Optional per-kernel-class CUDA-event timing (ck_profile): each launch
+  // group is bracketed by events on its own stream; algorithmic bytes per
+  // launch follow SURVEY.md §8(d).
+  struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes;
+    uint64_t launches;
+  };
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t ev_get() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      CK_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  struct ProfScope {
+    Context* c;
+    cudaStream_t st;
+    int cls;
+    double bytes;
+    uint64_t nl;
+    cudaEvent_t a = nullptr;
+    ProfScope(Context* c_, int cls_, double bytes_, uint64_t nl_, cudaStream_t st_)
+        : c(c_), st(st_), cls(cls_), bytes(bytes_), nl(nl_) {
+      if (c->prof) {
+        a = c->ev_get();
+        cudaEventRecord(a, st);
+      }
+    }
+    ~ProfScope() {
+      if (a) {
+        cudaEvent_t b = c->ev_get();
+        cudaEventRecord(b, st);
+        c->prof_recs.push_back({cls, a, b, bytes, nl});
+      }
+    }
+  };
 
   ~Context() {
     cudaSetDevice(device);
@@ -375,6 +421,8 @@ struct Context {
     pl->bc.prime_off = pl->bc.blob.add(dprime);
     pl->bc.ngroups = (int)groups.size();
     pl->bc.max_sc = max_sc;
+    pl->bc.src_rows = level;
+    pl->bc.dst_rows = drow.size();
     pl->bc.blob.upload();
     auto& ref = *pl;
     modup[level] = std::move(pl);
@@ -443,6 +491,8 @@ struct Context {
     pl->bc.prime_off = pl->bc.blob.add(dprime);
     pl->bc.ngroups = (int)groups.size();
     pl->bc.max_sc = (int)sc;
+    pl->bc.src_rows = (uint64_t)npoly * sc;
+    pl->bc.dst_rows = (uint64_t)npoly * out_q;
     pl->bc.blob.upload();
     // divisor = product of the source primes; one Montgomery inverse per row
     std::vector<uint32_t> dinv(out_q);
@@ -496,6 +546,7 @@ struct Context {
     a.tw = inverse ? d_inv : d_fwd;
     a.exits = inverse ? pl.blob.at<ExitConst>(pl.exits_off) : nullptr;
     a.entry = entry;
+    ProfScope ps(this, inverse ? 1 : 0, 8.0 * n * pl.njobs * batch, 2, st);
     if (inverse)
       ntt_inverse((int)logn, a, st);
     else
@@ -518,6 +569,7 @@ struct Context {
     a.dst_row = pl.blob.at<uint32_t>(pl.row_off);
     a.dst_prime = pl.blob.at<uint16_t>(pl.prime_off);
     a.primes = d_primes;
+    ProfScope ps(this, 2, 4.0 * n * (pl.src_rows + pl.dst_rows) * batch, 1, st);
     bconv((int)n, a, st);
     ++launches;
   }
@@ -559,6 +611,9 @@ struct Context {
     a.v = v;
     a.v_bs = 2ull * (level + alpha) * n;
     a.primes = d_primes;
+    // reads: D operand rows + 2D key rows per output row (+ d0, d1 for folded Q rows); writes v0, v1
+    ProfScope ps(this, 3, 4.0 * n * (level + alpha) * (3.0 * a.D + 2) * B + (fold ? 8.0 * n * level * B : 0.0), 1,
+                 st);
     key_mult((int)n, a, st);
     ++launches;
     counters[4] += (uint64_t)B * a.D;
@@ -575,6 +630,7 @@ struct Context {
     run_bconv(pl.bc, B, ts, (uint64_t)pl.npoly * pl.sc * N, o, (uint64_t)pl.npoly * pl.out_q * N, st);
     run_ntt(pl.ntt, false, B, o, (uint64_t)pl.npoly * pl.out_q * N, o, (uint64_t)pl.npoly * pl.out_q * N, 1, st);
     if (combine_now) {
+      ProfScope ps(this, 5, 12.0 * n * pl.out_q * pl.npoly * B, 1, st);
       combine((int)n, (int)pl.out_q, (int)pl.npoly, B, v, prow * N, v_bs, o, pl.out_q * N,
               (uint64_t)pl.npoly * pl.out_q * N, pl.consts.at<uint32_t>(0), d_primes, st);
       ++launches;
@@ -745,6 +801,44 @@ ck_status ck_context_counters(const ck_context* ctx, uint64_t out[7]) {
 ck_status ck_context_reset_counters(ck_context* ctx) {
   return guard([&] { std::fill(C(ctx)->counters, C(ctx)->counters + 7, 0); });
 }
+ck_status ck_profile(ck_context* ctx, int enable) {
+  return guard([&] {
+    Context* c = C(ctx);
+    CK_CUDA(cudaDeviceSynchronize());
+    for (auto& r : c->prof_recs) {
+      c->ev_pool.push_back(r.a);
+      c->ev_pool.push_back(r.b);
+    }
+    c->prof_recs.clear();
+    c->prof = enable != 0;
+  });
+}
+
+ck_status ck_profile_read(ck_context* ctx, ck_prof_stat* out, uint32_t max_classes, uint32_t* count) {
+  return guard([&] {
+    Context* c = C(ctx);
+    static const char* names[] = {"ntt_fwd", "ntt_inv", "bconv", "key_mult", "tensor", "combine", "hrot_tail"};
+    const uint32_t ncls = 7;
+    if (!out || !count) throw InvalidArgument("null argument");
+    CK_CUDA(cudaDeviceSynchronize());
+    std::vector<ck_prof_stat> st(ncls);
+    for (uint32_t i = 0; i < ncls; ++i) {
+      std::memset(&st[i], 0, sizeof(ck_prof_stat));
+      std::snprintf(st[i].name, sizeof(st[i].name), "%s", names[i]);
+    }
+    for (auto& r : c->prof_recs) {
+      float ms = 0;
+      CK_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      st[r.cls].groups += 1;
+      st[r.cls].launches += r.launches;
+      st[r.cls].ms += ms;
+      st[r.cls].bytes += r.bytes;
+    }
+    *count = std::min(ncls, max_classes);
+    std::copy(st.begin(), st.begin() + *count, out);
+  });
+}
+
 uint64_t ck_launch_count(const ck_context* ctx) {
   return ctx ? reinterpret_cast<const Context*>(ctx)->launches.load() : 0;
 }
@@ -862,6 +956,8 @@ ck_status ck_bconv(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count,
       pl->prime_off = pl->blob.add(dprime);
       pl->ngroups = 1;
       pl->max_sc = (int)src_count;
+      pl->src_rows = src_count;
+      pl->dst_rows = dst_count;
       pl->blob.upload();
     }
     c->run_bconv(*pl, 1, src_dev, 0, dst_dev, 0, S(stream));
@@ -1031,7 +1127,10 @@ ck_status ck_hmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32
     uint32_t* ts = v + v_w * B;
     uint32_t* cc = ts + ts_w * B;
     cudaStream_t st = S(stream);
-    tensor((int)N, (int)level, B, x, y, 2ull * level * N, t01, t01_w, d2, d2_w, c->d_primes, st);
+    {
+      Context::ProfScope ps(c, 4, 4.0 * N * level * 7 * B, 1, st);  // 4 rows in, 3 out
+      tensor((int)N, (int)level, B, x, y, 2ull * level * N, t01, t01_w, d2, d2_w, c->d_primes, st);
+    }
     ++c->launches;
     c->mod_up(level, B, d2, d2_w, is, ext, st);
     if (!lazy) {
@@ -1079,8 +1178,11 @@ ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_
     c->mod_up(level, B, a, ct_bs, is, ext, st);
     c->key_mult_v(level, B, ext, a, ct_bs, rot_evk, nullptr, 0, v, st);
     c->drop_divide(pl, B, v, v_w, ts, o, false, st);
-    hrot_tail((int)N, (int)level, B, v, v_w, rows * N, o, o_w, level * N, ct, ct_bs, pl.consts.at<uint32_t>(0),
-              c->rotation_map(r), out, ct_bs, c->d_primes, st);
+    {
+      Context::ProfScope ps(c, 6, 4.0 * N * level * 7 * B, 1, st);  // v0 v1 o0 o1 b in, 2 out
+      hrot_tail((int)N, (int)level, B, v, v_w, rows * N, o, o_w, level * N, ct, ct_bs, pl.consts.at<uint32_t>(0),
+                c->rotation_map(r), out, ct_bs, c->d_primes, st);
+    }
     ++c->launches;
     c->counters[1] += B;
     check_launch();
