@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -239,6 +240,9 @@ struct Context {
   uint2* d_fwd = nullptr;
   uint2* d_inv = nullptr;
   uint32_t* d_pmont = nullptr;  // P mod q_i (Montgomery), i < L
+  uint2* d_tw2f = nullptr;      // N = 2^16 row-pass tables (ntt256.cu), per-row permuted
+  uint2* d_tw2i = nullptr;
+  bool use_ntt256 = true;
   std::map<uint32_t, std::unique_ptr<ModUpPlan>> modup;
   std::map<std::tuple<int, uint32_t, uint32_t>, std::unique_ptr<SwitchPlan>> switches;
   std::map<int64_t, uint32_t*> rot_maps;
@@ -303,6 +307,8 @@ struct Context {
     if (d_fwd) cudaFree(d_fwd);
     if (d_inv) cudaFree(d_inv);
     if (d_pmont) cudaFree(d_pmont);
+    if (d_tw2f) cudaFree(d_tw2f);
+    if (d_tw2i) cudaFree(d_tw2i);
     if (scratch) cudaFree(scratch);
   }
 
@@ -547,10 +553,16 @@ struct Context {
     a.exits = inverse ? pl.blob.at<ExitConst>(pl.exits_off) : nullptr;
     a.entry = entry;
     ProfScope ps(this, inverse ? 1 : 0, 8.0 * n * pl.njobs * batch, 2, st);
-    if (inverse)
+    if (logn == 16 && d_tw2f && use_ntt256) {
+      if (inverse)
+        ntt256_inverse(a, d_tw2i, st);
+      else
+        ntt256_forward(a, d_tw2f, st);
+    } else if (inverse) {
       ntt_inverse((int)logn, a, st);
-    else
+    } else {
       ntt_forward((int)logn, a, st);
+    }
     launches += 2;
   }
   void run_bconv(const BconvPlan& pl, int batch, const uint32_t* src, uint64_t src_bs, uint32_t* dst, uint64_t dst_bs,
@@ -758,6 +770,44 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     CK_CUDA(cudaMemcpy(c->d_fwd, fwd.data(), fwd.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     CK_CUDA(cudaMalloc(&c->d_inv, inv.size() * sizeof(uint2)));
     CK_CUDA(cudaMemcpy(c->d_inv, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    c->use_ntt256 = std::getenv("CK32_GENERIC_NTT") == nullptr;  // A/B switch for parity tests
+    if (n == 65536) {
+      // Row-pass twiddles of ntt256.cu, permuted per row in thread-consumption
+      // order (same values as the reference tables, ntt.cpp:124-128).
+      std::vector<uint2> t2f((size_t)np * n), t2i((size_t)np * n);
+#pragma omp parallel for schedule(static)
+      for (int g = 0; g < (int)np; ++g) {
+        const uint2* F = fwd.data() + (size_t)g * n;
+        const uint2* I = inv.data() + (size_t)g * n;
+        for (uint32_t r = 0; r < 256; ++r) {
+          uint2* A = t2f.data() + ((size_t)g * 256 + r) * 256;
+          uint2* B = t2i.data() + ((size_t)g * 256 + r) * 256;
+          A[15] = B[255] = make_uint2(0, 0);
+          for (uint32_t s = 0; s < 4; ++s)  // forward phase A: stage 8+s, blk < 2^s
+            for (uint32_t blk = 0; blk < (1u << s); ++blk)
+              A[(1u << s) - 1 + blk] = F[(256u << s) + (r << s) + blk];
+          for (uint32_t s = 4; s < 8; ++s)  // forward phase B: stage 8+s, blk < 2^(s-4), thread tau
+            for (uint32_t blk = 0; blk < (1u << (s - 4)); ++blk)
+              for (uint32_t tau = 0; tau < 16; ++tau)
+                A[16 + ((1u << (s - 4)) - 1 + blk) * 16 + tau] = F[(256u << s) + (r << s) + (tau << (s - 4)) + blk];
+          for (uint32_t v = 0; v < 4; ++v) {  // inverse phase A: stage v, blk < 2^(3-v), thread tau
+            const uint32_t off = 16 - (16 >> v);
+            for (uint32_t blk = 0; blk < (8u >> v); ++blk)
+              for (uint32_t tau = 0; tau < 16; ++tau)
+                B[(off + blk) * 16 + tau] = I[(32768u >> v) + (r << (7 - v)) + (tau << (3 - v)) + blk];
+          }
+          for (uint32_t v = 4; v < 8; ++v) {  // inverse phase B: stage v, blk < 2^(7-v)
+            const uint32_t off = 16 - (16 >> (v - 4));
+            for (uint32_t blk = 0; blk < (128u >> v); ++blk)
+              B[240 + off + blk] = I[(32768u >> v) + (r << (7 - v)) + blk];
+          }
+        }
+      }
+      CK_CUDA(cudaMalloc(&c->d_tw2f, t2f.size() * sizeof(uint2)));
+      CK_CUDA(cudaMemcpy(c->d_tw2f, t2f.data(), t2f.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+      CK_CUDA(cudaMalloc(&c->d_tw2i, t2i.size() * sizeof(uint2)));
+      CK_CUDA(cudaMemcpy(c->d_tw2i, t2i.data(), t2i.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    }
     std::vector<uint32_t> pm(p.l);  // p_mont (ckks.cpp:171-175)
     for (uint32_t i = 0; i < p.l; ++i) {
       const uint32_t q = c->primes[i];

@@ -23,6 +23,10 @@ struct NttLaunch {
 };
 void ntt_forward(int logn, const NttLaunch& a, cudaStream_t st);
 void ntt_inverse(int logn, const NttLaunch& a, cudaStream_t st);
+// N = 2^16 specialisation (ntt256.cu); tw2 / tw2i are the per-row permuted
+// row-pass tables built by the host ([prime][256 rows][256] {w, w'}).
+bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st);
+bool ntt256_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st);
 
 // One base-conversion group: src rows [src_off, src_off+sc) of the source
 // buffer, dc destination rows dst_row[map_off + i] (row offsets in the
