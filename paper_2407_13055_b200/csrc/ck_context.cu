@@ -243,6 +243,7 @@ struct Context {
   uint2* d_tw2f = nullptr;      // N = 2^16 row-pass tables (ntt256.cu), per-row permuted
   uint2* d_tw2i = nullptr;
   bool use_ntt256 = true;
+  int ntt_chunk_limbs = 1 << 30;  // limbs per pass-1/pass-2 launch pair (CK32_NTT_CHUNK; measured: no gain)
   std::map<uint32_t, std::unique_ptr<ModUpPlan>> modup;
   std::map<std::tuple<int, uint32_t, uint32_t>, std::unique_ptr<SwitchPlan>> switches;
   std::map<int64_t, uint32_t*> rot_maps;
@@ -554,10 +555,27 @@ struct Context {
     a.entry = entry;
     ProfScope ps(this, inverse ? 1 : 0, 8.0 * n * pl.njobs * batch, 2, st);
     if (logn == 16 && d_tw2f && use_ntt256) {
-      if (inverse)
-        ntt256_inverse(a, d_tw2i, st);
-      else
-        ntt256_forward(a, d_tw2f, st);
+      // L2-resident chunks: pass 2 of a chunk reads pass 1's output while it
+      // is still in the 126 MB L2, so each limb crosses HBM once each way.
+      const int chunk = ntt_chunk_limbs;
+      const int bchunk = std::max(1, std::min(batch, chunk));
+      const int jchunk = std::max(1, chunk / bchunk);
+      for (int j0 = 0; j0 < pl.njobs; j0 += jchunk) {
+        for (int b0 = 0; b0 < batch; b0 += bchunk) {
+          NttLaunch c = a;
+          c.jobs = a.jobs + j0;
+          c.njobs = std::min(jchunk, pl.njobs - j0);
+          c.batch = std::min(bchunk, batch - b0);
+          c.src = src + (uint64_t)b0 * src_bs;
+          c.dst = dst + (uint64_t)b0 * dst_bs;
+          if (inverse)
+            ntt256_inverse(c, d_tw2i, st);
+          else
+            ntt256_forward(c, d_tw2f, st);
+          launches += 2;
+        }
+      }
+      launches -= 2;
     } else if (inverse) {
       ntt_inverse((int)logn, a, st);
     } else {
@@ -771,6 +789,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     CK_CUDA(cudaMalloc(&c->d_inv, inv.size() * sizeof(uint2)));
     CK_CUDA(cudaMemcpy(c->d_inv, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     c->use_ntt256 = std::getenv("CK32_GENERIC_NTT") == nullptr;  // A/B switch for parity tests
+    if (const char* ch = std::getenv("CK32_NTT_CHUNK")) c->ntt_chunk_limbs = std::max(1, std::atoi(ch));
     if (n == 65536) {
       // Row-pass twiddles of ntt256.cu, permuted per row in thread-consumption
       // order (same values as the reference tables, ntt.cpp:124-128).

@@ -1,23 +1,24 @@
 // N = 2^16 NTT / INTT specialised for sm_100a (256 x 256 decomposition).
 //
-// Same transform as ntt.cpp:176-272 (and the generic kernels in ntt.cu), but
-// every data movement is a full-width coalesced access and every twiddle is
-// either a warp-broadcast or a coalesced load of a per-row table laid out in
-// the order the threads consume it:
+// Same transform as ntt.cpp:176-272 (and the generic kernels in ntt.cu):
+// forward = DIF Cooley-Tukey, natural -> bit-reversed, Montgomery entry merge;
+// inverse = Gentleman-Sande, exit merge with the fused BConv part-1 factor.
 //
-//  column pass (fwd stages 0-7, inverse stages 8-15 + exit):
-//    a thread owns 4 adjacent columns (one uint4) x 16 rows.  Phase A reads
-//    16 uint4 straight from HBM, runs 4 radix-2 stages on all 4 columns with
-//    one twiddle per 4 butterflies, one smem transpose (uint4, conflict-free),
-//    phase B runs the other 4 stages and writes 16 uint4 straight back.
-//  row pass (fwd stages 8-15, inverse stages 0-7):
-//    16 threads (half a warp) own one 256-point row, 16 elements each; the
-//    exchange is a warp-local smem transpose (no CTA barrier).  The row's 30
-//    twiddle pairs are held in registers and reused for every batch item of
-//    the job (same prime), so twiddle traffic is amortised over the batch.
-//
-// Butterflies are Harvey-lazy Shoup (3 multiply-pipe ops each; IMAD.HI is
-// quarter rate on sm_100a, see tools/microbench_int.cu): values in [0, 4q).
+// Structure (one kernel per pass, persistent CTAs):
+//  * work items are tiles of one limb: 256 rows x 32 columns (column pass) or
+//    16 rows x 256 (row pass); every CTA loops over its items and
+//    double-buffers them in shared memory with cp.async (16-byte, L1
+//    bypass), so HBM streaming of item k+1 overlaps the butterflies of item k;
+//  * column pass: a thread owns 4 adjacent columns (uint4) x 16 rows, runs 4
+//    radix-2 stages (one twiddle per 4 butterflies, warp-broadcast from the
+//    tile's 256-entry table), writes back in place, then reads the transposed
+//    16 rows and runs the other 4 stages, storing 16 uint4 straight to HBM;
+//  * row pass: 16 threads (half a warp) own a 256-point row; the exchange is
+//    warp-local (no CTA barrier); the row's 30 twiddle pairs live in
+//    registers and are reused across consecutive batch items of the job.
+// Butterflies: Harvey-lazy Shoup (IMAD.HI + 2 IMAD, values in [0, 4q)).
+#include <cstdlib>
+
 #include "ck_common.cuh"
 #include "ck_kernels.h"
 
@@ -27,10 +28,18 @@ namespace {
 constexpr int kN = 65536;
 constexpr int kR = 256;
 
-__device__ __forceinline__ uint4 ldg4(const uint32_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ void stg4(uint32_t* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+}
 
-// forward CT butterfly on one lane, Harvey lazy: x,y in [0,4q) -> [0,4q)
+// forward CT butterfly, Harvey lazy: x,y in [0,4q) -> [0,4q)
 __device__ __forceinline__ void ct(uint32_t& x, uint32_t& y, uint32_t w, uint32_t wp, uint32_t q, uint32_t q2) {
   const uint32_t xx = sub_if(x, q2);
   const uint32_t t = shoup_mul(y, w, wp, q);
@@ -56,306 +65,398 @@ __device__ __forceinline__ void gs4(uint4& x, uint4& y, uint2 w, uint32_t q, uin
   gs(x.w, y.w, w.x, w.y, q, q2);
 }
 
-// Column tile: 256 rows x 64 columns; thread (tau = tid>>4, cq = tid&15).
-constexpr int kColTileCols = 64;
-constexpr int kColSmem = 256 * 16 * 16 + 256 * 8;  // uint4 tile + 256 twiddle pairs
+// ============================================================ column pass ==
+constexpr int kCT = 128;              // threads: tau = tid>>3 (16), cq = tid&7 (8)
+constexpr int kCCols = 32;            // columns per tile
+constexpr int kCTiles = kR / kCCols;  // 8 tiles per limb
+struct ColBuf {
+  uint4 tile[256 * (kCCols / 4)];  // [row][quad], 32 KB
+  uint2 tw[256];                   // the prime's first 256 twiddle pairs
+};
+constexpr int kColSmem = 2 * sizeof(ColBuf);
 
-// ------------------------------------------------------- forward, pass 1 --
-__global__ void __launch_bounds__(256, 2) k_fwd_col(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
-                                                    uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs,
-                                                    int batch, const PrimeDev* __restrict__ primes,
-                                                    const uint2* __restrict__ fwd_tw, int entry) {
-  extern __shared__ uint4 smc[];
-  uint4* tile = smc;                                   // [256][16]
-  uint2* tw = reinterpret_cast<uint2*>(smc + 256 * 16);  // [256]
-  const RowJob job = jobs[blockIdx.y];
-  const PrimeDev P = primes[job.prime];
-  const uint32_t q = P.q, q2 = P.q2;
-  const int tid = threadIdx.x, cq = tid & 15, tau = tid >> 4;
-  tw[tid] = __ldg(&fwd_tw[(size_t)job.prime * kN + tid]);
-  const int c0 = blockIdx.x * kColTileCols + 4 * cq;
-  __syncthreads();
-  for (int b = 0; b < batch; ++b) {
-    const uint32_t* g = src + b * src_bs + (size_t)job.src_off * kN + c0;
-    uint32_t* o = dst + b * dst_bs + (size_t)job.dst_off * kN + c0;
+__device__ __forceinline__ void col_prefetch(ColBuf& B, const uint32_t* g, const uint2* tw) {
+  // 256 rows x 128 B + 2 KB of twiddles, 16 B per cp.async
+  for (int e = threadIdx.x; e < 256 * 8; e += kCT) {
+    const int r = e >> 3, c4 = e & 7;
+    cp16(&B.tile[r * 8 + c4], g + r * kR + 4 * c4);
+  }
+  cp16(&B.tw[2 * threadIdx.x], tw + 2 * threadIdx.x);
+}
+
+// Decode the i-th column-pass item: tile fastest, then batch, then job.
+__device__ __forceinline__ void col_item(int it, int batch, int& job, int& b, int& tile) {
+  tile = it % kCTiles;
+  const int rest = it / kCTiles;
+  b = rest % batch;
+  job = rest / batch;
+}
+
+template <bool INV, bool DB>
+__global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
+                                             uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
+                                             int njobs, const PrimeDev* __restrict__ primes,
+                                             const uint2* __restrict__ tw_full, const ExitConst* __restrict__ exits,
+                                             int entry) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  ColBuf* buf = reinterpret_cast<ColBuf*>(smraw);
+  const int tid = threadIdx.x, cq = tid & 7, tau = tid >> 3;
+  const int items = njobs * batch * kCTiles;
+  auto prefetch = [&](ColBuf& B, int it) {
+    int job, b, tile;
+    col_item(it, batch, job, b, tile);
+    const RowJob J = jobs[job];
+    const uint32_t* base = INV ? dst + b * dst_bs + (size_t)J.dst_off * kN : src + b * src_bs + (size_t)J.src_off * kN;
+    col_prefetch(B, base + tile * kCCols, tw_full + (size_t)J.prime * kN);
+  };
+  int it = blockIdx.x;
+  if (it < items) prefetch(buf[0], it);
+  cp_commit();
+  for (int k = 0; it < items; ++k, it += gridDim.x) {
+    ColBuf& B = buf[DB ? (k & 1) : 0];
+    const int nxt = it + gridDim.x;
+    if (DB) {
+      if (nxt < items) prefetch(buf[(k + 1) & 1], nxt);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    int job, b, tile;
+    col_item(it, batch, job, b, tile);
+    const RowJob J = jobs[job];
+    const PrimeDev P = primes[J.prime];
+    const uint32_t q = P.q, q2 = P.q2;
+    uint32_t* out = dst + b * dst_bs + (size_t)J.dst_off * kN + tile * kCCols + 4 * cq;
     uint4 v[16];
+    if (!INV) {
+      // ---- forward, stages 0..7 (r bits 7..0). phase A rows tau + 16 j.
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = ldg4(g + (tau + 16 * j) * kR);
-    // phase A: stages 0..3, rows tau + 16j; twiddle 2^s + blk (shared by all threads)
+      for (int j = 0; j < 16; ++j) v[j] = B.tile[(tau + 16 * j) * 8 + cq];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int d = 8 >> t;
+      for (int t = 0; t < 4; ++t) {
+        const int d = 8 >> t;
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int blk = p / d, j = blk * 2 * d + p % d;
-        const uint2 w = tw[(1 << t) + blk];
-        {
-          if (t == 0 && entry) {  // reference entry merge: x*R, y*psi^{N/2}*R (ntt.cpp:27-35)
-            uint4& x = v[j];
-            uint4& y = v[j + d];
-#define CK_E(c)                                               \
-  {                                                           \
-    const uint32_t xx = shoup_mul(x.c, P.r, P.r_sh, q);       \
-    const uint32_t tt = shoup_mul(y.c, P.w1r, P.w1r_sh, q);   \
-    x.c = xx + tt;                                            \
-    y.c = xx - tt + q2;                                       \
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          if (t == 0 && entry) {  // entry merge x*R, y*psi^{N/2}*R (ntt.cpp:27-35)
+#define CK_E(c)                                                    \
+  {                                                                \
+    const uint32_t xx = shoup_mul(v[j].c, P.r, P.r_sh, q);         \
+    const uint32_t tt = shoup_mul(v[j + d].c, P.w1r, P.w1r_sh, q); \
+    v[j].c = xx + tt;                                              \
+    v[j + d].c = xx - tt + q2;                                     \
   }
             CK_E(x) CK_E(y) CK_E(z) CK_E(w)
 #undef CK_E
           } else {
-            ct4(v[j], v[j + d], w, q, q2);
+            ct4(v[j], v[j + d], B.tw[(1 << t) + blk], q, q2);
           }
         }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) tile[(tau + 16 * j) * 16 + cq] = v[j];
-    __syncthreads();
+      for (int j = 0; j < 16; ++j) B.tile[(tau + 16 * j) * 8 + cq] = v[j];
+      __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = tile[(16 * tau + j) * 16 + cq];
-    // phase B: stages 4..7, rows 16 tau + j; twiddle 2^s + tau*2^(s-4) + blk
+      for (int j = 0; j < 16; ++j) v[j] = B.tile[(16 * tau + j) * 8 + cq];
+      uint2 twb[15];  // phase-B twiddles to registers so the buffer can be refilled
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int d = 8 >> t;
+      for (int t = 0; t < 4; ++t)
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int blk = p / d, j = blk * 2 * d + p % d;
-        ct4(v[j], v[j + d], tw[(16 << t) + (tau << t) + blk], q, q2);
+        for (int blk = 0; blk < (1 << t); ++blk) twb[(1 << t) - 1 + blk] = B.tw[(16 << t) + (tau << t) + blk];
+      if (!DB) {
+        __syncthreads();
+        if (nxt < items) prefetch(buf[0], nxt);
+        cp_commit();
       }
-    }
+      // phase B rows 16 tau + j: twiddle 2^s + tau 2^(s-4) + blk
 #pragma unroll
-    for (int j = 0; j < 16; ++j) stg4(o + (16 * tau + j) * kR, v[j]);
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------ inverse, pass B (columns) --
-__global__ void __launch_bounds__(256) k_inv_col(const RowJob* __restrict__ jobs, uint32_t* __restrict__ dst,
-                                                    uint64_t dst_bs, int batch, const PrimeDev* __restrict__ primes,
-                                                    const uint2* __restrict__ inv_tw,
-                                                    const ExitConst* __restrict__ exits) {
-  extern __shared__ uint4 smc[];
-  uint4* tile = smc;
-  uint2* tw = reinterpret_cast<uint2*>(smc + 256 * 16);
-  const RowJob job = jobs[blockIdx.y];
-  const PrimeDev P = primes[job.prime];
-  const ExitConst ex = exits[job.epi];
-  const uint32_t q = P.q, q2 = P.q2;
-  const int tid = threadIdx.x, cq = tid & 15, tau = tid >> 4;
-  tw[tid] = __ldg(&inv_tw[(size_t)job.prime * kN + tid]);
-  const int c0 = blockIdx.x * kColTileCols + 4 * cq;
-  __syncthreads();
-  for (int b = 0; b < batch; ++b) {
-    uint32_t* o = dst + b * dst_bs + (size_t)job.dst_off * kN + c0;
-    uint4 v[16];
+      for (int t = 0; t < 4; ++t) {
+        const int d = 8 >> t;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = ldg4(o + (16 * tau + j) * kR);
-    // phase A: r bits 0..3 (global v = 8..11): twiddle 2^(7-t) + tau*2^(3-t) + blk
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int d = 1 << t;
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int blk = p / d, j = blk * 2 * d + p % d;
-        gs4(v[j], v[j + d], tw[(128 >> t) + (tau << (3 - t)) + blk], q, q2);
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          ct4(v[j], v[j + d], twb[(1 << t) - 1 + blk], q, q2);
+        }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) tile[(16 * tau + j) * 16 + cq] = v[j];
-    __syncthreads();
+      for (int j = 0; j < 16; ++j) stg4(out + (16 * tau + j) * kR, v[j]);
+    } else {
+      const ExitConst ex = exits[J.epi];
+      // ---- inverse, stages 8..15 (r bits 0..7). phase A rows 16 tau + j.
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = tile[(tau + 16 * j) * 16 + cq];
-    // phase B: r bits 4..7 (global v = 12..14), then the exit stage (v = 15)
+      for (int j = 0; j < 16; ++j) v[j] = B.tile[(16 * tau + j) * 8 + cq];
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const int d = 1 << t;
+      for (int t = 0; t < 4; ++t) {
+        const int d = 1 << t;
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int blk = p / d, j = blk * 2 * d + p % d;
-        gs4(v[j], v[j + d], tw[(8 >> t) + blk], q, q2);
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          gs4(v[j], v[j + d], B.tw[(128 >> t) + (tau << (3 - t)) + blk], q, q2);
+        }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {  // exit merge (ntt.cpp:76-84): N^-1 R^-1 (x part1) constants
-#define CK_X(c)                                                    \
-  {                                                                \
+      for (int j = 0; j < 16; ++j) B.tile[(16 * tau + j) * 8 + cq] = v[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = B.tile[(tau + 16 * j) * 8 + cq];
+      uint2 twb[15];  // index (8>>t)-1+blk, t < 3
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int blk = 0; blk < (8 >> t); ++blk) twb[(8 >> t) - 1 + blk] = B.tw[(8 >> t) + blk];
+      if (!DB) {
+        __syncthreads();
+        if (nxt < items) prefetch(buf[0], nxt);
+        cp_commit();
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int d = 1 << t;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          gs4(v[j], v[j + d], twb[(8 >> t) - 1 + blk], q, q2);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // exit merge (ntt.cpp:76-84)
+#define CK_X(c)                                                            \
+  {                                                                        \
     const uint32_t u = v[j].c + v[j + 8].c, dd = v[j].c - v[j + 8].c + q2; \
-    v[j].c = sub_if(shoup_mul(u, ex.x, ex.y, q), q);               \
-    v[j + 8].c = sub_if(shoup_mul(dd, ex.z, ex.w, q), q);          \
+    v[j].c = sub_if(shoup_mul(u, ex.x, ex.y, q), q);                       \
+    v[j + 8].c = sub_if(shoup_mul(dd, ex.z, ex.w, q), q);                  \
   }
-      CK_X(x) CK_X(y) CK_X(z) CK_X(w)
+        CK_X(x) CK_X(y) CK_X(z) CK_X(w)
 #undef CK_X
-    }
+      }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) stg4(o + (tau + 16 * j) * kR, v[j]);
-    __syncthreads();
+      for (int j = 0; j < 16; ++j) stg4(out + (tau + 16 * j) * kR, v[j]);
+    }
+    if (DB) __syncthreads();  // buffer k&1 is refilled by the prefetch of iteration k+1
   }
+  cp_wait<0>();
 }
 
-// Row tile: 16 rows; the 16 threads of a row are one half-warp.
-// smem position of element c in a row: c + 4*(c>>4) (conflict-free for both
-// the stride-16 scalar and the contiguous uint4 access); row stride 336.
-constexpr int kRowStride = 336;
+// =============================================================== row pass ==
+// 8 rows per tile, 16 threads (half a warp) per row.  The tile's per-row
+// permuted twiddle tables (256 pairs per row) are staged in shared memory
+// once per (job, row tile) and reused for every batch item; data tiles are
+// double-buffered with cp.async.
+constexpr int kRT = 128;
+constexpr int kRRows = kRT / 16;
+constexpr int kRowStride = 336;  // element c at c + 4*(c>>4): conflict-free for both access shapes
 __device__ __forceinline__ int rpos(int c) { return c + 4 * (c >> 4); }
+constexpr int kRowBufWords = kRRows * kRowStride;
+constexpr int kRowSmem = 2 * kRowBufWords * 4 + kRRows * kR * 8;
 
-// ------------------------------------------------------- forward, pass 2 --
-__global__ void __launch_bounds__(256) k_fwd_row(const RowJob* __restrict__ jobs, uint32_t* __restrict__ dst,
-                                                 uint64_t dst_bs, int batch, const PrimeDev* __restrict__ primes,
-                                                 const uint2* __restrict__ tw2) {
-  __shared__ __align__(16) uint32_t sm[16 * kRowStride];
-  const RowJob job = jobs[blockIdx.y];
-  const PrimeDev P = primes[job.prime];
-  const uint32_t q = P.q, q2 = P.q2;
-  const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15;
-  const int r = blockIdx.x * 16 + rho;
-  // per-row permuted twiddles: [0,15) phase A (shared by the row), 16 + k*16 + tau phase B
-  const uint2* T = tw2 + ((size_t)job.prime * kR + r) * kR;
-  uint2 wa[15], wb[15];
+__device__ __forceinline__ void row_prefetch(uint32_t* buf, const uint32_t* g) {
+  // kRRows rows x 256 words contiguous, 16 B per cp.async
 #pragma unroll
-  for (int k = 0; k < 15; ++k) {
-    wa[k] = __ldg(&T[k]);
-    wb[k] = __ldg(&T[16 + k * 16 + tau]);
-  }
-  uint32_t* line = sm + rho * kRowStride;
-  for (int b = 0; b < batch; ++b) {
-    uint32_t* row = dst + b * dst_bs + (size_t)job.dst_off * kN + (size_t)r * kR;
-    uint32_t v[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = row[tau + 16 * j];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int d = 8 >> t;
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int blk = p / d, j = blk * 2 * d + p % d;
-        const uint2 w = wa[(1 << t) - 1 + blk];
-        ct(v[j], v[j + d], w.x, w.y, q, q2);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) line[rpos(tau + 16 * j)] = v[j];
-    __syncwarp();
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const uint4 x = *reinterpret_cast<const uint4*>(line + rpos(16 * tau) + 4 * m);
-      v[4 * m] = x.x;
-      v[4 * m + 1] = x.y;
-      v[4 * m + 2] = x.z;
-      v[4 * m + 3] = x.w;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int d = 8 >> t;
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int blk = p / d, j = blk * 2 * d + p % d;
-        const uint2 w = wb[(1 << t) - 1 + blk];
-        ct(v[j], v[j + d], w.x, w.y, q, q2);
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-      stg4(row + 16 * tau + 4 * m, make_uint4(canon4(v[4 * m], q, q2), canon4(v[4 * m + 1], q, q2),
-                                              canon4(v[4 * m + 2], q, q2), canon4(v[4 * m + 3], q, q2)));
+  for (int k = 0; k < kRRows * 64 / kRT; ++k) {
+    const int e = threadIdx.x + k * kRT;
+    const int r = e >> 6, c = (e & 63) * 4;
+    cp16(buf + r * kRowStride + rpos(c), g + r * kR + c);
   }
 }
 
-// ------------------------------------------------- inverse, pass A (rows) --
-__global__ void __launch_bounds__(256) k_inv_row(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
-                                                 uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs,
-                                                 int batch, const PrimeDev* __restrict__ primes,
-                                                 const uint2* __restrict__ tw2i) {
-  __shared__ __align__(16) uint32_t sm[16 * kRowStride];
-  const RowJob job = jobs[blockIdx.y];
-  const PrimeDev P = primes[job.prime];
-  const uint32_t q = P.q, q2 = P.q2;
+template <bool INV>
+__global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
+                                             uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
+                                             int njobs, const PrimeDev* __restrict__ primes,
+                                             const uint2* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
+  uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * kRowBufWords * 4);  // [kRRows][256]
   const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15;
-  const int r = blockIdx.x * 16 + rho;
-  // per-row permuted inverse twiddles: k*16 + tau (phase A, k < 15), 240 + k (phase B)
-  const uint2* T = tw2i + ((size_t)job.prime * kR + r) * kR;
-  uint2 wa[15], wb[15];
-#pragma unroll
-  for (int k = 0; k < 15; ++k) {
-    wa[k] = __ldg(&T[k * 16 + tau]);
-    wb[k] = __ldg(&T[240 + k]);
-  }
-  uint32_t* line = sm + rho * kRowStride;
-  for (int b = 0; b < batch; ++b) {
-    const uint32_t* in = src + b * src_bs + (size_t)job.src_off * kN + (size_t)r * kR;
-    uint32_t* out = dst + b * dst_bs + (size_t)job.dst_off * kN + (size_t)r * kR;
+  constexpr int kTiles = kR / kRRows;
+  // items: (job, row tile, b), b fastest; contiguous chunk per CTA
+  const int items = njobs * kTiles * batch;
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
+  auto in_ptr = [&](int it) {
+    const int b = it % batch, rest = it / batch, tile = rest % kTiles;
+    const RowJob J = jobs[rest / kTiles];
+    // forward pass 2 works in place on dst; inverse pass A reads src
+    return INV ? src + b * src_bs + (size_t)J.src_off * kN + tile * kRRows * kR
+               : dst + b * dst_bs + (size_t)J.dst_off * kN + tile * kRRows * kR;
+  };
+  if (i0 < i1) row_prefetch(sbuf, in_ptr(i0));
+  cp_commit();
+  int cur_key = -1;
+  for (int it = i0, k = 0; it < i1; ++it, ++k) {
+    uint32_t* line_buf = sbuf + (k & 1) * kRowBufWords;
+    const int b = it % batch, key = it / batch, tile = key % kTiles;
+    const RowJob J = jobs[key / kTiles];
+    if (key != cur_key) {  // stage this tile's twiddle tables (kRRows x 2 KB)
+      __syncthreads();
+      const uint2* T = tw2 + ((size_t)J.prime * kR + tile * kRRows) * kR;
+      for (int e = tid; e < kRRows * kR / 2; e += kRT) cp16(&tws[2 * e], &T[2 * e]);
+      cp_commit();
+      cur_key = key;
+    }
+    if (it + 1 < i1) row_prefetch(sbuf + ((k + 1) & 1) * kRowBufWords, in_ptr(it + 1));
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    const PrimeDev P = primes[J.prime];
+    const uint32_t q = P.q, q2 = P.q2;
+    const int r = tile * kRRows + rho;
+    const uint2* W = tws + rho * kR;
+    uint32_t* line = line_buf + rho * kRowStride;
+    uint32_t* orow = dst + b * dst_bs + (size_t)J.dst_off * kN + (size_t)r * kR;
     uint32_t v[16];
+    if (!INV) {
+      // phase A: c = tau + 16 j, stages 8..11 (row-shared twiddles W[0..14])
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const uint4 x = ldg4(in + 16 * tau + 4 * m);
-      v[4 * m] = x.x;
-      v[4 * m + 1] = x.y;
-      v[4 * m + 2] = x.z;
-      v[4 * m + 3] = x.w;
-    }
-    // phase A: c bits 0..3; block offsets 0, 8, 12, 14
+      for (int j = 0; j < 16; ++j) v[j] = line[rpos(tau + 16 * j)];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int d = 1 << t;
-      const int off = 16 - (16 >> t);
+      for (int t = 0; t < 4; ++t) {
+        const int d = 8 >> t;
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int blk = p / d, j = blk * 2 * d + p % d;
-        const uint2 w = wa[off + blk];
-        gs(v[j], v[j + d], w.x, w.y, q, q2);
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = W[(1 << t) - 1 + blk];
+          ct(v[j], v[j + d], w.x, w.y, q, q2);
+        }
       }
-    }
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
-      *reinterpret_cast<uint4*>(line + rpos(16 * tau) + 4 * m) =
-          make_uint4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
-    __syncwarp();
+      for (int j = 0; j < 16; ++j) line[rpos(tau + 16 * j)] = v[j];
+      __syncwarp();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = line[rpos(tau + 16 * j)];
-    __syncwarp();
-    // phase B: c bits 4..7
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int d = 1 << t;
-      const int off = 16 - (16 >> t);
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int blk = p / d, j = blk * 2 * d + p % d;
-        const uint2 w = wb[off + blk];
-        gs(v[j], v[j + d], w.x, w.y, q, q2);
+      for (int m = 0; m < 4; ++m) {
+        const uint4 x = *reinterpret_cast<const uint4*>(line + rpos(16 * tau) + 4 * m);
+        v[4 * m] = x.x;
+        v[4 * m + 1] = x.y;
+        v[4 * m + 2] = x.z;
+        v[4 * m + 3] = x.w;
       }
-    }
+      // phase B: c = 16 tau + j, stages 12..15 (W[16 + k*16 + tau])
 #pragma unroll
-    for (int j = 0; j < 16; ++j) out[tau + 16 * j] = v[j];
+      for (int t = 0; t < 4; ++t) {
+        const int d = 8 >> t;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = W[16 + ((1 << t) - 1 + blk) * 16 + tau];
+          ct(v[j], v[j + d], w.x, w.y, q, q2);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        stg4(orow + 16 * tau + 4 * m, make_uint4(canon4(v[4 * m], q, q2), canon4(v[4 * m + 1], q, q2),
+                                                 canon4(v[4 * m + 2], q, q2), canon4(v[4 * m + 3], q, q2)));
+    } else {
+      // phase A: c = 16 tau + j, inverse stages 0..3 (W[k*16 + tau])
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const uint4 x = *reinterpret_cast<const uint4*>(line + rpos(16 * tau) + 4 * m);
+        v[4 * m] = x.x;
+        v[4 * m + 1] = x.y;
+        v[4 * m + 2] = x.z;
+        v[4 * m + 3] = x.w;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int d = 1 << t;
+        const int off = 16 - (16 >> t);
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = W[(off + blk) * 16 + tau];
+          gs(v[j], v[j + d], w.x, w.y, q, q2);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        *reinterpret_cast<uint4*>(line + rpos(16 * tau) + 4 * m) =
+            make_uint4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = line[rpos(tau + 16 * j)];
+      // phase B: c = tau + 16 j, inverse stages 4..7 (row-shared W[240 + k])
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int d = 1 << t;
+        const int off = 16 - (16 >> t);
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = W[240 + off + blk];
+          gs(v[j], v[j + d], w.x, w.y, q, q2);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) orow[tau + 16 * j] = v[j];
+    }
+    __syncthreads();  // data buffer k&1 is refilled by the prefetch of iteration k+1
   }
+  cp_wait<0>();
+}
+
+int g_col_grid[2] = {0, 0}, g_row_grid = 0;
+bool g_col_db = false;
+
+void init_grids() {
+  if (g_row_grid) return;
+  const char* v = std::getenv("CK32_NTT_COL_DB");
+  g_col_db = v && v[0] == '1';
+  const int col_smem_db = 2 * (int)sizeof(ColBuf), col_smem_sb = (int)sizeof(ColBuf);
+  cudaFuncSetAttribute(k_col<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem_db);
+  cudaFuncSetAttribute(k_col<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem_db);
+  cudaFuncSetAttribute(k_col<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem_sb);
+  cudaFuncSetAttribute(k_col<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem_sb);
+  cudaFuncSetAttribute(k_row<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmem);
+  cudaFuncSetAttribute(k_row<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmem);
+  int dev = 0, sms = 148, c1 = 1, c2 = 1, r1 = 1, r2 = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g_col_db) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, true>, kCT, col_smem_db);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, true>, kCT, col_smem_db);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, false>, kCT, col_smem_sb);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, false>, kCT, col_smem_sb);
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, k_row<false>, kRT, kRowSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, k_row<true>, kRT, kRowSmem);
+  g_col_grid[0] = sms * max(1, c1);
+  g_col_grid[1] = sms * max(1, c2);
+  g_row_grid = sms * max(1, min(r1, r2));
+}
+
+template <bool INV>
+void launch_col(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaStream_t st) {
+  const int items = a.njobs * a.batch * kCTiles;
+  const int grid = min(g_col_grid[INV], items);
+  if (g_col_db)
+    k_col<INV, true><<<grid, kCT, 2 * sizeof(ColBuf), st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
+                                                            a.primes, a.tw, a.exits, a.entry);
+  else
+    k_col<INV, false><<<grid, kCT, sizeof(ColBuf), st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
+                                                         a.primes, a.tw, a.exits, a.entry);
 }
 
 }  // namespace
 
 bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_fwd_col, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmem);
-    cudaFuncSetAttribute(k_inv_col, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmem);
-    attr = true;
-  }
-  k_fwd_col<<<dim3(kR / kColTileCols, a.njobs), 256, kColSmem, st>>>(a.jobs, a.src, a.src_bs, a.dst, a.dst_bs,
-                                                                      a.batch, a.primes, a.tw, a.entry);
-  k_fwd_row<<<dim3(kR / 16, a.njobs), 256, 0, st>>>(a.jobs, a.dst, a.dst_bs, a.batch, a.primes, tw2);
+  init_grids();
+  const int row_items = a.njobs * (kR / kRRows) * a.batch;
+  launch_col<false>(a, a.src, a.src_bs, st);
+  k_row<false><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs, a.batch,
+                                                                  a.njobs, a.primes, tw2);
   return true;
 }
 
 bool ntt256_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_fwd_col, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmem);
-    cudaFuncSetAttribute(k_inv_col, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmem);
-    attr = true;
-  }
-  k_inv_row<<<dim3(kR / 16, a.njobs), 256, 0, st>>>(a.jobs, a.src, a.src_bs, a.dst, a.dst_bs, a.batch, a.primes,
-                                                     tw2i);
-  k_inv_col<<<dim3(kR / kColTileCols, a.njobs), 256, kColSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.batch, a.primes,
-                                                                      a.tw, a.exits);
+  init_grids();
+  const int row_items = a.njobs * (kR / kRRows) * a.batch;
+  k_row<true><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.src, a.src_bs, a.dst, a.dst_bs, a.batch,
+                                                                 a.njobs, a.primes, tw2i);
+  NttLaunch b = a;
+  b.entry = 0;
+  launch_col<true>(b, a.dst, a.dst_bs, st);
   return true;
 }
 
