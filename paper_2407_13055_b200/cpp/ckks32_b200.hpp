@@ -1,0 +1,207 @@
+// ckks32_b200.hpp — header-only C++ mirror of the reference evaluator API
+// (/root/reference/proj/include/ckks32/ckks.hpp:102-219) over the C ABI of
+// include/ck32_b200.h.
+//
+// Same names, argument meaning, level/scale ledger and exception types as
+// the reference (std::invalid_argument / std::runtime_error); residues live in
+// device memory as canonical uint32 (the reference's correct_lazy() view).
+// The scale ledger is an exact rational over 64-bit limbs products; the
+// reference uses Boost cpp_rational (ckks.hpp:30) — here the numerator and
+// denominator are kept as explicit prime-product lists, so equality and
+// division by q_{l-2} q_{l-1} are exact without a big-integer library.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/ck32_b200.h"
+
+namespace ckks32::b200 {
+
+inline void check(ck_status s) {
+  if (s == CK_OK) return;
+  const std::string msg = ck_last_error();
+  if (s == CK_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+// Exact scale ledger: value = 2^pow2 * prod(num) / prod(den) (all factors are
+// basis primes or powers of two, which is all the hot path produces).
+struct Scale {
+  int pow2 = 0;
+  std::vector<uint32_t> num, den;
+  static Scale two_pow(int b) { return Scale{b, {}, {}}; }
+  Scale operator*(const Scale& o) const {
+    Scale r{pow2 + o.pow2, num, den};
+    r.num.insert(r.num.end(), o.num.begin(), o.num.end());
+    r.den.insert(r.den.end(), o.den.begin(), o.den.end());
+    r.normalize();
+    return r;
+  }
+  Scale divided_by(uint32_t a, uint32_t b) const {
+    Scale r = *this;
+    r.den.push_back(a);
+    r.den.push_back(b);
+    r.normalize();
+    return r;
+  }
+  void normalize() {
+    std::sort(num.begin(), num.end());
+    std::sort(den.begin(), den.end());
+    std::vector<uint32_t> n2, d2;
+    std::set_difference(num.begin(), num.end(), den.begin(), den.end(), std::back_inserter(n2));
+    std::set_difference(den.begin(), den.end(), num.begin(), num.end(), std::back_inserter(d2));
+    num = std::move(n2);
+    den = std::move(d2);
+  }
+  bool operator==(const Scale& o) const { return pow2 == o.pow2 && num == o.num && den == o.den; }
+};
+
+struct CkksParams {  // ckks.hpp:46-54
+  uint32_t n = 1u << 16, l = 54, alpha = 14, delta_bits = 48;
+  bool lazy_rescale = false;
+};
+
+// Owning device buffer of uint32 residues.
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  DeviceBuffer(ck_context* ctx, size_t words) : ctx_(ctx), words_(words) {
+    void* p = nullptr;
+    check(ck_malloc(ctx, words * 4, &p));
+    ptr_ = static_cast<uint32_t*>(p);
+  }
+  DeviceBuffer(DeviceBuffer&& o) noexcept { *this = std::move(o); }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    std::swap(ctx_, o.ctx_);
+    std::swap(ptr_, o.ptr_);
+    std::swap(words_, o.words_);
+    return *this;
+  }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  ~DeviceBuffer() {
+    if (ptr_) ck_free(ctx_, ptr_);
+  }
+  uint32_t* data() const { return ptr_; }
+  size_t words() const { return words_; }
+  void upload(const uint32_t* host, size_t words) {
+    check(ck_memcpy_h2d(ctx_, ptr_, host, words * 4, nullptr));
+    check(ck_stream_sync(ctx_, nullptr));
+  }
+  std::vector<uint32_t> download() const {
+    std::vector<uint32_t> h(words_);
+    check(ck_memcpy_d2h(ctx_, h.data(), ptr_, words_ * 4, nullptr));
+    check(ck_stream_sync(ctx_, nullptr));
+    return h;
+  }
+
+ private:
+  ck_context* ctx_ = nullptr;
+  uint32_t* ptr_ = nullptr;
+  size_t words_ = 0;
+};
+
+class CkksContext {  // ckks.cpp:160-176
+ public:
+  explicit CkksContext(CkksParams p, int device = 0, const std::vector<uint32_t>* primes = nullptr) : p_(p) {
+    ck_params cp{p.n, p.l, p.alpha, p.delta_bits, p.lazy_rescale ? 1 : 0};
+    ck_context* c = nullptr;
+    check(ck_context_create(&cp, primes ? primes->data() : nullptr, device, &c));
+    ctx_.reset(c);
+    primes_.resize(p.l + p.alpha);
+    check(ck_context_primes(c, primes_.data()));
+  }
+  const CkksParams& params() const { return p_; }
+  ck_context* raw() const { return ctx_.get(); }
+  const std::vector<uint32_t>& primes() const { return primes_; }
+  uint32_t num_digits(uint32_t level) const { return (level + p_.alpha - 1) / p_.alpha; }
+  Scale default_scale() const { return Scale::two_pow((int)p_.delta_bits); }
+  std::vector<uint64_t> counters() const {
+    std::vector<uint64_t> c(7);
+    check(ck_context_counters(ctx_.get(), c.data()));
+    return c;
+  }
+
+ private:
+  struct Del {
+    void operator()(ck_context* c) const { ck_context_destroy(c); }
+  };
+  CkksParams p_;
+  std::unique_ptr<ck_context, Del> ctx_;
+  std::vector<uint32_t> primes_;
+};
+
+struct Ciphertext {  // ckks.hpp:61-66; data = [2][level][n]
+  DeviceBuffer data;
+  Scale scale;
+  uint32_t level = 0;
+  bool pending_rescale = false;
+};
+
+enum class KeyKind : uint8_t { Relin = 0, Rotation = 1 };
+struct EvaluationKey {  // ckks.hpp:79-84; data = [D][2][L+alpha][n]
+  DeviceBuffer data;
+  KeyKind kind = KeyKind::Relin;
+  int64_t rotation = 0;
+};
+
+inline Ciphertext make_ciphertext(CkksContext& ctx, uint32_t level, Scale s) {
+  return Ciphertext{DeviceBuffer(ctx.raw(), 2ull * level * ctx.params().n), std::move(s), level, false};
+}
+
+inline Ciphertext rescale(CkksContext& ctx, const Ciphertext& ct) {  // ckks.cpp:789-802
+  if (ct.level < 4) throw std::invalid_argument("level exhausted");
+  Ciphertext out = make_ciphertext(ctx, ct.level - 2,
+                                   ct.scale.divided_by(ctx.primes()[ct.level - 2], ctx.primes()[ct.level - 1]));
+  check(ck_rescale(ctx.raw(), ct.level, 1, ct.data.data(), out.data.data(), nullptr));
+  return out;
+}
+
+inline Ciphertext hmult(CkksContext& ctx, const Ciphertext& x_in, const Ciphertext& y_in,
+                        const EvaluationKey& relin) {  // ckks.cpp:804-865
+  if (relin.kind != KeyKind::Relin) throw std::invalid_argument("hmult needs a relinearization key");
+  Ciphertext fx, fy;
+  const Ciphertext* x = &x_in;
+  const Ciphertext* y = &y_in;
+  if (x_in.pending_rescale) fx = rescale(ctx, x_in), x = &fx;  // Flushed (ckks.cpp:664-676)
+  if (y_in.pending_rescale) fy = rescale(ctx, y_in), y = &fy;
+  if (x->level != y->level) throw std::invalid_argument("level mismatch");
+  const uint32_t l = x->level;
+  if (l < 4) throw std::invalid_argument("level exhausted");
+  const bool lazy = ctx.params().lazy_rescale;
+  Scale s = x->scale * y->scale;
+  if (!lazy) s = s.divided_by(ctx.primes()[l - 2], ctx.primes()[l - 1]);
+  Ciphertext out = make_ciphertext(ctx, lazy ? l : l - 2, s);
+  out.pending_rescale = lazy;
+  check(ck_hmult(ctx.raw(), l, 1, x->data.data(), y->data.data(), relin.data.data(), out.data.data(), nullptr));
+  return out;
+}
+
+inline Ciphertext hrot(CkksContext& ctx, const Ciphertext& ct_in, int64_t r,
+                       const EvaluationKey& evk) {  // ckks.cpp:890-897
+  Ciphertext f;
+  const Ciphertext* ct = &ct_in;
+  if (ct_in.pending_rescale) f = rescale(ctx, ct_in), ct = &f;
+  if (evk.kind != KeyKind::Rotation || evk.rotation != r) throw std::invalid_argument("rotation key mismatch");
+  Ciphertext out = make_ciphertext(ctx, ct->level, ct->scale);
+  check(ck_hrot(ctx.raw(), ct->level, 1, ct->data.data(), r, evk.data.data(), out.data.data(), nullptr));
+  return out;
+}
+
+inline Ciphertext hadd(CkksContext& ctx, const Ciphertext& x, const Ciphertext& y) {  // ckks.cpp:557-571
+  if (x.level != y.level) throw std::invalid_argument("level mismatch");
+  if (x.pending_rescale != y.pending_rescale) throw std::invalid_argument("pending-rescale state mismatch");
+  if (!(x.scale == y.scale)) throw std::invalid_argument("scale mismatch beyond tolerance");
+  Ciphertext out = make_ciphertext(ctx, x.level, x.scale);
+  out.pending_rescale = x.pending_rescale;
+  check(ck_hadd(ctx.raw(), x.level, 1, x.data.data(), y.data.data(), out.data.data(), nullptr));
+  return out;
+}
+
+}  // namespace ckks32::b200

@@ -24,13 +24,22 @@ __device__ __forceinline__ uint32_t getc(const uint4& v, int k) {
 }
 
 // ------------------------------------------------------------------ bconv --
+// One thread = 4 adjacent coefficients x all destination rows of the group.
+// Per-destination constants (matrix row, q, -q^-1, output row offset) are
+// staged in shared memory so the MAC loop never waits on a global load; the
+// destination loop is unrolled by two for independent accumulator chains.
 template <int SC>
 __global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
   __shared__ uint32_t cm[kMaxRows * SC];
+  __shared__ uint4 rc[kMaxRows];  // {q, qinv_neg, dst row, 0}
   const BconvGroup G = a.groups[blockIdx.y];
   for (int e = threadIdx.x; e < G.dc * SC; e += kT) {
     const int i = e / SC, j = e % SC;
     cm[e] = j < (int)G.sc ? a.cmat[G.cmat_off + i * G.sc + j] : 0u;
+  }
+  for (int i = threadIdx.x; i < (int)G.dc; i += kT) {
+    const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
+    rc[i] = make_uint4(P.q, P.qinv_neg, a.dst_row[G.map_off + i], 0);
   }
   __syncthreads();
   const int x = (blockIdx.x * kT + threadIdx.x) * 4;
@@ -40,7 +49,7 @@ __global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
 #pragma unroll
   for (int j = 0; j < SC; ++j) s[j] = j < (int)G.sc ? ld4(src + (size_t)j * n) : make_uint4(0, 0, 0, 0);
   uint32_t* dst = a.dst + blockIdx.z * a.dst_bs + x;
-  for (int i = 0; i < (int)G.dc; ++i) {
+  auto one = [&](int i) {
     uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
 #pragma unroll
     for (int j = 0; j < SC; ++j) {
@@ -50,14 +59,20 @@ __global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
       acc2 += (uint64_t)s[j].z * c;
       acc3 += (uint64_t)s[j].w * c;
     }
-    const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
+    const uint4 R = rc[i];
     uint4 r;
-    r.x = sub_if(mont_reduce64(acc0, P.q, P.qinv_neg), P.q);
-    r.y = sub_if(mont_reduce64(acc1, P.q, P.qinv_neg), P.q);
-    r.z = sub_if(mont_reduce64(acc2, P.q, P.qinv_neg), P.q);
-    r.w = sub_if(mont_reduce64(acc3, P.q, P.qinv_neg), P.q);
-    st4(dst + (size_t)a.dst_row[G.map_off + i] * n, r);
+    r.x = sub_if(mont_reduce64(acc0, R.x, R.y), R.x);
+    r.y = sub_if(mont_reduce64(acc1, R.x, R.y), R.x);
+    r.z = sub_if(mont_reduce64(acc2, R.x, R.y), R.x);
+    r.w = sub_if(mont_reduce64(acc3, R.x, R.y), R.x);
+    st4(dst + (size_t)R.z * n, r);
+  };
+  int i = 0;
+  for (; i + 1 < (int)G.dc; i += 2) {
+    one(i);
+    one(i + 1);
   }
+  if (i < (int)G.dc) one(i);
 }
 
 // ----------------------------------------------------------------- tensor --

@@ -1,0 +1,81 @@
+// C++ drop-in check: drives the header-only mirror (paper_2407_13055_b200/cpp/
+// ckks32_b200.hpp) the way the reference's own tests drive ckks.hpp
+// (test_ckks.cpp:293-380): hmult + hrot on ciphertexts read from raw files,
+// results written back for the Python side to compare with the oracle, plus
+// the exception contract (std::invalid_argument on level / key misuse).
+//
+//   test_cpp_api <dir> <n> <l> <alpha> <level>
+// <dir>/x.bin, y.bin: [2][level][n] u32; evk.bin: [D][2][L+alpha][n] u32
+// writes <dir>/out_hmult.bin, out_hrot.bin
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <stdexcept>
+#include <vector>
+
+#include "../../paper_2407_13055_b200/cpp/ckks32_b200.hpp"
+
+using namespace ckks32::b200;
+
+static std::vector<uint32_t> read_file(const std::string& p, size_t words) {
+  std::vector<uint32_t> v(words);
+  std::ifstream f(p, std::ios::binary);
+  if (!f.read(reinterpret_cast<char*>(v.data()), words * 4)) throw std::runtime_error("short read " + p);
+  return v;
+}
+static void write_file(const std::string& p, const std::vector<uint32_t>& v) {
+  std::ofstream f(p, std::ios::binary);
+  f.write(reinterpret_cast<const char*>(v.data()), v.size() * 4);
+}
+
+int main(int argc, char** argv) {
+  if (argc < 6) {
+    std::fprintf(stderr, "usage: %s dir n l alpha level\n", argv[0]);
+    return 2;
+  }
+  const std::string dir = argv[1];
+  CkksParams p;
+  p.n = std::atoi(argv[2]);
+  p.l = std::atoi(argv[3]);
+  p.alpha = std::atoi(argv[4]);
+  p.delta_bits = 55;
+  const uint32_t level = std::atoi(argv[5]);
+  CkksContext ctx(p);
+  const size_t ctw = 2ull * level * p.n;
+  const size_t evw = (size_t)ctx.num_digits(p.l) * 2 * (p.l + p.alpha) * p.n;
+
+  Ciphertext x = make_ciphertext(ctx, level, ctx.default_scale());
+  Ciphertext y = make_ciphertext(ctx, level, ctx.default_scale());
+  x.data.upload(read_file(dir + "/x.bin", ctw).data(), ctw);
+  y.data.upload(read_file(dir + "/y.bin", ctw).data(), ctw);
+  EvaluationKey relin{DeviceBuffer(ctx.raw(), evw), KeyKind::Relin, 0};
+  relin.data.upload(read_file(dir + "/evk.bin", evw).data(), evw);
+  EvaluationKey rot{DeviceBuffer(ctx.raw(), evw), KeyKind::Rotation, 1};
+  rot.data.upload(read_file(dir + "/evk.bin", evw).data(), evw);
+
+  Ciphertext m = hmult(ctx, x, y, relin);
+  if (m.level != level - 2) throw std::runtime_error("hmult level ledger");
+  Ciphertext expect_scale = make_ciphertext(ctx, 2, ctx.default_scale() * ctx.default_scale());
+  if (!(m.scale == expect_scale.scale.divided_by(ctx.primes()[level - 2], ctx.primes()[level - 1])))
+    throw std::runtime_error("hmult scale ledger");
+  write_file(dir + "/out_hmult.bin", m.data.download());
+  Ciphertext r = hrot(ctx, x, 1, rot);
+  write_file(dir + "/out_hrot.bin", r.data.download());
+
+  int errors = 0;
+  try {  // rotation key passed to hmult (ckks.cpp:806-807)
+    hmult(ctx, x, y, rot);
+    ++errors;
+  } catch (const std::invalid_argument&) {
+  }
+  try {  // wrong rotation amount (ckks.cpp:872-873)
+    hrot(ctx, x, 2, rot);
+    ++errors;
+  } catch (const std::invalid_argument&) {
+  }
+  const uint64_t n_launch = ck_launch_count(ctx.raw());
+  std::printf("cpp api ok: hmult level %u -> %u, hrot level %u, %llu kernel launches, %d contract errors\n", level,
+              m.level, r.level, (unsigned long long)n_launch, errors);
+  return errors ? 1 : 0;
+}

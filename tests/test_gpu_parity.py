@@ -308,3 +308,30 @@ def test_lazy_then_rescale_equals_merged_ledger():
     assert pl.pending_rescale and pl.level == 8
     pr = ckks.rescale(Cl, pl)
     assert (pm.level, pm.scale) == (pr.level, pr.scale)
+
+
+def test_cpp_mirror_drop_in(tmp_path):
+    """The header-only C++ mirror (ckks32_b200.hpp) over the C ABI, driven by a
+    C++ program the way the reference's tests drive ckks.hpp."""
+    import subprocess
+    from pathlib import Path
+
+    exe = Path(__file__).resolve().parent.parent / "paper_2407_13055_b200" / "_lib" / "test_cpp_api"
+    if not exe.exists():
+        subprocess.run(["make", "-C", str(exe.parent.parent), "cpp_test"], check=True, capture_output=True)
+    n, l, a, db, level = 4096, 12, 4, 55, 10
+    O = _oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(level, 77)
+    np.stack([xb, xa]).astype("<u4").tofile(tmp_path / "x.bin")
+    np.stack([yb, ya]).astype("<u4").tofile(tmp_path / "y.bin")
+    evk.astype("<u4").tofile(tmp_path / "evk.bin")
+    r = subprocess.run([str(exe), str(tmp_path), str(n), str(l), str(a), str(level)], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "cpp api ok" in r.stdout
+    ob, oa = O.hmult(level, xb, xa, yb, ya, evk)
+    got = np.fromfile(tmp_path / "out_hmult.bin", dtype="<u4").reshape(2, level - 2, n)
+    np.testing.assert_array_equal(got, np.stack([canon(O, ob, level - 2), canon(O, oa, level - 2)]))
+    rb, ra = O.hrot(level, xb, xa, 1, evk)
+    got = np.fromfile(tmp_path / "out_hrot.bin", dtype="<u4").reshape(2, level, n)
+    np.testing.assert_array_equal(got, np.stack([canon(O, rb, level), canon(O, ra, level)]))
