@@ -212,10 +212,17 @@ struct BconvPlan {
   uint64_t src_rows = 0, dst_rows = 0;  // algorithmic rows read / written per batch item
 };
 // ModUp at one level: INTT(+part1) of the level rows, per-digit BConv, NTT.
+// Tables of the fused INTT-B -> BConv -> NTT-1 kernel (ntt256.cu k_conv_mid).
+struct ConvMidPlan {
+  Blob blob;
+  size_t groups_off = 0, cmat_off = 0, row_off = 0, prime_off = 0, sprime_off = 0, sexit_off = 0;
+  int ngroups = 0, max_sc = 1;
+};
 struct ModUpPlan {
   uint32_t level = 0, D = 0;
   NttPlan intt, ntt;
   BconvPlan bc;
+  ConvMidPlan cm;
   uint64_t ntt_rows = 0;
 };
 // drop_and_divide for npoly polynomials of (out_q + sc) rows each.
@@ -223,6 +230,7 @@ struct SwitchPlan {
   uint32_t out_q = 0, sc = 0, npoly = 0;
   NttPlan intt, ntt;
   BconvPlan bc;
+  ConvMidPlan cm;
   Blob consts;  // div_inv_mont [out_q]
 };
 
@@ -243,6 +251,8 @@ struct Context {
   uint2* d_tw2f = nullptr;      // N = 2^16 row-pass tables (ntt256.cu), per-row permuted
   uint2* d_tw2i = nullptr;
   bool use_ntt256 = true;
+  bool use_cluster = false;  // CK32_NTT_CLUSTER=1: single-pass 8-CTA cluster/DSMEM NTT (slower today)
+  bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
   int ntt_chunk_limbs = 1 << 30;  // limbs per pass-1/pass-2 launch pair (CK32_NTT_CHUNK; measured: no gain)
   std::map<uint32_t, std::unique_ptr<ModUpPlan>> modup;
   std::map<std::tuple<int, uint32_t, uint32_t>, std::unique_ptr<SwitchPlan>> switches;
@@ -364,6 +374,51 @@ struct Context {
     }
   }
 
+  // One k_conv_mid group: sources (global prime sg[j], rows src_off + j with
+  // part-1 exits), destinations (global prime dg[i], row drow[i]).
+  void add_conv_group(std::vector<ConvMidGroup>& groups, std::vector<uint32_t>& cmat, std::vector<uint32_t>& drow_all,
+                      std::vector<uint16_t>& dprime, std::vector<uint16_t>& sprime, std::vector<ExitConst>& sexit,
+                      uint32_t src_off, const std::vector<uint32_t>& sg, const std::vector<uint32_t>& dg,
+                      const std::vector<uint32_t>& drow) const {
+    std::vector<uint32_t> cm, part1;
+    bconv_consts(sg, dg, cm, part1);
+    ConvMidGroup G;
+    G.src_off = src_off;
+    G.sc = (uint32_t)sg.size();
+    G.dc = (uint32_t)dg.size();
+    G.cmat_off = (uint32_t)cmat.size();
+    G.map_off = (uint32_t)drow_all.size();
+    G.src_map_off = (uint32_t)sprime.size();
+    for (size_t i = 0; i < dg.size(); ++i)
+      for (size_t j = 0; j < sg.size(); ++j) {  // x R folded in: the NTT skips the entry merge
+        const uint32_t qi = q(dg[i]);
+        cmat.push_back(mulm(cm[i * sg.size() + j], r_mod(qi), qi));
+      }
+    for (size_t i = 0; i < dg.size(); ++i) {
+      drow_all.push_back(drow[i]);
+      dprime.push_back((uint16_t)dg[i]);
+    }
+    for (size_t j = 0; j < sg.size(); ++j) {
+      sprime.push_back((uint16_t)sg[j]);
+      sexit.push_back(exit_const(sg[j], part1[j]));
+    }
+    groups.push_back(G);
+  }
+  static void upload_conv(ConvMidPlan& cm, const std::vector<ConvMidGroup>& groups, const std::vector<uint32_t>& cmat,
+                          const std::vector<uint32_t>& drow, const std::vector<uint16_t>& dprime,
+                          const std::vector<uint16_t>& sprime, const std::vector<ExitConst>& sexit) {
+    cm.groups_off = cm.blob.add(groups);
+    cm.cmat_off = cm.blob.add(cmat);
+    cm.row_off = cm.blob.add(drow);
+    cm.prime_off = cm.blob.add(dprime);
+    cm.sprime_off = cm.blob.add(sprime);
+    cm.sexit_off = cm.blob.add(sexit);
+    cm.ngroups = (int)groups.size();
+    cm.max_sc = 1;
+    for (const auto& g : groups) cm.max_sc = std::max<int>(cm.max_sc, (int)g.sc);
+    cm.blob.upload();
+  }
+
   void check_bconv_width(const std::vector<uint32_t>& sg) const {
     // unsigned int64 accumulation is exact while sc * max(p) < 2^32 (the
     // reference's cap makes (alpha+2) * p < 2^32, rns.cpp:69-72)
@@ -386,6 +441,10 @@ struct Context {
     std::vector<uint32_t> cmat, drow;
     std::vector<uint16_t> dprime;
     int max_sc = 1;
+    std::vector<ConvMidGroup> cgroups;
+    std::vector<uint32_t> ccmat, cdrow;
+    std::vector<uint16_t> cdprime, csprime;
+    std::vector<ExitConst> csexit;
     for (uint32_t k = 0; k < pl->D; ++k) {  // modup_table (ckks.cpp:188-202)
       const uint32_t b = k * alpha, e = std::min((k + 1) * alpha, level);
       std::vector<uint32_t> sg, dg;
@@ -413,7 +472,12 @@ struct Context {
         ijobs.push_back({b + j, b + j, (uint16_t)(b + j), (uint16_t)exits.size()});
         exits.push_back(exit_const(b + j, part1[j]));
       }
+      std::vector<uint32_t> dr;
+      for (uint32_t i = 0; i < rows; ++i)
+        if (i < b || i >= e) dr.push_back(k * rows + i);
+      add_conv_group(cgroups, ccmat, cdrow, cdprime, csprime, csexit, b, sg, dg, dr);
     }
+    upload_conv(pl->cm, cgroups, ccmat, cdrow, cdprime, csprime, csexit);
     pl->intt.jobs_off = pl->intt.blob.add(ijobs);
     pl->intt.exits_off = pl->intt.blob.add(exits);
     pl->intt.njobs = (int)ijobs.size();
@@ -510,6 +574,18 @@ struct Context {
     }
     pl->consts.add(dinv);
     pl->consts.upload();
+    {
+      std::vector<ConvMidGroup> cgroups;
+      std::vector<uint32_t> ccmat, cdrow;
+      std::vector<uint16_t> cdprime, csprime;
+      std::vector<ExitConst> csexit;
+      for (uint32_t p = 0; p < npoly; ++p) {
+        std::vector<uint32_t> dr(out_q);
+        for (uint32_t i = 0; i < out_q; ++i) dr[i] = p * out_q + i;
+        add_conv_group(cgroups, ccmat, cdrow, cdprime, csprime, csexit, p * sc, sg, dg, dr);
+      }
+      upload_conv(pl->cm, cgroups, ccmat, cdrow, cdprime, csprime, csexit);
+    }
     auto& ref = *pl;
     switches[key] = std::move(pl);
     return ref;
@@ -554,7 +630,13 @@ struct Context {
     a.exits = inverse ? pl.blob.at<ExitConst>(pl.exits_off) : nullptr;
     a.entry = entry;
     ProfScope ps(this, inverse ? 1 : 0, 8.0 * n * pl.njobs * batch, 2, st);
-    if (logn == 16 && d_tw2f && use_ntt256) {
+    if (logn == 16 && d_tw2f && use_ntt256 && use_cluster && ntt_cluster_available()) {
+      if (inverse)
+        ntt_cluster_inverse(a, d_tw2i, st);
+      else
+        ntt_cluster_forward(a, d_tw2f, st);
+      launches += 1;
+    } else if (logn == 16 && d_tw2f && use_ntt256) {
       // L2-resident chunks: pass 2 of a chunk reads pass 1's output while it
       // is still in the 126 MB L2, so each limb crosses HBM once each way.
       const int chunk = ntt_chunk_limbs;
@@ -604,6 +686,58 @@ struct Context {
     ++launches;
   }
 
+  bool fused() const { return logn == 16 && d_tw2f && use_ntt256 && use_fused; }
+  NttLaunch ntt_args(const NttPlan& pl, bool inverse, int batch, const uint32_t* src, uint64_t src_bs, uint32_t* dst,
+                     uint64_t dst_bs) const {
+    NttLaunch a;
+    a.jobs = pl.blob.at<RowJob>(pl.jobs_off);
+    a.njobs = pl.njobs;
+    a.batch = batch;
+    a.src = src;
+    a.src_bs = src_bs;
+    a.dst = dst;
+    a.dst_bs = dst_bs;
+    a.primes = d_primes;
+    a.tw = inverse ? d_inv : d_fwd;
+    a.exits = inverse ? pl.blob.at<ExitConst>(pl.exits_off) : nullptr;
+    return a;
+  }
+  // fused path: INTT pass A -> [INTT pass B + BConv + NTT pass 1] -> NTT pass 2
+  void run_convert(const NttPlan& ipl, const ConvMidPlan& cm, const NttPlan& npl, int B, const uint32_t* src,
+                   uint64_t src_bs, uint32_t* mid, uint64_t mid_bs, uint32_t* dst, uint64_t dst_bs, double bytes_in,
+                   double bytes_out, cudaStream_t st) {
+    {
+      ProfScope ps(this, 1, 8.0 * n * ipl.njobs * B, 1, st);
+      ntt256_pass(2, ntt_args(ipl, true, B, src, src_bs, mid, mid_bs), d_tw2i, st);
+    }
+    {
+      ProfScope ps(this, 7, bytes_in + bytes_out, 1, st);
+      ConvMidLaunch a;
+      a.groups = cm.blob.at<ConvMidGroup>(cm.groups_off);
+      a.ngroups = cm.ngroups;
+      a.batch = B;
+      a.max_sc = cm.max_sc;
+      a.src = mid;
+      a.src_bs = mid_bs;
+      a.dst = dst;
+      a.dst_bs = dst_bs;
+      a.cmat = cm.blob.at<uint32_t>(cm.cmat_off);
+      a.dst_row = cm.blob.at<uint32_t>(cm.row_off);
+      a.dst_prime = cm.blob.at<uint16_t>(cm.prime_off);
+      a.src_prime = cm.blob.at<uint16_t>(cm.sprime_off);
+      a.src_exit = cm.blob.at<ExitConst>(cm.sexit_off);
+      a.primes = d_primes;
+      a.fwd_tw = d_fwd;
+      a.inv_tw = d_inv;
+      conv_mid(a, st);
+    }
+    {
+      ProfScope ps(this, 0, 8.0 * n * npl.njobs * B, 1, st);
+      ntt256_pass(1, ntt_args(npl, false, B, dst, dst_bs, dst, dst_bs), d_tw2f, st);
+    }
+    launches += 3;
+  }
+
   // ModUp (ckks.cpp:680-731) of B polynomials d (level rows, batch stride d_bs)
   // into ext [B][D][level+alpha]; uses `is` [B][level] as INTT scratch.
   // The digit rows of ext are NOT written: key_mult reads them from d.
@@ -611,10 +745,15 @@ struct Context {
               cudaStream_t st) {
     const ModUpPlan& pl = modup_plan(level);
     const uint64_t N = n;
-    run_ntt(pl.intt, true, B, d, d_bs, is, level * N, 0, st);
-    run_bconv(pl.bc, B, is, level * N, ext, (uint64_t)pl.D * (level + alpha) * N, st);
-    run_ntt(pl.ntt, false, B, ext, (uint64_t)pl.D * (level + alpha) * N, ext,
-            (uint64_t)pl.D * (level + alpha) * N, 1, st);
+    const uint64_t ext_bs = (uint64_t)pl.D * (level + alpha) * N;
+    if (fused()) {
+      run_convert(pl.intt, pl.cm, pl.ntt, B, d, d_bs, is, level * N, ext, ext_bs, 4.0 * N * level * B,
+                  4.0 * N * pl.ntt_rows * B, st);
+    } else {
+      run_ntt(pl.intt, true, B, d, d_bs, is, level * N, 0, st);
+      run_bconv(pl.bc, B, is, level * N, ext, ext_bs, st);
+      run_ntt(pl.ntt, false, B, ext, ext_bs, ext, ext_bs, 1, st);
+    }
     counters[0] += B;
     counters[3] += (uint64_t)B * level;
     counters[5] += (uint64_t)B * pl.D;
@@ -656,9 +795,15 @@ struct Context {
                    bool combine_now, cudaStream_t st) {
     const uint64_t N = n;
     const uint64_t prow = pl.out_q + pl.sc;
-    run_ntt(pl.intt, true, B, v, v_bs, ts, (uint64_t)pl.npoly * pl.sc * N, 0, st);
-    run_bconv(pl.bc, B, ts, (uint64_t)pl.npoly * pl.sc * N, o, (uint64_t)pl.npoly * pl.out_q * N, st);
-    run_ntt(pl.ntt, false, B, o, (uint64_t)pl.npoly * pl.out_q * N, o, (uint64_t)pl.npoly * pl.out_q * N, 1, st);
+    const uint64_t ts_bs = (uint64_t)pl.npoly * pl.sc * N, o_bs = (uint64_t)pl.npoly * pl.out_q * N;
+    if (fused()) {
+      run_convert(pl.intt, pl.cm, pl.ntt, B, v, v_bs, ts, ts_bs, o, o_bs, 4.0 * N * pl.npoly * pl.sc * B,
+                  4.0 * N * pl.npoly * pl.out_q * B, st);
+    } else {
+      run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
+      run_bconv(pl.bc, B, ts, ts_bs, o, o_bs, st);
+      run_ntt(pl.ntt, false, B, o, o_bs, o, o_bs, 1, st);
+    }
     if (combine_now) {
       ProfScope ps(this, 5, 12.0 * n * pl.out_q * pl.npoly * B, 1, st);
       combine((int)n, (int)pl.out_q, (int)pl.npoly, B, v, prow * N, v_bs, o, pl.out_q * N,
@@ -790,6 +935,8 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     CK_CUDA(cudaMemcpy(c->d_inv, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     c->use_ntt256 = std::getenv("CK32_GENERIC_NTT") == nullptr;  // A/B switch for parity tests
     if (const char* ch = std::getenv("CK32_NTT_CHUNK")) c->ntt_chunk_limbs = std::max(1, std::atoi(ch));
+    c->use_fused = std::getenv("CK32_FUSED") != nullptr;
+    c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;
     if (n == 65536) {
       // Row-pass twiddles of ntt256.cu, permuted per row in thread-consumption
       // order (same values as the reference tables, ntt.cpp:124-128).
@@ -886,8 +1033,9 @@ ck_status ck_profile(ck_context* ctx, int enable) {
 ck_status ck_profile_read(ck_context* ctx, ck_prof_stat* out, uint32_t max_classes, uint32_t* count) {
   return guard([&] {
     Context* c = C(ctx);
-    static const char* names[] = {"ntt_fwd", "ntt_inv", "bconv", "key_mult", "tensor", "combine", "hrot_tail"};
-    const uint32_t ncls = 7;
+    static const char* names[] = {"ntt_fwd", "ntt_inv", "bconv", "key_mult", "tensor", "combine", "hrot_tail",
+                                  "conv_mid"};
+    const uint32_t ncls = 8;
     if (!out || !count) throw InvalidArgument("null argument");
     CK_CUDA(cudaDeviceSynchronize());
     std::vector<ck_prof_stat> st(ncls);

@@ -27,6 +27,38 @@ void ntt_inverse(int logn, const NttLaunch& a, cudaStream_t st);
 // row-pass tables built by the host ([prime][256 rows][256] {w, w'}).
 bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st);
 bool ntt256_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st);
+// single-pass cluster/DSMEM variant (ntt_cluster.cu)
+bool ntt_cluster_available();
+void ntt_cluster_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st);
+void ntt_cluster_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st);
+// single pass: 0 fwd column, 1 fwd row (in place on dst), 2 inv row (src->dst), 3 inv column (in place on dst)
+void ntt256_pass(int which, const NttLaunch& a, const uint2* tw2, cudaStream_t st);
+
+// Fused INTT pass B (+part 1) -> BConv -> forward NTT pass 1 (ntt256.cu).
+struct ConvMidGroup {
+  uint32_t src_off;      // first source row (rows contiguous in src)
+  uint32_t sc, dc;       // source / destination row counts
+  uint32_t cmat_off;     // dc x sc constants ((P/P_j) mod q_i) R^2 mod q_i
+  uint32_t map_off;      // into dst_row / dst_prime
+  uint32_t src_map_off;  // into src_prime / src_exit
+};
+struct ConvMidLaunch {
+  const ConvMidGroup* groups = nullptr;
+  int ngroups = 0, batch = 1, max_sc = 1;
+  const uint32_t* src = nullptr;  // INTT pass-A output
+  uint64_t src_bs = 0;
+  uint32_t* dst = nullptr;        // forward pass-1 output (row pass pending)
+  uint64_t dst_bs = 0;
+  const uint32_t* cmat = nullptr;
+  const uint32_t* dst_row = nullptr;
+  const uint16_t* dst_prime = nullptr;
+  const uint16_t* src_prime = nullptr;
+  const ExitConst* src_exit = nullptr;
+  const PrimeDev* primes = nullptr;
+  const uint2* fwd_tw = nullptr;
+  const uint2* inv_tw = nullptr;
+};
+void conv_mid(const ConvMidLaunch& a, cudaStream_t st);
 
 // One base-conversion group: src rows [src_off, src_off+sc) of the source
 // buffer, dc destination rows dst_row[map_off + i] (row offsets in the

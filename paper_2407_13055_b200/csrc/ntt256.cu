@@ -438,7 +438,193 @@ void launch_col(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaSt
                                                          a.primes, a.tw, a.exits, a.entry);
 }
 
+// ===================================================== fused ModUp / ModDown ==
+// k_conv_mid: INTT pass B (+ exit, + BConv part 1) of the sc source rows,
+// BConv part 2 to the dc destination rows, and forward NTT pass 1 of every
+// destination row, for one 256 x 8 column tile, in one kernel:
+//   reference chain  inverse_row(part1) -> bconv_part2 -> forward_row
+//   (ckks.cpp:698-724 for ModUp, ckks.cpp:621-640 for drop_and_divide).
+// The converted rows never visit HBM between BConv and the first NTT pass;
+// the source tiles are read once from HBM (INTT pass-A output).
+// Layout: source tiles [s][256][2 quads] uint4 in smem with row swizzle
+// r ^ ((r>>4)&3) (conflict-free for both the stride-16 and the contiguous
+// row patterns), one 8 KB staging tile per warp for the destination
+// transpose.  Warp w runs the INTT of sources w, w+8, .. then the
+// destination rows w, w+8, ..; lane = (tau = lane>>1, cq = lane&1).
+constexpr int kMTC = 8;  // columns per tile
+constexpr int kMTiles = kR / kMTC;
+__device__ __forceinline__ int msw(int r) { return r ^ ((r >> 4) & 3); }
+
+template <int SC>
+__global__ void __launch_bounds__(256, 1) k_conv_mid(ConvMidLaunch a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint4* srct = reinterpret_cast<uint4*>(smraw);                 // [SC][256][2]
+  uint4* stg = srct + SC * 512 + (threadIdx.x >> 5) * 512;       // per-warp [256][2]
+  const ConvMidGroup G = a.groups[blockIdx.y];
+  const int b = blockIdx.z, c0 = blockIdx.x * kMTC;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tau = lane >> 1, cq = lane & 1;
+  // ---- load the source tiles (INTT pass-A output, [0, 2q))
+  const uint32_t* sbase = a.src + b * a.src_bs + (size_t)G.src_off * kN + c0;
+  for (int e = threadIdx.x; e < (int)G.sc * 512; e += 256) {
+    const int s = e >> 9, r = (e >> 1) & 255, h = e & 1;
+    cp16(&srct[s * 512 + msw(r) * 2 + h], sbase + (size_t)s * kN + r * kR + 4 * h);
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  // ---- phase I: inverse column pass of each source (exit folds N^-1 R^-1 part1)
+  for (int s = warp; s < (int)G.sc; s += 8) {
+    const int g = a.src_prime[G.src_map_off + s];
+    const PrimeDev P = a.primes[g];
+    const uint32_t q = P.q, q2 = P.q2;
+    const ExitConst ex = a.src_exit[G.src_map_off + s];
+    const uint2* tw = a.inv_tw + (size_t)g * kN;
+    uint4* T = srct + s * 512;
+    uint4 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = T[msw(16 * tau + j) * 2 + cq];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int d = 1 << t;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int blk = p / d, j = blk * 2 * d + p % d;
+        gs4(v[j], v[j + d], __ldg(&tw[(128 >> t) + (tau << (3 - t)) + blk]), q, q2);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) T[msw(16 * tau + j) * 2 + cq] = v[j];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = T[msw(tau + 16 * j) * 2 + cq];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int d = 1 << t;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int blk = p / d, j = blk * 2 * d + p % d;
+        gs4(v[j], v[j + d], __ldg(&tw[(8 >> t) + blk]), q, q2);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#define CK_X(c)                                                            \
+  {                                                                        \
+    const uint32_t u = v[j].c + v[j + 8].c, dd = v[j].c - v[j + 8].c + q2; \
+    v[j].c = sub_if(shoup_mul(u, ex.x, ex.y, q), q);                       \
+    v[j + 8].c = sub_if(shoup_mul(dd, ex.z, ex.w, q), q);                  \
+  }
+      CK_X(x) CK_X(y) CK_X(z) CK_X(w)
+#undef CK_X
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) T[msw(tau + 16 * j) * 2 + cq] = v[j];  // canonical coefficients
+  }
+  __syncthreads();
+  // ---- phase II: BConv (x R folded into the matrix) + forward pass 1 per destination
+  for (int i = warp; i < (int)G.dc; i += 8) {
+    const int g = a.dst_prime[G.map_off + i];
+    const PrimeDev P = a.primes[g];
+    const uint32_t q = P.q, q2 = P.q2;
+    const uint32_t* cm = a.cmat + G.cmat_off + i * G.sc;
+    uint32_t c[SC];
+#pragma unroll
+    for (int s = 0; s < SC; ++s) c[s] = s < (int)G.sc ? __ldg(&cm[s]) : 0u;
+    uint4 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int rr = msw(tau + 16 * j) * 2 + cq;
+      uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+      for (int s = 0; s < SC; ++s) {
+        if (s < (int)G.sc) {
+          const uint4 x = srct[s * 512 + rr];
+          a0 += (uint64_t)x.x * c[s];
+          a1 += (uint64_t)x.y * c[s];
+          a2 += (uint64_t)x.z * c[s];
+          a3 += (uint64_t)x.w * c[s];
+        }
+      }
+      v[j] = make_uint4(mont_reduce64(a0, q, P.qinv_neg), mont_reduce64(a1, q, P.qinv_neg),
+                        mont_reduce64(a2, q, P.qinv_neg), mont_reduce64(a3, q, P.qinv_neg));  // [0, 2q)
+    }
+    const uint2* tw = a.fwd_tw + (size_t)g * kN;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int d = 8 >> t;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int blk = p / d, j = blk * 2 * d + p % d;
+        ct4(v[j], v[j + d], __ldg(&tw[(1 << t) + blk]), q, q2);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) stg[msw(tau + 16 * j) * 2 + cq] = v[j];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = stg[msw(16 * tau + j) * 2 + cq];
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int d = 8 >> t;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int blk = p / d, j = blk * 2 * d + p % d;
+        ct4(v[j], v[j + d], __ldg(&tw[(16 << t) + (tau << t) + blk]), q, q2);
+      }
+    }
+    uint32_t* o = a.dst + b * a.dst_bs + (size_t)a.dst_row[G.map_off + i] * kN + c0 + 4 * cq;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) stg4(o + (16 * tau + j) * kR, v[j]);
+  }
+}
+
 }  // namespace
+
+void conv_mid(const ConvMidLaunch& a, cudaStream_t st) {
+  const int smem = (a.max_sc * 512 + 8 * 512) * 16;
+  dim3 grid(kMTiles, a.ngroups, a.batch);
+  switch (a.max_sc) {
+#define CK_SC(S)                                                                              \
+  case S: {                                                                                   \
+    static bool attr = false;                                                                 \
+    if (!attr) {                                                                              \
+      cudaFuncSetAttribute(k_conv_mid<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      attr = true;                                                                            \
+    }                                                                                         \
+    k_conv_mid<S><<<grid, 256, smem, st>>>(a);                                                \
+    break;                                                                                    \
+  }
+    CK_SC(1) CK_SC(2) CK_SC(3) CK_SC(4) CK_SC(5) CK_SC(6) CK_SC(7) CK_SC(8) CK_SC(9) CK_SC(10)
+#undef CK_SC
+    default: break;
+  }
+}
+
+// Individual passes (used when the fused kernels replace the other pass).
+void ntt256_pass(int which, const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
+  init_grids();
+  const int row_items = a.njobs * (kR / kRRows) * a.batch;
+  switch (which) {
+    case 0:
+      launch_col<false>(a, a.src, a.src_bs, st);
+      break;
+    case 1:  // forward row pass, in place on dst
+      k_row<false><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs,
+                                                                      a.batch, a.njobs, a.primes, tw2);
+      break;
+    case 2:  // inverse row pass src -> dst
+      k_row<true><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.src, a.src_bs, a.dst, a.dst_bs,
+                                                                     a.batch, a.njobs, a.primes, tw2);
+      break;
+    default: {
+      NttLaunch b = a;
+      b.entry = 0;
+      launch_col<true>(b, a.dst, a.dst_bs, st);
+    }
+  }
+}
 
 bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
   init_grids();
