@@ -260,8 +260,11 @@ struct Context {
   std::map<std::string, std::unique_ptr<NttPlan>> adhoc_ntt;
   std::map<std::string, std::unique_ptr<BconvPlan>> adhoc_bc;
   std::map<uint32_t, std::unique_ptr<Blob>> row_primes;  // (level+alpha)-row prime maps
-  void* scratch = nullptr;
-  size_t scratch_bytes = 0;
+  struct Scratch {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<cudaStream_t, Scratch> scratch;  // one arena per stream: mechanisms on different streams run concurrently
   uint64_t counters[7] = {0, 0, 0, 0, 0, 0, 0};  // modup moddown ntt intt keymult bconv rescale
   std::atomic<uint64_t> launches{0};
 
@@ -320,7 +323,8 @@ struct Context {
     if (d_pmont) cudaFree(d_pmont);
     if (d_tw2f) cudaFree(d_tw2f);
     if (d_tw2i) cudaFree(d_tw2i);
-    if (scratch) cudaFree(scratch);
+    for (auto& kv : scratch)
+      if (kv.second.ptr) cudaFree(kv.second.ptr);
   }
 
   uint32_t q(uint32_t g) const { return primes[g]; }
@@ -328,16 +332,17 @@ struct Context {
   uint32_t digits(uint32_t level) const { return (level + alpha - 1) / alpha; }
   size_t rowsz() const { return (size_t)n; }
 
-  void* scratch_get(size_t bytes) {
-    if (bytes > scratch_bytes) {
-      CK_CUDA(cudaDeviceSynchronize());
-      if (scratch) cudaFree(scratch);
-      scratch = nullptr;
+  void* scratch_get(size_t bytes, cudaStream_t st) {
+    Scratch& sc = scratch[st];
+    if (bytes > sc.bytes) {
+      CK_CUDA(cudaStreamSynchronize(st));
+      if (sc.ptr) cudaFree(sc.ptr);
+      sc.ptr = nullptr;
       const size_t want = bytes + bytes / 8;
-      CK_CUDA(cudaMalloc(&scratch, want));
-      scratch_bytes = want;
+      CK_CUDA(cudaMalloc(&sc.ptr, want));
+      sc.bytes = want;
     }
-    return scratch;
+    return sc.ptr;
   }
 
   // Inverse exit constants for prime g with plain epilogue factor e (ntt.cpp:76-84).
@@ -1230,7 +1235,7 @@ ck_status ck_mod_up(ck_context* ctx, uint32_t level, const uint32_t* d, uint32_t
     check_ptr(hoist);
     const uint64_t N = c->n;
     const uint32_t D = c->digits(level), rows = level + c->alpha;
-    uint32_t* is = static_cast<uint32_t*>(c->scratch_get(level * N * 4));
+    uint32_t* is = static_cast<uint32_t*>(c->scratch_get(level * N * 4, S(stream)));
     c->mod_up(level, 1, d, 0, is, hoist, S(stream));
     // the public HoistState carries the digit rows too (ckks.cpp:708-709)
     for (uint32_t k = 0; k < D; ++k) {
@@ -1254,7 +1259,7 @@ ck_status ck_key_mult(ck_context* ctx, uint32_t level, const uint32_t* hoist, co
     // level-row buffer; gather them out of the full HoistState first.
     const uint32_t rows = level + c->alpha;
     const uint64_t N = c->n;
-    uint32_t* dd = static_cast<uint32_t*>(c->scratch_get(level * N * 4));
+    uint32_t* dd = static_cast<uint32_t*>(c->scratch_get(level * N * 4, S(stream)));
     const uint32_t D = c->digits(level);
     for (uint32_t k = 0; k < D; ++k) {
       const uint32_t b = k * c->alpha, e = std::min((k + 1) * c->alpha, level);
@@ -1273,7 +1278,7 @@ ck_status ck_mod_down(ck_context* ctx, uint32_t level, const uint32_t* v, uint32
     check_ptr(v);
     check_ptr(out);
     const SwitchPlan& pl = c->switch_plan(0, level, 1);
-    uint32_t* ts = static_cast<uint32_t*>(c->scratch_get((size_t)pl.sc * c->n * 4));
+    uint32_t* ts = static_cast<uint32_t*>(c->scratch_get((size_t)pl.sc * c->n * 4, S(stream)));
     c->drop_divide(pl, 1, v, 0, ts, out, true, S(stream));
     c->counters[1] += 1;
     check_launch();
@@ -1292,7 +1297,7 @@ ck_status ck_key_switch(ck_context* ctx, uint32_t level, const uint32_t* d, cons
     const uint32_t D = c->digits(level), rows = level + c->alpha;
     const SwitchPlan& pl = c->switch_plan(0, level, 2);
     const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N;
-    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w) * 4));
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w) * 4, S(stream)));
     uint32_t *is = base, *ext = is + is_w, *v = ext + ext_w, *ts = v + v_w;
     c->mod_up(level, 1, d, 0, is, ext, S(stream));
     c->key_mult_v(level, 1, ext, d, 0, evk, nullptr, 0, v, S(stream));
@@ -1310,7 +1315,7 @@ ck_status ck_rescale(ck_context* ctx, uint32_t level, uint32_t batch, const uint
     check_ptr(ct);
     check_ptr(out);
     const SwitchPlan& pl = c->switch_plan(1, level, 2);
-    uint32_t* ts = static_cast<uint32_t*>(c->scratch_get((size_t)batch * 2 * pl.sc * c->n * 4));
+    uint32_t* ts = static_cast<uint32_t*>(c->scratch_get((size_t)batch * 2 * pl.sc * c->n * 4, S(stream)));
     c->drop_divide(pl, (int)batch, ct, 2ull * level * c->n, ts, out, true, S(stream));
     c->counters[6] += batch;
     check_launch();
@@ -1335,7 +1340,7 @@ ck_status ck_hmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32
     const size_t t01_w = 2ull * level * N, d2_w = level * N, is_w = level * N, ext_w = (size_t)D * rows * N,
                  v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N, c_w = lazy ? 2ull * level * N : 0;
     const size_t per = t01_w + d2_w + is_w + ext_w + v_w + ts_w + c_w;
-    uint32_t* base = static_cast<uint32_t*>(c->scratch_get(per * B * 4));
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get(per * B * 4, S(stream)));
     uint32_t* t01 = base;
     uint32_t* d2 = t01 + t01_w * B;
     uint32_t* is = d2 + d2_w * B;
@@ -1383,7 +1388,7 @@ ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_
     const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N,
                  o_w = 2ull * level * N;
     const size_t per = is_w + ext_w + v_w + ts_w + o_w;
-    uint32_t* base = static_cast<uint32_t*>(c->scratch_get(per * B * 4));
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get(per * B * 4, S(stream)));
     uint32_t* is = base;
     uint32_t* ext = is + is_w * B;
     uint32_t* v = ext + ext_w * B;
@@ -1461,7 +1466,7 @@ ck_status ck_hoisted_rotations(ck_context* ctx, uint32_t level, const uint32_t* 
     const SwitchPlan& pl = c->switch_plan(0, level, 2);
     const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N,
                  o_w = 2ull * level * N;
-    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w + o_w) * 4));
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w + o_w) * 4, S(stream)));
     uint32_t *is = base, *ext = is + is_w, *v = ext + ext_w, *ts = v + v_w, *o = ts + ts_w;
     cudaStream_t st = S(stream);
     const uint32_t* a = ct + level * N;
@@ -1498,7 +1503,7 @@ ck_status ck_hoisted_rotate_accumulate(ck_context* ctx, uint32_t level, const ui
     const SwitchPlan& pl = c->switch_plan(0, level, 2);
     const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N,
                  acc_w = 2ull * rows * N, o_w = 2ull * level * N;
-    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w + acc_w + o_w) * 4));
+    uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w + acc_w + o_w) * 4, S(stream)));
     uint32_t *is = base, *ext = is + is_w, *v = ext + ext_w, *ts = v + v_w, *acc = ts + ts_w, *o = acc + acc_w;
     cudaStream_t st = S(stream);
     const uint32_t* b = ct;

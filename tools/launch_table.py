@@ -17,7 +17,7 @@ def load(path):
         k = (int(r["ID"]), r["Kernel Name"], r["Grid Size"])
         unit = r["Metric Unit"]
         v = float(r["Metric Value"].replace(",", ""))
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
                  "Gbyte": 1e9}.get(unit, 1.0)
         per.setdefault(k, {})[r["Metric Name"]] = v * scale
     return per
