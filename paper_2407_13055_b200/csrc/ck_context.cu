@@ -252,6 +252,7 @@ struct Context {
   uint2* d_tw2i = nullptr;
   bool use_ntt256 = true;
   bool use_cluster = false;  // CK32_NTT_CLUSTER=1: single-pass 8-CTA cluster/DSMEM NTT (slower today)
+  bool use_row_km = true;  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
   bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
   int ntt_chunk_limbs = 1 << 30;  // limbs per pass-1/pass-2 launch pair (CK32_NTT_CHUNK; measured: no gain)
   std::map<uint32_t, std::unique_ptr<ModUpPlan>> modup;
@@ -765,6 +766,60 @@ struct Context {
     counters[2] += (uint64_t)B * pl.ntt_rows;
   }
 
+  // ModUp + KeyMult (+ fold) into v [B][2][level+alpha]. For N = 2^16 the
+  // extension's forward row pass is fused into KeyMult (k_row_keymult): ext
+  // only ever holds column-pass output.
+  void mod_up_key_mult(uint32_t level, int B, const uint32_t* d, uint64_t d_bs, uint32_t* is, uint32_t* ext,
+                       const uint32_t* evk, const uint32_t* fold, uint64_t fold_bs, uint32_t* v, cudaStream_t st) {
+    if (!(logn == 16 && d_tw2f && use_ntt256 && use_row_km)) {
+      mod_up(level, B, d, d_bs, is, ext, st);
+      key_mult_v(level, B, ext, d, d_bs, evk, fold, fold_bs, v, st);
+      return;
+    }
+    const ModUpPlan& pl = modup_plan(level);
+    const uint64_t N = n;
+    const uint64_t ext_bs = (uint64_t)pl.D * (level + alpha) * N;
+    run_ntt(pl.intt, true, B, d, d_bs, is, level * N, 0, st);
+    run_bconv(pl.bc, B, is, level * N, ext, ext_bs, st);
+    {
+      ProfScope ps(this, 0, 4.0 * n * pl.ntt.njobs * B, 1, st);  // column pass: half of the NTT traffic
+      NttLaunch a = ntt_args(pl.ntt, false, B, ext, ext_bs, ext, ext_bs);
+      a.entry = 1;
+      ntt256_pass(0, a, d_tw2f, st);
+    }
+    KeyMultLaunch a;
+    a.level = (int)level;
+    a.alpha = (int)alpha;
+    a.L = (int)L;
+    a.D = (int)pl.D;
+    a.batch = B;
+    a.ext = ext;
+    a.ext_bs = ext_bs;
+    a.d = d;
+    a.d_bs = d_bs;
+    a.evk = evk;
+    a.fold = fold;
+    a.fold_bs = fold_bs;
+    a.p_mont = d_pmont;
+    a.v = v;
+    a.v_bs = 2ull * (level + alpha) * n;
+    a.primes = d_primes;
+    {
+      // row pass (4N B per extension row) + KeyMult traffic
+      ProfScope ps(this, 8,
+                   4.0 * n * pl.ntt_rows * B + 4.0 * n * (level + alpha) * (2.0 * pl.D + 2) * B +
+                       (fold ? 8.0 * n * level * B : 0.0),
+                   1, st);
+      row_keymult(a, d_tw2f, st);
+    }
+    launches += 2;
+    counters[0] += B;
+    counters[3] += (uint64_t)B * level;
+    counters[5] += (uint64_t)B * pl.D;
+    counters[2] += (uint64_t)B * pl.ntt_rows;
+    counters[4] += (uint64_t)B * pl.D;
+  }
+
   // key_mult (+ optional fold) into v [B][2][level+alpha]
   void key_mult_v(uint32_t level, int B, const uint32_t* ext, const uint32_t* d, uint64_t d_bs, const uint32_t* evk,
                   const uint32_t* fold, uint64_t fold_bs, uint32_t* v, cudaStream_t st) {
@@ -941,6 +996,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     c->use_ntt256 = std::getenv("CK32_GENERIC_NTT") == nullptr;  // A/B switch for parity tests
     if (const char* ch = std::getenv("CK32_NTT_CHUNK")) c->ntt_chunk_limbs = std::max(1, std::atoi(ch));
     c->use_fused = std::getenv("CK32_FUSED") != nullptr;
+    c->use_row_km = std::getenv("CK32_NO_ROW_KEYMULT") == nullptr;
     c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;
     if (n == 65536) {
       // Row-pass twiddles of ntt256.cu, permuted per row in thread-consumption
@@ -1039,8 +1095,8 @@ ck_status ck_profile_read(ck_context* ctx, ck_prof_stat* out, uint32_t max_class
   return guard([&] {
     Context* c = C(ctx);
     static const char* names[] = {"ntt_fwd", "ntt_inv", "bconv", "key_mult", "tensor", "combine", "hrot_tail",
-                                  "conv_mid"};
-    const uint32_t ncls = 8;
+                                  "conv_mid", "ntt_row+keymult"};
+    const uint32_t ncls = 9;
     if (!out || !count) throw InvalidArgument("null argument");
     CK_CUDA(cudaDeviceSynchronize());
     std::vector<ck_prof_stat> st(ncls);
@@ -1299,8 +1355,7 @@ ck_status ck_key_switch(ck_context* ctx, uint32_t level, const uint32_t* d, cons
     const size_t is_w = level * N, ext_w = (size_t)D * rows * N, v_w = 2ull * rows * N, ts_w = 2ull * pl.sc * N;
     uint32_t* base = static_cast<uint32_t*>(c->scratch_get((is_w + ext_w + v_w + ts_w) * 4, S(stream)));
     uint32_t *is = base, *ext = is + is_w, *v = ext + ext_w, *ts = v + v_w;
-    c->mod_up(level, 1, d, 0, is, ext, S(stream));
-    c->key_mult_v(level, 1, ext, d, 0, evk, nullptr, 0, v, S(stream));
+    c->mod_up_key_mult(level, 1, d, 0, is, ext, evk, nullptr, 0, v, S(stream));
     c->drop_divide(pl, 1, v, 0, ts, out, true, S(stream));
     c->counters[1] += 1;
     check_launch();
@@ -1354,12 +1409,11 @@ ck_status ck_hmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32
       tensor((int)N, (int)level, B, x, y, 2ull * level * N, t01, t01_w, d2, d2_w, c->d_primes, st);
     }
     ++c->launches;
-    c->mod_up(level, B, d2, d2_w, is, ext, st);
     if (!lazy) {
-      c->key_mult_v(level, B, ext, d2, d2_w, relin_evk, t01, t01_w, v, st);  // fold P*d0/1 fused
+      c->mod_up_key_mult(level, B, d2, d2_w, is, ext, relin_evk, t01, t01_w, v, st);  // fold P*d0/1 fused
       c->drop_divide(pl, B, v, v_w, ts, out, true, st);
     } else {
-      c->key_mult_v(level, B, ext, d2, d2_w, relin_evk, nullptr, 0, v, st);
+      c->mod_up_key_mult(level, B, d2, d2_w, is, ext, relin_evk, nullptr, 0, v, st);
       c->drop_divide(pl, B, v, v_w, ts, cc, true, st);
       // out.b = d0 + c0, out.a = d1 + c1 (ckks.cpp:857-858)
       elementwise((int)N, (int)(2 * level), B, 0, t01, t01_w, cc, c_w, out, 2ull * level * N, nullptr,
@@ -1397,8 +1451,7 @@ ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_
     cudaStream_t st = S(stream);
     const uint64_t ct_bs = 2ull * level * N;
     const uint32_t* a = ct + level * N;
-    c->mod_up(level, B, a, ct_bs, is, ext, st);
-    c->key_mult_v(level, B, ext, a, ct_bs, rot_evk, nullptr, 0, v, st);
+    c->mod_up_key_mult(level, B, a, ct_bs, is, ext, rot_evk, nullptr, 0, v, st);
     c->drop_divide(pl, B, v, v_w, ts, o, false, st);
     {
       Context::ProfScope ps(c, 6, 4.0 * N * level * 7 * B, 1, st);  // v0 v1 o0 o1 b in, 2 out

@@ -17,6 +17,7 @@
 //    warp-local (no CTA barrier); the row's 30 twiddle pairs live in
 //    registers and are reused across consecutive batch items of the job.
 // Butterflies: Harvey-lazy Shoup (IMAD.HI + 2 IMAD, values in [0, 4q)).
+#include <algorithm>
 #include <cstdlib>
 
 #include "ck_common.cuh"
@@ -580,7 +581,186 @@ __global__ void __launch_bounds__(256, 1) k_conv_mid(ConvMidLaunch a) {
   }
 }
 
+// ============================================ NTT pass 2 fused with KeyMult ==
+// k_row_keymult: for output row i of v = [v0; v1] (level + alpha rows) and a
+// tile of 8 coefficient rows, run the forward row pass on every digit's
+// ModUp extension row (pass-1 output) — or take the digit's own row straight
+// from d (evaluation domain) — and accumulate the KeyMult products with both
+// key halves in int64, plus the merged-HMult fold P*d0 / P*d1:
+//   reference  forward_row (mod_up, ckks.cpp:718-724) -> key_mult
+//              (ckks.cpp:744-767) -> fold (ckks.cpp:831-842).
+// The extension never returns to HBM after its row pass.
+constexpr int kKT = 128;  // 8 rows x 16 threads
+constexpr int kKBuf = kRRows * kRowStride;
+constexpr int kKSmem = 2 * kKBuf * 4 + kRRows * kR * 8;
+
+__global__ void __launch_bounds__(kKT) k_row_keymult(KeyMultLaunch a, const uint2* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
+  uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * kKBuf * 4);
+  const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15;
+  constexpr int kTiles = kR / kRRows;
+  const int rows = a.level + a.alpha, B = a.batch;
+  const uint32_t LA = (uint32_t)(a.L + a.alpha);
+  const int items = rows * kTiles * B;  // (row i, tile, b), b fastest
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
+  int cur_key = -1;
+  int kbuf = 0;
+  for (int it = i0; it < i1; ++it) {
+    const int b = it % B, key = it / B, tile = key % kTiles, i = key / kTiles;
+    const int g = i < a.level ? i : a.L + (i - a.level);
+    const PrimeDev P = a.primes[g];
+    const uint32_t q = P.q, q2 = P.q2;
+    if (key != cur_key) {
+      __syncthreads();
+      const uint2* T = tw2 + ((size_t)g * kR + tile * kRRows) * kR;
+      for (int e = tid; e < kRRows * kR / 2; e += kKT) cp16(&tws[2 * e], &T[2 * e]);
+      cp_commit();
+      cur_key = key;
+    }
+    const int r = tile * kRRows + rho;
+    const uint2* W = tws + rho * kR;
+    uint64_t s0[16], s1[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s0[j] = s1[j] = 0;
+    const size_t rofs = (size_t)r * kR + 16 * tau;  // this thread's 16 coefficients after the row pass
+    for (int k = 0; k < a.D; ++k) {
+      const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+      uint32_t v[16];
+      if (i >= lo && i < hi) {  // the digit's own row: ModUp passes it through unchanged
+        const uint32_t* dr = a.d + b * a.d_bs + (size_t)i * kN + rofs;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const uint4 x = *reinterpret_cast<const uint4*>(dr + 4 * m);
+          v[4 * m] = x.x;
+          v[4 * m + 1] = x.y;
+          v[4 * m + 2] = x.z;
+          v[4 * m + 3] = x.w;
+        }
+      } else {
+        uint32_t* buf = sbuf + kbuf * kKBuf;
+        kbuf ^= 1;
+        const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)tile * kRRows * kR;
+#pragma unroll
+        for (int m = 0; m < kRRows * 64 / kKT; ++m) {
+          const int e = tid + m * kKT, rr = e >> 6, c = (e & 63) * 4;
+          cp16(buf + rr * kRowStride + rpos(c), gsrc + rr * kR + c);
+        }
+        cp_commit();
+        cp_wait<0>();
+        __syncthreads();
+        uint32_t* line = buf + rho * kRowStride;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = line[rpos(tau + 16 * j)];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int d = 8 >> t;
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = W[(1 << t) - 1 + blk];
+            ct(v[j], v[j + d], w.x, w.y, q, q2);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) line[rpos(tau + 16 * j)] = v[j];
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const uint4 x = *reinterpret_cast<const uint4*>(line + rpos(16 * tau) + 4 * m);
+          v[4 * m] = x.x;
+          v[4 * m + 1] = x.y;
+          v[4 * m + 2] = x.z;
+          v[4 * m + 3] = x.w;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int d = 8 >> t;
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = W[16 + ((1 << t) - 1 + blk) * 16 + tau];
+            ct(v[j], v[j + d], w.x, w.y, q, q2);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = canon4(v[j], q, q2);
+      }
+      // KeyMult MACs with both key halves (rows indexed by the global prime, ckks.cpp:747)
+      const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
+      const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const uint4 xb = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
+        const uint4 xa = __ldg(reinterpret_cast<const uint4*>(ea + 4 * m));
+        s0[4 * m] += (uint64_t)v[4 * m] * xb.x;
+        s0[4 * m + 1] += (uint64_t)v[4 * m + 1] * xb.y;
+        s0[4 * m + 2] += (uint64_t)v[4 * m + 2] * xb.z;
+        s0[4 * m + 3] += (uint64_t)v[4 * m + 3] * xb.w;
+        s1[4 * m] += (uint64_t)v[4 * m] * xa.x;
+        s1[4 * m + 1] += (uint64_t)v[4 * m + 1] * xa.y;
+        s1[4 * m + 2] += (uint64_t)v[4 * m + 2] * xa.z;
+        s1[4 * m + 3] += (uint64_t)v[4 * m + 3] * xa.w;
+      }
+      if ((k % 6) == 5) {  // keep the sums below q 2^32 (value unchanged mod q, rescaled by R)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          s0[j] = shoup_mul(mont_reduce64(s0[j], q, P.qinv_neg), P.r, P.r_sh, q);
+          s1[j] = shoup_mul(mont_reduce64(s1[j], q, P.qinv_neg), P.r, P.r_sh, q);
+        }
+      }
+    }
+    if (a.fold && i < a.level) {  // merged HMult: v += P * d0 / d1 (ckks.cpp:831-842)
+      const uint32_t pm = a.p_mont[i];
+      const uint32_t* f0 = a.fold + b * a.fold_bs + (size_t)i * kN + rofs;
+      const uint32_t* f1 = a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + rofs;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const uint4 x0 = *reinterpret_cast<const uint4*>(f0 + 4 * m);
+        const uint4 x1 = *reinterpret_cast<const uint4*>(f1 + 4 * m);
+        s0[4 * m] += (uint64_t)x0.x * pm;
+        s0[4 * m + 1] += (uint64_t)x0.y * pm;
+        s0[4 * m + 2] += (uint64_t)x0.z * pm;
+        s0[4 * m + 3] += (uint64_t)x0.w * pm;
+        s1[4 * m] += (uint64_t)x1.x * pm;
+        s1[4 * m + 1] += (uint64_t)x1.y * pm;
+        s1[4 * m + 2] += (uint64_t)x1.z * pm;
+        s1[4 * m + 3] += (uint64_t)x1.w * pm;
+      }
+    }
+    uint32_t* o0 = a.v + b * a.v_bs + (size_t)i * kN + rofs;
+    uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv_neg), q)));
+      stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv_neg), q)));
+    }
+  }
+  cp_wait<0>();
+}
+
 }  // namespace
+
+void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_row_keymult, cudaFuncAttributeMaxDynamicSharedMemorySize, kKSmem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult, kKT, kKSmem);
+    grid = sms * std::max(1, per);
+  }
+  const int items = (a.level + a.alpha) * (kR / kRRows) * a.batch;
+  k_row_keymult<<<std::min(grid, items), kKT, kKSmem, st>>>(a, tw2);
+}
 
 void conv_mid(const ConvMidLaunch& a, cudaStream_t st) {
   const int smem = (a.max_sc * 512 + 8 * 512) * 16;

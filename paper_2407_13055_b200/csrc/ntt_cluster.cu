@@ -2,18 +2,20 @@
 //
 // Same transform as ntt.cpp:176-272 (256 x 256 decomposition as ntt256.cu),
 // but each limb crosses HBM exactly once in each direction: the pass-1 /
-// pass-2 transpose goes through distributed shared memory instead of L2/HBM.
+// pass-2 transpose goes through distributed shared memory instead of HBM.
 //
-//   cluster of 8 CTAs (one per SM), CTA rank k:
+//   cluster of 8 CTAs, CTA rank k:
 //   forward  — pass 1 on columns [32k, 32k+32) of the limb (all 256 rows, in
 //              its own smem), cluster barrier, pass 2 on rows [32k, 32k+32)
-//              reading 7/8 of each row from the 7 peers' smem (DSMEM);
+//              reading 7/8 of each row from the 7 peers' smem (DSMEM),
+//              cluster barrier (the block may be refilled);
 //   inverse  — pass A on rows [32k, 32k+32), cluster barrier, pass B (+exit,
-//              +BConv part 1) on columns [32k, 32k+32) reading from peers.
-// Work items are (job, batch item) with the batch fastest: the 32 rows' worth
-// of per-row twiddle tables (64 KB) is staged once per job and reused for the
-// whole batch; the next item's input is prefetched with cp.async into the
-// second buffer right after the cluster barrier, overlapping pass 2.
+//              +BConv part 1) on columns [32k, 32k+32) reading from peers,
+//              cluster barrier.
+// A CTA needs < 80 KB of shared memory and <= 128 registers per thread so two
+// CTAs of different clusters share an SM: one cluster's loads and barriers
+// overlap the other's butterflies.  Row-pass twiddles are read from the
+// per-row permuted tables in L2 (warp-broadcast / coalesced).
 #include <algorithm>
 
 #include <cooperative_groups.h>
@@ -60,13 +62,12 @@ __device__ __forceinline__ void gs2(uint2& x, uint2& y, uint2 w, uint32_t q, uin
 
 // ---------------------------------------------------------------- forward --
 struct FwdSmem {
-  uint32_t col[2][256 * kB];  // column block, [row][32 cols], double buffered (2 x 32 KB)
-  uint2 rtw[kB * 256];        // per-row permuted twiddles of this CTA's 32 rows (64 KB)
-  uint2 ctw[256];             // column-pass twiddles
-  uint32_t stage[16 * kRS];   // row exchange (16 rows at a time)
+  uint32_t col[256 * kB];    // column block [row][32 cols] (32 KB)
+  uint2 ctw[256];            // column-pass twiddles of the current prime
+  uint32_t stage[16 * kRS];  // row exchange (16 rows at a time)
 };
 
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 2)
     k_fwd_cluster(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src, uint64_t src_bs,
                   uint32_t* __restrict__ dst, uint64_t dst_bs, int batch, int njobs, const PrimeDev* __restrict__ primes,
                   const uint2* __restrict__ fwd_tw, const uint2* __restrict__ tw2, int entry) {
@@ -77,39 +78,30 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
   const int cid = blockIdx.x / kCl, ncl = gridDim.x / kCl;
   const int tid = threadIdx.x;
   const int items = njobs * batch;
-  auto prefetch = [&](int it, int buf) {
-    const RowJob J = jobs[it / batch];
-    const uint32_t* g = src + (it % batch) * src_bs + (size_t)J.src_off * kN + kB * k;
+  const uint32_t* peer[kCl];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {  // 256 rows x 8 chunks of 16 B
-      const int e = tid + m * kT, r = e >> 3, c4 = e & 7;
-      cp16(&S.col[buf][r * kB + 4 * c4], g + r * kR + 4 * c4);
-    }
-  };
-  int it = cid;
-  if (it < items) prefetch(it, 0);
-  cp_commit();
-  int cur_job = -1;
-  for (int i = 0; it < items; ++i, it += ncl) {
-    const int buf = i & 1, job = it / batch, b = it % batch;
+  for (int kk = 0; kk < kCl; ++kk) peer[kk] = cluster.map_shared_rank(S.col, kk);
+  for (int it = cid; it < items; it += ncl) {
+    const int job = it / batch, b = it % batch;
     const RowJob J = jobs[job];
-    if (job != cur_job) {  // stage this prime's tables (reused over the batch)
-      __syncthreads();
-      const uint2* T = tw2 + ((size_t)J.prime * kR + kB * k) * kR;
+    {  // load this CTA's column block and the prime's column twiddles
+      const uint32_t* g = src + b * src_bs + (size_t)J.src_off * kN + kB * k;
 #pragma unroll
-      for (int m = 0; m < 16; ++m) cp16(&S.rtw[2 * (tid + m * kT)], &T[2 * (tid + m * kT)]);
+      for (int m = 0; m < 8; ++m) {
+        const int e = tid + m * kT, r = e >> 3, c4 = e & 7;
+        cp16(&S.col[r * kB + 4 * c4], g + r * kR + 4 * c4);
+      }
       if (tid < 128) cp16(&S.ctw[2 * tid], &fwd_tw[(size_t)J.prime * kN + 2 * tid]);
       cp_commit();
-      cur_job = job;
+      cp_wait_all();
+      __syncthreads();
     }
-    cp_wait_all();
-    __syncthreads();
     const PrimeDev P = primes[J.prime];
     const uint32_t q = P.q, q2 = P.q2;
     // ---- pass 1: columns 2cp, 2cp+1 of the block, stages 0..7
     {
       const int tau = tid >> 4, cp = tid & 15;
-      uint32_t* C = S.col[buf] + 2 * cp;
+      uint32_t* C = S.col + 2 * cp;
       uint2 v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = *reinterpret_cast<const uint2*>(C + (tau + 16 * j) * kB);
@@ -147,19 +139,14 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
       for (int j = 0; j < 16; ++j) *reinterpret_cast<uint2*>(C + (16 * tau + j) * kB) = v[j];
     }
     cluster.sync();  // every CTA's pass-1 block is complete and visible
-    if (it + ncl < items) prefetch(it + ncl, buf ^ 1);  // peers are past pass 2 of the previous item
-    cp_commit();
     // ---- pass 2: rows 32k .. 32k+31 (two rounds of 16), stages 8..15
     {
       const int rho = tid >> 4, tau = tid & 15;
-      const uint32_t* peer[kCl];
-#pragma unroll
-      for (int kk = 0; kk < kCl; ++kk) peer[kk] = cluster.map_shared_rank(S.col[buf], kk);
       uint32_t* line = S.stage + rho * kRS;
 #pragma unroll 1
       for (int round = 0; round < 2; ++round) {
-        const int lr = 16 * round + rho, r = kB * k + lr;
-        const uint2* W = S.rtw + lr * kR;
+        const int r = kB * k + 16 * round + rho;
+        const uint2* W = tw2 + ((size_t)J.prime * kR + r) * kR;  // per-row permuted table (L2)
         uint32_t v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = peer[j >> 1][r * kB + tau + 16 * (j & 1)];  // c = tau + 16 j
@@ -169,7 +156,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
 #pragma unroll
           for (int p = 0; p < 8; ++p) {
             const int blk = p / d, j = blk * 2 * d + p % d;
-            const uint2 w = W[(1 << t) - 1 + blk];
+            const uint2 w = __ldg(&W[(1 << t) - 1 + blk]);
             ct(v[j], v[j + d], w.x, w.y, q, q2);
           }
         }
@@ -191,7 +178,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
 #pragma unroll
           for (int p = 0; p < 8; ++p) {
             const int blk = p / d, j = blk * 2 * d + p % d;
-            const uint2 w = W[16 + ((1 << t) - 1 + blk) * 16 + tau];
+            const uint2 w = __ldg(&W[16 + ((1 << t) - 1 + blk) * 16 + tau]);
             ct(v[j], v[j + d], w.x, w.y, q, q2);
           }
         }
@@ -202,20 +189,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
                                         canon4(v[4 * m + 2], q, q2), canon4(v[4 * m + 3], q, q2)));
       }
     }
+    cluster.sync();  // peers are done reading this block
   }
-  cp_wait_all();
-  cluster.sync();  // no CTA may exit while a peer still reads its shared memory
 }
 
 // ---------------------------------------------------------------- inverse --
 struct InvSmem {
-  uint32_t rows[2][kB * kRS];  // row block, padded row layout, double buffered (2 x 43 KB)
-  uint2 rtw[kB * 256];         // per-row permuted inverse twiddles (64 KB)
-  uint2 ctw[256];              // column-pass inverse twiddles
-  uint32_t col[256 * kB];      // column-pass exchange (32 KB)
+  uint32_t rows[kB * kRS];  // row block, padded row layout (43 KB)
+  uint2 ctw[256];           // column-pass inverse twiddles
+  uint32_t col[256 * kB];   // column-pass exchange (32 KB)
 };
 
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 2)
     k_inv_cluster(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src, uint64_t src_bs,
                   uint32_t* __restrict__ dst, uint64_t dst_bs, int batch, int njobs, const PrimeDev* __restrict__ primes,
                   const uint2* __restrict__ inv_tw, const uint2* __restrict__ tw2i, const ExitConst* __restrict__ exits) {
@@ -226,33 +211,21 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
   const int cid = blockIdx.x / kCl, ncl = gridDim.x / kCl;
   const int tid = threadIdx.x;
   const int items = njobs * batch;
-  auto prefetch = [&](int it, int buf) {
-    const RowJob J = jobs[it / batch];
-    const uint32_t* g = src + (it % batch) * src_bs + (size_t)J.src_off * kN + (size_t)kB * k * kR;
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {  // 32 rows x 64 chunks of 16 B
-      const int e = tid + m * kT, r = e >> 6, c = (e & 63) * 4;
-      cp16(&S.rows[buf][r * kRS + rp(c)], g + r * kR + c);
-    }
-  };
-  int it = cid;
-  if (it < items) prefetch(it, 0);
-  cp_commit();
-  int cur_job = -1;
-  for (int i = 0; it < items; ++i, it += ncl) {
-    const int buf = i & 1, job = it / batch, b = it % batch;
+  for (int it = cid; it < items; it += ncl) {
+    const int job = it / batch, b = it % batch;
     const RowJob J = jobs[job];
-    if (job != cur_job) {
-      __syncthreads();
-      const uint2* T = tw2i + ((size_t)J.prime * kR + kB * k) * kR;
+    {
+      const uint32_t* g = src + b * src_bs + (size_t)J.src_off * kN + (size_t)kB * k * kR;
 #pragma unroll
-      for (int m = 0; m < 16; ++m) cp16(&S.rtw[2 * (tid + m * kT)], &T[2 * (tid + m * kT)]);
+      for (int m = 0; m < 8; ++m) {  // 32 rows x 64 chunks of 16 B
+        const int e = tid + m * kT, r = e >> 6, c = (e & 63) * 4;
+        cp16(&S.rows[r * kRS + rp(c)], g + r * kR + c);
+      }
       if (tid < 128) cp16(&S.ctw[2 * tid], &inv_tw[(size_t)J.prime * kN + 2 * tid]);
       cp_commit();
-      cur_job = job;
+      cp_wait_all();
+      __syncthreads();
     }
-    cp_wait_all();
-    __syncthreads();
     const PrimeDev P = primes[J.prime];
     const uint32_t q = P.q, q2 = P.q2;
     // ---- pass A: rows 32k .. 32k+31 (inverse stages 0..7), results stay in smem
@@ -261,8 +234,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
 #pragma unroll 1
       for (int round = 0; round < 2; ++round) {
         const int lr = 16 * round + rho;
-        uint32_t* line = S.rows[buf] + lr * kRS;
-        const uint2* W = S.rtw + lr * kR;
+        uint32_t* line = S.rows + lr * kRS;
+        const uint2* W = tw2i + ((size_t)J.prime * kR + kB * k + lr) * kR;
         uint32_t v[16];
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
@@ -278,7 +251,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
 #pragma unroll
           for (int p = 0; p < 8; ++p) {
             const int blk = p / d, j = blk * 2 * d + p % d;
-            const uint2 w = W[(off + blk) * 16 + tau];
+            const uint2 w = __ldg(&W[(off + blk) * 16 + tau]);
             gs(v[j], v[j + d], w.x, w.y, q, q2);
           }
         }
@@ -295,7 +268,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
 #pragma unroll
           for (int p = 0; p < 8; ++p) {
             const int blk = p / d, j = blk * 2 * d + p % d;
-            const uint2 w = W[240 + off + blk];
+            const uint2 w = __ldg(&W[240 + off + blk]);
             gs(v[j], v[j + d], w.x, w.y, q, q2);
           }
         }
@@ -305,15 +278,13 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
       }
     }
     cluster.sync();
-    if (it + ncl < items) prefetch(it + ncl, buf ^ 1);
-    cp_commit();
     // ---- pass B: columns 32k + 2cp, +1 (inverse stages 8..15 + exit)
     {
       const int tau = tid >> 4, cp = tid & 15;
       const ExitConst ex = exits[J.epi];
       const int c = kB * k + 2 * cp;
-      // rows 16 tau + j live in CTA (16 tau + j) >> 5 = tau >> 1, local row 16 (tau & 1) + j
-      const uint32_t* pr = cluster.map_shared_rank(S.rows[buf], tau >> 1) + (16 * (tau & 1)) * kRS + rp(c);
+      // rows 16 tau + j live in CTA tau >> 1 at local row 16 (tau & 1) + j
+      const uint32_t* pr = cluster.map_shared_rank(S.rows, tau >> 1) + (16 * (tau & 1)) * kRS + rp(c);
       uint2 v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = *reinterpret_cast<const uint2*>(pr + j * kRS);
@@ -351,11 +322,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1)
       uint32_t* o = dst + b * dst_bs + (size_t)J.dst_off * kN + c;
 #pragma unroll
       for (int j = 0; j < 16; ++j) *reinterpret_cast<uint2*>(o + (tau + 16 * j) * kR) = v[j];
-      __syncthreads();  // S.col is rewritten by the next item
     }
+    cluster.sync();  // peers are done reading this row block; S.col free
   }
-  cp_wait_all();
-  cluster.sync();
 }
 
 int g_fwd_clusters = 0, g_inv_clusters = 0;
@@ -411,5 +380,7 @@ void ntt_cluster_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st)
   k_inv_cluster<<<ncl * kCl, kT, sizeof(InvSmem), st>>>(a.jobs, a.src, a.src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
                                                          a.primes, a.tw, tw2i, a.exits);
 }
+
+int ntt_cluster_grid(bool inverse) { return inverse ? g_inv_clusters : g_fwd_clusters; }
 
 }  // namespace ck
