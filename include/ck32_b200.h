@@ -167,6 +167,51 @@ typedef struct {
 ck_status ck_profile(ck_context* ctx, int enable);
 ck_status ck_profile_read(ck_context* ctx, ck_prof_stat* out, uint32_t max_classes, uint32_t* count);
 
+/* ---- limb-sharded key switching (BASELINE config 4) -------------------------
+ * The reference runs one ciphertext on one host (key_switch, ckks.cpp:778-787;
+ * mod_up ckks.cpp:680-731; drop_and_divide ckks.cpp:611-655); these entry
+ * points split the same computation over `world` devices by RNS limb.  Rank s
+ * owns Q primes [q_lo, q_hi) and P primes L + [p_lo, p_hi) (balanced blocks).
+ * A shard-local polynomial at level l holds the owned Q rows below l (in
+ * order), then — when it carries them — the owned P rows.  A shard-local key
+ * is D x 2 x ((q_hi-q_lo) + (p_hi-p_lo)) rows: owned Q rows of every level,
+ * then owned P rows.  Every *_begin leaves INTT'd source rows in `send`; the
+ * host all-gathers the send buffers of all ranks (rank-major, equal sizes) and
+ * passes the result as `recv` to the matching second phase:
+ *   ModUp:   send [q_max][n]            recv [world][q_max][n]
+ *   switch:  send [2][s_max][n]         recv [world][2][s_max][n]
+ *            s_max = p_max (kind 0), 2 (kind 1), p_max + 2 (kind 2)
+ * Outputs are bit-identical to the single-device mechanisms restricted to the
+ * owned rows. */
+typedef struct ck_shard ck_shard;
+ck_status ck_shard_create(ck_context* ctx, uint32_t world, uint32_t rank, ck_shard** out);
+ck_status ck_shard_destroy(ck_shard* sh);
+/* out = {q_lo, q_hi, p_lo, p_hi, owned Q rows below level, q_max, p_max, world} */
+ck_status ck_shard_layout(const ck_shard* sh, uint32_t level, uint32_t out[8]);
+/* ModUp phase 1 (ckks.cpp:690-697): INTT + part 1 of the owned rows of d. */
+ck_status ck_shard_modup_begin(ck_shard* sh, uint32_t level, const uint32_t* d, uint32_t* send, ck_stream stream);
+/* ModUp phase 2 + KeyMult (ckks.cpp:698-770): BConv of every digit to the owned
+ * rows, NTT, multiply-accumulate with the shard-local key; optional fold
+ * v += P * (d0, d1) on the owned Q rows (fold = [2][owned Q rows], ckks.cpp:831-842).
+ * v = [2][owned Q rows + owned P rows]. */
+ck_status ck_shard_modup_keymult(ck_shard* sh, uint32_t level, const uint32_t* recv, const uint32_t* d,
+                                 const uint32_t* evk, const uint32_t* fold, uint32_t* v, ck_stream stream);
+/* drop_and_divide phase 1: INTT + part 1 of the owned source rows of v (two
+ * polynomials).  kind 0 = mod_down (v carries P rows), 1 = rescale (v is a
+ * shard-local ciphertext), 2 = merged ModDown + rescale (ckks.cpp:206-258). */
+ck_status ck_shard_switch_begin(ck_shard* sh, int kind, uint32_t level, const uint32_t* v, uint32_t* send,
+                                ck_stream stream);
+/* drop_and_divide phase 2: BConv to the owned output rows, NTT, combine
+ * (v - conv) * divisor^-1; then out_c += addend_c for bit c of add_mask (addend
+ * [2][owned output rows]); then, if rotate, the automorphism of rotation r on
+ * both polynomials (hrot tail, ckks.cpp:875-882). out = [2][owned output rows]. */
+ck_status ck_shard_switch_end(ck_shard* sh, int kind, uint32_t level, const uint32_t* recv, const uint32_t* v,
+                              const uint32_t* addend, uint32_t add_mask, int32_t rotate, int64_t r, uint32_t* out,
+                              ck_stream stream);
+/* hmult tensor (ckks.cpp:818-821) on the owned rows: d01 [2][lq], d2 [lq]. */
+ck_status ck_shard_tensor(ck_shard* sh, uint32_t level, const uint32_t* x, const uint32_t* y, uint32_t* d01,
+                          uint32_t* d2, ck_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

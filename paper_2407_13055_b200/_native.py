@@ -70,6 +70,14 @@ _SIGS = {
     "ck_hoisted_rotations": [_vp, _u32, _vp, _u32, ctypes.POINTER(_i64), ctypes.POINTER(_vp), _vp, _vp],
     "ck_hoisted_rotate_accumulate": [_vp, _u32, _vp, _u32, ctypes.POINTER(_i64), ctypes.POINTER(_vp),
                                      ctypes.POINTER(_vp), _vp, _vp],
+    "ck_shard_create": [_vp, _u32, _u32, ctypes.POINTER(_vp)],
+    "ck_shard_destroy": [_vp],
+    "ck_shard_layout": [_vp, _u32, _u32p],
+    "ck_shard_modup_begin": [_vp, _u32, _vp, _vp, _vp],
+    "ck_shard_modup_keymult": [_vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "ck_shard_switch_begin": [_vp, ctypes.c_int, _u32, _vp, _vp, _vp],
+    "ck_shard_switch_end": [_vp, ctypes.c_int, _u32, _vp, _vp, _vp, _u32, ctypes.c_int32, _i64, _vp, _vp],
+    "ck_shard_tensor": [_vp, _u32, _vp, _vp, _vp, _vp, _vp],
 }
 EXPORTS = sorted(list(_SIGS) + ["ck_last_error", "ck_version", "ck_launch_count"])
 

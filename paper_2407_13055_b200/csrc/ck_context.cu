@@ -876,6 +876,336 @@ struct Context {
   }
 };
 
+// ========================================================= limb sharding ==
+// One shard of a limb-sharded ciphertext:
+// rank s of G owns Q primes [qlo, qhi) and P primes L + [plo, phi) (balanced
+// contiguous blocks). Shard-local polynomials hold the owned rows only: the
+// owned Q rows below the level, then (when the polynomial carries them) the
+// owned P rows. NTT/INTT, KeyMult, the fold, the combine and the automorphism
+// are row-local; the only exchange is before each BConv, where every shard
+// needs all source rows (the digit rows in ModUp, the dropped rows in
+// ModDown / rescale): the host all-gathers the INTT'd source rows that
+// `modup_begin` / `switch_begin` leave in a send buffer.
+struct Shard {
+  Context* c = nullptr;
+  uint32_t G = 1, s = 0, qlo = 0, qhi = 0, plo = 0, phi = 0, qmax = 0, pmax = 0;
+
+  static uint32_t block_lo(uint32_t t, uint32_t total, uint32_t G) { return (uint32_t)((uint64_t)t * total / G); }
+  uint32_t q_lo(uint32_t t) const { return block_lo(t, c->L, G); }
+  uint32_t q_hi(uint32_t t) const { return block_lo(t + 1, c->L, G); }
+  uint32_t p_lo(uint32_t t) const { return block_lo(t, c->alpha, G); }
+  uint32_t p_hi(uint32_t t) const { return block_lo(t + 1, c->alpha, G); }
+  // owned Q rows of rank t below `level`
+  uint32_t lq_of(uint32_t t, uint32_t level) const {
+    const uint32_t lo = q_lo(t), hi = std::min(q_hi(t), level);
+    return hi > lo ? hi - lo : 0;
+  }
+  uint32_t lq(uint32_t level) const { return lq_of(s, level); }
+  uint32_t lp() const { return phi - plo; }
+  bool owns_t(uint32_t t, uint32_t g) const {
+    return g < c->L ? (g >= q_lo(t) && g < q_hi(t)) : (g - c->L >= p_lo(t) && g - c->L < p_hi(t));
+  }
+  // row of global prime g in a shard-local polynomial at `level` (Q rows then P rows)
+  uint32_t local_row(uint32_t level, uint32_t g) const { return g < c->L ? g - qlo : lq(level) + (g - c->L - plo); }
+  uint32_t smax(int kind) const { return kind == 0 ? pmax : kind == 1 ? 2 : pmax + 2; }
+
+  struct UpPlan {
+    NttPlan intt, ntt;
+    BconvPlan bc;
+    Blob maps;
+    size_t digit_off = 0, prime_off = 0, erow_off = 0;
+    uint32_t lq = 0, rows = 0, D = 0, ntt_rows = 0;
+  };
+  struct DownPlan {
+    NttPlan intt, ntt;
+    BconvPlan bc;
+    Blob consts;  // dinv [lqo]
+    uint32_t sc = 0, smax = 0, vrows = 0, lqo = 0, out_q = 0, own_sc = 0;
+    std::vector<uint32_t> rank_cnt;  // own sources per rank (gathered order = rank order)
+  };
+  std::map<uint32_t, std::unique_ptr<UpPlan>> up;
+  std::map<std::pair<int, uint32_t>, std::unique_ptr<DownPlan>> down;
+
+  const UpPlan& up_plan(uint32_t level) {
+    auto it = up.find(level);
+    if (it != up.end()) return *it->second;
+    auto pl = std::make_unique<UpPlan>();
+    const uint32_t alpha = c->alpha, L = c->L;
+    pl->lq = lq(level);
+    pl->rows = pl->lq + lp();
+    pl->D = c->digits(level);
+    auto gl = [&](uint32_t r) { return r < pl->lq ? qlo + r : L + plo + (r - pl->lq); };
+    std::vector<RowJob> ijobs, njobs;
+    std::vector<ExitConst> exits;
+    for (uint32_t r = 0; r < pl->lq; ++r) {  // INTT + part 1 of the owned digit rows (ckks.cpp:690-697)
+      const uint32_t g = qlo + r, k = g / alpha;
+      std::vector<uint32_t> sg, cm, part1;
+      for (uint32_t j = k * alpha; j < std::min((k + 1) * alpha, level); ++j) sg.push_back(j);
+      c->bconv_consts(sg, {}, cm, part1);
+      ijobs.push_back({r, r, (uint16_t)g, (uint16_t)exits.size()});
+      exits.push_back(c->exit_const(g, part1[g - k * alpha]));
+    }
+    std::vector<BconvGroup> groups;
+    std::vector<uint32_t> cmat, drow;
+    std::vector<uint16_t> dprime;
+    int max_sc = 1;
+    for (uint32_t k = 0; k < pl->D; ++k) {  // per digit: BConv to the owned rows outside the digit
+      const uint32_t b = k * alpha, e = std::min((k + 1) * alpha, level);
+      std::vector<uint32_t> sg, dg, part1;
+      for (uint32_t j = b; j < e; ++j) sg.push_back(j);
+      std::vector<uint32_t> rr;
+      for (uint32_t r = 0; r < pl->rows; ++r) {
+        const uint32_t g = gl(r);
+        if (g < b || g >= e) {
+          dg.push_back(g);
+          rr.push_back(r);
+        }
+      }
+      if (dg.empty()) continue;
+      c->check_bconv_width(sg);
+      BconvGroup G0;
+      G0.src_off = b;
+      G0.sc = (uint32_t)sg.size();
+      G0.dc = (uint32_t)dg.size();
+      G0.cmat_off = (uint32_t)cmat.size();
+      G0.map_off = (uint32_t)drow.size();
+      c->bconv_consts(sg, dg, cmat, part1);
+      max_sc = std::max<int>(max_sc, (int)sg.size());
+      for (size_t i = 0; i < dg.size(); ++i) {
+        drow.push_back(k * pl->rows + rr[i]);
+        dprime.push_back((uint16_t)dg[i]);
+        njobs.push_back({k * pl->rows + rr[i], k * pl->rows + rr[i], (uint16_t)dg[i], 0});
+      }
+      groups.push_back(G0);
+    }
+    pl->intt.jobs_off = pl->intt.blob.add(ijobs);
+    pl->intt.exits_off = pl->intt.blob.add(exits);
+    pl->intt.njobs = (int)ijobs.size();
+    pl->intt.blob.upload();
+    pl->ntt.jobs_off = pl->ntt.blob.add(njobs);
+    pl->ntt.njobs = (int)njobs.size();
+    pl->ntt.blob.upload();
+    pl->ntt_rows = (uint32_t)njobs.size();
+    pl->bc.groups_off = pl->bc.blob.add(groups);
+    pl->bc.cmat_off = pl->bc.blob.add(cmat);
+    pl->bc.row_off = pl->bc.blob.add(drow);
+    pl->bc.prime_off = pl->bc.blob.add(dprime);
+    pl->bc.ngroups = (int)groups.size();
+    pl->bc.max_sc = max_sc;
+    pl->bc.src_rows = (uint64_t)alpha * groups.size();
+    pl->bc.dst_rows = drow.size();
+    pl->bc.blob.upload();
+    std::vector<int16_t> digit(pl->rows);
+    std::vector<uint16_t> prime(pl->rows), erow(pl->rows);
+    for (uint32_t r = 0; r < pl->rows; ++r) {
+      const uint32_t g = gl(r);
+      prime[r] = (uint16_t)g;
+      digit[r] = r < pl->lq ? (int16_t)(g / alpha) : (int16_t)-1;
+      erow[r] = (uint16_t)(r < pl->lq ? r : (qhi - qlo) + (r - pl->lq));  // key rows: owned Q (all levels), owned P
+    }
+    pl->digit_off = pl->maps.add(digit);
+    pl->prime_off = pl->maps.add(prime);
+    pl->erow_off = pl->maps.add(erow);
+    pl->maps.upload();
+    auto& ref = *pl;
+    up[level] = std::move(pl);
+    return ref;
+  }
+
+  // kind 0 ModDown (sources P, out level), 1 rescale (sources 2 tail Q rows,
+  // out level-2), 2 merged (tail Q rows + P, out level-2)  (ckks.cpp:206-258)
+  const DownPlan& down_plan(int kind, uint32_t level) {
+    auto key = std::make_pair(kind, level);
+    auto it = down.find(key);
+    if (it != down.end()) return *it->second;
+    auto pl = std::make_unique<DownPlan>();
+    const uint32_t L = c->L, alpha = c->alpha;
+    std::vector<uint32_t> sg;
+    pl->out_q = level;
+    if (kind == 0) {
+      for (uint32_t j = 0; j < alpha; ++j) sg.push_back(L + j);
+    } else {
+      if (level < 4) throw InvalidArgument("level exhausted");
+      pl->out_q = level - 2;
+      sg = {level - 2, level - 1};
+      if (kind == 2)
+        for (uint32_t j = 0; j < alpha; ++j) sg.push_back(L + j);
+    }
+    c->check_bconv_width(sg);
+    pl->sc = (uint32_t)sg.size();
+    pl->smax = smax(kind);
+    pl->vrows = kind == 1 ? lq(level) : lq(level) + lp();
+    pl->lqo = lq(pl->out_q);
+    std::vector<uint32_t> cm0, part1;  // part 1 depends on the source set only
+    c->bconv_consts(sg, {}, cm0, part1);
+    std::map<uint32_t, uint32_t> p1;
+    for (size_t j = 0; j < sg.size(); ++j) p1[sg[j]] = part1[j];
+    std::vector<uint32_t> gathered;  // source order after the all-gather: rank order, then sg order
+    for (uint32_t t = 0; t < G; ++t) {
+      uint32_t cnt = 0;
+      for (uint32_t g : sg)
+        if (owns_t(t, g)) {
+          gathered.push_back(g);
+          ++cnt;
+        }
+      pl->rank_cnt.push_back(cnt);
+    }
+    std::vector<RowJob> ijobs, njobs;
+    std::vector<ExitConst> exits;
+    std::vector<uint32_t> own;
+    for (uint32_t g : sg)
+      if (owns_t(s, g)) own.push_back(g);
+    pl->own_sc = (uint32_t)own.size();
+    for (uint32_t u = 0; u < own.size(); ++u) exits.push_back(c->exit_const(own[u], p1[own[u]]));
+    for (uint32_t p = 0; p < 2; ++p)
+      for (uint32_t u = 0; u < own.size(); ++u)
+        ijobs.push_back({p * pl->vrows + local_row(level, own[u]), p * pl->smax + u, (uint16_t)own[u], (uint16_t)u});
+    std::vector<uint32_t> dg;
+    for (uint32_t r = 0; r < pl->lqo; ++r) dg.push_back(qlo + r);
+    std::vector<uint32_t> cmat, part1g;
+    if (!dg.empty()) c->bconv_consts(gathered, dg, cmat, part1g);
+    std::vector<BconvGroup> groups;
+    std::vector<uint32_t> drow;
+    std::vector<uint16_t> dprime;
+    for (uint32_t p = 0; p < 2 && !dg.empty(); ++p) {
+      BconvGroup G0;
+      G0.src_off = p * pl->sc;
+      G0.sc = pl->sc;
+      G0.dc = pl->lqo;
+      G0.cmat_off = 0;
+      G0.map_off = (uint32_t)drow.size();
+      groups.push_back(G0);
+      for (uint32_t r = 0; r < pl->lqo; ++r) {
+        drow.push_back(p * pl->lqo + r);
+        dprime.push_back((uint16_t)(qlo + r));
+        njobs.push_back({p * pl->lqo + r, p * pl->lqo + r, (uint16_t)(qlo + r), 0});
+      }
+    }
+    pl->intt.jobs_off = pl->intt.blob.add(ijobs);
+    pl->intt.exits_off = pl->intt.blob.add(exits);
+    pl->intt.njobs = (int)ijobs.size();
+    pl->intt.blob.upload();
+    pl->ntt.jobs_off = pl->ntt.blob.add(njobs);
+    pl->ntt.njobs = (int)njobs.size();
+    pl->ntt.blob.upload();
+    pl->bc.groups_off = pl->bc.blob.add(groups);
+    pl->bc.cmat_off = pl->bc.blob.add(cmat);
+    pl->bc.row_off = pl->bc.blob.add(drow);
+    pl->bc.prime_off = pl->bc.blob.add(dprime);
+    pl->bc.ngroups = (int)groups.size();
+    pl->bc.max_sc = (int)pl->sc;
+    pl->bc.src_rows = 2ull * pl->sc;
+    pl->bc.dst_rows = 2ull * pl->lqo;
+    pl->bc.blob.upload();
+    std::vector<uint32_t> dinv(std::max<uint32_t>(pl->lqo, 1), 0);
+    for (uint32_t r = 0; r < pl->lqo; ++r) {
+      const uint32_t qq = c->q(qlo + r);
+      uint32_t d = 1 % qq;
+      for (uint32_t g : sg) d = mulm(d, c->q(g) % qq, qq);
+      dinv[r] = to_mont(invm(d, qq), qq);
+    }
+    pl->consts.add(dinv);
+    pl->consts.upload();
+    auto& ref = *pl;
+    down[key] = std::move(pl);
+    return ref;
+  }
+
+  // ---- phases ----
+  void modup_begin(uint32_t level, const uint32_t* d, uint32_t* send, cudaStream_t st) {
+    const UpPlan& pl = up_plan(level);
+    c->run_ntt(pl.intt, true, 1, d, 0, send, 0, 0, st);
+    c->counters[3] += pl.lq;
+  }
+  void modup_keymult(uint32_t level, const uint32_t* recv, const uint32_t* d, const uint32_t* evk,
+                     const uint32_t* fold, uint32_t* v, cudaStream_t st) {
+    const UpPlan& pl = up_plan(level);
+    const uint64_t N = c->n;
+    uint32_t* compact = static_cast<uint32_t*>(c->scratch_get(((size_t)level + (size_t)pl.D * pl.rows) * N * 4, st));
+    uint32_t* ext = compact + (size_t)level * N;
+    for (uint32_t t = 0; t < G; ++t) {  // gathered blocks -> global row order
+      const uint32_t cnt = lq_of(t, level);
+      if (cnt)
+        CK_CUDA(cudaMemcpyAsync(compact + (size_t)q_lo(t) * N, recv + (size_t)t * qmax * N, (size_t)cnt * N * 4,
+                                cudaMemcpyDeviceToDevice, st));
+    }
+    if (pl.bc.ngroups) {
+      c->run_bconv(pl.bc, 1, compact, 0, ext, 0, st);
+      c->run_ntt(pl.ntt, false, 1, ext, 0, ext, 0, 1, st);
+    }
+    ShardKeyMultLaunch a;
+    a.rows = (int)pl.rows;
+    a.lq = (int)pl.lq;
+    a.D = (int)pl.D;
+    a.erows = (int)((qhi - qlo) + lp());
+    a.ext = ext;
+    a.d = d;
+    a.evk = evk;
+    a.fold = fold;
+    a.digit = pl.maps.at<int16_t>(pl.digit_off);
+    a.prime = pl.maps.at<uint16_t>(pl.prime_off);
+    a.erow = pl.maps.at<uint16_t>(pl.erow_off);
+    a.p_mont = c->d_pmont;
+    a.v = v;
+    a.primes = c->d_primes;
+    {
+      Context::ProfScope ps(c, 3, 4.0 * N * pl.rows * (3.0 * pl.D + 2), 1, st);
+      shard_key_mult((int)N, a, st);
+    }
+    c->launches += 1;
+    c->counters[0] += 1;
+    c->counters[5] += pl.D;
+    c->counters[2] += pl.ntt_rows;
+    c->counters[4] += pl.D;
+  }
+  void switch_begin(int kind, uint32_t level, const uint32_t* v, uint32_t* send, cudaStream_t st) {
+    const DownPlan& pl = down_plan(kind, level);
+    c->run_ntt(pl.intt, true, 1, v, 0, send, 0, 0, st);
+    c->counters[3] += 2ull * pl.own_sc;
+  }
+  void switch_end(int kind, uint32_t level, const uint32_t* recv, const uint32_t* v, const uint32_t* add,
+                  uint32_t add_mask, const uint32_t* src_map, uint32_t* out, cudaStream_t st) {
+    const DownPlan& pl = down_plan(kind, level);
+    const uint64_t N = c->n;
+    uint32_t* compact = static_cast<uint32_t*>(c->scratch_get((2ull * pl.sc + 2ull * pl.lqo) * N * 4, st));
+    uint32_t* o = compact + 2ull * pl.sc * N;
+    uint32_t off = 0;
+    for (uint32_t t = 0; t < G; ++t) {  // [G][2][smax] -> [2][sc] in gathered order
+      const uint32_t cnt = pl.rank_cnt[t];
+      for (uint32_t p = 0; p < 2 && cnt; ++p)
+        CK_CUDA(cudaMemcpyAsync(compact + ((size_t)p * pl.sc + off) * N,
+                                recv + ((size_t)t * 2 * pl.smax + (size_t)p * pl.smax) * N, (size_t)cnt * N * 4,
+                                cudaMemcpyDeviceToDevice, st));
+      off += cnt;
+    }
+    if (pl.lqo) {
+      c->run_bconv(pl.bc, 1, compact, 0, o, 0, st);
+      c->run_ntt(pl.ntt, false, 1, o, 0, o, 0, 1, st);
+      ShardTailLaunch a;
+      a.v = v;
+      a.v_ps = (uint64_t)pl.vrows * N;
+      a.o = o;
+      a.o_ps = (uint64_t)pl.lqo * N;
+      a.dinv = pl.consts.at<uint32_t>(0);
+      a.prime_base = (int)qlo;
+      a.add = add;
+      a.add_ps = (uint64_t)pl.lqo * N;
+      a.add_mask = add_mask;
+      a.src_map = src_map;
+      a.out = out;
+      a.out_ps = (uint64_t)pl.lqo * N;
+      a.primes = c->d_primes;
+      {
+        Context::ProfScope ps(c, 5, 4.0 * N * pl.lqo * (add ? 7 : 6), 1, st);
+        shard_tail((int)N, (int)pl.lqo, a, st);
+      }
+      c->launches += 1;
+    }
+    c->counters[5] += 2;
+    c->counters[2] += 2ull * pl.lqo;
+  }
+};
+
 namespace {
 
 void check_launch() {
@@ -1599,6 +1929,132 @@ ck_status ck_hoisted_rotate_accumulate(ck_context* ctx, uint32_t level, const ui
       ++c->launches;
       c->counters[1] += 1;
     }
+    check_launch();
+  });
+}
+
+/* ---- limb sharding ------------------------------------------------------ */
+static Shard* SH(ck_shard* s) {
+  if (!s) throw InvalidArgument("null shard");
+  return reinterpret_cast<Shard*>(s);
+}
+static void check_kind(int kind) {
+  if (kind < 0 || kind > 2) throw InvalidArgument("switch kind must be 0 (mod_down), 1 (rescale) or 2 (merged)");
+}
+
+ck_status ck_shard_create(ck_context* ctx, uint32_t world, uint32_t rank, ck_shard** out) {
+  return guard([&] {
+    Context* c = C(ctx);
+    if (!out) throw InvalidArgument("null argument");
+    if (world == 0 || rank >= world) throw InvalidArgument("rank out of range");
+    if (world > c->L) throw InvalidArgument("more shards than Q primes");
+    auto s = std::make_unique<Shard>();
+    s->c = c;
+    s->G = world;
+    s->s = rank;
+    s->qlo = s->q_lo(rank);
+    s->qhi = s->q_hi(rank);
+    s->plo = s->p_lo(rank);
+    s->phi = s->p_hi(rank);
+    for (uint32_t t = 0; t < world; ++t) {
+      s->qmax = std::max(s->qmax, s->q_hi(t) - s->q_lo(t));
+      s->pmax = std::max(s->pmax, s->p_hi(t) - s->p_lo(t));
+    }
+    *out = reinterpret_cast<ck_shard*>(s.release());
+  });
+}
+ck_status ck_shard_destroy(ck_shard* sh) {
+  return guard([&] { delete SH(sh); });
+}
+ck_status ck_shard_layout(const ck_shard* sh, uint32_t level, uint32_t out[8]) {
+  return guard([&] {
+    const Shard* s = reinterpret_cast<const Shard*>(sh);
+    if (!s || !out) throw InvalidArgument("null argument");
+    check_level(s->c, level);
+    out[0] = s->qlo;
+    out[1] = s->qhi;
+    out[2] = s->plo;
+    out[3] = s->phi;
+    out[4] = s->lq(level);
+    out[5] = s->qmax;
+    out[6] = s->pmax;
+    out[7] = s->G;
+  });
+}
+ck_status ck_shard_modup_begin(ck_shard* sh, uint32_t level, const uint32_t* d, uint32_t* send, ck_stream stream) {
+  return guard([&] {
+    Shard* s = SH(sh);
+    check_level(s->c, level);
+    if (s->lq(level)) {
+      check_ptr(d);
+      check_ptr(send);
+    }
+    s->modup_begin(level, d, send, S(stream));
+    check_launch();
+  });
+}
+ck_status ck_shard_modup_keymult(ck_shard* sh, uint32_t level, const uint32_t* recv, const uint32_t* d,
+                                 const uint32_t* evk, const uint32_t* fold, uint32_t* v, ck_stream stream) {
+  return guard([&] {
+    Shard* s = SH(sh);
+    check_level(s->c, level);
+    check_ptr(recv);
+    check_ptr(evk);
+    if (s->up_plan(level).rows == 0) return;  // nothing owned at this level
+    check_ptr(v);
+    if (s->lq(level)) check_ptr(d);
+    s->modup_keymult(level, recv, d, evk, fold, v, S(stream));
+    check_launch();
+  });
+}
+ck_status ck_shard_switch_begin(ck_shard* sh, int kind, uint32_t level, const uint32_t* v, uint32_t* send,
+                                ck_stream stream) {
+  return guard([&] {
+    Shard* s = SH(sh);
+    check_kind(kind);
+    check_level(s->c, level, kind == 0 ? 1 : 4);
+    check_ptr(send);
+    if (s->down_plan(kind, level).own_sc) check_ptr(v);
+    s->switch_begin(kind, level, v, send, S(stream));
+    check_launch();
+  });
+}
+ck_status ck_shard_switch_end(ck_shard* sh, int kind, uint32_t level, const uint32_t* recv, const uint32_t* v,
+                              const uint32_t* addend, uint32_t add_mask, int32_t rotate, int64_t r, uint32_t* out,
+                              ck_stream stream) {
+  return guard([&] {
+    Shard* s = SH(sh);
+    check_kind(kind);
+    check_level(s->c, level, kind == 0 ? 1 : 4);
+    check_ptr(recv);
+    const uint32_t lqo = s->down_plan(kind, level).lqo;
+    if (lqo) {
+      check_ptr(v);
+      check_ptr(out);
+    }
+    const uint32_t* map = rotate && lqo ? s->c->rotation_map(r) : nullptr;
+    s->switch_end(kind, level, recv, v, addend, add_mask, map, out, S(stream));
+    check_launch();
+  });
+}
+ck_status ck_shard_tensor(ck_shard* sh, uint32_t level, const uint32_t* x, const uint32_t* y, uint32_t* d01,
+                          uint32_t* d2, ck_stream stream) {
+  return guard([&] {
+    Shard* s = SH(sh);
+    check_level(s->c, level, 4);
+    const uint32_t lq = s->lq(level);
+    if (!lq) return;
+    check_ptr(x);
+    check_ptr(y);
+    check_ptr(d01);
+    check_ptr(d2);
+    const uint64_t N = s->c->n;
+    cudaStream_t st = S(stream);
+    {
+      Context::ProfScope ps(s->c, 4, 4.0 * N * lq * 7, 1, st);
+      tensor((int)N, (int)lq, 1, x, y, 2ull * lq * N, d01, 2ull * lq * N, d2, lq * N, s->c->d_primes + s->qlo, st);
+    }
+    ++s->c->launches;
     check_launch();
   });
 }

@@ -134,4 +134,37 @@ void addmul_permuted(int n, int rows, int batch, uint32_t* acc, uint64_t acc_bs,
                      const uint32_t* y, uint64_t y_bs, const uint32_t* src_map, const uint16_t* row_prime,
                      const PrimeDev* primes, cudaStream_t st);
 
+// Limb-sharded key switching (shard.cu): KeyMult over a shard's rows (any
+// subset of Q_l + P) with per-row maps, and the drop-and-divide tail.
+struct ShardKeyMultLaunch {
+  int rows = 0, lq = 0, D = 0, erows = 0;
+  const uint32_t* ext = nullptr;   // [D][rows][n]
+  const uint32_t* d = nullptr;     // [lq][n] ModUp input (pass-through rows)
+  const uint32_t* evk = nullptr;   // [D][2][erows][n] shard-local key rows
+  const uint32_t* fold = nullptr;  // [2][lq][n] or null
+  const int16_t* digit = nullptr;  // [rows] digit of the row (-1 for P rows)
+  const uint16_t* prime = nullptr; // [rows] global prime index
+  const uint16_t* erow = nullptr;  // [rows] row in the shard-local key
+  const uint32_t* p_mont = nullptr;
+  uint32_t* v = nullptr;           // [2][rows][n]
+  const PrimeDev* primes = nullptr;
+};
+void shard_key_mult(int n, const ShardKeyMultLaunch& a, cudaStream_t st);
+struct ShardTailLaunch {
+  const uint32_t* v = nullptr;  // poly stride v_ps, rows [0, rows) are the output rows
+  uint64_t v_ps = 0;
+  const uint32_t* o = nullptr;  // converted rows, poly stride o_ps
+  uint64_t o_ps = 0;
+  const uint32_t* dinv = nullptr;  // [rows] divisor^-1 (Montgomery)
+  int prime_base = 0;              // global prime of row 0
+  const uint32_t* add = nullptr;   // optional addend, poly stride add_ps
+  uint64_t add_ps = 0;
+  uint32_t add_mask = 0;           // bit c: add to poly c
+  const uint32_t* src_map = nullptr;  // optional automorphism gather
+  uint32_t* out = nullptr;
+  uint64_t out_ps = 0;
+  const PrimeDev* primes = nullptr;
+};
+void shard_tail(int n, int rows, const ShardTailLaunch& a, cudaStream_t st);
+
 }  // namespace ck

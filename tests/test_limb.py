@@ -1,0 +1,250 @@
+"""Limb-sharded key switching (BASELINE config 4).
+
+CPU tests drive ``limb.LimbShardedEvaluator`` with the oracle-backed shard
+(tests/shard_oracle.py, test infrastructure) — in one process (virtual
+shards) and over gloo with world size 2 — and compare the reassembled
+ciphertexts with the oracle's single-host mechanisms.  GPU tests drive the
+native ``ck_shard_*`` path with virtual shards on one B200 and compare with
+the single-device mechanisms (themselves pinned to the reference) and with
+the reference's full-size hashes at N=2^17 (config 4)."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2407_13055_b200.limb import LimbShardedEvaluator, LocalExchange, ShardLayout, TorchExchange
+
+N, L, A, DB = 256, 6, 2, 55
+
+
+def _canon(O, a, level):
+    return O.canonical(a, O.gidx(level)).astype(np.int64)
+
+
+def _oracle():
+    from pyoracle import Oracle
+    return Oracle(N, L, A, DB)
+
+
+# ---------------------------------------------------------------- layout --
+@pytest.mark.parametrize("Lq,alpha", [(6, 2), (24, 8), (8, 3), (54, 14)])
+def test_layout_partition(Lq, alpha):
+    for world in range(1, 9):
+        if world > Lq:
+            continue
+        lays = [ShardLayout(Lq, alpha, world, r) for r in range(world)]
+        assert lays[0].q_lo == 0 and lays[-1].q_hi == Lq
+        assert lays[0].p_lo == 0 and lays[-1].p_hi == alpha
+        for a, b in zip(lays, lays[1:]):
+            assert a.q_hi == b.q_lo and a.p_hi == b.p_lo
+        sizes = [x.q_hi - x.q_lo for x in lays]
+        assert max(sizes) - min(sizes) <= 1 and max(sizes) == lays[0].q_max
+        for level in range(1, Lq + 1):
+            assert sum(x.lq(level) for x in lays) == level
+            rows = sum((x.q_rows(level) for x in lays), [])
+            assert rows == list(range(level))
+        full = torch.arange(2 * Lq * 4).reshape(2, Lq, 4)
+        assert torch.equal(lays[0].assemble_ct([x.split_ct(full, Lq) for x in lays], Lq), full)
+
+
+# ------------------------------------------- virtual shards, oracle backend --
+def _run_mechanisms(ev, lays, O, level, seed, lazy=False):
+    xb, xa, yb, ya, evk = O.synthetic(level, seed)
+    x = torch.from_numpy(np.stack([xb, xa]))
+    y = torch.from_numpy(np.stack([yb, ya]))
+    K = torch.from_numpy(evk)
+    xs = [lay.split_ct(x, level) for lay in lays]
+    ys = [lay.split_ct(y, level) for lay in lays]
+    ks = [lay.split_key(K) for lay in lays]
+    got = {}
+    got["hmult"] = torch.cat(ev.hmult(level, xs, ys, ks), dim=1).numpy()
+    got["hrot1"] = torch.cat(ev.hrot(level, xs, 1, ks), dim=1).numpy()
+    got["hrot-3"] = torch.cat(ev.hrot(level, xs, -3, ks), dim=1).numpy()
+    got["rescale"] = torch.cat(ev.rescale(level, xs), dim=1).numpy()
+    got["ks"] = torch.cat(ev.key_switch(level, [x_[1].contiguous() for x_ in xs], ks), dim=1).numpy()
+    want = {}
+    lo = level if lazy else level - 2
+    ob, oa = O.hmult(level, xb, xa, yb, ya, evk, lazy=lazy)
+    want["hmult"] = np.stack([_canon(O, ob, lo), _canon(O, oa, lo)])
+    for r in (1, -3):
+        ob, oa = O.hrot(level, xb, xa, r, evk)
+        want[f"hrot{r}"] = np.stack([_canon(O, ob, level), _canon(O, oa, level)])
+    ob, oa = O.rescale(level, xb, xa)
+    want["rescale"] = np.stack([_canon(O, ob, level - 2), _canon(O, oa, level - 2)])
+    c0, c1 = O.key_switch(level, xa, evk)
+    want["ks"] = np.stack([_canon(O, c0, level), _canon(O, c1, level)])
+    return got, want
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("lazy", [False, True])
+def test_virtual_shards_match_oracle(world, lazy):
+    from shard_oracle import OracleShard
+
+    O = _oracle()
+    shards = [OracleShard(O, world, r) for r in range(world)]
+    ev = LimbShardedEvaluator(shards, LocalExchange(), lazy_rescale=lazy)
+    for level, seed in ((L, 31), (4, 32)):
+        got, want = _run_mechanisms(ev, [s.layout for s in shards], O, level, seed, lazy)
+        for k in want:
+            np.testing.assert_array_equal(got[k], want[k], err_msg=f"{k} level {level} world {world}")
+
+
+# ------------------------------------------------------ gloo, world size 2 --
+def _gloo_worker(rank, world, port, q):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    for p in (os.path.dirname(here), os.path.join(os.path.dirname(here), "oracle"), here):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    from shard_oracle import OracleShard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        O = _oracle()
+        sh = OracleShard(O, world, rank)
+        ev = LimbShardedEvaluator([sh], TorchExchange())
+        level = L
+        xb, xa, yb, ya, evk = O.synthetic(level, 77)
+        x = torch.from_numpy(np.stack([xb, xa]))
+        y = torch.from_numpy(np.stack([yb, ya]))
+        lay = sh.layout
+        k = lay.split_key(torch.from_numpy(evk))
+        hm = ev.hmult(level, [lay.split_ct(x, level)], [lay.split_ct(y, level)], [k])[0]
+        hr = ev.hrot(level, [lay.split_ct(x, level)], 5, [k])[0]
+        q.put((rank, hm.numpy(), hr.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_matches_oracle():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    parts = dict()
+    for _ in range(2):
+        r, hm, hr = q.get(timeout=300)
+        parts[r] = (hm, hr)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    O = _oracle()
+    xb, xa, yb, ya, evk = O.synthetic(L, 77)
+    ob, oa = O.hmult(L, xb, xa, yb, ya, evk)
+    np.testing.assert_array_equal(np.concatenate([parts[0][0], parts[1][0]], axis=1),
+                                  np.stack([_canon(O, ob, L - 2), _canon(O, oa, L - 2)]))
+    ob, oa = O.hrot(L, xb, xa, 5, evk)
+    np.testing.assert_array_equal(np.concatenate([parts[0][1], parts[1][1]], axis=1),
+                                  np.stack([_canon(O, ob, L), _canon(O, oa, L)]))
+
+
+# ------------------------------------------------------------------- GPU --
+def _gpu_ctx(n, l, a, db, lazy=False):
+    from paper_2407_13055_b200 import ckks
+    return ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db, lazy_rescale=lazy))
+
+
+def _sharded_vs_single(C, O, world, level, seed, lazy=False, rots=(1,)):
+    from fractions import Fraction
+
+    from paper_2407_13055_b200 import ckks
+    from paper_2407_13055_b200.limb import ShardBackend
+
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(C.device)
+    xb, xa, yb, ya, evk = O.synthetic(level, seed)
+    x, y, K = dev(np.stack([xb, xa])), dev(np.stack([yb, ya])), dev(evk)
+    shards = [ShardBackend(C, world, r) for r in range(world)]
+    lays = [s.layout for s in shards]
+    ev = LimbShardedEvaluator(shards, LocalExchange(), lazy_rescale=lazy)
+    xs = [lay.split_ct(x, level) for lay in lays]
+    ys = [lay.split_ct(y, level) for lay in lays]
+    ks = [lay.split_key(K) for lay in lays]
+    X = ckks.Ciphertext(x, Fraction(1 << O.delta_bits), level)
+    Y = ckks.Ciphertext(y, Fraction(1 << O.delta_bits), level)
+    got = torch.cat(ev.hmult(level, xs, ys, ks), dim=1)
+    want = ckks.hmult(C, X, Y, ckks.EvaluationKey(K))
+    assert torch.equal(got, want.data), f"hmult world {world} level {level}"
+    for r in rots:
+        got = torch.cat(ev.hrot(level, xs, r, ks), dim=1)
+        want = ckks.hrot(C, X, r, ckks.EvaluationKey(K, ckks.ROTATION, r))
+        assert torch.equal(got, want.data), f"hrot {r} world {world} level {level}"
+    if level >= 4:
+        got = torch.cat(ev.rescale(level, xs), dim=1)
+        assert torch.equal(got, ckks.rescale(C, X).data), f"rescale world {world}"
+    got = torch.cat(ev.key_switch(level, [x_[1].contiguous() for x_ in xs], ks), dim=1)
+    c0, c1 = ckks.key_switch(C, ckks.Polynomial(x[1].contiguous(), level), ckks.EvaluationKey(K))
+    assert torch.equal(got, torch.stack([c0.data, c1.data])), f"key_switch world {world}"
+    for s in shards:
+        s.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_gpu_virtual_shards_small_vs_oracle_and_single(world):
+    from pyoracle import Oracle
+
+    n, l, a, db = 1024, 8, 3, 55
+    O = Oracle(n, l, a, db)
+    for lazy in (False, True):
+        C = _gpu_ctx(n, l, a, db, lazy)
+        for level, seed in ((8, 3), (5, 4)):
+            _sharded_vs_single(C, O, world, level, seed, lazy, rots=(1, -5))
+        C.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_gpu_virtual_shards_n65536(world):
+    from pyoracle import Oracle
+
+    n, l, a, db = 65536, 24, 8, 55
+    O = Oracle(n, l, a, db)
+    C = _gpu_ctx(n, l, a, db)
+    for level in (24, 13):
+        _sharded_vs_single(C, O, world, level, 40 + level)
+    C.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_gpu_config4_n131072_matches_reference_hash(world):
+    """BASELINE config 4: single-ciphertext limb-sharded HMult / HRot at
+    N=2^17, l=24, alpha=8 — reassembled output equals the reference's hash."""
+    from golden_util import FULL, sha
+    from pyoracle import Oracle
+
+    from paper_2407_13055_b200.limb import ShardBackend
+
+    cfg = FULL["configs"]["n131072_l24_a8_d55"]
+    n, l, a, db = cfg["n"], cfg["l"], cfg["alpha"], cfg["delta_bits"]
+    O = Oracle(n, l, a, db)
+    C = _gpu_ctx(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(24, FULL["seed"])
+    dev = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(C.device)
+    x, y, K = dev(np.stack([xb, xa])), dev(np.stack([yb, ya])), dev(evk)
+    shards = [ShardBackend(C, world, r) for r in range(world)]
+    ev = LimbShardedEvaluator(shards, LocalExchange())
+    lays = [s.layout for s in shards]
+    xs = [lay.split_ct(x, 24) for lay in lays]
+    ys = [lay.split_ct(y, 24) for lay in lays]
+    ks = [lay.split_key(K) for lay in lays]
+    hm = torch.cat(ev.hmult(24, xs, ys, ks), dim=1).cpu().numpy()
+    assert sha(hm) == cfg["ops"]["hmult@24@0"]
+    hr = torch.cat(ev.hrot(24, xs, 1, ks), dim=1).cpu().numpy()
+    assert sha(hr) == cfg["ops"]["hrot@24@1"]
+    for s in shards:
+        s.close()
+    C.close()
