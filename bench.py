@@ -46,6 +46,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also report the HRot level sweep (config 2)")
+    ap.add_argument("--workload", default="dp", choices=["dp", "limb"],
+                    help="dp: batched independent ciphertexts (configs 1-3, the headline); limb: one ciphertext "
+                         "limb-sharded over the ranks at N=2^17 (config 4)")
+    ap.add_argument("--virtual-shards", type=int, default=0,
+                    help="limb workload on ONE GPU: drive this many shards from one process (exchange = local "
+                         "copies); measures the summed shard compute, not multi-GPU speed")
     return ap.parse_args()
 
 
@@ -159,6 +165,9 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.workload == "limb":
+        run_limb(args)
         return
     import numpy as np
     import torch
@@ -376,6 +385,120 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_limb(args):
+    """Config 4: one ciphertext, RNS limbs sharded over the ranks (N=2^17,
+    l=24, alpha=8); one step = 1 HMult+relin (merged rescale) + 1 HRot(r=1),
+    each with two all-gathers (ModUp sources, ModDown sources) over NCCL."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_13055_b200 import ckks, dp
+    from paper_2407_13055_b200.limb import (MERGED, MOD_DOWN, LimbShardedEvaluator, LocalExchange, ShardBackend,
+                                            TorchExchange, exchange_bytes)
+
+    n = 1 << 17
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=L, alpha=ALPHA, delta_bits=DB), device=local)
+    q = torch.tensor(C.primes.astype(np.int64), device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321)  # same synthetic ciphertext and keys on every rank
+
+    def rand_rows(prefix, rows):
+        u = torch.randint(0, 1 << 62, (*prefix, len(rows), n), device=dev, generator=gen, dtype=torch.int64)
+        return (u % q[rows].view(*([1] * len(prefix)), -1, 1)).to(torch.int32).contiguous()
+
+    full = torch.cat([torch.arange(L, device=dev), L + torch.arange(ALPHA, device=dev)])
+    qrows = torch.arange(LEVEL, device=dev)
+    D = C.num_digits(L)
+    relin, rotk = rand_rows((D, 2), full), rand_rows((D, 2), full)
+    x, y = rand_rows((2,), qrows), rand_rows((2,), qrows)
+    if args.virtual_shards and world == 1:
+        G = args.virtual_shards
+        shards = [ShardBackend(C, G, r) for r in range(G)]
+        exch = LocalExchange()
+    else:
+        G = world
+        shards = [ShardBackend(C, world, rank)]
+        exch = TorchExchange() if world > 1 else LocalExchange()
+    lays = [s.layout for s in shards]
+    ev = LimbShardedEvaluator(shards, exch)
+    xs = [lay.split_ct(x, LEVEL) for lay in lays]
+    ys = [lay.split_ct(y, LEVEL) for lay in lays]
+    rk = [lay.split_key(relin) for lay in lays]
+    ok = [lay.split_key(rotk) for lay in lays]
+    del relin, rotk
+    st = torch.cuda.current_stream(dev)
+
+    def step():
+        ev.hmult(LEVEL, xs, ys, rk)
+        ev.hrot(LEVEL, xs, 1, ok)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+    l0 = C.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(args.steps):
+            step()
+        b.record(st)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = dp.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
+    launches = C.launch_count() - l0
+    # correctness spot check against the single-device path (rank-local rows)
+    if world == 1:
+        X = ckks.Ciphertext(x, Fraction(1 << DB), LEVEL)
+        Y = ckks.Ciphertext(y, Fraction(1 << DB), LEVEL)
+        full_hm = ckks.hmult(C, X, Y, ckks.EvaluationKey(_unsplit(rk, lays)))
+        got = torch.cat(ev.hmult(LEVEL, xs, ys, rk), dim=1)
+        exact = bool(torch.equal(got, full_hm.data))
+    else:
+        exact = None
+    if rank == 0:
+        xb = exchange_bytes(lays[0], n, LEVEL, MERGED) + exchange_bytes(lays[0], n, LEVEL, MOD_DOWN)
+        line = {
+            "metric": "single-ciphertext limb-sharded HMult+relin & HRot ops/s at N=2^17 (l=24, alpha=8, dnum=3)",
+            "value": round(2 * args.steps / (ms / 1e3), 2), "unit": "ops/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int32 residues (u32 mod q < 2^29, int64 accum)",
+            "data": "synthetic uniform residues (ciphertext and keys), random-init",
+            "config": {"workload": "BASELINE config 4: 1 HMult+relin (merged rescale) + 1 HRot(r=1) per step on one "
+                                   "ciphertext at N=2^17, l=24, alpha=8, limbs sharded over the ranks; all-gather "
+                                   "of the BConv source rows (NCCL) before ModUp and ModDown",
+                       "n": n, "l": L, "alpha": ALPHA, "level": LEVEL, "shards": G,
+                       "virtual_shards_on_one_gpu": bool(args.virtual_shards and world == 1),
+                       "parallelism": f"limb-sharded x{G}"},
+            "exchange_bytes_received_per_rank_per_step": xb,
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+            "bit_exact_vs_single_device": exact,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _unsplit(keys, lays):
+    """reassemble shard-local keys [D][2][q+p] into the full [D][2][L+alpha] key"""
+    import torch
+    qs = [k[:, :, :lay.q_hi - lay.q_lo] for k, lay in zip(keys, lays)]
+    ps = [k[:, :, lay.q_hi - lay.q_lo:] for k, lay in zip(keys, lays)]
+    return torch.cat(qs + ps, dim=2).contiguous()
 
 
 if __name__ == "__main__":
