@@ -57,6 +57,13 @@ __device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t b, uint32_t q,
   const uint32_t m = lo * qinv_neg;
   return hi + __umulhi(m, q) + (lo != 0u);
 }
+// acc + a*b with a, b < 2^32: one IMAD.WIDE.U32 (the compiler otherwise
+// sometimes widens a register-promoted operand and emits a 64x32 multiply)
+__device__ __forceinline__ uint64_t mac_wide(uint64_t acc, uint32_t a, uint32_t b) {
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(acc));
+  return d;
+}
 // Montgomery reduction of a 64-bit accumulator t < q*2^32 -> [0, 2q)
 __device__ __forceinline__ uint32_t mont_reduce64(uint64_t t, uint32_t q, uint32_t qinv_neg) {
   const uint32_t lo = static_cast<uint32_t>(t);

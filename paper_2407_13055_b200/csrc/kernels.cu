@@ -54,10 +54,10 @@ __global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
 #pragma unroll
     for (int j = 0; j < SC; ++j) {
       const uint32_t c = cm[i * SC + j];
-      acc0 += (uint64_t)s[j].x * c;
-      acc1 += (uint64_t)s[j].y * c;
-      acc2 += (uint64_t)s[j].z * c;
-      acc3 += (uint64_t)s[j].w * c;
+      acc0 = mac_wide(acc0, s[j].x, c);
+      acc1 = mac_wide(acc1, s[j].y, c);
+      acc2 = mac_wide(acc2, s[j].z, c);
+      acc3 = mac_wide(acc3, s[j].w, c);
     }
     const uint4 R = rc[i];
     uint4 r;
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kT) k_tensor(int n, int level, const uint32_t*
   {                                                                                          \
     const uint32_t bb = xb.c, ba = xa.c, cb = yb.c, ca = ya.c;                               \
     o0.c = sub_if(mont_mul(bb, cb, P.q, P.qinv_neg), P.q);                                   \
-    o1.c = sub_if(mont_reduce64((uint64_t)bb * ca + (uint64_t)ba * cb, P.q, P.qinv_neg), P.q); \
+    o1.c = sub_if(mont_reduce64(mac_wide(mac_wide(0ull, bb, ca), ba, cb), P.q, P.qinv_neg), P.q); \
     o2.c = sub_if(mont_mul(ba, ca, P.q, P.qinv_neg), P.q);                                   \
   }
   CK_T(x) CK_T(y) CK_T(z) CK_T(w)
@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(kT) k_key_mult(KeyMultLaunch a, int n) {
     const uint4 ea = ld4(a.evk + (((size_t)k * 2 + 1) * LA + g) * n + xo);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      s0[c] += (uint64_t)getc(dv, c) * getc(eb, c);
-      s1[c] += (uint64_t)getc(dv, c) * getc(ea, c);
+      s0[c] = mac_wide(s0[c], getc(dv, c), getc(eb, c));
+      s1[c] = mac_wide(s1[c], getc(dv, c), getc(ea, c));
     }
     if (++terms == 7) {
       renorm();
@@ -145,8 +145,8 @@ __global__ void __launch_bounds__(kT) k_key_mult(KeyMultLaunch a, int n) {
     if (terms == 7) renorm();
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      s0[c] += (uint64_t)getc(f0, c) * pm;
-      s1[c] += (uint64_t)getc(f1, c) * pm;
+      s0[c] = mac_wide(s0[c], getc(f0, c), pm);
+      s1[c] = mac_wide(s1[c], getc(f1, c), pm);
     }
   }
   uint4 r0, r1;

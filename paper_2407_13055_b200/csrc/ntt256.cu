@@ -541,10 +541,10 @@ __global__ void __launch_bounds__(256, 1) k_conv_mid(ConvMidLaunch a) {
       for (int s = 0; s < SC; ++s) {
         if (s < (int)G.sc) {
           const uint4 x = srct[s * 512 + rr];
-          a0 += (uint64_t)x.x * c[s];
-          a1 += (uint64_t)x.y * c[s];
-          a2 += (uint64_t)x.z * c[s];
-          a3 += (uint64_t)x.w * c[s];
+          a0 = mac_wide(a0, x.x, c[s]);
+          a1 = mac_wide(a1, x.y, c[s]);
+          a2 = mac_wide(a2, x.z, c[s]);
+          a3 = mac_wide(a3, x.w, c[s]);
         }
       }
       v[j] = make_uint4(mont_reduce64(a0, q, P.qinv_neg), mont_reduce64(a1, q, P.qinv_neg),
@@ -694,14 +694,14 @@ __global__ void __launch_bounds__(kKT) k_row_keymult(KeyMultLaunch a, const uint
       for (int m = 0; m < 4; ++m) {
         const uint4 xb = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
         const uint4 xa = __ldg(reinterpret_cast<const uint4*>(ea + 4 * m));
-        s0[4 * m] += (uint64_t)v[4 * m] * xb.x;
-        s0[4 * m + 1] += (uint64_t)v[4 * m + 1] * xb.y;
-        s0[4 * m + 2] += (uint64_t)v[4 * m + 2] * xb.z;
-        s0[4 * m + 3] += (uint64_t)v[4 * m + 3] * xb.w;
-        s1[4 * m] += (uint64_t)v[4 * m] * xa.x;
-        s1[4 * m + 1] += (uint64_t)v[4 * m + 1] * xa.y;
-        s1[4 * m + 2] += (uint64_t)v[4 * m + 2] * xa.z;
-        s1[4 * m + 3] += (uint64_t)v[4 * m + 3] * xa.w;
+        s0[4 * m] = mac_wide(s0[4 * m], v[4 * m], xb.x);
+        s0[4 * m + 1] = mac_wide(s0[4 * m + 1], v[4 * m + 1], xb.y);
+        s0[4 * m + 2] = mac_wide(s0[4 * m + 2], v[4 * m + 2], xb.z);
+        s0[4 * m + 3] = mac_wide(s0[4 * m + 3], v[4 * m + 3], xb.w);
+        s1[4 * m] = mac_wide(s1[4 * m], v[4 * m], xa.x);
+        s1[4 * m + 1] = mac_wide(s1[4 * m + 1], v[4 * m + 1], xa.y);
+        s1[4 * m + 2] = mac_wide(s1[4 * m + 2], v[4 * m + 2], xa.z);
+        s1[4 * m + 3] = mac_wide(s1[4 * m + 3], v[4 * m + 3], xa.w);
       }
       if ((k % 6) == 5) {  // keep the sums below q 2^32 (value unchanged mod q, rescaled by R)
 #pragma unroll
@@ -719,14 +719,14 @@ __global__ void __launch_bounds__(kKT) k_row_keymult(KeyMultLaunch a, const uint
       for (int m = 0; m < 4; ++m) {
         const uint4 x0 = *reinterpret_cast<const uint4*>(f0 + 4 * m);
         const uint4 x1 = *reinterpret_cast<const uint4*>(f1 + 4 * m);
-        s0[4 * m] += (uint64_t)x0.x * pm;
-        s0[4 * m + 1] += (uint64_t)x0.y * pm;
-        s0[4 * m + 2] += (uint64_t)x0.z * pm;
-        s0[4 * m + 3] += (uint64_t)x0.w * pm;
-        s1[4 * m] += (uint64_t)x1.x * pm;
-        s1[4 * m + 1] += (uint64_t)x1.y * pm;
-        s1[4 * m + 2] += (uint64_t)x1.z * pm;
-        s1[4 * m + 3] += (uint64_t)x1.w * pm;
+        s0[4 * m] = mac_wide(s0[4 * m], x0.x, pm);
+        s0[4 * m + 1] = mac_wide(s0[4 * m + 1], x0.y, pm);
+        s0[4 * m + 2] = mac_wide(s0[4 * m + 2], x0.z, pm);
+        s0[4 * m + 3] = mac_wide(s0[4 * m + 3], x0.w, pm);
+        s1[4 * m] = mac_wide(s1[4 * m], x1.x, pm);
+        s1[4 * m + 1] = mac_wide(s1[4 * m + 1], x1.y, pm);
+        s1[4 * m + 2] = mac_wide(s1[4 * m + 2], x1.z, pm);
+        s1[4 * m + 3] = mac_wide(s1[4 * m + 3], x1.w, pm);
       }
     }
     uint32_t* o0 = a.v + b * a.v_bs + (size_t)i * kN + rofs;

@@ -43,8 +43,8 @@ __global__ void __launch_bounds__(kST) k_shard_key_mult(ShardKeyMultLaunch a, in
     const uint4 ea = ld4(a.evk + (((size_t)k * 2 + 1) * a.erows + er) * n + xo);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      s0[c] += (uint64_t)getc(dv, c) * getc(eb, c);
-      s1[c] += (uint64_t)getc(dv, c) * getc(ea, c);
+      s0[c] = mac_wide(s0[c], getc(dv, c), getc(eb, c));
+      s1[c] = mac_wide(s1[c], getc(dv, c), getc(ea, c));
     }
     if (++terms == 7) {
       renorm();
@@ -58,8 +58,8 @@ __global__ void __launch_bounds__(kST) k_shard_key_mult(ShardKeyMultLaunch a, in
     if (terms == 7) renorm();
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      s0[c] += (uint64_t)getc(f0, c) * pm;
-      s1[c] += (uint64_t)getc(f1, c) * pm;
+      s0[c] = mac_wide(s0[c], getc(f0, c), pm);
+      s1[c] = mac_wide(s1[c], getc(f1, c), pm);
     }
   }
   uint4 r0, r1;
