@@ -466,6 +466,11 @@ struct Context {
       G.cmat_off = (uint32_t)cmat.size();
       G.map_off = (uint32_t)drow.size();
       bconv_consts(sg, dg, cmat, part1);
+      for (size_t i = 0; i < dg.size(); ++i)  // x R: the forward NTT then skips its entry merge
+        for (size_t j = 0; j < sg.size(); ++j) {
+          uint32_t& cij = cmat[G.cmat_off + i * sg.size() + j];
+          cij = mulm(cij, r_mod(q(dg[i])), q(dg[i]));
+        }
       max_sc = std::max<int>(max_sc, (int)sg.size());
       for (uint32_t i = 0; i < rows; ++i)
         if (i < b || i >= e) {
@@ -533,6 +538,8 @@ struct Context {
     for (uint32_t i = 0; i < out_q; ++i) dg[i] = i;
     std::vector<uint32_t> cmat, part1;
     bconv_consts(sg, dg, cmat, part1);
+    for (uint32_t i = 0; i < out_q; ++i)  // x R: the forward NTT then skips its entry merge
+      for (uint32_t j = 0; j < sc; ++j) cmat[i * sc + j] = mulm(cmat[i * sc + j], r_mod(q(dg[i])), q(dg[i]));
     std::vector<RowJob> ijobs, njobs;
     std::vector<ExitConst> exits;
     std::vector<BconvGroup> groups;
@@ -758,7 +765,7 @@ struct Context {
     } else {
       run_ntt(pl.intt, true, B, d, d_bs, is, level * N, 0, st);
       run_bconv(pl.bc, B, is, level * N, ext, ext_bs, st);
-      run_ntt(pl.ntt, false, B, ext, ext_bs, ext, ext_bs, 1, st);
+      run_ntt(pl.ntt, false, B, ext, ext_bs, ext, ext_bs, 0, st);  // BConv output already carries R
     }
     counters[0] += B;
     counters[3] += (uint64_t)B * level;
@@ -784,7 +791,7 @@ struct Context {
     {
       ProfScope ps(this, 0, 4.0 * n * pl.ntt.njobs * B, 1, st);  // column pass: half of the NTT traffic
       NttLaunch a = ntt_args(pl.ntt, false, B, ext, ext_bs, ext, ext_bs);
-      a.entry = 1;
+      a.entry = 0;  // BConv output already carries R
       ntt256_pass(0, a, d_tw2f, st);
     }
     KeyMultLaunch a;
@@ -862,7 +869,7 @@ struct Context {
     } else {
       run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
       run_bconv(pl.bc, B, ts, ts_bs, o, o_bs, st);
-      run_ntt(pl.ntt, false, B, o, o_bs, o, o_bs, 1, st);
+      run_ntt(pl.ntt, false, B, o, o_bs, o, o_bs, 0, st);  // BConv output already carries R
     }
     if (combine_now) {
       ProfScope ps(this, 5, 12.0 * n * pl.out_q * pl.npoly * B, 1, st);

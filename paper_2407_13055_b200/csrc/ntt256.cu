@@ -103,12 +103,16 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
   ColBuf* buf = reinterpret_cast<ColBuf*>(smraw);
   const int tid = threadIdx.x, cq = tid & 7, tau = tid >> 3;
   const int items = njobs * batch * kCTiles;
+  // the item decoded (and its job loaded) when it is prefetched is reused
+  // when it is processed
+  int nb = 0, ntile = 0;
+  RowJob nJ{};
   auto prefetch = [&](ColBuf& B, int it) {
-    int job, b, tile;
-    col_item(it, batch, job, b, tile);
-    const RowJob J = jobs[job];
-    const uint32_t* base = INV ? dst + b * dst_bs + (size_t)J.dst_off * kN : src + b * src_bs + (size_t)J.src_off * kN;
-    col_prefetch(B, base + tile * kCCols, tw_full + (size_t)J.prime * kN);
+    int job;
+    col_item(it, batch, job, nb, ntile);
+    nJ = jobs[job];
+    const uint32_t* base = INV ? dst + nb * dst_bs + (size_t)nJ.dst_off * kN : src + nb * src_bs + (size_t)nJ.src_off * kN;
+    col_prefetch(B, base + ntile * kCCols, tw_full + (size_t)nJ.prime * kN);
   };
   int it = blockIdx.x;
   if (it < items) prefetch(buf[0], it);
@@ -116,6 +120,8 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
   for (int k = 0; it < items; ++k, it += gridDim.x) {
     ColBuf& B = buf[DB ? (k & 1) : 0];
     const int nxt = it + gridDim.x;
+    const int b = nb, tile = ntile;
+    const RowJob J = nJ;
     if (DB) {
       if (nxt < items) prefetch(buf[(k + 1) & 1], nxt);
       cp_commit();
@@ -124,9 +130,6 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
       cp_wait<0>();
     }
     __syncthreads();
-    int job, b, tile;
-    col_item(it, batch, job, b, tile);
-    const RowJob J = jobs[job];
     const PrimeDev P = primes[J.prime];
     const uint32_t q = P.q, q2 = P.q2;
     uint32_t* out = dst + b * dst_bs + (size_t)J.dst_off * kN + tile * kCCols + 4 * cq;
@@ -262,6 +265,26 @@ __device__ __forceinline__ void row_prefetch(uint32_t* buf, const uint32_t* g) {
   }
 }
 
+// (job, row tile, b) item cursor, b fastest
+struct RowCursor {
+  int b, tile, job;
+  __device__ __forceinline__ void init(int it, int batch) {
+    b = it % batch;
+    const int key = it / batch;
+    tile = key % (kR / kRRows);
+    job = key / (kR / kRRows);
+  }
+  __device__ __forceinline__ void next(int batch) {
+    if (++b == batch) {
+      b = 0;
+      if (++tile == kR / kRRows) {
+        tile = 0;
+        ++job;
+      }
+    }
+  }
+};
+
 template <bool INV>
 __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
                                              uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
@@ -276,35 +299,56 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
   const int items = njobs * kTiles * batch;
   const int chunk = (items + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
-  auto in_ptr = [&](int it) {
-    const int b = it % batch, rest = it / batch, tile = rest % kTiles;
-    const RowJob J = jobs[rest / kTiles];
+  if (i0 >= i1) return;
+  // item cursors (job, row tile, b), advanced incrementally: no divisions and
+  // no dependent job/prime loads inside the loop except at (job, tile) changes
+  RowCursor c;
+  c.init(i0, batch);
+  RowJob Jc = jobs[c.job];
+  RowCursor nx = c;
+  RowJob Jn = Jc;
+  auto in_ptr = [&](const RowCursor& x, const RowJob& J) {
     // forward pass 2 works in place on dst; inverse pass A reads src
-    return INV ? src + b * src_bs + (size_t)J.src_off * kN + tile * kRRows * kR
-               : dst + b * dst_bs + (size_t)J.dst_off * kN + tile * kRRows * kR;
+    return INV ? src + x.b * src_bs + (size_t)J.src_off * kN + x.tile * kRRows * kR
+               : dst + x.b * dst_bs + (size_t)J.dst_off * kN + x.tile * kRRows * kR;
   };
-  if (i0 < i1) row_prefetch(sbuf, in_ptr(i0));
+  row_prefetch(sbuf, in_ptr(nx, Jn));
   cp_commit();
-  int cur_key = -1;
+  // this thread's 15 per-thread twiddle pairs (forward phase B / inverse phase
+  // A), kept in registers across the batch items of one (job, row tile)
+  uint2 twr[15];
+  uint32_t q = 0, q2 = 0;
   for (int it = i0, k = 0; it < i1; ++it, ++k) {
     uint32_t* line_buf = sbuf + (k & 1) * kRowBufWords;
-    const int b = it % batch, key = it / batch, tile = key % kTiles;
-    const RowJob J = jobs[key / kTiles];
-    if (key != cur_key) {  // stage this tile's twiddle tables (kRRows x 2 KB)
+    const int b = c.b, tile = c.tile;
+    const RowJob J = Jc;
+    const bool reload = it == i0 || b == 0;
+    if (reload) {  // stage this tile's twiddle tables (kRRows x 2 KB)
       __syncthreads();
       const uint2* T = tw2 + ((size_t)J.prime * kR + tile * kRRows) * kR;
       for (int e = tid; e < kRRows * kR / 2; e += kRT) cp16(&tws[2 * e], &T[2 * e]);
       cp_commit();
-      cur_key = key;
     }
-    if (it + 1 < i1) row_prefetch(sbuf + ((k + 1) & 1) * kRowBufWords, in_ptr(it + 1));
+    if (it + 1 < i1) {
+      const int pj = nx.job;
+      nx.next(batch);
+      if (nx.job != pj) Jn = jobs[nx.job];
+      row_prefetch(sbuf + ((k + 1) & 1) * kRowBufWords, in_ptr(nx, Jn));
+    }
     cp_commit();
     cp_wait<1>();
     __syncthreads();
-    const PrimeDev P = primes[J.prime];
-    const uint32_t q = P.q, q2 = P.q2;
     const int r = tile * kRRows + rho;
     const uint2* W = tws + rho * kR;
+    if (reload) {
+      const PrimeDev P = primes[J.prime];
+      q = P.q;
+      q2 = P.q2;
+    }
+    if (reload) {
+#pragma unroll
+      for (int i = 0; i < 15; ++i) twr[i] = INV ? W[i * 16 + tau] : W[16 + i * 16 + tau];
+    }
     uint32_t* line = line_buf + rho * kRowStride;
     uint32_t* orow = dst + b * dst_bs + (size_t)J.dst_off * kN + (size_t)r * kR;
     uint32_t v[16];
@@ -340,7 +384,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = W[16 + ((1 << t) - 1 + blk) * 16 + tau];
+          const uint2 w = twr[(1 << t) - 1 + blk];
           ct(v[j], v[j + d], w.x, w.y, q, q2);
         }
       }
@@ -365,7 +409,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = W[(off + blk) * 16 + tau];
+          const uint2 w = twr[off + blk];
           gs(v[j], v[j + d], w.x, w.y, q, q2);
         }
       }
@@ -391,6 +435,8 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
 #pragma unroll
       for (int j = 0; j < 16; ++j) orow[tau + 16 * j] = v[j];
     }
+    c = nx;
+    Jc = Jn;
     __syncthreads();  // data buffer k&1 is refilled by the prefetch of iteration k+1
   }
   cp_wait<0>();
