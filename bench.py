@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=2, help="concurrent sub-batches (CUDA streams) per GPU")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=4, help="ciphertexts per H2D/compute/D2H chunk")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also report the HRot level sweep (config 2)")
     ap.add_argument("--workload", default="dp", choices=["dp", "limb"],
@@ -57,28 +58,50 @@ def parse():
 
 # ----------------------------------------------------------------- clocks --
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
 
-    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
-             "clocks_event_reasons.sw_power_cap"
+    NVML (nvidia-ml-py) is polled every 2 ms from a thread — an nvidia-smi
+    process takes ~100 ms per query, longer than a default timed region —
+    with one nvidia-smi query as the fallback when NVML is unavailable."""
+
+    # nvmlClocksEventReason* bits (nvml.h)
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.sm, self.mx, self.bits = [], [], 0
         self._stop = threading.Event()
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                for line in out.stdout.strip().splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
+            while True:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                self.bits |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                if self._stop.wait(0.002):
+                    break
+            nv.nvmlShutdown()
+            return
+        except Exception:
+            pass
+        try:
+            out = subprocess.run(["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm,"
+                                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+            r = [x.strip() for x in out.stdout.strip().split(",")]
+            self.sm.append(float(r[0]))
+            self.mx.append(float(r[1]))
+            for bit, v in zip((0x8, 0x40, 0x20, 0x4), r[2:6]):
+                if v.lower() == "active":
+                    self.bits |= bit
+        except Exception:
+            pass
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -90,18 +113,10 @@ class ClockSampler:
         self._t.join(timeout=6)
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            for nm, v in zip(names, r[5:9]):
-                if v.strip().lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(v for k, v in self.REASONS.items() if self.bits & k), "samples": len(self.sm)}
 
 
 def peaks():
@@ -174,6 +189,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2407_13055_b200 import ckks, dp
+    from paper_2407_13055_b200.pipeline import HostPipeline
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -317,16 +333,16 @@ def main():
         hy.copy_(Y.data[:Be].cpu())
         ho1 = torch.empty((Be, 2, LEVEL - 2, N_RING), dtype=torch.int32).pin_memory()
         ho2 = torch.empty((Be, 2, LEVEL, N_RING), dtype=torch.int32).pin_memory()
-        dx = torch.empty_like(X.data[:Be])
-        dy = torch.empty_like(dx)
+        pipe = HostPipeline(dev, chunk=max(1, min(args.e2e_chunk, Be)), depth=2)
 
-        def e2e_step():
-            dx.copy_(hx, non_blocking=True)
-            dy.copy_(hy, non_blocking=True)
-            o1 = ckks.hmult(C, ckks.Ciphertext(dx, s, LEVEL), ckks.Ciphertext(dy, s, LEVEL), relin)
-            o2 = ckks.hrot(C, ckks.Ciphertext(dx, s, LEVEL), 1, rot)
-            ho1.copy_(o1.data, non_blocking=True)
-            ho2.copy_(o2.data, non_blocking=True)
+        def e2e_fn(d):
+            cx = ckks.Ciphertext(d[0], s, LEVEL)
+            o1 = ckks.hmult(C, cx, ckks.Ciphertext(d[1], s, LEVEL), relin)
+            o2 = ckks.hrot(C, cx, 1, rot)
+            return o1.data, o2.data
+
+        def e2e_step():  # the whole batch: H2D, HMult + HRot, D2H (chunked, overlapped)
+            return pipe.run([hx, hy], e2e_fn, [ho1, ho2])
 
         e2e_step()
         torch.cuda.synchronize(dev)
@@ -334,14 +350,16 @@ def main():
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         for _ in range(args.steps):
-            e2e_step()
+            last = e2e_step()
+        st.wait_event(last)
         b.record(st)
         torch.cuda.synchronize(dev)
         e_ms = dp.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
         e2e = {"value": round(2 * Be * args.steps * world / (e_ms / 1e3), 2), "unit": UNIT,
                "h2d_bytes_per_step": int(hx.numel() * 4 * 2), "d2h_bytes_per_step": int((ho1.numel() + ho2.numel()) * 4),
                "path": "ckks.hmult / ckks.hrot (C ABI) on ciphertexts copied from pinned host memory; results copied "
-                       "back each step"}
+                       "back each step (pipeline.HostPipeline: chunks of %d, H2D / compute / D2H on separate "
+                       "streams)" % pipe.chunk}
 
     sweep = None
     if args.sweep:

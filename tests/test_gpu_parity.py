@@ -251,6 +251,46 @@ def test_batched_equals_unbatched():
         np.testing.assert_array_equal(hr[b], one)
 
 
+@pytest.mark.parametrize("chunk,depth", [(2, 2), (3, 3), (8, 2)])
+def test_host_pipeline_equals_direct(chunk, depth):
+    """pipeline.HostPipeline (chunked H2D / compute / D2H on separate streams,
+    used by bench.py's e2e leg) returns exactly the direct batched results,
+    also across back-to-back runs that overlap."""
+    from paper_2407_13055_b200.pipeline import HostPipeline
+
+    n, l, a, db, B, level = 4096, 24, 8, 55, 7, 24
+    C = ctx_for(n, l, a, db)
+    O = _oracle(n, l, a, db)
+    xs, ys = [], []
+    for b in range(B):
+        xb, xa, yb, ya, evk = O.synthetic(level, 700 + b)
+        xs.append(np.stack([xb, xa]))
+        ys.append(np.stack([yb, ya]))
+    K = ckks.EvaluationKey(dev(evk))
+    KR = ckks.EvaluationKey(K.data, ckks.ROTATION, 1)
+    s = Fraction(1 << 55)
+    X = ckks.Ciphertext(dev(np.stack(xs)), s, level)
+    Y = ckks.Ciphertext(dev(np.stack(ys)), s, level)
+    want1 = host(ckks.hmult(C, X, Y, K).data)
+    want2 = host(ckks.hrot(C, X, 1, KR).data)
+    hx, hy = X.data.cpu().pin_memory(), Y.data.cpu().pin_memory()
+    ho1 = torch.zeros((B, 2, level - 2, n), dtype=torch.int32).pin_memory()
+    ho2 = torch.zeros((B, 2, level, n), dtype=torch.int32).pin_memory()
+    pipe = HostPipeline(torch.device("cuda", 0), chunk=chunk, depth=depth)
+
+    def fn(d):
+        cx = ckks.Ciphertext(d[0], s, level)
+        return ckks.hmult(C, cx, ckks.Ciphertext(d[1], s, level), K).data, ckks.hrot(C, cx, 1, KR).data
+
+    for _ in range(3):
+        ev = pipe.run([hx, hy], fn, [ho1, ho2])
+    ev.synchronize()
+    np.testing.assert_array_equal(ho1.numpy().astype(np.uint32), want1)
+    np.testing.assert_array_equal(ho2.numpy().astype(np.uint32), want2)
+    with pytest.raises(ValueError):
+        pipe.run([X.data, hy], fn, [ho1, ho2])  # device tensor where a pinned host one is required
+
+
 def test_counters_follow_reference_profile():
     # HMult at l=24: ntt 116, intt 44, bconv 5, keymult 3 (SURVEY.md §8d); HRot: ntt 120, intt 40
     n, l, a, db = 1024, 24, 8, 55
