@@ -210,7 +210,53 @@ struct BconvPlan {
   size_t groups_off = 0, cmat_off = 0, row_off = 0, prime_off = 0;
   int ngroups = 0, max_sc = 1;
   uint64_t src_rows = 0, dst_rows = 0;  // algorithmic rows read / written per batch item
+  // tensor-core path (bconv_tc.cu): per-group split-word B tables
+  bool tc_ok = false;
+  size_t tc_tab_off = 0, tc_boff_off = 0;
+  int tc_max_npad = 0, tc_max_dc = 0;
 };
+
+// Split-word B tables of the tcgen05 BConv (bconv_tc.cu) for every group of a
+// plan: row n = 4 i + a (destination i, byte a), column k = 4 j + b (source j,
+// byte b) holds byte a of (C[i][j] * 2^(8b) mod q_i), laid out in the UMMA
+// canonical K-major no-swizzle layout (8-row x 16-byte core matrices).
+template <class QF>
+void add_bconv_tc(BconvPlan& bp, const std::vector<BconvGroup>& groups, const std::vector<uint32_t>& cmat,
+                  const std::vector<uint16_t>& dprime, QF qf, uint32_t n) {
+  int max_sc = 0, max_dc = 0;
+  for (const auto& G : groups) {
+    max_sc = std::max(max_sc, (int)G.sc);
+    max_dc = std::max(max_dc, (int)G.dc);
+  }
+  bp.tc_ok = !groups.empty() && bconv_tc_supported((int)n, max_sc, max_dc);
+  if (!bp.tc_ok) return;
+  const int KB = max_sc > 8 ? 64 : 32, sbo = (KB / 16) * 128;
+  std::vector<uint8_t> tab;
+  std::vector<uint32_t> offs;
+  for (const auto& G : groups) {
+    const int npad = (4 * (int)G.dc + 15) / 16 * 16;
+    bp.tc_max_npad = std::max(bp.tc_max_npad, npad);
+    const size_t off = tab.size();
+    offs.push_back((uint32_t)off);
+    tab.resize(off + (size_t)npad * KB, 0);
+    for (uint32_t i = 0; i < G.dc; ++i) {
+      const uint32_t qi = qf(dprime[G.map_off + i]);
+      for (uint32_t j = 0; j < G.sc; ++j) {
+        const uint64_t c = cmat[G.cmat_off + i * G.sc + j];
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t cp = (uint32_t)((c << (8 * b)) % qi);
+          for (int a = 0; a < 4; ++a) {
+            const int nr = 4 * (int)i + a, kc = 4 * (int)j + b;
+            tab[off + (nr / 8) * sbo + (kc / 16) * 128 + (nr % 8) * 16 + (kc % 16)] = (uint8_t)(cp >> (8 * a));
+          }
+        }
+      }
+    }
+  }
+  bp.tc_max_dc = max_dc;
+  bp.tc_boff_off = bp.blob.add(offs);
+  bp.tc_tab_off = bp.blob.add(tab);
+}
 // ModUp at one level: INTT(+part1) of the level rows, per-digit BConv, NTT.
 // Tables of the fused INTT-B -> BConv -> NTT-1 kernel (ntt256.cu k_conv_mid).
 struct ConvMidPlan {
@@ -252,7 +298,8 @@ struct Context {
   uint2* d_tw2i = nullptr;
   bool use_ntt256 = true;
   bool use_cluster = false;  // CK32_NTT_CLUSTER=1: single-pass 8-CTA cluster/DSMEM NTT (slower today)
-  bool use_row_km = true;  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
+  bool use_row_km = true;
+  bool use_tc = false;  // CK32_TC=1: tcgen05 split-word BConv (bit-exact; slower than the CUDA-core kernel today)  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
   bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
   int ntt_chunk_limbs = 1 << 30;  // limbs per pass-1/pass-2 launch pair (CK32_NTT_CHUNK; measured: no gain)
   std::map<uint32_t, std::unique_ptr<ModUpPlan>> modup;
@@ -505,6 +552,7 @@ struct Context {
     pl->bc.max_sc = max_sc;
     pl->bc.src_rows = level;
     pl->bc.dst_rows = drow.size();
+    add_bconv_tc(pl->bc, groups, cmat, dprime, [&](uint32_t g) { return q(g); }, n);
     pl->bc.blob.upload();
     auto& ref = *pl;
     modup[level] = std::move(pl);
@@ -577,6 +625,7 @@ struct Context {
     pl->bc.max_sc = (int)sc;
     pl->bc.src_rows = (uint64_t)npoly * sc;
     pl->bc.dst_rows = (uint64_t)npoly * out_q;
+    add_bconv_tc(pl->bc, groups, cmat, dprime, [&](uint32_t g) { return q(g); }, n);
     pl->bc.blob.upload();
     // divisor = product of the source primes; one Montgomery inverse per row
     std::vector<uint32_t> dinv(out_q);
@@ -695,7 +744,16 @@ struct Context {
     a.dst_prime = pl.blob.at<uint16_t>(pl.prime_off);
     a.primes = d_primes;
     ProfScope ps(this, 2, 4.0 * n * (pl.src_rows + pl.dst_rows) * batch, 1, st);
-    bconv((int)n, a, st);
+    if (use_tc && pl.tc_ok) {
+      BconvTc t;
+      t.btab = pl.blob.at<unsigned char>(pl.tc_tab_off);
+      t.boff = pl.blob.at<uint32_t>(pl.tc_boff_off);
+      t.max_npad = pl.tc_max_npad;
+      t.max_dc = pl.tc_max_dc;
+      bconv_tc((int)n, a, t, st);
+    } else {
+      bconv((int)n, a, st);
+    }
     ++launches;
   }
 
@@ -1001,6 +1059,7 @@ struct Shard {
     pl->bc.max_sc = max_sc;
     pl->bc.src_rows = (uint64_t)alpha * groups.size();
     pl->bc.dst_rows = drow.size();
+    add_bconv_tc(pl->bc, groups, cmat, dprime, [&](uint32_t g) { return c->q(g); }, c->n);
     pl->bc.blob.upload();
     std::vector<int16_t> digit(pl->rows);
     std::vector<uint16_t> prime(pl->rows), erow(pl->rows);
@@ -1103,6 +1162,7 @@ struct Shard {
     pl->bc.max_sc = (int)pl->sc;
     pl->bc.src_rows = 2ull * pl->sc;
     pl->bc.dst_rows = 2ull * pl->lqo;
+    add_bconv_tc(pl->bc, groups, cmat, dprime, [&](uint32_t g) { return c->q(g); }, c->n);
     pl->bc.blob.upload();
     std::vector<uint32_t> dinv(std::max<uint32_t>(pl->lqo, 1), 0);
     for (uint32_t r = 0; r < pl->lqo; ++r) {
@@ -1334,6 +1394,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     if (const char* ch = std::getenv("CK32_NTT_CHUNK")) c->ntt_chunk_limbs = std::max(1, std::atoi(ch));
     c->use_fused = std::getenv("CK32_FUSED") != nullptr;
     c->use_row_km = std::getenv("CK32_NO_ROW_KEYMULT") == nullptr;
+    c->use_tc = std::getenv("CK32_TC") != nullptr;
     c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;
     if (n == 65536) {
       // Row-pass twiddles of ntt256.cu, permuted per row in thread-consumption
@@ -1573,6 +1634,7 @@ ck_status ck_bconv(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count,
       pl->max_sc = (int)src_count;
       pl->src_rows = src_count;
       pl->dst_rows = dst_count;
+      add_bconv_tc(*pl, groups, cmat, dprime, [&](uint32_t g) { return c->q(g); }, c->n);
       pl->blob.upload();
     }
     c->run_bconv(*pl, 1, src_dev, 0, dst_dev, 0, S(stream));

@@ -82,6 +82,14 @@ struct BconvLaunch {
   const PrimeDev* primes = nullptr;
 };
 void bconv(int n, const BconvLaunch& a, cudaStream_t st);
+// tensor-core BConv (bconv_tc.cu): tcgen05 u8 split-word GEMM, TMEM accumulator
+struct BconvTc {
+  const unsigned char* btab = nullptr;  // per-group B tables (canonical UMMA layout)
+  const uint32_t* boff = nullptr;       // byte offset of each group's table
+  int max_npad = 0, max_dc = 0;
+};
+bool bconv_tc_supported(int n, int max_sc, int max_dc);
+void bconv_tc(int n, const BconvLaunch& a, const BconvTc& t, cudaStream_t st);
 
 // tensor product of two ciphertexts (ckks.cpp:818-821): d0 = b b', d1 = b a' + a b', d2 = a a'
 void tensor(int n, int level, int batch, const uint32_t* x, const uint32_t* y, uint64_t ct_bs, uint32_t* d01,

@@ -91,6 +91,52 @@ def test_bconv_matches_oracle(n, shape):
     np.testing.assert_array_equal(host(got), want)
 
 
+@pytest.fixture
+def tc_env(monkeypatch):
+    """Contexts created inside the test run BConv on the tcgen05 split-word
+    GEMM (CK32_TC=1, read at context creation; bconv_tc.cu)."""
+    monkeypatch.setenv("CK32_TC", "1")
+    made = []
+
+    def make(n, l, a, db=55):
+        c = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db))
+        made.append(c)
+        return c
+    yield make
+    for c in made:
+        c.close()
+
+
+@pytest.mark.parametrize("n", [1024, 65536])
+@pytest.mark.parametrize("shape", [(8, 24), (10, 22), (2, 22), (1, 3), (16, 40), (16, 64)])
+def test_bconv_tensor_core_matches_oracle(tc_env, n, shape):
+    sc, dc = shape
+    l, a = 64, 16
+    C = tc_env(n, l, a, 48)
+    O = _oracle(n, l, a, 48)
+    src_g = list(range(l - sc, l)) if sc <= 10 else [l + j for j in range(sc)]
+    dst_g = list(range(dc))
+    src = O.canonical(O.random_rows(Rng(sc * 77 + dc), np.array(src_g, np.uint32)), np.array(src_g, np.uint32))
+    got = ckks.bconv(C, dev(src), src_g, dst_g)
+    want = O.canonical(O.bconv(src.astype(np.int32), src_g, dst_g), np.array(dst_g, np.uint32))
+    np.testing.assert_array_equal(host(got), want)
+
+
+@pytest.mark.parametrize("level", [24, 17, 9, 4])
+def test_mechanisms_tensor_core_bconv_match_oracle(tc_env, level):
+    n, l, a, db = 4096, 24, 8, 55
+    C = tc_env(n, l, a, db)
+    O = _oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(level, 31 + level)
+    x, y = ct(np.stack([xb, xa]), level), ct(np.stack([yb, ya]), level)
+    ob, oa = O.hmult(level, xb, xa, yb, ya, evk)
+    got = host(ckks.hmult(C, x, y, ckks.EvaluationKey(dev(evk))).data)
+    np.testing.assert_array_equal(got, np.stack([canon(O, ob, level - 2), canon(O, oa, level - 2)]))
+    ob, oa = O.hrot(level, xb, xa, 5, evk)
+    got = host(ckks.hrot(C, x, 5, ckks.EvaluationKey(dev(evk), ckks.ROTATION, 5)).data)
+    np.testing.assert_array_equal(got, np.stack([canon(O, ob, level), canon(O, oa, level)]))
+
+
 @pytest.mark.parametrize("r", [1, 3, -2, 1 << 14, 12345])
 def test_automorphism_and_group_law(r):
     n, l, a = 65536, 4, 2
