@@ -47,9 +47,10 @@ def parse():
     ap.add_argument("--e2e-chunk", type=int, default=4, help="ciphertexts per H2D/compute/D2H chunk")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also report the HRot level sweep (config 2)")
-    ap.add_argument("--workload", default="dp", choices=["dp", "limb"],
+    ap.add_argument("--workload", default="dp", choices=["dp", "limb", "helr"],
                     help="dp: batched independent ciphertexts (configs 1-3, the headline); limb: one ciphertext "
-                         "limb-sharded over the ranks at N=2^17 (config 4)")
+                         "limb-sharded over the ranks at N=2^17 (config 4); helr: HELR-style logistic-regression "
+                         "iteration (config 5)")
     ap.add_argument("--virtual-shards", type=int, default=0,
                     help="limb workload on ONE GPU: drive this many shards from one process (exchange = local "
                          "copies); measures the summed shard compute, not multi-GPU speed")
@@ -183,6 +184,9 @@ def main():
         return
     if args.workload == "limb":
         run_limb(args)
+        return
+    if args.workload == "helr":
+        run_helr(args)
         return
     import numpy as np
     import torch
@@ -505,6 +509,86 @@ def run_limb(args):
             "exchange_bytes_received_per_rank_per_step": xb,
             "gpu_launches": int(launches), "clocks": clk.summary(),
             "bit_exact_vs_single_device": exact,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_helr(args):
+    """Config 5: HELR-style logistic-regression iteration (helr.py) at N=2^16,
+    l=24, one mini-batch of 8 ciphertexts x (128 samples x 256 features) per
+    GPU (1024 samples, the batch of Cheddar's HELR run).
+    Synthetic ciphertexts, keys and plaintext constants (uniform residues)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_13055_b200 import ckks, dp
+    from paper_2407_13055_b200.helr import HelrIteration, HelrShape
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    shape = HelrShape(n=N_RING, features=256, cts=8)
+    C = ckks.CkksContext(ckks.CkksParams(n=N_RING, l=L, alpha=ALPHA, delta_bits=DB), device=local)
+    q = torch.tensor(C.primes.astype(np.int64), device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(777 + rank)
+
+    def rand_rows(prefix, rows):
+        u = torch.randint(0, 1 << 62, (*prefix, len(rows), N_RING), device=dev, generator=gen, dtype=torch.int64)
+        return (u % q[rows].view(*([1] * len(prefix)), -1, 1)).to(torch.int32).contiguous()
+
+    full = torch.cat([torch.arange(L, device=dev), L + torch.arange(ALPHA, device=dev)])
+    D = C.num_digits(L)
+    relin = ckks.EvaluationKey(rand_rows((D, 2), full))
+    keys = {r: ckks.EvaluationKey(rand_rows((D, 2), full), ckks.ROTATION, r) for r in shape.rotations()}
+
+    def const(level, scale):
+        return ckks.Plaintext(ckks.Polynomial(rand_rows((), torch.arange(level, device=dev)), level, 0), scale, level)
+
+    it = HelrIteration(C, shape, relin, keys, {k: const for k in ("a3", "a1", "a0", "gamma")})
+    s = Fraction(1 << DB)
+    Z = ckks.Ciphertext(rand_rows((shape.cts, 2), torch.arange(L, device=dev)), s, L)
+    W = ckks.Ciphertext(rand_rows((2,), torch.arange(L, device=dev)), s, L)
+    st = torch.cuda.current_stream(dev)
+    for _ in range(max(args.warmup, 0)):
+        it.step(Z, W)
+    torch.cuda.synchronize(dev)
+    l0 = C.launch_count()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(args.steps):
+            it.step(Z, W)
+        b.record(st)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = dp.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
+    if rank == 0:
+        per = ms / args.steps
+        line = {
+            "metric": "HELR-style logistic-regression iterations/s (1024-sample mini-batch per GPU, N=2^16, l=24)",
+            "value": round(world * args.steps / (ms / 1e3), 2), "unit": "it/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per, 4), "ms_per_iteration": round(per, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32 residues (u32 mod q < 2^29, int64 accum)",
+            "data": "synthetic uniform residues (ciphertexts, keys, plaintext constants), random-init",
+            "config": {"workload": "BASELINE config 5: one HELR-style gradient step (helr.py): 8 ciphertexts x 128 "
+                                   "samples x 256 features, degree-3 sigmoid, rotate-and-sum over features and "
+                                   "samples, batched mechanisms", "n": N_RING, "l": L, "alpha": ALPHA,
+                       "features": shape.features, "samples": shape.cts * shape.samples_per_ct,
+                       "rns_limbs_consumed": it.levels_used(), "ops_per_iteration": it.op_profile(),
+                       "parallelism": f"dp{world} (one mini-batch per GPU)"},
+            "gpu_launches": int(C.launch_count() - l0), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
