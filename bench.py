@@ -320,10 +320,19 @@ def main():
                          "GBps": round(p["bytes"] / (p["ms"] * 1e6), 1),
                          "frac": round(p["bytes"] / (p["ms"] * 1e6) / hbm, 4)})
 
+    try:
+        traffic_ratio = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+    except Exception:
+        traffic_ratio = {}
+
     def roof(p):
         ach = p["bytes"] / (p["ms"] * 1e6)
+        per_group = p["bytes"] / max(p["groups"], 1)
+        tr = traffic_ratio.get(p["name"], {}).get("ratio")
         return {"kernel": p["name"], "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": None, "peak_kind": peak_kind,
+                "frac": round(ach / hbm, 4), "traffic": round(tr * per_group) if tr else None,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full DRAM bytes per algorithmic byte)"
+                if tr else None, "peak_kind": peak_kind,
                 "bytes_per_launch_group": round(p["bytes"] / max(p["groups"], 1)),
                 "avg_group_ms": round(p["ms"] / max(p["groups"], 1), 4)}
 
