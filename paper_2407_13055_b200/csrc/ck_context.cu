@@ -1546,19 +1546,20 @@ ck_status ck_ntt_forward(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, con
     Context* c = C(ctx);
     check_ptr(rows_dev);
     if (!gidx && rows) throw InvalidArgument("null prime index list");
-    std::string key = "F";
-    std::vector<RowJob> jobs;
-    for (uint32_t i = 0; i < rows; ++i) {
-      if (gidx[i] >= c->primes.size()) throw InvalidArgument("prime index out of range");
-      jobs.push_back({i, i, (uint16_t)gidx[i], 0});
-      key += std::to_string(gidx[i]) + ",";
-    }
+    std::string key(1, 'F');
+    key.append(reinterpret_cast<const char*>(gidx), sizeof(uint32_t) * rows);
     auto& pl = c->adhoc_ntt[key];
     if (!pl) {
-      pl = std::make_unique<NttPlan>();
-      pl->jobs_off = pl->blob.add(jobs);
-      pl->njobs = (int)jobs.size();
-      pl->blob.upload();
+      std::vector<RowJob> jobs;
+      for (uint32_t i = 0; i < rows; ++i) {
+        if (gidx[i] >= c->primes.size()) throw InvalidArgument("prime index out of range");
+        jobs.push_back({i, i, (uint16_t)gidx[i], 0});
+      }
+      auto np = std::make_unique<NttPlan>();
+      np->jobs_off = np->blob.add(jobs);
+      np->njobs = (int)jobs.size();
+      np->blob.upload();
+      pl = std::move(np);
     }
     c->run_ntt(*pl, false, 1, rows_dev, 0, rows_dev, 0, 1, S(stream));
     check_launch();
@@ -1572,25 +1573,29 @@ ck_status ck_intt_inverse(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, co
     Context* c = C(ctx);
     check_ptr(rows_dev);
     if (!gidx && rows) throw InvalidArgument("null prime index list");
-    std::string key = "I";
-    std::vector<RowJob> jobs;
-    std::vector<ExitConst> exits;
-    for (uint32_t i = 0; i < rows; ++i) {
-      if (gidx[i] >= c->primes.size()) throw InvalidArgument("prime index out of range");
-      const uint32_t q = c->q(gidx[i]);
-      // epilogue given in Montgomery form (ntt.hpp:72-73): plain factor = e * R^-1
-      const uint32_t e = epilogue_mont ? mulm(epilogue_mont[i] % q, invm(r_mod(q), q), q) : 1u;
-      jobs.push_back({i, i, (uint16_t)gidx[i], (uint16_t)i});
-      exits.push_back(c->exit_const(gidx[i], e));
-      key += std::to_string(gidx[i]) + ":" + std::to_string(e) + ",";
-    }
+    // plan cache key: the raw prime-index and epilogue words (no per-call
+    // modular arithmetic on a hit: the exit constants are built once)
+    std::string key(1, 'I');
+    key.append(reinterpret_cast<const char*>(gidx), sizeof(uint32_t) * rows);
+    if (epilogue_mont) key.append(reinterpret_cast<const char*>(epilogue_mont), sizeof(uint32_t) * rows);
     auto& pl = c->adhoc_ntt[key];
     if (!pl) {
-      pl = std::make_unique<NttPlan>();
-      pl->jobs_off = pl->blob.add(jobs);
-      pl->exits_off = pl->blob.add(exits);
-      pl->njobs = (int)jobs.size();
-      pl->blob.upload();
+      std::vector<RowJob> jobs;
+      std::vector<ExitConst> exits;
+      for (uint32_t i = 0; i < rows; ++i) {
+        if (gidx[i] >= c->primes.size()) throw InvalidArgument("prime index out of range");
+        const uint32_t q = c->q(gidx[i]);
+        // epilogue given in Montgomery form (ntt.hpp:72-73): plain factor = e * R^-1
+        const uint32_t e = epilogue_mont ? mulm(epilogue_mont[i] % q, invm(r_mod(q), q), q) : 1u;
+        jobs.push_back({i, i, (uint16_t)gidx[i], (uint16_t)i});
+        exits.push_back(c->exit_const(gidx[i], e));
+      }
+      auto np = std::make_unique<NttPlan>();
+      np->jobs_off = np->blob.add(jobs);
+      np->exits_off = np->blob.add(exits);
+      np->njobs = (int)jobs.size();
+      np->blob.upload();
+      pl = std::move(np);
     }
     c->run_ntt(*pl, true, 1, rows_dev, 0, rows_dev, 0, 0, S(stream));
     check_launch();

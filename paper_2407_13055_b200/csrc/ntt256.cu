@@ -93,29 +93,41 @@ __device__ __forceinline__ void col_item(int it, int batch, int& job, int& b, in
   job = rest / batch;
 }
 
-template <bool INV, bool DB>
-__global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
+// TWR: the twiddle tables ride in their own 2-slot ring (slot = item parity)
+// instead of inside the tile buffer, so phase B reads them from shared memory
+// after the next item's prefetch has started (no 15 twiddle pairs in
+// registers: 124 -> ~96 registers, MINB CTAs per SM).
+template <bool INV, bool DB, bool TWR = false, int MINB = 1>
+__global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
                                              uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
                                              int njobs, const PrimeDev* __restrict__ primes,
                                              const uint2* __restrict__ tw_full, const ExitConst* __restrict__ exits,
                                              int entry) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ColBuf* buf = reinterpret_cast<ColBuf*>(smraw);
+  uint2* twring = reinterpret_cast<uint2*>(smraw + (DB ? 2 : 1) * sizeof(ColBuf));  // [2][256] (TWR)
   const int tid = threadIdx.x, cq = tid & 7, tau = tid >> 3;
   const int items = njobs * batch * kCTiles;
   // the item decoded (and its job loaded) when it is prefetched is reused
   // when it is processed
   int nb = 0, ntile = 0;
   RowJob nJ{};
-  auto prefetch = [&](ColBuf& B, int it) {
+  auto prefetch = [&](ColBuf& B, int it, int k) {
     int job;
     col_item(it, batch, job, nb, ntile);
     nJ = jobs[job];
     const uint32_t* base = INV ? dst + nb * dst_bs + (size_t)nJ.dst_off * kN : src + nb * src_bs + (size_t)nJ.src_off * kN;
-    col_prefetch(B, base + ntile * kCCols, tw_full + (size_t)nJ.prime * kN);
+    if (TWR) {
+      const uint32_t* g = base + ntile * kCCols;
+      for (int e = threadIdx.x; e < 256 * 8; e += kCT) cp16(&B.tile[(e >> 3) * 8 + (e & 7)], g + (e >> 3) * kR + 4 * (e & 7));
+      const uint2* tw = tw_full + (size_t)nJ.prime * kN;
+      cp16(&twring[(k & 1) * 256 + 2 * threadIdx.x], tw + 2 * threadIdx.x);
+    } else {
+      col_prefetch(B, base + ntile * kCCols, tw_full + (size_t)nJ.prime * kN);
+    }
   };
   int it = blockIdx.x;
-  if (it < items) prefetch(buf[0], it);
+  if (it < items) prefetch(buf[0], it, 0);
   cp_commit();
   for (int k = 0; it < items; ++k, it += gridDim.x) {
     ColBuf& B = buf[DB ? (k & 1) : 0];
@@ -123,7 +135,7 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
     const int b = nb, tile = ntile;
     const RowJob J = nJ;
     if (DB) {
-      if (nxt < items) prefetch(buf[(k + 1) & 1], nxt);
+      if (nxt < items) prefetch(buf[(k + 1) & 1], nxt, k + 1);
       cp_commit();
       cp_wait<1>();
     } else {
@@ -132,6 +144,7 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
     __syncthreads();
     const PrimeDev P = primes[J.prime];
     const uint32_t q = P.q, q2 = P.q2;
+    const uint2* TW = TWR ? twring + (k & 1) * 256 : B.tw;
     uint32_t* out = dst + b * dst_bs + (size_t)J.dst_off * kN + tile * kCCols + 4 * cq;
     uint4 v[16];
     if (!INV) {
@@ -155,7 +168,7 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
             CK_E(x) CK_E(y) CK_E(z) CK_E(w)
 #undef CK_E
           } else {
-            ct4(v[j], v[j + d], B.tw[(1 << t) + blk], q, q2);
+            ct4(v[j], v[j + d], TW[(1 << t) + blk], q, q2);
           }
         }
       }
@@ -164,14 +177,16 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = B.tile[(16 * tau + j) * 8 + cq];
-      uint2 twb[15];  // phase-B twiddles to registers so the buffer can be refilled
+      uint2 twb[TWR ? 1 : 15];  // phase-B twiddles to registers so the buffer can be refilled
+      if (!TWR) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < 4; ++t)
 #pragma unroll
-        for (int blk = 0; blk < (1 << t); ++blk) twb[(1 << t) - 1 + blk] = B.tw[(16 << t) + (tau << t) + blk];
+          for (int blk = 0; blk < (1 << t); ++blk) twb[(1 << t) - 1 + blk] = B.tw[(16 << t) + (tau << t) + blk];
+      }
       if (!DB) {
         __syncthreads();
-        if (nxt < items) prefetch(buf[0], nxt);
+        if (nxt < items) prefetch(buf[0], nxt, k + 1);
         cp_commit();
       }
       // phase B rows 16 tau + j: twiddle 2^s + tau 2^(s-4) + blk
@@ -181,7 +196,7 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
-          ct4(v[j], v[j + d], twb[(1 << t) - 1 + blk], q, q2);
+          ct4(v[j], v[j + d], TWR ? TW[(16 << t) + (tau << t) + blk] : twb[(1 << t) - 1 + blk], q, q2);
         }
       }
 #pragma unroll
@@ -197,7 +212,7 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
-          gs4(v[j], v[j + d], B.tw[(128 >> t) + (tau << (3 - t)) + blk], q, q2);
+          gs4(v[j], v[j + d], TW[(128 >> t) + (tau << (3 - t)) + blk], q, q2);
         }
       }
 #pragma unroll
@@ -205,14 +220,16 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = B.tile[(tau + 16 * j) * 8 + cq];
-      uint2 twb[15];  // index (8>>t)-1+blk, t < 3
+      uint2 twb[TWR ? 1 : 15];  // index (8>>t)-1+blk, t < 3
+      if (!TWR) {
 #pragma unroll
-      for (int t = 0; t < 3; ++t)
+        for (int t = 0; t < 3; ++t)
 #pragma unroll
-        for (int blk = 0; blk < (8 >> t); ++blk) twb[(8 >> t) - 1 + blk] = B.tw[(8 >> t) + blk];
+          for (int blk = 0; blk < (8 >> t); ++blk) twb[(8 >> t) - 1 + blk] = B.tw[(8 >> t) + blk];
+      }
       if (!DB) {
         __syncthreads();
-        if (nxt < items) prefetch(buf[0], nxt);
+        if (nxt < items) prefetch(buf[0], nxt, k + 1);
         cp_commit();
       }
 #pragma unroll
@@ -221,7 +238,7 @@ __global__ void __launch_bounds__(kCT) k_col(const RowJob* __restrict__ jobs, co
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
-          gs4(v[j], v[j + d], twb[(8 >> t) - 1 + blk], q, q2);
+          gs4(v[j], v[j + d], TWR ? TW[(8 >> t) + blk] : twb[(8 >> t) - 1 + blk], q, q2);
         }
       }
 #pragma unroll
@@ -444,11 +461,18 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
 
 int g_col_grid[2] = {0, 0}, g_row_grid = 0;
 bool g_col_db = false;
+int g_col_var = 2;  // CK32_COL: 0 = twiddles in registers, 1 = twiddle ring (4 CTAs/SM), 2 = ring, 5 CTAs/SM (default)
+constexpr int kColRingSmem = (int)sizeof(ColBuf) + 2 * 256 * 8;
 
 void init_grids() {
   if (g_row_grid) return;
   const char* v = std::getenv("CK32_NTT_COL_DB");
   g_col_db = v && v[0] == '1';
+  if (const char* cv = std::getenv("CK32_COL")) g_col_var = std::atoi(cv);
+  cudaFuncSetAttribute(k_col<false, false, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColRingSmem);
+  cudaFuncSetAttribute(k_col<true, false, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColRingSmem);
+  cudaFuncSetAttribute(k_col<false, false, true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColRingSmem);
+  cudaFuncSetAttribute(k_col<true, false, true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColRingSmem);
   const int col_smem_db = 2 * (int)sizeof(ColBuf), col_smem_sb = (int)sizeof(ColBuf);
   cudaFuncSetAttribute(k_col<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem_db);
   cudaFuncSetAttribute(k_col<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem_db);
@@ -459,7 +483,15 @@ void init_grids() {
   int dev = 0, sms = 148, c1 = 1, c2 = 1, r1 = 1, r2 = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (g_col_db) {
+  if (g_col_var == 1 || g_col_var == 2) {
+    if (g_col_var == 1) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, false, true, 4>, kCT, kColRingSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, false, true, 4>, kCT, kColRingSmem);
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, false, true, 5>, kCT, kColRingSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, false, true, 5>, kCT, kColRingSmem);
+    }
+  } else if (g_col_db) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, true>, kCT, col_smem_db);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, true>, kCT, col_smem_db);
   } else {
@@ -477,7 +509,13 @@ template <bool INV>
 void launch_col(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaStream_t st) {
   const int items = a.njobs * a.batch * kCTiles;
   const int grid = min(g_col_grid[INV], items);
-  if (g_col_db)
+  if (g_col_var == 1)
+    k_col<INV, false, true, 4><<<grid, kCT, kColRingSmem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
+                                                                 a.primes, a.tw, a.exits, a.entry);
+  else if (g_col_var == 2)
+    k_col<INV, false, true, 5><<<grid, kCT, kColRingSmem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
+                                                                 a.primes, a.tw, a.exits, a.entry);
+  else if (g_col_db)
     k_col<INV, true><<<grid, kCT, 2 * sizeof(ColBuf), st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
                                                             a.primes, a.tw, a.exits, a.entry);
   else
