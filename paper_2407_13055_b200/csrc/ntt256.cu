@@ -678,7 +678,10 @@ constexpr int kKT = 128;  // 8 rows x 16 threads
 constexpr int kKBuf = kRRows * kRowStride;
 constexpr int kKSmem = 2 * kKBuf * 4 + kRRows * kR * 8;
 
-__global__ void __launch_bounds__(kKT) k_row_keymult(KeyMultLaunch a, const uint2* __restrict__ tw2) {
+// EARLY: the key halves of digit k are loaded into registers before its row
+// pass (their L2 latency hides behind the butterflies) at MINB CTAs per SM.
+template <bool EARLY = false, int MINB = 1>
+__global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, const uint2* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
   uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * kKBuf * 4);
@@ -711,6 +714,16 @@ __global__ void __launch_bounds__(kKT) k_row_keymult(KeyMultLaunch a, const uint
     const size_t rofs = (size_t)r * kR + 16 * tau;  // this thread's 16 coefficients after the row pass
     for (int k = 0; k < a.D; ++k) {
       const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+      uint4 kb[4], ka[4];
+      if (EARLY) {
+        const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
+        const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          kb[m] = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
+          ka[m] = __ldg(reinterpret_cast<const uint4*>(ea + 4 * m));
+        }
+      }
       uint32_t v[16];
       if (i >= lo && i < hi) {  // the digit's own row: ModUp passes it through unchanged
         const uint32_t* dr = a.d + b * a.d_bs + (size_t)i * kN + rofs;
@@ -776,8 +789,8 @@ __global__ void __launch_bounds__(kKT) k_row_keymult(KeyMultLaunch a, const uint
       const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const uint4 xb = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
-        const uint4 xa = __ldg(reinterpret_cast<const uint4*>(ea + 4 * m));
+        const uint4 xb = EARLY ? kb[m] : __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
+        const uint4 xa = EARLY ? ka[m] : __ldg(reinterpret_cast<const uint4*>(ea + 4 * m));
         s0[4 * m] = mac_wide(s0[4 * m], v[4 * m], xb.x);
         s0[4 * m + 1] = mac_wide(s0[4 * m + 1], v[4 * m + 1], xb.y);
         s0[4 * m + 2] = mac_wide(s0[4 * m + 2], v[4 * m + 2], xb.z);
@@ -832,18 +845,36 @@ __global__ void __launch_bounds__(kKT) k_row_keymult(KeyMultLaunch a, const uint
 
 }  // namespace
 
-void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
+// CK32_KM selects the k_row_keymult variant for A/B runs: 0 = key halves
+// loaded before the row pass, 4 CTAs/SM (default: 4.83 vs 4.77 TB/s), 1 = same
+// at 3 CTAs/SM (4.20), 2 = loaded after the row pass (the first version).
+template <bool EARLY, int MINB>
+static void launch_km(const KeyMultLaunch& a, const uint2* tw2, int items, cudaStream_t st) {
   static int grid = 0;
   if (!grid) {
-    cudaFuncSetAttribute(k_row_keymult, cudaFuncAttributeMaxDynamicSharedMemorySize, kKSmem);
+    cudaFuncSetAttribute(k_row_keymult<EARLY, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kKSmem);
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult, kKT, kKSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult<EARLY, MINB>, kKT, kKSmem);
     grid = sms * std::max(1, per);
   }
+  k_row_keymult<EARLY, MINB><<<std::min(grid, items), kKT, kKSmem, st>>>(a, tw2);
+}
+
+void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
+  static int ver = -1;
+  if (ver < 0) {
+    const char* e = std::getenv("CK32_KM");
+    ver = e ? std::atoi(e) : 0;
+  }
   const int items = (a.level + a.alpha) * (kR / kRRows) * a.batch;
-  k_row_keymult<<<std::min(grid, items), kKT, kKSmem, st>>>(a, tw2);
+  if (ver == 1)
+    launch_km<true, 3>(a, tw2, items, st);
+  else if (ver == 2)
+    launch_km<false, 4>(a, tw2, items, st);
+  else
+    launch_km<true, 4>(a, tw2, items, st);
 }
 
 void conv_mid(const ConvMidLaunch& a, cudaStream_t st) {
