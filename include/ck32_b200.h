@@ -147,6 +147,20 @@ ck_status ck_hoisted_rotate_accumulate(ck_context* ctx, uint32_t level, const ui
                                        const int64_t* rots, const uint32_t* const* pts,
                                        const uint32_t* const* evks, uint32_t* out, ck_stream stream);
 
+/* encode (ckks.cpp:278-319): `count` <= n/2 complex slots (re, im doubles,
+ * device memory) -> plaintext rows [level (+alpha if p_extend)][n] in the
+ * evaluation domain, Montgomery form (canonical residues).  scale_log2 is
+ * log2_rational(scale) (ckks.cpp:140-158); residues are bit-identical to the
+ * reference when the scale is a power of two. */
+ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, double scale_log2, uint32_t level,
+                    int p_extend, uint32_t* out_dev, ck_stream stream);
+/* decode (ckks.cpp:321-362): plaintext rows [level][n] (evaluation,
+ * Montgomery) -> n/2 complex slots (re, im doubles, device memory).  The CRT
+ * lift uses the minimal prime prefix covering scale_log2 + 40 bits (as the
+ * reference) and supports up to 4 primes. */
+ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2, double* slots_dev,
+                    ck_stream stream);
+
 /* Number of this library's kernel launches issued since context creation
  * (evidence for bench.py's gpu_launches). */
 uint64_t ck_launch_count(const ck_context* ctx);

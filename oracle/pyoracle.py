@@ -266,6 +266,11 @@ class Reference:
         lib.ref_mechanism_bench.argtypes = [ctypes.c_char_p] + [ctypes.c_uint32] * 7 + [
             ctypes.c_uint64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
             ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_uint64)]
+        _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        lib.ref_encode.argtypes = [ctypes.c_uint32] * 4 + [_f64p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                                           ctypes.c_uint32, ctypes.c_int, _u32p, ctypes.c_size_t]
+        lib.ref_decode.argtypes = [ctypes.c_uint32] * 4 + [_u32p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                                           _f64p]
         self.lib = lib
 
     def _check(self, rc):
@@ -302,6 +307,22 @@ class Reference:
         w = ctypes.c_size_t()
         self._check(self.lib.ref_synthetic_op(n, l, alpha, db, level, op.encode(), seed, rot, out, cap, ctypes.byref(w)))
         return out[: w.value].copy()
+
+    def encode(self, n, l, alpha, db, slots, num, den, level, p_extend=False):
+        """reference encode (ckks.cpp:278-319) -> canonical plaintext rows"""
+        z = np.asarray(slots, np.complex128)
+        flat = np.ascontiguousarray(np.stack([z.real, z.imag], -1).reshape(-1))
+        rows = level + (alpha if p_extend else 0)
+        out = np.zeros(rows * n, np.uint32)
+        self._check(self.lib.ref_encode(n, l, alpha, db, flat, len(z), num, den, level, int(p_extend), out, out.size))
+        return out.reshape(rows, n)
+
+    def decode(self, n, l, alpha, db, rows, level, num, den):
+        """reference decode (ckks.cpp:321-362) of canonical evaluation-domain rows"""
+        out = np.zeros(n, np.float64)
+        self._check(self.lib.ref_decode(n, l, alpha, db, np.ascontiguousarray(rows[:level], np.uint32), level,
+                                        num, den, out))
+        return out[0::2] + 1j * out[1::2]
 
     def mechanism_bench(self, op, n, l, alpha, db, level, reps, warmup, seed=42):
         med, mn = ctypes.c_double(), ctypes.c_double()

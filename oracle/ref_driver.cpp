@@ -341,4 +341,46 @@ int ref_mechanism_bench(const char* op, uint32_t n, uint32_t l, uint32_t alpha, 
   }
 }
 
+// encode (ckks.cpp:278-319) of `count` complex slots (re, im interleaved) at
+// scale num/den; writes the plaintext rows as canonical residues.
+int ref_encode(uint32_t n, uint32_t l, uint32_t alpha, uint32_t db, const double* slots, uint32_t count,
+               uint64_t num, uint64_t den, uint32_t level, int p_extend, uint32_t* out, size_t cap) {
+  try {
+    CkksContext ctx(make_params(n, l, alpha, db, false));
+    std::vector<std::complex<double>> z(count);
+    for (uint32_t t = 0; t < count; ++t) z[t] = {slots[2 * t], slots[2 * t + 1]};
+    const Rational scale = Rational(BigInt(num)) / Rational(BigInt(den));
+    Plaintext pt = encode(ctx, z, scale, level, p_extend != 0);
+    put_canonical(pt.poly, out, 0, cap);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// decode (ckks.cpp:321-362) of plaintext rows given as canonical residues
+// (evaluation domain, Montgomery); writes n/2 complex slots.
+int ref_decode(uint32_t n, uint32_t l, uint32_t alpha, uint32_t db, const uint32_t* rows, uint32_t level,
+               uint64_t num, uint64_t den, double* out) {
+  try {
+    CkksContext ctx(make_params(n, l, alpha, db, false));
+    Plaintext pt;
+    pt.scale = Rational(BigInt(num)) / Rational(BigInt(den));
+    pt.level = level;
+    pt.poly = Polynomial(ctx.basis(), level, 0, Domain::Evaluation, true, &ctx.pool());
+    for (uint32_t i = 0; i < level; ++i)
+      for (uint32_t k = 0; k < n; ++k) pt.poly.row(i)[k] = static_cast<int32_t>(rows[static_cast<size_t>(i) * n + k]);
+    const auto z = decode(ctx, pt);
+    for (uint32_t t = 0; t < n / 2; ++t) {
+      out[2 * t] = z[t].real();
+      out[2 * t + 1] = z[t].imag();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 }  // extern "C"

@@ -70,6 +70,8 @@ _SIGS = {
     "ck_hoisted_rotations": [_vp, _u32, _vp, _u32, ctypes.POINTER(_i64), ctypes.POINTER(_vp), _vp, _vp],
     "ck_hoisted_rotate_accumulate": [_vp, _u32, _vp, _u32, ctypes.POINTER(_i64), ctypes.POINTER(_vp),
                                      ctypes.POINTER(_vp), _vp, _vp],
+    "ck_encode": [_vp, _vp, _u32, ctypes.c_double, _u32, ctypes.c_int, _vp, _vp],
+    "ck_decode": [_vp, _vp, _u32, ctypes.c_double, _vp, _vp],
     "ck_shard_create": [_vp, _u32, _u32, ctypes.POINTER(_vp)],
     "ck_shard_destroy": [_vp],
     "ck_shard_layout": [_vp, _u32, _u32p],

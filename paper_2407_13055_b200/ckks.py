@@ -15,6 +15,7 @@ streamed once.
 from __future__ import annotations
 
 import ctypes
+import math
 from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import List, Optional, Sequence, Tuple
@@ -397,6 +398,51 @@ def hoisted_rotate_accumulate(ctx: CkksContext, ct_in: Ciphertext, rotations: Se
     nat.call("ck_hoisted_rotate_accumulate", ctx.handle, l, _ptr(ct.data), cnt, rots, pp, kp, _ptr(out),
              ctx.stream())
     return Ciphertext(out, ct.scale * pts[0].scale, l, False)
+
+
+# --------------------------------------------------------------- encoding --
+def log2_rational(r: Fraction) -> float:
+    """ckks.cpp:140-158, operation for operation (52-bit mantissa window)."""
+    num, den = r.numerator, r.denominator
+    if num <= 0:
+        raise ValueError("log2 of non-positive rational")
+    bn, bd = num.bit_length() - 1, den.bit_length() - 1
+    shift = 0
+    if bn > 52:
+        num >>= bn - 52
+        shift += bn - 52
+    if bd > 52:
+        den >>= bd - 52
+        shift -= bd - 52
+    return float(shift) + math.log2(float(num) / float(den))
+
+
+def encode(ctx: CkksContext, slots, scale: Fraction, level: int, p_extend: bool = False) -> Plaintext:
+    """encode (ckks.cpp:278-319) on the GPU: slot scatter, the reference's
+    radix-2 IDFT, psi^-k twist, rounding and RNS reduction, forward NTT."""
+    z = torch.as_tensor(np.asarray(slots, dtype=np.complex128) if not torch.is_tensor(slots) else slots)
+    if z.numel() > ctx.n // 2:
+        raise ValueError("too many slots")
+    if level < 1 or level > ctx.params.l:
+        raise ValueError("level out of range")
+    if scale <= 0 or log2_rational(Fraction(scale)) > 60.0:
+        raise ValueError("scale out of the representable range")
+    zr = torch.view_as_real(z.to(torch.complex128).reshape(-1)).contiguous().to(ctx.device)
+    rows = level + (ctx.params.alpha if p_extend else 0)
+    out = ctx.empty(rows, ctx.n)
+    nat.call("ck_encode", ctx.handle, ctypes.c_void_p(zr.data_ptr() if zr.numel() else 0), z.numel(),
+             ctypes.c_double(log2_rational(Fraction(scale))), level, int(p_extend), _ptr(out), ctx.stream())
+    return Plaintext(Polynomial(out, level, ctx.params.alpha if p_extend else 0), Fraction(scale), level)
+
+
+def decode(ctx: CkksContext, pt: Plaintext) -> np.ndarray:
+    """decode (ckks.cpp:321-362) on the GPU -> n/2 complex slots (numpy)."""
+    _check_eval_mont(pt.poly, "decode")
+    out = torch.empty(ctx.n, dtype=torch.float64, device=ctx.device)
+    nat.call("ck_decode", ctx.handle, _ptr(pt.poly.data), pt.level, ctypes.c_double(log2_rational(pt.scale)),
+             _ptr(out), ctx.stream())
+    h = out.cpu().numpy()
+    return h[0::2] + 1j * h[1::2]
 
 
 # ----------------------------------------------------------- kernel level --

@@ -12,6 +12,8 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
+#include <complex>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -201,6 +203,81 @@ inline Ciphertext hadd(CkksContext& ctx, const Ciphertext& x, const Ciphertext& 
   Ciphertext out = make_ciphertext(ctx, x.level, x.scale);
   out.pending_rescale = x.pending_rescale;
   check(ck_hadd(ctx.raw(), x.level, 1, x.data.data(), y.data.data(), out.data.data(), nullptr));
+  return out;
+}
+
+struct Plaintext {  // ckks.hpp:56-59; data = [level (+alpha)][n], evaluation domain, Montgomery
+  DeviceBuffer data;
+  Scale scale;
+  uint32_t level = 0;
+  uint32_t p_count = 0;
+};
+
+// log2 of the ledger value; exact for power-of-two scales (the encode path is
+// bit-identical to the reference there, ckks.cpp:297-299)
+inline double scale_log2(const Scale& s) {
+  double v = s.pow2;
+  for (uint32_t a : s.num) v += std::log2((double)a);
+  for (uint32_t b : s.den) v -= std::log2((double)b);
+  return v;
+}
+
+// encode (ckks.cpp:278-319): host slots -> device plaintext
+inline Plaintext encode(CkksContext& ctx, const std::vector<std::complex<double>>& slots, const Scale& scale,
+                        uint32_t level, bool p_extend = false) {
+  const uint32_t n = ctx.params().n;
+  if (slots.size() > n / 2) throw std::invalid_argument("too many slots");
+  if (level < 1 || level > ctx.params().l) throw std::invalid_argument("level out of range");
+  const uint32_t pc = p_extend ? ctx.params().alpha : 0;
+  Plaintext pt{DeviceBuffer(ctx.raw(), (size_t)(level + pc) * n), scale, level, pc};
+  void* dz = nullptr;
+  const size_t bytes = std::max<size_t>(slots.size(), 1) * 16;
+  check(ck_malloc(ctx.raw(), bytes, &dz));
+  try {
+    if (!slots.empty()) check(ck_memcpy_h2d(ctx.raw(), dz, slots.data(), slots.size() * 16, nullptr));
+    check(ck_encode(ctx.raw(), static_cast<const double*>(dz), (uint32_t)slots.size(), scale_log2(scale), level,
+                    p_extend ? 1 : 0, pt.data.data(), nullptr));
+    check(ck_stream_sync(ctx.raw(), nullptr));
+  } catch (...) {
+    ck_free(ctx.raw(), dz);
+    throw;
+  }
+  check(ck_free(ctx.raw(), dz));
+  return pt;
+}
+
+// decode (ckks.cpp:321-362): device plaintext -> n/2 host slots
+inline std::vector<std::complex<double>> decode(CkksContext& ctx, const Plaintext& pt) {
+  const uint32_t n = ctx.params().n;
+  void* dz = nullptr;
+  check(ck_malloc(ctx.raw(), (size_t)n / 2 * 16, &dz));
+  std::vector<std::complex<double>> out(n / 2);
+  try {
+    check(ck_decode(ctx.raw(), pt.data.data(), pt.level, scale_log2(pt.scale), static_cast<double*>(dz), nullptr));
+    check(ck_memcpy_d2h(ctx.raw(), out.data(), dz, out.size() * 16, nullptr));
+    check(ck_stream_sync(ctx.raw(), nullptr));
+  } catch (...) {
+    ck_free(ctx.raw(), dz);
+    throw;
+  }
+  check(ck_free(ctx.raw(), dz));
+  return out;
+}
+
+inline Ciphertext pmult(CkksContext& ctx, const Ciphertext& ct, const Plaintext& pt) {  // ckks.cpp:586-600
+  if (ct.level != pt.level || pt.p_count != 0) throw std::invalid_argument("level mismatch");
+  Ciphertext out = make_ciphertext(ctx, ct.level, ct.scale * pt.scale);
+  out.pending_rescale = ct.pending_rescale;
+  check(ck_pmult(ctx.raw(), ct.level, 1, ct.data.data(), pt.data.data(), out.data.data(), nullptr));
+  return out;
+}
+
+inline Ciphertext padd(CkksContext& ctx, const Ciphertext& ct, const Plaintext& pt) {  // ckks.cpp:573-584
+  if (ct.level != pt.level || pt.p_count != 0) throw std::invalid_argument("level mismatch");
+  if (!(ct.scale == pt.scale)) throw std::invalid_argument("scale mismatch beyond tolerance");
+  Ciphertext out = make_ciphertext(ctx, ct.level, ct.scale);
+  out.pending_rescale = ct.pending_rescale;
+  check(ck_padd(ctx.raw(), ct.level, 1, ct.data.data(), pt.data.data(), out.data.data(), nullptr));
   return out;
 }
 

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -361,9 +362,77 @@ struct Context {
     }
   };
 
+  // encode / decode tables (encode.cu), built on first use
+  double2 *d_fft_fwd = nullptr, *d_fft_inv = nullptr, *d_twist_enc = nullptr, *d_twist_dec = nullptr;
+  uint32_t* d_jidx = nullptr;
+  std::map<uint32_t, CrtConst> crt_consts;  // prefix length -> CRT constants
+
+  // Host tables restating ckks.cpp:63-99 and :301-303, :346: per-stage FFT
+  // twiddles with the reference's recurrence (w *= wl, std::complex<double>,
+  // host-compiled like the reference so every value is bit-identical), the
+  // encode twist psi^-k, the decode twist psi^k, and the slot order 5^t.
+  void enc_tables() {
+    if (d_jidx) return;
+    const uint32_t nn = n;
+    std::vector<double2> tw[2] = {std::vector<double2>(nn - 1), std::vector<double2>(nn - 1)};
+    for (int inv = 0; inv < 2; ++inv)
+      for (uint32_t len = 2; len <= nn; len <<= 1) {
+        const double ang = (inv ? -2.0 : 2.0) * M_PI / static_cast<double>(len);
+        const std::complex<double> wl(std::cos(ang), std::sin(ang));
+        std::complex<double> w(1.0, 0.0);
+        for (uint32_t j = 0; j < len / 2; ++j) {
+          tw[inv][len / 2 - 1 + j] = make_double2(w.real(), w.imag());
+          w *= wl;
+        }
+      }
+    std::vector<double2> te(nn), td(nn);
+    const double ange = -M_PI / static_cast<double>(nn);
+    for (uint32_t k = 0; k < nn; ++k) {
+      te[k] = make_double2(std::cos(ange * k), std::sin(ange * k));
+      const double angd = M_PI * k / static_cast<double>(nn);
+      td[k] = make_double2(std::cos(angd), std::sin(angd));
+    }
+    std::vector<uint32_t> jidx(nn / 2);
+    uint64_t g = 1;
+    for (uint32_t t = 0; t < nn / 2; ++t) {
+      jidx[t] = static_cast<uint32_t>((g - 1) / 2);
+      g = g * 5 % (2ull * nn);
+    }
+    auto up = [](auto& v, auto*& d) {
+      CK_CUDA(cudaMalloc(&d, sizeof(v[0]) * std::max<size_t>(v.size(), 1)));
+      CK_CUDA(cudaMemcpy(d, v.data(), sizeof(v[0]) * v.size(), cudaMemcpyHostToDevice));
+    };
+    up(tw[0], d_fft_fwd);
+    up(tw[1], d_fft_inv);
+    up(te, d_twist_enc);
+    up(td, d_twist_dec);
+    up(jidx, d_jidx);
+  }
+  const CrtConst& crt_const(uint32_t cnt) {
+    auto it = crt_consts.find(cnt);
+    if (it != crt_consts.end()) return it->second;
+    CrtConst cc;
+    cc.c = (int)cnt;
+    unsigned __int128 M = 1;
+    for (uint32_t i = 0; i < cnt; ++i) M *= q(i);
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const unsigned __int128 Mi = M / q(i);
+      cc.q[i] = q(i);
+      cc.y[i] = invm((uint32_t)(Mi % q(i)), q(i));
+      cc.mi_lo[i] = (uint64_t)Mi;
+      cc.mi_hi[i] = (uint64_t)(Mi >> 64);
+    }
+    cc.m_lo = (uint64_t)M;
+    cc.m_hi = (uint64_t)(M >> 64);
+    return crt_consts.emplace(cnt, cc).first->second;
+  }
+
   ~Context() {
     cudaSetDevice(device);
     cudaDeviceSynchronize();
+    for (auto* d : {d_fft_fwd, d_fft_inv, d_twist_enc, d_twist_dec})
+      if (d) cudaFree(d);
+    if (d_jidx) cudaFree(d_jidx);
     for (auto& kv : rot_maps) cudaFree(kv.second);
     if (d_primes) cudaFree(d_primes);
     if (d_fwd) cudaFree(d_fwd);
@@ -1908,6 +1977,73 @@ ck_status ck_padd(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_
 ck_status ck_pmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, const uint32_t* pt,
                    uint32_t* out, ck_stream stream) {
   return ct_ew(ctx, 2, level, batch, ct, pt, true, false, out, stream);
+}
+
+ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, double scale_log2, uint32_t level,
+                    int p_extend, uint32_t* out_dev, ck_stream stream) {
+  ck_status st0 = guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(out_dev);
+    if (count > c->n / 2) throw InvalidArgument("too many slots");  // ckks.cpp:281-285
+    if (count && !slots_dev) throw InvalidArgument("null slot pointer");
+    if (!(scale_log2 <= 60.0)) throw InvalidArgument("scale out of the representable range");
+    c->enc_tables();
+    cudaStream_t st = S(stream);
+    const uint32_t rows = level + (p_extend ? c->alpha : 0);
+    const size_t N = c->n;
+    char* base = static_cast<char*>(c->scratch_get(2 * N * sizeof(double2) + 4 * rows + 16, st));
+    double2* a = reinterpret_cast<double2*>(base);
+    uint32_t* rq = reinterpret_cast<uint32_t*>(base + 2 * N * sizeof(double2));
+    std::vector<uint32_t> hq(rows);
+    for (uint32_t i = 0; i < rows; ++i) hq[i] = c->q(c->gidx(level, i));
+    CK_CUDA(cudaMemcpyAsync(rq, hq.data(), 4 * rows, cudaMemcpyHostToDevice, st));
+    enc_scatter((int)N, reinterpret_cast<const double2*>(slots_dev), (int)count, c->d_jidx, a, st);
+    fft_pow2_dev((int)c->logn, a, a + N, c->d_fft_inv, st);  // IDFT (1/n folded into enc_round)
+    enc_round((int)N, a + N, c->d_twist_enc, std::exp2(scale_log2), (int)rows, rq, out_dev, st);
+    CK_CUDA(cudaStreamSynchronize(st));  // hq is pageable host memory
+    c->launches += 4 + (c->logn > 12 ? c->logn - 12 : 0);
+  });
+  if (st0 != CK_OK) return st0;
+  // coefficient (plain) -> evaluation (Montgomery), as ntt_forward does (ckks.cpp:316)
+  Context* c = C(ctx);
+  std::vector<uint32_t> g(level + (p_extend ? c->alpha : 0));
+  for (uint32_t i = 0; i < g.size(); ++i) g[i] = c->gidx(level, i);
+  return ck_ntt_forward(ctx, out_dev, (uint32_t)g.size(), g.data(), stream);
+}
+
+ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2, double* slots_dev,
+                    ck_stream stream) {
+  return guard([&] {
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(pt_dev);
+    check_ptr(slots_dev);
+    // minimal Q prefix whose product dominates the scale with 40 bits of headroom (ckks.cpp:325-332)
+    const double need_bits = scale_log2 + 40.0;
+    uint32_t cnt = 1;
+    double bits = std::log2(static_cast<double>(c->q(0)));
+    while (cnt < level && bits < need_bits) {
+      bits += std::log2(static_cast<double>(c->q(cnt)));
+      ++cnt;
+    }
+    if (cnt > 4) throw InvalidArgument("decode: CRT lift over more than 4 primes is not supported");
+    c->enc_tables();
+    cudaStream_t st = S(stream);
+    const size_t N = c->n;
+    char* base = static_cast<char*>(c->scratch_get(2 * N * sizeof(double2) + 4 * N * cnt, st));
+    double2* a = reinterpret_cast<double2*>(base);
+    uint32_t* rows = reinterpret_cast<uint32_t*>(base + 2 * N * sizeof(double2));
+    CK_CUDA(cudaMemcpyAsync(rows, pt_dev, 4 * N * cnt, cudaMemcpyDeviceToDevice, st));
+    std::vector<uint32_t> g(cnt);
+    for (uint32_t i = 0; i < cnt; ++i) g[i] = i;
+    const ck_status si = ck_intt_inverse(ctx, rows, cnt, g.data(), nullptr, stream);
+    if (si != CK_OK) throw std::runtime_error(ck_last_error());
+    dec_crt((int)N, rows, c->crt_const(cnt), c->d_twist_dec, std::exp2(-scale_log2), a, st);
+    fft_pow2_dev((int)c->logn, a, a + N, c->d_fft_fwd, st);
+    dec_gather((int)N, a + N, c->d_jidx, reinterpret_cast<double2*>(slots_dev), st);
+    c->launches += 3 + (c->logn > 12 ? c->logn - 12 : 0);
+  });
 }
 
 ck_status ck_hoisted_rotations(ck_context* ctx, uint32_t level, const uint32_t* ct, uint32_t count,

@@ -91,6 +91,25 @@ struct BconvTc {
 bool bconv_tc_supported(int n, int max_sc, int max_dc);
 void bconv_tc(int n, const BconvLaunch& a, const BconvTc& t, cudaStream_t st);
 
+// CKKS encode / decode (encode.cu, ckks.cpp:278-362)
+struct CrtConst {  // CRT lift over the first c <= 4 primes (128-bit)
+  int c = 0;
+  uint32_t q[4] = {1, 1, 1, 1};
+  uint64_t y[4] = {0, 0, 0, 0};            // (M / q_i)^-1 mod q_i
+  uint64_t mi_lo[4] = {0, 0, 0, 0}, mi_hi[4] = {0, 0, 0, 0};  // M / q_i
+  uint64_t m_lo = 0, m_hi = 0;             // M
+};
+// reference fft_pow2 (ckks.cpp:63-87) on n = 2^logn points: src gathered in
+// bit-reversed order, result in dst; tw = per-stage twiddles (stage len at
+// offset len/2 - 1), built by the host with the reference's recurrence
+void fft_pow2_dev(int logn, const double2* src, double2* dst, const double2* tw, cudaStream_t st);
+void enc_scatter(int n, const double2* slots, int count, const uint32_t* jidx, double2* a, cudaStream_t st);
+void enc_round(int n, const double2* a, const double2* twist, double scale, int rows, const uint32_t* row_q,
+               uint32_t* out, cudaStream_t st);
+void dec_crt(int n, const uint32_t* rows, const CrtConst& cc, const double2* twist, double inv_scale, double2* a,
+             cudaStream_t st);
+void dec_gather(int n, const double2* a, const uint32_t* jidx, double2* out, cudaStream_t st);
+
 // tensor product of two ciphertexts (ckks.cpp:818-821): d0 = b b', d1 = b a' + a b', d2 = a a'
 void tensor(int n, int level, int batch, const uint32_t* x, const uint32_t* y, uint64_t ct_bs, uint32_t* d01,
             uint64_t d01_bs, uint32_t* d2, uint64_t d2_bs, const PrimeDev* primes, cudaStream_t st);

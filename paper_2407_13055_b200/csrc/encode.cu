@@ -1,0 +1,172 @@
+// CKKS encode / decode on the GPU, restating
+// ckks.cpp:278-362 of the reference:
+//
+//   encode: slots -> a[jidx[t]] = z_t, a[n-1-jidx[t]] = conj(z_t)       (scatter)
+//           a = IDFT(a) by fft_pow2(invert) (ckks.cpp:63-87)             (FFT)
+//           m_k = llround(Re(a_k * psi^-k) * scale)  mod every q_i       (round + reduce)
+//           -> forward NTT (entry merge) in the caller                   (plaintext rows)
+//   decode: INTT of the first c rows (caller) -> CRT lift of c <= 4 primes
+//           (128-bit), centre, / scale -> a_k = coeff * (cos, sin)(pi k / n)
+//           -> fft_pow2(forward) -> out[t] = a[jidx[t]]
+//
+// The FFT reproduces the reference's radix-2 iterative transform operation by
+// operation: the same bit-reversed order, the same per-stage twiddle values
+// (the host builds them with the reference's recurrence w *= wl in double),
+// and complex products / sums rounded exactly as libstdc++ evaluates them
+// (x86-64, no FMA): every product and sum below uses the _rn intrinsics so the
+// compiler cannot contract them into FMAs.  With a power-of-two scale the
+// encoded residues are therefore bit-identical to the reference's.
+#include <algorithm>
+
+#include "ck_common.cuh"
+#include "ck_kernels.h"
+
+namespace ck {
+namespace {
+
+constexpr int kFftBlock = 4096;  // elements per shared-memory FFT block (64 KB)
+constexpr int kFftThreads = 512;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 w) {  // (a.x w.x - a.y w.y, a.x w.y + a.y w.x)
+  return make_double2(__dsub_rn(__dmul_rn(a.x, w.x), __dmul_rn(a.y, w.y)),
+                      __dadd_rn(__dmul_rn(a.x, w.y), __dmul_rn(a.y, w.x)));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+
+__device__ __forceinline__ uint32_t brev(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
+
+// stages len = 2 .. B of one B-element block, input gathered in bit-reversed order
+__global__ void __launch_bounds__(kFftThreads) k_fft_first(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                           const double2* __restrict__ tw, int logn, int B) {
+  extern __shared__ double2 sa[];
+  const int base = blockIdx.x * B;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) sa[i] = src[brev((uint32_t)(base + i), logn)];
+  __syncthreads();
+  for (int len = 2; len <= B; len <<= 1) {
+    const int half = len >> 1;
+    const double2* w = tw + (half - 1);
+    for (int b = threadIdx.x; b < B / 2; b += blockDim.x) {
+      const int i = (b / half) * len, j = b % half;
+      const double2 u = sa[i + j];
+      const double2 v = cmul(sa[i + j + half], w[j]);
+      sa[i + j] = cadd(u, v);
+      sa[i + j + half] = csub(u, v);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < B; i += blockDim.x) dst[base + i] = sa[i];
+}
+
+// one radix-2 stage of length len, in place
+__global__ void k_fft_stage(double2* __restrict__ a, const double2* __restrict__ tw, int n, int len) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n / 2) return;
+  const int half = len >> 1;
+  const int i = (b / half) * len, j = b % half;
+  const double2 u = a[i + j];
+  const double2 v = cmul(a[i + j + half], tw[(half - 1) + j]);
+  a[i + j] = cadd(u, v);
+  a[i + j + half] = csub(u, v);
+}
+
+__global__ void k_enc_scatter(int n, const double2* __restrict__ slots, int count, const uint32_t* __restrict__ jidx,
+                              double2* __restrict__ a) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const double2 z = slots[t];
+  const uint32_t j = jidx[t];
+  a[j] = z;
+  a[n - 1 - j] = make_double2(z.x, -z.y);
+}
+
+// m_k = llround((Re(a_k tw_k) / n) * scale), then canonical m mod q for every row
+__global__ void k_enc_round(int n, const double2* __restrict__ a, const double2* __restrict__ twist, double inv_n,
+                            double scale, int rows, const uint32_t* __restrict__ row_q, uint32_t* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double2 x = a[k], t = twist[k];
+  const double re = __dsub_rn(__dmul_rn(x.x, t.x), __dmul_rn(x.y, t.y));
+  const long long m = llround(__dmul_rn(__dmul_rn(re, inv_n), scale));
+  for (int i = 0; i < rows; ++i) {
+    const long long q = row_q[i];
+    long long r = m % q;  // correct() of modarith.hpp:46-50
+    if (r < 0) r += q;
+    out[(size_t)i * n + k] = (uint32_t)r;
+  }
+}
+
+// correctly rounded conversion of a 128-bit magnitude to double
+__device__ __forceinline__ double u128_to_double(unsigned __int128 v) {
+  const uint64_t hi = (uint64_t)(v >> 64);
+  if (hi == 0) return __ull2double_rn((uint64_t)v);
+  const int sh = 64 - __clzll(hi);  // bits above the low 64
+  const unsigned __int128 mask = (((unsigned __int128)1) << sh) - 1;
+  uint64_t t = (uint64_t)(v >> sh);
+  if ((v & mask) != 0) t |= 1;  // sticky below the 53-bit rounding point (t has 64 significant bits)
+  return ldexp(__ull2double_rn(t), sh);
+}
+
+__global__ void k_dec_crt(int n, const uint32_t* __restrict__ rows, CrtConst cc, const double2* __restrict__ twist,
+                          double inv_scale, double2* __restrict__ a) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  unsigned __int128 v = 0;
+  for (int i = 0; i < cc.c; ++i) {
+    const uint32_t r = rows[(size_t)i * n + k];
+    const uint64_t t = (uint64_t)r * cc.y[i] % cc.q[i];  // (r * (M/q_i)^-1) mod q_i
+    const unsigned __int128 Mi = ((unsigned __int128)cc.mi_hi[i] << 64) | cc.mi_lo[i];
+    v += Mi * t;  // < M each, sum < 4M < 2^128
+  }
+  const unsigned __int128 M = ((unsigned __int128)cc.m_hi << 64) | cc.m_lo;
+  while (v >= M) v -= M;
+  double coeff;
+  if (v > (M >> 1)) coeff = -u128_to_double(M - v);  // centred lift (ckks.cpp:344)
+  else coeff = u128_to_double(v);
+  coeff = __dmul_rn(coeff, inv_scale);
+  const double2 t = twist[k];
+  a[k] = make_double2(__dmul_rn(coeff, t.x), __dmul_rn(coeff, t.y));
+}
+
+__global__ void k_dec_gather(int n, const double2* __restrict__ a, const uint32_t* __restrict__ jidx,
+                             double2* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n / 2) out[t] = a[jidx[t]];
+}
+
+inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+void fft_pow2_dev(int logn, const double2* src, double2* dst, const double2* tw, cudaStream_t st) {
+  const int n = 1 << logn;
+  const int B = std::min(n, kFftBlock);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_first, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftBlock * (int)sizeof(double2));
+    attr = true;
+  }
+  k_fft_first<<<n / B, std::min(kFftThreads, std::max(32, B / 2)), B * sizeof(double2), st>>>(src, dst, tw, logn, B);
+  for (int len = 2 * B; len <= n; len <<= 1) k_fft_stage<<<cdiv(n / 2, 256), 256, 0, st>>>(dst, tw, n, len);
+}
+
+void enc_scatter(int n, const double2* slots, int count, const uint32_t* jidx, double2* a, cudaStream_t st) {
+  cudaMemsetAsync(a, 0, sizeof(double2) * n, st);
+  if (count) k_enc_scatter<<<cdiv(count, 256), 256, 0, st>>>(n, slots, count, jidx, a);
+}
+
+void enc_round(int n, const double2* a, const double2* twist, double scale, int rows, const uint32_t* row_q,
+               uint32_t* out, cudaStream_t st) {
+  k_enc_round<<<cdiv(n, 256), 256, 0, st>>>(n, a, twist, 1.0 / n, scale, rows, row_q, out);
+}
+
+void dec_crt(int n, const uint32_t* rows, const CrtConst& cc, const double2* twist, double inv_scale, double2* a,
+             cudaStream_t st) {
+  k_dec_crt<<<cdiv(n, 256), 256, 0, st>>>(n, rows, cc, twist, inv_scale, a);
+}
+
+void dec_gather(int n, const double2* a, const uint32_t* jidx, double2* out, cudaStream_t st) {
+  k_dec_gather<<<cdiv(n / 2, 256), 256, 0, st>>>(n, a, jidx, out);
+}
+
+}  // namespace ck

@@ -7,6 +7,8 @@
 //   test_cpp_api <dir> <n> <l> <alpha> <level>
 // <dir>/x.bin, y.bin: [2][level][n] u32; evk.bin: [D][2][L+alpha][n] u32
 // writes <dir>/out_hmult.bin, out_hrot.bin
+#include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -73,6 +75,21 @@ int main(int argc, char** argv) {
     hrot(ctx, x, 2, rot);
     ++errors;
   } catch (const std::invalid_argument&) {
+  }
+  {  // encode -> decode round trip through the mirror (ckks.cpp:278-362)
+    std::vector<std::complex<double>> z(p.n / 2);
+    for (size_t t = 0; t < z.size(); ++t) z[t] = {std::sin(0.1 * t), std::cos(0.37 * t)};
+    Plaintext pt = encode(ctx, z, ctx.default_scale(), level);
+    const auto back = decode(ctx, pt);
+    double err = 0;
+    for (size_t t = 0; t < z.size(); ++t) err = std::max(err, std::abs(back[t] - z[t]));
+    if (!(err < 1e-9)) throw std::runtime_error("encode/decode round trip error");
+    try {  // too many slots (ckks.cpp:281)
+      z.resize(p.n / 2 + 1);
+      encode(ctx, z, ctx.default_scale(), level);
+      ++errors;
+    } catch (const std::invalid_argument&) {
+    }
   }
   const uint64_t n_launch = ck_launch_count(ctx.raw());
   std::printf("cpp api ok: hmult level %u -> %u, hrot level %u, %llu kernel launches, %d contract errors\n", level,

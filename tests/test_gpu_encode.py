@@ -1,0 +1,87 @@
+"""GPU encode / decode (ckks.cpp:278-362) against the
+reference itself (oracle/_ref, built read-only from /root/reference).
+
+* encode at a power-of-two scale: plaintext residues bit-identical to the
+  reference (the FFT replays the reference's operation order and twiddles);
+* decode: slots within 2^-40 of the reference's decode of the same plaintext
+  (floating-point output; the only freedom is the Rational->double rounding);
+* round trip and the reference's argument errors."""
+from __future__ import annotations
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2407_13055_b200 import ckks  # noqa: E402
+from pyoracle import Reference  # noqa: E402
+
+_CTX = {}
+
+
+def ctx_for(n, l, a, db=55):
+    if (n, l, a, db) not in _CTX:
+        _CTX[(n, l, a, db)] = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db))
+    return _CTX[(n, l, a, db)]
+
+
+def unit_slots(count, seed):  # bench.cpp:305-311 distribution
+    r = np.random.default_rng(seed).uniform(-1.0, 1.0, (count, 2))
+    return r[:, 0] + 1j * r[:, 1]
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not Reference.available:
+        pytest.skip("reference build (oracle/_ref) absent")
+    return Reference()
+
+
+@pytest.mark.parametrize("n,l,a,level,count,p_extend", [
+    (1024, 8, 3, 8, 512, False), (1024, 8, 3, 5, 100, True), (1024, 8, 3, 1, 0, False),
+    (65536, 24, 8, 24, 32768, False), (65536, 24, 8, 13, 32768, True), (8, 4, 2, 4, 4, False)])
+def test_encode_bit_exact_vs_reference(ref, n, l, a, level, count, p_extend):
+    C = ctx_for(n, l, a)
+    z = unit_slots(count, 1000 + n + level)
+    for bits in (55, 40):
+        want = ref.encode(n, l, a, 55, z, 1 << bits, 1, level, p_extend)
+        pt = ckks.encode(C, z, Fraction(1 << bits), level, p_extend)
+        got = pt.poly.data.cpu().numpy().astype(np.uint32)
+        np.testing.assert_array_equal(got, want)
+        assert pt.poly.q_count == level and pt.poly.p_count == (a if p_extend else 0)
+
+
+@pytest.mark.parametrize("n,l,a,level", [(1024, 8, 3, 8), (65536, 24, 8, 24), (65536, 24, 8, 3)])
+def test_decode_matches_reference(ref, n, l, a, level):
+    C = ctx_for(n, l, a)
+    z = unit_slots(n // 2, 7 + n)
+    rows = ref.encode(n, l, a, 55, z, 1 << 55, 1, level)
+    want = ref.decode(n, l, a, 55, rows, level, 1 << 55, 1)
+    pt = ckks.Plaintext(ckks.Polynomial(torch.from_numpy(rows.astype(np.int64).astype(np.int32)).cuda(), level, 0),
+                        Fraction(1 << 55), level)
+    got = ckks.decode(C, pt)
+    err = np.abs(got - want).max()
+    assert err <= 2.0 ** -40, err
+    assert np.abs(got - z).max() < 2.0 ** -30
+
+
+def test_round_trip_non_power_of_two_scale():
+    n, l, a = 65536, 24, 8
+    C = ctx_for(n, l, a)
+    z = unit_slots(n // 2, 99)
+    scale = Fraction(3 << 53, 5)
+    back = ckks.decode(C, ckks.encode(C, z, scale, 24))
+    assert np.abs(back - z).max() < 2.0 ** -30
+
+
+def test_encode_errors_mirror_reference():
+    C = ctx_for(1024, 8, 3)
+    with pytest.raises(ValueError):
+        ckks.encode(C, unit_slots(513, 1), Fraction(1 << 55), 8)  # too many slots (ckks.cpp:281)
+    with pytest.raises(ValueError):
+        ckks.encode(C, unit_slots(4, 1), Fraction(1 << 55), 9)  # level out of range (ckks.cpp:282-283)
+    with pytest.raises(ValueError):
+        ckks.encode(C, unit_slots(4, 1), Fraction(1 << 61), 8)  # scale out of range (ckks.cpp:284-285)
