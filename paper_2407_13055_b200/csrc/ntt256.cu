@@ -66,6 +66,51 @@ __device__ __forceinline__ void gs4(uint4& x, uint4& y, uint2 w, uint32_t q, uin
   gs(x.w, y.w, w.x, w.y, q, q2);
 }
 
+// Four radix-2 CT stages over v[16] (uint4 lanes: 64 butterflies per stage),
+// stage t pairing rows at distance 8 >> t with twiddle tw(t, blk).  The
+// butterflies of a stage are issued in two groups of 16 with the three
+// multiplies of every butterfly in separate passes (all IMAD.HI, then all
+// q * hi, then all y * w - q * hi), so 16 independent multiplies sit between
+// dependent ones instead of 4 (the `wait` stall of the per-butterfly order).
+template <int T0, class TWF>
+__device__ __forceinline__ void ct_stages16(uint4 (&v)[16], TWF tw, uint32_t q, uint32_t q2) {
+#pragma unroll
+  for (int t = T0; t < 4; ++t) {
+    const int d = 8 >> t;
+    uint2 w[8];
+#pragma unroll
+    for (int blk = 0; blk < (1 << t); ++blk) w[blk] = tw(t, blk);
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      uint32_t h[16];
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) {
+        const int p = 4 * g + pp, blk = p / d, j = blk * 2 * d + p % d;
+        h[4 * pp + 0] = __umulhi(v[j + d].x, w[blk].y);
+        h[4 * pp + 1] = __umulhi(v[j + d].y, w[blk].y);
+        h[4 * pp + 2] = __umulhi(v[j + d].z, w[blk].y);
+        h[4 * pp + 3] = __umulhi(v[j + d].w, w[blk].y);
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) h[e] *= q;
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) {
+        const int p = 4 * g + pp, blk = p / d, j = blk * 2 * d + p % d;
+        const uint32_t ww = w[blk].x;
+        uint32_t* y = &v[j + d].x;
+        uint32_t* x = &v[j].x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t tt = y[c] * ww - h[4 * pp + c];  // shoup_mul: [0, 2q)
+          const uint32_t xx = sub_if(x[c], q2);
+          x[c] = xx + tt;
+          y[c] = xx - tt + q2;
+        }
+      }
+    }
+  }
+}
+
 // ============================================================ column pass ==
 constexpr int kCT = 128;              // threads: tau = tid>>3 (16), cq = tid&7 (8)
 constexpr int kCCols = 32;            // columns per tile
@@ -151,26 +196,22 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
       // ---- forward, stages 0..7 (r bits 7..0). phase A rows tau + 16 j.
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = B.tile[(tau + 16 * j) * 8 + cq];
+      if (entry) {  // stage 0 with the entry merge x*R, y*psi^{N/2}*R (ntt.cpp:27-35)
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int d = 8 >> t;
-#pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int blk = p / d, j = blk * 2 * d + p % d;
-          if (t == 0 && entry) {  // entry merge x*R, y*psi^{N/2}*R (ntt.cpp:27-35)
+        for (int j = 0; j < 8; ++j) {
 #define CK_E(c)                                                    \
   {                                                                \
     const uint32_t xx = shoup_mul(v[j].c, P.r, P.r_sh, q);         \
-    const uint32_t tt = shoup_mul(v[j + d].c, P.w1r, P.w1r_sh, q); \
+    const uint32_t tt = shoup_mul(v[j + 8].c, P.w1r, P.w1r_sh, q); \
     v[j].c = xx + tt;                                              \
-    v[j + d].c = xx - tt + q2;                                     \
+    v[j + 8].c = xx - tt + q2;                                     \
   }
-            CK_E(x) CK_E(y) CK_E(z) CK_E(w)
+          CK_E(x) CK_E(y) CK_E(z) CK_E(w)
 #undef CK_E
-          } else {
-            ct4(v[j], v[j + d], TW[(1 << t) + blk], q, q2);
-          }
         }
+        ct_stages16<1>(v, [&](int t, int blk) { return TW[(1 << t) + blk]; }, q, q2);
+      } else {
+        ct_stages16<0>(v, [&](int t, int blk) { return TW[(1 << t) + blk]; }, q, q2);
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) B.tile[(tau + 16 * j) * 8 + cq] = v[j];
@@ -190,15 +231,8 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
         cp_commit();
       }
       // phase B rows 16 tau + j: twiddle 2^s + tau 2^(s-4) + blk
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int d = 8 >> t;
-#pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int blk = p / d, j = blk * 2 * d + p % d;
-          ct4(v[j], v[j + d], TWR ? TW[(16 << t) + (tau << t) + blk] : twb[(1 << t) - 1 + blk], q, q2);
-        }
-      }
+      ct_stages16<0>(v, [&](int t, int blk) { return TWR ? TW[(16 << t) + (tau << t) + blk] : twb[(1 << t) - 1 + blk]; },
+                     q, q2);
 #pragma unroll
       for (int j = 0; j < 16; ++j) stg4(out + (16 * tau + j) * kR, v[j]);
     } else {
