@@ -274,6 +274,36 @@ def test_hmult_hrot_oracle_sweep_mid_size(level):
         np.testing.assert_array_equal(got, np.stack([canon(O, ob, level), canon(O, oa, level)]))
 
 
+@pytest.mark.parametrize("level", [54, 41, 28, 15, 4])
+def test_reference_default_params_match_oracle(level):
+    """The reference's default CkksParams (ckks.hpp:46-54: l=54, alpha=14,
+    delta 2^48 -> D=4 digits, a ragged 12-row last digit, 14-wide BConv
+    sources and the 16-row merged ModDown) at N=4096, HMult and HRot vs the
+    oracle, batched over 2 ciphertexts."""
+    n, l, a, db = 4096, 54, 14, 48
+    C = ctx_for(n, l, a, db)
+    O = _oracle(n, l, a, db)
+    xs, ys, want_m, want_r = [], [], [], []
+    evk = None
+    for b in range(2):
+        xb, xa, yb, ya, evk_b = O.synthetic(level, 4242 + 10 * level + b)
+        evk = evk_b if evk is None else evk  # one key for the whole batch
+        xs.append(np.stack([xb, xa]))
+        ys.append(np.stack([yb, ya]))
+        if level >= 4:
+            ob, oa = O.hmult(level, xb, xa, yb, ya, evk)
+            want_m.append(np.stack([canon(O, ob, level - 2), canon(O, oa, level - 2)]))
+        ob, oa = O.hrot(level, xb, xa, 3, evk)
+        want_r.append(np.stack([canon(O, ob, level), canon(O, oa, level)]))
+    K = ckks.EvaluationKey(dev(evk))
+    X = ckks.Ciphertext(dev(np.stack(xs)), Fraction(1 << db), level)
+    Y = ckks.Ciphertext(dev(np.stack(ys)), Fraction(1 << db), level)
+    got = host(ckks.hmult(C, X, Y, K).data)
+    np.testing.assert_array_equal(got, np.stack(want_m))
+    got = host(ckks.hrot(C, X, 3, ckks.EvaluationKey(K.data, ckks.ROTATION, 3)).data)
+    np.testing.assert_array_equal(got, np.stack(want_r))
+
+
 def test_batched_equals_unbatched():
     n, l, a, db = 65536, 24, 8, 55
     C = ctx_for(n, l, a, db)
