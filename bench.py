@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=4, help="ciphertexts per H2D/compute/D2H chunk")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-small", action="store_true", help="skip the B=1 eager / CUDA-graph measurement")
     ap.add_argument("--sweep", action="store_true", help="also report the HRot level sweep (config 2)")
     ap.add_argument("--workload", default="dp", choices=["dp", "limb", "helr"],
                     help="dp: batched independent ciphertexts (configs 1-3, the headline); limb: one ciphertext "
@@ -374,6 +375,38 @@ def main():
                        "back each step (pipeline.HostPipeline: chunks of %d, H2D / compute / D2H on separate "
                        "streams)" % pipe.chunk}
 
+    # ---- single-ciphertext serving (B = 1): eager C-ABI calls vs one CUDA graph replay
+    small = None
+    if not args.no_small:
+        from paper_2407_13055_b200.pipeline import CapturedStep
+
+        X1 = ckks.Ciphertext(X.data[:1].contiguous(), s, LEVEL)
+        Y1 = ckks.Ciphertext(Y.data[:1].contiguous(), s, LEVEL)
+
+        def one():
+            return ckks.hmult(C, X1, Y1, relin).data, ckks.hrot(C, X1, 1, rot).data
+
+        reps = 50
+        for _ in range(3):
+            one()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            one()
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        eager_ms = a.elapsed_time(b) / reps
+        cap = CapturedStep(dev, one)
+        a.record(st)
+        for _ in range(reps):
+            cap.replay()
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        graph_ms = a.elapsed_time(b) / reps
+        small = {"batch": 1, "eager_ops_per_s": round(2 / (eager_ms / 1e3), 1),
+                 "cuda_graph_ops_per_s": round(2 / (graph_ms / 1e3), 1),
+                 "note": "one HMult+relin + one HRot per step on one ciphertext; graph = pipeline.CapturedStep"}
+
     sweep = None
     if args.sweep:
         sweep = {}
@@ -411,6 +444,8 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if small:
+            line["single_ciphertext"] = small
         if sweep:
             line["hrot_level_sweep_ops_per_s"] = sweep
         print(json.dumps(line), flush=True)

@@ -101,3 +101,38 @@ class HostPipeline:
         end = torch.cuda.Event()
         end.record(self.d2h)
         return end
+
+
+class CapturedStep:
+    """A fixed sequence of evaluator calls captured once in a CUDA graph and
+    replayed (small batches / single-ciphertext serving, where the ~1 us
+    GPU-side gap between the ~23 kernels of every mechanism is a large share
+    of the time: +19% ops/s at B = 1, `profiles/round1_session2.md`).
+
+    ``fn()`` must read its inputs from, and return, tensors that stay alive
+    (static buffers): refresh inputs in place (``x.copy_(new)``) between
+    replays.  The native library allocates nothing during the capture as
+    long as ``fn`` ran once before (its per-stream scratch arena is sized by
+    the warm-up), which ``CapturedStep`` does.
+    """
+
+    def __init__(self, device: torch.device, fn: Callable[[], object], warmup: int = 2):
+        self.device = torch.device(device)
+        self.stream = torch.cuda.Stream(self.device)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(self.stream):
+            for _ in range(max(1, warmup)):
+                fn()
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self.outputs = fn()
+
+    def replay(self):
+        """Enqueue one replay on the capture stream (ordered after the caller's
+        current stream) and make the caller's stream wait for it."""
+        cur = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(cur)
+        self.graph.replay()
+        cur.wait_stream(self.stream)
+        return self.outputs

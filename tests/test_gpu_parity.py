@@ -367,6 +367,32 @@ def test_host_pipeline_equals_direct(chunk, depth):
         pipe.run([X.data, hy], fn, [ho1, ho2])  # device tensor where a pinned host one is required
 
 
+def test_captured_step_replays_bit_exactly():
+    """pipeline.CapturedStep: HMult + HRot captured in a CUDA graph, replayed
+    on fresh inputs copied into the static buffers, equals eager calls."""
+    from paper_2407_13055_b200.pipeline import CapturedStep
+
+    n, l, a, db, level = 4096, 24, 8, 55, 24
+    C = ctx_for(n, l, a, db)
+    O = _oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(level, 808)
+    K = ckks.EvaluationKey(dev(evk))
+    KR = ckks.EvaluationKey(K.data, ckks.ROTATION, 1)
+    s = Fraction(1 << 55)
+    X = ckks.Ciphertext(dev(np.stack([xb, xa])), s, level)
+    Y = ckks.Ciphertext(dev(np.stack([yb, ya])), s, level)
+    step = CapturedStep(torch.device("cuda", 0), lambda: (ckks.hmult(C, X, Y, K).data, ckks.hrot(C, X, 1, KR).data))
+    for seed in (809, 810):
+        nb, na, mb, ma, _ = O.synthetic(level, seed)
+        X.data.copy_(dev(np.stack([nb, na])))
+        Y.data.copy_(dev(np.stack([mb, ma])))
+        m, r = step.replay()
+        want_m = host(ckks.hmult(C, X, Y, K).data)
+        want_r = host(ckks.hrot(C, X, 1, KR).data)
+        np.testing.assert_array_equal(host(m), want_m)
+        np.testing.assert_array_equal(host(r), want_r)
+
+
 def test_counters_follow_reference_profile():
     # HMult at l=24: ntt 116, intt 44, bconv 5, keymult 3 (SURVEY.md §8d); HRot: ntt 120, intt 40
     n, l, a, db = 1024, 24, 8, 55
