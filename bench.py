@@ -403,9 +403,29 @@ def main():
         b.record(st)
         torch.cuda.synchronize(dev)
         graph_ms = a.elapsed_time(b) / reps
+        s2 = torch.cuda.Stream(dev)
+
+        def one_forked():  # HMult and HRot on two streams inside the same graph
+            cur = torch.cuda.current_stream(dev)
+            s2.wait_stream(cur)
+            m = ckks.hmult(C, X1, Y1, relin).data
+            with torch.cuda.stream(s2):
+                r = ckks.hrot(C, X1, 1, rot).data
+            cur.wait_stream(s2)
+            return m, r
+
+        cap2 = CapturedStep(dev, one_forked)
+        a.record(st)
+        for _ in range(reps):
+            cap2.replay()
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        graph2_ms = a.elapsed_time(b) / reps
         small = {"batch": 1, "eager_ops_per_s": round(2 / (eager_ms / 1e3), 1),
                  "cuda_graph_ops_per_s": round(2 / (graph_ms / 1e3), 1),
-                 "note": "one HMult+relin + one HRot per step on one ciphertext; graph = pipeline.CapturedStep"}
+                 "cuda_graph_2_streams_ops_per_s": round(2 / (graph2_ms / 1e3), 1),
+                 "note": "one HMult+relin + one HRot per step on one ciphertext; graph = pipeline.CapturedStep "
+                         "(2 streams: HMult and HRot forked inside the graph)"}
 
     sweep = None
     if args.sweep:
