@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
                                              int entry) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ColBuf* buf = reinterpret_cast<ColBuf*>(smraw);
-  uint2* twring = reinterpret_cast<uint2*>(smraw + (DB ? 2 : 1) * sizeof(ColBuf));  // [2][256] (TWR)
+  // [2][256] twiddle ring (TWR): right after the single tile buffer (ColBuf::tw unused)
+  uint2* twring = reinterpret_cast<uint2*>(smraw + (DB ? 2 * sizeof(ColBuf) : (TWR ? sizeof(ColBuf::tile) : sizeof(ColBuf))));
   const int tid = threadIdx.x, cq = tid & 7, tau = tid >> 3;
   const int items = njobs * batch * kCTiles;
   // the item decoded (and its job loaded) when it is prefetched is reused
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
 int g_col_grid[2] = {0, 0}, g_row_grid = 0;
 bool g_col_db = false;
 int g_col_var = 2;  // CK32_COL: 0 = twiddles in registers, 1 = twiddle ring (4 CTAs/SM), 2 = ring, 5 CTAs/SM (default)
-constexpr int kColRingSmem = (int)sizeof(ColBuf) + 2 * 256 * 8;
+constexpr int kColRingSmem = (int)sizeof(ColBuf::tile) + 2 * 256 * 8;  // 36 KB (6 CTAs/SM measured no faster than 5)
 
 void init_grids() {
   if (g_row_grid) return;
@@ -507,6 +508,7 @@ void init_grids() {
   cudaFuncSetAttribute(k_col<true, false, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColRingSmem);
   cudaFuncSetAttribute(k_col<false, false, true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColRingSmem);
   cudaFuncSetAttribute(k_col<true, false, true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColRingSmem);
+
   const int col_smem_db = 2 * (int)sizeof(ColBuf), col_smem_sb = (int)sizeof(ColBuf);
   cudaFuncSetAttribute(k_col<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem_db);
   cudaFuncSetAttribute(k_col<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem_db);
