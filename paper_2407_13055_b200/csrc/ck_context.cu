@@ -300,6 +300,7 @@ struct Context {
   bool use_ntt256 = true;
   bool use_cluster = false;  // CK32_NTT_CLUSTER=1: single-pass 8-CTA cluster/DSMEM NTT (slower today)
   bool use_row_km = true;
+  bool use_fused_combine = true;  // CK32_NO_FUSED_COMBINE=1: separate k_combine after the ModDown NTT
   bool use_tc = false;  // CK32_TC=1: tcgen05 split-word BConv (bit-exact; slower than the CUDA-core kernel today)  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
   bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
   int ntt_chunk_limbs = 1 << 30;  // limbs per pass-1/pass-2 launch pair (CK32_NTT_CHUNK; measured: no gain)
@@ -993,6 +994,24 @@ struct Context {
     if (fused()) {
       run_convert(pl.intt, pl.cm, pl.ntt, B, v, v_bs, ts, ts_bs, o, o_bs, 4.0 * N * pl.npoly * pl.sc * B,
                   4.0 * N * pl.npoly * pl.out_q * B, st);
+    } else if (combine_now && logn == 16 && d_tw2f && use_ntt256 && !use_cluster && ntt_chunk_limbs >= (1 << 30) &&
+               use_fused_combine) {
+      run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
+      run_bconv(pl.bc, B, ts, ts_bs, o, o_bs, st);
+      {  // forward NTT with the combine fused into its row pass
+        // NTT (8N B per row) + the combine's extra read of v (4N B per row)
+        ProfScope ps(this, 9, 8.0 * n * pl.ntt.njobs * B + 4.0 * n * pl.out_q * pl.npoly * B, 2, st);
+        NttLaunch a = ntt_args(pl.ntt, false, B, o, o_bs, o, o_bs);
+        CombineArgs cb;
+        cb.v = v;
+        cb.v_bs = v_bs;
+        cb.prow = (uint32_t)prow;
+        cb.out_q = pl.out_q;
+        cb.dinv = pl.consts.at<uint32_t>(0);
+        ntt256_forward_combine(a, d_tw2f, cb, st);
+        launches += 2;
+      }
+      combine_now = false;
     } else {
       run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
       run_bconv(pl.bc, B, ts, ts_bs, o, o_bs, st);
@@ -1464,6 +1483,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     c->use_fused = std::getenv("CK32_FUSED") != nullptr;
     c->use_row_km = std::getenv("CK32_NO_ROW_KEYMULT") == nullptr;
     c->use_tc = std::getenv("CK32_TC") != nullptr;
+    c->use_fused_combine = std::getenv("CK32_NO_FUSED_COMBINE") == nullptr;
     c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;
     if (n == 65536) {
       // Row-pass twiddles of ntt256.cu, permuted per row in thread-consumption
@@ -1562,8 +1582,8 @@ ck_status ck_profile_read(ck_context* ctx, ck_prof_stat* out, uint32_t max_class
   return guard([&] {
     Context* c = C(ctx);
     static const char* names[] = {"ntt_fwd", "ntt_inv", "bconv", "key_mult", "tensor", "combine", "hrot_tail",
-                                  "conv_mid", "ntt_row+keymult"};
-    const uint32_t ncls = 9;
+                                  "conv_mid", "ntt_row+keymult", "ntt_fwd+combine"};
+    const uint32_t ncls = 10;
     if (!out || !count) throw InvalidArgument("null argument");
     CK_CUDA(cudaDeviceSynchronize());
     std::vector<ck_prof_stat> st(ncls);

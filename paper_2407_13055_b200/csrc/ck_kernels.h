@@ -27,6 +27,15 @@ void ntt_inverse(int logn, const NttLaunch& a, cudaStream_t st);
 // row-pass tables built by the host ([prime][256 rows][256] {w, w'}).
 bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st);
 bool ntt256_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st);
+// forward NTT whose row pass also applies the drop-and-divide combine
+// (ckks.cpp:643-651): dst row (p, i) <- (v[p * prow + i] - NTT) * dinv[i]
+struct CombineArgs {
+  const uint32_t* v = nullptr;  // [B][npoly][prow][n]
+  uint64_t v_bs = 0;
+  uint32_t prow = 0, out_q = 1;
+  const uint32_t* dinv = nullptr;  // [out_q] divisor^-1, Montgomery
+};
+bool ntt256_forward_combine(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, cudaStream_t st);
 // single-pass cluster/DSMEM variant (ntt_cluster.cu)
 bool ntt_cluster_available();
 void ntt_cluster_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st);

@@ -337,11 +337,14 @@ struct RowCursor {
   }
 };
 
-template <bool INV>
+// COMB (forward only): drop-and-divide combine fused into the store,
+// out = (v - NTT(.)) * divisor^-1 (ckks.cpp:643-651), so the NTT output never
+// makes the extra HBM round trip through k_combine.
+template <bool INV, bool COMB = false>
 __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
                                              uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
                                              int njobs, const PrimeDev* __restrict__ primes,
-                                             const uint2* __restrict__ tw2) {
+                                             const uint2* __restrict__ tw2, CombineArgs cb = CombineArgs{}) {
   extern __shared__ __align__(16) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
   uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * kRowBufWords * 4);  // [kRRows][256]
@@ -440,10 +443,26 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
           ct(v[j], v[j + d], w.x, w.y, q, q2);
         }
       }
+      if (COMB) {  // J.dst_off = p * out_q + i; v row p * prow + i; prime i
+        const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
+        const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + (size_t)r * kR + 16 * tau;
+        const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv_neg;
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
-        stg4(orow + 16 * tau + 4 * m, make_uint4(canon4(v[4 * m], q, q2), canon4(v[4 * m + 1], q, q2),
-                                                 canon4(v[4 * m + 2], q, q2), canon4(v[4 * m + 3], q, q2)));
+        for (int m = 0; m < 4; ++m) {
+          const uint4 vv = *reinterpret_cast<const uint4*>(vr + 4 * m);
+          uint4 o;
+          o.x = sub_if(mont_mul(vv.x - canon4(v[4 * m], q, q2) + q, di, q, qinv), q);
+          o.y = sub_if(mont_mul(vv.y - canon4(v[4 * m + 1], q, q2) + q, di, q, qinv), q);
+          o.z = sub_if(mont_mul(vv.z - canon4(v[4 * m + 2], q, q2) + q, di, q, qinv), q);
+          o.w = sub_if(mont_mul(vv.w - canon4(v[4 * m + 3], q, q2) + q, di, q, qinv), q);
+          stg4(orow + 16 * tau + 4 * m, o);
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          stg4(orow + 16 * tau + 4 * m, make_uint4(canon4(v[4 * m], q, q2), canon4(v[4 * m + 1], q, q2),
+                                                   canon4(v[4 * m + 2], q, q2), canon4(v[4 * m + 3], q, q2)));
+      }
     } else {
       // phase A: c = 16 tau + j, inverse stages 0..3 (W[k*16 + tau])
 #pragma unroll
@@ -963,6 +982,20 @@ bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
   launch_col<false>(a, a.src, a.src_bs, st);
   k_row<false><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs, a.batch,
                                                                   a.njobs, a.primes, tw2);
+  return true;
+}
+
+bool ntt256_forward_combine(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, cudaStream_t st) {
+  init_grids();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_row<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmem);
+    attr = true;
+  }
+  const int row_items = a.njobs * (kR / kRRows) * a.batch;
+  launch_col<false>(a, a.src, a.src_bs, st);
+  k_row<false, true><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs,
+                                                                        a.batch, a.njobs, a.primes, tw2, cb);
   return true;
 }
 
