@@ -735,11 +735,15 @@ constexpr int kKSmem = 2 * kKBuf * 4 + kRRows * kR * 8;
 
 // EARLY: the key halves of digit k are loaded into registers before its row
 // pass (their L2 latency hides behind the butterflies) at MINB CTAs per SM.
-template <bool EARLY = false, int MINB = 1>
+// ALLD (D <= 3): the extension tiles of all D digits of an item are requested
+// together at the item start (one cp.async group per digit, one buffer per
+// digit), so only the first digit's load latency is exposed; digit k waits
+// for its own group.  Otherwise each digit's tile is loaded when needed.
+template <bool EARLY = false, int MINB = 1, bool ALLD = false>
 __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, const uint2* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
-  uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * kKBuf * 4);
+  uint2* tws = reinterpret_cast<uint2*>(smraw + (ALLD ? 3 : 2) * kKBuf * 4);
   const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15;
   constexpr int kTiles = kR / kRRows;
   const int rows = a.level + a.alpha, B = a.batch;
@@ -754,12 +758,28 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
     const int g = i < a.level ? i : a.L + (i - a.level);
     const PrimeDev P = a.primes[g];
     const uint32_t q = P.q, q2 = P.q2;
+    if (ALLD) __syncthreads();  // every thread is done with the previous item's tile buffers
     if (key != cur_key) {
-      __syncthreads();
+      if (!ALLD) __syncthreads();
       const uint2* T = tw2 + ((size_t)g * kR + tile * kRRows) * kR;
       for (int e = tid; e < kRRows * kR / 2; e += kKT) cp16(&tws[2 * e], &T[2 * e]);
       cp_commit();
       cur_key = key;
+    }
+    if (ALLD) {
+      for (int k = 0; k < a.D; ++k) {
+        const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+        if (!(i >= lo && i < hi)) {
+          const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)tile * kRRows * kR;
+          uint32_t* buf = sbuf + k * kKBuf;
+#pragma unroll
+          for (int m = 0; m < kRRows * 64 / kKT; ++m) {
+            const int e = tid + m * kKT, rr = e >> 6, c = (e & 63) * 4;
+            cp16(buf + rr * kRowStride + rpos(c), gsrc + rr * kR + c);
+          }
+        }
+        cp_commit();
+      }
     }
     const int r = tile * kRRows + rho;
     const uint2* W = tws + rho * kR;
@@ -791,16 +811,25 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
           v[4 * m + 3] = x.w;
         }
       } else {
-        uint32_t* buf = sbuf + kbuf * kKBuf;
-        kbuf ^= 1;
-        const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)tile * kRRows * kR;
+        uint32_t* buf;
+        if (ALLD) {
+          buf = sbuf + k * kKBuf;
+          const int pend = a.D - 1 - k;  // later digits' groups may still be in flight
+          if (pend >= 2) cp_wait<2>();
+          else if (pend == 1) cp_wait<1>();
+          else cp_wait<0>();
+        } else {
+          buf = sbuf + kbuf * kKBuf;
+          kbuf ^= 1;
+          const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)tile * kRRows * kR;
 #pragma unroll
-        for (int m = 0; m < kRRows * 64 / kKT; ++m) {
-          const int e = tid + m * kKT, rr = e >> 6, c = (e & 63) * 4;
-          cp16(buf + rr * kRowStride + rpos(c), gsrc + rr * kR + c);
+          for (int m = 0; m < kRRows * 64 / kKT; ++m) {
+            const int e = tid + m * kKT, rr = e >> 6, c = (e & 63) * 4;
+            cp16(buf + rr * kRowStride + rpos(c), gsrc + rr * kR + c);
+          }
+          cp_commit();
+          cp_wait<0>();
         }
-        cp_commit();
-        cp_wait<0>();
         __syncthreads();
         uint32_t* line = buf + rho * kRowStride;
 #pragma unroll
@@ -901,20 +930,23 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
 }  // namespace
 
 // CK32_KM selects the k_row_keymult variant for A/B runs: 0 = key halves
-// loaded before the row pass, 4 CTAs/SM (default: 4.83 vs 4.77 TB/s), 1 = same
-// at 3 CTAs/SM (4.20), 2 = loaded after the row pass (the first version).
-template <bool EARLY, int MINB>
+// loaded before the row pass, all digit tiles of an item requested at once
+// (default when D <= 3), 3 = the same with per-digit tile loads (4.83 TB/s),
+// 1 = per-digit loads at 3 CTAs/SM (4.20), 2 = key halves loaded after the
+// row pass (the first version, 4.77).
+template <bool EARLY, int MINB, bool ALLD = false>
 static void launch_km(const KeyMultLaunch& a, const uint2* tw2, int items, cudaStream_t st) {
   static int grid = 0;
+  constexpr int smem = ALLD ? kKSmem + kKBuf * 4 : kKSmem;
   if (!grid) {
-    cudaFuncSetAttribute(k_row_keymult<EARLY, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kKSmem);
+    cudaFuncSetAttribute(k_row_keymult<EARLY, MINB, ALLD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult<EARLY, MINB>, kKT, kKSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult<EARLY, MINB, ALLD>, kKT, smem);
     grid = sms * std::max(1, per);
   }
-  k_row_keymult<EARLY, MINB><<<std::min(grid, items), kKT, kKSmem, st>>>(a, tw2);
+  k_row_keymult<EARLY, MINB, ALLD><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
 }
 
 void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
@@ -928,8 +960,10 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
     launch_km<true, 3>(a, tw2, items, st);
   else if (ver == 2)
     launch_km<false, 4>(a, tw2, items, st);
-  else
+  else if (ver == 3 || a.D > 3)
     launch_km<true, 4>(a, tw2, items, st);
+  else
+    launch_km<true, 4, true>(a, tw2, items, st);
 }
 
 void conv_mid(const ConvMidLaunch& a, cudaStream_t st) {
