@@ -97,6 +97,12 @@ ck_status ck_intt_inverse(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, co
 ck_status ck_bconv(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,
                    uint32_t* dst_dev, uint32_t dst_count, const uint32_t* dst_gidx, ck_stream stream);
 /* apply_automorphism, evaluation domain (automorphism.cpp:76-100), rotation r */
+/* mod_switch (bconv.cpp:176-213): src rows (evaluation, Montgomery) over the
+ * primes src_gidx -> dst rows over Q_[0, dst_q) then P_[0, dst_p)
+ * (evaluation, Montgomery): INTT with the part-1 epilogue, BConv part 2,
+ * forward NTT.  dst_dev holds dst_q + dst_p rows. */
+ck_status ck_mod_switch(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,
+                        uint32_t* dst_dev, uint32_t dst_q, uint32_t dst_p, ck_stream stream);
 ck_status ck_automorphism(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t rows, int64_t r,
                           ck_stream stream);
 /* ew_add / ew_sub / ew_mul over Q-prefix rows (poly.cpp:146-164) */

@@ -53,6 +53,7 @@ _SIGS = {
     "ck_ntt_forward": [_vp, _vp, _u32, _u32p, _vp],
     "ck_intt_inverse": [_vp, _vp, _u32, _u32p, _u32p, _vp],
     "ck_bconv": [_vp, _vp, _u32, _u32p, _vp, _u32, _u32p, _vp],
+    "ck_mod_switch": [_vp, _vp, _u32, _u32p, _vp, _u32, _u32, _vp],
     "ck_automorphism": [_vp, _vp, _vp, _u32, _i64, _vp],
     "ck_ew_add": [_vp, _vp, _vp, _vp, _u32, _vp],
     "ck_ew_sub": [_vp, _vp, _vp, _vp, _u32, _vp],

@@ -478,6 +478,19 @@ def bconv(ctx: CkksContext, src: torch.Tensor, src_gidx: Sequence[int], dst_gidx
     return out
 
 
+def mod_switch(ctx: CkksContext, a: Polynomial, src_gidx: Sequence[int], dst_q_count: int,
+               dst_p_count: int = 0) -> Polynomial:
+    """mod_switch (bconv.cpp:176-213): evaluation-domain rows over `src_gidx`
+    -> rows over Q_[0, dst_q) + P_[0, dst_p), evaluation domain, Montgomery."""
+    _check_eval_mont(a, "mod_switch")
+    if a.rows != len(src_gidx):
+        raise ValueError("input rows do not match table source")
+    out = ctx.empty(dst_q_count + dst_p_count, ctx.n)
+    nat.call("ck_mod_switch", ctx.handle, _ptr(a.data.contiguous()), len(src_gidx), nat.u32_array(src_gidx),
+             _ptr(out), dst_q_count, dst_p_count, ctx.stream())
+    return Polynomial(out, dst_q_count, dst_p_count)
+
+
 def apply_automorphism(ctx: CkksContext, p: Polynomial, r: int) -> Polynomial:  # automorphism.cpp:76-100
     if p.domain != EVALUATION:
         raise ValueError("only the evaluation-domain gather is implemented on the GPU")

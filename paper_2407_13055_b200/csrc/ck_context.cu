@@ -1737,6 +1737,38 @@ ck_status ck_bconv(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count,
   });
 }
 
+ck_status ck_mod_switch(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,
+                        uint32_t* dst_dev, uint32_t dst_q, uint32_t dst_p, ck_stream stream) {
+  // bconv.cpp:176-213: INTT with the part-1 epilogue, BConv part 2, forward NTT
+  std::vector<uint32_t> sg, dg, part1_mont;
+  Context* c = nullptr;
+  uint32_t* work = nullptr;
+  ck_status st0 = guard([&] {
+    c = C(ctx);
+    check_ptr(src_dev);
+    check_ptr(dst_dev);
+    if (src_count == 0 || !src_gidx) throw InvalidArgument("input rows do not match table source");
+    if (dst_q > c->L || dst_p > c->alpha || dst_q + dst_p == 0)
+      throw InvalidArgument("output rows do not match table destination");
+    sg.assign(src_gidx, src_gidx + src_count);
+    for (uint32_t g : sg)
+      if (g >= c->primes.size()) throw InvalidArgument("source prime mismatch");
+    for (uint32_t i = 0; i < dst_q; ++i) dg.push_back(i);
+    for (uint32_t j = 0; j < dst_p; ++j) dg.push_back(c->L + j);
+    std::vector<uint32_t> cmat, part1;
+    c->bconv_consts(sg, dg, cmat, part1);
+    for (size_t j = 0; j < sg.size(); ++j) part1_mont.push_back(to_mont(part1[j], c->q(sg[j])));
+    work = static_cast<uint32_t*>(c->scratch_get((size_t)src_count * c->n * 4, S(stream)));
+    CK_CUDA(cudaMemcpyAsync(work, src_dev, (size_t)src_count * c->n * 4, cudaMemcpyDeviceToDevice, S(stream)));
+  });
+  if (st0 != CK_OK) return st0;
+  ck_status s1 = ck_intt_inverse(ctx, work, src_count, sg.data(), part1_mont.data(), stream);
+  if (s1 != CK_OK) return s1;
+  s1 = ck_bconv(ctx, work, src_count, sg.data(), dst_dev, (uint32_t)dg.size(), dg.data(), stream);
+  if (s1 != CK_OK) return s1;
+  return ck_ntt_forward(ctx, dst_dev, (uint32_t)dg.size(), dg.data(), stream);
+}
+
 ck_status ck_automorphism(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t rows, int64_t r,
                           ck_stream stream) {
   return guard([&] {

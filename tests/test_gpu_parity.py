@@ -477,3 +477,58 @@ def test_cpp_mirror_drop_in(tmp_path):
     rb, ra = O.hrot(level, xb, xa, 1, evk)
     got = np.fromfile(tmp_path / "out_hrot.bin", dtype="<u4").reshape(2, level, n)
     np.testing.assert_array_equal(got, np.stack([canon(O, rb, level), canon(O, ra, level)]))
+
+
+# ------------------------------------------------------------- mod_switch --
+@pytest.mark.parametrize("n", [16, 32, 64, 65536])
+def test_mod_switch_error_characterization(n):
+    """test_bconv.cpp:147-190 on the GPU: P basis -> Q prefix; after INTT the
+    output equals (exact + e P) mod q with 0 <= e < alpha (alpha = 2)."""
+    l, a = 2, 2
+    C = ctx_for(n, l, a, 48)
+    O = _oracle(n, l, a, 48)
+    P = [int(p) for p in O.primes[l:]]
+    rng = np.random.default_rng(113 + n)
+    coeffs = np.stack([rng.integers(0, p, n) for p in P]).astype(np.uint32)
+    src_g = [l, l + 1]
+    poly = ckks.ntt_forward(C, ckks.Polynomial(dev(coeffs), 0, a, ckks.COEFFICIENT, False))
+    out = ckks.mod_switch(C, poly, src_g, 2, 0)
+    assert out.domain == ckks.EVALUATION and out.mont
+    back = host(ckks.intt_inverse(C, out).data).astype(object)
+    Pprod = P[0] * P[1]
+    # CRT of the source residues (exact integer in [0, P))
+    inv = [pow(Pprod // p, -1, p) for p in P]
+    exact = [(int(coeffs[0, j]) * inv[0] * (Pprod // P[0]) + int(coeffs[1, j]) * inv[1] * (Pprod // P[1])) % Pprod
+             for j in range(n)]
+    for i in range(2):
+        q = int(O.primes[i])
+        for j in range(n):
+            assert int(back[i, j]) in {(exact[j] + e * Pprod) % q for e in range(a)}
+
+
+def test_mod_switch_small_constant_is_exact():
+    """test_bconv.cpp:192-208: a small constant polynomial switches exactly."""
+    n, l, a = 16, 2, 1
+    C = ctx_for(n, l, a, 48)
+    coeffs = np.arange(1, n + 1, dtype=np.uint32)[None, :]
+    poly = ckks.ntt_forward(C, ckks.Polynomial(dev(coeffs), 0, a, ckks.COEFFICIENT, False))
+    out = ckks.intt_inverse(C, ckks.mod_switch(C, poly, [l], 2, 0))
+    np.testing.assert_array_equal(host(out.data), np.stack([np.arange(1, n + 1)] * 2).astype(np.uint32))
+
+
+@pytest.mark.parametrize("n", [1024, 65536])
+def test_mod_switch_matches_oracle_composition(n):
+    """bconv.cpp:176-213 = inverse_row(part1) -> bconv_part2 -> forward_row,
+    composed from the oracle's pinned INTT / BConv / NTT."""
+    l, a = 12, 4
+    C = ctx_for(n, l, a, 48)
+    O = _oracle(n, l, a, 48)
+    src_g = np.array([l + j for j in range(a)], np.uint32)
+    dst_g = np.array(list(range(6)) + [l, l + 1], np.uint32)
+    x = O.random_rows(Rng(n + 5), src_g)  # canonical evaluation-domain residues
+    out = ckks.mod_switch(C, ckks.Polynomial(dev(x), 0, a), list(src_g), 6, 2)
+    part1 = [int(v) for v in O.bconv_part1(src_g)]
+    coef = O.canonical(O.intt(x, src_g, part1), src_g)
+    conv = O.bconv(coef.astype(np.int32), list(src_g), list(dst_g))
+    want = O.canonical(O.ntt_fwd(conv, dst_g), dst_g)
+    np.testing.assert_array_equal(host(out.data), want)
