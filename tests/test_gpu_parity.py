@@ -434,6 +434,17 @@ def test_errors_mirror_reference():
         ckks.ntt_forward(C, p)
     with pytest.raises(ValueError):
         ckks.CkksContext(ckks.CkksParams(n=1000, l=4, alpha=2))
+    # mod_switch argument checks (bconv.cpp:180-197)
+    pe = ckks.Polynomial(dev(xb), 4)
+    with pytest.raises(ValueError):  # rows do not match the table source
+        ckks.mod_switch(C, pe, [0, 1], 2)
+    with pytest.raises(ValueError):  # coefficient-domain input
+        ckks.mod_switch(C, ckks.Polynomial(dev(xb), 4, 0, ckks.COEFFICIENT, False), [0, 1, 2, 3], 2)
+    with pytest.raises(ValueError):  # destination wider than the basis
+        ckks.mod_switch(C, pe, [0, 1, 2, 3], l + 1)
+    # decode checks (ckks.cpp:322)
+    with pytest.raises(ValueError):
+        ckks.decode(C, ckks.Plaintext(ckks.Polynomial(dev(xb), 4, 0, ckks.COEFFICIENT, False), Fraction(1 << 55), 4))
 
 
 def test_lazy_then_rescale_equals_merged_ledger():
