@@ -167,6 +167,25 @@ ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, do
 ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2, double* slots_dev,
                     ck_stream stream);
 
+/* Element-wise parts of decrypt / encrypt (ckks.cpp:497-553).  All operands
+ * are evaluation-domain Montgomery rows (canonical); the randomness of
+ * encrypt is supplied by the caller (the reference samples it on the host with
+ * mt19937_64, ckks.cpp:390-430) and turned into evaluation form with
+ * ck_coeffs_to_eval.
+ *   decrypt     out [B][level]   = ct.b + ct.a * s        (ct [B][2][level], s [level])
+ *   encrypt_sk  out [2][level]   = (m + e - a s, a)
+ *   encrypt_pk  out [2][level]   = (v pk.b + e0 + m, v pk.a + e1)   (pk [2][level]) */
+ck_status ck_decrypt(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, const uint32_t* s,
+                     uint32_t* out, ck_stream stream);
+ck_status ck_encrypt_sk(ck_context* ctx, uint32_t level, const uint32_t* pt, const uint32_t* a, const uint32_t* e,
+                        const uint32_t* s, uint32_t* out, ck_stream stream);
+ck_status ck_encrypt_pk(ck_context* ctx, uint32_t level, const uint32_t* pt, const uint32_t* v, const uint32_t* e0,
+                        const uint32_t* e1, const uint32_t* pk, uint32_t* out, ck_stream stream);
+/* coeffs_to_eval (ckks.cpp:366-380): n signed int64 coefficients (device) ->
+ * rows [level + p_rows][n], each reduced mod its prime then forward NTT. */
+ck_status ck_coeffs_to_eval(ck_context* ctx, const int64_t* coeffs, uint32_t level, uint32_t p_rows, uint32_t* out,
+                            ck_stream stream);
+
 /* Number of this library's kernel launches issued since context creation
  * (evidence for bench.py's gpu_launches). */
 uint64_t ck_launch_count(const ck_context* ctx);

@@ -167,6 +167,13 @@ int ref_gen_fixtures(uint32_t n, uint32_t l, uint32_t alpha, uint32_t db, uint64
 
     auto u = unit_slots(rng, ctx.slots());
     auto v = unit_slots(rng, ctx.slots());
+    auto Wz = [&](const std::string& name, const std::vector<std::complex<double>>& z) {
+      std::vector<uint8_t> b(z.size() * 16);
+      std::memcpy(b.data(), z.data(), b.size());
+      W(name, b);
+    };
+    Wz("slots_u.f64", u);  // complex<double> (re, im) little-endian
+    Wz("slots_v.f64", v);
     auto pt_u = encode(ctx, u, ctx.default_scale(), l);
     auto pt_v = encode(ctx, v, ctx.default_scale(), l);
     auto ct_u = encrypt(ctx, pt_u, sk, rng);
@@ -177,6 +184,8 @@ int ref_gen_fixtures(uint32_t n, uint32_t l, uint32_t alpha, uint32_t db, uint64
 
     // mechanisms
     W("out_hmult.bin", serialize_ciphertext(hmult(ctx, ct_u, ct_v, relin)));
+    W("out_decrypt_u.bin", serialize_poly(decrypt(ctx, ct_u, sk).poly));
+    W("out_decrypt_hmult.bin", serialize_poly(decrypt(ctx, hmult(ctx, ct_u, ct_v, relin), sk).poly));
     W("out_hrot1.bin", serialize_ciphertext(hrot(ctx, ct_u, 1, rot1)));
     W("out_hrot3.bin", serialize_ciphertext(hrot(ctx, ct_u, 3, rot3)));
     W("out_rescale.bin", serialize_ciphertext(rescale(ctx, ct_u)));

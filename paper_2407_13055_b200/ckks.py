@@ -445,6 +445,81 @@ def decode(ctx: CkksContext, pt: Plaintext) -> np.ndarray:
     return h[0::2] + 1j * h[1::2]
 
 
+# ------------------------------------------------------ encrypt / decrypt --
+def decrypt(ctx: CkksContext, ct: Ciphertext, s: torch.Tensor) -> Plaintext:
+    """decrypt (ckks.cpp:541-553): m = b + a s (evaluation, Montgomery).
+    `s` holds at least ct.level rows of the secret (sk.s of the reference)."""
+    _check_pair(ctx, ct)
+    rows = s[: ct.level].contiguous()
+    shape = list(ct.data.shape)
+    del shape[-3]
+    out = torch.empty(shape, dtype=torch.int32, device=ctx.device)
+    nat.call("ck_decrypt", ctx.handle, ct.level, ct.batch, _ptr(ct.data), _ptr(rows), _ptr(out), ctx.stream())
+    return Plaintext(Polynomial(out, ct.level, 0), ct.scale, ct.level)
+
+
+def coeffs_to_eval(ctx: CkksContext, coeffs, level: int, p_rows: int = 0) -> Polynomial:
+    """coeffs_to_eval (ckks.cpp:366-380): signed integer coefficients ->
+    evaluation-domain Montgomery rows over Q_level (+ p_rows P primes)."""
+    c = torch.as_tensor(np.asarray(coeffs, dtype=np.int64) if not torch.is_tensor(coeffs) else coeffs)
+    c = c.to(device=ctx.device, dtype=torch.int64).contiguous()
+    if c.numel() != ctx.n:
+        raise ValueError("need n coefficients")
+    out = ctx.empty(level + p_rows, ctx.n)
+    nat.call("ck_coeffs_to_eval", ctx.handle, _ptr(c), level, p_rows, _ptr(out), ctx.stream())
+    return Polynomial(out, level, p_rows)
+
+
+def encrypt_sk(ctx: CkksContext, pt: Plaintext, s: torch.Tensor, a: torch.Tensor, e: Polynomial) -> Ciphertext:
+    """Secret-key encrypt (ckks.cpp:497-516) with caller-supplied randomness:
+    `a` uniform evaluation-domain rows, `e` the Gaussian error in evaluation
+    form (coeffs_to_eval).  (b, a) = (m + e - a s, a)."""
+    _check_eval_mont(pt.poly, "encrypt")
+    if pt.poly.p_count != 0:
+        raise ValueError("cannot encrypt a P-extended plaintext")
+    l = pt.level
+    out = ctx.empty(2, l, ctx.n)
+    nat.call("ck_encrypt_sk", ctx.handle, l, _ptr(pt.poly.data[:l].contiguous()), _ptr(a[:l].contiguous()),
+             _ptr(e.data[:l].contiguous()), _ptr(s[:l].contiguous()), _ptr(out), ctx.stream())
+    return Ciphertext(out, pt.scale, l)
+
+
+def encrypt_pk(ctx: CkksContext, pt: Plaintext, pk: Ciphertext, v: Polynomial, e0: Polynomial,
+               e1: Polynomial) -> Ciphertext:
+    """Public-key encrypt (ckks.cpp:518-539) with caller-supplied randomness
+    (v ternary, e0 / e1 Gaussian, all in evaluation form):
+    (b, a) = (v pk.b + e0 + m, v pk.a + e1)."""
+    _check_eval_mont(pt.poly, "encrypt")
+    if pt.poly.p_count != 0:
+        raise ValueError("cannot encrypt a P-extended plaintext")
+    l = pt.level
+    pkl = torch.stack([pk.data[0, :l], pk.data[1, :l]]).contiguous()
+    out = ctx.empty(2, l, ctx.n)
+    nat.call("ck_encrypt_pk", ctx.handle, l, _ptr(pt.poly.data[:l].contiguous()), _ptr(v.data[:l].contiguous()),
+             _ptr(e0.data[:l].contiguous()), _ptr(e1.data[:l].contiguous()), _ptr(pkl), _ptr(out), ctx.stream())
+    return Ciphertext(out, pt.scale, l)
+
+
+# Host-side samplers for the encryption randomness (numpy Generator; the
+# reference samples with std::mt19937_64, ckks.cpp:390-430, so the streams
+# differ — the GPU arithmetic on given randomness is what is bit-exact).
+def sample_ternary(n: int, hamming: int, rng: np.random.Generator) -> np.ndarray:
+    c = np.zeros(n, np.int64)
+    idx = rng.choice(n, size=hamming, replace=False)
+    c[idx] = rng.choice(np.array([-1, 1], np.int64), size=hamming)
+    return c
+
+
+def sample_gaussian(n: int, sigma: float, rng: np.random.Generator) -> np.ndarray:
+    return np.rint(rng.normal(0.0, sigma, n)).astype(np.int64)
+
+
+def uniform_eval(ctx: CkksContext, level: int, rng: np.random.Generator) -> torch.Tensor:
+    q = ctx.q_primes[:level].astype(np.int64)[:, None]
+    return torch.from_numpy((rng.integers(0, 1 << 62, (level, ctx.n), dtype=np.int64) % q).astype(np.int32)).to(
+        ctx.device)
+
+
 # ----------------------------------------------------------- kernel level --
 def ntt_forward(ctx: CkksContext, p: Polynomial) -> Polynomial:  # ntt.cpp:288-299
     if p.domain != COEFFICIENT:

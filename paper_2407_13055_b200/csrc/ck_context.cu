@@ -2098,6 +2098,70 @@ ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, dou
   });
 }
 
+ck_status ck_decrypt(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, const uint32_t* s,
+                     uint32_t* out, ck_stream stream) {
+  return guard([&] {  // ckks.cpp:541-553
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(ct);
+    check_ptr(s);
+    check_ptr(out);
+    crypt((int)c->n, (int)level, (int)batch, 0, ct, 2ull * level * c->n, s, nullptr, nullptr, nullptr, out,
+          (uint64_t)level * c->n, c->d_primes, S(stream));
+    ++c->launches;
+    check_launch();
+  });
+}
+ck_status ck_encrypt_sk(ck_context* ctx, uint32_t level, const uint32_t* pt, const uint32_t* a, const uint32_t* e,
+                        const uint32_t* s, uint32_t* out, ck_stream stream) {
+  return guard([&] {  // ckks.cpp:497-516, randomness (a uniform, e Gaussian in eval form) supplied
+    Context* c = C(ctx);
+    check_level(c, level);
+    for (const void* p : {(const void*)pt, (const void*)a, (const void*)e, (const void*)s, (const void*)out})
+      check_ptr(p);
+    crypt((int)c->n, (int)level, 1, 1, pt, 0, a, e, s, nullptr, out, 0, c->d_primes, S(stream));
+    ++c->launches;
+    check_launch();
+  });
+}
+ck_status ck_encrypt_pk(ck_context* ctx, uint32_t level, const uint32_t* pt, const uint32_t* v, const uint32_t* e0,
+                        const uint32_t* e1, const uint32_t* pk, uint32_t* out, ck_stream stream) {
+  return guard([&] {  // ckks.cpp:518-539, randomness (v ternary, e0 e1 Gaussian in eval form) supplied
+    Context* c = C(ctx);
+    check_level(c, level);
+    for (const void* p : {(const void*)pt, (const void*)v, (const void*)e0, (const void*)e1, (const void*)pk,
+                          (const void*)out})
+      check_ptr(p);
+    crypt((int)c->n, (int)level, 1, 2, pt, 0, v, e0, e1, pk, out, 0, c->d_primes, S(stream));
+    ++c->launches;
+    check_launch();
+  });
+}
+ck_status ck_coeffs_to_eval(ck_context* ctx, const int64_t* coeffs, uint32_t level, uint32_t p_rows, uint32_t* out,
+                            ck_stream stream) {
+  ck_status st0 = guard([&] {  // ckks.cpp:366-380: reduce mod every prime, then ntt_forward
+    Context* c = C(ctx);
+    check_level(c, level);
+    check_ptr(coeffs);
+    check_ptr(out);
+    if (p_rows > c->alpha) throw InvalidArgument("too many P rows");
+    const uint32_t rows = level + p_rows;
+    std::vector<uint16_t> rp(rows);
+    for (uint32_t i = 0; i < rows; ++i) rp[i] = (uint16_t)c->gidx(level, i);
+    uint16_t* d_rp = static_cast<uint16_t*>(c->scratch_get(2 * rows + 16, S(stream)));
+    CK_CUDA(cudaMemcpyAsync(d_rp, rp.data(), 2 * rows, cudaMemcpyHostToDevice, S(stream)));
+    reduce_coeffs((int)c->n, (int)rows, reinterpret_cast<const long long*>(coeffs), d_rp, c->d_primes, out, S(stream));
+    CK_CUDA(cudaStreamSynchronize(S(stream)));  // rp is pageable host memory
+    ++c->launches;
+    check_launch();
+  });
+  if (st0 != CK_OK) return st0;
+  Context* c = C(ctx);
+  std::vector<uint32_t> g(level + p_rows);
+  for (uint32_t i = 0; i < g.size(); ++i) g[i] = c->gidx(level, i);
+  return ck_ntt_forward(ctx, out, (uint32_t)g.size(), g.data(), stream);
+}
+
 ck_status ck_hoisted_rotations(ck_context* ctx, uint32_t level, const uint32_t* ct, uint32_t count,
                                const int64_t* rots, const uint32_t* const* evks, uint32_t* out, ck_stream stream) {
   return guard([&] {

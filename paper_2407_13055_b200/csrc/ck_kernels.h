@@ -159,6 +159,12 @@ void hrot_tail(int n, int level, int batch, const uint32_t* v, uint64_t v_bs, ui
 void elementwise(int n, int rows, int batch, int op, const uint32_t* a, uint64_t a_bs, const uint32_t* b,
                  uint64_t b_bs, uint32_t* o, uint64_t o_bs, const uint16_t* row_prime, const PrimeDev* primes,
                  cudaStream_t st, int prime_mod = 0);
+// decrypt / encrypt element-wise parts (ckks.cpp:497-553), see kernels.cu
+void crypt(int n, int level, int batch, int op, const uint32_t* x, uint64_t x_bs, const uint32_t* y, const uint32_t* z,
+           const uint32_t* w, const uint32_t* u, uint32_t* out, uint64_t out_bs, const PrimeDev* primes,
+           cudaStream_t st);
+void reduce_coeffs(int n, int rows, const long long* c, const uint16_t* row_prime, const PrimeDev* primes,
+                   uint32_t* out, cudaStream_t st);
 // out[i][j] = in[i][src[j]] (automorphism.cpp:82-87)
 void permute(int n, int rows, int batch, const uint32_t* in, uint64_t in_bs, uint32_t* out, uint64_t out_bs,
              const uint32_t* src_map, cudaStream_t st);

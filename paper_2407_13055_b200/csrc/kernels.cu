@@ -232,6 +232,51 @@ __global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_
   st4(o + b * o_bs + r, z);
 }
 
+// ------------------------------------------------- encrypt / decrypt parts --
+// Element-wise parts of decrypt / encrypt (ckks.cpp:497-553) on one batch of
+// ciphertexts [B][2][level][n]; every operand is evaluation domain, Montgomery
+// form, canonical.  op 0 decrypt: m = b + a s.  op 1 secret-key encrypt:
+// b = m + e - a s, a = a.  op 2 public-key encrypt: b = v pk.b + e0 + m,
+// a = v pk.a + e1.  (x, y, z, w) are the op's operands in that order.
+__global__ void __launch_bounds__(kT) k_crypt(int n, int level, int op, const uint32_t* __restrict__ x,
+                                              uint64_t x_bs, const uint32_t* __restrict__ y,
+                                              const uint32_t* __restrict__ z, const uint32_t* __restrict__ w,
+                                              const uint32_t* __restrict__ u, uint32_t* __restrict__ out,
+                                              uint64_t out_bs, const PrimeDev* __restrict__ primes) {
+  const int k = blockIdx.x * kT + threadIdx.x;
+  if (k >= n) return;
+  const int i = blockIdx.y, b = blockIdx.z;
+  const PrimeDev P = primes[i];
+  const uint32_t q = P.q;
+  const size_t r = (size_t)i * n + k;
+  if (op == 0) {  // x = ct [2][level], y = s
+    const uint32_t cb = x[b * x_bs + r], ca = x[b * x_bs + (size_t)level * n + r];
+    out[b * out_bs + r] = sub_if(cb + sub_if(mont_mul(ca, y[r], q, P.qinv_neg), q), q);
+  } else if (op == 1) {  // x = m, y = a, z = e, w = s
+    const uint32_t as = sub_if(mont_mul(y[r], w[r], q, P.qinv_neg), q);
+    out[r] = sub_if(sub_if(x[r] + z[r], q) + q - as, q);
+    out[(size_t)level * n + r] = y[r];
+  } else {  // x = m, y = v, z = e0, w = e1, u = pk [2][level] (b then a)
+    const uint32_t vb = sub_if(mont_mul(y[r], u[r], q, P.qinv_neg), q);
+    const uint32_t va = sub_if(mont_mul(y[r], u[(size_t)level * n + r], q, P.qinv_neg), q);
+    out[r] = sub_if(sub_if(vb + z[r], q) + x[r], q);
+    out[(size_t)level * n + r] = sub_if(va + w[r], q);
+  }
+}
+
+// int64 coefficients -> canonical residues of every row (coeffs_to_eval's
+// reduction, ckks.cpp:366-380, correct() of modarith.hpp:46-50)
+__global__ void __launch_bounds__(kT) k_reduce_coeffs(int n, const long long* __restrict__ c,
+                                                      const uint16_t* __restrict__ row_prime,
+                                                      const PrimeDev* __restrict__ primes, uint32_t* __restrict__ out) {
+  const int k = blockIdx.x * kT + threadIdx.x;
+  if (k >= n) return;
+  const long long q = primes[row_prime[blockIdx.y]].q;
+  long long v = c[k] % q;
+  if (v < 0) v += q;
+  out[(size_t)blockIdx.y * n + k] = (uint32_t)v;
+}
+
 __global__ void __launch_bounds__(kT) k_permute(int n, const uint32_t* __restrict__ in, uint64_t in_bs,
                                                 uint32_t* __restrict__ out, uint64_t out_bs,
                                                 const uint32_t* __restrict__ src) {
@@ -305,6 +350,19 @@ void elementwise(int n, int rows, int batch, int op, const uint32_t* a, uint64_t
   dim3 grid(cdiv(n / 4, kT), rows, batch);
   k_elementwise<<<grid, kT, 0, st>>>(n, op, a, a_bs, b, b_bs, o, o_bs, row_prime, primes,
                                      prime_mod > 0 ? prime_mod : rows);
+}
+
+void crypt(int n, int level, int batch, int op, const uint32_t* x, uint64_t x_bs, const uint32_t* y, const uint32_t* z,
+           const uint32_t* w, const uint32_t* u, uint32_t* out, uint64_t out_bs, const PrimeDev* primes,
+           cudaStream_t st) {
+  dim3 grid(cdiv(n, kT), level, batch);
+  k_crypt<<<grid, kT, 0, st>>>(n, level, op, x, x_bs, y, z, w, u, out, out_bs, primes);
+}
+
+void reduce_coeffs(int n, int rows, const long long* c, const uint16_t* row_prime, const PrimeDev* primes,
+                   uint32_t* out, cudaStream_t st) {
+  dim3 grid(cdiv(n, kT), rows);
+  k_reduce_coeffs<<<grid, kT, 0, st>>>(n, c, row_prime, primes, out);
 }
 
 void permute(int n, int rows, int batch, const uint32_t* in, uint64_t in_bs, uint32_t* out, uint64_t out_bs,
