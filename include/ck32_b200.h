@@ -79,6 +79,7 @@ ck_status ck_malloc(ck_context* ctx, size_t bytes, void** dptr);
 ck_status ck_free(ck_context* ctx, void* dptr);
 ck_status ck_memcpy_h2d(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream);
 ck_status ck_memcpy_d2h(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream);
+ck_status ck_memcpy_d2d(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream);
 ck_status ck_stream_sync(ck_context* ctx, ck_stream stream);
 
 /* ---- kernel-level entry points ------------------------------------------ */

@@ -47,6 +47,7 @@ _SIGS = {
     "ck_free": [_vp, _vp],
     "ck_memcpy_h2d": [_vp, _vp, _vp, ctypes.c_size_t, _vp],
     "ck_memcpy_d2h": [_vp, _vp, _vp, ctypes.c_size_t, _vp],
+    "ck_memcpy_d2d": [_vp, _vp, _vp, ctypes.c_size_t, _vp],
     "ck_stream_sync": [_vp, _vp],
     "ck_profile": [_vp, ctypes.c_int],
     "ck_profile_read": [_vp, ctypes.POINTER(ck_prof_stat), _u32, ctypes.POINTER(ctypes.c_uint32)],

@@ -281,4 +281,84 @@ inline Ciphertext padd(CkksContext& ctx, const Ciphertext& ct, const Plaintext& 
   return out;
 }
 
+// --- key switching building blocks (ckks.hpp:179-189) -----------------------
+struct Polynomial {  // poly.hpp:74-119 (device rows, Q prefix then P rows; evaluation domain, Montgomery)
+  DeviceBuffer data;
+  uint32_t q_count = 0, p_count = 0;
+};
+struct HoistState {  // ckks.hpp:88-91: D x (level + alpha) rows
+  DeviceBuffer digits;
+  uint32_t level = 0, D = 0;
+};
+
+inline HoistState mod_up(CkksContext& ctx, const Polynomial& d) {  // ckks.cpp:680-731
+  if (d.p_count != 0) throw std::invalid_argument("mod_up input must be Q-only");
+  const uint32_t l = d.q_count, D = ctx.num_digits(l), n = ctx.params().n;
+  HoistState h{DeviceBuffer(ctx.raw(), (size_t)D * (l + ctx.params().alpha) * n), l, D};
+  check(ck_mod_up(ctx.raw(), l, d.data.data(), h.digits.data(), nullptr));
+  return h;
+}
+
+inline std::pair<Polynomial, Polynomial> key_mult(CkksContext& ctx, const HoistState& h,
+                                                  const EvaluationKey& evk) {  // ckks.cpp:733-770
+  const uint32_t rows = h.level + ctx.params().alpha, n = ctx.params().n;
+  DeviceBuffer v(ctx.raw(), 2ull * rows * n);
+  check(ck_key_mult(ctx.raw(), h.level, h.digits.data(), evk.data.data(), v.data(), nullptr));
+  Polynomial v0{DeviceBuffer(ctx.raw(), (size_t)rows * n), h.level, ctx.params().alpha};
+  Polynomial v1{DeviceBuffer(ctx.raw(), (size_t)rows * n), h.level, ctx.params().alpha};
+  check(ck_memcpy_d2d(ctx.raw(), v0.data.data(), v.data(), (size_t)rows * n * 4, nullptr));
+  check(ck_memcpy_d2d(ctx.raw(), v1.data.data(), v.data() + (size_t)rows * n, (size_t)rows * n * 4, nullptr));
+  return {std::move(v0), std::move(v1)};
+}
+
+inline Polynomial mod_down(CkksContext& ctx, const Polynomial& v) {  // ckks.cpp:772-776
+  if (v.p_count != ctx.params().alpha) throw std::invalid_argument("mod_down expects a P-extended polynomial");
+  Polynomial out{DeviceBuffer(ctx.raw(), (size_t)v.q_count * ctx.params().n), v.q_count, 0};
+  check(ck_mod_down(ctx.raw(), v.q_count, v.data.data(), out.data.data(), nullptr));
+  return out;
+}
+
+inline std::pair<Polynomial, Polynomial> key_switch(CkksContext& ctx, const Polynomial& d,
+                                                    const EvaluationKey& evk) {  // ckks.cpp:778-787
+  if (d.p_count != 0) throw std::invalid_argument("mod_up input must be Q-only");
+  const uint32_t l = d.q_count, n = ctx.params().n;
+  DeviceBuffer out(ctx.raw(), 2ull * l * n);
+  check(ck_key_switch(ctx.raw(), l, d.data.data(), evk.data.data(), out.data(), nullptr));
+  Polynomial c0{DeviceBuffer(ctx.raw(), (size_t)l * n), l, 0}, c1{DeviceBuffer(ctx.raw(), (size_t)l * n), l, 0};
+  check(ck_memcpy_d2d(ctx.raw(), c0.data.data(), out.data(), (size_t)l * n * 4, nullptr));
+  check(ck_memcpy_d2d(ctx.raw(), c1.data.data(), out.data() + (size_t)l * n, (size_t)l * n * 4, nullptr));
+  return {std::move(c0), std::move(c1)};
+}
+
+// hoisted_rotations (ckks.cpp:899-925): one ModUp shared by every rotation
+inline std::vector<Ciphertext> hoisted_rotations(CkksContext& ctx, const Ciphertext& ct,
+                                                 const std::vector<int64_t>& rots,
+                                                 const std::vector<const EvaluationKey*>& evks) {
+  if (rots.size() != evks.size()) throw std::invalid_argument("rotation/key count mismatch");
+  std::vector<const uint32_t*> kp(rots.size());
+  for (size_t i = 0; i < rots.size(); ++i) {
+    if (rots[i] != 0 && (!evks[i] || evks[i]->kind != KeyKind::Rotation || evks[i]->rotation != rots[i]))
+      throw std::invalid_argument("rotation key mismatch");
+    kp[i] = rots[i] != 0 ? evks[i]->data.data() : nullptr;
+  }
+  const size_t w = 2ull * ct.level * ctx.params().n;
+  DeviceBuffer all(ctx.raw(), std::max<size_t>(1, rots.size()) * w);
+  check(ck_hoisted_rotations(ctx.raw(), ct.level, ct.data.data(), (uint32_t)rots.size(), rots.data(), kp.data(),
+                             all.data(), nullptr));
+  std::vector<Ciphertext> out;
+  for (size_t i = 0; i < rots.size(); ++i) {
+    Ciphertext c = make_ciphertext(ctx, ct.level, ct.scale);
+    check(ck_memcpy_d2d(ctx.raw(), c.data.data(), all.data() + i * w, w * 4, nullptr));
+    out.push_back(std::move(c));
+  }
+  return out;
+}
+
+// decrypt (ckks.cpp:541-553): m = b + a s; `s` = the secret's evaluation rows (>= level)
+inline Plaintext decrypt(CkksContext& ctx, const Ciphertext& ct, const DeviceBuffer& s) {
+  Plaintext pt{DeviceBuffer(ctx.raw(), (size_t)ct.level * ctx.params().n), ct.scale, ct.level, 0};
+  check(ck_decrypt(ctx.raw(), ct.level, 1, ct.data.data(), s.data(), pt.data.data(), nullptr));
+  return pt;
+}
+
 }  // namespace ckks32::b200

@@ -1626,6 +1626,9 @@ ck_status ck_memcpy_h2d(ck_context* ctx, void* dst, const void* src, size_t byte
 ck_status ck_memcpy_d2h(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream) {
   return guard([&] { CK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(stream))); (void)ctx; });
 }
+ck_status ck_memcpy_d2d(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream) {
+  return guard([&] { CK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, S(stream))); (void)ctx; });
+}
 ck_status ck_stream_sync(ck_context* ctx, ck_stream stream) {
   return guard([&] { CK_CUDA(cudaStreamSynchronize(S(stream))); (void)ctx; });
 }

@@ -91,6 +91,20 @@ int main(int argc, char** argv) {
     } catch (const std::invalid_argument&) {
     }
   }
+  {  // key-switching building blocks: key_switch == mod_down(key_mult(mod_up(d))) (ckks.cpp:778-787)
+    Polynomial d{DeviceBuffer(ctx.raw(), (size_t)level * p.n), level, 0};
+    check(ck_memcpy_d2d(ctx.raw(), d.data.data(), x.data.data() + (size_t)level * p.n, (size_t)level * p.n * 4,
+                        nullptr));
+    auto ks = key_switch(ctx, d, relin);
+    HoistState h = mod_up(ctx, d);
+    auto v = key_mult(ctx, h, relin);
+    Polynomial c0 = mod_down(ctx, v.first), c1 = mod_down(ctx, v.second);
+    if (ks.first.data.download() != c0.data.download() || ks.second.data.download() != c1.data.download())
+      throw std::runtime_error("key_switch != mod_down(key_mult(mod_up))");
+    // hoisted rotation by 1 == hrot by 1 (ckks.cpp:899-925)
+    auto hr = hoisted_rotations(ctx, x, {1}, {&rot});
+    if (hr[0].data.download() != r.data.download()) throw std::runtime_error("hoisted rotation != hrot");
+  }
   const uint64_t n_launch = ck_launch_count(ctx.raw());
   std::printf("cpp api ok: hmult level %u -> %u, hrot level %u, %llu kernel launches, %d contract errors\n", level,
               m.level, r.level, (unsigned long long)n_launch, errors);
