@@ -182,6 +182,13 @@ ck_status ck_encrypt_sk(ck_context* ctx, uint32_t level, const uint32_t* pt, con
                         const uint32_t* s, uint32_t* out, ck_stream stream);
 ck_status ck_encrypt_pk(ck_context* ctx, uint32_t level, const uint32_t* pt, const uint32_t* v, const uint32_t* e0,
                         const uint32_t* e1, const uint32_t* pk, uint32_t* out, ck_stream stream);
+/* One evaluation-key digit (evk_gen, ckks.cpp:459-474) over the full L+alpha
+ * rows: out_b = e + s_src * g - a * s_dst (s_src squared first when
+ * square_src: relinearisation).  g_mont: L+alpha host words, the digit's
+ * gadget factor P * dhat * (dhat^-1 mod d_k) reduced mod every prime, in
+ * Montgomery form; a, e and the secrets are evaluation-domain Montgomery rows. */
+ck_status ck_evk_digit(ck_context* ctx, const uint32_t* s_src, const uint32_t* s_dst, const uint32_t* a,
+                       const uint32_t* e, const uint32_t* g_mont, int square_src, uint32_t* out_b, ck_stream stream);
 /* coeffs_to_eval (ckks.cpp:366-380): n signed int64 coefficients (device) ->
  * rows [level + p_rows][n], each reduced mod its prime then forward NTT. */
 ck_status ck_coeffs_to_eval(ck_context* ctx, const int64_t* coeffs, uint32_t level, uint32_t p_rows, uint32_t* out,

@@ -77,6 +77,7 @@ _SIGS = {
     "ck_decrypt": [_vp, _u32, _u32, _vp, _vp, _vp, _vp],
     "ck_encrypt_sk": [_vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp],
     "ck_encrypt_pk": [_vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "ck_evk_digit": [_vp, _vp, _vp, _vp, _vp, _u32p, ctypes.c_int, _vp, _vp],
     "ck_coeffs_to_eval": [_vp, _vp, _u32, _u32, _vp, _vp],
     "ck_shard_create": [_vp, _u32, _u32, ctypes.POINTER(_vp)],
     "ck_shard_destroy": [_vp],

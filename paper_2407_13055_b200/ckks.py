@@ -500,6 +500,60 @@ def encrypt_pk(ctx: CkksContext, pt: Plaintext, pk: Ciphertext, v: Polynomial, e
     return Ciphertext(out, pt.scale, l)
 
 
+def keygen(ctx: CkksContext, rng: np.random.Generator) -> torch.Tensor:
+    """keygen (ckks.cpp:399-405): ternary secret of Hamming weight
+    params.hamming (host sampling) -> evaluation rows over the full L + alpha
+    basis (the reference's sk.s)."""
+    c = sample_ternary(ctx.n, min(ctx.params.hamming, ctx.n // 4), rng)
+    return coeffs_to_eval(ctx, c, ctx.params.l, ctx.params.alpha).data
+
+
+def pubkey_gen(ctx: CkksContext, s: torch.Tensor, rng: np.random.Generator) -> Ciphertext:
+    """pubkey_gen (ckks.cpp:407-424): (b, a) = (e - a s, a) at level L."""
+    l = ctx.params.l
+    zero = Plaintext(Polynomial(torch.zeros((l, ctx.n), dtype=torch.int32, device=ctx.device), l), Fraction(1), l)
+    return encrypt_sk(ctx, zero, s, uniform_eval(ctx, l, rng),
+                      coeffs_to_eval(ctx, sample_gaussian(ctx.n, ctx.params.sigma, rng), l))
+
+
+def evk_gen(ctx: CkksContext, s: torch.Tensor, kind: str, rotation: int, rng: np.random.Generator) -> EvaluationKey:
+    """evk_gen (ckks.cpp:426-477): digit k encrypts g_k s_src under s_dst over
+    PQ, g_k = P * dhat_k * (dhat_k^-1 mod d_k); relinearisation: s_src = s^2,
+    s_dst = s; rotation r: s_src = s, s_dst = phi_{-r}(s)."""
+    L, A, n = ctx.params.l, ctx.params.alpha, ctx.n
+    rows = L + A
+    primes = [int(v) for v in ctx.primes[:rows]]
+    full = Polynomial(s[:rows].contiguous(), L, A)
+    if kind == RELIN:
+        s_src, s_dst, square = full.data, full.data, 1
+    else:
+        s_src, square = full.data, 0
+        s_dst = apply_automorphism(ctx, full, -rotation).data
+    q_full = 1
+    for q in primes[:L]:
+        q_full *= q
+    P = 1
+    for q in primes[L:]:
+        P *= q
+    D = ctx.num_digits(L)
+    out = ctx.empty(D, 2, rows, n)
+    for k in range(D):
+        dk = 1
+        for q in primes[k * A: min((k + 1) * A, L)]:
+            dk *= q
+        dhat = q_full // dk
+        g = P * dhat * pow(dhat, -1, dk)
+        gm = [((g % q) << 32) % q for q in primes]
+        a_k = torch.cat([uniform_eval(ctx, L, rng),
+                         torch.from_numpy((rng.integers(0, 1 << 62, (A, n), dtype=np.int64)
+                                           % np.array(primes[L:], np.int64)[:, None]).astype(np.int32)).to(ctx.device)])
+        e_k = coeffs_to_eval(ctx, sample_gaussian(n, ctx.params.sigma, rng), L, A).data
+        out[k, 1] = a_k
+        nat.call("ck_evk_digit", ctx.handle, _ptr(s_src), _ptr(s_dst), _ptr(out[k, 1]), _ptr(e_k),
+                 nat.u32_array(gm), square, _ptr(out[k, 0]), ctx.stream())
+    return EvaluationKey(out, kind, rotation if kind == ROTATION else 0)
+
+
 # Host-side samplers for the encryption randomness (numpy Generator; the
 # reference samples with std::mt19937_64, ckks.cpp:390-430, so the streams
 # differ — the GPU arithmetic on given randomness is what is bit-exact).

@@ -2140,6 +2140,28 @@ ck_status ck_encrypt_pk(ck_context* ctx, uint32_t level, const uint32_t* pt, con
     check_launch();
   });
 }
+ck_status ck_evk_digit(ck_context* ctx, const uint32_t* s_src, const uint32_t* s_dst, const uint32_t* a,
+                       const uint32_t* e, const uint32_t* g_mont, int square_src, uint32_t* out_b, ck_stream stream) {
+  return guard([&] {  // evk_gen digit (ckks.cpp:459-474) over the full L + alpha rows
+    Context* c = C(ctx);
+    for (const void* p : {(const void*)s_src, (const void*)s_dst, (const void*)a, (const void*)e, (const void*)out_b})
+      check_ptr(p);
+    if (!g_mont) throw InvalidArgument("null gadget constants");
+    const uint32_t rows = c->L + c->alpha;
+    char* base = static_cast<char*>(c->scratch_get(6 * rows + 16, S(stream)));
+    uint32_t* d_g = reinterpret_cast<uint32_t*>(base);
+    uint16_t* d_rp = reinterpret_cast<uint16_t*>(base + 4 * rows);
+    std::vector<uint16_t> rp(rows);
+    for (uint32_t i = 0; i < rows; ++i) rp[i] = (uint16_t)i;
+    CK_CUDA(cudaMemcpyAsync(d_g, g_mont, 4 * rows, cudaMemcpyHostToDevice, S(stream)));
+    CK_CUDA(cudaMemcpyAsync(d_rp, rp.data(), 2 * rows, cudaMemcpyHostToDevice, S(stream)));
+    evk_digit((int)c->n, (int)rows, s_src, s_dst, a, e, d_g, d_rp, square_src, c->d_primes, out_b, S(stream));
+    CK_CUDA(cudaStreamSynchronize(S(stream)));  // host arrays are pageable
+    ++c->launches;
+    check_launch();
+  });
+}
+
 ck_status ck_coeffs_to_eval(ck_context* ctx, const int64_t* coeffs, uint32_t level, uint32_t p_rows, uint32_t* out,
                             ck_stream stream) {
   ck_status st0 = guard([&] {  // ckks.cpp:366-380: reduce mod every prime, then ntt_forward

@@ -163,6 +163,9 @@ void elementwise(int n, int rows, int batch, int op, const uint32_t* a, uint64_t
 void crypt(int n, int level, int batch, int op, const uint32_t* x, uint64_t x_bs, const uint32_t* y, const uint32_t* z,
            const uint32_t* w, const uint32_t* u, uint32_t* out, uint64_t out_bs, const PrimeDev* primes,
            cudaStream_t st);
+void evk_digit(int n, int rows, const uint32_t* s_src, const uint32_t* s_dst, const uint32_t* a, const uint32_t* e,
+               const uint32_t* gm, const uint16_t* row_prime, int square, const PrimeDev* primes, uint32_t* out,
+               cudaStream_t st);
 void reduce_coeffs(int n, int rows, const long long* c, const uint16_t* row_prime, const PrimeDev* primes,
                    uint32_t* out, cudaStream_t st);
 // out[i][j] = in[i][src[j]] (automorphism.cpp:82-87)

@@ -264,6 +264,26 @@ __global__ void __launch_bounds__(kT) k_crypt(int n, int level, int op, const ui
   }
 }
 
+// One evaluation-key digit over the full PQ basis (evk_gen, ckks.cpp:459-474):
+// b = e + s_src * g - a * s_dst, with s_src squared first for relinearisation.
+__global__ void __launch_bounds__(kT) k_evk_digit(int n, const uint32_t* __restrict__ s_src,
+                                                  const uint32_t* __restrict__ s_dst, const uint32_t* __restrict__ a,
+                                                  const uint32_t* __restrict__ e, const uint32_t* __restrict__ gm,
+                                                  const uint16_t* __restrict__ row_prime, int square,
+                                                  const PrimeDev* __restrict__ primes, uint32_t* __restrict__ out) {
+  const int k = blockIdx.x * kT + threadIdx.x;
+  if (k >= n) return;
+  const int i = blockIdx.y;
+  const PrimeDev P = primes[row_prime[i]];
+  const uint32_t q = P.q;
+  const size_t r = (size_t)i * n + k;
+  uint32_t src = s_src[r];
+  if (square) src = sub_if(mont_mul(src, src, q, P.qinv_neg), q);
+  const uint32_t sg = sub_if(mont_mul(src, gm[i], q, P.qinv_neg), q);
+  const uint32_t as = sub_if(mont_mul(a[r], s_dst[r], q, P.qinv_neg), q);
+  out[r] = sub_if(sub_if(e[r] + sg, q) + q - as, q);
+}
+
 // int64 coefficients -> canonical residues of every row (coeffs_to_eval's
 // reduction, ckks.cpp:366-380, correct() of modarith.hpp:46-50)
 __global__ void __launch_bounds__(kT) k_reduce_coeffs(int n, const long long* __restrict__ c,
@@ -357,6 +377,13 @@ void crypt(int n, int level, int batch, int op, const uint32_t* x, uint64_t x_bs
            cudaStream_t st) {
   dim3 grid(cdiv(n, kT), level, batch);
   k_crypt<<<grid, kT, 0, st>>>(n, level, op, x, x_bs, y, z, w, u, out, out_bs, primes);
+}
+
+void evk_digit(int n, int rows, const uint32_t* s_src, const uint32_t* s_dst, const uint32_t* a, const uint32_t* e,
+               const uint32_t* gm, const uint16_t* row_prime, int square, const PrimeDev* primes, uint32_t* out,
+               cudaStream_t st) {
+  dim3 grid(cdiv(n, kT), rows);
+  k_evk_digit<<<grid, kT, 0, st>>>(n, s_src, s_dst, a, e, gm, row_prime, square, primes, out);
 }
 
 void reduce_coeffs(int n, int rows, const long long* c, const uint16_t* row_prime, const PrimeDev* primes,

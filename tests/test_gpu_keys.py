@@ -1,0 +1,54 @@
+"""Key generation on the GPU (keygen / pubkey_gen / evk_gen, ckks.cpp:399-477;
+host-sampled randomness) and a fully GPU-side encrypted round trip:
+encode -> public-key encrypt -> HMult+relin / HRot -> decrypt -> decode,
+compared with the plaintext slot arithmetic within CKKS precision."""
+from __future__ import annotations
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2407_13055_b200 import ckks  # noqa: E402
+
+
+def unit(count, rng):
+    r = rng.uniform(-1.0, 1.0, (count, 2))
+    return r[:, 0] + 1j * r[:, 1]
+
+
+@pytest.mark.parametrize("n,l,a,db", [(1024, 8, 3, 48), (8192, 12, 4, 48)])
+def test_gpu_keys_encrypted_round_trip(n, l, a, db):
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db))
+    rng = np.random.default_rng(2024 + n)
+    s = ckks.keygen(C, rng)
+    assert s.shape == (l + a, n)
+    pk = ckks.pubkey_gen(C, s, rng)
+    relin = ckks.evk_gen(C, s, ckks.RELIN, 0, rng)
+    rot = ckks.evk_gen(C, s, ckks.ROTATION, 3, rng)
+    delta = Fraction(1 << db)
+
+    def enc(z):
+        pt = ckks.encode(C, z, delta, l)
+        v = ckks.coeffs_to_eval(C, ckks.sample_ternary(n, min(64, n // 4), rng), l)
+        e0 = ckks.coeffs_to_eval(C, ckks.sample_gaussian(n, 3.2, rng), l)
+        e1 = ckks.coeffs_to_eval(C, ckks.sample_gaussian(n, 3.2, rng), l)
+        return ckks.encrypt_pk(C, pt, pk, v, e0, e1)
+
+    def dec(ct):
+        return ckks.decode(C, ckks.decrypt(C, ct, s))
+
+    z1, z2 = unit(n // 2, rng), unit(n // 2, rng)
+    c1, c2 = enc(z1), enc(z2)
+    assert np.abs(dec(c1) - z1).max() < 2.0 ** -20
+    prod = ckks.hmult(C, c1, c2, relin)
+    assert np.abs(dec(prod) - z1 * z2).max() < 2.0 ** -12
+    r = ckks.hrot(C, c1, 3, rot)
+    assert np.abs(dec(r) - np.roll(z1, -3)).max() < 2.0 ** -12
+    # depth: a second multiplication on the product
+    prod2 = ckks.hmult(C, prod, ckks.hmult(C, c2, c2, relin), relin)
+    assert np.abs(dec(prod2) - z1 * z2 ** 3).max() < 2.0 ** -8
+    C.close()
