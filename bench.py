@@ -617,7 +617,7 @@ def run_helr(args):
     def const(level, scale):
         return ckks.Plaintext(ckks.Polynomial(rand_rows((), torch.arange(level, device=dev)), level, 0), scale, level)
 
-    it = HelrIteration(C, shape, relin, keys, {k: const for k in ("a3", "a1", "a0", "gamma")})
+    it = HelrIteration(C, shape, relin, keys, {k: const for k in ("mask", "a3", "a1", "a0", "gamma", "one")})
     s = Fraction(1 << DB)
     Z = ckks.Ciphertext(rand_rows((shape.cts, 2), torch.arange(L, device=dev)), s, L)
     W = ckks.Ciphertext(rand_rows((2,), torch.arange(L, device=dev)), s, L)
@@ -647,9 +647,9 @@ def run_helr(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "int32 residues (u32 mod q < 2^29, int64 accum)",
             "data": "synthetic uniform residues (ciphertexts, keys, plaintext constants), random-init",
-            "config": {"workload": "BASELINE config 5: one HELR-style gradient step (helr.py): 8 ciphertexts x 128 "
-                                   "samples x 256 features, degree-3 sigmoid, rotate-and-sum over features and "
-                                   "samples, batched mechanisms", "n": N_RING, "l": L, "alpha": ALPHA,
+            "config": {"workload": "BASELINE config 5: one HELR gradient step (helr.py): 8 ciphertexts x 128 "
+                                   "samples x 256 features, inner products by rotate-and-sum, mask + replicate, "
+                                   "degree-3 sigmoid, gradient sum over samples, batched mechanisms", "n": N_RING, "l": L, "alpha": ALPHA,
                        "features": shape.features, "samples": shape.cts * shape.samples_per_ct,
                        "rns_limbs_consumed": it.levels_used(), "ops_per_iteration": it.op_profile(),
                        "parallelism": f"dp{world} (one mini-batch per GPU)"},

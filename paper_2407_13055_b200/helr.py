@@ -15,15 +15,22 @@ per ciphertext.  The weight ciphertext W holds the model replicated per
 sample.  One iteration (gradient step with a degree-3 sigmoid):
 
     ip    = Z * W                                  HMult            (l -> l-2)
-    ip    = sum_{s=1,2,..,F/2} rot_s(ip)            log2(F) HRot + HAdd
-    x2    = ip * ip                                 HMult            (-> l-4)
-    t     = rescale(x2 (*) a3) (+) a1               PMult, rescale, PAdd (-> l-6)
-    sig   = t * ip|_(l-6)                           HMult            (-> l-8)
-    sig   = sig (+) a0                              PAdd
-    g     = sig * Z|_(l-8)                          HMult            (-> l-10)
+    ip    = sum_{s=1,2,..,F/2} rot_s(ip)            log2(F) HRot + HAdd: slot (i, 0) = <z_i, w>
+    ip    = rescale(ip (*) mask)                    PMult, rescale   (-> l-4): keep the (i, 0) slots
+    ip    = sum_{s=1,2,..,F/2} rot_{-s}(ip)         log2(F) HRot + HAdd: <z_i, w> in all F slots of i
+    x2    = ip * ip                                 HMult            (-> l-6)
+    t     = rescale(x2 (*) a3) (+) a1               PMult, rescale, PAdd (-> l-8)
+    sig   = t * ip|_(l-8)                           HMult            (-> l-10)
+    sig   = sig (+) a0                              PAdd: sig_i = a0 + a1 ip_i + a3 ip_i^3
+    g     = sig * Z|_(l-10)                         HMult            (-> l-12)
     g     = sum_{s=F,2F,..,N/4} rot_s(g)            log2(S) HRot + HAdd
-    g     = sum over the cts ciphertexts            HAdd tree
-    W'    = W|_(l-12) (+) rescale(g (*) gamma)      PMult, rescale, HAdd (-> l-12)
+    g     = sum over the cts ciphertexts            HAdd tree: slot (i, f) = sum_i' sig_i' z_i'f
+    W'    = rescale(W|_(l-12) (*) 1) + rescale(g (*) gamma)   2 PMult, 2 rescale, HAdd (-> l-14)
+
+so W' holds w + gamma * sum_i P(<z_i, w>) z_i in every sample's slots: one
+gradient step of logistic regression with the degree-3 polynomial P
+(HELR: z_i = y_i (1, x_i), P(t) ~ sigmoid(-t)); tests/test_gpu_helr.py
+checks the decrypted W' against the same step in numpy.
 
 `x|_m` keeps the first m RNS rows (a ciphertext mod Q_l is one mod Q_m).
 The ciphertexts of a mini-batch are processed as ONE batched ciphertext, so
@@ -67,8 +74,11 @@ class HelrShape:
             s <<= 1
         return out
 
+    def replicate_rotations(self) -> List[int]:
+        return [-r for r in self.feature_rotations()]
+
     def rotations(self) -> List[int]:
-        return self.feature_rotations() + self.sample_rotations()
+        return self.feature_rotations() + self.replicate_rotations() + self.sample_rotations()
 
 
 def drop(ct: ckks.Ciphertext, level: int) -> ckks.Ciphertext:
@@ -100,7 +110,7 @@ def batch_sum(ctx: ckks.CkksContext, ct: ckks.Ciphertext) -> ckks.Ciphertext:
 class HelrIteration:
     """One HELR-style gradient step over a mini-batch of encrypted samples.
 
-    `consts` maps 'a3', 'a1', 'a0', 'gamma' to a callable (level, scale) ->
+    `consts` maps 'mask', 'a3', 'a1', 'a0', 'gamma', 'one' to a callable (level, scale) ->
     Plaintext (evaluation domain, Montgomery, Q-prefix rows): the caller's
     encoder.  The scales requested here make every addition exact-scale."""
 
@@ -121,7 +131,7 @@ class HelrIteration:
         return self._pt_cache[key]
 
     def levels_used(self) -> int:
-        return 12
+        return 14
 
     def step(self, Z: ckks.Ciphertext, W: ckks.Ciphertext) -> ckks.Ciphertext:
         C, sh = self.ctx, self.shape
@@ -129,30 +139,32 @@ class HelrIteration:
             raise ValueError("Z must be a batch of `cts` ciphertexts")
         if W.batched:
             raise ValueError("W is one ciphertext")
-        if Z.level != W.level or Z.level < 14:
-            raise ValueError("Z and W must share a level >= 14")
+        if Z.level != W.level or Z.level < 16:
+            raise ValueError("Z and W must share a level >= 16")
         l = Z.level
+        D = self.ctx.default_scale()
         Wb = ckks.Ciphertext(W.data.unsqueeze(0).expand(sh.cts, *W.data.shape).contiguous(), W.scale, l)
         ip = ckks.hmult(C, Z, Wb, self.relin)                                     # l-2
         ip = rotsum(C, ip, sh.feature_rotations(), self.keys)
-        x2 = ckks.hmult(C, ip, ip, self.relin)                                    # l-4
-        t = ckks.pmult(C, x2, self._pt("a3", x2.level, self.ctx.default_scale()))
-        t = ckks.rescale(C, t)                                                    # l-6
+        ip = ckks.rescale(C, ckks.pmult(C, ip, self._pt("mask", ip.level, D)))     # l-4
+        ip = rotsum(C, ip, sh.replicate_rotations(), self.keys)
+        x2 = ckks.hmult(C, ip, ip, self.relin)                                    # l-6
+        t = ckks.rescale(C, ckks.pmult(C, x2, self._pt("a3", x2.level, D)))       # l-8
         t = ckks.padd(C, t, self._pt("a1", t.level, t.scale))
-        sig = ckks.hmult(C, t, drop(ip, t.level), self.relin)                     # l-8
+        sig = ckks.hmult(C, t, drop(ip, t.level), self.relin)                     # l-10
         sig = ckks.padd(C, sig, self._pt("a0", sig.level, sig.scale))
-        g = ckks.hmult(C, sig, drop(Z, sig.level), self.relin)                    # l-10
+        g = ckks.hmult(C, sig, drop(Z, sig.level), self.relin)                    # l-12
         g = rotsum(C, g, sh.sample_rotations(), self.keys)
         g = batch_sum(C, g)
-        # W' = W + gamma * g with the plaintext scale chosen so the sum is exact-scale
-        lo = g.level - 2
-        qq = int(C.q_primes[g.level - 2]) * int(C.q_primes[g.level - 1])
-        upd = ckks.pmult(C, g, self._pt("gamma", g.level, W.scale * qq / g.scale))
-        upd = ckks.rescale(C, upd)                                                # l-12
-        return ckks.hadd(C, drop(W, lo), upd)
+        # W' = W * 1 + g * gamma: both products rescaled to the common scale
+        # g.scale * Delta / qq, so the final HAdd meets the exact-scale check with
+        # every plaintext scale <= 2^60 (encode's range, ckks.cpp:284-285)
+        upd = ckks.rescale(C, ckks.pmult(C, g, self._pt("gamma", g.level, D)))   # l-14
+        wl = ckks.rescale(C, ckks.pmult(C, drop(W, g.level), self._pt("one", g.level, g.scale * D / W.scale)))
+        return ckks.hadd(C, wl, upd)
 
     def op_profile(self) -> Dict[str, int]:
         """Mechanism calls per iteration (each batched over `cts` where it applies)."""
         sh = self.shape
-        return {"hmult": 4, "hrot": len(sh.rotations()), "pmult": 2, "rescale": 2, "padd": 2,
+        return {"hmult": 4, "hrot": len(sh.rotations()), "pmult": 4, "rescale": 4, "padd": 2,
                 "hadd": len(sh.rotations()) + (sh.cts - 1).bit_length() + 1}

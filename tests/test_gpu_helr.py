@@ -93,18 +93,23 @@ def test_helr_iteration_bit_exact_vs_oracle():
     s = Fraction(1 << DB)
     it = HelrIteration(C, shape, ckks.EvaluationKey(dev(relin)),
                        {r: ckks.EvaluationKey(dev(k), ckks.ROTATION, r) for r, k in rots.items()},
-                       {k: const(k) for k in ("a3", "a1", "a0", "gamma")})
+                       {k: const(k) for k in ("mask", "a3", "a1", "a0", "gamma", "one")})
     Zg = ckks.Ciphertext(dev(np.stack([np.stack([z.b, z.a]) for z in Zs])), s, L)
     Wg = ckks.Ciphertext(dev(np.stack([W.b, W.a])), s, L)
     out = it.step(Zg, Wg)
     torch.cuda.synchronize()
-    assert out.level == L - 12
+    assert out.level == L - 14
 
     # ---- the same sequence through the oracle, ciphertext by ciphertext
     gs = []
     for z in Zs:
         ip = o_hmult(O, z, W, relin)
         for r in shape.feature_rotations():
+            rr = o_hrot(O, ip, r, rots[r])
+            ip = OCt(o_add(O, ip.b, rr.b), o_add(O, ip.a, rr.a), ip.level)
+        p = pts[("mask", ip.level)]
+        ip = o_rescale(O, OCt(o_mont(O, ip.b, p), o_mont(O, ip.a, p), ip.level))
+        for r in shape.replicate_rotations():
             rr = o_hrot(O, ip, r, rots[r])
             ip = OCt(o_add(O, ip.b, rr.b), o_add(O, ip.a, rr.a), ip.level)
         x2 = o_hmult(O, ip, ip, relin)
@@ -125,7 +130,59 @@ def test_helr_iteration_bit_exact_vs_oracle():
     g = gs[0]
     p = pts[("gamma", g.level)]
     upd = o_rescale(O, OCt(o_mont(O, g.b, p), o_mont(O, g.a, p), g.level))
-    Wd = o_drop(W, upd.level)
-    want = np.stack([o_add(O, Wd.b, upd.b), o_add(O, Wd.a, upd.a)])
+    Wd = o_drop(W, g.level)
+    p1 = pts[("one", g.level)]
+    wl = o_rescale(O, OCt(o_mont(O, Wd.b, p1), o_mont(O, Wd.a, p1), g.level))
+    want = np.stack([o_add(O, wl.b, upd.b), o_add(O, wl.a, upd.a)])
     np.testing.assert_array_equal(out.data.cpu().numpy().astype(np.uint32), want)
+    C.close()
+
+
+def test_helr_iteration_decrypts_to_the_logistic_regression_step():
+    """Real data end to end on the GPU: keys (keygen / evk_gen), encoded and
+    encrypted samples z_i = y_i (1, x_i) and weights, one HELR step, decrypt
+    and decode -> w + gamma * sum_i P(<z_i, w>) z_i computed in numpy."""
+    n, l, a, db = 8192, 24, 8, 55
+    shape = HelrShape(n=n, features=16, cts=2)
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db))
+    rng = np.random.default_rng(31337)
+    s = ckks.keygen(C, rng)
+    pk = ckks.pubkey_gen(C, s, rng)
+    relin = ckks.evk_gen(C, s, ckks.RELIN, 0, rng)
+    keys = {r: ckks.evk_gen(C, s, ckks.ROTATION, r, rng) for r in shape.rotations()}
+    delta = Fraction(1 << db)
+    F, S = shape.features, shape.samples_per_ct
+    nsamp = shape.cts * S
+    x = rng.normal(0.0, 0.3, (nsamp, F - 1))
+    y = rng.choice([-1.0, 1.0], nsamp)
+    z = y[:, None] * np.concatenate([np.ones((nsamp, 1)), x], 1) / 4.0  # |<z, w>| stays well inside [-8, 8]
+    w = rng.normal(0.0, 0.5, F)
+    a0, a1, a3, gamma = 0.5, -0.15012, 0.001593, 1.0 / nsamp  # HELR's degree-3 sigmoid(-t)
+
+    def enc(slots):
+        pt = ckks.encode(C, slots, delta, l)
+        v = ckks.coeffs_to_eval(C, ckks.sample_ternary(n, 64, rng), l)
+        e0 = ckks.coeffs_to_eval(C, ckks.sample_gaussian(n, 3.2, rng), l)
+        e1 = ckks.coeffs_to_eval(C, ckks.sample_gaussian(n, 3.2, rng), l)
+        return ckks.encrypt_pk(C, pt, pk, v, e0, e1)
+
+    Zc = [enc(z[k * S:(k + 1) * S].reshape(-1)) for k in range(shape.cts)]
+    Z = ckks.Ciphertext(torch.stack([c.data for c in Zc]), delta, l)
+    W = enc(np.tile(w, S))
+    mask = np.tile(np.eye(1, F).ravel(), S)
+    vals = {"mask": mask, "a3": a3, "a1": a1, "a0": a0, "gamma": gamma, "one": 1.0}
+
+    def const(name):
+        def make(level, scale):
+            v = vals[name]
+            return ckks.encode(C, v if np.ndim(v) else np.full(n // 2, v), scale, level)
+        return make
+
+    it = HelrIteration(C, shape, relin, keys, {k: const(k) for k in vals})
+    out = it.step(Z, W)
+    got = ckks.decode(C, ckks.decrypt(C, out, s)).real.reshape(S, F)
+    ip = z @ w
+    grad = ((a0 + a1 * ip + a3 * ip ** 3)[:, None] * z).sum(0)
+    want = w + gamma * grad
+    assert np.abs(got - want[None, :]).max() < 1e-6
     C.close()
