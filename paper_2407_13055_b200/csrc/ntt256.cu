@@ -739,7 +739,10 @@ constexpr int kKSmem = 2 * kKBuf * 4 + kRRows * kR * 8;
 // together at the item start (one cp.async group per digit, one buffer per
 // digit), so only the first digit's load latency is exposed; digit k waits
 // for its own group.  Otherwise each digit's tile is loaded when needed.
-template <bool EARLY = false, int MINB = 1, bool ALLD = false>
+// WL (with ALLD): every warp stages its own two rows of the tile and of the
+// twiddle tables, so the CTA never synchronises: the four warps are
+// independent pipelines (no __syncthreads in the loop).
+template <bool EARLY = false, int MINB = 1, bool ALLD = false, bool WL = false>
 __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, const uint2* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
@@ -758,11 +761,19 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
     const int g = i < a.level ? i : a.L + (i - a.level);
     const PrimeDev P = a.primes[g];
     const uint32_t q = P.q, q2 = P.q2;
-    if (ALLD) __syncthreads();  // every thread is done with the previous item's tile buffers
+    const int warp = tid >> 5, lane = tid & 31;
+    if (ALLD) {  // every thread (warp) is done with the previous item's tile buffers
+      if (WL) __syncwarp();
+      else __syncthreads();
+    }
     if (key != cur_key) {
       if (!ALLD) __syncthreads();
       const uint2* T = tw2 + ((size_t)g * kR + tile * kRRows) * kR;
-      for (int e = tid; e < kRRows * kR / 2; e += kKT) cp16(&tws[2 * e], &T[2 * e]);
+      if (WL) {  // this warp's two rows of the tables
+        for (int e = lane; e < 2 * kR / 2; e += 32) cp16(&tws[2 * warp * kR + 2 * e], &T[2 * warp * kR + 2 * e]);
+      } else {
+        for (int e = tid; e < kRRows * kR / 2; e += kKT) cp16(&tws[2 * e], &T[2 * e]);
+      }
       cp_commit();
       cur_key = key;
     }
@@ -772,10 +783,18 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
         if (!(i >= lo && i < hi)) {
           const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)tile * kRRows * kR;
           uint32_t* buf = sbuf + k * kKBuf;
+          if (WL) {  // this warp's two rows
 #pragma unroll
-          for (int m = 0; m < kRRows * 64 / kKT; ++m) {
-            const int e = tid + m * kKT, rr = e >> 6, c = (e & 63) * 4;
-            cp16(buf + rr * kRowStride + rpos(c), gsrc + rr * kR + c);
+            for (int m = 0; m < 4; ++m) {
+              const int e = lane + 32 * m, rr = 2 * warp + (e >> 6), c = (e & 63) * 4;
+              cp16(buf + rr * kRowStride + rpos(c), gsrc + rr * kR + c);
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < kRRows * 64 / kKT; ++m) {
+              const int e = tid + m * kKT, rr = e >> 6, c = (e & 63) * 4;
+              cp16(buf + rr * kRowStride + rpos(c), gsrc + rr * kR + c);
+            }
           }
         }
         cp_commit();
@@ -818,6 +837,8 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
           if (pend >= 2) cp_wait<2>();
           else if (pend == 1) cp_wait<1>();
           else cp_wait<0>();
+          if (WL) __syncwarp();
+          else __syncthreads();
         } else {
           buf = sbuf + kbuf * kKBuf;
           kbuf ^= 1;
@@ -829,8 +850,8 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
           }
           cp_commit();
           cp_wait<0>();
+          __syncthreads();
         }
-        __syncthreads();
         uint32_t* line = buf + rho * kRowStride;
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = line[rpos(tau + 16 * j)];
@@ -934,19 +955,19 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
 // (default when D <= 3), 3 = the same with per-digit tile loads (4.83 TB/s),
 // 1 = per-digit loads at 3 CTAs/SM (4.20), 2 = key halves loaded after the
 // row pass (the first version, 4.77).
-template <bool EARLY, int MINB, bool ALLD = false>
+template <bool EARLY, int MINB, bool ALLD = false, bool WL = false>
 static void launch_km(const KeyMultLaunch& a, const uint2* tw2, int items, cudaStream_t st) {
   static int grid = 0;
   constexpr int smem = ALLD ? kKSmem + kKBuf * 4 : kKSmem;
   if (!grid) {
-    cudaFuncSetAttribute(k_row_keymult<EARLY, MINB, ALLD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_row_keymult<EARLY, MINB, ALLD, WL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult<EARLY, MINB, ALLD>, kKT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult<EARLY, MINB, ALLD, WL>, kKT, smem);
     grid = sms * std::max(1, per);
   }
-  k_row_keymult<EARLY, MINB, ALLD><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
+  k_row_keymult<EARLY, MINB, ALLD, WL><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
 }
 
 void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
@@ -962,8 +983,10 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
     launch_km<false, 4>(a, tw2, items, st);
   else if (ver == 3 || a.D > 3)
     launch_km<true, 4>(a, tw2, items, st);
-  else
+  else if (ver == 4)
     launch_km<true, 4, true>(a, tw2, items, st);
+  else
+    launch_km<true, 4, true, true>(a, tw2, items, st);
 }
 
 void conv_mid(const ConvMidLaunch& a, cudaStream_t st) {
