@@ -317,6 +317,15 @@ __device__ __forceinline__ void row_prefetch(uint32_t* buf, const uint32_t* g) {
   }
 }
 
+// the two rows (2 warp, 2 warp + 1) of a kRRows x 256 tile that warp `warp` owns
+__device__ __forceinline__ void row_prefetch_warp(uint32_t* buf, const uint32_t* g, int warp, int lane) {
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int e = lane + 32 * m, r = 2 * warp + (e >> 6), c = (e & 63) * 4;
+    cp16(buf + r * kRowStride + rpos(c), g + r * kR + c);
+  }
+}
+
 // (job, row tile, b) item cursor, b fastest
 struct RowCursor {
   int b, tile, job;
@@ -367,7 +376,8 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
     return INV ? src + x.b * src_bs + (size_t)J.src_off * kN + x.tile * kRRows * kR
                : dst + x.b * dst_bs + (size_t)J.dst_off * kN + x.tile * kRRows * kR;
   };
-  row_prefetch(sbuf, in_ptr(nx, Jn));
+  const int warp = tid >> 5, lane = tid & 31;
+  row_prefetch_warp(sbuf, in_ptr(nx, Jn), warp, lane);
   cp_commit();
   // this thread's 15 per-thread twiddle pairs (forward phase B / inverse phase
   // A), kept in registers across the batch items of one (job, row tile)
@@ -378,21 +388,21 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
     const int b = c.b, tile = c.tile;
     const RowJob J = Jc;
     const bool reload = it == i0 || b == 0;
-    if (reload) {  // stage this tile's twiddle tables (kRRows x 2 KB)
-      __syncthreads();
-      const uint2* T = tw2 + ((size_t)J.prime * kR + tile * kRRows) * kR;
-      for (int e = tid; e < kRRows * kR / 2; e += kRT) cp16(&tws[2 * e], &T[2 * e]);
+    if (reload) {  // stage this warp's two rows of the tile's twiddle tables (2 x 2 KB)
+      __syncwarp();
+      const uint2* T = tw2 + ((size_t)J.prime * kR + tile * kRRows + 2 * warp) * kR;
+      for (int e = lane; e < kR; e += 32) cp16(&tws[2 * warp * kR + 2 * e], &T[2 * e]);
       cp_commit();
     }
     if (it + 1 < i1) {
       const int pj = nx.job;
       nx.next(batch);
       if (nx.job != pj) Jn = jobs[nx.job];
-      row_prefetch(sbuf + ((k + 1) & 1) * kRowBufWords, in_ptr(nx, Jn));
+      row_prefetch_warp(sbuf + ((k + 1) & 1) * kRowBufWords, in_ptr(nx, Jn), warp, lane);
     }
     cp_commit();
     cp_wait<1>();
-    __syncthreads();
+    __syncwarp();  // each warp owns its two rows of every buffer: no CTA barrier
     const int r = tile * kRRows + rho;
     const uint2* W = tws + rho * kR;
     if (reload) {
@@ -508,7 +518,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
     }
     c = nx;
     Jc = Jn;
-    __syncthreads();  // data buffer k&1 is refilled by the prefetch of iteration k+1
+    __syncwarp();  // this warp's rows of buffer k&1 are refilled by the prefetch of iteration k+1
   }
   cp_wait<0>();
 }
