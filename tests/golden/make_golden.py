@@ -41,6 +41,9 @@ FULL = {  # config -> list of (op, level, rot)
                           + [("hrot", lv, 1) for lv in range(24, 0, -2)]
                           + [("hrot", 24, 5), ("hrot", 24, -3), ("hrot", 24, 16384)]),
     "n131072_l24_a8_d55": (131072, 24, 8, 55, [("hmult", 24, 0), ("hrot", 24, 1), ("ntt", 24, 0)]),
+    # the reference's default CkksParams (ckks.hpp:46-54): D = 4 digits with a ragged 12-row last digit
+    "n65536_l54_a14_d48": (65536, 54, 14, 48, [("hmult", 54, 0), ("hrot", 54, 1), ("hmult", 30, 0),
+                                               ("key_switch", 54, 0), ("hrot", 13, -7)]),
 }
 SEED = 4242
 
