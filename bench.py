@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--e2e-chunk", type=int, default=4, help="ciphertexts per H2D/compute/D2H chunk")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="skip the B=1 eager / CUDA-graph measurement")
-    ap.add_argument("--sweep", action="store_true", help="also report the HRot level sweep (config 2)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the HRot level x batch sweep (config 2)")
     ap.add_argument("--workload", default="dp", choices=["dp", "limb", "helr"],
                     help="dp: batched independent ciphertexts (configs 1-3, the headline); limb: one ciphertext "
                          "limb-sharded over the ranks at N=2^17 (config 4); helr: HELR-style logistic-regression "
@@ -428,19 +428,22 @@ def main():
                  "note": "one HMult+relin + one HRot per step on one ciphertext; graph = pipeline.CapturedStep "
                          "(2 streams: HMult and HRot forked inside the graph)"}
 
-    sweep = None
-    if args.sweep:
-        sweep = {}
-        for lv in range(LEVEL, 0, -2):
-            Xl = ckks.Ciphertext(X.data[:, :, :lv].contiguous(), s, lv)
+    # ---- config 2: HRot over every level (batch B) and a batch sweep at four levels
+    sweep = grid = None
+    if not args.no_sweep:
+        def hrot_rate(Bs, lv, reps=3):
+            Xl = ckks.Ciphertext(X.data[:Bs, :, :lv].contiguous(), s, lv)
             ckks.hrot(C, Xl, 1, rot)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
-            for _ in range(3):
+            for _ in range(reps):
                 ckks.hrot(C, Xl, 1, rot)
             b.record(st)
             torch.cuda.synchronize(dev)
-            sweep[lv] = round(3 * B / (a.elapsed_time(b) / 1e3), 1)
+            return round(reps * Bs / (a.elapsed_time(b) / 1e3), 1)
+
+        sweep = {lv: hrot_rate(B, lv) for lv in range(LEVEL, 0, -2)}
+        grid = {f"l{lv}": {f"B{bs}": hrot_rate(bs, lv) for bs in (1, 4, 16, B) if bs <= B} for lv in (24, 16, 8, 2)}
 
     if rank == 0:
         cpu = None if args.no_cpu or world > 1 else cpu_baseline_leg()
@@ -469,6 +472,7 @@ def main():
             line["single_ciphertext"] = small
         if sweep:
             line["hrot_level_sweep_ops_per_s"] = sweep
+            line["hrot_level_batch_sweep_ops_per_s"] = grid
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
