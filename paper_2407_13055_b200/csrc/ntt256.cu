@@ -16,7 +16,10 @@
 //  * row pass: 16 threads (half a warp) own a 256-point row; the exchange is
 //    warp-local (no CTA barrier); the row's 30 twiddle pairs live in
 //    registers and are reused across consecutive batch items of the job.
-// Butterflies: Harvey-lazy Shoup (IMAD.HI + 2 IMAD, values in [0, 4q)).
+// Butterflies: Harvey-lazy Shoup (IMAD.HI + 2 IMAD).  Inverse: values in
+// [0, 2q).  Forward: values in [0, 8q) (q < 2^29), x reduced by 4q only at
+// every other stage (`ctl`), the column pass hands [0, 8q) to the row pass
+// through HBM and the row pass canonicalises once at the end.
 #include <algorithm>
 #include <cstdlib>
 
@@ -47,6 +50,21 @@ __device__ __forceinline__ void ct(uint32_t& x, uint32_t& y, uint32_t w, uint32_
   x = xx + t;
   y = xx - t + q2;
 }
+// forward CT butterfly on the lazy [0, 8q) schedule (q < 2^29, so 8q < 2^32):
+// RED reduces x from [0, 8q) to [0, 4q) (outputs [0, 6q)); without it the
+// bound grows by 2q (outputs < B + 2q).  Reducing at every other stage keeps
+// every value below 8q with half the sub_if work of `ct`.
+template <bool RED>
+__device__ __forceinline__ void ctl(uint32_t& x, uint32_t& y, uint32_t w, uint32_t wp, uint32_t q, uint32_t q2,
+                                    uint32_t q4) {
+  const uint32_t xx = RED ? sub_if(x, q4) : x;
+  const uint32_t t = shoup_mul(y, w, wp, q);
+  x = xx + t;
+  y = xx - t + q2;
+}
+__device__ __forceinline__ uint32_t canon8(uint32_t x, uint32_t q, uint32_t q2, uint32_t q4) {
+  return sub_if(sub_if(sub_if(x, q4), q2), q);  // [0, 8q) -> [0, q)
+}
 // inverse GS butterfly: x,y in [0,2q) -> [0,2q)
 __device__ __forceinline__ void gs(uint32_t& x, uint32_t& y, uint32_t w, uint32_t wp, uint32_t q, uint32_t q2) {
   const uint32_t u = sub_if(x + y, q2);
@@ -72,8 +90,10 @@ __device__ __forceinline__ void gs4(uint4& x, uint4& y, uint2 w, uint32_t q, uin
 // multiplies of every butterfly in separate passes (all IMAD.HI, then all
 // q * hi, then all y * w - q * hi), so 16 independent multiplies sit between
 // dependent ones instead of 4 (the `wait` stall of the per-butterfly order).
-template <int T0, class TWF>
-__device__ __forceinline__ void ct_stages16(uint4 (&v)[16], TWF tw, uint32_t q, uint32_t q2) {
+// RED: bit t set = stage t reduces x from [0, 8q) to [0, 4q) first (lazy
+// schedule of `ctl`); clear = x is used as is.
+template <int T0, unsigned RED, class TWF>
+__device__ __forceinline__ void ct_stages16(uint4 (&v)[16], TWF tw, uint32_t q, uint32_t q2, uint32_t q4) {
 #pragma unroll
   for (int t = T0; t < 4; ++t) {
     const int d = 8 >> t;
@@ -102,7 +122,7 @@ __device__ __forceinline__ void ct_stages16(uint4 (&v)[16], TWF tw, uint32_t q, 
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const uint32_t tt = y[c] * ww - h[4 * pp + c];  // shoup_mul: [0, 2q)
-          const uint32_t xx = sub_if(x[c], q2);
+          const uint32_t xx = ((RED >> t) & 1u) ? sub_if(x[c], q4) : x[c];
           x[c] = xx + tt;
           y[c] = xx - tt + q2;
         }
@@ -189,7 +209,7 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
     }
     __syncthreads();
     const PrimeDev P = primes[J.prime];
-    const uint32_t q = P.q, q2 = P.q2;
+    const uint32_t q = P.q, q2 = P.q2, q4 = 2 * P.q2;
     const uint2* TW = TWR ? twring + (k & 1) * 256 : B.tw;
     uint32_t* out = dst + b * dst_bs + (size_t)J.dst_off * kN + tile * kCCols + 4 * cq;
     uint4 v[16];
@@ -210,9 +230,9 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
           CK_E(x) CK_E(y) CK_E(z) CK_E(w)
 #undef CK_E
         }
-        ct_stages16<1>(v, [&](int t, int blk) { return TW[(1 << t) + blk]; }, q, q2);
+        ct_stages16<1, 0x4>(v, [&](int t, int blk) { return TW[(1 << t) + blk]; }, q, q2, q4);
       } else {
-        ct_stages16<0>(v, [&](int t, int blk) { return TW[(1 << t) + blk]; }, q, q2);
+        ct_stages16<0, 0x4>(v, [&](int t, int blk) { return TW[(1 << t) + blk]; }, q, q2, q4);
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) B.tile[(tau + 16 * j) * 8 + cq] = v[j];
@@ -232,8 +252,8 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
         cp_commit();
       }
       // phase B rows 16 tau + j: twiddle 2^s + tau 2^(s-4) + blk
-      ct_stages16<0>(v, [&](int t, int blk) { return TWR ? TW[(16 << t) + (tau << t) + blk] : twb[(1 << t) - 1 + blk]; },
-                     q, q2);
+      ct_stages16<0, 0x5>(
+          v, [&](int t, int blk) { return TWR ? TW[(16 << t) + (tau << t) + blk] : twb[(1 << t) - 1 + blk]; }, q, q2, q4);
 #pragma unroll
       for (int j = 0; j < 16; ++j) stg4(out + (16 * tau + j) * kR, v[j]);
     } else {
@@ -382,7 +402,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
   // this thread's 15 per-thread twiddle pairs (forward phase B / inverse phase
   // A), kept in registers across the batch items of one (job, row tile)
   uint2 twr[15];
-  uint32_t q = 0, q2 = 0;
+  uint32_t q = 0, q2 = 0, q4 = 0;
   for (int it = i0, k = 0; it < i1; ++it, ++k) {
     uint32_t* line_buf = sbuf + (k & 1) * kRowBufWords;
     const int b = c.b, tile = c.tile;
@@ -409,6 +429,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
       const PrimeDev P = primes[J.prime];
       q = P.q;
       q2 = P.q2;
+      q4 = 2 * P.q2;
     }
     if (reload) {
 #pragma unroll
@@ -428,7 +449,8 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
         for (int p = 0; p < 8; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
           const uint2 w = W[(1 << t) - 1 + blk];
-          ct(v[j], v[j + d], w.x, w.y, q, q2);
+          if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
         }
       }
 #pragma unroll
@@ -450,7 +472,8 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
         for (int p = 0; p < 8; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
           const uint2 w = twr[(1 << t) - 1 + blk];
-          ct(v[j], v[j + d], w.x, w.y, q, q2);
+          if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
         }
       }
       if (COMB) {  // J.dst_off = p * out_q + i; v row p * prow + i; prime i
@@ -461,17 +484,17 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
         for (int m = 0; m < 4; ++m) {
           const uint4 vv = *reinterpret_cast<const uint4*>(vr + 4 * m);
           uint4 o;
-          o.x = sub_if(mont_mul(vv.x - canon4(v[4 * m], q, q2) + q, di, q, qinv), q);
-          o.y = sub_if(mont_mul(vv.y - canon4(v[4 * m + 1], q, q2) + q, di, q, qinv), q);
-          o.z = sub_if(mont_mul(vv.z - canon4(v[4 * m + 2], q, q2) + q, di, q, qinv), q);
-          o.w = sub_if(mont_mul(vv.w - canon4(v[4 * m + 3], q, q2) + q, di, q, qinv), q);
+          o.x = sub_if(mont_mul(vv.x - canon8(v[4 * m], q, q2, q4) + q, di, q, qinv), q);
+          o.y = sub_if(mont_mul(vv.y - canon8(v[4 * m + 1], q, q2, q4) + q, di, q, qinv), q);
+          o.z = sub_if(mont_mul(vv.z - canon8(v[4 * m + 2], q, q2, q4) + q, di, q, qinv), q);
+          o.w = sub_if(mont_mul(vv.w - canon8(v[4 * m + 3], q, q2, q4) + q, di, q, qinv), q);
           stg4(orow + 16 * tau + 4 * m, o);
         }
       } else {
 #pragma unroll
         for (int m = 0; m < 4; ++m)
-          stg4(orow + 16 * tau + 4 * m, make_uint4(canon4(v[4 * m], q, q2), canon4(v[4 * m + 1], q, q2),
-                                                   canon4(v[4 * m + 2], q, q2), canon4(v[4 * m + 3], q, q2)));
+          stg4(orow + 16 * tau + 4 * m, make_uint4(canon8(v[4 * m], q, q2, q4), canon8(v[4 * m + 1], q, q2, q4),
+                                                   canon8(v[4 * m + 2], q, q2, q4), canon8(v[4 * m + 3], q, q2, q4)));
       }
     } else {
       // phase A: c = 16 tau + j, inverse stages 0..3 (W[k*16 + tau])
@@ -770,7 +793,7 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
     const int b = it % B, key = it / B, tile = key % kTiles, i = key / kTiles;
     const int g = i < a.level ? i : a.L + (i - a.level);
     const PrimeDev P = a.primes[g];
-    const uint32_t q = P.q, q2 = P.q2;
+    const uint32_t q = P.q, q2 = P.q2, q4 = 2 * P.q2;
     const int warp = tid >> 5, lane = tid & 31;
     if (ALLD) {  // every thread (warp) is done with the previous item's tile buffers
       if (WL) __syncwarp();
@@ -872,7 +895,8 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
           for (int p = 0; p < 8; ++p) {
             const int blk = p / d, j = blk * 2 * d + p % d;
             const uint2 w = W[(1 << t) - 1 + blk];
-            ct(v[j], v[j + d], w.x, w.y, q, q2);
+            if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
           }
         }
 #pragma unroll
@@ -893,11 +917,12 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
           for (int p = 0; p < 8; ++p) {
             const int blk = p / d, j = blk * 2 * d + p % d;
             const uint2 w = W[16 + ((1 << t) - 1 + blk) * 16 + tau];
-            ct(v[j], v[j + d], w.x, w.y, q, q2);
+            if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
           }
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = canon4(v[j], q, q2);
+        for (int j = 0; j < 16; ++j) v[j] = canon8(v[j], q, q2, q4);
       }
       // KeyMult MACs with both key halves (rows indexed by the global prime, ckks.cpp:747)
       const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
