@@ -302,6 +302,7 @@ struct Context {
   bool use_row_km = true;
   bool use_fused_combine = true;  // CK32_NO_FUSED_COMBINE=1: separate k_combine after the ModDown NTT
   bool use_tc = false;  // CK32_TC=1: tcgen05 split-word BConv (bit-exact; slower than the CUDA-core kernel today)  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
+  int bconv_fp64 = 0;   // CK32_BCONV_FP64=1|2|3: exact BConv dot products on the FP64 pipe for all / 1 of 2 / 2 of 3 rows
   bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
   int ntt_chunk_limbs = 1 << 30;  // limbs per pass-1/pass-2 launch pair (CK32_NTT_CHUNK; measured: no gain)
   std::map<uint32_t, std::unique_ptr<ModUpPlan>> modup;
@@ -822,7 +823,7 @@ struct Context {
       t.max_dc = pl.tc_max_dc;
       bconv_tc((int)n, a, t, st);
     } else {
-      bconv((int)n, a, st);
+      bconv((int)n, a, st, bconv_fp64);
     }
     ++launches;
   }
@@ -1483,6 +1484,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     c->use_fused = std::getenv("CK32_FUSED") != nullptr;
     c->use_row_km = std::getenv("CK32_NO_ROW_KEYMULT") == nullptr;
     c->use_tc = std::getenv("CK32_TC") != nullptr;
+    if (const char* f = std::getenv("CK32_BCONV_FP64")) c->bconv_fp64 = std::atoi(f);
     c->use_fused_combine = std::getenv("CK32_NO_FUSED_COMBINE") == nullptr;
     c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;
     if (n == 65536) {

@@ -90,7 +90,9 @@ struct BconvLaunch {
   const uint16_t* dst_prime = nullptr;
   const PrimeDev* primes = nullptr;
 };
-void bconv(int n, const BconvLaunch& a, cudaStream_t st);
+// fp64_mode 0: IMAD.WIDE dot products (k_bconv); 1-3: exact dot products on
+// the FP64 pipe for all / every other / two of three destination rows
+void bconv(int n, const BconvLaunch& a, cudaStream_t st, int fp64_mode = 0);
 // tensor-core BConv (bconv_tc.cu): tcgen05 u8 split-word GEMM, TMEM accumulator
 struct BconvTc {
   const unsigned char* btab = nullptr;  // per-group B tables (canonical UMMA layout)

@@ -75,6 +75,221 @@ __global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
   if (i < (int)G.dc) one(i);
 }
 
+// ------------------------------------------------------- bconv, FP64 pipe --
+// The CUDA-core BConv above is bound by the integer multiply pipe (IMAD.WIDE
+// occupies fmaheavy for two issue slots; ncu: fmaheavy 79%, math-pipe
+// throttle the top stall).  B200 has a full-rate FP64 pipe next to it, and
+// the dot products sum_j s_j c_ij can be computed EXACTLY there:
+//   c = c_lo + 2^15 c_hi (c_lo < 2^15, c_hi < 2^14 as c < q < 2^29),
+//   s < 2^32, SC <= 16  =>  sum_j s_j c_lo < 2^51, sum_j s_j c_hi < 2^50;
+// each partial sum is accumulated by DFMA on top of 2^52, where the spacing of
+// doubles is exactly 1, so every product (< 2^49) and every partial sum is an
+// exactly representable integer and no rounding ever happens.  The integer is
+// then read straight from the bit pattern (bits(2^52 + S) = 0x4330... + S) and
+// t = S_lo + 2^15 S_hi is the same 64-bit sum the IMAD.WIDE path forms, so
+// the Montgomery reduction and the canonical output are bit-identical.
+// MODE selects which destination rows go to the FP64 pipe: 1 = all, 2 = every
+// other row (the rest on IMAD.WIDE), 3 = two of every three.  Two adjacent
+// coefficients per thread (uint2) keep the double copies of the sources in
+// registers.
+constexpr int kTD = 256;
+template <int SC, int MODE>
+__global__ void __launch_bounds__(kTD) k_bconv_df(BconvLaunch a, int n) {
+  __shared__ uint32_t cm[kMaxRows * SC];
+  __shared__ double2 cd[kMaxRows * SC];
+  __shared__ uint4 rc[kMaxRows];  // {q, qinv_neg, dst row, 0}
+  const BconvGroup G = a.groups[blockIdx.y];
+  for (int e = threadIdx.x; e < G.dc * SC; e += kTD) {
+    const int i = e / SC, j = e % SC;
+    const uint32_t c = j < (int)G.sc ? a.cmat[G.cmat_off + i * G.sc + j] : 0u;
+    cm[e] = c;
+    cd[e] = make_double2((double)(c & 0x7fffu), (double)(c >> 15));
+  }
+  for (int i = threadIdx.x; i < (int)G.dc; i += kTD) {
+    const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
+    rc[i] = make_uint4(P.q, P.qinv_neg, a.dst_row[G.map_off + i], 0);
+  }
+  __syncthreads();
+  const int x = (blockIdx.x * kTD + threadIdx.x) * 2;
+  if (x >= n) return;
+  const uint32_t* src = a.src + blockIdx.z * a.src_bs + (size_t)G.src_off * n + x;
+  uint2 s[SC];
+  double2 sd[SC];
+#pragma unroll
+  for (int j = 0; j < SC; ++j) {
+    s[j] = j < (int)G.sc ? *reinterpret_cast<const uint2*>(src + (size_t)j * n) : make_uint2(0, 0);
+    sd[j] = make_double2((double)s[j].x, (double)s[j].y);
+  }
+  uint32_t* dst = a.dst + blockIdx.z * a.dst_bs + x;
+  auto store = [&](int i, uint64_t t0, uint64_t t1) {
+    const uint4 R = rc[i];
+    *reinterpret_cast<uint2*>(dst + (size_t)R.z * n) =
+        make_uint2(sub_if(mont_reduce64(t0, R.x, R.y), R.x), sub_if(mont_reduce64(t1, R.x, R.y), R.x));
+  };
+  auto row_fp = [&](int i) {
+    constexpr double kM = 4503599627370496.0;  // 2^52
+    double l0 = kM, h0 = kM, l1 = kM, h1 = kM;
+#pragma unroll
+    for (int j = 0; j < SC; ++j) {
+      const double2 c = cd[i * SC + j];
+      l0 = __fma_rn(sd[j].x, c.x, l0);
+      h0 = __fma_rn(sd[j].x, c.y, h0);
+      l1 = __fma_rn(sd[j].y, c.x, l1);
+      h1 = __fma_rn(sd[j].y, c.y, h1);
+    }
+    // (bits(l) - K) + ((bits(h) - K) << 15), K = bits(2^52), folded
+    constexpr uint64_t kK = 0x4330000000000000ull, kKK = kK + (kK << 15);
+    const uint64_t t0 = (uint64_t)__double_as_longlong(l0) + ((uint64_t)__double_as_longlong(h0) << 15) - kKK;
+    const uint64_t t1 = (uint64_t)__double_as_longlong(l1) + ((uint64_t)__double_as_longlong(h1) << 15) - kKK;
+    store(i, t0, t1);
+  };
+  auto row_int = [&](int i) {
+    uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+    for (int j = 0; j < SC; ++j) {
+      const uint32_t c = cm[i * SC + j];
+      a0 = mac_wide(a0, s[j].x, c);
+      a1 = mac_wide(a1, s[j].y, c);
+    }
+    store(i, a0, a1);
+  };
+  int i = 0;
+  if (MODE == 1) {
+    for (; i + 1 < (int)G.dc; i += 2) {
+      row_fp(i);
+      row_fp(i + 1);
+    }
+  } else if (MODE == 2) {
+    for (; i + 1 < (int)G.dc; i += 2) {
+      row_fp(i);
+      row_int(i + 1);
+    }
+  } else {
+    for (; i + 2 < (int)G.dc; i += 3) {
+      row_fp(i);
+      row_int(i + 2);
+      row_fp(i + 1);
+    }
+  }
+  for (; i < (int)G.dc; ++i) row_fp(i);
+}
+
+// Generic-width pieces for the FP64 / warp-specialised variants: CPT adjacent
+// coefficients per thread, rows [r0, r1) of group G.
+template <int SC, int CPT>
+struct BconvRows {
+  const uint32_t* cm;
+  const double2* cd;
+  const uint4* rc;
+  uint32_t* dst;
+  int n;
+  __device__ __forceinline__ void store(int i, const uint64_t (&t)[CPT]) const {
+    const uint4 R = rc[i];
+    uint32_t o[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) o[k] = sub_if(mont_reduce64(t[k], R.x, R.y), R.x);
+    uint32_t* p = dst + (size_t)R.z * n;
+    if (CPT == 4) *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3 % CPT]);
+    else *reinterpret_cast<uint2*>(p) = make_uint2(o[0], o[1 % CPT]);
+  }
+  __device__ __forceinline__ void fp(int i, const double (&sd)[SC][CPT]) const {
+    constexpr double kM = 4503599627370496.0;  // 2^52
+    constexpr uint64_t kK = 0x4330000000000000ull, kKK = kK + (kK << 15);
+    double l[CPT], h[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) l[k] = h[k] = kM;
+#pragma unroll
+    for (int j = 0; j < SC; ++j) {
+      const double2 c = cd[i * SC + j];
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        l[k] = __fma_rn(sd[j][k], c.x, l[k]);
+        h[k] = __fma_rn(sd[j][k], c.y, h[k]);
+      }
+    }
+    uint64_t t[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k)
+      t[k] = (uint64_t)__double_as_longlong(l[k]) + ((uint64_t)__double_as_longlong(h[k]) << 15) - kKK;
+    store(i, t);
+  }
+  __device__ __forceinline__ void in(int i, const uint32_t (&s)[SC][CPT]) const {
+    uint64_t t[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) t[k] = 0;
+#pragma unroll
+    for (int j = 0; j < SC; ++j) {
+      const uint32_t c = cm[i * SC + j];
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) t[k] = mac_wide(t[k], s[j][k], c);
+    }
+    store(i, t);
+  }
+};
+
+template <int SC, int CPT>
+__device__ __forceinline__ void bconv_load(const uint32_t* src, int n, int sc, uint32_t (&s)[SC][CPT]) {
+#pragma unroll
+  for (int j = 0; j < SC; ++j) {
+    if (CPT == 4) {
+      const uint4 v = j < sc ? *reinterpret_cast<const uint4*>(src + (size_t)j * n) : make_uint4(0, 0, 0, 0);
+      s[j][0] = v.x, s[j][1 % CPT] = v.y, s[j][2 % CPT] = v.z, s[j][3 % CPT] = v.w;
+    } else {
+      const uint2 v = j < sc ? *reinterpret_cast<const uint2*>(src + (size_t)j * n) : make_uint2(0, 0);
+      s[j][0] = v.x, s[j][1 % CPT] = v.y;
+    }
+  }
+}
+
+// Warp-specialised BConv: the first half of the CTA's warps runs the
+// IMAD.WIDE dot products for destination rows [0, h), the second half the
+// exact FP64 dot products for rows [h, dc), on the SAME coefficients, so the
+// SM's fmaheavy and FP64 pipes work side by side.  h = dc - dc * FP / 6.
+constexpr int kTW = 256;
+template <int SC, int FP>
+__global__ void __launch_bounds__(kTW) k_bconv_ws(BconvLaunch a, int n) {
+  constexpr int CPT = 4;
+  __shared__ uint32_t cm[kMaxRows * SC];
+  __shared__ double2 cd[kMaxRows * SC];
+  __shared__ uint4 rc[kMaxRows];
+  const BconvGroup G = a.groups[blockIdx.y];
+  for (int e = threadIdx.x; e < G.dc * SC; e += kTW) {
+    const int i = e / SC, j = e % SC;
+    const uint32_t c = j < (int)G.sc ? a.cmat[G.cmat_off + i * G.sc + j] : 0u;
+    cm[e] = c;
+    cd[e] = make_double2((double)(c & 0x7fffu), (double)(c >> 15));
+  }
+  for (int i = threadIdx.x; i < (int)G.dc; i += kTW) {
+    const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
+    rc[i] = make_uint4(P.q, P.qinv_neg, a.dst_row[G.map_off + i], 0);
+  }
+  __syncthreads();
+  const bool fpw = threadIdx.x >= kTW / 2;
+  const int t = threadIdx.x % (kTW / 2);
+  const int x = (blockIdx.x * (kTW / 2) + t) * CPT;
+  if (x >= n) return;
+  const uint32_t* src = a.src + blockIdx.z * a.src_bs + (size_t)G.src_off * n + x;
+  const BconvRows<SC, CPT> R{cm, cd, rc, a.dst + blockIdx.z * a.dst_bs + x, n};
+  const int dc = (int)G.dc, h = dc - dc * FP / 6;
+  uint32_t s[SC][CPT];
+  bconv_load<SC, CPT>(src, n, (int)G.sc, s);
+  if (!fpw) {
+    int i = 0;
+    for (; i + 1 < h; i += 2) {
+      R.in(i, s);
+      R.in(i + 1, s);
+    }
+    if (i < h) R.in(i, s);
+  } else {
+    double sd[SC][CPT];
+#pragma unroll
+    for (int j = 0; j < SC; ++j)
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) sd[j][k] = (double)s[j][k];
+    for (int i = h; i < dc; ++i) R.fp(i, sd);
+  }
+}
+
 // ----------------------------------------------------------------- tensor --
 __global__ void __launch_bounds__(kT) k_tensor(int n, int level, const uint32_t* __restrict__ x,
                                                const uint32_t* __restrict__ y, uint64_t ct_bs,
@@ -326,10 +541,40 @@ inline unsigned cdiv(unsigned a, unsigned b) { return (a + b - 1) / b; }
 
 }  // namespace
 
-void bconv(int n, const BconvLaunch& a, cudaStream_t st) {
-  dim3 grid(cdiv(n / 4, kT), a.ngroups, a.batch);
+void bconv(int n, const BconvLaunch& a, cudaStream_t st, int fp64_mode) {
   const int sc = a.max_sc;
   const BconvLaunch b = a;
+  if (fp64_mode >= 4 && fp64_mode <= 8 && sc <= 16) {  // warp-specialised, FP64 share (mode - 3) / 6 of the rows
+    dim3 grid(cdiv(n / 4, kTW / 2), a.ngroups, a.batch);
+    switch (sc * 16 + fp64_mode) {
+#define CK_WS(S)                                                           \
+  case S * 16 + 4: k_bconv_ws<S, 1><<<grid, kTW, 0, st>>>(b, n); break; \
+  case S * 16 + 5: k_bconv_ws<S, 2><<<grid, kTW, 0, st>>>(b, n); break; \
+  case S * 16 + 6: k_bconv_ws<S, 3><<<grid, kTW, 0, st>>>(b, n); break; \
+  case S * 16 + 7: k_bconv_ws<S, 4><<<grid, kTW, 0, st>>>(b, n); break; \
+  case S * 16 + 8: k_bconv_ws<S, 6><<<grid, kTW, 0, st>>>(b, n); break;
+      CK_WS(1) CK_WS(2) CK_WS(3) CK_WS(4) CK_WS(5) CK_WS(6) CK_WS(7) CK_WS(8) CK_WS(9) CK_WS(10) CK_WS(11)
+      CK_WS(12) CK_WS(13) CK_WS(14) CK_WS(15) CK_WS(16)
+#undef CK_WS
+      default: break;
+    }
+    return;
+  }
+  if (fp64_mode >= 1 && fp64_mode <= 3 && sc <= 16) {
+    dim3 grid(cdiv(n / 2, kTD), a.ngroups, a.batch);
+    switch (sc * 4 + fp64_mode) {
+#define CK_DF(S)                                                       \
+  case S * 4 + 1: k_bconv_df<S, 1><<<grid, kTD, 0, st>>>(b, n); break; \
+  case S * 4 + 2: k_bconv_df<S, 2><<<grid, kTD, 0, st>>>(b, n); break; \
+  case S * 4 + 3: k_bconv_df<S, 3><<<grid, kTD, 0, st>>>(b, n); break;
+      CK_DF(1) CK_DF(2) CK_DF(3) CK_DF(4) CK_DF(5) CK_DF(6) CK_DF(7) CK_DF(8) CK_DF(9) CK_DF(10) CK_DF(11)
+      CK_DF(12) CK_DF(13) CK_DF(14) CK_DF(15) CK_DF(16)
+#undef CK_DF
+      default: break;
+    }
+    return;
+  }
+  dim3 grid(cdiv(n / 4, kT), a.ngroups, a.batch);
   switch (sc) {
 #define CK_SC(S) case S: k_bconv<S><<<grid, kT, 0, st>>>(b, n); break;
     CK_SC(1) CK_SC(2) CK_SC(3) CK_SC(4) CK_SC(5) CK_SC(6) CK_SC(7) CK_SC(8) CK_SC(9) CK_SC(10) CK_SC(11)

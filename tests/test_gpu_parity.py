@@ -107,6 +107,26 @@ def tc_env(monkeypatch):
         c.close()
 
 
+@pytest.mark.parametrize("mode", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("shape", [(8, 24), (10, 22), (1, 3), (16, 64)])
+def test_bconv_fp64_pipe_matches_oracle(monkeypatch, mode, shape):
+    """Exact BConv dot products on the FP64 pipe (CK32_BCONV_FP64, kernels.cu
+    k_bconv_df / k_bconv_ws): bit-identical to the oracle for every row split,
+    including 16 sources (the largest exactness bound)."""
+    monkeypatch.setenv("CK32_BCONV_FP64", str(mode))
+    n, l, a = 65536, 64, 16
+    sc, dc = shape
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=48))
+    O = _oracle(n, l, a, 48)
+    src_g = list(range(l - sc, l)) if sc <= 10 else [l + j for j in range(sc)]
+    dst_g = list(range(dc))
+    src = O.canonical(O.random_rows(Rng(sc * 91 + dc + mode), np.array(src_g, np.uint32)), np.array(src_g, np.uint32))
+    got = ckks.bconv(C, dev(src), src_g, dst_g)
+    want = O.canonical(O.bconv(src.astype(np.int32), src_g, dst_g), np.array(dst_g, np.uint32))
+    np.testing.assert_array_equal(host(got), want)
+    C.close()
+
+
 @pytest.mark.parametrize("n", [1024, 65536])
 @pytest.mark.parametrize("shape", [(8, 24), (10, 22), (2, 22), (1, 3), (16, 40), (16, 64)])
 def test_bconv_tensor_core_matches_oracle(tc_env, n, shape):
