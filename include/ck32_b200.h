@@ -255,6 +255,27 @@ ck_status ck_shard_switch_begin(ck_shard* sh, int kind, uint32_t level, const ui
 ck_status ck_shard_switch_end(ck_shard* sh, int kind, uint32_t level, const uint32_t* recv, const uint32_t* v,
                               const uint32_t* addend, uint32_t add_mask, int32_t rotate, int64_t r, uint32_t* out,
                               ck_stream stream);
+/* Peer exchange ("peer-mapped loads inside BConv"), replacing
+ * the host all-gather: every rank allocates ONE exchange buffer, the ranks map
+ * each other's buffers (CUDA IPC across processes: ck_ipc_*; plain pointers
+ * for shards of one process) and pass all bases in rank order to
+ * ck_shard_set_peers.  After that, send == NULL in *_begin and recv == NULL in
+ * the second phases select the peer path: phase 1 INTTs into the rank's own
+ * buffer and publishes an epoch flag to every peer (system-scope release);
+ * phase 2 waits for all peers' flags (bounded: ck_shard_set_timeout, default
+ * 10 s; a timeout sets the error word read by ck_shard_peer_error instead of
+ * hanging) and its BConv loads the source rows straight from the peers'
+ * buffers.  Every rank must issue every phase in the same order (as with a
+ * collective).  The buffers are double-buffered per exchange kind, so a
+ * buffer is rewritten only after all peers have finished reading it. */
+ck_status ck_shard_exchange_buffer(ck_shard* sh, void** base, uint64_t* bytes);
+ck_status ck_shard_set_peers(ck_shard* sh, const uint64_t* bases, uint32_t world);
+ck_status ck_shard_set_timeout(ck_shard* sh, uint64_t timeout_ns);
+ck_status ck_shard_peer_error(ck_shard* sh, uint32_t* err);
+/* CUDA IPC of an exchange buffer (64-byte cudaIpcMemHandle_t) */
+ck_status ck_ipc_get_handle(const void* base, unsigned char handle[64]);
+ck_status ck_ipc_open_handle(const unsigned char handle[64], void** base);
+ck_status ck_ipc_close(void* base);
 /* hmult tensor (ckks.cpp:818-821) on the owned rows: d01 [2][lq], d2 [lq]. */
 ck_status ck_shard_tensor(ck_shard* sh, uint32_t level, const uint32_t* x, const uint32_t* y, uint32_t* d01,
                           uint32_t* d2, ck_stream stream);

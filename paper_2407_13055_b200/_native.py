@@ -87,6 +87,13 @@ _SIGS = {
     "ck_shard_switch_begin": [_vp, ctypes.c_int, _u32, _vp, _vp, _vp],
     "ck_shard_switch_end": [_vp, ctypes.c_int, _u32, _vp, _vp, _vp, _u32, ctypes.c_int32, _i64, _vp, _vp],
     "ck_shard_tensor": [_vp, _u32, _vp, _vp, _vp, _vp, _vp],
+    "ck_shard_exchange_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint64)],
+    "ck_shard_set_peers": [_vp, ctypes.POINTER(ctypes.c_uint64), _u32],
+    "ck_shard_set_timeout": [_vp, ctypes.c_uint64],
+    "ck_shard_peer_error": [_vp, _u32p],
+    "ck_ipc_get_handle": [_vp, ctypes.POINTER(ctypes.c_ubyte)],
+    "ck_ipc_open_handle": [ctypes.POINTER(ctypes.c_ubyte), ctypes.POINTER(_vp)],
+    "ck_ipc_close": [_vp],
 }
 EXPORTS = sorted(list(_SIGS) + ["ck_last_error", "ck_version", "ck_launch_count"])
 

@@ -799,7 +799,7 @@ struct Context {
     launches += 2;
   }
   void run_bconv(const BconvPlan& pl, int batch, const uint32_t* src, uint64_t src_bs, uint32_t* dst, uint64_t dst_bs,
-                 cudaStream_t st) {
+                 cudaStream_t st, const uint64_t* src_rows = nullptr) {
     if (batch == 0) return;
     BconvLaunch a;
     a.groups = pl.blob.at<BconvGroup>(pl.groups_off);
@@ -814,8 +814,9 @@ struct Context {
     a.dst_row = pl.blob.at<uint32_t>(pl.row_off);
     a.dst_prime = pl.blob.at<uint16_t>(pl.prime_off);
     a.primes = d_primes;
+    a.src_rows = src_rows;
     ProfScope ps(this, 2, 4.0 * n * (pl.src_rows + pl.dst_rows) * batch, 1, st);
-    if (use_tc && pl.tc_ok) {
+    if (use_tc && pl.tc_ok && !src_rows) {
       BconvTc t;
       t.btab = pl.blob.at<unsigned char>(pl.tc_tab_off);
       t.boff = pl.blob.at<uint32_t>(pl.tc_boff_off);
@@ -1041,6 +1042,9 @@ struct Context {
 // ModDown / rescale): the host all-gathers the INTT'd source rows that
 // `modup_begin` / `switch_begin` leave in a send buffer.
 struct Shard {
+  ~Shard() {
+    if (xbuf) cudaFree(xbuf);
+  }
   Context* c = nullptr;
   uint32_t G = 1, s = 0, qlo = 0, qhi = 0, plo = 0, phi = 0, qmax = 0, pmax = 0;
 
@@ -1267,10 +1271,114 @@ struct Shard {
     return ref;
   }
 
-  // ---- phases ----
+  // ---- peer exchange ("peer-mapped loads inside BConv") ----
+  // Every rank owns one exchange allocation, mapped by all peers (CUDA IPC
+  // across processes, plain pointers between virtual shards of one process):
+  //   [ModUp send x 2][switch send x 2][flags: 2 kinds x G words][error word]
+  // Phase 1 writes the rank's INTT rows into its own send buffer (parity =
+  // epoch & 1, so a buffer is rewritten only after every peer has signalled
+  // the following exchange of that kind, i.e. finished reading it) and
+  // publishes the epoch into every peer's flag word; phase 2 waits for all
+  // peers' flags, then its BConv reads the source rows straight from the
+  // peers' send buffers through a row-address table -- no all-gather buffer,
+  // no copy: the NVLink transfer happens inside the BConv loads.
+  void* xbuf = nullptr;
+  uint64_t up_words = 0, sw_words = 0, xbytes = 0;
+  std::vector<uint64_t> peers;  // exchange base of every rank (own included)
+  uint32_t epoch[2] = {0, 0};
+  Blob sig_tab;                 // [2 kinds][G] peer flag addresses for this rank
+  Blob up_tab;                  // [2 parities][L] ModUp source-row addresses
+  std::map<std::pair<int, uint32_t>, std::unique_ptr<Blob>> down_tab;  // [2 parities][2 sc]
+  uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
+
+  uint64_t up_off(uint32_t par) const { return (uint64_t)par * up_words * 4; }
+  uint64_t sw_off(uint32_t par) const { return (2 * up_words + (uint64_t)par * sw_words) * 4; }
+  uint64_t flag_off(int kind, uint32_t t) const { return (2 * up_words + 2 * sw_words) * 4 + ((uint64_t)kind * G + t) * 4; }
+  uint64_t err_off() const { return flag_off(0, 0) + 2ull * G * 4; }
+  uint32_t* own_flags(int kind) const { return reinterpret_cast<uint32_t*>(static_cast<char*>(xbuf) + flag_off(kind, 0)); }
+  uint32_t* err_word() const { return reinterpret_cast<uint32_t*>(static_cast<char*>(xbuf) + err_off()); }
+
+  void* exchange_buffer(uint64_t* bytes) {
+    if (!xbuf) {
+      up_words = (uint64_t)qmax * c->n;
+      sw_words = 2ull * (pmax + 2) * c->n;
+      xbytes = err_off() + 256;
+      CK_CUDA(cudaMalloc(&xbuf, xbytes));
+      CK_CUDA(cudaMemset(xbuf, 0, xbytes));
+    }
+    if (bytes) *bytes = xbytes;
+    return xbuf;
+  }
+  void set_peers(const uint64_t* bases, uint32_t world) {
+    if (world != G) throw InvalidArgument("peer table size != world");
+    exchange_buffer(nullptr);
+    peers.assign(bases, bases + G);
+    if (peers[s] != reinterpret_cast<uint64_t>(xbuf)) throw InvalidArgument("peer table: own entry is not this shard's buffer");
+    std::vector<uint64_t> sig(2ull * G);
+    for (int k = 0; k < 2; ++k)
+      for (uint32_t t = 0; t < G; ++t) sig[k * G + t] = peers[t] + flag_off(k, s);
+    sig_tab = Blob();
+    sig_tab.add(sig);
+    sig_tab.upload();
+    std::vector<uint64_t> ut(2ull * c->L);  // global Q row g -> owner's send buffer row g - q_lo(owner)
+    for (uint32_t par = 0; par < 2; ++par)
+      for (uint32_t t = 0; t < G; ++t)
+        for (uint32_t g = q_lo(t); g < q_hi(t); ++g)
+          ut[par * c->L + g] = peers[t] + up_off(par) + (uint64_t)(g - q_lo(t)) * c->n * 4;
+    up_tab = Blob();
+    up_tab.add(ut);
+    up_tab.upload();
+    down_tab.clear();
+    epoch[0] = epoch[1] = 0;
+  }
+  bool peer_mode() const { return !peers.empty(); }
+  const uint64_t* down_rows(int kind, uint32_t level, uint32_t par) {
+    auto key = std::make_pair(kind, level);
+    auto it = down_tab.find(key);
+    if (it == down_tab.end()) {
+      const DownPlan& pl = down_plan(kind, level);
+      std::vector<uint64_t> rt(4ull * pl.sc);  // gathered order: rank t's u-th own source, polys p
+      for (uint32_t q = 0; q < 2; ++q) {
+        uint32_t off = 0;
+        for (uint32_t t = 0; t < G; ++t) {
+          for (uint32_t u = 0; u < pl.rank_cnt[t]; ++u)
+            for (uint32_t p = 0; p < 2; ++p)
+              rt[(size_t)q * 2 * pl.sc + p * pl.sc + off + u] =
+                  peers[t] + sw_off(q) + ((uint64_t)p * pl.smax + u) * c->n * 4;
+          off += pl.rank_cnt[t];
+        }
+      }
+      auto b = std::make_unique<Blob>();
+      b->add(rt);
+      b->upload();
+      it = down_tab.emplace(key, std::move(b)).first;
+    }
+    return it->second->at<uint64_t>(0) + (size_t)par * 2 * down_plan(kind, level).sc;
+  }
+  void peer_wait(int kind, cudaStream_t st) {
+    if (!peer_mode()) throw InvalidArgument("no recv buffer and no peer exchange set up");
+    shard_wait(own_flags(kind), (int)G, epoch[kind], err_word(), timeout_ns, st);
+    c->launches += 1;
+  }
+  uint32_t peer_error() const {
+    uint32_t e = 0;
+    if (xbuf) CK_CUDA(cudaMemcpy(&e, err_word(), 4, cudaMemcpyDeviceToHost));
+    return e;
+  }
+
+  // ---- phases ----  (send == nullptr / recv == nullptr: peer exchange)
   void modup_begin(uint32_t level, const uint32_t* d, uint32_t* send, cudaStream_t st) {
     const UpPlan& pl = up_plan(level);
-    c->run_ntt(pl.intt, true, 1, d, 0, send, 0, 0, st);
+    if (!send) {
+      if (!peer_mode()) throw InvalidArgument("no send buffer and no peer exchange set up");
+      const uint32_t e = ++epoch[0];
+      send = reinterpret_cast<uint32_t*>(static_cast<char*>(xbuf) + up_off(e & 1));
+      c->run_ntt(pl.intt, true, 1, d, 0, send, 0, 0, st);
+      shard_signal(sig_tab.at<uint64_t>(0), (int)G, e, st);
+      c->launches += 1;
+    } else {
+      c->run_ntt(pl.intt, true, 1, d, 0, send, 0, 0, st);
+    }
     c->counters[3] += pl.lq;
   }
   void modup_keymult(uint32_t level, const uint32_t* recv, const uint32_t* d, const uint32_t* evk,
@@ -1279,14 +1387,22 @@ struct Shard {
     const uint64_t N = c->n;
     uint32_t* compact = static_cast<uint32_t*>(c->scratch_get(((size_t)level + (size_t)pl.D * pl.rows) * N * 4, st));
     uint32_t* ext = compact + (size_t)level * N;
-    for (uint32_t t = 0; t < G; ++t) {  // gathered blocks -> global row order
-      const uint32_t cnt = lq_of(t, level);
-      if (cnt)
-        CK_CUDA(cudaMemcpyAsync(compact + (size_t)q_lo(t) * N, recv + (size_t)t * qmax * N, (size_t)cnt * N * 4,
-                                cudaMemcpyDeviceToDevice, st));
+    const uint64_t* rows = nullptr;
+    if (!recv) {  // peer exchange: wait for every rank's phase 1, read their rows in place
+      if (!peer_mode()) throw InvalidArgument("no recv buffer and no peer exchange set up");
+      const uint32_t e = epoch[0];
+      peer_wait(0, st);
+      rows = up_tab.at<uint64_t>(0) + (size_t)(e & 1) * c->L;
+    } else {
+      for (uint32_t t = 0; t < G; ++t) {  // gathered blocks -> global row order
+        const uint32_t cnt = lq_of(t, level);
+        if (cnt)
+          CK_CUDA(cudaMemcpyAsync(compact + (size_t)q_lo(t) * N, recv + (size_t)t * qmax * N, (size_t)cnt * N * 4,
+                                  cudaMemcpyDeviceToDevice, st));
+      }
     }
     if (pl.bc.ngroups) {
-      c->run_bconv(pl.bc, 1, compact, 0, ext, 0, st);
+      c->run_bconv(pl.bc, 1, compact, 0, ext, 0, st, rows);
       c->run_ntt(pl.ntt, false, 1, ext, 0, ext, 0, 1, st);
     }
     ShardKeyMultLaunch a;
@@ -1316,7 +1432,16 @@ struct Shard {
   }
   void switch_begin(int kind, uint32_t level, const uint32_t* v, uint32_t* send, cudaStream_t st) {
     const DownPlan& pl = down_plan(kind, level);
-    c->run_ntt(pl.intt, true, 1, v, 0, send, 0, 0, st);
+    if (!send) {
+      if (!peer_mode()) throw InvalidArgument("no send buffer and no peer exchange set up");
+      const uint32_t e = ++epoch[1];
+      send = reinterpret_cast<uint32_t*>(static_cast<char*>(xbuf) + sw_off(e & 1));
+      c->run_ntt(pl.intt, true, 1, v, 0, send, 0, 0, st);
+      shard_signal(sig_tab.at<uint64_t>(0) + G, (int)G, e, st);
+      c->launches += 1;
+    } else {
+      c->run_ntt(pl.intt, true, 1, v, 0, send, 0, 0, st);
+    }
     c->counters[3] += 2ull * pl.own_sc;
   }
   void switch_end(int kind, uint32_t level, const uint32_t* recv, const uint32_t* v, const uint32_t* add,
@@ -1325,17 +1450,25 @@ struct Shard {
     const uint64_t N = c->n;
     uint32_t* compact = static_cast<uint32_t*>(c->scratch_get((2ull * pl.sc + 2ull * pl.lqo) * N * 4, st));
     uint32_t* o = compact + 2ull * pl.sc * N;
-    uint32_t off = 0;
-    for (uint32_t t = 0; t < G; ++t) {  // [G][2][smax] -> [2][sc] in gathered order
-      const uint32_t cnt = pl.rank_cnt[t];
-      for (uint32_t p = 0; p < 2 && cnt; ++p)
-        CK_CUDA(cudaMemcpyAsync(compact + ((size_t)p * pl.sc + off) * N,
-                                recv + ((size_t)t * 2 * pl.smax + (size_t)p * pl.smax) * N, (size_t)cnt * N * 4,
-                                cudaMemcpyDeviceToDevice, st));
-      off += cnt;
+    const uint64_t* rows = nullptr;
+    if (!recv) {  // peer exchange
+      if (!peer_mode()) throw InvalidArgument("no recv buffer and no peer exchange set up");
+      const uint32_t e = epoch[1];
+      peer_wait(1, st);
+      rows = down_rows(kind, level, e & 1);
+    } else {
+      uint32_t off = 0;
+      for (uint32_t t = 0; t < G; ++t) {  // [G][2][smax] -> [2][sc] in gathered order
+        const uint32_t cnt = pl.rank_cnt[t];
+        for (uint32_t p = 0; p < 2 && cnt; ++p)
+          CK_CUDA(cudaMemcpyAsync(compact + ((size_t)p * pl.sc + off) * N,
+                                  recv + ((size_t)t * 2 * pl.smax + (size_t)p * pl.smax) * N, (size_t)cnt * N * 4,
+                                  cudaMemcpyDeviceToDevice, st));
+        off += cnt;
+      }
     }
     if (pl.lqo) {
-      c->run_bconv(pl.bc, 1, compact, 0, o, 0, st);
+      c->run_bconv(pl.bc, 1, compact, 0, o, 0, st, rows);
       c->run_ntt(pl.ntt, false, 1, o, 0, o, 0, 1, st);
       ShardTailLaunch a;
       a.v = v;
@@ -2319,6 +2452,50 @@ ck_status ck_shard_create(ck_context* ctx, uint32_t world, uint32_t rank, ck_sha
 ck_status ck_shard_destroy(ck_shard* sh) {
   return guard([&] { delete SH(sh); });
 }
+ck_status ck_shard_exchange_buffer(ck_shard* sh, void** base, uint64_t* bytes) {
+  return guard([&] {
+    if (!base) throw InvalidArgument("null argument");
+    *base = SH(sh)->exchange_buffer(bytes);
+  });
+}
+ck_status ck_shard_set_peers(ck_shard* sh, const uint64_t* bases, uint32_t world) {
+  return guard([&] {
+    check_ptr(bases);
+    SH(sh)->set_peers(bases, world);
+  });
+}
+ck_status ck_shard_set_timeout(ck_shard* sh, uint64_t timeout_ns) {
+  return guard([&] { SH(sh)->timeout_ns = timeout_ns; });
+}
+ck_status ck_shard_peer_error(ck_shard* sh, uint32_t* err) {
+  return guard([&] {
+    if (!err) throw InvalidArgument("null argument");
+    *err = SH(sh)->peer_error();
+  });
+}
+ck_status ck_ipc_get_handle(const void* base, unsigned char handle[64]) {
+  return guard([&] {
+    if (!base || !handle) throw InvalidArgument("null argument");
+    cudaIpcMemHandle_t h;
+    CK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(base)));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle, &h, 64);
+  });
+}
+ck_status ck_ipc_open_handle(const unsigned char handle[64], void** base) {
+  return guard([&] {
+    if (!base || !handle) throw InvalidArgument("null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    CK_CUDA(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+ck_status ck_ipc_close(void* base) {
+  return guard([&] {
+    if (!base) throw InvalidArgument("null argument");
+    CK_CUDA(cudaIpcCloseMemHandle(base));
+  });
+}
 ck_status ck_shard_layout(const ck_shard* sh, uint32_t level, uint32_t out[8]) {
   return guard([&] {
     const Shard* s = reinterpret_cast<const Shard*>(sh);
@@ -2340,7 +2517,7 @@ ck_status ck_shard_modup_begin(ck_shard* sh, uint32_t level, const uint32_t* d, 
     check_level(s->c, level);
     if (s->lq(level)) {
       check_ptr(d);
-      check_ptr(send);
+      if (!s->peer_mode()) check_ptr(send);
     }
     s->modup_begin(level, d, send, S(stream));
     check_launch();
@@ -2351,9 +2528,12 @@ ck_status ck_shard_modup_keymult(ck_shard* sh, uint32_t level, const uint32_t* r
   return guard([&] {
     Shard* s = SH(sh);
     check_level(s->c, level);
-    check_ptr(recv);
+    if (!s->peer_mode()) check_ptr(recv);
     check_ptr(evk);
-    if (s->up_plan(level).rows == 0) return;  // nothing owned at this level
+    if (s->up_plan(level).rows == 0) {  // nothing owned at this level (a peer rank still waits: buffer reuse)
+      if (!recv) s->peer_wait(0, S(stream));
+      return;
+    }
     check_ptr(v);
     if (s->lq(level)) check_ptr(d);
     s->modup_keymult(level, recv, d, evk, fold, v, S(stream));
@@ -2366,7 +2546,7 @@ ck_status ck_shard_switch_begin(ck_shard* sh, int kind, uint32_t level, const ui
     Shard* s = SH(sh);
     check_kind(kind);
     check_level(s->c, level, kind == 0 ? 1 : 4);
-    check_ptr(send);
+    if (!s->peer_mode()) check_ptr(send);
     if (s->down_plan(kind, level).own_sc) check_ptr(v);
     s->switch_begin(kind, level, v, send, S(stream));
     check_launch();
@@ -2379,7 +2559,7 @@ ck_status ck_shard_switch_end(ck_shard* sh, int kind, uint32_t level, const uint
     Shard* s = SH(sh);
     check_kind(kind);
     check_level(s->c, level, kind == 0 ? 1 : 4);
-    check_ptr(recv);
+    if (!s->peer_mode()) check_ptr(recv);
     const uint32_t lqo = s->down_plan(kind, level).lqo;
     if (lqo) {
       check_ptr(v);

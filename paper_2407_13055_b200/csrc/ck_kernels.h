@@ -89,6 +89,10 @@ struct BconvLaunch {
   const uint32_t* dst_row = nullptr;
   const uint16_t* dst_prime = nullptr;
   const PrimeDev* primes = nullptr;
+  // optional (batch 1): source row r of the launch is the absolute address
+  // src_rows[r] instead of src + r * n -- rows may live in PEER GPUs' memory
+  // (limb-sharded exchange through peer-mapped loads, shard.cu)
+  const uint64_t* src_rows = nullptr;
 };
 // fp64_mode 0: IMAD.WIDE dot products (k_bconv); 1-3: exact dot products on
 // the FP64 pipe for all / every other / two of three destination rows
@@ -213,5 +217,11 @@ struct ShardTailLaunch {
   const PrimeDev* primes = nullptr;
 };
 void shard_tail(int n, int rows, const ShardTailLaunch& a, cudaStream_t st);
+// peer exchange handshake (shard.cu): signal stores `epoch` (release, system
+// scope) to the G flag words sig[0..G); wait spins (acquire, system scope)
+// until flags[t] >= epoch for every t < G, or sets *err and gives up after
+// `timeout_ns`.
+void shard_signal(const uint64_t* sig, int G, uint32_t epoch, cudaStream_t st);
+void shard_wait(const uint32_t* flags, int G, uint32_t epoch, uint32_t* err, uint64_t timeout_ns, cudaStream_t st);
 
 }  // namespace ck

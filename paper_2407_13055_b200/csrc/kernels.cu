@@ -46,8 +46,15 @@ __global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
   if (x >= n) return;
   const uint32_t* src = a.src + blockIdx.z * a.src_bs + (size_t)G.src_off * n + x;
   uint4 s[SC];
+  if (a.src_rows) {  // rows by absolute address (possibly peer memory); plain loads
 #pragma unroll
-  for (int j = 0; j < SC; ++j) s[j] = j < (int)G.sc ? ld4(src + (size_t)j * n) : make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < SC; ++j)
+      s[j] = j < (int)G.sc ? ld4(reinterpret_cast<const uint32_t*>(a.src_rows[G.src_off + j]) + x)
+                           : make_uint4(0, 0, 0, 0);
+  } else {
+#pragma unroll
+    for (int j = 0; j < SC; ++j) s[j] = j < (int)G.sc ? ld4(src + (size_t)j * n) : make_uint4(0, 0, 0, 0);
+  }
   uint32_t* dst = a.dst + blockIdx.z * a.dst_bs + x;
   auto one = [&](int i) {
     uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
@@ -544,6 +551,7 @@ inline unsigned cdiv(unsigned a, unsigned b) { return (a + b - 1) / b; }
 void bconv(int n, const BconvLaunch& a, cudaStream_t st, int fp64_mode) {
   const int sc = a.max_sc;
   const BconvLaunch b = a;
+  if (a.src_rows) fp64_mode = 0;  // the pointer-table form is implemented by k_bconv only
   if (fp64_mode >= 4 && fp64_mode <= 8 && sc <= 16) {  // warp-specialised, FP64 share (mode - 3) / 6 of the rows
     dim3 grid(cdiv(n / 4, kTW / 2), a.ngroups, a.batch);
     switch (sc * 16 + fp64_mode) {

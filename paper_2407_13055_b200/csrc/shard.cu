@@ -90,7 +90,54 @@ __global__ void __launch_bounds__(kST) k_shard_tail(ShardTailLaunch a, int n) {
   a.out[(size_t)c * a.out_ps + (size_t)r * n + j] = x;
 }
 
+// Peer exchange handshake.  Producer: after the phase-1 INTT (stream order)
+// one thread per peer publishes the epoch into that peer's flag word for this
+// rank with a system-scope release; the INTT's writes to the exchange buffer
+// happen-before it.  Consumer: one thread per peer spins with system-scope
+// acquire loads on its local flag word until the peer's epoch arrives; the
+// BConv that reads the peers' buffers is the next kernel on the stream.  The
+// spin is bounded (globaltimer) so a missing peer reports an error instead of
+// hanging the GPU.
+__global__ void k_shard_signal(const uint64_t* __restrict__ sig, int G, uint32_t epoch) {
+  const int t = threadIdx.x;
+  if (t >= G) return;
+  uint32_t* p = reinterpret_cast<uint32_t*>(sig[t]);
+  asm volatile("fence.sc.sys;\n" ::: "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(epoch) : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_shard_wait(const uint32_t* __restrict__ flags, int G, uint32_t epoch, uint32_t* err,
+                             uint64_t timeout_ns) {
+  const int t = threadIdx.x;
+  if (t >= G) return;
+  const uint64_t t0 = globaltimer();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flags + t) : "memory");
+    if ((int32_t)(v - epoch) >= 0) break;
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicExch(err, 1u);
+      break;
+    }
+    __nanosleep(200);
+  }
+}
+
 }  // namespace
+
+void shard_signal(const uint64_t* sig, int G, uint32_t epoch, cudaStream_t st) {
+  k_shard_signal<<<1, 32 * ((G + 31) / 32), 0, st>>>(sig, G, epoch);
+}
+
+void shard_wait(const uint32_t* flags, int G, uint32_t epoch, uint32_t* err, uint64_t timeout_ns, cudaStream_t st) {
+  k_shard_wait<<<1, 32 * ((G + 31) / 32), 0, st>>>(flags, G, epoch, err, timeout_ns);
+}
 
 void shard_key_mult(int n, const ShardKeyMultLaunch& a, cudaStream_t st) {
   if (a.rows == 0) return;

@@ -17,9 +17,15 @@ once for ModUp (sources: the digit rows) and once for ModDown / rescale
 (sources: the P rows and/or the dropped Q rows).  The compute phases are the
 C-ABI entry points ``ck_shard_*`` (include/ck32_b200.h); the exchange is a
 pluggable object: :class:`TorchExchange` (one rank per process,
-``torch.distributed`` all-gather — NCCL on GPUs, gloo in the CPU tests) or
+``torch.distributed`` all-gather — NCCL on GPUs, gloo in the CPU tests),
 :class:`LocalExchange` (several shards driven from one process, used to check
-the sharded path against the single-device one on one GPU).
+the sharded path against the single-device one on one GPU), or the
+peer-memory exchanges :class:`IpcPeerExchange` (one rank per process, buffers
+mapped with CUDA IPC) and :class:`LocalPeerExchange` (shards of one process):
+there is no gather at all -- phase 1 leaves the INTT rows in the rank's own
+exchange buffer and raises a flag in every peer, phase 2 waits for the flags
+and its BConv loads the rows straight from the peers' buffers over NVLink
+("peer-mapped loads inside BConv").
 
 Outputs are bit-identical to the single-device mechanisms on the owned rows:
 the partition does not change any arithmetic.
@@ -150,6 +156,62 @@ class TorchExchange:
         return [out]
 
 
+class LocalPeerExchange:
+    """Peer-memory exchange between shards driven from one process (one GPU:
+    the 'peers' are the other shards' buffers on the same device)."""
+    peer = True
+
+    def __init__(self, backends: Sequence):
+        bases = [be.exchange_buffer() for be in backends]
+        for be in backends:
+            be.set_peers(bases)
+        self.backends = list(backends)
+
+    def errors(self) -> List[int]:
+        return [be.peer_error() for be in self.backends]
+
+    def close(self):
+        pass
+
+
+class IpcPeerExchange:
+    """Peer-memory exchange, one shard per process: every rank exports its
+    exchange buffer with CUDA IPC, the handles travel over ``torch.distributed``
+    (all_gather_object) and every rank maps its peers' buffers once."""
+    peer = True
+
+    def __init__(self, backend, group=None):
+        import torch.distributed as dist
+        from . import _native as nat
+        self.nat, self.backend = nat, backend
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        base = backend.exchange_buffer()
+        h = (ctypes.c_ubyte * 64)()
+        nat.call("ck_ipc_get_handle", ctypes.c_void_p(base), h)
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        self.opened = []
+        bases = []
+        for t, hb in enumerate(handles):
+            if t == rank:
+                bases.append(base)
+                continue
+            p = ctypes.c_void_p()
+            nat.call("ck_ipc_open_handle", (ctypes.c_ubyte * 64).from_buffer_copy(hb), ctypes.byref(p))
+            self.opened.append(p)
+            bases.append(p.value)
+        backend.set_peers(bases)
+        dist.barrier(group=group)
+
+    def errors(self) -> List[int]:
+        return [self.backend.peer_error()]
+
+    def close(self):
+        for p in self.opened:
+            self.nat.call("ck_ipc_close", p)
+        self.opened = []
+
+
 # ---------------------------------------------------------- device backend --
 class ShardBackend:
     """One shard on the GPU: the ``ck_shard_*`` C-ABI entry points."""
@@ -180,6 +242,24 @@ class ShardBackend:
         except Exception:
             pass
 
+    # -- peer exchange (send / recv = None in the phase calls) --
+    def exchange_buffer(self) -> int:
+        base, nbytes = ctypes.c_void_p(), ctypes.c_uint64()
+        self.nat.call("ck_shard_exchange_buffer", self._h, ctypes.byref(base), ctypes.byref(nbytes))
+        return base.value
+
+    def set_peers(self, bases: Sequence[int]):
+        arr = (ctypes.c_uint64 * len(bases))(*bases)
+        self.nat.call("ck_shard_set_peers", self._h, arr, len(bases))
+
+    def set_timeout(self, seconds: float):
+        self.nat.call("ck_shard_set_timeout", self._h, int(seconds * 1e9))
+
+    def peer_error(self) -> int:
+        e = ctypes.c_uint32()
+        self.nat.call("ck_shard_peer_error", self._h, ctypes.byref(e))
+        return e.value
+
     def _p(self, t: Optional[torch.Tensor]):
         if t is None:
             return None
@@ -197,8 +277,9 @@ class ShardBackend:
                       self.ctx.stream())
         return d01, d2
 
-    def modup_begin(self, level, d):
-        send = torch.zeros((self.layout.q_max, self.ctx.n), dtype=torch.int32, device=self.ctx.device)
+    def modup_begin(self, level, d, peer=False):
+        send = None if peer else torch.zeros((self.layout.q_max, self.ctx.n), dtype=torch.int32,
+                                             device=self.ctx.device)
         self.nat.call("ck_shard_modup_begin", self._h, level, self._p(d), self._p(send), self.ctx.stream())
         return send
 
@@ -209,8 +290,9 @@ class ShardBackend:
                       self._p(fold), self._p(v), self.ctx.stream())
         return v
 
-    def switch_begin(self, kind, level, v):
-        send = torch.zeros((2, self.layout.s_max(kind), self.ctx.n), dtype=torch.int32, device=self.ctx.device)
+    def switch_begin(self, kind, level, v, peer=False):
+        send = None if peer else torch.zeros((2, self.layout.s_max(kind), self.ctx.n), dtype=torch.int32,
+                                             device=self.ctx.device)
         self.nat.call("ck_shard_switch_begin", self._h, kind, level, self._p(v), self._p(send), self.ctx.stream())
         return send
 
@@ -235,20 +317,25 @@ class LimbShardedEvaluator:
     def __init__(self, backends: Sequence, exchange, lazy_rescale: bool = False):
         self.backends = list(backends)
         self.x = exchange
+        self.peer = bool(getattr(exchange, "peer", False))
         self.lazy_rescale = lazy_rescale
 
     def _gather(self, sends):
+        if self.peer:  # the rows stay in the peers' exchange buffers
+            return [None] * len(sends)
         return self.x.all_gather(sends)
 
     def key_switch_v(self, level: int, ds, evks, folds=None):
         """ModUp + KeyMult (+ fold): v = [2][lq + lp] per shard (ckks.cpp:680-770)."""
-        sends = [be.modup_begin(level, d) for be, d in zip(self.backends, ds)]
+        kw = {"peer": True} if self.peer else {}
+        sends = [be.modup_begin(level, d, **kw) for be, d in zip(self.backends, ds)]
         recvs = self._gather(sends)
         folds = folds or [None] * len(self.backends)
         return [be.modup_keymult(level, r, d, e, f) for be, r, d, e, f in zip(self.backends, recvs, ds, evks, folds)]
 
     def _switch(self, kind, level, vs, addends=None, add_mask=0, rot=None):
-        sends = [be.switch_begin(kind, level, v) for be, v in zip(self.backends, vs)]
+        kw = {"peer": True} if self.peer else {}
+        sends = [be.switch_begin(kind, level, v, **kw) for be, v in zip(self.backends, vs)]
         recvs = self._gather(sends)
         addends = addends or [None] * len(self.backends)
         return [be.switch_end(kind, level, r, v, a, add_mask, rot)

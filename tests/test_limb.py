@@ -157,18 +157,19 @@ def _gpu_ctx(n, l, a, db, lazy=False):
     return ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db, lazy_rescale=lazy))
 
 
-def _sharded_vs_single(C, O, world, level, seed, lazy=False, rots=(1,)):
+def _sharded_vs_single(C, O, world, level, seed, lazy=False, rots=(1,), peer=False):
     from fractions import Fraction
 
     from paper_2407_13055_b200 import ckks
-    from paper_2407_13055_b200.limb import ShardBackend
+    from paper_2407_13055_b200.limb import LocalPeerExchange, ShardBackend
 
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(C.device)
     xb, xa, yb, ya, evk = O.synthetic(level, seed)
     x, y, K = dev(np.stack([xb, xa])), dev(np.stack([yb, ya])), dev(evk)
     shards = [ShardBackend(C, world, r) for r in range(world)]
     lays = [s.layout for s in shards]
-    ev = LimbShardedEvaluator(shards, LocalExchange(), lazy_rescale=lazy)
+    xch = LocalPeerExchange(shards) if peer else LocalExchange()
+    ev = LimbShardedEvaluator(shards, xch, lazy_rescale=lazy)
     xs = [lay.split_ct(x, level) for lay in lays]
     ys = [lay.split_ct(y, level) for lay in lays]
     ks = [lay.split_key(K) for lay in lays]
@@ -187,13 +188,16 @@ def _sharded_vs_single(C, O, world, level, seed, lazy=False, rots=(1,)):
     got = torch.cat(ev.key_switch(level, [x_[1].contiguous() for x_ in xs], ks), dim=1)
     c0, c1 = ckks.key_switch(C, ckks.Polynomial(x[1].contiguous(), level), ckks.EvaluationKey(K))
     assert torch.equal(got, torch.stack([c0.data, c1.data])), f"key_switch world {world}"
+    if peer:
+        assert xch.errors() == [0] * world
     for s in shards:
         s.close()
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_gpu_virtual_shards_small_vs_oracle_and_single(world):
+def test_gpu_virtual_shards_small_vs_oracle_and_single(world, peer):
     from pyoracle import Oracle
 
     n, l, a, db = 1024, 8, 3, 55
@@ -201,26 +205,55 @@ def test_gpu_virtual_shards_small_vs_oracle_and_single(world):
     for lazy in (False, True):
         C = _gpu_ctx(n, l, a, db, lazy)
         for level, seed in ((8, 3), (5, 4)):
-            _sharded_vs_single(C, O, world, level, seed, lazy, rots=(1, -5))
+            _sharded_vs_single(C, O, world, level, seed, lazy, rots=(1, -5), peer=peer)
         C.close()
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_gpu_virtual_shards_n65536(world):
+def test_gpu_virtual_shards_n65536(world, peer):
     from pyoracle import Oracle
 
     n, l, a, db = 65536, 24, 8, 55
     O = Oracle(n, l, a, db)
     C = _gpu_ctx(n, l, a, db)
     for level in (24, 13):
-        _sharded_vs_single(C, O, world, level, 40 + level)
+        _sharded_vs_single(C, O, world, level, 40 + level, peer=peer)
     C.close()
 
 
 @pytest.mark.gpu
+def test_gpu_peer_exchange_rejects_bad_tables_and_times_out():
+    """ck_shard_set_peers validates the table; a peer that never signals makes
+    the bounded wait report an error instead of hanging the GPU."""
+    from paper_2407_13055_b200.limb import ShardBackend
+
+    C = _gpu_ctx(1024, 8, 3, 55)
+    shards = [ShardBackend(C, 2, r) for r in range(2)]
+    bases = [s.exchange_buffer() for s in shards]
+    with pytest.raises(ValueError):
+        shards[0].set_peers(bases[:1])  # wrong world size
+    with pytest.raises(ValueError):
+        shards[0].set_peers([bases[1], bases[1]])  # own entry is not its buffer
+    for s in shards:
+        s.set_peers(bases)
+    shards[0].set_timeout(0.05)
+    d = torch.zeros((shards[0].layout.lq(8), 1024), dtype=torch.int32, device=C.device)
+    shards[0].modup_begin(8, d, peer=True)  # rank 1 never runs phase 1
+    key = shards[0].layout.split_key(torch.zeros((3, 2, 11, 1024), dtype=torch.int32, device=C.device))
+    shards[0].modup_keymult(8, None, d, key)
+    torch.cuda.synchronize()
+    assert shards[0].peer_error() == 1
+    for s in shards:
+        s.close()
+    C.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_gpu_config4_n131072_matches_reference_hash(world):
+def test_gpu_config4_n131072_matches_reference_hash(world, peer):
     """BASELINE config 4: single-ciphertext limb-sharded HMult / HRot at
     N=2^17, l=24, alpha=8 — reassembled output equals the reference's hash."""
     from golden_util import FULL, sha
@@ -236,7 +269,11 @@ def test_gpu_config4_n131072_matches_reference_hash(world):
     dev = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(C.device)
     x, y, K = dev(np.stack([xb, xa])), dev(np.stack([yb, ya])), dev(evk)
     shards = [ShardBackend(C, world, r) for r in range(world)]
-    ev = LimbShardedEvaluator(shards, LocalExchange())
+    if peer:
+        from paper_2407_13055_b200.limb import LocalPeerExchange
+        ev = LimbShardedEvaluator(shards, LocalPeerExchange(shards))
+    else:
+        ev = LimbShardedEvaluator(shards, LocalExchange())
     lays = [s.layout for s in shards]
     xs = [lay.split_ct(x, 24) for lay in lays]
     ys = [lay.split_ct(y, 24) for lay in lays]
@@ -248,3 +285,84 @@ def test_gpu_config4_n131072_matches_reference_hash(world):
     for s in shards:
         s.close()
     C.close()
+
+
+def _ipc_worker(rank, world, port, q):
+    """One shard per process, both on cuda:0: the exchange buffers are mapped
+    with CUDA IPC (IpcPeerExchange) exactly as on an NVLink node."""
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    for p in (os.path.dirname(here), os.path.join(os.path.dirname(here), "oracle"), here):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    from pyoracle import Oracle
+
+    from paper_2407_13055_b200.limb import IpcPeerExchange, ShardBackend
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, l, a, db = 1024, 8, 3, 55
+        O = Oracle(n, l, a, db)
+        C = _gpu_ctx(n, l, a, db)
+        be = ShardBackend(C, world, rank)
+        be.set_timeout(60.0)
+        xch = IpcPeerExchange(be)
+        ev = LimbShardedEvaluator([be], xch)
+        dev = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(C.device)
+        xb, xa, yb, ya, evk = O.synthetic(l, 91)
+        lay = be.layout
+        x, y, k = lay.split_ct(dev(np.stack([xb, xa])), l), lay.split_ct(dev(np.stack([yb, ya])), l), \
+            lay.split_key(dev(evk))
+        out = []
+        for _ in range(2):  # repeated exchanges of both kinds: double-buffer reuse
+            out.append(ev.hmult(l, [x], [y], [k])[0].cpu().numpy())
+            out.append(ev.hrot(l, [x], 3, [k])[0].cpu().numpy())
+            out.append(ev.rescale(l, [x])[0].cpu().numpy())
+            out.append(ev.rescale(l, [x])[0].cpu().numpy())
+        torch.cuda.synchronize()
+        q.put((rank, out, xch.errors()))
+        dist.barrier()
+        xch.close()
+        be.close()
+        C.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_ipc_peer_exchange_two_processes():
+    """Config 4's peer-memory exchange across processes (CUDA IPC, flags with
+    system-scope release / acquire): both ranks share cuda:0 here; the same
+    code maps NVLink peers on a multi-GPU node.  Bit-exact vs the oracle."""
+    from pyoracle import Oracle
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    parts = {}
+    for _ in range(2):
+        r, out, err = q.get(timeout=600)
+        assert err == [0]
+        parts[r] = out
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n, l, a, db = 1024, 8, 3, 55
+    O = Oracle(n, l, a, db)
+    xb, xa, yb, ya, evk = O.synthetic(l, 91)
+    ob, oa = O.hmult(l, xb, xa, yb, ya, evk)
+    hm = np.stack([_canon(O, ob, l - 2), _canon(O, oa, l - 2)])
+    ob, oa = O.hrot(l, xb, xa, 3, evk)
+    hr = np.stack([_canon(O, ob, l), _canon(O, oa, l)])
+    ob, oa = O.rescale(l, xb, xa)
+    rs = np.stack([_canon(O, ob, l - 2), _canon(O, oa, l - 2)])
+    for i, want in enumerate([hm, hr, rs, rs] * 2):
+        got = np.concatenate([parts[0][i], parts[1][i]], axis=1).astype(np.int64)
+        np.testing.assert_array_equal(got, want)
