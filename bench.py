@@ -52,6 +52,9 @@ def parse():
                     help="dp: batched independent ciphertexts (configs 1-3, the headline); limb: one ciphertext "
                          "limb-sharded over the ranks at N=2^17 (config 4); helr: HELR-style logistic-regression "
                          "iteration (config 5)")
+    ap.add_argument("--exchange", choices=["gather", "peer"], default="peer",
+                    help="config 4 exchange: NCCL all-gather + copy, or peer-mapped loads inside BConv "
+                         "(CUDA IPC across ranks; default)")
     ap.add_argument("--virtual-shards", type=int, default=0,
                     help="limb workload on ONE GPU: drive this many shards from one process (exchange = local "
                          "copies); measures the summed shard compute, not multi-GPU speed")
@@ -487,8 +490,8 @@ def run_limb(args):
     import torch.distributed as dist
 
     from paper_2407_13055_b200 import ckks, dp
-    from paper_2407_13055_b200.limb import (MERGED, MOD_DOWN, LimbShardedEvaluator, LocalExchange, ShardBackend,
-                                            TorchExchange, exchange_bytes)
+    from paper_2407_13055_b200.limb import (MERGED, MOD_DOWN, IpcPeerExchange, LimbShardedEvaluator, LocalExchange,
+                                            LocalPeerExchange, ShardBackend, TorchExchange, exchange_bytes)
 
     n = 1 << 17
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -515,11 +518,14 @@ def run_limb(args):
     if args.virtual_shards and world == 1:
         G = args.virtual_shards
         shards = [ShardBackend(C, G, r) for r in range(G)]
-        exch = LocalExchange()
+        exch = LocalPeerExchange(shards) if args.exchange == "peer" else LocalExchange()
     else:
         G = world
         shards = [ShardBackend(C, world, rank)]
-        exch = TorchExchange() if world > 1 else LocalExchange()
+        if args.exchange == "peer":
+            exch = IpcPeerExchange(shards[0]) if world > 1 else LocalPeerExchange(shards)
+        else:
+            exch = TorchExchange() if world > 1 else LocalExchange()
     lays = [s.layout for s in shards]
     ev = LimbShardedEvaluator(shards, exch)
     xs = [lay.split_ct(x, LEVEL) for lay in lays]
@@ -560,6 +566,9 @@ def run_limb(args):
         exact = bool(torch.equal(got, full_hm.data))
     else:
         exact = None
+    peer_errors = exch.errors() if hasattr(exch, "errors") else None
+    if peer_errors and any(peer_errors):
+        raise RuntimeError(f"peer exchange timed out: {peer_errors}")
     if rank == 0:
         xb = exchange_bytes(lays[0], n, LEVEL, MERGED) + exchange_bytes(lays[0], n, LEVEL, MOD_DOWN)
         line = {
@@ -570,8 +579,11 @@ def run_limb(args):
             "dtype": "int32 residues (u32 mod q < 2^29, int64 accum)",
             "data": "synthetic uniform residues (ciphertext and keys), random-init",
             "config": {"workload": "BASELINE config 4: 1 HMult+relin (merged rescale) + 1 HRot(r=1) per step on one "
-                                   "ciphertext at N=2^17, l=24, alpha=8, limbs sharded over the ranks; all-gather "
-                                   "of the BConv source rows (NCCL) before ModUp and ModDown",
+                                   "ciphertext at N=2^17, l=24, alpha=8, limbs sharded over the ranks; BConv source "
+                                   "rows exchanged before ModUp and ModDown: "
+                                   + ("peer-mapped loads inside BConv (CUDA IPC, epoch flags)" if args.exchange == "peer"
+                                      else "NCCL all-gather + copy"),
+                       "exchange": args.exchange,
                        "n": n, "l": L, "alpha": ALPHA, "level": LEVEL, "shards": G,
                        "virtual_shards_on_one_gpu": bool(args.virtual_shards and world == 1),
                        "parallelism": f"limb-sharded x{G}"},
@@ -580,6 +592,10 @@ def run_limb(args):
             "bit_exact_vs_single_device": exact,
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()  # no rank frees its exchange buffer while a peer may still read it
+    if hasattr(exch, "close"):
+        exch.close()
     if world > 1:
         dist.destroy_process_group()
 
