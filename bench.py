@@ -88,6 +88,7 @@ class ClockSampler:
             while True:
                 self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
                 self.bits |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self._ready.set()
                 if self._stop.wait(0.002):
                     break
             nv.nvmlShutdown()
@@ -99,6 +100,7 @@ class ClockSampler:
                                   "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                                   "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                                   "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+            self._ready.set()
             r = [x.strip() for x in out.stdout.strip().split(",")]
             self.sm.append(float(r[0]))
             self.mx.append(float(r[1]))
@@ -109,8 +111,11 @@ class ClockSampler:
             pass
 
     def __enter__(self):
+        # NVML initialises before the timed region starts: wait for the first sample
+        self._ready = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(timeout=5)
         return self
 
     def __exit__(self, *a):
@@ -340,6 +345,18 @@ def main():
                 "bytes_per_launch_group": round(p["bytes"] / max(p["groups"], 1)),
                 "avg_group_ms": round(p["ms"] / max(p["groups"], 1), 4)}
 
+    def int_pipe(p):
+        """INT-pipe view of an NTT class (report it beside GB/s).
+        A radix-2 N=2^16 limb is 16 x 32768 butterflies for 524,288 algorithmic
+        bytes, so butterflies/s == algorithmic B/s."""
+        bfly_s = p["bytes"] / (p["ms"] * 1e-3)
+        mhz = clk.summary().get("sm_mhz") or 1965.0
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        per = bfly_s / (sms * mhz * 1e6)
+        return {"butterflies_per_clk_per_sm": round(per, 2), "ceiling": 11.7,
+                "ceiling_source": "Shoup butterfly microbenchmark, tools/microbench_bfly2.cu "
+                                  "(profiles/round1_session2.md)", "frac": round(per / 11.7, 3)}
+
     # ---- e2e: host ciphertexts in pinned memory, H2D + compute + D2H every step
     e2e = None
     if not args.no_e2e:
@@ -464,7 +481,7 @@ def main():
             "hmult_ops_per_s": round(B * args.steps * world / (hm_ms / 1e3), 2),
             "hrot_ops_per_s": round(B * args.steps * world / (hr_ms / 1e3), 2),
             "roofline": roof(dom),
-            "roofline_ntt": roof(ntt),
+            "roofline_ntt": dict(roof(ntt), int_pipe=int_pipe(ntt)),
             "kernels": kern,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
