@@ -171,8 +171,8 @@ ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, dou
 /* Element-wise parts of decrypt / encrypt (ckks.cpp:497-553).  All operands
  * are evaluation-domain Montgomery rows (canonical); the randomness of
  * encrypt is supplied by the caller (the reference samples it on the host with
- * mt19937_64, ckks.cpp:390-430) and turned into evaluation form with
- * ck_coeffs_to_eval.
+ * mt19937_64, ckks.cpp:390-430; ck_sample_* below replay that stream) and
+ * turned into evaluation form with ck_coeffs_to_eval.
  *   decrypt     out [B][level]   = ct.b + ct.a * s        (ct [B][2][level], s [level])
  *   encrypt_sk  out [2][level]   = (m + e - a s, a)
  *   encrypt_pk  out [2][level]   = (v pk.b + e0 + m, v pk.a + e1)   (pk [2][level]) */
@@ -255,6 +255,21 @@ ck_status ck_shard_switch_begin(ck_shard* sh, int kind, uint32_t level, const ui
 ck_status ck_shard_switch_end(ck_shard* sh, int kind, uint32_t level, const uint32_t* recv, const uint32_t* v,
                               const uint32_t* addend, uint32_t add_mask, int32_t rotate, int64_t r, uint32_t* out,
                               ck_stream stream);
+/* The reference's randomness, host side as in the reference: a
+ * std::mt19937_64(seed) consumed exactly as ckks.cpp does, so a seed
+ * reproduces the reference's keys and ciphertexts bit for bit.
+ *   ck_sample_gaussian   sample_gaussian x n   (ckks.cpp:33-47)
+ *   ck_sample_ternary    ternary_coeffs        (ckks.cpp:51-60)
+ *   ck_sample_uniform    uniform_eval residues (ckks.cpp:383-395), out [rows][n] host
+ *   ck_rng_draws         raw 64-bit outputs (e.g. for std::uniform_real_distribution slots) */
+typedef struct ck_rng ck_rng;
+ck_status ck_rng_create(uint64_t seed, ck_rng** out);
+ck_status ck_rng_destroy(ck_rng* rng);
+ck_status ck_rng_draws(ck_rng* rng, uint64_t count, uint64_t* out);
+ck_status ck_sample_gaussian(ck_rng* rng, uint32_t n, double sigma, int64_t* out);
+ck_status ck_sample_ternary(ck_rng* rng, uint32_t n, uint32_t h, int64_t* out);
+ck_status ck_sample_uniform(ck_rng* rng, const uint32_t* q, uint32_t rows, uint32_t n, uint32_t* out);
+
 /* Peer exchange ("peer-mapped loads inside BConv"), replacing
  * the host all-gather: every rank allocates ONE exchange buffer, the ranks map
  * each other's buffers (CUDA IPC across processes: ck_ipc_*; plain pointers

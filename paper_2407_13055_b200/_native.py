@@ -87,6 +87,12 @@ _SIGS = {
     "ck_shard_switch_begin": [_vp, ctypes.c_int, _u32, _vp, _vp, _vp],
     "ck_shard_switch_end": [_vp, ctypes.c_int, _u32, _vp, _vp, _vp, _u32, ctypes.c_int32, _i64, _vp, _vp],
     "ck_shard_tensor": [_vp, _u32, _vp, _vp, _vp, _vp, _vp],
+    "ck_rng_create": [ctypes.c_uint64, ctypes.POINTER(_vp)],
+    "ck_rng_destroy": [_vp],
+    "ck_rng_draws": [_vp, ctypes.c_uint64, _vp],
+    "ck_sample_gaussian": [_vp, _u32, ctypes.c_double, _vp],
+    "ck_sample_ternary": [_vp, _u32, _u32, _vp],
+    "ck_sample_uniform": [_vp, _vp, _u32, _u32, _vp],
     "ck_shard_exchange_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint64)],
     "ck_shard_set_peers": [_vp, ctypes.POINTER(ctypes.c_uint64), _u32],
     "ck_shard_set_timeout": [_vp, ctypes.c_uint64],

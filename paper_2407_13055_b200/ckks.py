@@ -500,7 +500,47 @@ def encrypt_pk(ctx: CkksContext, pt: Plaintext, pk: Ciphertext, v: Polynomial, e
     return Ciphertext(out, pt.scale, l)
 
 
-def keygen(ctx: CkksContext, rng: np.random.Generator) -> torch.Tensor:
+class RefRng:
+    """The reference's randomness: ``std::mt19937_64(seed)`` consumed draw for
+    draw as ckks.cpp does (host side, sequential, like the reference; C ABI
+    ``ck_rng_*`` / ``ck_sample_*``).  Pass it wherever an ``rng`` is taken and
+    keys / ciphertexts come out bit-identical to the reference's for the same
+    seed (tests/test_gpu_keys.py against the golden fixtures).  A numpy
+    Generator is accepted too (different stream, same distributions)."""
+
+    def __init__(self, seed: int):
+        h = ctypes.c_void_p()
+        nat.call("ck_rng_create", ctypes.c_uint64(seed), ctypes.byref(h))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            nat.call("ck_rng_destroy", self._h)
+            self._h = None
+
+    def draws(self, count: int) -> np.ndarray:
+        out = np.empty(count, np.uint64)
+        nat.call("ck_rng_draws", self._h, ctypes.c_uint64(count), out.ctypes.data)
+        return out
+
+    def gaussian(self, n: int, sigma: float) -> np.ndarray:
+        out = np.empty(n, np.int64)
+        nat.call("ck_sample_gaussian", self._h, n, ctypes.c_double(sigma), out.ctypes.data)
+        return out
+
+    def ternary(self, n: int, h: int) -> np.ndarray:
+        out = np.empty(n, np.int64)
+        nat.call("ck_sample_ternary", self._h, n, h, out.ctypes.data)
+        return out
+
+    def uniform(self, primes: Sequence[int], n: int) -> np.ndarray:
+        q = np.ascontiguousarray(np.asarray(primes, np.uint32))
+        out = np.empty((len(q), n), np.uint32)
+        nat.call("ck_sample_uniform", self._h, q.ctypes.data, len(q), n, out.ctypes.data)
+        return out
+
+
+def keygen(ctx: CkksContext, rng) -> torch.Tensor:
     """keygen (ckks.cpp:399-405): ternary secret of Hamming weight
     params.hamming (host sampling) -> evaluation rows over the full L + alpha
     basis (the reference's sk.s)."""
@@ -508,12 +548,31 @@ def keygen(ctx: CkksContext, rng: np.random.Generator) -> torch.Tensor:
     return coeffs_to_eval(ctx, c, ctx.params.l, ctx.params.alpha).data
 
 
-def pubkey_gen(ctx: CkksContext, s: torch.Tensor, rng: np.random.Generator) -> Ciphertext:
+def pubkey_gen(ctx: CkksContext, s: torch.Tensor, rng) -> Ciphertext:
     """pubkey_gen (ckks.cpp:407-424): (b, a) = (e - a s, a) at level L."""
     l = ctx.params.l
     zero = Plaintext(Polynomial(torch.zeros((l, ctx.n), dtype=torch.int32, device=ctx.device), l), Fraction(1), l)
-    return encrypt_sk(ctx, zero, s, uniform_eval(ctx, l, rng),
-                      coeffs_to_eval(ctx, sample_gaussian(ctx.n, ctx.params.sigma, rng), l))
+    a = uniform_eval(ctx, l, rng)
+    return encrypt_sk(ctx, zero, s, a, coeffs_to_eval(ctx, sample_gaussian(ctx.n, ctx.params.sigma, rng), l))
+
+
+def encrypt(ctx: CkksContext, pt: Plaintext, key, rng) -> Ciphertext:
+    """encrypt (ckks.hpp:164-167): `key` is the secret (sk.s rows, a tensor)
+    or a public key (Ciphertext); the randomness is drawn in the reference's
+    order (secret key: a, then e, ckks.cpp:504-505; public key: v, e0, e1,
+    ckks.cpp:523-526) and the arithmetic runs on the GPU."""
+    l, n = pt.level, ctx.n
+    if isinstance(key, Ciphertext):
+        v = coeffs_to_eval(ctx, sample_ternary(n, min(ctx.params.hamming, n // 4), rng), l)
+        e0 = coeffs_to_eval(ctx, sample_gaussian(n, ctx.params.sigma, rng), l)
+        e1 = coeffs_to_eval(ctx, sample_gaussian(n, ctx.params.sigma, rng), l)
+        return encrypt_pk(ctx, pt, key, v, e0, e1)
+    _check_eval_mont(pt.poly, "encrypt")
+    if pt.poly.p_count != 0:
+        raise ValueError("cannot encrypt a P-extended plaintext")
+    a = uniform_eval(ctx, l, rng)
+    e = coeffs_to_eval(ctx, sample_gaussian(n, ctx.params.sigma, rng), l)
+    return encrypt_sk(ctx, pt, key, a, e)
 
 
 def evk_gen(ctx: CkksContext, s: torch.Tensor, kind: str, rotation: int, rng: np.random.Generator) -> EvaluationKey:
@@ -544,9 +603,7 @@ def evk_gen(ctx: CkksContext, s: torch.Tensor, kind: str, rotation: int, rng: np
         dhat = q_full // dk
         g = P * dhat * pow(dhat, -1, dk)
         gm = [((g % q) << 32) % q for q in primes]
-        a_k = torch.cat([uniform_eval(ctx, L, rng),
-                         torch.from_numpy((rng.integers(0, 1 << 62, (A, n), dtype=np.int64)
-                                           % np.array(primes[L:], np.int64)[:, None]).astype(np.int32)).to(ctx.device)])
+        a_k = _uniform_rows(ctx, primes, rng)  # Q rows then P rows, as uniform_eval(l, alpha)
         e_k = coeffs_to_eval(ctx, sample_gaussian(n, ctx.params.sigma, rng), L, A).data
         out[k, 1] = a_k
         nat.call("ck_evk_digit", ctx.handle, _ptr(s_src), _ptr(s_dst), _ptr(out[k, 1]), _ptr(e_k),
@@ -554,24 +611,35 @@ def evk_gen(ctx: CkksContext, s: torch.Tensor, kind: str, rotation: int, rng: np
     return EvaluationKey(out, kind, rotation if kind == ROTATION else 0)
 
 
-# Host-side samplers for the encryption randomness (numpy Generator; the
-# reference samples with std::mt19937_64, ckks.cpp:390-430, so the streams
-# differ — the GPU arithmetic on given randomness is what is bit-exact).
-def sample_ternary(n: int, hamming: int, rng: np.random.Generator) -> np.ndarray:
+# Host-side samplers for the encryption randomness: with a RefRng the
+# reference's own stream (bit-exact keys / ciphertexts); with a numpy
+# Generator the same distributions from a different stream.
+def sample_ternary(n: int, hamming: int, rng) -> np.ndarray:
+    if isinstance(rng, RefRng):
+        return rng.ternary(n, hamming)
     c = np.zeros(n, np.int64)
     idx = rng.choice(n, size=hamming, replace=False)
     c[idx] = rng.choice(np.array([-1, 1], np.int64), size=hamming)
     return c
 
 
-def sample_gaussian(n: int, sigma: float, rng: np.random.Generator) -> np.ndarray:
+def sample_gaussian(n: int, sigma: float, rng) -> np.ndarray:
+    if isinstance(rng, RefRng):
+        return rng.gaussian(n, sigma)
     return np.rint(rng.normal(0.0, sigma, n)).astype(np.int64)
 
 
-def uniform_eval(ctx: CkksContext, level: int, rng: np.random.Generator) -> torch.Tensor:
-    q = ctx.q_primes[:level].astype(np.int64)[:, None]
-    return torch.from_numpy((rng.integers(0, 1 << 62, (level, ctx.n), dtype=np.int64) % q).astype(np.int32)).to(
-        ctx.device)
+def _uniform_rows(ctx: CkksContext, primes: Sequence[int], rng) -> torch.Tensor:
+    if isinstance(rng, RefRng):
+        u = rng.uniform(primes, ctx.n)
+    else:
+        q = np.asarray(primes, np.int64)[:, None]
+        u = rng.integers(0, 1 << 62, (len(primes), ctx.n), dtype=np.int64) % q
+    return torch.from_numpy(u.astype(np.int64).astype(np.int32)).to(ctx.device)
+
+
+def uniform_eval(ctx: CkksContext, level: int, rng) -> torch.Tensor:
+    return _uniform_rows(ctx, [int(v) for v in ctx.q_primes[:level]], rng)
 
 
 # ----------------------------------------------------------- kernel level --

@@ -16,6 +16,7 @@
 #include <complex>
 #include <cstdint>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -66,6 +67,8 @@ struct Scale {
 
 struct CkksParams {  // ckks.hpp:46-54
   uint32_t n = 1u << 16, l = 54, alpha = 14, delta_bits = 48;
+  uint32_t hamming = 256;  // secret Hamming weight (host-side sampling)
+  double sigma = 3.2;      // error standard deviation
   bool lazy_rescale = false;
 };
 
@@ -359,6 +362,117 @@ inline Plaintext decrypt(CkksContext& ctx, const Ciphertext& ct, const DeviceBuf
   Plaintext pt{DeviceBuffer(ctx.raw(), (size_t)ct.level * ctx.params().n), ct.scale, ct.level, 0};
   check(ck_decrypt(ctx.raw(), ct.level, 1, ct.data.data(), s.data(), pt.data.data(), nullptr));
   return pt;
+}
+
+// ---- keys and encryption with the caller's std::mt19937_64 (ckks.hpp:155-167) ----
+// The randomness is drawn on the host from the caller's generator in the
+// reference's order and with its formulas (Box-Muller on two 53-bit draws,
+// Fisher-Yates ternary positions, rng() % q residues: ckks.cpp:33-60,
+// 383-395), so a generator state yields the reference's keys and ciphertexts
+// bit for bit; the arithmetic (coeffs_to_eval NTTs, the products) is on the GPU.
+namespace detail {
+inline std::vector<int64_t> gaussian(std::mt19937_64& rng, uint32_t n, double sigma) {
+  std::vector<int64_t> out(n);
+  for (auto& v : out) {
+    const double u1 = (static_cast<double>(rng() >> 11) + 0.5) * 0x1p-53;
+    const double u2 = static_cast<double>(rng() >> 11) * 0x1p-53;
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    v = std::llround(r * std::cos(2.0 * 3.141592653589793238462643383279502884 * u2) * sigma);
+  }
+  return out;
+}
+inline std::vector<int64_t> ternary(std::mt19937_64& rng, uint32_t n, uint32_t h) {
+  if (h > n) throw std::invalid_argument("hamming weight exceeds n");
+  std::vector<uint32_t> pos(n);
+  for (uint32_t i = 0; i < n; ++i) pos[i] = i;
+  std::vector<int64_t> out(n, 0);
+  for (uint32_t i = 0; i < h; ++i) {  // partial Fisher-Yates: position i picks from [i, n)
+    std::swap(pos[i], pos[i + static_cast<uint32_t>(rng() % (n - i))]);
+    out[pos[i]] = (rng() & 1) ? 1 : -1;
+  }
+  return out;
+}
+// coeffs_to_eval (ckks.cpp:366-380) on the GPU: [level + pc][n]
+inline DeviceBuffer coeffs_to_eval(CkksContext& ctx, const std::vector<int64_t>& c, uint32_t level, uint32_t pc) {
+  const uint32_t n = ctx.params().n;
+  DeviceBuffer dc(ctx.raw(), 2ull * n);
+  dc.upload(reinterpret_cast<const uint32_t*>(c.data()), 2ull * n);
+  DeviceBuffer out(ctx.raw(), (size_t)(level + pc) * n);
+  check(ck_coeffs_to_eval(ctx.raw(), reinterpret_cast<const int64_t*>(dc.data()), level, pc, out.data(), nullptr));
+  check(ck_stream_sync(ctx.raw(), nullptr));
+  return out;
+}
+// uniform_eval (ckks.cpp:383-395): Q rows [0, qc) then P rows [0, pc), rng() % q
+inline DeviceBuffer uniform_eval(CkksContext& ctx, std::mt19937_64& rng, uint32_t qc, uint32_t pc) {
+  const uint32_t n = ctx.params().n, L = ctx.params().l;
+  std::vector<uint32_t> h((size_t)(qc + pc) * n);
+  for (uint32_t i = 0; i < qc + pc; ++i) {
+    const uint64_t q = ctx.primes()[i < qc ? i : L + (i - qc)];
+    for (uint32_t k = 0; k < n; ++k) h[(size_t)i * n + k] = static_cast<uint32_t>(rng() % q);
+  }
+  DeviceBuffer out(ctx.raw(), h.size());
+  out.upload(h.data(), h.size());
+  return out;
+}
+}  // namespace detail
+
+struct SecretKey {  // ckks.hpp:68-71: coefficients and evaluation rows over L + alpha
+  std::vector<int64_t> coeffs;
+  DeviceBuffer s;
+};
+struct PublicKey {  // ckks.hpp:73-77: (b, a) at level L, data = [2][L][n]
+  DeviceBuffer data;
+};
+
+inline SecretKey keygen(CkksContext& ctx, std::mt19937_64& rng) {  // ckks.cpp:399-405
+  SecretKey sk;
+  sk.coeffs = detail::ternary(rng, ctx.params().n, ctx.params().hamming);
+  sk.s = detail::coeffs_to_eval(ctx, sk.coeffs, ctx.params().l, ctx.params().alpha);
+  return sk;
+}
+
+namespace detail {
+inline void encrypt_sk_into(CkksContext& ctx, uint32_t l, const uint32_t* m, const SecretKey& sk,
+                            std::mt19937_64& rng, uint32_t* out) {
+  DeviceBuffer a = uniform_eval(ctx, rng, l, 0);
+  DeviceBuffer e = coeffs_to_eval(ctx, gaussian(rng, ctx.params().n, ctx.params().sigma), l, 0);
+  check(ck_encrypt_sk(ctx.raw(), l, m, a.data(), e.data(), sk.s.data(), out, nullptr));
+  check(ck_stream_sync(ctx.raw(), nullptr));
+}
+}  // namespace detail
+
+inline PublicKey pubkey_gen(CkksContext& ctx, const SecretKey& sk, std::mt19937_64& rng) {  // ckks.cpp:407-424
+  const uint32_t l = ctx.params().l, n = ctx.params().n;
+  DeviceBuffer zero(ctx.raw(), (size_t)l * n);
+  std::vector<uint32_t> z((size_t)l * n, 0);
+  zero.upload(z.data(), z.size());
+  PublicKey pk{DeviceBuffer(ctx.raw(), 2ull * l * n)};
+  detail::encrypt_sk_into(ctx, l, zero.data(), sk, rng, pk.data.data());
+  return pk;
+}
+
+// encrypt (ckks.cpp:497-539): (m + e - a s, a) / (v pk.b + e0 + m, v pk.a + e1)
+inline Ciphertext encrypt(CkksContext& ctx, const Plaintext& pt, const SecretKey& sk, std::mt19937_64& rng) {
+  if (pt.p_count != 0) throw std::invalid_argument("cannot encrypt a P-extended plaintext");
+  Ciphertext ct = make_ciphertext(ctx, pt.level, pt.scale);
+  detail::encrypt_sk_into(ctx, pt.level, pt.data.data(), sk, rng, ct.data.data());
+  return ct;
+}
+inline Ciphertext encrypt(CkksContext& ctx, const Plaintext& pt, const PublicKey& pk, std::mt19937_64& rng) {
+  if (pt.p_count != 0) throw std::invalid_argument("cannot encrypt a P-extended plaintext");
+  const uint32_t l = pt.level, n = ctx.params().n, L = ctx.params().l;
+  DeviceBuffer v = detail::coeffs_to_eval(ctx, detail::ternary(rng, n, ctx.params().hamming), l, 0);
+  DeviceBuffer e0 = detail::coeffs_to_eval(ctx, detail::gaussian(rng, n, ctx.params().sigma), l, 0);
+  DeviceBuffer e1 = detail::coeffs_to_eval(ctx, detail::gaussian(rng, n, ctx.params().sigma), l, 0);
+  DeviceBuffer pkl(ctx.raw(), 2ull * l * n);  // the level-l prefix of both halves
+  check(ck_memcpy_d2d(ctx.raw(), pkl.data(), pk.data.data(), (size_t)l * n * 4, nullptr));
+  check(ck_memcpy_d2d(ctx.raw(), pkl.data() + (size_t)l * n, pk.data.data() + (size_t)L * n, (size_t)l * n * 4,
+                      nullptr));
+  Ciphertext ct = make_ciphertext(ctx, l, pt.scale);
+  check(ck_encrypt_pk(ctx.raw(), l, pt.data.data(), v.data(), e0.data(), e1.data(), pkl.data(), ct.data.data(),
+                      nullptr));
+  check(ck_stream_sync(ctx.raw(), nullptr));
+  return ct;
 }
 
 }  // namespace ckks32::b200

@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -1764,6 +1765,66 @@ ck_status ck_memcpy_d2h(ck_context* ctx, void* dst, const void* src, size_t byte
 ck_status ck_memcpy_d2d(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream) {
   return guard([&] { CK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, S(stream))); (void)ctx; });
 }
+// ---- the reference's randomness (host side, as in the reference) ----
+// std::mt19937_64 consumed draw for draw like ckks.cpp: sample_gaussian
+// (:33-40, Box-Muller on two 53-bit draws, llround), ternary_coeffs (:51-60,
+// Fisher-Yates positions + sign bit), uniform_eval (:383-395, rng() % q row
+// by row).  Compiled by the same g++/glibc as the reference, with the same
+// expressions, so a seed reproduces the reference's keys and ciphertexts.
+struct ck_rng {
+  std::mt19937_64 g;
+};
+ck_status ck_rng_create(uint64_t seed, ck_rng** out) {
+  return guard([&] {
+    if (!out) throw InvalidArgument("null argument");
+    *out = new ck_rng{std::mt19937_64(seed)};
+  });
+}
+ck_status ck_rng_destroy(ck_rng* r) {
+  return guard([&] { delete r; });
+}
+ck_status ck_rng_draws(ck_rng* r, uint64_t count, uint64_t* out) {
+  return guard([&] {
+    if (!r || (count && !out)) throw InvalidArgument("null argument");
+    for (uint64_t i = 0; i < count; ++i) out[i] = r->g();
+  });
+}
+ck_status ck_sample_gaussian(ck_rng* r, uint32_t n, double sigma, int64_t* out) {
+  return guard([&] {
+    if (!r || (n && !out)) throw InvalidArgument("null argument");
+    constexpr double kPi = 3.141592653589793238462643383279502884;  // std::numbers::pi
+    for (uint32_t i = 0; i < n; ++i) {
+      const double u1 = (static_cast<double>(r->g() >> 11) + 0.5) * 0x1p-53;
+      const double u2 = static_cast<double>(r->g() >> 11) * 0x1p-53;
+      const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * kPi * u2);
+      out[i] = std::llround(z * sigma);
+    }
+  });
+}
+ck_status ck_sample_ternary(ck_rng* r, uint32_t n, uint32_t h, int64_t* out) {
+  return guard([&] {
+    if (!r || !out) throw InvalidArgument("null argument");
+    if (h > n) throw InvalidArgument("hamming weight exceeds n");
+    std::vector<uint32_t> idx(n);
+    for (uint32_t i = 0; i < n; ++i) idx[i] = i;
+    for (uint32_t i = 0; i < n; ++i) out[i] = 0;
+    for (uint32_t i = 0; i < h; ++i) {
+      const uint32_t j = i + static_cast<uint32_t>(r->g() % (n - i));
+      std::swap(idx[i], idx[j]);
+      out[idx[i]] = (r->g() & 1) ? 1 : -1;
+    }
+  });
+}
+ck_status ck_sample_uniform(ck_rng* r, const uint32_t* q, uint32_t rows, uint32_t n, uint32_t* out) {
+  return guard([&] {
+    if (!r || (rows && (!q || !out))) throw InvalidArgument("null argument");
+    for (uint32_t i = 0; i < rows; ++i) {
+      if (q[i] == 0) throw InvalidArgument("zero modulus");
+      for (uint32_t k = 0; k < n; ++k) out[(size_t)i * n + k] = static_cast<uint32_t>(r->g() % q[i]);
+    }
+  });
+}
+
 ck_status ck_stream_sync(ck_context* ctx, ck_stream stream) {
   return guard([&] { CK_CUDA(cudaStreamSynchronize(S(stream))); (void)ctx; });
 }

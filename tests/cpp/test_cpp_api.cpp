@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <fstream>
 #include <iostream>
+#include <random>
+#include <string>
 #include <stdexcept>
 #include <vector>
 
@@ -31,7 +33,46 @@ static void write_file(const std::string& p, const std::vector<uint32_t>& v) {
   f.write(reinterpret_cast<const char*>(v.data()), v.size() * 4);
 }
 
+// keys mode: keygen + encode + secret-key encrypt with the reference's own
+// generator type, in the fixture driver's order (oracle/ref_driver.cpp
+// ref_gen_fixtures: keygen, 3 x evk_gen (skipped here: discard), slots u, v)
+//   test_cpp_api keys <dir> <seed> <n> <l> <alpha> <delta_bits>
+// writes <dir>/sk_rows.bin [L+alpha][n], ct_u.bin, ct_v.bin [2][l][n]
+static int keys_mode(char** argv) {
+  const std::string dir = argv[2];
+  std::mt19937_64 rng(std::strtoull(argv[3], nullptr, 10));
+  CkksParams p;
+  p.n = std::atoi(argv[4]);
+  p.l = std::atoi(argv[5]);
+  p.alpha = std::atoi(argv[6]);
+  p.delta_bits = std::atoi(argv[7]);
+  p.hamming = std::min<uint32_t>(p.hamming, p.n / 4);  // bench.cpp:337
+  CkksContext ctx(p);
+  SecretKey sk = keygen(ctx, rng);
+  write_file(dir + "/sk_rows.bin", sk.s.download());
+  const uint64_t D = ctx.num_digits(p.l);
+  rng.discard(3 * D * ((uint64_t)(p.l + p.alpha) * p.n + 2ull * p.n));  // relin, rot1, rot3 evk_gen draws
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  std::vector<std::complex<double>> z[2];  // slots u, v drawn before either encryption
+  for (auto& zz : z) {
+    zz.resize(p.n / 2);
+    for (auto& v : zz) {
+      const double re = dist(rng);
+      v = {re, dist(rng)};
+    }
+  }
+  for (int i = 0; i < 2; ++i) {
+    Plaintext pt = encode(ctx, z[i], ctx.default_scale(), p.l);
+    if (i == 1) write_file(dir + "/pt_v.bin", pt.data.download());
+    Ciphertext ct = encrypt(ctx, pt, sk, rng);
+    write_file(dir + (i ? "/ct_v.bin" : "/ct_u.bin"), ct.data.download());
+  }
+  std::printf("cpp keys ok\n");
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 8 && std::string(argv[1]) == "keys") return keys_mode(argv);
   if (argc < 6) {
     std::fprintf(stderr, "usage: %s dir n l alpha level\n", argv[0]);
     return 2;

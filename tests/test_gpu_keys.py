@@ -52,3 +52,47 @@ def test_gpu_keys_encrypted_round_trip(n, l, a, db):
     prod2 = ckks.hmult(C, prod, ckks.hmult(C, c2, c2, relin), relin)
     assert np.abs(dec(prod2) - z1 * z2 ** 3).max() < 2.0 ** -8
     C.close()
+
+
+from golden_util import SMALL_DIRS, SMALL_SEEDS, Fixture, parse_small_name, ref_unit_slots  # noqa: E402
+
+
+@pytest.mark.parametrize("d", SMALL_DIRS, ids=lambda p: p.name)
+def test_reference_rng_reproduces_reference_keys_and_ciphertexts(d):
+    """With the reference's randomness (ckks.RefRng = std::mt19937_64(seed)
+    consumed as ckks.cpp does) the GPU keygen / evk_gen / encode / encrypt
+    reproduce the reference's own fixtures bit for bit: sk.s, the relin and
+    rotation keys, and both secret-key ciphertexts (ref_driver.cpp
+    ref_gen_fixtures order)."""
+    F = Fixture(d)
+    n, l, a = parse_small_name(d)
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=F.db))
+    rng = ckks.RefRng(SMALL_SEEDS[(n, l, a)])
+    s = ckks.keygen(C, rng)
+    np.testing.assert_array_equal(s.cpu().numpy().astype(np.uint32), F.poly("sk").rows)
+    for name, kind, r in (("evk_relin", ckks.RELIN, 0), ("evk_rot1", ckks.ROTATION, 1), ("evk_rot3", ckks.ROTATION, 3)):
+        k = ckks.evk_gen(C, s, kind, r, rng)
+        np.testing.assert_array_equal(k.data.cpu().numpy().astype(np.uint32), F.evk(name).stacked(), err_msg=name)
+    u = ref_unit_slots(rng.draws(n))
+    v = ref_unit_slots(rng.draws(n))
+    for name, z in (("ct_u", u), ("ct_v", v)):
+        ct = ckks.encrypt(C, ckks.encode(C, z, C.default_scale(), l), s, rng)
+        want = F.ct(name)
+        np.testing.assert_array_equal(ct.data.cpu().numpy().astype(np.uint32), Fixture.ct_rows(want), err_msg=name)
+        assert ct.scale == want.scale and ct.level == want.level
+    C.close()
+
+
+def test_reference_rng_public_key_encrypt_decrypts():
+    """pubkey_gen + public-key encrypt with the reference's stream (v, e0, e1
+    order of ckks.cpp:523-526) decrypt to the message."""
+    n, l, a, db = 1024, 8, 3, 48
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db))
+    rng = ckks.RefRng(99)
+    s = ckks.keygen(C, rng)
+    pk = ckks.pubkey_gen(C, s, rng)
+    z = ref_unit_slots(rng.draws(n))
+    ct = ckks.encrypt(C, ckks.encode(C, z, C.default_scale(), l), pk, rng)
+    back = ckks.decode(C, ckks.decrypt(C, ct, s))
+    assert np.abs(back - z).max() < 2.0 ** -20
+    C.close()

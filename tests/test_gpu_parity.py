@@ -510,6 +510,35 @@ def test_cpp_mirror_drop_in(tmp_path):
     np.testing.assert_array_equal(got, np.stack([canon(O, rb, level), canon(O, ra, level)]))
 
 
+def test_cpp_mirror_keys_with_std_mt19937_64(tmp_path):
+    """keygen / encode / encrypt of the C++ mirror take the caller's
+    std::mt19937_64 (ckks.hpp:160-167) and reproduce the reference's own
+    fixtures bit for bit (sk.s, ct_u, ct_v of tests/golden)."""
+    import subprocess
+    from pathlib import Path
+
+    from golden_util import SMALL_DIRS, SMALL_SEEDS, Fixture, parse_small_name
+
+    exe = Path(__file__).resolve().parent.parent / "paper_2407_13055_b200" / "_lib" / "test_cpp_api"
+    if not exe.exists():
+        subprocess.run(["make", "-C", str(exe.parent.parent), "cpp_test"], check=True, capture_output=True)
+    for d in SMALL_DIRS:
+        F = Fixture(d)
+        n, l, a = parse_small_name(d)
+        r = subprocess.run([str(exe), "keys", str(tmp_path), str(SMALL_SEEDS[(n, l, a)]), str(n), str(l), str(a),
+                            str(F.db)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and "cpp keys ok" in r.stdout, r.stdout + r.stderr
+        sk = np.fromfile(tmp_path / "sk_rows.bin", dtype="<u4").reshape(l + a, n)
+        np.testing.assert_array_equal(sk, F.poly("sk").rows)
+        np.testing.assert_array_equal(np.fromfile(tmp_path / "pt_v.bin", dtype="<u4").reshape(l, n),
+                                      F.poly("pt_v").rows, err_msg=f"{d.name} pt_v")
+        for name in ("ct_u", "ct_v"):
+            got = np.fromfile(tmp_path / f"{name}.bin", dtype="<u4").reshape(2, l, n)
+            want = Fixture.ct_rows(F.ct(name))
+            np.testing.assert_array_equal(got[1], want[1], err_msg=f"{d.name} {name}.a")
+            np.testing.assert_array_equal(got[0], want[0], err_msg=f"{d.name} {name}.b")
+
+
 # ------------------------------------------------------------- mod_switch --
 @pytest.mark.parametrize("n", [16, 32, 64, 65536])
 def test_mod_switch_error_characterization(n):
