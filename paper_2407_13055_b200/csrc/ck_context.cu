@@ -23,9 +23,21 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ck32_b200.h"
 #include "ck_common.cuh"
 #include "ck_kernels.h"
+
+// NVTX range per C-ABI mechanism call (tracing), visible in Nsight
+// timelines; a no-op (one pointer test) when no tool is attached.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define CK_RANGE(name) NvtxRange ck_nvtx_range_(name)
 
 namespace ck {
 namespace {
@@ -1831,6 +1843,7 @@ ck_status ck_stream_sync(ck_context* ctx, ck_stream stream) {
 
 ck_status ck_ntt_forward(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, const uint32_t* gidx, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_ntt_forward");
     Context* c = C(ctx);
     check_ptr(rows_dev);
     if (!gidx && rows) throw InvalidArgument("null prime index list");
@@ -1858,6 +1871,7 @@ ck_status ck_ntt_forward(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, con
 ck_status ck_intt_inverse(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
                           const uint32_t* epilogue_mont, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_intt_inverse");
     Context* c = C(ctx);
     check_ptr(rows_dev);
     if (!gidx && rows) throw InvalidArgument("null prime index list");
@@ -1894,6 +1908,7 @@ ck_status ck_intt_inverse(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, co
 ck_status ck_bconv(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,
                    uint32_t* dst_dev, uint32_t dst_count, const uint32_t* dst_gidx, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_bconv");
     Context* c = C(ctx);
     check_ptr(src_dev);
     check_ptr(dst_dev);
@@ -1971,6 +1986,7 @@ ck_status ck_mod_switch(ck_context* ctx, const uint32_t* src_dev, uint32_t src_c
 ck_status ck_automorphism(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t rows, int64_t r,
                           ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_mod_switch");
     Context* c = C(ctx);
     check_ptr(in_dev);
     check_ptr(out_dev);
@@ -2009,6 +2025,7 @@ ck_status ck_ew_mul(ck_context* ctx, const uint32_t* a, const uint32_t* b, uint3
 
 ck_status ck_mod_up(ck_context* ctx, uint32_t level, const uint32_t* d, uint32_t* hoist, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_mod_up");
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(d);
@@ -2030,6 +2047,7 @@ ck_status ck_mod_up(ck_context* ctx, uint32_t level, const uint32_t* d, uint32_t
 ck_status ck_key_mult(ck_context* ctx, uint32_t level, const uint32_t* hoist, const uint32_t* evk, uint32_t* v,
                       ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_key_mult");
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(hoist);
@@ -2053,6 +2071,7 @@ ck_status ck_key_mult(ck_context* ctx, uint32_t level, const uint32_t* hoist, co
 
 ck_status ck_mod_down(ck_context* ctx, uint32_t level, const uint32_t* v, uint32_t* out, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_mod_down");
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(v);
@@ -2068,6 +2087,7 @@ ck_status ck_mod_down(ck_context* ctx, uint32_t level, const uint32_t* v, uint32
 ck_status ck_key_switch(ck_context* ctx, uint32_t level, const uint32_t* d, const uint32_t* evk, uint32_t* out,
                         ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_key_switch");
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(d);
@@ -2089,6 +2109,7 @@ ck_status ck_key_switch(ck_context* ctx, uint32_t level, const uint32_t* d, cons
 ck_status ck_rescale(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, uint32_t* out,
                      ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_rescale");
     Context* c = C(ctx);
     check_level(c, level, 4);
     check_ptr(ct);
@@ -2104,6 +2125,7 @@ ck_status ck_rescale(ck_context* ctx, uint32_t level, uint32_t batch, const uint
 ck_status ck_hmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* x, const uint32_t* y,
                    const uint32_t* relin_evk, uint32_t* out, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_hmult");
     Context* c = C(ctx);
     check_level(c, level, 4);  // ckks.cpp:815
     check_ptr(x);
@@ -2152,6 +2174,7 @@ ck_status ck_hmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32
 ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, int64_t r,
                   const uint32_t* rot_evk, uint32_t* out, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_hrot");
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(ct);
@@ -2232,6 +2255,7 @@ ck_status ck_pmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32
 
 ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, double scale_log2, uint32_t level,
                     int p_extend, uint32_t* out_dev, ck_stream stream) {
+  CK_RANGE("ck_encode");
   ck_status st0 = guard([&] {
     Context* c = C(ctx);
     check_level(c, level);
@@ -2266,6 +2290,7 @@ ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, do
 ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2, double* slots_dev,
                     ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_decode");
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(pt_dev);
@@ -2299,7 +2324,8 @@ ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, dou
 
 ck_status ck_decrypt(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_t* ct, const uint32_t* s,
                      uint32_t* out, ck_stream stream) {
-  return guard([&] {  // ckks.cpp:541-553
+  return guard([&] {
+    CK_RANGE("ck_decrypt");  // ckks.cpp:541-553
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(ct);
@@ -2313,7 +2339,8 @@ ck_status ck_decrypt(ck_context* ctx, uint32_t level, uint32_t batch, const uint
 }
 ck_status ck_encrypt_sk(ck_context* ctx, uint32_t level, const uint32_t* pt, const uint32_t* a, const uint32_t* e,
                         const uint32_t* s, uint32_t* out, ck_stream stream) {
-  return guard([&] {  // ckks.cpp:497-516, randomness (a uniform, e Gaussian in eval form) supplied
+  return guard([&] {
+    CK_RANGE("ck_encrypt_sk");  // ckks.cpp:497-516, randomness (a uniform, e Gaussian in eval form) supplied
     Context* c = C(ctx);
     check_level(c, level);
     for (const void* p : {(const void*)pt, (const void*)a, (const void*)e, (const void*)s, (const void*)out})
@@ -2325,7 +2352,8 @@ ck_status ck_encrypt_sk(ck_context* ctx, uint32_t level, const uint32_t* pt, con
 }
 ck_status ck_encrypt_pk(ck_context* ctx, uint32_t level, const uint32_t* pt, const uint32_t* v, const uint32_t* e0,
                         const uint32_t* e1, const uint32_t* pk, uint32_t* out, ck_stream stream) {
-  return guard([&] {  // ckks.cpp:518-539, randomness (v ternary, e0 e1 Gaussian in eval form) supplied
+  return guard([&] {
+    CK_RANGE("ck_encrypt_pk");  // ckks.cpp:518-539, randomness (v ternary, e0 e1 Gaussian in eval form) supplied
     Context* c = C(ctx);
     check_level(c, level);
     for (const void* p : {(const void*)pt, (const void*)v, (const void*)e0, (const void*)e1, (const void*)pk,
@@ -2386,6 +2414,7 @@ ck_status ck_coeffs_to_eval(ck_context* ctx, const int64_t* coeffs, uint32_t lev
 ck_status ck_hoisted_rotations(ck_context* ctx, uint32_t level, const uint32_t* ct, uint32_t count,
                                const int64_t* rots, const uint32_t* const* evks, uint32_t* out, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_hoisted_rotations");
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(ct);
@@ -2423,6 +2452,7 @@ ck_status ck_hoisted_rotate_accumulate(ck_context* ctx, uint32_t level, const ui
                                        const int64_t* rots, const uint32_t* const* pts,
                                        const uint32_t* const* evks, uint32_t* out, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_hoisted_rotate_accumulate");
     Context* c = C(ctx);
     check_level(c, level);
     check_ptr(ct);
@@ -2574,6 +2604,7 @@ ck_status ck_shard_layout(const ck_shard* sh, uint32_t level, uint32_t out[8]) {
 }
 ck_status ck_shard_modup_begin(ck_shard* sh, uint32_t level, const uint32_t* d, uint32_t* send, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_shard_modup_begin");
     Shard* s = SH(sh);
     check_level(s->c, level);
     if (s->lq(level)) {
@@ -2587,6 +2618,7 @@ ck_status ck_shard_modup_begin(ck_shard* sh, uint32_t level, const uint32_t* d, 
 ck_status ck_shard_modup_keymult(ck_shard* sh, uint32_t level, const uint32_t* recv, const uint32_t* d,
                                  const uint32_t* evk, const uint32_t* fold, uint32_t* v, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_shard_modup_keymult");
     Shard* s = SH(sh);
     check_level(s->c, level);
     if (!s->peer_mode()) check_ptr(recv);
@@ -2604,6 +2636,7 @@ ck_status ck_shard_modup_keymult(ck_shard* sh, uint32_t level, const uint32_t* r
 ck_status ck_shard_switch_begin(ck_shard* sh, int kind, uint32_t level, const uint32_t* v, uint32_t* send,
                                 ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_shard_switch_begin");
     Shard* s = SH(sh);
     check_kind(kind);
     check_level(s->c, level, kind == 0 ? 1 : 4);
@@ -2617,6 +2650,7 @@ ck_status ck_shard_switch_end(ck_shard* sh, int kind, uint32_t level, const uint
                               const uint32_t* addend, uint32_t add_mask, int32_t rotate, int64_t r, uint32_t* out,
                               ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_shard_switch_end");
     Shard* s = SH(sh);
     check_kind(kind);
     check_level(s->c, level, kind == 0 ? 1 : 4);
@@ -2634,6 +2668,7 @@ ck_status ck_shard_switch_end(ck_shard* sh, int kind, uint32_t level, const uint
 ck_status ck_shard_tensor(ck_shard* sh, uint32_t level, const uint32_t* x, const uint32_t* y, uint32_t* d01,
                           uint32_t* d2, ck_stream stream) {
   return guard([&] {
+    CK_RANGE("ck_shard_tensor");
     Shard* s = SH(sh);
     check_level(s->c, level, 4);
     const uint32_t lq = s->lq(level);
