@@ -451,8 +451,10 @@ def main():
     # ---- config 2: HRot over every level (batch B) and a batch sweep at four levels
     sweep = grid = None
     if not args.no_sweep:
+        Xbig = X.data.repeat(max(1, 128 // B), 1, 1, 1) if B < 128 else X.data  # up to B = 128
+
         def hrot_rate(Bs, lv, reps=3):
-            Xl = ckks.Ciphertext(X.data[:Bs, :, :lv].contiguous(), s, lv)
+            Xl = ckks.Ciphertext(Xbig[:Bs, :, :lv].contiguous(), s, lv)
             ckks.hrot(C, Xl, 1, rot)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
@@ -463,7 +465,9 @@ def main():
             return round(reps * Bs / (a.elapsed_time(b) / 1e3), 1)
 
         sweep = {lv: hrot_rate(B, lv) for lv in range(LEVEL, 0, -2)}
-        grid = {f"l{lv}": {f"B{bs}": hrot_rate(bs, lv) for bs in (1, 4, 16, B) if bs <= B} for lv in (24, 16, 8, 2)}
+        grid = {f"l{lv}": {f"B{bs}": hrot_rate(bs, lv) for bs in (1, 2, 4, 8, 16, 32, 64, 128) if bs <= Xbig.shape[0]}
+                for lv in range(LEVEL, 0, -2)}
+        del Xbig
 
     if rank == 0:
         cpu = None if args.no_cpu or world > 1 else cpu_baseline_leg()
