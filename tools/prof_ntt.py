@@ -1,6 +1,6 @@
 """Standalone driver for profiling the NTT / INTT kernels (ncu target).
 
-    python tools/prof_ntt.py [rows] [reps]
+    [LOGN=17] python tools/prof_ntt.py [rows] [reps]
 
 Transforms `rows` limbs (cycling over the 32 primes of config 1) in one
 batched launch pair, `reps` times, and prints the CUDA-event time per limb.
@@ -18,7 +18,8 @@ from paper_2407_13055_b200 import ckks  # noqa: E402
 def main():
     rows = int(sys.argv[1]) if len(sys.argv) > 1 else 768
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-    n, l, a = 1 << 16, 24, 8
+    import os
+    n, l, a = 1 << int(os.environ.get("LOGN", "16")), 24, 8
     C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=55))
     g = np.array([i % (l + a) for i in range(rows)], np.uint32)
     q = torch.tensor(C.primes[g].astype(np.int64), device="cuda")
