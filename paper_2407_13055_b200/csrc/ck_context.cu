@@ -804,6 +804,11 @@ struct Context {
         }
       }
       launches -= 2;
+    } else if (logn == 17 && d_tw2f && use_ntt256) {
+      if (inverse)
+        ntt131k_inverse(a, d_tw2i, st);
+      else
+        ntt131k_forward(a, d_tw2f, st);
     } else if (inverse) {
       ntt_inverse((int)logn, a, st);
     } else {
@@ -1663,6 +1668,40 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
             for (uint32_t blk = 0; blk < (128u >> v); ++blk)
               B[240 + off + blk] = I[(32768u >> v) + (r << (7 - v)) + blk];
           }
+        }
+      }
+      CK_CUDA(cudaMalloc(&c->d_tw2f, t2f.size() * sizeof(uint2)));
+      CK_CUDA(cudaMemcpy(c->d_tw2f, t2f.data(), t2f.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+      CK_CUDA(cudaMalloc(&c->d_tw2i, t2i.size() * sizeof(uint2)));
+      CK_CUDA(cudaMemcpy(c->d_tw2i, t2i.data(), t2i.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    } else if (n == 131072) {
+      // Row-pass twiddles of the 512-point rows (ntt256.cu k_row512), per row r
+      // of 512 in consumption order; x = 512 r + c, forward stage 8 + s uses
+      // F[2^(8+s) + (r << s) + (c >> (9 - s))], inverse stage v uses
+      // I[N / 2^(v+1) + (r << (8 - v)) + (c >> (v + 1))] (ntt.cpp:124-128).
+      std::vector<uint2> t2f((size_t)np * n), t2i((size_t)np * n);
+#pragma omp parallel for schedule(static)
+      for (int g = 0; g < (int)np; ++g) {
+        const uint2* F = fwd.data() + (size_t)g * n;
+        const uint2* I = inv.data() + (size_t)g * n;
+        for (uint32_t r = 0; r < 256; ++r) {
+          uint2* A = t2f.data() + ((size_t)g * 256 + r) * 512;
+          uint2* B = t2i.data() + ((size_t)g * 256 + r) * 512;
+          A[31] = B[511] = make_uint2(0, 0);
+          for (uint32_t s = 0; s < 5; ++s)  // forward phase A (c = tau + 16 j): row-shared, blk = j >> (5 - s)
+            for (uint32_t blk = 0; blk < (1u << s); ++blk) A[(1u << s) - 1 + blk] = F[(256u << s) + (r << s) + blk];
+          for (uint32_t s = 5; s < 9; ++s)  // forward phase B (c = 32 tau + j): per thread, blk = j >> (9 - s)
+            for (uint32_t blk = 0; blk < (1u << (s - 4)); ++blk)
+              for (uint32_t tau = 0; tau < 16; ++tau)
+                A[32 + (((1u << (s - 4)) - 2) + blk) * 16 + tau] = F[(256u << s) + (r << s) + (tau << (s - 4)) + blk];
+          const uint32_t offi[4] = {0, 16, 24, 28}, offr[5] = {0, 16, 24, 28, 30};
+          for (uint32_t v = 0; v < 4; ++v)  // inverse phase A (c = 32 tau + j): per thread, blk = j >> (v + 1)
+            for (uint32_t blk = 0; blk < (16u >> v); ++blk)
+              for (uint32_t tau = 0; tau < 16; ++tau)
+                B[(offi[v] + blk) * 16 + tau] = I[(65536u >> v) + (r << (8 - v)) + (tau << (4 - v)) + blk];
+          for (uint32_t v = 4; v < 9; ++v)  // inverse phase B (c = tau + 16 j): row-shared, blk = j >> (v - 3)
+            for (uint32_t blk = 0; blk < (256u >> v); ++blk)
+              B[480 + offr[v - 4] + blk] = I[(65536u >> v) + (r << (8 - v)) + blk];
         }
       }
       CK_CUDA(cudaMalloc(&c->d_tw2f, t2f.size() * sizeof(uint2)));

@@ -27,6 +27,9 @@ void ntt_inverse(int logn, const NttLaunch& a, cudaStream_t st);
 // row-pass tables built by the host ([prime][256 rows][256] {w, w'}).
 bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st);
 bool ntt256_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st);
+// N = 2^17 (256 columns x 512-point rows; row tables [prime][256][512])
+bool ntt131k_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st);
+bool ntt131k_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st);
 // forward NTT whose row pass also applies the drop-and-divide combine
 // (ckks.cpp:643-651): dst row (p, i) <- (v[p * prow + i] - NTT) * dinv[i]
 struct CombineArgs {

@@ -151,9 +151,10 @@ __device__ __forceinline__ void col_prefetch(ColBuf& B, const uint32_t* g, const
 }
 
 // Decode the i-th column-pass item: tile fastest, then batch, then job.
+template <int TILES = kCTiles>
 __device__ __forceinline__ void col_item(int it, int batch, int& job, int& b, int& tile) {
-  tile = it % kCTiles;
-  const int rest = it / kCTiles;
+  tile = it % TILES;
+  const int rest = it / TILES;
   b = rest % batch;
   job = rest / batch;
 }
@@ -162,7 +163,9 @@ __device__ __forceinline__ void col_item(int it, int batch, int& job, int& b, in
 // instead of inside the tile buffer, so phase B reads them from shared memory
 // after the next item's prefetch has started (no 15 twiddle pairs in
 // registers: 124 -> ~96 registers, MINB CTAs per SM).
-template <bool INV, bool DB, bool TWR = false, int MINB = 1>
+// LOGR: log2 of the row length (8: N = 2^16 = 256 x 256; 9: N = 2^17 =
+// 256 columns of a 256 x 512 matrix, the same 256-point column transform).
+template <bool INV, bool DB, bool TWR = false, int MINB = 1, int LOGR = 8>
 __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
                                              uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
                                              int njobs, const PrimeDev* __restrict__ primes,
@@ -173,23 +176,24 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
   // [2][256] twiddle ring (TWR): right after the single tile buffer (ColBuf::tw unused)
   uint2* twring = reinterpret_cast<uint2*>(smraw + (DB ? 2 * sizeof(ColBuf) : (TWR ? sizeof(ColBuf::tile) : sizeof(ColBuf))));
   const int tid = threadIdx.x, cq = tid & 7, tau = tid >> 3;
-  const int items = njobs * batch * kCTiles;
+  constexpr int RS = 1 << LOGR, NT = 256 << LOGR, TILES = RS / kCCols;  // row stride, limb size, tiles per limb
+  const int items = njobs * batch * TILES;
   // the item decoded (and its job loaded) when it is prefetched is reused
   // when it is processed
   int nb = 0, ntile = 0;
   RowJob nJ{};
   auto prefetch = [&](ColBuf& B, int it, int k) {
     int job;
-    col_item(it, batch, job, nb, ntile);
+    col_item<TILES>(it, batch, job, nb, ntile);
     nJ = jobs[job];
-    const uint32_t* base = INV ? dst + nb * dst_bs + (size_t)nJ.dst_off * kN : src + nb * src_bs + (size_t)nJ.src_off * kN;
+    const uint32_t* base = INV ? dst + nb * dst_bs + (size_t)nJ.dst_off * NT : src + nb * src_bs + (size_t)nJ.src_off * NT;
     if (TWR) {
       const uint32_t* g = base + ntile * kCCols;
-      for (int e = threadIdx.x; e < 256 * 8; e += kCT) cp16(&B.tile[(e >> 3) * 8 + (e & 7)], g + (e >> 3) * kR + 4 * (e & 7));
-      const uint2* tw = tw_full + (size_t)nJ.prime * kN;
+      for (int e = threadIdx.x; e < 256 * 8; e += kCT) cp16(&B.tile[(e >> 3) * 8 + (e & 7)], g + (e >> 3) * RS + 4 * (e & 7));
+      const uint2* tw = tw_full + (size_t)nJ.prime * NT;
       cp16(&twring[(k & 1) * 256 + 2 * threadIdx.x], tw + 2 * threadIdx.x);
     } else {
-      col_prefetch(B, base + ntile * kCCols, tw_full + (size_t)nJ.prime * kN);
+      col_prefetch(B, base + ntile * kCCols, tw_full + (size_t)nJ.prime * NT);  // LOGR = 8 only
     }
   };
   int it = blockIdx.x;
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
     const PrimeDev P = primes[J.prime];
     const uint32_t q = P.q, q2 = P.q2, q4 = 2 * P.q2;
     const uint2* TW = TWR ? twring + (k & 1) * 256 : B.tw;
-    uint32_t* out = dst + b * dst_bs + (size_t)J.dst_off * kN + tile * kCCols + 4 * cq;
+    uint32_t* out = dst + b * dst_bs + (size_t)J.dst_off * NT + tile * kCCols + 4 * cq;
     uint4 v[16];
     if (!INV) {
       // ---- forward, stages 0..7 (r bits 7..0). phase A rows tau + 16 j.
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
       ct_stages16<0, 0x5>(
           v, [&](int t, int blk) { return TWR ? TW[(16 << t) + (tau << t) + blk] : twb[(1 << t) - 1 + blk]; }, q, q2, q4);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) stg4(out + (16 * tau + j) * kR, v[j]);
+      for (int j = 0; j < 16; ++j) stg4(out + (16 * tau + j) * RS, v[j]);
     } else {
       const ExitConst ex = exits[J.epi];
       // ---- inverse, stages 8..15 (r bits 0..7). phase A rows 16 tau + j.
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
 #undef CK_X
       }
 #pragma unroll
-      for (int j = 0; j < 16; ++j) stg4(out + (tau + 16 * j) * kR, v[j]);
+      for (int j = 0; j < 16; ++j) stg4(out + (tau + 16 * j) * RS, v[j]);
     }
     if (DB) __syncthreads();  // buffer k&1 is refilled by the prefetch of iteration k+1
   }
@@ -1066,6 +1070,222 @@ void ntt256_pass(int which, const NttLaunch& a, const uint2* tw2, cudaStream_t s
       launch_col<true>(b, a.dst, a.dst_bs, st);
     }
   }
+}
+
+// ================================================ N = 2^17: 512-point rows ==
+// N = 2^17 as 256 columns x 512-point rows (x = 512 r + c): the column pass is
+// k_col<.., LOGR = 9> (stages 0-7), the row pass below runs the other 9
+// stages on rows of 512.  16 threads per row, 32 elements per thread:
+//   forward  phase A: c = tau + 16 j, stages 8-12 (row-shared twiddles W[0..30])
+//            phase B: c = 32 tau + j, stages 13-16 (per-thread twiddles)
+//   inverse  phase A: c = 32 tau + j, stages v = 0-3 (per-thread twiddles)
+//            phase B: c = tau + 16 j, stages v = 4-8 (row-shared)
+// Row layout in shared memory: c -> c + 4 (c >> 5) (the 32-word chunks of
+// phase B start on distinct bank quads), rows 592 words apart (the two rows
+// of a warp sit on opposite bank halves for the stride-16 accesses).  Each
+// warp stages its own two rows of the data tile and of the per-row twiddle
+// tables (512 pairs, host-permuted in consumption order): no CTA barrier.
+constexpr int kR5 = 512, kN5 = 256 * kR5, kR5Stride = 592;
+constexpr int kR5Buf = kRRows * kR5Stride;
+constexpr int kR5Smem = 2 * kR5Buf * 4 + kRRows * kR5 * 8;
+__device__ __forceinline__ int rpos5(int c) { return c + 4 * (c >> 5); }
+
+template <bool INV>
+__global__ void __launch_bounds__(kRT) k_row512(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
+                                                uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs,
+                                                int batch, int njobs, const PrimeDev* __restrict__ primes,
+                                                const uint2* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
+  uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * kR5Buf * 4);  // [kRRows][512]
+  const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15, warp = tid >> 5, lane = tid & 31;
+  constexpr int kTiles = 256 / kRRows;
+  const int items = njobs * kTiles * batch;
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
+  if (i0 >= i1) return;
+  RowCursor c;
+  c.init(i0, batch);
+  RowJob Jc = jobs[c.job];
+  RowCursor nx = c;
+  RowJob Jn = Jc;
+  auto in_ptr = [&](const RowCursor& x, const RowJob& J) {
+    return INV ? src + x.b * src_bs + (size_t)J.src_off * kN5 + x.tile * kRRows * kR5
+               : dst + x.b * dst_bs + (size_t)J.dst_off * kN5 + x.tile * kRRows * kR5;
+  };
+  auto prefetch = [&](uint32_t* buf, const uint32_t* g) {  // this warp's two rows, 16 B per cp.async
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int e = lane + 32 * m, r = 2 * warp + (e >> 7), cc = (e & 127) * 4;
+      cp16(buf + r * kR5Stride + rpos5(cc), g + r * kR5 + cc);
+    }
+  };
+  prefetch(sbuf, in_ptr(nx, Jn));
+  cp_commit();
+  uint32_t q = 0, q2 = 0, q4 = 0;
+  for (int it = i0, k = 0; it < i1; ++it, ++k) {
+    uint32_t* line_buf = sbuf + (k & 1) * kR5Buf;
+    const int b = c.b, tile = c.tile;
+    const RowJob J = Jc;
+    const bool reload = it == i0 || b == 0;
+    if (reload) {  // this warp's two rows of the tile's twiddle tables (2 x 4 KB)
+      __syncwarp();
+      const uint2* T = tw2 + ((size_t)J.prime * 256 + tile * kRRows + 2 * warp) * kR5;
+      for (int e = lane; e < kR5; e += 32) cp16(&tws[2 * warp * kR5 + 2 * e], &T[2 * e]);
+      cp_commit();
+    }
+    if (it + 1 < i1) {
+      const int pj = nx.job;
+      nx.next(batch);
+      if (nx.job != pj) Jn = jobs[nx.job];
+      prefetch(sbuf + ((k + 1) & 1) * kR5Buf, in_ptr(nx, Jn));
+    }
+    cp_commit();
+    cp_wait<1>();
+    __syncwarp();
+    if (reload) {
+      const PrimeDev P = primes[J.prime];
+      q = P.q;
+      q2 = P.q2;
+      q4 = 2 * P.q2;
+    }
+    const int r = tile * kRRows + rho;
+    const uint2* W = tws + rho * kR5;
+    uint32_t* line = line_buf + rho * kR5Stride;
+    uint32_t* orow = dst + b * dst_bs + (size_t)J.dst_off * kN5 + (size_t)r * kR5;
+    uint32_t v[32];
+    if (!INV) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = line[rpos5(tau + 16 * j)];
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {  // stages 8 + t: pairs (j, j + (16 >> t)), twiddle W[2^t - 1 + (j >> (5 - t))]
+        const int d = 16 >> t;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = W[(1 << t) - 1 + blk];
+          if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) line[rpos5(tau + 16 * j)] = v[j];
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint4 x = *reinterpret_cast<const uint4*>(line + rpos5(32 * tau) + 4 * m);
+        v[4 * m] = x.x;
+        v[4 * m + 1] = x.y;
+        v[4 * m + 2] = x.z;
+        v[4 * m + 3] = x.w;
+      }
+#pragma unroll
+      for (int t = 5; t < 9; ++t) {  // stages 8 + t: pairs (j, j + (256 >> t)), per-thread twiddles
+        const int d = 256 >> t, off = (1 << (t - 4)) - 2;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = W[32 + (off + blk) * 16 + tau];
+          if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        stg4(orow + 32 * tau + 4 * m, make_uint4(canon8(v[4 * m], q, q2, q4), canon8(v[4 * m + 1], q, q2, q4),
+                                                 canon8(v[4 * m + 2], q, q2, q4), canon8(v[4 * m + 3], q, q2, q4)));
+    } else {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint4 x = *reinterpret_cast<const uint4*>(line + rpos5(32 * tau) + 4 * m);
+        v[4 * m] = x.x;
+        v[4 * m + 1] = x.y;
+        v[4 * m + 2] = x.z;
+        v[4 * m + 3] = x.w;
+      }
+      constexpr int kOffI[4] = {0, 16, 24, 28};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {  // inverse stages t: pairs (j, j + 2^t), per-thread twiddles
+        const int d = 1 << t;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = W[(kOffI[t] + blk) * 16 + tau];
+          gs(v[j], v[j + d], w.x, w.y, q, q2);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        *reinterpret_cast<uint4*>(line + rpos5(32 * tau) + 4 * m) =
+            make_uint4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = line[rpos5(tau + 16 * j)];
+      constexpr int kOffR[5] = {0, 16, 24, 28, 30};
+#pragma unroll
+      for (int t = 4; t < 9; ++t) {  // inverse stages t: pairs (j, j + 2^(t-4)), row-shared twiddles
+        const int d = 1 << (t - 4);
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = W[480 + kOffR[t - 4] + blk];
+          gs(v[j], v[j + d], w.x, w.y, q, q2);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) orow[tau + 16 * j] = v[j];
+    }
+    c = nx;
+    Jc = Jn;
+    __syncwarp();
+  }
+  cp_wait<0>();
+}
+
+template <bool INV>
+void launch_col9(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaStream_t st) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_col<INV, false, true, 5, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColRingSmem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_col<INV, false, true, 5, 9>, kCT, kColRingSmem);
+    grid = sms * std::max(1, per);
+  }
+  const int items = a.njobs * a.batch * (kR5 / kCCols);
+  k_col<INV, false, true, 5, 9><<<min(grid, items), kCT, kColRingSmem, st>>>(
+      a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs, a.primes, a.tw, a.exits, a.entry);
+}
+
+template <bool INV>
+void launch_row512(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, const uint2* tw2, cudaStream_t st) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_row512<INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR5Smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row512<INV>, kRT, kR5Smem);
+    grid = sms * std::max(1, per);
+  }
+  const int items = a.njobs * (256 / kRRows) * a.batch;
+  k_row512<INV><<<min(grid, items), kRT, kR5Smem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
+                                                         a.primes, tw2);
+}
+
+bool ntt131k_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
+  launch_col9<false>(a, a.src, a.src_bs, st);
+  launch_row512<false>(a, a.dst, a.dst_bs, tw2, st);  // in place on dst
+  return true;
+}
+
+bool ntt131k_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st) {
+  launch_row512<true>(a, a.src, a.src_bs, tw2i, st);
+  NttLaunch b = a;
+  b.entry = 0;
+  launch_col9<true>(b, a.dst, a.dst_bs, st);
+  return true;
 }
 
 bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
