@@ -1563,6 +1563,54 @@ extern "C" {
 const char* ck_last_error(void) { return ck::g_err.c_str(); }
 const char* ck_version(void) { return "ck32-b200 0.1.0 (sm_100a)"; }
 
+// Row-pass twiddle tables of k_rowx (ntt256.cu) for rows of R = 2^LOGR,
+// N = 256 R, x = R r + c, in consumption order per row (512 or 256 pairs):
+//   forward stage 8 + s uses F[(256 << s) + (r << s) + (c >> (LOGR - s))]:
+//     phase A (c = tau + TPR j, s < 5): row-shared, [2^s - 1 + (j >> (5 - s))]
+//     phase B (c = 32 tau + j, s >= 5): per thread, [32 + (off(s) + blk) TPR + tau]
+//   inverse stage v uses I[(N >> (v + 1)) + (r << (LOGR - 1 - v)) + (c >> (v + 1))]:
+//     phase A (c = 32 tau + j, v < LOGR - 5): per thread, [(offI(v) + blk) TPR + tau]
+//     phase B (c = tau + TPR j): row-shared, [RS_BASE + offR + blk]
+// (same values as the reference tables, ntt.cpp:124-128).
+static void build_rowx_tables(const std::vector<uint2>& fwd, const std::vector<uint2>& inv, uint32_t n, int logr,
+                              uint32_t np, uint2** d_f, uint2** d_i) {
+  const uint32_t R = 1u << logr, TPR = R / 32, PB = logr - 5;
+  const uint32_t rs_base = TPR * (32 - (1u << (5 - PB)));
+  std::vector<uint2> tf((size_t)np * n), ti((size_t)np * n);
+#pragma omp parallel for schedule(static)
+  for (int g = 0; g < (int)np; ++g) {
+    const uint2* F = fwd.data() + (size_t)g * n;
+    const uint2* I = inv.data() + (size_t)g * n;
+    for (uint32_t r = 0; r < 256; ++r) {
+      uint2* A = tf.data() + ((size_t)g * 256 + r) * R;
+      uint2* B = ti.data() + ((size_t)g * 256 + r) * R;
+      A[31] = B[R - 1] = make_uint2(0, 0);
+      for (uint32_t s = 0; s < 5; ++s)
+        for (uint32_t blk = 0; blk < (1u << s); ++blk) A[(1u << s) - 1 + blk] = F[(256u << s) + (r << s) + blk];
+      for (uint32_t s = 5; s < (uint32_t)logr; ++s) {
+        const uint32_t off = (1u << (s - PB)) - (1u << (5 - PB));
+        for (uint32_t blk = 0; blk < (1u << (s - PB)); ++blk)
+          for (uint32_t tau = 0; tau < TPR; ++tau)
+            A[32 + (off + blk) * TPR + tau] = F[(256u << s) + (r << s) + (tau << (s - PB)) + blk];
+      }
+      const uint32_t offi[4] = {0, 16, 24, 28}, offr[5] = {0, 16, 24, 28, 30};
+      for (uint32_t v = 0; v < PB; ++v)
+        for (uint32_t blk = 0; blk < (16u >> v); ++blk)
+          for (uint32_t tau = 0; tau < TPR; ++tau)
+            B[(offi[v] + blk) * TPR + tau] = I[(n >> (v + 1)) + (r << (logr - 1 - v)) + (tau << (4 - v)) + blk];
+      for (uint32_t t = 0; t < 5; ++t) {
+        const uint32_t v = PB + t;
+        for (uint32_t blk = 0; blk < (16u >> t); ++blk)
+          B[rs_base + offr[t] + blk] = I[(n >> (v + 1)) + (r << (logr - 1 - v)) + blk];
+      }
+    }
+  }
+  CK_CUDA(cudaMalloc(d_f, tf.size() * sizeof(uint2)));
+  CK_CUDA(cudaMemcpy(*d_f, tf.data(), tf.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+  CK_CUDA(cudaMalloc(d_i, ti.size() * sizeof(uint2)));
+  CK_CUDA(cudaMemcpy(*d_i, ti.data(), ti.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+}
+
 ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int device, ck_context** out) {
   return guard([&] {
     if (!params || !out) throw InvalidArgument("null argument");
@@ -1675,40 +1723,9 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
       CK_CUDA(cudaMalloc(&c->d_tw2i, t2i.size() * sizeof(uint2)));
       CK_CUDA(cudaMemcpy(c->d_tw2i, t2i.data(), t2i.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     } else if (n == 131072) {
-      // Row-pass twiddles of the 512-point rows (ntt256.cu k_row512), per row r
-      // of 512 in consumption order; x = 512 r + c, forward stage 8 + s uses
-      // F[2^(8+s) + (r << s) + (c >> (9 - s))], inverse stage v uses
-      // I[N / 2^(v+1) + (r << (8 - v)) + (c >> (v + 1))] (ntt.cpp:124-128).
-      std::vector<uint2> t2f((size_t)np * n), t2i((size_t)np * n);
-#pragma omp parallel for schedule(static)
-      for (int g = 0; g < (int)np; ++g) {
-        const uint2* F = fwd.data() + (size_t)g * n;
-        const uint2* I = inv.data() + (size_t)g * n;
-        for (uint32_t r = 0; r < 256; ++r) {
-          uint2* A = t2f.data() + ((size_t)g * 256 + r) * 512;
-          uint2* B = t2i.data() + ((size_t)g * 256 + r) * 512;
-          A[31] = B[511] = make_uint2(0, 0);
-          for (uint32_t s = 0; s < 5; ++s)  // forward phase A (c = tau + 16 j): row-shared, blk = j >> (5 - s)
-            for (uint32_t blk = 0; blk < (1u << s); ++blk) A[(1u << s) - 1 + blk] = F[(256u << s) + (r << s) + blk];
-          for (uint32_t s = 5; s < 9; ++s)  // forward phase B (c = 32 tau + j): per thread, blk = j >> (9 - s)
-            for (uint32_t blk = 0; blk < (1u << (s - 4)); ++blk)
-              for (uint32_t tau = 0; tau < 16; ++tau)
-                A[32 + (((1u << (s - 4)) - 2) + blk) * 16 + tau] = F[(256u << s) + (r << s) + (tau << (s - 4)) + blk];
-          const uint32_t offi[4] = {0, 16, 24, 28}, offr[5] = {0, 16, 24, 28, 30};
-          for (uint32_t v = 0; v < 4; ++v)  // inverse phase A (c = 32 tau + j): per thread, blk = j >> (v + 1)
-            for (uint32_t blk = 0; blk < (16u >> v); ++blk)
-              for (uint32_t tau = 0; tau < 16; ++tau)
-                B[(offi[v] + blk) * 16 + tau] = I[(65536u >> v) + (r << (8 - v)) + (tau << (4 - v)) + blk];
-          for (uint32_t v = 4; v < 9; ++v)  // inverse phase B (c = tau + 16 j): row-shared, blk = j >> (v - 3)
-            for (uint32_t blk = 0; blk < (256u >> v); ++blk)
-              B[480 + offr[v - 4] + blk] = I[(65536u >> v) + (r << (8 - v)) + blk];
-        }
-      }
-      CK_CUDA(cudaMalloc(&c->d_tw2f, t2f.size() * sizeof(uint2)));
-      CK_CUDA(cudaMemcpy(c->d_tw2f, t2f.data(), t2f.size() * sizeof(uint2), cudaMemcpyHostToDevice));
-      CK_CUDA(cudaMalloc(&c->d_tw2i, t2i.size() * sizeof(uint2)));
-      CK_CUDA(cudaMemcpy(c->d_tw2i, t2i.data(), t2i.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+      build_rowx_tables(fwd, inv, n, 9, np, &c->d_tw2f, &c->d_tw2i);
     }
+
     std::vector<uint32_t> pm(p.l);  // p_mont (ckks.cpp:171-175)
     for (uint32_t i = 0; i < p.l; ++i) {
       const uint32_t q = c->primes[i];

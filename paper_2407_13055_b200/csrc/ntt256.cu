@@ -350,6 +350,27 @@ __device__ __forceinline__ void row_prefetch_warp(uint32_t* buf, const uint32_t*
   }
 }
 
+// (job, row tile, b) item cursor, b fastest; TILES row tiles per limb
+template <int TILES>
+struct RowCursorT {
+  int b, tile, job;
+  __device__ __forceinline__ void init(int it, int batch) {
+    b = it % batch;
+    const int key = it / batch;
+    tile = key % TILES;
+    job = key / TILES;
+  }
+  __device__ __forceinline__ void next(int batch) {
+    if (++b == batch) {
+      b = 0;
+      if (++tile == TILES) {
+        tile = 0;
+        ++job;
+      }
+    }
+  }
+};
+
 // (job, row tile, b) item cursor, b fastest
 struct RowCursor {
   int b, tile, job;
@@ -1085,60 +1106,70 @@ void ntt256_pass(int which, const NttLaunch& a, const uint2* tw2, cudaStream_t s
 // of a warp sit on opposite bank halves for the stride-16 accesses).  Each
 // warp stages its own two rows of the data tile and of the per-row twiddle
 // tables (512 pairs, host-permuted in consumption order): no CTA barrier.
-constexpr int kR5 = 512, kN5 = 256 * kR5, kR5Stride = 592;
-constexpr int kR5Buf = kRRows * kR5Stride;
-constexpr int kR5Smem = 2 * kR5Buf * 4 + kRRows * kR5 * 8;
+constexpr int kR5 = 512;
 __device__ __forceinline__ int rpos5(int c) { return c + 4 * (c >> 5); }
+// Row-pass geometry for rows of R = 2^LOGR (LOGR = 8 or 9), 32 elements per
+// thread: TPR threads per row, RPC rows per 128-thread CTA, padded stride.
+template <int LOGR>
+struct RowX {
+  static constexpr int R = 1 << LOGR, N = 256 * R, TPR = R / 32, RPC = 128 / TPR, RPW = 32 / TPR;
+  static constexpr int STRIDE = R + R / 8 + (TPR == 16 ? 16 : 8);  // rows of a warp on distinct bank groups
+  static constexpr int BUF = RPC * STRIDE;
+  static constexpr int SMEM = 2 * BUF * 4 + RPC * R * 8;
+  static constexpr int PB = LOGR - 5;                  // phase-B forward stages / phase-A inverse stages + 1
+  static constexpr int RS_BASE = TPR * (32 - (1 << (5 - PB)));  // inverse: per-thread entries before the row-shared ones
+};
 
-template <bool INV>
-__global__ void __launch_bounds__(kRT) k_row512(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
-                                                uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs,
-                                                int batch, int njobs, const PrimeDev* __restrict__ primes,
-                                                const uint2* __restrict__ tw2) {
+template <bool INV, int LOGR>
+__global__ void __launch_bounds__(kRT) k_rowx(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
+                                              uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
+                                              int njobs, const PrimeDev* __restrict__ primes,
+                                              const uint2* __restrict__ tw2) {
+  using G = RowX<LOGR>;
   extern __shared__ __align__(16) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
-  uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * kR5Buf * 4);  // [kRRows][512]
-  const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15, warp = tid >> 5, lane = tid & 31;
-  constexpr int kTiles = 256 / kRRows;
+  uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * G::BUF * 4);  // [RPC][R]
+  const int tid = threadIdx.x, rho = tid / G::TPR, tau = tid % G::TPR, warp = tid >> 5, lane = tid & 31;
+  constexpr int kTiles = 256 / G::RPC;
   const int items = njobs * kTiles * batch;
   const int chunk = (items + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
   if (i0 >= i1) return;
-  RowCursor c;
+  RowCursorT<kTiles> c;
   c.init(i0, batch);
   RowJob Jc = jobs[c.job];
-  RowCursor nx = c;
+  RowCursorT<kTiles> nx = c;
   RowJob Jn = Jc;
-  auto in_ptr = [&](const RowCursor& x, const RowJob& J) {
-    return INV ? src + x.b * src_bs + (size_t)J.src_off * kN5 + x.tile * kRRows * kR5
-               : dst + x.b * dst_bs + (size_t)J.dst_off * kN5 + x.tile * kRRows * kR5;
+  auto in_ptr = [&](const RowCursorT<kTiles>& x, const RowJob& J) {
+    return INV ? src + x.b * src_bs + (size_t)J.src_off * G::N + x.tile * G::RPC * G::R
+               : dst + x.b * dst_bs + (size_t)J.dst_off * G::N + x.tile * G::RPC * G::R;
   };
-  auto prefetch = [&](uint32_t* buf, const uint32_t* g) {  // this warp's two rows, 16 B per cp.async
+  auto prefetch = [&](uint32_t* buf, const uint32_t* g) {  // this warp's RPW rows, 16 B per cp.async
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-      const int e = lane + 32 * m, r = 2 * warp + (e >> 7), cc = (e & 127) * 4;
-      cp16(buf + r * kR5Stride + rpos5(cc), g + r * kR5 + cc);
+      const int e = lane + 32 * m, r = G::RPW * warp + e / (G::R / 4), cc = (e % (G::R / 4)) * 4;
+      cp16(buf + r * G::STRIDE + rpos5(cc), g + r * G::R + cc);
     }
   };
   prefetch(sbuf, in_ptr(nx, Jn));
   cp_commit();
   uint32_t q = 0, q2 = 0, q4 = 0;
   for (int it = i0, k = 0; it < i1; ++it, ++k) {
-    uint32_t* line_buf = sbuf + (k & 1) * kR5Buf;
+    uint32_t* line_buf = sbuf + (k & 1) * G::BUF;
     const int b = c.b, tile = c.tile;
     const RowJob J = Jc;
     const bool reload = it == i0 || b == 0;
-    if (reload) {  // this warp's two rows of the tile's twiddle tables (2 x 4 KB)
+    if (reload) {  // this warp's rows of the tile's twiddle tables (1024 pairs)
       __syncwarp();
-      const uint2* T = tw2 + ((size_t)J.prime * 256 + tile * kRRows + 2 * warp) * kR5;
-      for (int e = lane; e < kR5; e += 32) cp16(&tws[2 * warp * kR5 + 2 * e], &T[2 * e]);
+      const uint2* T = tw2 + ((size_t)J.prime * 256 + tile * G::RPC + G::RPW * warp) * G::R;
+      for (int e = lane; e < 512; e += 32) cp16(&tws[G::RPW * warp * G::R + 2 * e], &T[2 * e]);
       cp_commit();
     }
     if (it + 1 < i1) {
       const int pj = nx.job;
       nx.next(batch);
       if (nx.job != pj) Jn = jobs[nx.job];
-      prefetch(sbuf + ((k + 1) & 1) * kR5Buf, in_ptr(nx, Jn));
+      prefetch(sbuf + ((k + 1) & 1) * G::BUF, in_ptr(nx, Jn));
     }
     cp_commit();
     cp_wait<1>();
@@ -1149,16 +1180,16 @@ __global__ void __launch_bounds__(kRT) k_row512(const RowJob* __restrict__ jobs,
       q2 = P.q2;
       q4 = 2 * P.q2;
     }
-    const int r = tile * kRRows + rho;
-    const uint2* W = tws + rho * kR5;
-    uint32_t* line = line_buf + rho * kR5Stride;
-    uint32_t* orow = dst + b * dst_bs + (size_t)J.dst_off * kN5 + (size_t)r * kR5;
+    const int r = tile * G::RPC + rho;
+    const uint2* W = tws + rho * G::R;
+    uint32_t* line = line_buf + rho * G::STRIDE;
+    uint32_t* orow = dst + b * dst_bs + (size_t)J.dst_off * G::N + (size_t)r * G::R;
     uint32_t v[32];
     if (!INV) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = line[rpos5(tau + 16 * j)];
+      for (int j = 0; j < 32; ++j) v[j] = line[rpos5(tau + G::TPR * j)];
 #pragma unroll
-      for (int t = 0; t < 5; ++t) {  // stages 8 + t: pairs (j, j + (16 >> t)), twiddle W[2^t - 1 + (j >> (5 - t))]
+      for (int t = 0; t < 5; ++t) {  // row stage t: pairs (j, j + (16 >> t)), twiddle W[2^t - 1 + (j >> (5 - t))]
         const int d = 16 >> t;
 #pragma unroll
         for (int p = 0; p < 16; ++p) {
@@ -1169,7 +1200,7 @@ __global__ void __launch_bounds__(kRT) k_row512(const RowJob* __restrict__ jobs,
         }
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) line[rpos5(tau + 16 * j)] = v[j];
+      for (int j = 0; j < 32; ++j) line[rpos5(tau + G::TPR * j)] = v[j];
       __syncwarp();
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
@@ -1180,12 +1211,12 @@ __global__ void __launch_bounds__(kRT) k_row512(const RowJob* __restrict__ jobs,
         v[4 * m + 3] = x.w;
       }
 #pragma unroll
-      for (int t = 5; t < 9; ++t) {  // stages 8 + t: pairs (j, j + (256 >> t)), per-thread twiddles
-        const int d = 256 >> t, off = (1 << (t - 4)) - 2;
+      for (int t = 5; t < LOGR; ++t) {  // row stage t: pairs (j, j + (R/2 >> t)), per-thread twiddles
+        const int d = (G::R / 2) >> t, cnt0 = 1 << (5 - G::PB), off = (1 << (t - G::PB)) - cnt0;
 #pragma unroll
         for (int p = 0; p < 16; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = W[32 + (off + blk) * 16 + tau];
+          const uint2 w = W[32 + (off + blk) * G::TPR + tau];
           if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
           else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
         }
@@ -1205,12 +1236,12 @@ __global__ void __launch_bounds__(kRT) k_row512(const RowJob* __restrict__ jobs,
       }
       constexpr int kOffI[4] = {0, 16, 24, 28};
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {  // inverse stages t: pairs (j, j + 2^t), per-thread twiddles
+      for (int t = 0; t < G::PB; ++t) {  // inverse stages t: pairs (j, j + 2^t), per-thread twiddles
         const int d = 1 << t;
 #pragma unroll
         for (int p = 0; p < 16; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = W[(kOffI[t] + blk) * 16 + tau];
+          const uint2 w = W[(kOffI[t] + blk) * G::TPR + tau];
           gs(v[j], v[j + d], w.x, w.y, q, q2);
         }
       }
@@ -1220,20 +1251,20 @@ __global__ void __launch_bounds__(kRT) k_row512(const RowJob* __restrict__ jobs,
             make_uint4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
       __syncwarp();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = line[rpos5(tau + 16 * j)];
+      for (int j = 0; j < 32; ++j) v[j] = line[rpos5(tau + G::TPR * j)];
       constexpr int kOffR[5] = {0, 16, 24, 28, 30};
 #pragma unroll
-      for (int t = 4; t < 9; ++t) {  // inverse stages t: pairs (j, j + 2^(t-4)), row-shared twiddles
-        const int d = 1 << (t - 4);
+      for (int t = 0; t < 5; ++t) {  // inverse stages PB + t: pairs (j, j + 2^t), row-shared twiddles
+        const int d = 1 << t;
 #pragma unroll
         for (int p = 0; p < 16; ++p) {
           const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = W[480 + kOffR[t - 4] + blk];
+          const uint2 w = W[G::RS_BASE + kOffR[t] + blk];
           gs(v[j], v[j + d], w.x, w.y, q, q2);
         }
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) orow[tau + 16 * j] = v[j];
+      for (int j = 0; j < 32; ++j) orow[tau + G::TPR * j] = v[j];
     }
     c = nx;
     Jc = Jn;
@@ -1258,30 +1289,31 @@ void launch_col9(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaS
       a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs, a.primes, a.tw, a.exits, a.entry);
 }
 
-template <bool INV>
-void launch_row512(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, const uint2* tw2, cudaStream_t st) {
+template <bool INV, int LOGR>
+void launch_rowx(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, const uint2* tw2, cudaStream_t st) {
+  using G = RowX<LOGR>;
   static int grid = 0;
   if (!grid) {
-    cudaFuncSetAttribute(k_row512<INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR5Smem);
+    cudaFuncSetAttribute(k_rowx<INV, LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row512<INV>, kRT, kR5Smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rowx<INV, LOGR>, kRT, G::SMEM);
     grid = sms * std::max(1, per);
   }
-  const int items = a.njobs * (256 / kRRows) * a.batch;
-  k_row512<INV><<<min(grid, items), kRT, kR5Smem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
-                                                         a.primes, tw2);
+  const int items = a.njobs * (256 / G::RPC) * a.batch;
+  k_rowx<INV, LOGR><<<min(grid, items), kRT, G::SMEM, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
+                                                             a.primes, tw2);
 }
 
 bool ntt131k_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
   launch_col9<false>(a, a.src, a.src_bs, st);
-  launch_row512<false>(a, a.dst, a.dst_bs, tw2, st);  // in place on dst
+  launch_rowx<false, 9>(a, a.dst, a.dst_bs, tw2, st);  // in place on dst
   return true;
 }
 
 bool ntt131k_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st) {
-  launch_row512<true>(a, a.src, a.src_bs, tw2i, st);
+  launch_rowx<true, 9>(a, a.src, a.src_bs, tw2i, st);
   NttLaunch b = a;
   b.entry = 0;
   launch_col9<true>(b, a.dst, a.dst_bs, st);
