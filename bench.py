@@ -130,6 +130,27 @@ class ClockSampler:
                 "reasons": sorted(v for k, v in self.REASONS.items() if self.bits & k), "samples": len(self.sm)}
 
 
+def dist_setup():
+    """(world, rank, local device index) for this process; initialises the
+    process group (NCCL; CK32_DIST_BACKEND=gloo exercises the N > 1 code path
+    with several ranks sharing the GPUs of a smaller box, LOCAL_RANK modulo
+    the device count)."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    if world > 1:
+        backend = os.environ.get("CK32_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return world, rank, local
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -205,12 +226,7 @@ def main():
     from paper_2407_13055_b200 import ckks, dp
     from paper_2407_13055_b200.pipeline import HostPipeline
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
 
     def barrier():
@@ -516,13 +532,8 @@ def run_limb(args):
                                             LocalPeerExchange, ShardBackend, TorchExchange, exchange_bytes)
 
     n = 1 << 17
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
     C = ckks.CkksContext(ckks.CkksParams(n=n, l=L, alpha=ALPHA, delta_bits=DB), device=local)
     q = torch.tensor(C.primes.astype(np.int64), device=dev)
     gen = torch.Generator(device=dev)
@@ -634,12 +645,7 @@ def run_helr(args):
     from paper_2407_13055_b200 import ckks, dp
     from paper_2407_13055_b200.helr import HelrIteration, HelrShape
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
     shape = HelrShape(n=N_RING, features=256, cts=8)
     C = ckks.CkksContext(ckks.CkksParams(n=N_RING, l=L, alpha=ALPHA, delta_bits=DB), device=local)
