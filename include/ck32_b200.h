@@ -158,7 +158,7 @@ ck_status ck_hoisted_rotate_accumulate(ck_context* ctx, uint32_t level, const ui
  * device memory) -> plaintext rows [level (+alpha if p_extend)][n] in the
  * evaluation domain, Montgomery form (canonical residues).  scale_log2 is
  * log2_rational(scale) (ckks.cpp:140-158); residues are bit-identical to the
- * reference when the scale is a power of two. */
+ * reference at every scale (its powl / x87 long double rounding is replayed). */
 ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, double scale_log2, uint32_t level,
                     int p_extend, uint32_t* out_dev, ck_stream stream);
 /* decode (ckks.cpp:321-362): plaintext rows [level][n] (evaluation,

@@ -216,13 +216,60 @@ struct Plaintext {  // ckks.hpp:56-59; data = [level (+alpha)][n], evaluation do
   uint32_t p_count = 0;
 };
 
-// log2 of the ledger value; exact for power-of-two scales (the encode path is
-// bit-identical to the reference there, ckks.cpp:297-299)
+// log2_rational (ckks.cpp:140-158) of the ledger value, operation for
+// operation: numerator and denominator as exact big integers (the prime
+// products times the power of two), each cut to its top 53 bits, then
+// shift + log2(num / den).  encode feeds this to the same powl / x87
+// rounding as the reference, so plaintexts are bit-identical at any scale.
+namespace detail {
+struct BigU {  // little-endian 32-bit limbs
+  std::vector<uint32_t> w{1};
+  void mul(uint32_t m) {
+    uint64_t carry = 0;
+    for (auto& x : w) {
+      const uint64_t t = (uint64_t)x * m + carry;
+      x = (uint32_t)t;
+      carry = t >> 32;
+    }
+    if (carry) w.push_back((uint32_t)carry);
+  }
+  void shl(int b) {
+    for (; b >= 31; b -= 31) mul(1u << 31);
+    if (b > 0) mul(1u << b);
+  }
+  int msb() const { return 32 * ((int)w.size() - 1) + 31 - __builtin_clz(w.back()); }
+  uint64_t bits(int lo) const {  // floor(value / 2^lo), < 2^53 when lo = msb - 52
+    uint64_t v = 0;
+    for (int i = 52; i >= 0; --i) {
+      const int b = lo + i;
+      if (b >= 0 && b / 32 < (int)w.size() && (w[b / 32] >> (b % 32) & 1u)) v |= 1ull << i;
+    }
+    return v;
+  }
+};
+}  // namespace detail
 inline double scale_log2(const Scale& s) {
-  double v = s.pow2;
-  for (uint32_t a : s.num) v += std::log2((double)a);
-  for (uint32_t b : s.den) v -= std::log2((double)b);
-  return v;
+  detail::BigU num, den;
+  for (uint32_t a : s.num) num.mul(a);
+  for (uint32_t b : s.den) den.mul(b);
+  if (s.pow2 >= 0) num.shl(s.pow2);
+  else den.shl(-s.pow2);
+  const int bn = num.msb(), bd = den.msb();
+  int64_t shift = 0;
+  double n = 0, d = 0;
+  if (bn > 52) {
+    n = (double)num.bits(bn - 52);
+    shift += bn - 52;
+  } else {
+    n = (double)num.bits(0);
+  }
+  if (bd > 52) {
+    d = (double)den.bits(bd - 52);
+    shift -= bd - 52;
+  } else {
+    d = (double)den.bits(0);
+  }
+  return static_cast<double>(shift) + std::log2(n / d);
 }
 
 // encode (ckks.cpp:278-319): host slots -> device plaintext

@@ -2331,7 +2331,13 @@ ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, do
     CK_CUDA(cudaMemcpyAsync(rq, hq.data(), 4 * rows, cudaMemcpyHostToDevice, st));
     enc_scatter((int)N, reinterpret_cast<const double2*>(slots_dev), (int)count, c->d_jidx, a, st);
     fft_pow2_dev((int)c->logn, a, a + N, c->d_fft_inv, st);  // IDFT (1/n folded into enc_round)
-    enc_round((int)N, a + N, c->d_twist_enc, std::exp2(scale_log2), (int)rows, rq, out_dev, st);
+    // the reference's scale: powl(2.0L, (long double)log2_rational(scale)) (ckks.cpp:297-299),
+    // same glibc / x87 on the host; its 64-bit significand and exponent go to the kernel
+    const long double scale_v = std::pow(2.0L, static_cast<long double>(scale_log2));
+    int sexp = 0;
+    const long double sfrac = std::frexp(scale_v, &sexp);  // [0.5, 1)
+    const unsigned long long smant = static_cast<unsigned long long>(std::ldexp(sfrac, 64));
+    enc_round((int)N, a + N, c->d_twist_enc, smant, sexp - 64, (int)rows, rq, out_dev, st);
     CK_CUDA(cudaStreamSynchronize(st));  // hq is pageable host memory
     c->launches += 4 + (c->logn > 12 ? c->logn - 12 : 0);
   });

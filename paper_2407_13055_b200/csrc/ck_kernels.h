@@ -122,8 +122,9 @@ struct CrtConst {  // CRT lift over the first c <= 4 primes (128-bit)
 // offset len/2 - 1), built by the host with the reference's recurrence
 void fft_pow2_dev(int logn, const double2* src, double2* dst, const double2* tw, cudaStream_t st);
 void enc_scatter(int n, const double2* slots, int count, const uint32_t* jidx, double2* a, cudaStream_t st);
-void enc_round(int n, const double2* a, const double2* twist, double scale, int rows, const uint32_t* row_q,
-               uint32_t* out, cudaStream_t st);
+// scale = scale_mant * 2^scale_exp: the reference's long double scale (64-bit significand)
+void enc_round(int n, const double2* a, const double2* twist, unsigned long long scale_mant, int scale_exp, int rows,
+               const uint32_t* row_q, uint32_t* out, cudaStream_t st);
 void dec_crt(int n, const uint32_t* rows, const CrtConst& cc, const double2* twist, double inv_scale, double2* a,
              cudaStream_t st);
 void dec_gather(int n, const double2* a, const uint32_t* jidx, double2* out, cudaStream_t st);

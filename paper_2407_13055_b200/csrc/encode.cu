@@ -14,8 +14,10 @@
 // (the host builds them with the reference's recurrence w *= wl in double),
 // and complex products / sums rounded exactly as libstdc++ evaluates them
 // (x86-64, no FMA): every product and sum below uses the _rn intrinsics so the
-// compiler cannot contract them into FMAs.  With a power-of-two scale the
-// encoded residues are therefore bit-identical to the reference's.
+// compiler cannot contract them into FMAs; the final scaling and rounding
+// replays the reference's 80-bit long double arithmetic on integers
+// (llroundl_x87), so the encoded residues are bit-identical to the
+// reference's for every scale.
 #include <algorithm>
 
 #include "ck_common.cuh"
@@ -80,14 +82,48 @@ __global__ void k_enc_scatter(int n, const double2* __restrict__ slots, int coun
   a[n - 1 - j] = make_double2(z.x, -z.y);
 }
 
-// m_k = llround((Re(a_k tw_k) / n) * scale), then canonical m mod q for every row
+// llroundl(c * S) exactly as the reference evaluates it on x86-64: c a double,
+// S = ms * 2^es the 64-bit-significand long double scale (powl(2.0L, log2),
+// ckks.cpp:297-305), the product rounded once to a 64-bit significand
+// (x87 extended, round to nearest even), then to an integer (half away from
+// zero).  Done on integers: c = mc * 2^ec (53-bit mc), P = mc * ms (<= 117
+// bits, exact), round P to 64 significant bits, shift by ec + es.
+__device__ __forceinline__ long long llroundl_x87(double c, unsigned long long ms, int es) {
+  if (c == 0.0) return 0;
+  int e;
+  const double f = frexp(fabs(c), &e);                                  // |c| = f 2^e, f in [0.5, 1)
+  const unsigned long long mc = (unsigned long long)ldexp(f, 53);        // exact 53-bit integer
+  unsigned __int128 P = (unsigned __int128)mc * ms;
+  int E = e - 53 + es;
+  const int L = 128 - (int)((P >> 64) ? __clzll((unsigned long long)(P >> 64)) : 64 + __clzll((unsigned long long)P));
+  if (L > 64) {  // round to 64 significant bits, nearest even
+    const int d = L - 64;
+    const unsigned __int128 half = (unsigned __int128)1 << (d - 1), mask = ((unsigned __int128)1 << d) - 1;
+    const unsigned __int128 rem = P & mask;
+    P >>= d;
+    if (rem > half || (rem == half && (P & 1))) P += 1;
+    E += d;
+  }
+  unsigned long long mag;
+  if (E >= 0) {
+    mag = (unsigned long long)(P << E);  // |c S| < 2^63 for the reference's scale bound
+  } else {
+    const int sft = -E;
+    if (sft >= 127) mag = 0;
+    else mag = (unsigned long long)((P + ((unsigned __int128)1 << (sft - 1))) >> sft);  // half away from zero
+  }
+  return c < 0 ? -(long long)mag : (long long)mag;
+}
+
+// m_k = llroundl((Re(a_k tw_k) / n) * S), then canonical m mod q for every row
 __global__ void k_enc_round(int n, const double2* __restrict__ a, const double2* __restrict__ twist, double inv_n,
-                            double scale, int rows, const uint32_t* __restrict__ row_q, uint32_t* __restrict__ out) {
+                            unsigned long long ms, int es, int rows, const uint32_t* __restrict__ row_q,
+                            uint32_t* __restrict__ out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const double2 x = a[k], t = twist[k];
   const double re = __dsub_rn(__dmul_rn(x.x, t.x), __dmul_rn(x.y, t.y));
-  const long long m = llround(__dmul_rn(__dmul_rn(re, inv_n), scale));
+  const long long m = llroundl_x87(__dmul_rn(re, inv_n), ms, es);
   for (int i = 0; i < rows; ++i) {
     const long long q = row_q[i];
     long long r = m % q;  // correct() of modarith.hpp:46-50
@@ -155,9 +191,9 @@ void enc_scatter(int n, const double2* slots, int count, const uint32_t* jidx, d
   if (count) k_enc_scatter<<<cdiv(count, 256), 256, 0, st>>>(n, slots, count, jidx, a);
 }
 
-void enc_round(int n, const double2* a, const double2* twist, double scale, int rows, const uint32_t* row_q,
-               uint32_t* out, cudaStream_t st) {
-  k_enc_round<<<cdiv(n, 256), 256, 0, st>>>(n, a, twist, 1.0 / n, scale, rows, row_q, out);
+void enc_round(int n, const double2* a, const double2* twist, unsigned long long scale_mant, int scale_exp, int rows,
+               const uint32_t* row_q, uint32_t* out, cudaStream_t st) {
+  k_enc_round<<<cdiv(n, 256), 256, 0, st>>>(n, a, twist, 1.0 / n, scale_mant, scale_exp, rows, row_q, out);
 }
 
 void dec_crt(int n, const uint32_t* rows, const CrtConst& cc, const double2* twist, double inv_scale, double2* a,

@@ -71,3 +71,34 @@ def test_invalid_arguments_map_to_value_error():
 
 def test_version_string():
     assert b"sm_100a" in nat.lib().ck_version()
+
+
+def test_cpp_mirror_scale_log2_matches_log2_rational(tmp_path):
+    """The C++ mirror computes log2_rational (ckks.cpp:140-158) on its
+    prime-product scale ledger bit for bit like the Python mirror (which is
+    the reference's algorithm), so its encode gets the same powl scale."""
+    import shutil
+    import subprocess
+    from fractions import Fraction
+    from pathlib import Path
+
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    root = Path(__file__).resolve().parent.parent
+    exe = tmp_path / "t"
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", str(root / "include"),
+                    str(root / "tests" / "cpp" / "test_scale_log2.cpp"), "-o", str(exe)], check=True)
+    from paper_2407_13055_b200.ckks import log2_rational
+    primes = [268369921, 268361729, 268238849, 268271617, 399769601, 402849793]
+    cases = [(55, [], []), (110, [], primes[:2]), (55, primes[2:3], primes[:1]), (-3, primes[:3], []),
+             (0, primes, primes[:1]), (110, [7], [3, 5]), (20, [], [3])]
+    inp = "\n".join(f"{p2} {','.join(map(str, a)) or '-'} {','.join(map(str, b)) or '-'}" for p2, a, b in cases)
+    out = subprocess.run([str(exe)], input=inp, capture_output=True, text=True, check=True).stdout.split()
+    for (p2, a, b), got in zip(cases, out):
+        num, den = 1, 1
+        for x in a:
+            num *= x
+        for x in b:
+            den *= x
+        r = Fraction(num * (2 ** p2 if p2 >= 0 else 1), den * (2 ** -p2 if p2 < 0 else 1))
+        assert float.fromhex(got) == log2_rational(r), (p2, a, b)

@@ -1,8 +1,9 @@
 """GPU encode / decode (ckks.cpp:278-362) against the
 reference itself (oracle/_ref, built read-only from /root/reference).
 
-* encode at a power-of-two scale: plaintext residues bit-identical to the
-  reference (the FFT replays the reference's operation order and twiddles);
+* encode at any scale: plaintext residues bit-identical to the reference
+  (the FFT replays the reference's operation order and twiddles, the final
+  scaling replays its 80-bit long double rounding);
 * decode: slots within 2^-40 of the reference's decode of the same plaintext
   (floating-point output; the only freedom is the Rational->double rounding);
 * round trip and the reference's argument errors."""
@@ -52,6 +53,20 @@ def test_encode_bit_exact_vs_reference(ref, n, l, a, level, count, p_extend):
         got = pt.poly.data.cpu().numpy().astype(np.uint32)
         np.testing.assert_array_equal(got, want)
         assert pt.poly.q_count == level and pt.poly.p_count == (a if p_extend else 0)
+
+
+@pytest.mark.parametrize("num,den", [(3 << 53, 5), (7 << 50, 9), ((1 << 60) - 1, 3), (1 << 20, 3), (123456789, 1),
+                                     (18446744073709551557, 17)])
+@pytest.mark.parametrize("n,l,a,level", [(1024, 8, 3, 8), (65536, 24, 8, 24)])
+def test_encode_non_power_of_two_scale_bit_exact(ref, n, l, a, level, num, den):
+    """Any scale: the reference rounds c * powl(2, log2(scale)) in x87 long
+    double and llroundl()s it; the GPU replays that on integers
+    (encode.cu llroundl_x87) -> residues bit-identical to the reference."""
+    C = ctx_for(n, l, a)
+    z = unit_slots(n // 2, 4242 + num % 97)
+    want = ref.encode(n, l, a, 55, z, num, den, level, False)
+    got = ckks.encode(C, z, Fraction(num, den), level).poly.data.cpu().numpy().astype(np.uint32)
+    np.testing.assert_array_equal(got, want)
 
 
 @pytest.mark.parametrize("n,l,a,level", [(1024, 8, 3, 8), (65536, 24, 8, 24), (65536, 24, 8, 3)])

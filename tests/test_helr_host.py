@@ -9,3 +9,4 @@ def test_helr_shape_rotations():
     assert sh.sample_rotations() == [256 << k for k in range(7)]
     small = HelrShape(n=1024, features=16, cts=4)
     assert small.rotations() == [1, 2, 4, 8, -1, -2, -4, -8, 16, 32, 64, 128, 256]
+
