@@ -124,7 +124,7 @@ int main(int argc, char** argv) {
     const auto back = decode(ctx, pt);
     double err = 0;
     for (size_t t = 0; t < z.size(); ++t) err = std::max(err, std::abs(back[t] - z[t]));
-    if (!(err < 1e-9)) throw std::runtime_error("encode/decode round trip error");
+    if (!(err < 1e-9)) throw std::runtime_error("encode/decode round trip error " + std::to_string(err));
     try {  // too many slots (ckks.cpp:281)
       z.resize(p.n / 2 + 1);
       encode(ctx, z, ctx.default_scale(), level);
