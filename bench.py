@@ -181,7 +181,7 @@ def cpu_baseline_leg():
                           "median of 5 reps each (1 ciphertext at a time, OpenMP inside the op)",
                 "hmult_ms": round(hm["median_ns"] / 1e6, 2), "hrot_ms": round(hr["median_ns"] / 1e6, 2),
                 "build": "reference sources -O3 as shipped (asserts live), Boost shim"}
-    except Exception as e:  # reference not built: fall back to the C restatement
+    except Exception as e:  # reference build (oracle/_ref) missing: report it as unavailable
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": f"{type(e).__name__}: {e}"}
 
 
