@@ -96,3 +96,29 @@ def test_reference_rng_public_key_encrypt_decrypts():
     back = ckks.decode(C, ckks.decrypt(C, ct, s))
     assert np.abs(back - z).max() < 2.0 ** -20
     C.close()
+
+
+def test_baby_step_linear_transform_16x16_like_reference():
+    """test_ckks.cpp:468-503 on the GPU, with the reference's own inputs: the
+    same toy parameters (n=32, l=4, alpha=2, delta 2^48), the same
+    std::mt19937_64(211) stream consumed in the same order (keygen, x, the
+    16x16 matrix, encrypt, then per rotation evk_gen), the diagonals encoded
+    P-extended, one hoisted_rotate_accumulate; decrypted M x within 1e-4."""
+    n, l, a = 32, 4, 2
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=48))
+    rng = ckks.RefRng(211)
+    s = ckks.keygen(C, rng)
+    slots = n // 2
+    x = ref_unit_slots(rng.draws(2 * slots))
+    m = [ref_unit_slots(rng.draws(2 * slots)) for _ in range(slots)]
+    ct = ckks.encrypt(C, ckks.encode(C, x, C.default_scale(), l), s, rng)
+    keys, diags = [], []
+    for r in range(slots):
+        keys.append(ckks.evk_gen(C, s, ckks.ROTATION, r, rng) if r else None)
+        diag = np.array([m[t][(t + r) % slots] for t in range(slots)])
+        diags.append(ckks.encode(C, diag, C.default_scale(), l, p_extend=True))
+    y_ct = ckks.hoisted_rotate_accumulate(C, ct, list(range(slots)), diags, keys)
+    y = ckks.decode(C, ckks.decrypt(C, y_ct, s))
+    want = np.array([sum(m[t][j] * x[j] for j in range(slots)) for t in range(slots)])
+    assert np.abs(y - want).max() < 1e-4
+    C.close()
