@@ -122,3 +122,32 @@ def test_baby_step_linear_transform_16x16_like_reference():
     want = np.array([sum(m[t][j] * x[j] for j in range(slots)) for t in range(slots)])
     assert np.abs(y - want).max() < 1e-4
     C.close()
+
+
+def test_acceptance_c7_noise_bound_default_params():
+    """Acceptance criterion C7 (acceptance_main.cpp:303-350) on the GPU with
+    the reference's own inputs: default parameters (N=2^16, L=54, alpha=14,
+    delta 2^48), keys from mt19937_64(42) (keygen, relin, rot 1), 100 message
+    seeds mt19937_64(1000 + seed) (u, v, encrypt u, encrypt v); hadd,
+    pmult + rescale, hmult, hrot(1) all decrypt within 2^-20."""
+    C = ckks.CkksContext(ckks.CkksParams())
+    key_rng = ckks.RefRng(42)
+    s = ckks.keygen(C, key_rng)
+    relin = ckks.evk_gen(C, s, ckks.RELIN, 0, key_rng)
+    rot1 = ckks.evk_gen(C, s, ckks.ROTATION, 1, key_rng)
+    slots, l, D = C.n // 2, C.params.l, C.default_scale()
+    dec = lambda ct: ckks.decode(C, ckks.decrypt(C, ct, s))
+    err = {"hadd": 0.0, "pmult": 0.0, "hmult": 0.0, "hrot": 0.0}
+    for seed in range(100):
+        rng = ckks.RefRng(1000 + seed)
+        u = ref_unit_slots(rng.draws(2 * slots))
+        v = ref_unit_slots(rng.draws(2 * slots))
+        pt_u, pt_v = ckks.encode(C, u, D, l), ckks.encode(C, v, D, l)
+        cu = ckks.encrypt(C, pt_u, s, rng)
+        cv = ckks.encrypt(C, pt_v, s, rng)
+        err["hadd"] = max(err["hadd"], np.abs(dec(ckks.hadd(C, cu, cv)) - (u + v)).max())
+        err["pmult"] = max(err["pmult"], np.abs(dec(ckks.rescale(C, ckks.pmult(C, cu, pt_v))) - u * v).max())
+        err["hmult"] = max(err["hmult"], np.abs(dec(ckks.hmult(C, cu, cv, relin)) - u * v).max())
+        err["hrot"] = max(err["hrot"], np.abs(dec(ckks.hrot(C, cu, 1, rot1)) - np.roll(u, -1)).max())
+    assert max(err.values()) <= 2.0 ** -20, err
+    C.close()
