@@ -189,6 +189,19 @@ std::vector<uint32_t> generate_basis(uint32_t n, uint32_t l, uint32_t alpha, uin
 // One cudaMalloc holding a plan's small tables (job lists, constants, maps).
 class Blob {
  public:
+  Blob() = default;
+  Blob(const Blob&) = delete;  // owns a device allocation
+  Blob& operator=(const Blob&) = delete;
+  Blob(Blob&& o) noexcept : host_(std::move(o.host_)), dev_(o.dev_) { o.dev_ = nullptr; }
+  Blob& operator=(Blob&& o) noexcept {
+    if (this != &o) {
+      if (dev_) cudaFree(dev_);
+      host_ = std::move(o.host_);
+      dev_ = o.dev_;
+      o.dev_ = nullptr;
+    }
+    return *this;
+  }
   template <class T>
   size_t add(const std::vector<T>& v) {
     const size_t off = (host_.size() + 15) / 16 * 16;
@@ -380,7 +393,7 @@ struct Context {
   // encode / decode tables (encode.cu), built on first use
   double2 *d_fft_fwd = nullptr, *d_fft_inv = nullptr, *d_twist_enc = nullptr, *d_twist_dec = nullptr;
   uint32_t* d_jidx = nullptr;
-  std::map<uint32_t, CrtConst> crt_consts;  // prefix length -> CRT constants
+  std::map<uint32_t, Blob> crt_consts;  // prefix length -> device CRT constants
 
   // Host tables restating ckks.cpp:63-99 and :301-303, :346: per-stage FFT
   // twiddles with the reference's recurrence (w *= wl, std::complex<double>,
@@ -423,23 +436,42 @@ struct Context {
     up(td, d_twist_dec);
     up(jidx, d_jidx);
   }
-  const CrtConst& crt_const(uint32_t cnt) {
+  // CRT constants of the first cnt primes (multi-precision, ckks.cpp:337-346),
+  // uploaded once per prefix length
+  const CrtConst* crt_const(uint32_t cnt) {
     auto it = crt_consts.find(cnt);
-    if (it != crt_consts.end()) return it->second;
+    if (it != crt_consts.end()) return it->second.at<CrtConst>(0);
+    if (cnt > (uint32_t)kMaxCrt) throw InvalidArgument("decode: CRT lift over more than 16 primes is not supported");
+    auto mul = [](std::vector<uint32_t>& v, uint32_t m) {  // v *= m (little-endian limbs)
+      uint64_t carry = 0;
+      for (auto& x : v) {
+        const uint64_t t = (uint64_t)x * m + carry;
+        x = (uint32_t)t;
+        carry = t >> 32;
+      }
+      if (carry) v.push_back((uint32_t)carry);
+    };
     CrtConst cc;
     cc.c = (int)cnt;
-    unsigned __int128 M = 1;
-    for (uint32_t i = 0; i < cnt; ++i) M *= q(i);
+    std::vector<uint32_t> M{1};
+    for (uint32_t i = 0; i < cnt; ++i) mul(M, q(i));
+    for (size_t j = 0; j < M.size() && j < (size_t)kMaxCrt + 1; ++j) cc.m[j] = M[j];
     for (uint32_t i = 0; i < cnt; ++i) {
-      const unsigned __int128 Mi = M / q(i);
+      std::vector<uint32_t> Mi{1};
+      uint64_t mi_mod_qi = 1;  // (M / q_i) mod q_i
+      for (uint32_t k = 0; k < cnt; ++k)
+        if (k != i) {
+          mul(Mi, q(k));
+          mi_mod_qi = mi_mod_qi * (q(k) % q(i)) % q(i);
+        }
       cc.q[i] = q(i);
-      cc.y[i] = invm((uint32_t)(Mi % q(i)), q(i));
-      cc.mi_lo[i] = (uint64_t)Mi;
-      cc.mi_hi[i] = (uint64_t)(Mi >> 64);
+      cc.y[i] = invm((uint32_t)mi_mod_qi, q(i));
+      for (size_t j = 0; j < Mi.size() && j < (size_t)kMaxCrt; ++j) cc.mi[i][j] = Mi[j];
     }
-    cc.m_lo = (uint64_t)M;
-    cc.m_hi = (uint64_t)(M >> 64);
-    return crt_consts.emplace(cnt, cc).first->second;
+    Blob b;
+    b.add(std::vector<CrtConst>{cc});
+    b.upload();
+    return crt_consts.emplace(cnt, std::move(b)).first->second.at<CrtConst>(0);
   }
 
   ~Context() {
@@ -2365,7 +2397,6 @@ ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, dou
       bits += std::log2(static_cast<double>(c->q(cnt)));
       ++cnt;
     }
-    if (cnt > 4) throw InvalidArgument("decode: CRT lift over more than 4 primes is not supported");
     c->enc_tables();
     cudaStream_t st = S(stream);
     const size_t N = c->n;

@@ -110,12 +110,13 @@ bool bconv_tc_supported(int n, int max_sc, int max_dc);
 void bconv_tc(int n, const BconvLaunch& a, const BconvTc& t, cudaStream_t st);
 
 // CKKS encode / decode (encode.cu, ckks.cpp:278-362)
-struct CrtConst {  // CRT lift over the first c <= 4 primes (128-bit)
+constexpr int kMaxCrt = 16;  // decode: CRT lift over up to 16 primes (~460 bits)
+struct CrtConst {  // CRT over the first c primes, multi-precision (32-bit limbs, little endian)
   int c = 0;
-  uint32_t q[4] = {1, 1, 1, 1};
-  uint64_t y[4] = {0, 0, 0, 0};            // (M / q_i)^-1 mod q_i
-  uint64_t mi_lo[4] = {0, 0, 0, 0}, mi_hi[4] = {0, 0, 0, 0};  // M / q_i
-  uint64_t m_lo = 0, m_hi = 0;             // M
+  uint32_t q[kMaxCrt] = {};
+  uint32_t y[kMaxCrt] = {};                // (M / q_i)^-1 mod q_i
+  uint32_t mi[kMaxCrt][kMaxCrt] = {};      // M / q_i (c limbs)
+  uint32_t m[kMaxCrt + 1] = {};            // M (c limbs)
 };
 // reference fft_pow2 (ckks.cpp:63-87) on n = 2^logn points: src gathered in
 // bit-reversed order, result in dst; tw = per-stage twiddles (stage len at
@@ -125,7 +126,7 @@ void enc_scatter(int n, const double2* slots, int count, const uint32_t* jidx, d
 // scale = scale_mant * 2^scale_exp: the reference's long double scale (64-bit significand)
 void enc_round(int n, const double2* a, const double2* twist, unsigned long long scale_mant, int scale_exp, int rows,
                const uint32_t* row_q, uint32_t* out, cudaStream_t st);
-void dec_crt(int n, const uint32_t* rows, const CrtConst& cc, const double2* twist, double inv_scale, double2* a,
+void dec_crt(int n, const uint32_t* rows, const CrtConst* cc_dev, const double2* twist, double inv_scale, double2* a,
              cudaStream_t st);
 void dec_gather(int n, const double2* a, const uint32_t* jidx, double2* out, cudaStream_t st);
 

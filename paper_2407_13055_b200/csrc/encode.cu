@@ -5,8 +5,8 @@
 //           a = IDFT(a) by fft_pow2(invert) (ckks.cpp:63-87)             (FFT)
 //           m_k = llround(Re(a_k * psi^-k) * scale)  mod every q_i       (round + reduce)
 //           -> forward NTT (entry merge) in the caller                   (plaintext rows)
-//   decode: INTT of the first c rows (caller) -> CRT lift of c <= 4 primes
-//           (128-bit), centre, / scale -> a_k = coeff * (cos, sin)(pi k / n)
+//   decode: INTT of the first c rows (caller) -> CRT lift of c <= 16 primes
+//           (multi-precision limbs), centre, / scale -> a_k = coeff * (cos, sin)(pi k / n)
 //           -> fft_pow2(forward) -> out[t] = a[jidx[t]]
 //
 // The FFT reproduces the reference's radix-2 iterative transform operation by
@@ -132,36 +132,95 @@ __global__ void k_enc_round(int n, const double2* __restrict__ a, const double2*
   }
 }
 
-// correctly rounded conversion of a 128-bit magnitude to double
-__device__ __forceinline__ double u128_to_double(unsigned __int128 v) {
-  const uint64_t hi = (uint64_t)(v >> 64);
-  if (hi == 0) return __ull2double_rn((uint64_t)v);
-  const int sh = 64 - __clzll(hi);  // bits above the low 64
-  const unsigned __int128 mask = (((unsigned __int128)1) << sh) - 1;
-  uint64_t t = (uint64_t)(v >> sh);
-  if ((v & mask) != 0) t |= 1;  // sticky below the 53-bit rounding point (t has 64 significant bits)
-  return ldexp(__ull2double_rn(t), sh);
+// correctly rounded conversion of a little-endian multi-limb magnitude to double
+__device__ __forceinline__ double limbs_to_double(const uint32_t* v, int nl) {
+  int top = nl - 1;
+  while (top >= 0 && v[top] == 0) --top;
+  if (top < 0) return 0.0;
+  if (top <= 1) return __ull2double_rn(((uint64_t)(top == 1 ? v[1] : 0) << 32) | v[0]);
+  // top 64 bits starting at the highest set bit, plus a sticky bit for everything below
+  const int lz = __clz(v[top]);
+  const int hb = 32 * top + 31 - lz;  // index of the highest set bit
+  const int lo = hb - 63;             // bit index of the 64-bit window's lsb (>= 1 here)
+  uint64_t w = 0;
+  for (int i = 63; i >= 0; --i) {
+    const int b = lo + i;
+    w = (w << 1) | ((v[b >> 5] >> (b & 31)) & 1u);
+  }
+  bool sticky = false;
+  for (int b = 0; b < lo && !sticky; ++b) sticky = (v[b >> 5] >> (b & 31)) & 1u;
+  if (sticky) w |= 1;  // below the 53-bit rounding point: only breaks ties
+  return ldexp(__ull2double_rn(w), lo);
 }
 
-__global__ void k_dec_crt(int n, const uint32_t* __restrict__ rows, CrtConst cc, const double2* __restrict__ twist,
-                          double inv_scale, double2* __restrict__ a) {
+// CRT lift (multi-precision), centred, / scale, twisted: a_k = coeff (cos, sin)(pi k / n)
+__global__ void k_dec_crt(int n, const uint32_t* __restrict__ rows, const CrtConst* __restrict__ ccp,
+                          const double2* __restrict__ twist, double inv_scale, double2* __restrict__ a) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  unsigned __int128 v = 0;
-  for (int i = 0; i < cc.c; ++i) {
+  const CrtConst& cc = *ccp;
+  const int c = cc.c, nl = c + 1;
+  uint32_t acc[kMaxCrt + 1];
+  for (int j = 0; j < nl; ++j) acc[j] = 0;
+  for (int i = 0; i < c; ++i) {  // acc += ((r_i y_i) mod q_i) * (M / q_i)
     const uint32_t r = rows[(size_t)i * n + k];
-    const uint64_t t = (uint64_t)r * cc.y[i] % cc.q[i];  // (r * (M/q_i)^-1) mod q_i
-    const unsigned __int128 Mi = ((unsigned __int128)cc.mi_hi[i] << 64) | cc.mi_lo[i];
-    v += Mi * t;  // < M each, sum < 4M < 2^128
+    const uint32_t t = (uint32_t)((uint64_t)r * cc.y[i] % cc.q[i]);
+    uint64_t carry = 0;
+    for (int j = 0; j < c; ++j) {
+      const uint64_t s = (uint64_t)t * cc.mi[i][j] + acc[j] + carry;
+      acc[j] = (uint32_t)s;
+      carry = s >> 32;
+    }
+    for (int j = c; j < nl && carry; ++j) {
+      const uint64_t s = (uint64_t)acc[j] + carry;
+      acc[j] = (uint32_t)s;
+      carry = s >> 32;
+    }
   }
-  const unsigned __int128 M = ((unsigned __int128)cc.m_hi << 64) | cc.m_lo;
-  while (v >= M) v -= M;
-  double coeff;
-  if (v > (M >> 1)) coeff = -u128_to_double(M - v);  // centred lift (ckks.cpp:344)
-  else coeff = u128_to_double(v);
+  auto geq_m = [&]() {  // acc >= M ?
+    for (int j = nl - 1; j >= 0; --j) {
+      const uint32_t mj = j < c ? cc.m[j] : 0u;
+      if (acc[j] != mj) return acc[j] > mj;
+    }
+    return true;
+  };
+  while (geq_m()) {  // sum < c M: at most c subtractions
+    int64_t borrow = 0;
+    for (int j = 0; j < nl; ++j) {
+      const int64_t s = (int64_t)acc[j] - (j < c ? cc.m[j] : 0u) - borrow;
+      acc[j] = (uint32_t)s;
+      borrow = s < 0;
+    }
+  }
+  // centred lift (ckks.cpp:344): v > M / 2  <=>  2 v > M
+  bool neg = false;
+  {
+    uint32_t carry = 0;
+    int cmp = 0;  // compare 2 acc with M, from the top
+    uint32_t twice[kMaxCrt + 1];
+    for (int j = 0; j < nl; ++j) {
+      twice[j] = (acc[j] << 1) | carry;
+      carry = acc[j] >> 31;
+    }
+    for (int j = nl - 1; j >= 0 && cmp == 0; --j) {
+      const uint32_t mj = j < c ? cc.m[j] : 0u;
+      if (twice[j] != mj) cmp = twice[j] > mj ? 1 : -1;
+    }
+    neg = cmp > 0;
+  }
+  if (neg) {  // acc = M - acc
+    int64_t borrow = 0;
+    for (int j = 0; j < nl; ++j) {
+      const int64_t s = (int64_t)(j < c ? cc.m[j] : 0u) - acc[j] - borrow;
+      acc[j] = (uint32_t)s;
+      borrow = s < 0;
+    }
+  }
+  double coeff = limbs_to_double(acc, nl);
+  if (neg) coeff = -coeff;
   coeff = __dmul_rn(coeff, inv_scale);
-  const double2 t = twist[k];
-  a[k] = make_double2(__dmul_rn(coeff, t.x), __dmul_rn(coeff, t.y));
+  const double2 tw = twist[k];
+  a[k] = make_double2(__dmul_rn(coeff, tw.x), __dmul_rn(coeff, tw.y));
 }
 
 __global__ void k_dec_gather(int n, const double2* __restrict__ a, const uint32_t* __restrict__ jidx,
@@ -196,9 +255,9 @@ void enc_round(int n, const double2* a, const double2* twist, unsigned long long
   k_enc_round<<<cdiv(n, 256), 256, 0, st>>>(n, a, twist, 1.0 / n, scale_mant, scale_exp, rows, row_q, out);
 }
 
-void dec_crt(int n, const uint32_t* rows, const CrtConst& cc, const double2* twist, double inv_scale, double2* a,
+void dec_crt(int n, const uint32_t* rows, const CrtConst* cc_dev, const double2* twist, double inv_scale, double2* a,
              cudaStream_t st) {
-  k_dec_crt<<<cdiv(n, 256), 256, 0, st>>>(n, rows, cc, twist, inv_scale, a);
+  k_dec_crt<<<cdiv(n, 128), 128, 0, st>>>(n, rows, cc_dev, twist, inv_scale, a);
 }
 
 void dec_gather(int n, const double2* a, const uint32_t* jidx, double2* out, cudaStream_t st) {

@@ -151,3 +151,75 @@ def test_acceptance_c7_noise_bound_default_params():
         err["hrot"] = max(err["hrot"], np.abs(dec(ckks.hrot(C, cu, 1, rot1)) - np.roll(u, -1)).max())
     assert max(err.values()) <= 2.0 ** -20, err
     C.close()
+
+
+def test_acceptance_c8_hoisting_counters():
+    """Acceptance C8 (acceptance_main.cpp:354-408) on the GPU with the
+    reference's inputs (n=2^10, l=8, alpha=2, h=64, mt19937_64(29)): 8
+    separate HRots cost 8 ModUps, hoisted_rotations 1, and
+    hoisted_rotate_accumulate 1 ModUp + 1 ModDown."""
+    C = ckks.CkksContext(ckks.CkksParams(n=1024, l=8, alpha=2, delta_bits=48, hamming=64))
+    rng = ckks.RefRng(29)
+    s = ckks.keygen(C, rng)
+    rots = list(range(1, 9))
+    keys = [ckks.evk_gen(C, s, ckks.ROTATION, r, rng) for r in rots]
+    u = ref_unit_slots(rng.draws(C.n))
+    ct = ckks.encrypt(C, ckks.encode(C, u, C.default_scale(), 8), s, rng)
+    C.reset_counters()
+    outs = [ckks.hrot(C, ct, r, k) for r, k in zip(rots, keys)]
+    unhoisted = C.counters()["modup"]
+    C.reset_counters()
+    hoisted = ckks.hoisted_rotations(C, ct, rots, keys)
+    assert C.counters()["modup"] == 1 and unhoisted == 8
+    for a, b in zip(outs, hoisted):  # singleton-hoist == hrot, bit-exact (test_ckks.cpp:382-466)
+        assert torch.equal(a.data, b.data)
+    pts = [ckks.encode(C, np.full(C.n // 2, 0.125 * (i + 1)), C.default_scale(), 8, p_extend=True)
+           for i in range(len(rots))]
+    C.reset_counters()
+    acc = ckks.hoisted_rotate_accumulate(C, ct, rots, pts, keys)
+    c = C.counters()
+    assert (c["modup"], c["moddown"]) == (1, 1)
+    want = sum(0.125 * (i + 1) * np.roll(u, -r) for i, r in enumerate(rots))
+    back = ckks.decode(C, ckks.decrypt(C, acc, s))
+    assert np.abs(back - want).max() < 1e-6
+    C.close()
+
+
+def test_acceptance_c9_merged_vs_lazy_hmult():
+    """Acceptance C9 (acceptance_main.cpp:413-478) on the GPU with the
+    reference's inputs: n=2^12, l=12, alpha=3, h=128, keys mt19937_64(7) in
+    a merged and a lazy-rescale context, 50 message seeds (500 + seed); the
+    lazy path defers the rescale, the flushed ledgers are identical, the two
+    decryptions agree within their combined noise and the noise bounds stay
+    within 4x of each other."""
+    base = dict(n=4096, l=12, alpha=3, delta_bits=48, hamming=128)
+    Cm = ckks.CkksContext(ckks.CkksParams(**base))
+    Cu = ckks.CkksContext(ckks.CkksParams(**base, lazy_rescale=True))
+    kr_m, kr_u = ckks.RefRng(7), ckks.RefRng(7)
+    sk_m, sk_u = ckks.keygen(Cm, kr_m), ckks.keygen(Cu, kr_u)
+    relin_m = ckks.evk_gen(Cm, sk_m, ckks.RELIN, 0, kr_m)
+    relin_u = ckks.evk_gen(Cu, sk_u, ckks.RELIN, 0, kr_u)
+    slots = Cm.n // 2
+    bound_m = bound_u = 0.0
+    for seed in range(50):
+        rng_m, rng_u = ckks.RefRng(500 + seed), ckks.RefRng(500 + seed)
+        u = ref_unit_slots(rng_m.draws(2 * slots))
+        v = ref_unit_slots(rng_m.draws(2 * slots))
+        rng_u.draws(4 * slots)  # the same draws keep both encryption streams aligned
+
+        def enc(C, sk, r, m):
+            return ckks.encrypt(C, ckks.encode(C, m, C.default_scale(), 12), sk, r)
+
+        ct_m = ckks.hmult(Cm, enc(Cm, sk_m, rng_m, u), enc(Cm, sk_m, rng_m, v), relin_m)
+        ct_l = ckks.hmult(Cu, enc(Cu, sk_u, rng_u, u), enc(Cu, sk_u, rng_u, v), relin_u)
+        assert ct_l.pending_rescale
+        ct_f = ckks.rescale(Cu, ct_l)
+        assert (ct_m.level, ct_m.scale) == (ct_f.level, ct_f.scale)
+        dm = ckks.decode(Cm, ckks.decrypt(Cm, ct_m, sk_m))
+        du = ckks.decode(Cu, ckks.decrypt(Cu, ct_f, sk_u))
+        e_m, e_u = np.abs(dm - u * v).max(), np.abs(du - u * v).max()
+        bound_m, bound_u = max(bound_m, e_m), max(bound_u, e_u)
+        assert np.abs(dm - du).max() <= e_m + e_u + 1e-12
+    assert bound_m <= 4 * bound_u + 1e-12 and bound_u <= 4 * bound_m + 1e-12
+    Cm.close()
+    Cu.close()
