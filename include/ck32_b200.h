@@ -164,7 +164,7 @@ ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, do
 /* decode (ckks.cpp:321-362): plaintext rows [level][n] (evaluation,
  * Montgomery) -> n/2 complex slots (re, im doubles, device memory).  The CRT
  * lift uses the minimal prime prefix covering scale_log2 + 40 bits (as the
-  * reference), multi-precision, up to 16 primes. */
+ * reference), multi-precision, up to 16 primes. */
 ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2, double* slots_dev,
                     ck_stream stream);
 
