@@ -39,6 +39,12 @@ struct Scale {
   int pow2 = 0;
   std::vector<uint32_t> num, den;
   static Scale two_pow(int b) { return Scale{b, {}, {}}; }
+  // 2^p2 * prod(n) / prod(d) for arbitrary positive integer factors, reduced
+  static Scale rational(int p2, std::vector<uint32_t> n, std::vector<uint32_t> d) {
+    Scale r{p2, std::move(n), std::move(d)};
+    r.normalize();
+    return r;
+  }
   Scale operator*(const Scale& o) const {
     Scale r{pow2 + o.pow2, num, den};
     r.num.insert(r.num.end(), o.num.begin(), o.num.end());
@@ -53,7 +59,52 @@ struct Scale {
     r.normalize();
     return r;
   }
+  // canonical form (the reference's Rational is always reduced): factors of
+  // two folded into pow2, every other factor split into primes, common primes
+  // cancelled -- equal values compare equal and log2_rational sees the reduced
+  // fraction.  Basis primes pass the primality test at once.
+  static bool is_prime32(uint32_t n) {  // deterministic Miller-Rabin for 32-bit n
+    if (n < 2) return false;
+    for (uint32_t p : {2u, 3u, 5u, 7u, 11u, 13u})
+      if (n % p == 0) return n == p;
+    uint32_t d = n - 1;
+    int r = 0;
+    while (!(d & 1)) d >>= 1, ++r;
+    for (uint64_t a : {2ull, 7ull, 61ull}) {
+      uint64_t x = 1, b = a % n, e = d;
+      for (; e; e >>= 1, b = b * b % n)
+        if (e & 1) x = x * b % n;
+      if (x == 1 || x == n - 1) continue;
+      bool comp = true;
+      for (int i = 1; i < r && comp; ++i) {
+        x = x * x % n;
+        if (x == n - 1) comp = false;
+      }
+      if (comp) return false;
+    }
+    return true;
+  }
+  static void split(std::vector<uint32_t>& v, int& twos) {
+    std::vector<uint32_t> out;
+    for (uint32_t f : v) {
+      if (f == 0) throw std::invalid_argument("zero scale factor");
+      while (!(f & 1)) f >>= 1, ++twos;
+      if (f == 1) continue;
+      if (is_prime32(f)) {
+        out.push_back(f);
+        continue;
+      }
+      for (uint32_t p = 3; (uint64_t)p * p <= f; p += 2)
+        while (f % p == 0) out.push_back(p), f /= p;
+      if (f > 1) out.push_back(f);
+    }
+    v = std::move(out);
+  }
   void normalize() {
+    int tn = 0, td = 0;
+    split(num, tn);
+    split(den, td);
+    pow2 += tn - td;
     std::sort(num.begin(), num.end());
     std::sort(den.begin(), den.end());
     std::vector<uint32_t> n2, d2;

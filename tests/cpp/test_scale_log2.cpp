@@ -26,7 +26,7 @@ int main() {
     int p2;
     std::string a, b;
     ss >> p2 >> a >> b;
-    Scale s{p2, parse(a), parse(b)};
+    Scale s = Scale::rational(p2, parse(a), parse(b));
     std::printf("%a\n", scale_log2(s));
   }
   return 0;

@@ -91,7 +91,8 @@ def test_cpp_mirror_scale_log2_matches_log2_rational(tmp_path):
     from paper_2407_13055_b200.ckks import log2_rational
     primes = [268369921, 268361729, 268238849, 268271617, 399769601, 402849793]
     cases = [(55, [], []), (110, [], primes[:2]), (55, primes[2:3], primes[:1]), (-3, primes[:3], []),
-             (0, primes, primes[:1]), (110, [7], [3, 5]), (20, [], [3])]
+             (0, primes, primes[:1]), (110, [7], [3, 5]), (20, [], [3]),
+             (53, [6, 35], [4, 21]), (0, [1 << 20, 9], [3 << 10]), (-7, [4294967291], [65537, 6])]
     inp = "\n".join(f"{p2} {','.join(map(str, a)) or '-'} {','.join(map(str, b)) or '-'}" for p2, a, b in cases)
     out = subprocess.run([str(exe)], input=inp, capture_output=True, text=True, check=True).stdout.split()
     for (p2, a, b), got in zip(cases, out):
