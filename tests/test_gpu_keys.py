@@ -223,3 +223,81 @@ def test_acceptance_c9_merged_vs_lazy_hmult():
     assert bound_m <= 4 * bound_u + 1e-12 and bound_u <= 4 * bound_m + 1e-12
     Cm.close()
     Cu.close()
+
+
+def _crt_centered(rows, primes):
+    """CRT-lift canonical coefficient rows [l][n] over `primes`, centred."""
+    M = 1
+    for q in primes:
+        M *= q
+    out = []
+    for k in range(rows.shape[1]):
+        v = 0
+        for i, q in enumerate(primes):
+            Mi = M // q
+            v += int(rows[i, k]) * Mi * pow(Mi, -1, q)
+        v %= M
+        out.append(v - M if v > M // 2 else v)
+    return out, M
+
+
+def _toy(n=256, l=6, a=2):  # test_ckks.cpp toy_params
+    return ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=48, hamming=64))
+
+
+def test_key_switch_retargets_decryption_like_reference():
+    """test_ckks.cpp:155-191 on the GPU with its inputs (mt19937_64(149):
+    keygen, relin key, random d): c0 + c1 s - d s^2 has centred coefficients
+    within 2^24."""
+    C = _toy()
+    rng = ckks.RefRng(149)
+    s = ckks.keygen(C, rng)
+    relin = ckks.evk_gen(C, s, ckks.RELIN, 0, rng)
+    l, n = C.params.l, C.n
+    primes = [int(q) for q in C.q_primes[:l]]
+    d = rng.uniform(primes, n)
+    c0, c1 = ckks.key_switch(C, ckks.Polynomial(torch.from_numpy(d.astype(np.int64).astype(np.int32)).cuda(), l),
+                             relin)
+    S = s[:l].cpu().numpy().astype(np.uint32).astype(object)
+    C0 = c0.data.cpu().numpy().astype(np.uint32).astype(object)
+    C1 = c1.data.cpu().numpy().astype(np.uint32).astype(object)
+    D = d.astype(object)
+    e = np.empty((l, n), dtype=np.int64)
+    for i, q in enumerate(primes):
+        rinv = pow(1 << 32, -1, q)
+        got = (C0[i] + C1[i] * S[i] * rinv) % q
+        want = (D[i] * S[i] * S[i] * rinv * rinv) % q
+        e[i] = ((got - want) % q).astype(np.int64)
+    poly = ckks.intt_inverse(C, ckks.Polynomial(torch.from_numpy(e.astype(np.int32)).cuda(), l))
+    coeffs, _ = _crt_centered(poly.data.cpu().numpy().astype(np.uint32), primes)
+    assert max(abs(x) for x in coeffs) <= 1 << 24
+    C.close()
+
+
+def test_rescale_is_floor_divide_like_reference():
+    """test_ckks.cpp:193-237 on the GPU with its inputs (mt19937_64(151):
+    keygen, slots, encode, encrypt): after rescale, b's coefficients equal
+    floor(v / (q_{l-2} q_{l-1})) - e with e in {0, 1}; level l-2, scale
+    divided by q_{l-2} q_{l-1}; a second rescale drops two more primes."""
+    C = _toy()
+    rng = ckks.RefRng(151)
+    s = ckks.keygen(C, rng)
+    n, l = C.n, C.params.l
+    u = ref_unit_slots(rng.draws(n))
+    ct = ckks.encrypt(C, ckks.encode(C, u, C.default_scale(), l), s, rng)
+    primes = [int(q) for q in C.q_primes[:l]]
+    qq = primes[l - 2] * primes[l - 1]
+    before = ckks.intt_inverse(C, ckks.Polynomial(ct.data[0].clone(), l)).data.cpu().numpy().astype(np.uint32)
+    rs = ckks.rescale(C, ct)
+    assert rs.level == l - 2 and rs.scale == ct.scale / qq
+    after = ckks.intt_inverse(C, ckks.Polynomial(rs.data[0].clone(), l - 2)).data.cpu().numpy().astype(np.uint32)
+    M_full = 1
+    for q in primes:
+        M_full *= q
+    M_low = M_full // qq
+    for k in range(n):
+        v = sum(int(before[i, k]) * (M_full // q) * pow(M_full // q, -1, q) for i, q in enumerate(primes)) % M_full
+        got = sum(int(after[i, k]) * (M_low // q) * pow(M_low // q, -1, q) for i, q in enumerate(primes[:l - 2])) % M_low
+        assert (v // qq - got) % M_low in (0, 1)
+    assert ckks.rescale(C, rs).level == l - 4
+    C.close()
