@@ -301,3 +301,95 @@ def test_rescale_is_floor_divide_like_reference():
         assert (v // qq - got) % M_low in (0, 1)
     assert ckks.rescale(C, rs).level == l - 4
     C.close()
+
+
+# ---- test_ckks.cpp:239-380 on the GPU, each with the reference's own inputs
+def _slots(rng, C):
+    return ref_unit_slots(rng.draws(C.n))
+
+
+def test_pmult_rescale_like_reference():  # test_ckks.cpp:239-259, mt19937_64(157)
+    C = _toy()
+    rng = ckks.RefRng(157)
+    s = ckks.keygen(C, rng)
+    u, v = _slots(rng, C), _slots(rng, C)
+    l, D = C.params.l, C.default_scale()
+    ct = ckks.encrypt(C, ckks.encode(C, u, D, l), s, rng)
+    out = ckks.decode(C, ckks.decrypt(C, ckks.rescale(C, ckks.pmult(C, ct, ckks.encode(C, v, D, l))), s))
+    assert np.abs(out - u * v).max() < 1e-5
+    ones = ckks.encode(C, np.ones(C.n // 2), D, l)
+    out_id = ckks.decode(C, ckks.decrypt(C, ckks.rescale(C, ckks.pmult(C, ct, ones)), s))
+    assert np.abs(out_id - u).max() < 1e-5
+    C.close()
+
+
+def test_hadd_padd_and_scale_check_like_reference():  # test_ckks.cpp:261-289, mt19937_64(163)
+    C = _toy()
+    rng = ckks.RefRng(163)
+    s = ckks.keygen(C, rng)
+    u, v = _slots(rng, C), _slots(rng, C)
+    l, D = C.params.l, C.default_scale()
+    cu = ckks.encrypt(C, ckks.encode(C, u, D, l), s, rng)
+    cv = ckks.encrypt(C, ckks.encode(C, v, D, l), s, rng)
+    assert np.abs(ckks.decode(C, ckks.decrypt(C, ckks.hadd(C, cu, cv), s)) - (u + v)).max() < 1e-5
+    pv = ckks.encode(C, v, D, l)
+    assert np.abs(ckks.decode(C, ckks.decrypt(C, ckks.padd(C, cu, pv), s)) - (u + v)).max() < 1e-5
+    bad = ckks.Ciphertext(cv.data.clone(), cv.scale * Fraction(1025, 1024), cv.level)
+    with pytest.raises(ValueError):
+        ckks.hadd(C, cu, bad)
+    C.close()
+
+
+def test_hmult_merged_and_identity_like_reference():  # test_ckks.cpp:291-318, mt19937_64(167)
+    C = _toy()
+    rng = ckks.RefRng(167)
+    s = ckks.keygen(C, rng)
+    relin = ckks.evk_gen(C, s, ckks.RELIN, 0, rng)
+    u, v = _slots(rng, C), _slots(rng, C)
+    l, D = C.params.l, C.default_scale()
+    cu = ckks.encrypt(C, ckks.encode(C, u, D, l), s, rng)
+    cv = ckks.encrypt(C, ckks.encode(C, v, D, l), s, rng)
+    prod = ckks.hmult(C, cu, cv, relin)
+    assert prod.level == l - 2 and not prod.pending_rescale
+    assert np.abs(ckks.decode(C, ckks.decrypt(C, prod, s)) - u * v).max() < 1e-4
+    c1 = ckks.encrypt(C, ckks.encode(C, np.ones(C.n // 2), D, l), s, rng)
+    assert np.abs(ckks.decode(C, ckks.decrypt(C, ckks.hmult(C, cu, c1, relin), s)) - u).max() < 1e-4
+    C.close()
+
+
+def test_merged_and_lazy_hmult_agree_like_reference():  # test_ckks.cpp:320-362, seeds 173 / 179 / 191
+    Cm = _toy()
+    Cl = ckks.CkksContext(ckks.CkksParams(n=256, l=6, alpha=2, delta_bits=48, hamming=64, lazy_rescale=True))
+    ra, rb = ckks.RefRng(173), ckks.RefRng(173)
+    sm, sl = ckks.keygen(Cm, ra), ckks.keygen(Cl, rb)
+    relm, rell = ckks.evk_gen(Cm, sm, ckks.RELIN, 0, ra), ckks.evk_gen(Cl, sl, ckks.RELIN, 0, rb)
+    msg = ckks.RefRng(179)
+    u, v = _slots(msg, Cm), _slots(msg, Cm)
+    ea, eb = ckks.RefRng(191), ckks.RefRng(191)
+    l, D = 6, Cm.default_scale()
+    cum, cvm = (ckks.encrypt(Cm, ckks.encode(Cm, z, D, l), sm, ea) for z in (u, v))
+    cul, cvl = (ckks.encrypt(Cl, ckks.encode(Cl, z, D, l), sl, eb) for z in (u, v))
+    pm = ckks.hmult(Cm, cum, cvm, relm)
+    pl = ckks.hmult(Cl, cul, cvl, rell)
+    assert pl.pending_rescale and pl.level == l
+    pr = ckks.rescale(Cl, pl)
+    assert (pm.level, pm.scale) == (pr.level, pr.scale)
+    om = ckks.decode(Cm, ckks.decrypt(Cm, pm, sm))
+    ol = ckks.decode(Cl, ckks.decrypt(Cl, pr, sl))
+    assert np.abs(om - ol).max() < 1e-4
+    Cm.close()
+    Cl.close()
+
+
+def test_hrot_rotates_left_like_reference():  # test_ckks.cpp:364-380, mt19937_64(193)
+    C = _toy()
+    rng = ckks.RefRng(193)
+    s = ckks.keygen(C, rng)
+    u = _slots(rng, C)
+    l, D = C.params.l, C.default_scale()
+    ct = ckks.encrypt(C, ckks.encode(C, u, D, l), s, rng)
+    for r in (1, 3, C.n // 4):
+        evk = ckks.evk_gen(C, s, ckks.ROTATION, r, rng)
+        out = ckks.decode(C, ckks.decrypt(C, ckks.hrot(C, ct, r, evk), s))
+        assert np.abs(out - np.roll(u, -r)).max() < 1e-5
+    C.close()
