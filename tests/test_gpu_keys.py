@@ -393,3 +393,33 @@ def test_hrot_rotates_left_like_reference():  # test_ckks.cpp:364-380, mt19937_6
         out = ckks.decode(C, ckks.decrypt(C, ckks.hrot(C, ct, r, evk), s))
         assert np.abs(out - np.roll(u, -r)).max() < 1e-5
     C.close()
+
+
+def test_level_and_scale_ledger_like_reference():  # test_ckks.cpp:505-550, mt19937_64(223)
+    C = ckks.CkksContext(ckks.CkksParams(n=32, l=8, alpha=2, delta_bits=48, hamming=8))
+    rng = ckks.RefRng(223)
+    s = ckks.keygen(C, rng)
+    relin = ckks.evk_gen(C, s, ckks.RELIN, 0, rng)
+    u = _slots(rng, C)
+    D = C.default_scale()
+    primes = [int(q) for q in C.q_primes]
+    for _ in range(10):
+        ct = ckks.encrypt(C, ckks.encode(C, u, D, 8), s, rng)
+        scale, level = D, 8
+        for _ in range(6):
+            op = int(rng.draws(1)[0]) % 4
+            if op == 0:
+                ct = ckks.hadd(C, ct, ct)
+            elif op == 1:
+                ct = ckks.pmult(C, ct, ckks.encode(C, u, D, level))
+                scale *= D
+            elif op == 2 and level >= 4:
+                ct = ckks.rescale(C, ct)
+                scale /= primes[level - 2] * primes[level - 1]
+                level -= 2
+            elif op == 3 and level >= 4:
+                ct = ckks.hmult(C, ct, ct, relin)
+                scale = scale * scale / (primes[level - 2] * primes[level - 1])
+                level -= 2
+            assert ct.level == level and ct.scale == scale
+    C.close()
