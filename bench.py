@@ -360,7 +360,11 @@ def main():
                 "traffic_source": "profiles/ncu_traffic.json (ncu --set full DRAM bytes per algorithmic byte)"
                 if tr else None, "peak_kind": peak_kind,
                 "bytes_per_launch_group": round(p["bytes"] / max(p["groups"], 1)),
-                "avg_group_ms": round(p["ms"] / max(p["groups"], 1), 4)}
+                "avg_group_ms": round(p["ms"] / max(p["groups"], 1), 4),
+                "timing": "CUDA events around every launch group on its launching stream (ck_profile), over "
+                          "steps of the same workload run on one stream right after the timed region: in the "
+                          "2-stream timed region the two streams' kernels overlap, so per-kernel spans there "
+                          "would count the other stream's time"}
 
     def int_pipe(p):
         """INT-pipe view of an NTT class (report it beside GB/s).
