@@ -549,6 +549,45 @@ inline PublicKey pubkey_gen(CkksContext& ctx, const SecretKey& sk, std::mt19937_
   return pk;
 }
 
+// evk_gen (ckks.cpp:426-477): digit k = (b_k, a_k) with b_k = e_k + g_k s_src - a_k s_dst
+// over the full L + alpha rows; relinearisation s_src = s^2, s_dst = s;
+// rotation r s_src = s, s_dst = phi_{-r}(s).  The gadget factor
+// g_k = P dhat_k (dhat_k^-1 mod d_k) needs no big integers here: it is
+// P mod q for the primes q of digit k and 0 mod every other prime.
+inline EvaluationKey evk_gen(CkksContext& ctx, const SecretKey& sk, KeyKind kind, int64_t rotation,
+                             std::mt19937_64& rng) {
+  const uint32_t L = ctx.params().l, A = ctx.params().alpha, n = ctx.params().n, rows = L + A;
+  const uint32_t D = ctx.num_digits(L);
+  const size_t poly = (size_t)rows * n;
+  EvaluationKey evk{DeviceBuffer(ctx.raw(), (size_t)D * 2 * poly), kind, kind == KeyKind::Rotation ? rotation : 0};
+  const uint32_t* s = sk.s.data();
+  DeviceBuffer rot;
+  const uint32_t* s_dst = s;
+  if (kind == KeyKind::Rotation) {
+    rot = DeviceBuffer(ctx.raw(), poly);
+    check(ck_automorphism(ctx.raw(), s, rot.data(), rows, -rotation, nullptr));
+    s_dst = rot.data();
+  }
+  const auto& pr = ctx.primes();
+  for (uint32_t k = 0; k < D; ++k) {
+    std::vector<uint32_t> gm(rows, 0u);
+    for (uint32_t i = k * A; i < std::min((k + 1) * A, L); ++i) {
+      const uint64_t q = pr[i];
+      uint64_t pm = 1;
+      for (uint32_t j = 0; j < A; ++j) pm = pm * (pr[L + j] % q) % q;
+      gm[i] = (uint32_t)((pm << 32) % q);  // Montgomery form
+    }
+    DeviceBuffer a = detail::uniform_eval(ctx, rng, L, A);
+    DeviceBuffer e = detail::coeffs_to_eval(ctx, detail::gaussian(rng, n, ctx.params().sigma), L, A);
+    uint32_t* bk = evk.data.data() + (size_t)k * 2 * poly;
+    check(ck_memcpy_d2d(ctx.raw(), bk + poly, a.data(), poly * 4, nullptr));
+    check(ck_evk_digit(ctx.raw(), s, s_dst, a.data(), e.data(), gm.data(), kind == KeyKind::Relin ? 1 : 0, bk,
+                       nullptr));
+  }
+  check(ck_stream_sync(ctx.raw(), nullptr));
+  return evk;
+}
+
 // encrypt (ckks.cpp:497-539): (m + e - a s, a) / (v pk.b + e0 + m, v pk.a + e1)
 inline Ciphertext encrypt(CkksContext& ctx, const Plaintext& pt, const SecretKey& sk, std::mt19937_64& rng) {
   if (pt.p_count != 0) throw std::invalid_argument("cannot encrypt a P-extended plaintext");

@@ -35,9 +35,9 @@ static void write_file(const std::string& p, const std::vector<uint32_t>& v) {
 
 // keys mode: keygen + encode + secret-key encrypt with the reference's own
 // generator type, in the fixture driver's order (oracle/ref_driver.cpp
-// ref_gen_fixtures: keygen, 3 x evk_gen (skipped here: discard), slots u, v)
+// ref_gen_fixtures: keygen, relin / rot 1 / rot 3 evk_gen, slots u, v)
 //   test_cpp_api keys <dir> <seed> <n> <l> <alpha> <delta_bits>
-// writes <dir>/sk_rows.bin [L+alpha][n], ct_u.bin, ct_v.bin [2][l][n]
+// writes <dir>/sk_rows.bin [L+alpha][n], evk_*.bin [D][2][L+alpha][n], ct_u.bin, ct_v.bin [2][l][n]
 static int keys_mode(char** argv) {
   const std::string dir = argv[2];
   std::mt19937_64 rng(std::strtoull(argv[3], nullptr, 10));
@@ -50,8 +50,9 @@ static int keys_mode(char** argv) {
   CkksContext ctx(p);
   SecretKey sk = keygen(ctx, rng);
   write_file(dir + "/sk_rows.bin", sk.s.download());
-  const uint64_t D = ctx.num_digits(p.l);
-  rng.discard(3 * D * ((uint64_t)(p.l + p.alpha) * p.n + 2ull * p.n));  // relin, rot1, rot3 evk_gen draws
+  write_file(dir + "/evk_relin.bin", evk_gen(ctx, sk, KeyKind::Relin, 0, rng).data.download());
+  write_file(dir + "/evk_rot1.bin", evk_gen(ctx, sk, KeyKind::Rotation, 1, rng).data.download());
+  write_file(dir + "/evk_rot3.bin", evk_gen(ctx, sk, KeyKind::Rotation, 3, rng).data.download());
   std::uniform_real_distribution<double> dist(-1.0, 1.0);
   std::vector<std::complex<double>> z[2];  // slots u, v drawn before either encryption
   for (auto& zz : z) {

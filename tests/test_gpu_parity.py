@@ -511,9 +511,10 @@ def test_cpp_mirror_drop_in(tmp_path):
 
 
 def test_cpp_mirror_keys_with_std_mt19937_64(tmp_path):
-    """keygen / encode / encrypt of the C++ mirror take the caller's
-    std::mt19937_64 (ckks.hpp:160-167) and reproduce the reference's own
-    fixtures bit for bit (sk.s, ct_u, ct_v of tests/golden)."""
+    """keygen / evk_gen / encode / encrypt of the C++ mirror take the
+    caller's std::mt19937_64 (ckks.hpp:155-167) and reproduce the reference's
+    own fixtures bit for bit (sk.s, relin / rot 1 / rot 3 keys, ct_u, ct_v of
+    tests/golden)."""
     import subprocess
     from pathlib import Path
 
@@ -530,6 +531,10 @@ def test_cpp_mirror_keys_with_std_mt19937_64(tmp_path):
         assert r.returncode == 0 and "cpp keys ok" in r.stdout, r.stdout + r.stderr
         sk = np.fromfile(tmp_path / "sk_rows.bin", dtype="<u4").reshape(l + a, n)
         np.testing.assert_array_equal(sk, F.poly("sk").rows)
+        for name in ("evk_relin", "evk_rot1", "evk_rot3"):
+            want = F.evk(name).stacked()
+            got = np.fromfile(tmp_path / f"{name}.bin", dtype="<u4").reshape(want.shape)
+            np.testing.assert_array_equal(got, want, err_msg=f"{d.name} {name}")
         np.testing.assert_array_equal(np.fromfile(tmp_path / "pt_v.bin", dtype="<u4").reshape(l, n),
                                       F.poly("pt_v").rows, err_msg=f"{d.name} pt_v")
         for name in ("ct_u", "ct_v"):
