@@ -281,8 +281,12 @@ ck_status ck_sample_uniform(ck_rng* rng, const uint32_t* q, uint32_t rows, uint3
  * 10 s; a timeout sets the error word read by ck_shard_peer_error instead of
  * hanging) and its BConv loads the source rows straight from the peers'
  * buffers.  Every rank must issue every phase in the same order (as with a
- * collective).  The buffers are double-buffered per exchange kind, so a
- * buffer is rewritten only after all peers have finished reading it. */
+ * collective) and on ONE stream per rank: the double-buffer reuse argument
+ * (a buffer is rewritten only after all peers have finished reading it)
+ * relies on each rank's phases being stream-ordered.  After a timeout the
+ * phase-2 outputs are poisoned (0xFFFFFFFF, never a canonical residue) and
+ * ck_shard_peer_error reports it; ck_shard_set_peers clears the flag and
+ * error words (callers barrier after it). */
 ck_status ck_shard_exchange_buffer(ck_shard* sh, void** base, uint64_t* bytes);
 ck_status ck_shard_set_peers(ck_shard* sh, const uint64_t* bases, uint32_t world);
 ck_status ck_shard_set_timeout(ck_shard* sh, uint64_t timeout_ns);

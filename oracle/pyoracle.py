@@ -24,6 +24,7 @@ HERE = Path(__file__).resolve().parent
 REF_DIR = HERE / "_ref"
 ORACLE_SO = REF_DIR / "libck32_oracle.so"
 REF_SO = REF_DIR / "libckks32_ref_driver.so"
+REF_SO_NDEBUG = REF_DIR / "libckks32_ref_nd_driver.so"
 
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
@@ -252,10 +253,15 @@ class Reference:
 
     available = REF_SO.exists()
 
-    def __init__(self):
-        if not REF_SO.exists():
-            raise FileNotFoundError(f"{REF_SO} not built (make -C oracle ref needs /root/reference)")
-        lib = ctypes.CDLL(str(REF_SO))
+    def __init__(self, ndebug: bool = False):
+        """ndebug=False: the reference as shipped (-O3, asserts live,
+        proj/CMakeLists.txt:10); ndebug=True: the same sources with -DNDEBUG
+        (make -C oracle ref-ndebug)."""
+        so = REF_SO_NDEBUG if ndebug else REF_SO
+        if not so.exists():
+            raise FileNotFoundError(f"{so} not built (make -C oracle ref{'-ndebug' if ndebug else ''} "
+                                    f"needs /root/reference)")
+        lib = ctypes.CDLL(str(so))
         lib.ref_last_error.restype = ctypes.c_char_p
         lib.ref_basis.argtypes = [ctypes.c_uint32] * 4 + [_u32p]
         lib.ref_twiddles.argtypes = [ctypes.c_uint32] * 5 + [_u32p, _u32p, _u32p]

@@ -992,10 +992,15 @@ struct Context {
     a.v_bs = 2ull * (level + alpha) * n;
     a.primes = d_primes;
     {
-      // row pass (4N B per extension row) + KeyMult traffic
+      // Per ciphertext: the row pass reads the extension rows' column-pass
+      // output (4N B per row; its result never leaves the SM), KeyMult reads
+      // the digits' own rows in place from d (4N B x level) and writes v0, v1
+      // (2 (level + alpha) rows), the fold reads d0, d1 (2 level rows).  The
+      // key (2D (level + alpha) rows) is shared by the whole batch: counted
+      // once per launch.
       ProfScope ps(this, 8,
-                   4.0 * n * pl.ntt_rows * B + 4.0 * n * (level + alpha) * (2.0 * pl.D + 2) * B +
-                       (fold ? 8.0 * n * level * B : 0.0),
+                   4.0 * n * B * (pl.ntt_rows + level + 2.0 * (level + alpha)) + (fold ? 8.0 * n * level * B : 0.0) +
+                       4.0 * n * 2.0 * pl.D * (level + alpha),
                    1, st);
       row_keymult(a, d_tw2f, st);
     }
@@ -1027,9 +1032,14 @@ struct Context {
     a.v = v;
     a.v_bs = 2ull * (level + alpha) * n;
     a.primes = d_primes;
-    // reads: D operand rows + 2D key rows per output row (+ d0, d1 for folded Q rows); writes v0, v1
-    ProfScope ps(this, 3, 4.0 * n * (level + alpha) * (3.0 * a.D + 2) * B + (fold ? 8.0 * n * level * B : 0.0), 1,
-                 st);
+    // per ciphertext: D operand rows per output row (extension rows + the
+    // digits' own rows read in place), writes v0, v1 (+ d0, d1 for the folded
+    // Q rows); the key's 2D rows per output row are read once per launch
+    // (one key for the whole batch)
+    ProfScope ps(this, 3,
+                 4.0 * n * (level + alpha) * (a.D + 2.0) * B + (fold ? 8.0 * n * level * B : 0.0) +
+                     4.0 * n * (level + alpha) * 2.0 * a.D,
+                 1, st);
     key_mult((int)n, a, st);
     ++launches;
     counters[4] += (uint64_t)B * a.D;
@@ -1379,6 +1389,13 @@ struct Shard {
     up_tab.add(ut);
     up_tab.upload();
     down_tab.clear();
+    // A fresh peer set restarts the epochs, so the flag words and the error
+    // word must restart too: stale flags from an earlier peer set would
+    // satisfy the next wait at once (and let BConv read rows that are not
+    // written yet).  Callers barrier after set_peers, so no peer publishes
+    // into this buffer before the reset has landed.
+    CK_CUDA(cudaMemset(static_cast<char*>(xbuf) + flag_off(0, 0), 0, 2ull * G * 4 + 4));
+    CK_CUDA(cudaDeviceSynchronize());
     epoch[0] = epoch[1] = 0;
   }
   bool peer_mode() const { return !peers.empty(); }
@@ -1470,6 +1487,7 @@ struct Shard {
     a.p_mont = c->d_pmont;
     a.v = v;
     a.primes = c->d_primes;
+    a.err = recv ? nullptr : err_word();
     {
       Context::ProfScope ps(c, 3, 4.0 * N * pl.rows * (3.0 * pl.D + 2), 1, st);
       shard_key_mult((int)N, a, st);
@@ -1534,6 +1552,7 @@ struct Shard {
       a.out = out;
       a.out_ps = (uint64_t)pl.lqo * N;
       a.primes = c->d_primes;
+      a.err = recv ? nullptr : err_word();
       {
         Context::ProfScope ps(c, 5, 4.0 * N * pl.lqo * (add ? 7 : 6), 1, st);
         shard_tail((int)N, (int)pl.lqo, a, st);

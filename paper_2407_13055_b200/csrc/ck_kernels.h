@@ -204,6 +204,7 @@ struct ShardKeyMultLaunch {
   const uint32_t* p_mont = nullptr;
   uint32_t* v = nullptr;           // [2][rows][n]
   const PrimeDev* primes = nullptr;
+  const uint32_t* err = nullptr;   // peer exchange error word: when set, v is poisoned (0xFFFFFFFF)
 };
 void shard_key_mult(int n, const ShardKeyMultLaunch& a, cudaStream_t st);
 struct ShardTailLaunch {
@@ -220,6 +221,7 @@ struct ShardTailLaunch {
   uint32_t* out = nullptr;
   uint64_t out_ps = 0;
   const PrimeDev* primes = nullptr;
+  const uint32_t* err = nullptr;   // peer exchange error word: when set, out is poisoned (0xFFFFFFFF)
 };
 void shard_tail(int n, int rows, const ShardTailLaunch& a, cudaStream_t st);
 // peer exchange handshake (shard.cu): signal stores `epoch` (release, system

@@ -12,6 +12,9 @@ namespace ck {
 namespace {
 
 constexpr int kST = 256;
+// Written instead of results when the peer exchange's error word is set: not a
+// canonical residue of any prime (all q < 2^29), so it cannot pass for one.
+constexpr uint32_t kPoison = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint4 ld4(const uint32_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ void st4(uint32_t* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
@@ -71,6 +74,9 @@ __global__ void __launch_bounds__(kST) k_shard_key_mult(ShardKeyMultLaunch a, in
   r1.y = sub_if(mont_reduce64(s1[1], P.q, P.qinv_neg), P.q);
   r1.z = sub_if(mont_reduce64(s1[2], P.q, P.qinv_neg), P.q);
   r1.w = sub_if(mont_reduce64(s1[3], P.q, P.qinv_neg), P.q);
+  if (a.err && *(volatile const uint32_t*)a.err) {  // a peer never arrived: poison, never silently wrong
+    r0 = r1 = make_uint4(kPoison, kPoison, kPoison, kPoison);
+  }
   st4(a.v + (size_t)r * n + xo, r0);
   st4(a.v + (size_t)(a.rows + r) * n + xo, r1);
 }
@@ -87,6 +93,7 @@ __global__ void __launch_bounds__(kST) k_shard_tail(ShardTailLaunch a, int n) {
   const uint32_t vv = a.v[(size_t)c * a.v_ps + e], oo = a.o[(size_t)c * a.o_ps + e];
   uint32_t x = sub_if(mont_mul(vv - oo + P.q, a.dinv[r], P.q, P.qinv_neg), P.q);
   if (a.add && (a.add_mask >> c & 1)) x = sub_if(x + a.add[(size_t)c * a.add_ps + e], P.q);
+  if (a.err && *(volatile const uint32_t*)a.err) x = kPoison;  // peer exchange timed out
   a.out[(size_t)c * a.out_ps + (size_t)r * n + j] = x;
 }
 

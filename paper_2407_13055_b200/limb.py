@@ -320,6 +320,16 @@ class LimbShardedEvaluator:
         self.peer = bool(getattr(exchange, "peer", False))
         self.lazy_rescale = lazy_rescale
 
+    def synchronize(self) -> None:
+        """Sync point: wait for the device, then raise if a peer exchange
+        timed out.  (A timed-out phase 2 never yields silently wrong rows: the
+        shard KeyMult / tail kernels write 0xFFFFFFFF, not a residue, when the
+        error word is set -- but only this check turns it into an exception.)"""
+        torch.cuda.synchronize(self.backends[0].ctx.device)
+        errs = self.x.errors() if hasattr(self.x, "errors") else []
+        if any(errs):
+            raise RuntimeError(f"limb-sharded peer exchange timed out (error words {errs}); outputs are poisoned")
+
     def _gather(self, sends):
         if self.peer:  # the rows stay in the peers' exchange buffers
             return [None] * len(sends)

@@ -45,3 +45,58 @@ def test_device_line_contract():
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert "int_pipe" in d["roofline_ntt"]
+
+
+def _row_keymult_bytes(n, level, alpha, batch, fold):
+    """Algorithmic bytes of one fused NTT-row-pass + KeyMult launch group
+    (ck_context.cu mod_up_key_mult): per ciphertext the extension rows'
+    column-pass output, the digits' own rows, v0 / v1 (+ d0 / d1 for the
+    fold); the key's 2D (level + alpha) rows ONCE per launch."""
+    D = -(-level // alpha)
+    ntt_rows = sum(level + alpha - min(alpha, level - k * alpha) for k in range(D))
+    per_ct = ntt_rows + level + 2 * (level + alpha) + (2 * level if fold else 0)
+    return 4 * n * (batch * per_ct + 2 * D * (level + alpha))
+
+
+def test_roofline_bytes_agree_with_ncu_dram_traffic():
+    """The headline roofline's algorithmic bytes for the dominant kernel must
+    be what the kernel actually has to move: ncu's DRAM read+write for the
+    same launch lands within [0.9, 1.15] of them (round 1 counted the key once
+    per ciphertext and the ratio was 0.61)."""
+    t = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["ntt_row+keymult"]
+    algo = _row_keymult_bytes(1 << 16, 24, 8, 16, fold=True)
+    assert algo == t["algorithmic_bytes"]
+    assert 0.9 <= t["ncu_dram_bytes"] / algo <= 1.15
+
+
+@pytest.mark.gpu
+def test_profile_bytes_follow_formula():
+    """ck_profile's bytes for the fused row pass + KeyMult class equal the
+    formula above (HMult folds d0 / d1, HRot does not)."""
+    import torch
+    from fractions import Fraction
+    from paper_2407_13055_b200 import ckks
+
+    n, l, a, B = 1 << 16, 24, 8, 4
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=55), device=0)
+    q = torch.tensor(C.primes.astype("int64"), device="cuda")
+
+    def rows(prefix, idx):
+        u = torch.randint(0, 1 << 62, (*prefix, len(idx), n), device="cuda", dtype=torch.int64)
+        return (u % q[idx].view(*([1] * len(prefix)), -1, 1)).to(torch.int32).contiguous()
+
+    full = list(range(l + a))
+    key = rows((3, 2), full)
+    X = ckks.Ciphertext(rows((B, 2), list(range(l))), Fraction(1 << 55), l)
+    for op, fold in (("hmult", True), ("hrot", False)):
+        C.profile(True)
+        if op == "hmult":
+            ckks.hmult(C, X, X, ckks.EvaluationKey(key))
+        else:
+            ckks.hrot(C, X, 1, ckks.EvaluationKey(key, ckks.ROTATION, 1))
+        prof = {p["name"]: p for p in C.profile_read()}
+        C.profile(False)
+        got = prof["ntt_row+keymult"]
+        assert got["groups"] == 1
+        assert got["bytes"] == _row_keymult_bytes(n, l, a, B, fold), op
+    C.close()

@@ -242,9 +242,43 @@ def test_gpu_peer_exchange_rejects_bad_tables_and_times_out():
     d = torch.zeros((shards[0].layout.lq(8), 1024), dtype=torch.int32, device=C.device)
     shards[0].modup_begin(8, d, peer=True)  # rank 1 never runs phase 1
     key = shards[0].layout.split_key(torch.zeros((3, 2, 11, 1024), dtype=torch.int32, device=C.device))
+    v = shards[0].modup_keymult(8, None, d, key)
+    torch.cuda.synchronize()
+    assert shards[0].peer_error() == 1
+    # the consumer never hands out silently wrong rows: every output word is poison
+    assert bool((v == -1).all())
+    from paper_2407_13055_b200.limb import LimbShardedEvaluator, LocalPeerExchange
+
+    class _Exch:
+        peer = True
+
+        def errors(self):
+            return [s.peer_error() for s in shards]
+
+    with pytest.raises(RuntimeError, match="timed out"):
+        LimbShardedEvaluator(shards, _Exch()).synchronize()
+    # a fresh peer set clears the flag and error words (stale epochs must not
+    # satisfy the next wait): rank 1 publishes epoch 1, then the peers are set
+    # again; rank 0's wait for epoch 1 must time out again instead of passing
+    for s in shards:
+        s.set_peers(bases)
+    assert shards[0].peer_error() == 0
+    shards[1].modup_begin(8, d, peer=True)
+    torch.cuda.synchronize()
+    for s in shards:
+        s.set_peers(bases)
+    shards[0].set_timeout(0.05)
+    shards[0].modup_begin(8, d, peer=True)
     shards[0].modup_keymult(8, None, d, key)
     torch.cuda.synchronize()
     assert shards[0].peer_error() == 1
+    ev = LimbShardedEvaluator(shards, LocalPeerExchange(shards))  # both ranks present: clean
+    for s in shards:
+        s.set_timeout(10.0)
+    x = [torch.zeros((2, s.layout.lq(8), 1024), dtype=torch.int32, device=C.device) for s in shards]
+    ev.key_switch(8, [xi[1].contiguous() for xi in x], [key, shards[1].layout.split_key(
+        torch.zeros((3, 2, 11, 1024), dtype=torch.int32, device=C.device))])
+    ev.synchronize()
     for s in shards:
         s.close()
     C.close()
