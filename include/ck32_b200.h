@@ -68,6 +68,8 @@ ck_status ck_context_destroy(ck_context* ctx);
 /* generate_basis (rns.cpp:63-117) on the host only: l Q primes then alpha P
  * primes, identical to the reference's deterministic choice. */
 ck_status ck_generate_basis(uint32_t n, uint32_t l, uint32_t alpha, uint32_t delta_bits, uint32_t* primes_out);
+/* the parameters the context was created with (CkksParams subset) */
+ck_status ck_context_params(const ck_context* ctx, ck_params* out);
 /* RnsBasis q_primes then p_primes (rns.hpp:23-40) */
 ck_status ck_context_primes(const ck_context* ctx, uint32_t* primes_out);
 /* OpCounters (ckks.hpp:34-44): modup, moddown, ntt, intt, keymult, bconv, rescale */
@@ -106,6 +108,29 @@ ck_status ck_mod_switch(ck_context* ctx, const uint32_t* src_dev, uint32_t src_c
                         uint32_t* dst_dev, uint32_t dst_q, uint32_t dst_p, ck_stream stream);
 ck_status ck_automorphism(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t rows, int64_t r,
                           ck_stream stream);
+/* apply_automorphism (automorphism.cpp:76-100) for any Galois element
+ * (AutomorphismMap::rotation: 5^-r mod 2n; ::conjugation: 2n-1), evaluation
+ * domain (bit-reversed column gather) or coefficient domain (coeff_domain = 1:
+ * a(X) -> a(X^(g^-1)) with the negacyclic sign flips, canonical negation),
+ * over a polynomial of q_rows Q-prefix rows then p_rows P rows. */
+ck_status ck_automorphism_galois(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t q_rows,
+                                 uint32_t p_rows, uint64_t galois, int coeff_domain, ck_stream stream);
+/* ew_add / ew_sub / ew_mul (op 0 / 1 / 2, poly.cpp:121-164) over a polynomial
+ * of q_rows Q-prefix rows then p_rows P rows (P-extended operands as the
+ * reference accepts them); out may alias a or b (ew_add_inplace /
+ * ew_sub_inplace, poly.cpp:182-205). */
+ck_status ck_ew_binary(ck_context* ctx, int op, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t q_rows,
+                       uint32_t p_rows, ck_stream stream);
+/* ew_mul_const (poly.hpp:127-128): row i times consts_mont[i] (host array of
+ * q_rows + p_rows canonical Montgomery constants); out may alias a. */
+ck_status ck_ew_mul_const(ck_context* ctx, const uint32_t* a, const uint32_t* consts_mont, uint32_t* out,
+                          uint32_t q_rows, uint32_t p_rows, ck_stream stream);
+/* bconv_part2 (bconv.cpp:96-174) with the caller's BConvTable::c (centred
+ * Montgomery constants, [dst_count][src_count], bconv.hpp:20-22) instead of
+ * the library's own table: src canonical (coefficient domain) rows. */
+ck_status ck_bconv_table(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,
+                         uint32_t* dst_dev, uint32_t dst_count, const uint32_t* dst_gidx, const int32_t* c_centered,
+                         ck_stream stream);
 /* ew_add / ew_sub / ew_mul over Q-prefix rows (poly.cpp:146-164) */
 ck_status ck_ew_add(ck_context* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t rows,
                     ck_stream stream);
@@ -193,6 +218,38 @@ ck_status ck_evk_digit(ck_context* ctx, const uint32_t* s_src, const uint32_t* s
  * rows [level + p_rows][n], each reduced mod its prime then forward NTT. */
 ck_status ck_coeffs_to_eval(ck_context* ctx, const int64_t* coeffs, uint32_t level, uint32_t p_rows, uint32_t* out,
                             ck_stream stream);
+
+/* ---- wire formats, byte-compatible with the reference --
+ * Blobs live in host memory; rows move directly between device memory and the
+ * blob (device rows are canonical, exactly what the reference writes).
+ * Writers: out == NULL only reports the length in *len; otherwise cap must
+ * cover it.  Readers validate like the reference (magic, version, ring degree,
+ * basis hash, truncation: CK_RUNTIME_ERROR for polynomial / basis blobs,
+ * CK_INVALID_ARGUMENT for ciphertext / key headers) and additionally reject
+ * residues >= q (the device only holds canonical values).  A ciphertext's
+ * scale is its reduced Rational as two big-endian magnitudes (export_bits
+ * order), numerator then denominator. */
+/* serialize_basis / deserialize_basis (rns.cpp:188-216) */
+ck_status ck_serialize_basis(const ck_context* ctx, uint8_t* out, size_t cap, size_t* len);
+ck_status ck_deserialize_basis(const uint8_t* in, size_t len, ck_params* params, uint32_t* primes, uint32_t cap);
+/* serialize_poly / deserialize_poly (poly.cpp:297-352); meta = {q_count, p_count, domain, mont} */
+ck_status ck_serialize_poly(ck_context* ctx, const uint32_t* rows_dev, uint32_t q_count, uint32_t p_count, int domain,
+                            int mont, uint8_t* out, size_t cap, size_t* len, ck_stream stream);
+ck_status ck_deserialize_poly(ck_context* ctx, const uint8_t* in, size_t len, uint32_t* rows_dev, uint32_t cap_rows,
+                              uint32_t meta[4], ck_stream stream);
+/* serialize_ciphertext / deserialize_ciphertext (ckks.cpp:1092-1121): ct [2][level] */
+ck_status ck_serialize_ciphertext(ck_context* ctx, const uint32_t* ct_dev, uint32_t level, int pending_rescale,
+                                  const uint8_t* scale_num, size_t num_len, const uint8_t* scale_den, size_t den_len,
+                                  uint8_t* out, size_t cap, size_t* len, ck_stream stream);
+ck_status ck_deserialize_ciphertext(ck_context* ctx, const uint8_t* in, size_t len, uint32_t* ct_dev,
+                                    uint32_t cap_level, uint32_t* level, int* pending_rescale, uint8_t* scale_num,
+                                    size_t num_cap, size_t* num_len, uint8_t* scale_den, size_t den_cap,
+                                    size_t* den_len, ck_stream stream);
+/* serialize_evk / deserialize_evk (ckks.cpp:1123-1154): evk [D][2][L+alpha] */
+ck_status ck_serialize_evk(ck_context* ctx, const uint32_t* evk_dev, uint32_t digits, int kind, int64_t rotation,
+                           uint8_t* out, size_t cap, size_t* len, ck_stream stream);
+ck_status ck_deserialize_evk(ck_context* ctx, const uint8_t* in, size_t len, uint32_t* evk_dev, uint32_t cap_digits,
+                             int* kind, int64_t* rotation, uint32_t* digits, ck_stream stream);
 
 /* Number of this library's kernel launches issued since context creation
  * (evidence for bench.py's gpu_launches). */

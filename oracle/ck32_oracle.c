@@ -758,6 +758,54 @@ int cko_hmult(const cko_ctx* c, uint32_t level, const int32_t* xb, const int32_t
   return 0;
 }
 
+/* element-wise over a polynomial whose row i lives at global prime gidx[i]
+ * (Q-prefix then P rows, poly.hpp:103-106): op 0 ew_add, 1 ew_sub (narrow to
+ * (-q, q), poly.cpp:121-156), 2 ew_mul (Montgomery, poly.cpp:158-164),
+ * 3 ew_mul_const with one Montgomery constant per row (poly.cpp:166-180). */
+void cko_ew_rows(const cko_ctx* c, int op, uint32_t rows, const uint32_t* gidx, const int32_t* x, const int32_t* y,
+                 const uint32_t* consts, int32_t* o) {
+  for (uint32_t i = 0; i < rows; ++i) {
+    const ckp* P = &c->pc[gidx[i]];
+    for (uint32_t k = 0; k < c->n; ++k) {
+      const size_t e = (size_t)i * c->n + k;
+      if (op == 0) o[e] = narrow1((int64_t)x[e] + y[e], (int32_t)P->q);
+      else if (op == 1) o[e] = narrow1((int64_t)x[e] - y[e], (int32_t)P->q);
+      else if (op == 2) o[e] = mont_mul(x[e], y[e], P);
+      else o[e] = mont_mul(x[e], (int32_t)consts[i], P);
+    }
+  }
+}
+
+/* apply_automorphism for Galois element g with inverse gi (automorphism.cpp:
+ * 38-61, 76-100): evaluation domain o[j] = in[src(j)], src the inverse of
+ * dest(i) = brev(phi_g(brev(i))); coefficient domain: coefficient k goes to
+ * k gi mod 2n, negated past n. */
+void cko_automorphism(const cko_ctx* c, uint32_t rows, uint64_t g, uint64_t gi, int coeff, const int32_t* in,
+                      int32_t* o) {
+  const uint32_t n = c->n;
+  uint32_t bits = 0;
+  while ((1u << bits) < n) ++bits;
+  uint32_t* src = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t ph = (uint32_t)((((2ull * bit_reverse(i, bits) + 1) * g) % (2ull * n) - 1) / 2);
+    src[bit_reverse(ph, bits)] = i;
+  }
+  for (uint32_t r = 0; r < rows; ++r) {
+    const int32_t* a = in + (size_t)r * n;
+    int32_t* b = o + (size_t)r * n;
+    if (!coeff) {
+      for (uint32_t j = 0; j < n; ++j) b[j] = a[src[j]];
+    } else {
+      for (uint32_t k = 0; k < n; ++k) {
+        const uint64_t e = (uint64_t)k * gi % (2ull * n);
+        if (e < n) b[e] = a[k];
+        else b[e - n] = -a[k];
+      }
+    }
+  }
+  free(src);
+}
+
 /* -------------------------------------------------------- automorphism -- */
 void cko_rotation_src_map(uint32_t n, int64_t r, uint32_t* src) { /* automorphism.cpp:11-69 */
   uint32_t bits = 0;

@@ -80,6 +80,12 @@ void cko_rotation_src_map(uint32_t n, int64_t r, uint32_t* src);
 /* element-wise (poly.cpp:146-205, ckks.cpp:557-600) over `rows` Q-prefix rows */
 void cko_ew_add(const cko_ctx* c, uint32_t rows, const int32_t* x, const int32_t* y, int32_t* o);
 void cko_ew_mul(const cko_ctx* c, uint32_t rows, const int32_t* x, const int32_t* y, int32_t* o);
+/* element-wise over rows at global primes gidx[]: op 0 add, 1 sub, 2 mul, 3 mul_const (consts[rows]) */
+void cko_ew_rows(const cko_ctx* c, int op, uint32_t rows, const uint32_t* gidx, const int32_t* x, const int32_t* y,
+                 const uint32_t* consts, int32_t* o);
+/* apply_automorphism for Galois element g (inverse gi), evaluation or coefficient domain */
+void cko_automorphism(const cko_ctx* c, uint32_t rows, uint64_t g, uint64_t gi, int coeff, const int32_t* in,
+                      int32_t* o);
 /* hoisted_rotate_accumulate (ckks.cpp:945-1012); pts are P-extended (level+alpha rows);
  * evks[i] ignored when rots[i]==0 */
 int cko_hoisted_accumulate(const cko_ctx* c, uint32_t level, const int32_t* b, const int32_t* a, uint32_t count,

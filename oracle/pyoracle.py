@@ -70,6 +70,9 @@ def _oracle_lib():
         lib.cko_rotation_src_map.argtypes = [ctypes.c_uint32, ctypes.c_int64, _u32p]
         lib.cko_ew_add.argtypes = [_vp, ctypes.c_uint32, _i32p, _i32p, _i32p]
         lib.cko_ew_mul.argtypes = [_vp, ctypes.c_uint32, _i32p, _i32p, _i32p]
+        lib.cko_ew_rows.argtypes = [_vp, ctypes.c_int, ctypes.c_uint32, _u32p, _i32p, _i32p, _vp, _i32p]
+        lib.cko_automorphism.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, _i32p,
+                                         _i32p]
         lib.cko_hoisted_accumulate.argtypes = [_vp, ctypes.c_uint32, _i32p, _i32p, ctypes.c_uint32,
                                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_vp),
                                                ctypes.POINTER(_vp), _i32p, _i32p]
@@ -241,6 +244,24 @@ class Oracle:
         c = lambda x: np.ascontiguousarray(x, np.int32)
         self.lib.cko_hoisted_accumulate(self._c, level, c(b), c(a), cnt, ra, pa, ea, ob, oa)
         return ob, oa
+
+    def ew(self, op: int, x: np.ndarray, y, gidx, consts=None) -> np.ndarray:
+        """ew_add/sub/mul/mul_const (op 0..3, poly.cpp:121-180) over rows at gidx."""
+        g = np.ascontiguousarray(gidx, np.uint32)
+        x = np.ascontiguousarray(x, np.int32)
+        y = np.ascontiguousarray(x if y is None else y, np.int32)
+        k = None if consts is None else np.ascontiguousarray(consts, np.uint32)
+        o = np.zeros_like(x)
+        self.lib.cko_ew_rows(self._c, op, len(g), g, x, y, None if k is None else k.ctypes.data, o)
+        return o
+
+    def automorphism(self, x: np.ndarray, galois: int, coeff: bool) -> np.ndarray:
+        """apply_automorphism (automorphism.cpp:76-100) for a Galois element."""
+        gi = pow(int(galois), -1, 2 * self.n)
+        x = np.ascontiguousarray(x, np.int32)
+        o = np.zeros_like(x)
+        self.lib.cko_automorphism(self._c, x.shape[0], int(galois), gi, int(coeff), x, o)
+        return o
 
     def rotation_src_map(self, r: int) -> np.ndarray:
         out = np.zeros(self.n, np.uint32)

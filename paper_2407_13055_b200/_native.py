@@ -56,6 +56,10 @@ _SIGS = {
     "ck_bconv": [_vp, _vp, _u32, _u32p, _vp, _u32, _u32p, _vp],
     "ck_mod_switch": [_vp, _vp, _u32, _u32p, _vp, _u32, _u32, _vp],
     "ck_automorphism": [_vp, _vp, _vp, _u32, _i64, _vp],
+    "ck_automorphism_galois": [_vp, _vp, _vp, _u32, _u32, ctypes.c_uint64, ctypes.c_int, _vp],
+    "ck_ew_binary": [_vp, ctypes.c_int, _vp, _vp, _vp, _u32, _u32, _vp],
+    "ck_ew_mul_const": [_vp, _vp, _u32p, _vp, _u32, _u32, _vp],
+    "ck_bconv_table": [_vp, _vp, _u32, _u32p, _vp, _u32, _u32p, ctypes.POINTER(ctypes.c_int32), _vp],
     "ck_ew_add": [_vp, _vp, _vp, _vp, _u32, _vp],
     "ck_ew_sub": [_vp, _vp, _vp, _vp, _u32, _vp],
     "ck_ew_mul": [_vp, _vp, _vp, _vp, _u32, _vp],
@@ -100,6 +104,21 @@ _SIGS = {
     "ck_ipc_get_handle": [_vp, ctypes.POINTER(ctypes.c_ubyte)],
     "ck_ipc_open_handle": [ctypes.POINTER(ctypes.c_ubyte), ctypes.POINTER(_vp)],
     "ck_ipc_close": [_vp],
+    "ck_context_params": [_vp, ctypes.POINTER(ck_params)],
+    "ck_serialize_basis": [_vp, _vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
+    "ck_deserialize_basis": [_vp, ctypes.c_size_t, ctypes.POINTER(ck_params), _u32p, _u32],
+    "ck_serialize_poly": [_vp, _vp, _u32, _u32, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t,
+                          ctypes.POINTER(ctypes.c_size_t), _vp],
+    "ck_deserialize_poly": [_vp, _vp, ctypes.c_size_t, _vp, _u32, _u32p, _vp],
+    "ck_serialize_ciphertext": [_vp, _vp, _u32, ctypes.c_int, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t, _vp,
+                                ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), _vp],
+    "ck_deserialize_ciphertext": [_vp, _vp, ctypes.c_size_t, _vp, _u32, _u32p, ctypes.POINTER(ctypes.c_int), _vp,
+                                  ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), _vp, ctypes.c_size_t,
+                                  ctypes.POINTER(ctypes.c_size_t), _vp],
+    "ck_serialize_evk": [_vp, _vp, _u32, ctypes.c_int, _i64, _vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t),
+                         _vp],
+    "ck_deserialize_evk": [_vp, _vp, ctypes.c_size_t, _vp, _u32, ctypes.POINTER(ctypes.c_int),
+                           ctypes.POINTER(_i64), _u32p, _vp],
 }
 EXPORTS = sorted(list(_SIGS) + ["ck_last_error", "ck_version", "ck_launch_count"])
 

@@ -688,37 +688,144 @@ def mod_switch(ctx: CkksContext, a: Polynomial, src_gidx: Sequence[int], dst_q_c
     return Polynomial(out, dst_q_count, dst_p_count)
 
 
-def apply_automorphism(ctx: CkksContext, p: Polynomial, r: int) -> Polynomial:  # automorphism.cpp:76-100
-    if p.domain != EVALUATION:
-        raise ValueError("only the evaluation-domain gather is implemented on the GPU")
+def galois_for_rotation(n: int, r: int) -> int:
+    """5^-r mod 2n (automorphism.cpp:11-23)."""
+    return pow(5, (-r) % (n // 2), 2 * n)
+
+
+def apply_automorphism(ctx: CkksContext, p: Polynomial, r: int, galois: Optional[int] = None) -> Polynomial:
+    """apply_automorphism (automorphism.cpp:76-100): rotation by r slots
+    (AutomorphismMap::rotation) or, when ``galois`` is given, any Galois
+    element (conjugation = 2n - 1); evaluation-domain column gather or the
+    coefficient-domain signed permutation."""
     out = torch.empty_like(p.data)
-    nat.call("ck_automorphism", ctx.handle, _ptr(p.data), _ptr(out), p.rows, int(r), ctx.stream())
+    if galois is None and p.domain == EVALUATION:
+        nat.call("ck_automorphism", ctx.handle, _ptr(p.data), _ptr(out), p.rows, int(r), ctx.stream())
+    else:
+        g = galois_for_rotation(ctx.n, r) if galois is None else int(galois)
+        nat.call("ck_automorphism_galois", ctx.handle, _ptr(p.data), _ptr(out), p.q_count, p.p_count, g,
+                 int(p.domain == COEFFICIENT), ctx.stream())
     return Polynomial(out, p.q_count, p.p_count, p.domain, p.mont)
 
 
-def ew_add(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:
-    return _ew(ctx, "ck_ew_add", a, b, a.mont)
+EW_ADD, EW_SUB, EW_MUL = 0, 1, 2
 
 
-def ew_sub(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:
-    return _ew(ctx, "ck_ew_sub", a, b, a.mont)
+def ew_add(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:  # poly.cpp:146-150
+    return _ew(ctx, EW_ADD, a, b, a.mont)
 
 
-def ew_mul(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:
+def ew_sub(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:  # poly.cpp:152-156
+    return _ew(ctx, EW_SUB, a, b, a.mont)
+
+
+def ew_mul(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:  # poly.cpp:158-164
     if not a.mont or not b.mont:
         raise ValueError("ew_mul expects Montgomery-form operands")
-    return _ew(ctx, "ck_ew_mul", a, b, True)
+    return _ew(ctx, EW_MUL, a, b, True)
 
 
-def _ew(ctx, fn, a: Polynomial, b: Polynomial, mont_out: bool) -> Polynomial:  # poly.cpp:138-164
-    if a.q_count != b.q_count or a.p_count != b.p_count:
+def ew_add_inplace(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:  # poly.cpp:182-192
+    return _ew(ctx, EW_ADD, a, b, a.mont, out=a)
+
+
+def ew_sub_inplace(ctx: CkksContext, a: Polynomial, b: Polynomial) -> Polynomial:  # poly.cpp:194-205
+    return _ew(ctx, EW_SUB, a, b, a.mont, out=a)
+
+
+def ew_mul_const(ctx: CkksContext, a: Polynomial, consts_mont: Sequence[int]) -> Polynomial:  # poly.cpp:166-180
+    if len(consts_mont) != a.rows:
+        raise ValueError("constant count mismatch")
+    out = torch.empty_like(a.data)
+    nat.call("ck_ew_mul_const", ctx.handle, _ptr(a.data), nat.u32_array([int(c) for c in consts_mont]), _ptr(out),
+             a.q_count, a.p_count, ctx.stream())
+    return Polynomial(out, a.q_count, a.p_count, a.domain, a.mont)
+
+
+def _ew(ctx, op, a: Polynomial, b: Polynomial, mont_out: bool, out: Optional[Polynomial] = None) -> Polynomial:
+    if a.q_count != b.q_count or a.p_count != b.p_count:  # check_binary, poly.cpp:115-119
         raise ValueError("basis prefix mismatch")
     if a.domain != b.domain:
         raise ValueError("domain mismatch")
     if a.mont != b.mont:
         raise ValueError("Montgomery flag mismatch")
-    if a.p_count:
-        raise ValueError("element-wise kernels take Q-prefix polynomials")
-    out = torch.empty_like(a.data)
-    nat.call(fn, ctx.handle, _ptr(a.data), _ptr(b.data), _ptr(out), a.rows, ctx.stream())
-    return Polynomial(out, a.q_count, a.p_count, a.domain, mont_out)
+    if out is not None:
+        nat.call("ck_ew_binary", ctx.handle, op, _ptr(a.data), _ptr(b.data), _ptr(out.data), a.q_count, a.p_count,
+                 ctx.stream())
+        return out
+    o = torch.empty_like(a.data)
+    nat.call("ck_ew_binary", ctx.handle, op, _ptr(a.data), _ptr(b.data), _ptr(o), a.q_count, a.p_count, ctx.stream())
+    return Polynomial(o, a.q_count, a.p_count, a.domain, mont_out)
+
+
+# ------------------------------------------------------------ wire formats --
+# Byte-compatible with the reference's serialisers (ckks.cpp:1090-1154,
+# poly.cpp:295-352, rns.cpp:168-216) through the C ABI: rows go straight
+# between device memory and the blob.
+def _blob(fn, args, stream=None) -> bytes:
+    """Call a ck_serialize_* writer twice: length query (out = NULL), then fill."""
+    tail = [] if stream is None else [stream]
+    n = ctypes.c_size_t()
+    nat.call(fn, *args, None, 0, ctypes.byref(n), *tail)
+    buf = ctypes.create_string_buffer(max(1, n.value))
+    nat.call(fn, *args, buf, n.value, ctypes.byref(n), *tail)
+    return buf.raw[: n.value]
+
+
+def _be(v: int) -> bytes:
+    return v.to_bytes(max(1, (v.bit_length() + 7) // 8), "big")
+
+
+def serialize_basis(ctx: CkksContext) -> bytes:  # rns.cpp:188-199
+    return _blob("ck_serialize_basis", [ctx.handle])
+
+
+def serialize_poly(ctx: CkksContext, p: Polynomial) -> bytes:  # poly.cpp:297-320
+    return _blob("ck_serialize_poly", [ctx.handle, _ptr(p.data.contiguous()), p.q_count, p.p_count,
+                                       int(p.domain == EVALUATION), int(p.mont)], ctx.stream())
+
+
+def deserialize_poly(ctx: CkksContext, blob: bytes) -> Polynomial:  # poly.cpp:322-352
+    out = ctx.empty(ctx.params.l + ctx.params.alpha, ctx.n)
+    meta = (ctypes.c_uint32 * 4)()
+    nat.call("ck_deserialize_poly", ctx.handle, blob, len(blob), _ptr(out), out.shape[0], meta, ctx.stream())
+    qc, pc, dom, mont = list(meta)
+    return Polynomial(out[: qc + pc].clone(), qc, pc, EVALUATION if dom else COEFFICIENT, bool(mont))
+
+
+def serialize_ciphertext(ctx: CkksContext, ct: Ciphertext) -> bytes:  # ckks.cpp:1092-1105
+    if ct.batched:
+        raise ValueError("serialize one ciphertext at a time")
+    s = Fraction(ct.scale)
+    num, den = _be(s.numerator), _be(s.denominator)
+    return _blob("ck_serialize_ciphertext", [ctx.handle, _ptr(ct.data.contiguous()), ct.level,
+                                             int(ct.pending_rescale), num, len(num), den, len(den)], ctx.stream())
+
+
+def deserialize_ciphertext(ctx: CkksContext, blob: bytes) -> Ciphertext:  # ckks.cpp:1107-1121
+    out = ctx.empty(2, ctx.params.l, ctx.n)
+    lv, pend = ctypes.c_uint32(), ctypes.c_int()
+    nb, db = ctypes.create_string_buffer(len(blob)), ctypes.create_string_buffer(len(blob))
+    nl, dl = ctypes.c_size_t(), ctypes.c_size_t()
+    flat = out.view(-1)
+    nat.call("ck_deserialize_ciphertext", ctx.handle, blob, len(blob), _ptr(flat), ctx.params.l, ctypes.byref(lv),
+             ctypes.byref(pend), nb, len(blob), ctypes.byref(nl), db, len(blob), ctypes.byref(dl), ctx.stream())
+    level = lv.value
+    data = flat[: 2 * level * ctx.n].view(2, level, ctx.n).clone()
+    scale = Fraction(int.from_bytes(nb.raw[: nl.value], "big"), int.from_bytes(db.raw[: dl.value], "big"))
+    return Ciphertext(data, scale, level, bool(pend.value))
+
+
+def serialize_evk(ctx: CkksContext, evk: "EvaluationKey") -> bytes:  # ckks.cpp:1123-1137
+    D = evk.data.shape[0]
+    return _blob("ck_serialize_evk", [ctx.handle, _ptr(evk.data.contiguous()), D, 0 if evk.kind == RELIN else 1,
+                                      int(evk.rotation)], ctx.stream())
+
+
+def deserialize_evk(ctx: CkksContext, blob: bytes) -> "EvaluationKey":  # ckks.cpp:1139-1154
+    D = ctx.num_digits(ctx.params.l)
+    out = ctx.empty(D, 2, ctx.params.l + ctx.params.alpha, ctx.n)
+    kind, rot, d = ctypes.c_int(), ctypes.c_int64(), ctypes.c_uint32()
+    nat.call("ck_deserialize_evk", ctx.handle, blob, len(blob), _ptr(out), D, ctypes.byref(kind), ctypes.byref(rot),
+             ctypes.byref(d), ctx.stream())
+    return EvaluationKey(out[: d.value].contiguous(), RELIN if kind.value == 0 else ROTATION, rot.value)

@@ -41,8 +41,11 @@ struct NvtxRange {
 
 namespace ck {
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
+// the message ck_last_error() returns, for ABI entry points in other files (wire.cpp)
+void set_last_error(const char* msg) { g_err = msg; }
+namespace {
 
 struct InvalidArgument : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
@@ -337,6 +340,21 @@ struct Context {
   std::map<std::string, std::unique_ptr<NttPlan>> adhoc_ntt;
   std::map<std::string, std::unique_ptr<BconvPlan>> adhoc_bc;
   std::map<uint32_t, std::unique_ptr<Blob>> row_primes;  // (level+alpha)-row prime maps
+  std::map<std::pair<uint32_t, uint32_t>, std::unique_ptr<Blob>> poly_maps;  // (q_rows, p_rows) -> row prime map
+  // row -> global prime of a Polynomial with q_rows Q-prefix rows then p_rows
+  // P rows (poly.hpp:103-106), cached on the device
+  const uint16_t* poly_row_primes(uint32_t q_rows, uint32_t p_rows) {
+    if (q_rows > L || p_rows > alpha || q_rows + p_rows == 0) throw InvalidArgument("rows exceed the basis");
+    auto& b = poly_maps[{q_rows, p_rows}];
+    if (!b) {
+      std::vector<uint16_t> rp(q_rows + p_rows);
+      for (uint32_t i = 0; i < q_rows + p_rows; ++i) rp[i] = (uint16_t)(i < q_rows ? i : L + (i - q_rows));
+      b = std::make_unique<Blob>();
+      b->add(rp);
+      b->upload();
+    }
+    return b->at<uint16_t>(0);
+  }
   struct Scratch {
     void* ptr = nullptr;
     size_t bytes = 0;
@@ -493,7 +511,10 @@ struct Context {
 
   uint32_t q(uint32_t g) const { return primes[g]; }
   uint32_t gidx(uint32_t level, uint32_t row) const { return row < level ? row : L + (row - level); }
-  uint32_t digits(uint32_t level) const { return (level + alpha - 1) / alpha; }
+  uint32_t digits(uint32_t level) const {
+    if (alpha == 0) throw InvalidArgument("key switching needs P primes (alpha = 0)");
+    return (level + alpha - 1) / alpha;
+  }
   size_t rowsz() const { return (size_t)n; }
 
   void* scratch_get(size_t bytes, cudaStream_t st) {
@@ -1668,8 +1689,12 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     const ck_params& p = *params;
     if (p.n < 8 || (p.n & (p.n - 1)) != 0 || p.n > (1u << 17))
       throw InvalidArgument("ring degree must be a power of two in [8, 2^17]");
-    if (p.l < 2 || p.l % 2 != 0) throw InvalidArgument("level count must be even and >= 2");
-    if (p.alpha < 1) throw InvalidArgument("alpha must be positive");
+    // generate_basis needs an even l (double-prime pairs) and alpha >= 1; a
+    // caller-supplied basis may be any shape the reference accepts (e.g. the
+    // kernel-level tests' generate_basis(n, 2, 0, ...)): mechanisms that need
+    // P primes check alpha when they run.
+    if (p.l < 1 || (!primes && (p.l % 2 != 0 || p.alpha < 1)))
+      throw InvalidArgument("level count must be even and >= 2, alpha >= 1");
     if (p.l + p.alpha > (uint32_t)kMaxRows) throw InvalidArgument("too many primes");
     auto c = std::make_unique<Context>();
     c->p = p;
@@ -1800,6 +1825,13 @@ ck_status ck_generate_basis(uint32_t n, uint32_t l, uint32_t alpha, uint32_t del
 
 ck_status ck_context_destroy(ck_context* ctx) {
   return guard([&] { delete C(ctx); });
+}
+
+ck_status ck_context_params(const ck_context* ctx, ck_params* out) {
+  return guard([&] {
+    if (!ctx || !out) throw InvalidArgument("null argument");
+    *out = reinterpret_cast<const Context*>(ctx)->p;
+  });
 }
 
 ck_status ck_context_primes(const ck_context* ctx, uint32_t* out) {
@@ -2093,7 +2125,7 @@ ck_status ck_mod_switch(ck_context* ctx, const uint32_t* src_dev, uint32_t src_c
 ck_status ck_automorphism(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t rows, int64_t r,
                           ck_stream stream) {
   return guard([&] {
-    CK_RANGE("ck_mod_switch");
+    CK_RANGE("ck_automorphism");
     Context* c = C(ctx);
     check_ptr(in_dev);
     check_ptr(out_dev);
@@ -2101,6 +2133,128 @@ ck_status ck_automorphism(ck_context* ctx, const uint32_t* in_dev, uint32_t* out
     permute((int)c->n, (int)rows, 1, in_dev, 0, out_dev, 0, c->rotation_map(r), S(stream));
     ++c->launches;
     check_launch();
+  });
+}
+
+ck_status ck_automorphism_galois(ck_context* ctx, const uint32_t* in_dev, uint32_t* out_dev, uint32_t q_rows,
+                                 uint32_t p_rows, uint64_t galois, int coeff_domain, ck_stream stream) {
+  return guard([&] {
+    CK_RANGE("ck_automorphism_galois");
+    Context* c = C(ctx);
+    check_ptr(in_dev);
+    check_ptr(out_dev);
+    if (in_dev == out_dev) throw InvalidArgument("automorphism is out-of-place");
+    const uint64_t two_n = 2ull * c->n;
+    const uint64_t g = galois % two_n;
+    if ((g & 1) == 0) throw InvalidArgument("Galois element must be odd");
+    uint64_t gi = 1;  // g^-1 = g^(n-1) mod 2n: the unit group mod 2n has order n
+    for (uint64_t e = c->n - 1, b = g; e; e >>= 1, b = b * b % two_n)
+      if (e & 1) gi = gi * b % two_n;
+    if (gi * g % two_n != 1) throw InvalidArgument("Galois element not invertible");
+    automorphism_galois((int)c->n, (int)c->logn, (int)(q_rows + p_rows), (uint32_t)g, (uint32_t)gi, coeff_domain ? 1 : 0,
+                        in_dev, out_dev, c->poly_row_primes(q_rows, p_rows), c->d_primes, S(stream));
+    ++c->launches;
+    check_launch();
+  });
+}
+
+ck_status ck_ew_binary(ck_context* ctx, int op, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t q_rows,
+                       uint32_t p_rows, ck_stream stream) {
+  return guard([&] {
+    CK_RANGE("ck_ew_binary");
+    Context* c = C(ctx);
+    check_ptr(a);
+    check_ptr(b);
+    check_ptr(out);
+    if (op < 0 || op > 2) throw InvalidArgument("element-wise op must be 0 (add), 1 (sub) or 2 (mul)");
+    elementwise((int)c->n, (int)(q_rows + p_rows), 1, op, a, 0, b, 0, out, 0, c->poly_row_primes(q_rows, p_rows),
+                c->d_primes, S(stream));
+    ++c->launches;
+    check_launch();
+  });
+}
+
+ck_status ck_ew_mul_const(ck_context* ctx, const uint32_t* a, const uint32_t* consts_mont, uint32_t* out,
+                          uint32_t q_rows, uint32_t p_rows, ck_stream stream) {
+  return guard([&] {
+    CK_RANGE("ck_ew_mul_const");
+    Context* c = C(ctx);
+    check_ptr(a);
+    check_ptr(out);
+    check_ptr(consts_mont);
+    const uint16_t* rp = c->poly_row_primes(q_rows, p_rows);
+    const uint32_t rows = q_rows + p_rows;
+    std::vector<uint32_t> k(rows);
+    for (uint32_t i = 0; i < rows; ++i) {
+      const uint32_t q = c->q(i < q_rows ? i : c->L + (i - q_rows));
+      k[i] = consts_mont[i] % q;  // canonical, poly.hpp:121-122
+    }
+    uint32_t* d = nullptr;  // stream-ordered: safe for concurrent calls on other streams
+    CK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), rows * 4, S(stream)));
+    CK_CUDA(cudaMemcpyAsync(d, k.data(), rows * 4, cudaMemcpyHostToDevice, S(stream)));
+    elementwise((int)c->n, (int)rows, 1, 3, a, 0, a, 0, out, 0, rp, c->d_primes, S(stream), 0, d);
+    CK_CUDA(cudaFreeAsync(d, S(stream)));  // (a pageable-source copy has staged k before returning)
+    ++c->launches;
+    check_launch();
+  });
+}
+
+ck_status ck_bconv_table(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,
+                         uint32_t* dst_dev, uint32_t dst_count, const uint32_t* dst_gidx, const int32_t* c_centered,
+                         ck_stream stream) {
+  return guard([&] {
+    CK_RANGE("ck_bconv_table");
+    Context* c = C(ctx);
+    check_ptr(src_dev);
+    check_ptr(dst_dev);
+    check_ptr(c_centered);
+    if (src_count == 0 || !src_gidx || !dst_gidx) throw InvalidArgument("empty conversion");
+    std::vector<uint32_t> sg(src_gidx, src_gidx + src_count), dg(dst_gidx, dst_gidx + dst_count);
+    for (uint32_t g : sg)
+      if (g >= c->primes.size()) throw InvalidArgument("prime index out of range");
+    for (uint32_t g : dg)
+      if (g >= c->primes.size()) throw InvalidArgument("prime index out of range");
+    c->check_bconv_width(sg);
+    // the caller's table (BConvTable::c, centred Montgomery constants,
+    // bconv.hpp:20-22) lifted to canonical [0, q_i): the same residue class,
+    // so the canonical outputs equal the reference's
+    std::vector<uint32_t> cmat((size_t)dst_count * src_count);
+    for (uint32_t i = 0; i < dst_count; ++i) {
+      const int64_t qi = c->q(dg[i]);
+      for (uint32_t j = 0; j < src_count; ++j) {
+        int64_t v = c_centered[(size_t)i * src_count + j] % qi;
+        if (v < 0) v += qi;
+        cmat[(size_t)i * src_count + j] = (uint32_t)v;
+      }
+    }
+    std::string key("T");
+    key.append(reinterpret_cast<const char*>(sg.data()), sg.size() * 4);
+    key.append(reinterpret_cast<const char*>(dg.data()), dg.size() * 4);
+    key.append(reinterpret_cast<const char*>(cmat.data()), cmat.size() * 4);
+    auto& pl = c->adhoc_bc[key];
+    if (!pl) {
+      pl = std::make_unique<BconvPlan>();
+      std::vector<uint32_t> drow(dst_count);
+      std::vector<uint16_t> dprime(dst_count);
+      for (uint32_t i = 0; i < dst_count; ++i) {
+        drow[i] = i;
+        dprime[i] = (uint16_t)dg[i];
+      }
+      std::vector<BconvGroup> groups = {{0, src_count, dst_count, 0, 0}};
+      pl->groups_off = pl->blob.add(groups);
+      pl->cmat_off = pl->blob.add(cmat);
+      pl->row_off = pl->blob.add(drow);
+      pl->prime_off = pl->blob.add(dprime);
+      pl->ngroups = 1;
+      pl->max_sc = (int)src_count;
+      pl->src_rows = src_count;
+      pl->dst_rows = dst_count;
+      add_bconv_tc(*pl, groups, cmat, dprime, [&](uint32_t g) { return c->q(g); }, c->n);
+      pl->blob.upload();
+    }
+    c->run_bconv(*pl, 1, src_dev, 0, dst_dev, 0, S(stream));
+    check_launch();
+    c->counters[5] += 1;
   });
 }
 
@@ -2183,6 +2337,7 @@ ck_status ck_mod_down(ck_context* ctx, uint32_t level, const uint32_t* v, uint32
     check_level(c, level);
     check_ptr(v);
     check_ptr(out);
+    if (c->alpha == 0) throw InvalidArgument("key switching needs P primes (alpha = 0)");
     const SwitchPlan& pl = c->switch_plan(0, level, 1);
     uint32_t* ts = static_cast<uint32_t*>(c->scratch_get((size_t)pl.sc * c->n * 4, S(stream)));
     c->drop_divide(pl, 1, v, 0, ts, out, true, S(stream));

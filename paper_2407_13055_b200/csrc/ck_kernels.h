@@ -169,7 +169,11 @@ void hrot_tail(int n, int level, int batch, const uint32_t* v, uint64_t v_bs, ui
 // of one polynomial when several polynomials are stacked; <= 0 means `rows`).
 void elementwise(int n, int rows, int batch, int op, const uint32_t* a, uint64_t a_bs, const uint32_t* b,
                  uint64_t b_bs, uint32_t* o, uint64_t o_bs, const uint16_t* row_prime, const PrimeDev* primes,
-                 cudaStream_t st, int prime_mod = 0);
+                 cudaStream_t st, int prime_mod = 0, const uint32_t* row_consts = nullptr);
+// apply_automorphism for Galois element g (inverse gi), evaluation or
+// coefficient domain (automorphism.cpp:76-100), out-of-place gather
+void automorphism_galois(int n, int logn, int rows, uint32_t g, uint32_t gi, int coeff, const uint32_t* in,
+                         uint32_t* out, const uint16_t* row_prime, const PrimeDev* primes, cudaStream_t st);
 // decrypt / encrypt element-wise parts (ckks.cpp:497-553), see kernels.cu
 void crypt(int n, int level, int batch, int op, const uint32_t* x, uint64_t x_bs, const uint32_t* y, const uint32_t* z,
            const uint32_t* w, const uint32_t* u, uint32_t* out, uint64_t out_bs, const PrimeDev* primes,

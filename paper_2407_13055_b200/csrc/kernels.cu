@@ -430,18 +430,30 @@ __global__ void __launch_bounds__(kT) k_hrot_tail(int n, int level, const uint32
 }
 
 // ------------------------------------------------------------ elementwise --
-__global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_t* __restrict__ a, uint64_t a_bs,
-                                                    const uint32_t* __restrict__ bp, uint64_t b_bs,
-                                                    uint32_t* __restrict__ o, uint64_t o_bs,
+// op 0 add, 1 sub, 2 Montgomery mul (poly.cpp:146-164), 3 multiply row i by
+// the canonical Montgomery constant rc[i] (ew_mul_const, poly.cpp:166-180).
+// o may alias a or b (ew_add_inplace / ew_sub_inplace, poly.cpp:182-205):
+// every thread reads its 4 words of each operand before writing them.
+__global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_t* a, uint64_t a_bs,
+                                                    const uint32_t* bp, uint64_t b_bs, uint32_t* o, uint64_t o_bs,
                                                     const uint16_t* __restrict__ row_prime,
-                                                    const PrimeDev* __restrict__ primes, int prime_mod) {
+                                                    const PrimeDev* __restrict__ primes, int prime_mod,
+                                                    const uint32_t* __restrict__ rc) {
   const int xo = (blockIdx.x * kT + threadIdx.x) * 4;
   if (xo >= n) return;
   const int i = blockIdx.y, b = blockIdx.z;
   const PrimeDev P = primes[row_prime ? row_prime[i] : i % prime_mod];
   const size_t r = (size_t)i * n + xo;
-  const uint4 x = ld4(a + b * a_bs + r), y = ld4(bp + b * b_bs + r);
+  const uint4 x = *reinterpret_cast<const uint4*>(a + b * a_bs + r);
   uint4 z;
+  if (op == 3) {
+    const uint32_t c = rc[i];
+    z = make_uint4(sub_if(mont_mul(x.x, c, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.y, c, P.q, P.qinv_neg), P.q),
+                   sub_if(mont_mul(x.z, c, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.w, c, P.q, P.qinv_neg), P.q));
+    *reinterpret_cast<uint4*>(o + b * o_bs + r) = z;
+    return;
+  }
+  const uint4 y = *reinterpret_cast<const uint4*>(bp + b * b_bs + r);
   if (op == 0) {
     z = make_uint4(sub_if(x.x + y.x, P.q), sub_if(x.y + y.y, P.q), sub_if(x.z + y.z, P.q), sub_if(x.w + y.w, P.q));
   } else if (op == 1) {
@@ -451,7 +463,43 @@ __global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_
     z = make_uint4(sub_if(mont_mul(x.x, y.x, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.y, y.y, P.q, P.qinv_neg), P.q),
                    sub_if(mont_mul(x.z, y.z, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.w, y.w, P.q, P.qinv_neg), P.q));
   }
-  st4(o + b * o_bs + r, z);
+  *reinterpret_cast<uint4*>(o + b * o_bs + r) = z;
+}
+
+// ------------------------------------------------------------ automorphism --
+// apply_automorphism (automorphism.cpp:76-100) for any Galois element g (odd,
+// mod 2n) with inverse gi, indices computed on the fly (no map table), as a
+// gather so every warp writes 32 contiguous words:
+//  * evaluation domain (bit-reversed columns): out[j] = in[src(j)] with
+//    src(j) = brev(phi_gi(brev(j))), phi_g(i) = ((2i+1) g mod 2n - 1) / 2
+//    (the inverse of dest(i) = brev(phi_g(brev(i))), automorphism.cpp:40-46);
+//  * coefficient domain: the reference scatters coefficient k to
+//    k * gi mod 2n with a sign flip past n (automorphism.cpp:50-61, :90-97);
+//    gathered, out[m] = +in[k] if k = m g mod 2n < n, else -in[k - n],
+//    negation canonical (q - v, 0 stays 0).
+__global__ void __launch_bounds__(kT) k_automorphism_galois(int n, int logn, uint32_t g, uint32_t gi, int coeff,
+                                                            const uint32_t* __restrict__ in,
+                                                            uint32_t* __restrict__ out,
+                                                            const uint16_t* __restrict__ row_prime,
+                                                            const PrimeDev* __restrict__ primes) {
+  const uint32_t j = blockIdx.x * kT + threadIdx.x;
+  if (j >= (uint32_t)n) return;
+  const size_t r = (size_t)blockIdx.y * n;
+  const uint32_t mask2n = 2u * n - 1u;
+  if (!coeff) {
+    const uint32_t bj = __brev(j) >> (32 - logn);
+    const uint32_t ph = (((2u * bj + 1u) * gi) & mask2n) >> 1;  // ((2i+1) gi mod 2n - 1) / 2
+    out[r + j] = __ldg(&in[r + (__brev(ph) >> (32 - logn))]);
+    return;
+  }
+  const uint32_t k = (j * g) & mask2n;
+  if (k < (uint32_t)n) {
+    out[r + j] = __ldg(&in[r + k]);
+  } else {
+    const uint32_t q = primes[row_prime[blockIdx.y]].q;
+    const uint32_t v = __ldg(&in[r + k - n]);
+    out[r + j] = v ? q - v : 0u;
+  }
 }
 
 // ------------------------------------------------- encrypt / decrypt parts --
@@ -619,10 +667,16 @@ void hrot_tail(int n, int level, int batch, const uint32_t* v, uint64_t v_bs, ui
 
 void elementwise(int n, int rows, int batch, int op, const uint32_t* a, uint64_t a_bs, const uint32_t* b,
                  uint64_t b_bs, uint32_t* o, uint64_t o_bs, const uint16_t* row_prime, const PrimeDev* primes,
-                 cudaStream_t st, int prime_mod) {
+                 cudaStream_t st, int prime_mod, const uint32_t* row_consts) {
   dim3 grid(cdiv(n / 4, kT), rows, batch);
   k_elementwise<<<grid, kT, 0, st>>>(n, op, a, a_bs, b, b_bs, o, o_bs, row_prime, primes,
-                                     prime_mod > 0 ? prime_mod : rows);
+                                     prime_mod > 0 ? prime_mod : rows, row_consts);
+}
+
+void automorphism_galois(int n, int logn, int rows, uint32_t g, uint32_t gi, int coeff, const uint32_t* in,
+                         uint32_t* out, const uint16_t* row_prime, const PrimeDev* primes, cudaStream_t st) {
+  dim3 grid(cdiv(n, kT), rows);
+  k_automorphism_galois<<<grid, kT, 0, st>>>(n, logn, g, gi, coeff, in, out, row_prime, primes);
 }
 
 void crypt(int n, int level, int batch, int op, const uint32_t* x, uint64_t x_bs, const uint32_t* y, const uint32_t* z,

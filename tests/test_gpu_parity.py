@@ -597,3 +597,126 @@ def test_mod_switch_matches_oracle_composition(n):
     conv = O.bconv(coef.astype(np.int32), list(src_g), list(dst_g))
     want = O.canonical(O.ntt_fwd(conv, dst_g), dst_g)
     np.testing.assert_array_equal(host(out.data), want)
+
+
+# ------------------------------------------- element-wise (a5), automorphism (a13)
+@pytest.mark.parametrize("n", [1024, 65536])
+@pytest.mark.parametrize("q_rows,p_rows", [(8, 0), (5, 3), (8, 3), (1, 1)])
+def test_elementwise_ops_match_oracle(n, q_rows, p_rows):
+    """ew_add / ew_sub / ew_mul / ew_mul_const and the in-place add / sub
+    (poly.cpp:121-205) over Q-prefix and P-extended polynomials, canonical
+    residues equal to the oracle's."""
+    l, a = 8, 3
+    C = ctx_for(n, l, a)
+    O = Oracle(n, l, a, 55)
+    rng = Rng(17 * n + q_rows)
+    g = O.gidx(q_rows, p_rows)
+    x, y = O.random_rows(rng, g), O.random_rows(rng, g)
+    X = ckks.Polynomial(dev(x), q_rows, p_rows)
+    Y = ckks.Polynomial(dev(y), q_rows, p_rows)
+    for op, fn in ((0, ckks.ew_add), (1, ckks.ew_sub), (2, ckks.ew_mul)):
+        got = host(fn(C, X, Y).data)
+        np.testing.assert_array_equal(got, O.canonical(O.ew(op, x, y, g), g), err_msg=f"op {op}")
+    k = [int(v) for v in (np.arange(1, len(g) + 1) * 7919 + 3) % O.primes[g]]
+    got = host(ckks.ew_mul_const(C, X, k).data)
+    np.testing.assert_array_equal(got, O.canonical(O.ew(3, x, None, g, k), g))
+    Z = X.clone()
+    ckks.ew_add_inplace(C, Z, Y)
+    np.testing.assert_array_equal(host(Z.data), O.canonical(O.ew(0, x, y, g), g))
+    ckks.ew_sub_inplace(C, Z, Y)
+    np.testing.assert_array_equal(host(Z.data), x.astype(np.uint32))
+    if p_rows:  # basis prefix mismatch (check_binary, poly.cpp:115-119)
+        with pytest.raises(ValueError):
+            ckks.ew_add(C, X, ckks.Polynomial(Y.data, q_rows + p_rows, 0))
+
+
+@pytest.mark.parametrize("n", [16, 1024, 65536])
+@pytest.mark.parametrize("which", ["r1", "r-3", "r5", "r_n/4", "conj"])
+def test_automorphism_both_domains_match_oracle(n, which):
+    """apply_automorphism (automorphism.cpp:76-100): the evaluation-domain
+    gather and the coefficient-domain signed permutation for rotation and
+    conjugation maps, over a P-extended polynomial; and the coefficient
+    variant commutes with the NTT (test_automorphism.cpp:71-96)."""
+    l, a = 4, 2
+    C = ctx_for(n, l, a, 48)
+    O = Oracle(n, l, a, 48)
+    r = {"r1": 1, "r-3": -3, "r5": 5, "r_n/4": n // 4}.get(which, 0)
+    gal = 2 * n - 1 if which == "conj" else ckks.galois_for_rotation(n, r)
+    g = O.gidx(l, a)
+    x = O.random_rows(Rng(n + 99), g)
+    for coeff in (False, True):
+        P = ckks.Polynomial(dev(x), l, a, ckks.COEFFICIENT if coeff else ckks.EVALUATION, not coeff)
+        got = host(ckks.apply_automorphism(C, P, r, galois=gal).data)
+        np.testing.assert_array_equal(got, O.canonical(O.automorphism(x, gal, coeff), g), err_msg=f"coeff={coeff}")
+        if which != "conj" and not coeff:  # the rotation entry point agrees with the Galois one
+            np.testing.assert_array_equal(host(ckks.apply_automorphism(C, P, r).data), got)
+    # commutation: NTT(phi_coeff(x)) == phi_eval(NTT(x))
+    A = ckks.Polynomial(dev(x), l, a, ckks.COEFFICIENT, False)
+    lhs = ckks.ntt_forward(C, ckks.apply_automorphism(C, A, r, galois=gal))
+    rhs = ckks.apply_automorphism(C, ckks.ntt_forward(C, A.clone()), r, galois=gal)
+    np.testing.assert_array_equal(host(lhs.data), host(rhs.data))
+
+
+# ------------------------------------------------------- wire formats (f2) ----
+@pytest.mark.parametrize("d", [pytest.param(d, id=d.name) for d in SMALL_DIRS])
+def test_wire_formats_through_the_c_abi_are_byte_exact(d):
+    """Ciphertexts, keys, polynomials and the basis read by the C ABI's
+    deserialisers straight into device memory, HMult / HRot / key switching
+    on the GPU, results written by the C ABI's serialisers: every blob is
+    byte-identical to the one the reference wrote (ckks.cpp:1090-1154,
+    poly.cpp:295-352, rns.cpp:168-216)."""
+    fx = Fixture(d)
+    C = ctx_for(fx.n, fx.l, fx.alpha, fx.db)
+    blob = lambda name: (d / f"{name}.bin").read_bytes()
+    assert ckks.serialize_basis(C) == blob("basis")
+    cu, cv = ckks.deserialize_ciphertext(C, blob("ct_u")), ckks.deserialize_ciphertext(C, blob("ct_v"))
+    assert ckks.serialize_ciphertext(C, cu) == blob("ct_u")
+    relin = ckks.deserialize_evk(C, blob("evk_relin"))
+    rot1 = ckks.deserialize_evk(C, blob("evk_rot1"))
+    assert (relin.kind, rot1.kind, rot1.rotation) == (ckks.RELIN, ckks.ROTATION, 1)
+    assert ckks.serialize_evk(C, relin) == blob("evk_relin")
+    assert ckks.serialize_evk(C, rot1) == blob("evk_rot1")
+    assert ckks.serialize_ciphertext(C, ckks.hmult(C, cu, cv, relin)) == blob("out_hmult")
+    assert ckks.serialize_ciphertext(C, ckks.hrot(C, cu, 1, rot1)) == blob("out_hrot1")
+    assert ckks.serialize_ciphertext(C, ckks.rescale(C, cu)) == blob("out_rescale")
+    Cl = ctx_for(fx.n, fx.l, fx.alpha, fx.db, lazy=True)
+    out_lazy = ckks.hmult(Cl, cu, cv, relin)
+    assert out_lazy.pending_rescale and ckks.serialize_ciphertext(Cl, out_lazy) == blob("out_hmult_lazy")
+    d_a = ckks.Polynomial(cu.data[1].contiguous(), fx.l)
+    c0, c1 = ckks.key_switch(C, d_a, relin)
+    assert ckks.serialize_poly(C, c0) == blob("out_keyswitch_c0")
+    assert ckks.serialize_poly(C, c1) == blob("out_keyswitch_c1")
+    p = ckks.deserialize_poly(C, blob("in_ntt_coeff"))
+    assert (p.q_count, p.p_count, p.domain, p.mont) == (fx.l, fx.alpha, ckks.COEFFICIENT, False)
+    assert ckks.serialize_poly(C, ckks.ntt_forward(C, p)) == blob("out_ntt_coeff")
+    sk = ckks.deserialize_poly(C, blob("sk"))
+    assert ckks.serialize_poly(C, sk) == blob("sk")
+
+
+@pytest.mark.parametrize("d", [pytest.param(SMALL_DIRS[0], id=SMALL_DIRS[0].name)])
+def test_wire_readers_reject_like_the_reference(d):
+    """Truncation, bad magic, basis-hash and shape mismatches are errors of
+    the reference's classes (runtime_error for polynomials, invalid_argument
+    for ciphertext / key headers); non-canonical residues are rejected."""
+    fx = Fixture(d)
+    C = ctx_for(fx.n, fx.l, fx.alpha, fx.db)
+    ct = (d / "ct_u.bin").read_bytes()
+    pol = (d / "sk.bin").read_bytes()
+    with pytest.raises(ValueError, match="header"):
+        ckks.deserialize_ciphertext(C, b"XXXX" + ct[4:])
+    with pytest.raises(ValueError, match="truncated"):
+        ckks.deserialize_ciphertext(C, ct[: len(ct) // 2])
+    with pytest.raises(RuntimeError, match="magic"):
+        ckks.deserialize_poly(C, b"XXXX" + pol[4:])
+    with pytest.raises(RuntimeError, match="truncated"):
+        ckks.deserialize_poly(C, pol[:-4])
+    bad_hash = bytearray(pol)
+    bad_hash[24] ^= 1
+    with pytest.raises(RuntimeError, match="hash"):
+        ckks.deserialize_poly(C, bytes(bad_hash))
+    big = bytearray(pol)
+    big[32:36] = (0xFFFFFFF0).to_bytes(4, "little")
+    with pytest.raises(RuntimeError, match="range"):
+        ckks.deserialize_poly(C, bytes(big))
+    with pytest.raises(ValueError):
+        ckks.deserialize_evk(C, (d / "ct_u.bin").read_bytes())

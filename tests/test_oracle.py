@@ -180,3 +180,42 @@ def test_reference_unit_suite_passes_against_shims():
     r = subprocess.run([str(REF_DIR / "ref_unit_tests")], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "test cases failed: 0" in r.stdout
+
+
+@pytest.mark.parametrize("n", [16, 256])
+def test_oracle_automorphism_restatement(n):
+    """cko_automorphism: the evaluation-domain gather for a rotation's Galois
+    element equals the rotation map (automorphism.cpp:38-69), conjugation is an
+    involution, and the coefficient-domain variant commutes with the NTT
+    (the reference's own property, test_automorphism.cpp:71-96)."""
+    from pyoracle import Oracle, Rng
+
+    O = Oracle(n, 4, 2, 48)
+    g = O.gidx(4, 2)
+    x = O.random_rows(Rng(n), g)
+    for r in (1, -3, 5):
+        gal = pow(5, (-r) % (n // 2), 2 * n)
+        np.testing.assert_array_equal(O.automorphism(x, gal, False), x[:, O.rotation_src_map(r)])
+        lhs = O.ntt_fwd(O.automorphism(x, gal, True), g)
+        rhs = O.automorphism(O.ntt_fwd(x, g), gal, False)
+        np.testing.assert_array_equal(O.canonical(lhs, g), O.canonical(rhs, g))
+    conj = 2 * n - 1
+    for coeff in (False, True):
+        twice = O.automorphism(O.automorphism(x, conj, coeff), conj, coeff)
+        np.testing.assert_array_equal(O.canonical(twice, g), O.canonical(x, g))
+
+
+def test_oracle_elementwise_restatement():
+    """cko_ew_rows over P-extended rows: add/sub round trip, mul by the
+    Montgomery one R mod q is the identity, mul_const by R is the identity."""
+    from pyoracle import Oracle, Rng
+
+    O = Oracle(64, 4, 2, 48)
+    g = O.gidx(3, 2)
+    x, y = O.random_rows(Rng(1), g), O.random_rows(Rng(2), g)
+    s = O.ew(0, x, y, g)
+    np.testing.assert_array_equal(O.canonical(O.ew(1, s, y, g), g), O.canonical(x, g))
+    R = [(1 << 32) % int(q) for q in O.primes[g]]
+    one = np.repeat(np.array(R, np.int64)[:, None], 64, 1)
+    np.testing.assert_array_equal(O.canonical(O.ew(2, x, one, g), g), O.canonical(x, g))
+    np.testing.assert_array_equal(O.canonical(O.ew(3, x, None, g, R), g), O.canonical(x, g))
