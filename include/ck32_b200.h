@@ -83,6 +83,10 @@ ck_status ck_memcpy_h2d(ck_context* ctx, void* dst, const void* src, size_t byte
 ck_status ck_memcpy_d2h(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream);
 ck_status ck_memcpy_d2d(ck_context* ctx, void* dst, const void* src, size_t bytes, ck_stream stream);
 ck_status ck_stream_sync(ck_context* ctx, ck_stream stream);
+/* a non-blocking CUDA stream on the context's device, for callers without
+ * the CUDA runtime headers (the C++ mirror's CkksContext::set_stream) */
+ck_status ck_stream_create(ck_context* ctx, ck_stream* out);
+ck_status ck_stream_destroy(ck_context* ctx, ck_stream stream);
 
 /* ---- kernel-level entry points ------------------------------------------ */
 /* ntt_forward (ntt.cpp:288-299) over `rows` rows in place; gidx[i] = global
@@ -189,7 +193,11 @@ ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, do
 /* decode (ckks.cpp:321-362): plaintext rows [level][n] (evaluation,
  * Montgomery) -> n/2 complex slots (re, im doubles, device memory).  The CRT
  * lift uses the minimal prime prefix covering scale_log2 + 40 bits (as the
- * reference), multi-precision, up to 16 primes. */
+ * reference), multi-precision, up to 16 primes.  Precision contract: the
+ * reference rounds Rational(v) / scale to double once; here the centred lift
+ * is rounded to double and multiplied by 2^-scale_log2, so slots agree with
+ * the reference's within 2^-40 (not bit for bit) at every scale
+ * (tests/test_gpu_encode.py). */
 ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2, double* slots_dev,
                     ck_stream stream);
 

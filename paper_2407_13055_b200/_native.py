@@ -49,6 +49,8 @@ _SIGS = {
     "ck_memcpy_d2h": [_vp, _vp, _vp, ctypes.c_size_t, _vp],
     "ck_memcpy_d2d": [_vp, _vp, _vp, ctypes.c_size_t, _vp],
     "ck_stream_sync": [_vp, _vp],
+    "ck_stream_create": [_vp, ctypes.POINTER(_vp)],
+    "ck_stream_destroy": [_vp, _vp],
     "ck_profile": [_vp, ctypes.c_int],
     "ck_profile_read": [_vp, ctypes.POINTER(ck_prof_stat), _u32, ctypes.POINTER(ctypes.c_uint32)],
     "ck_ntt_forward": [_vp, _vp, _u32, _u32p, _vp],

@@ -1976,6 +1976,32 @@ ck_status ck_sample_uniform(ck_rng* r, const uint32_t* q, uint32_t rows, uint32_
   });
 }
 
+ck_status ck_stream_create(ck_context* ctx, ck_stream* out) {
+  return guard([&] {
+    if (!ctx || !out) throw InvalidArgument("null argument");
+    CK_CUDA(cudaSetDevice(C(ctx)->device));
+    cudaStream_t st;
+    CK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    *out = st;
+  });
+}
+
+ck_status ck_stream_destroy(ck_context* ctx, ck_stream stream) {
+  return guard([&] {
+    if (!ctx) throw InvalidArgument("null argument");
+    if (stream) {
+      CK_CUDA(cudaStreamSynchronize(S(stream)));
+      Context* c = C(ctx);
+      auto it = c->scratch.find(S(stream));  // the stream's scratch arena goes with it
+      if (it != c->scratch.end()) {
+        if (it->second.ptr) CK_CUDA(cudaFree(it->second.ptr));
+        c->scratch.erase(it);
+      }
+      CK_CUDA(cudaStreamDestroy(S(stream)));
+    }
+  });
+}
+
 ck_status ck_stream_sync(ck_context* ctx, ck_stream stream) {
   return guard([&] { CK_CUDA(cudaStreamSynchronize(S(stream))); (void)ctx; });
 }

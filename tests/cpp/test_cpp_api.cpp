@@ -147,6 +147,78 @@ int main(int argc, char** argv) {
     auto hr = hoisted_rotations(ctx, x, {1}, {&rot});
     if (hr[0].data.download() != r.data.download()) throw std::runtime_error("hoisted rotation != hrot");
   }
+  {  // batched overloads on a non-default stream: element i of the batch == the single-ciphertext result
+    ck_stream st = nullptr;
+    check(ck_stream_create(ctx.raw(), &st));
+    ctx.set_stream(st);
+    CiphertextBatch X = make_batch(ctx, 3, level, ctx.default_scale()), Y = make_batch(ctx, 3, level, ctx.default_scale());
+    for (uint32_t i = 0; i < 3; ++i) {
+      check(ck_memcpy_d2d(ctx.raw(), X[i].data.data(), x.data.data(), ctw * 4, st));
+      check(ck_memcpy_d2d(ctx.raw(), Y[i].data.data(), y.data.data(), ctw * 4, st));
+    }
+    CiphertextBatch M = hmult(ctx, X, Y, relin), R = hrot(ctx, X, 1, rot);
+    ctx.sync();
+    for (uint32_t i = 0; i < 3; ++i)
+      if (M[i].data.download(st) != m.data.download() || R[i].data.download(st) != r.data.download())
+        throw std::runtime_error("batched hmult/hrot != single");
+    if (!(M.scale == m.scale) || M.level != m.level) throw std::runtime_error("batched ledger");
+    ctx.set_stream(nullptr);
+    check(ck_stream_destroy(ctx.raw(), st));
+  }
+  {  // hoisted_rotate_accumulate with one plaintext, rotation 1 ==
+     // mod_down of (key_mult -> automorphism -> * pt) accumulated, checked against
+     // the identity pt = R (Montgomery one): sum = hrot(x, 1)
+    const uint32_t rows = level + p.alpha;
+    std::vector<uint32_t> one((size_t)rows * p.n);
+    for (uint32_t i = 0; i < rows; ++i) {
+      const uint64_t q = ctx.primes()[i < level ? i : p.l + (i - level)];
+      for (uint32_t k = 0; k < p.n; ++k) one[(size_t)i * p.n + k] = (uint32_t)((1ull << 32) % q);
+    }
+    Plaintext pt1{DeviceBuffer(ctx.raw(), one.size()), Scale::two_pow(0), level, p.alpha};
+    pt1.data.upload(one.data(), one.size());
+    Ciphertext acc = hoisted_rotate_accumulate(ctx, x, {1}, {&pt1}, {&rot});
+    if (acc.data.download() != r.data.download()) throw std::runtime_error("hoisted accumulate(pt = 1) != hrot");
+  }
+  {  // kernel level: NTT round trip on the host row mirror, automorphism group law, ew identities
+    Polynomial c{DeviceBuffer(ctx.raw(), (size_t)3 * p.n), 2, 1, Domain::Coefficient, false};
+    c.host.assign((size_t)3 * p.n, 0);
+    for (uint32_t i = 0; i < 3; ++i) {
+      const uint32_t q = ctx.primes()[i < 2 ? i : p.l];
+      for (uint32_t k = 0; k < p.n; ++k) c.row(i)[k] = (uint32_t)((k * 2654435761ull + i) % q);
+    }
+    c.push();
+    const auto orig = c.host;
+    ntt_forward(ctx, c);
+    try {  // domain discipline (ntt.cpp:288-291)
+      ntt_forward(ctx, c);
+      ++errors;
+    } catch (const std::invalid_argument&) {
+    }
+    auto rot3 = apply_automorphism(ctx, c, AutomorphismMap::rotation(p.n, 3));
+    auto back = apply_automorphism(ctx, rot3, AutomorphismMap::rotation(p.n, -3));
+    if (back.data.download() != c.data.download()) throw std::runtime_error("rot 3 then rot -3 != identity");
+    auto sum = ew_add(ctx, c, rot3);
+    ew_sub_inplace(ctx, sum, rot3);
+    if (sum.data.download() != c.data.download()) throw std::runtime_error("ew_add then ew_sub_inplace");
+    intt_inverse(ctx, c);
+    c.pull();
+    if (c.host != orig) throw std::runtime_error("ntt round trip on the host mirror");
+    if (c.row(1)[5] != orig[p.n + 5]) throw std::runtime_error("row() view");
+  }
+  {  // scale tolerance (ckks.cpp:131-136): 2^-41 relative passes, 2^-39 fails
+    Ciphertext xs = make_ciphertext(ctx, level, Scale::rational(0, {(1u << 31) + 1u}, {}));
+    Ciphertext ys = make_ciphertext(ctx, level, Scale::rational(0, {(1u << 31) + 1u}, {}));
+    check(ck_memcpy_d2d(ctx.raw(), xs.data.data(), x.data.data(), ctw * 4, nullptr));
+    check(ck_memcpy_d2d(ctx.raw(), ys.data.data(), y.data.data(), ctw * 4, nullptr));
+    ys.scale = Scale::rational(-41, {(1u << 31) + 1u, (1u << 30) + 1u, 2u}, {(1u << 30) + 1u});  // equal
+    (void)hadd(ctx, xs, ys);
+    ys.scale = Scale::rational(0, {(1u << 31) + 2u}, {});  // 2^-31 relative: beyond 2^-40
+    try {
+      hadd(ctx, xs, ys);
+      ++errors;
+    } catch (const std::invalid_argument&) {
+    }
+  }
   const uint64_t n_launch = ck_launch_count(ctx.raw());
   std::printf("cpp api ok: hmult level %u -> %u, hrot level %u, %llu kernel launches, %d contract errors\n", level,
               m.level, r.level, (unsigned long long)n_launch, errors);

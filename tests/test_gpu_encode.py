@@ -100,3 +100,22 @@ def test_encode_errors_mirror_reference():
         ckks.encode(C, unit_slots(4, 1), Fraction(1 << 55), 9)  # level out of range (ckks.cpp:282-283)
     with pytest.raises(ValueError):
         ckks.encode(C, unit_slots(4, 1), Fraction(1 << 61), 8)  # scale out of range (ckks.cpp:284-285)
+
+
+@pytest.mark.parametrize("num,den", [(3 << 53, 5), ((1 << 60) - 1, 3), (18446744073709551557, 17 * 19)])
+def test_decode_matches_reference_at_non_power_of_two_scale(ref, num, den):
+    """decode at scales that are not powers of two (what a rescale leaves,
+    Delta^2 / (q q')): the reference divides the exact CRT value by the exact
+    Rational scale and rounds once (ckks.cpp:345-353); the GPU multiplies the
+    double-rounded value by 2^-log2(scale), so agreement is to 2^-40 here,
+    not bit for bit (at power-of-two scales the two coincide up to the same
+    bound, test_decode_matches_reference)."""
+    n, l, a, level = 65536, 24, 8, 24
+    C = ctx_for(n, l, a)
+    z = unit_slots(n // 2, 31 + num % 101)
+    rows = ref.encode(n, l, a, 55, z, num, den, level)
+    want = ref.decode(n, l, a, 55, rows, level, num, den)
+    pt = ckks.Plaintext(ckks.Polynomial(torch.from_numpy(rows.astype(np.int64).astype(np.int32)).cuda(), level, 0),
+                        Fraction(num, den), level)
+    got = ckks.decode(C, pt)
+    assert np.abs(got - want).max() <= 2.0 ** -40
