@@ -56,6 +56,8 @@ def parse():
                     help="config 4 exchange: NCCL all-gather + copy, or peer-mapped loads inside BConv "
                          "(CUDA IPC across ranks; default)")
     ap.add_argument("--no-graph", action="store_true", help="helr: skip the CUDA-graph replay measurement")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="default line: skip the config 4 (limb, N=2^17) and config 5 (HELR) sub-measurements")
     ap.add_argument("--virtual-shards", type=int, default=0,
                     help="limb workload on ONE GPU: drive this many shards from one process (exchange = local "
                          "copies); measures the summed shard compute, not multi-GPU speed")
@@ -532,6 +534,39 @@ def main():
                 for lv in range(LEVEL, 0, -2)}
         del Xbig
 
+    # ---- BASELINE configs 4 and 5 on this GPU, so the driver-run line carries
+    # them: the N=2^17 single-ciphertext workload unsharded and as 8 virtual
+    # limb shards (peer-memory exchange between the shards' buffers), and one
+    # HELR iteration eager and replayed as a CUDA graph.  (Multi-GPU runs of
+    # these use --workload limb / helr under torchrun.)
+    extra = {}
+    if world == 1 and not args.no_extra:
+        import copy
+
+        C.close()
+        torch.cuda.empty_cache()
+        c4 = {}
+        for g in (0, 8):
+            a4 = copy.copy(args)
+            a4.virtual_shards, a4.exchange = g, "peer"
+            d = limb_measure(a4, 1, 0, local)
+            c4["unsharded" if g == 0 else f"virtual_shards_{g}"] = {
+                "ops_per_s": d["value"], "ms_per_step": d["ms_per_step"],
+                "graph_ms_per_step": d["graph_ms_per_step"], "graph_ops_per_s": d["graph_ops_per_s"],
+                "bit_exact_vs_single_device": d["bit_exact_vs_single_device"], "gpu_launches": d["gpu_launches"]}
+            torch.cuda.empty_cache()
+        extra["config4_limb_n131072"] = dict(
+            c4, workload="BASELINE config 4: 1 HMult+relin + 1 HRot(r=1) per step on ONE ciphertext at N=2^17, "
+                         "l=24, alpha=8; virtual shards = the limb-sharded path driven on one GPU (shard-local "
+                         "kernels + peer-memory BConv exchange), i.e. summed shard compute, not multi-GPU speed")
+        a5 = copy.copy(args)
+        a5.no_graph = False
+        d = helr_measure(a5, 1, 0, local)
+        extra["config5_helr"] = {"it_per_s": d["value"], "ms_per_iteration": d["ms_per_iteration"],
+                                 "eager_ms_per_iteration": d["eager_ms_per_iteration"],
+                                 "graph_ms_per_iteration": d["graph_ms_per_iteration"],
+                                 "gpu_launches": d["gpu_launches"], "workload": d["config"]["workload"]}
+
     if rank == 0:
         cpu = None if args.no_cpu or world > 1 else cpu_baseline_leg()
         line = {
@@ -560,6 +595,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        line.update(extra)
         if small:
             line["single_ciphertext"] = small
         if sweep:
@@ -574,6 +610,17 @@ def run_limb(args):
     """Config 4: one ciphertext, RNS limbs sharded over the ranks (N=2^17,
     l=24, alpha=8); one step = 1 HMult+relin (merged rescale) + 1 HRot(r=1),
     each with two all-gathers (ModUp sources, ModDown sources) over NCCL."""
+    import torch.distributed as dist
+
+    world, rank, local = dist_setup()
+    line = limb_measure(args, world, rank, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def limb_measure(args, world, rank, local, graph=True):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -583,7 +630,6 @@ def run_limb(args):
                                             LocalPeerExchange, ShardBackend, TorchExchange, exchange_bytes)
 
     n = 1 << 17
-    world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
     C = ckks.CkksContext(ckks.CkksParams(n=n, l=L, alpha=ALPHA, delta_bits=DB), device=local)
     q = torch.tensor(C.primes.astype(np.int64), device=dev)
@@ -641,6 +687,25 @@ def run_limb(args):
         dist.barrier()
     ms = dp.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
     launches = C.launch_count() - l0
+    # One process driving every shard on one stream (virtual shards, or G = 1):
+    # the whole step replayed as one CUDA graph, which removes the host launch
+    # cost of the ~G x 30 small kernels per mechanism.  (Across processes the
+    # peer exchange's epochs are host-side values, so a captured step could
+    # not be replayed there.)
+    graph_ms = None
+    if graph and world == 1:
+        from paper_2407_13055_b200.pipeline import CapturedStep
+        cap = CapturedStep(dev, step)
+        for _ in range(max(args.warmup, 1)):
+            cap.replay()
+        torch.cuda.synchronize(dev)
+        a.record(st)
+        for _ in range(args.steps):
+            cap.replay()
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        graph_ms = a.elapsed_time(b)
+        del cap
     # correctness spot check against the single-device path (rank-local rows)
     if world == 1:
         X = ckks.Ciphertext(x, Fraction(1 << DB), LEVEL)
@@ -653,6 +718,7 @@ def run_limb(args):
     peer_errors = exch.errors() if hasattr(exch, "errors") else None
     if peer_errors and any(peer_errors):
         raise RuntimeError(f"peer exchange timed out: {peer_errors}")
+    line = None
     if rank == 0:
         xb = exchange_bytes(lays[0], n, LEVEL, MERGED) + exchange_bytes(lays[0], n, LEVEL, MOD_DOWN)
         line = {
@@ -672,16 +738,19 @@ def run_limb(args):
                        "virtual_shards_on_one_gpu": bool(args.virtual_shards and world == 1),
                        "parallelism": f"limb-sharded x{G}"},
             "exchange_bytes_received_per_rank_per_step": xb,
+            "graph_ms_per_step": round(graph_ms / args.steps, 4) if graph_ms else None,
+            "graph_ops_per_s": round(2 * args.steps / (graph_ms / 1e3), 2) if graph_ms else None,
             "gpu_launches": int(launches), "clocks": clk.summary(),
             "bit_exact_vs_single_device": exact,
         }
-        print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()  # no rank frees its exchange buffer while a peer may still read it
     if hasattr(exch, "close"):
         exch.close()
-    if world > 1:
-        dist.destroy_process_group()
+    for sh in shards:
+        sh.close()
+    C.close()
+    return line
 
 
 def run_helr(args):
@@ -689,6 +758,17 @@ def run_helr(args):
     l=24, one mini-batch of 8 ciphertexts x (128 samples x 256 features) per
     GPU (1024 samples, the batch of Cheddar's HELR run).
     Synthetic ciphertexts, keys and plaintext constants (uniform residues)."""
+    import torch.distributed as dist
+
+    world, rank, local = dist_setup()
+    line = helr_measure(args, world, rank, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def helr_measure(args, world, rank, local):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -696,7 +776,6 @@ def run_helr(args):
     from paper_2407_13055_b200 import ckks, dp
     from paper_2407_13055_b200.helr import HelrIteration, HelrShape
 
-    world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
     shape = HelrShape(n=N_RING, features=256, cts=8)
     C = ckks.CkksContext(ckks.CkksParams(n=N_RING, l=L, alpha=ALPHA, delta_bits=DB), device=local)
@@ -754,6 +833,7 @@ def run_helr(args):
         torch.cuda.synchronize(dev)
         graph_ms = dp.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
         ms = min(ms, graph_ms)
+    line = None
     if rank == 0:
         per = ms / args.steps
         line = {
@@ -773,9 +853,8 @@ def run_helr(args):
                        "parallelism": f"dp{world} (one mini-batch per GPU)"},
             "gpu_launches": int(C.launch_count() - l0), "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    C.close()
+    return line
 
 
 def _unsplit(keys, lays):

@@ -1008,6 +1008,207 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
   cp_wait<0>();
 }
 
+// k_row_keymult_pf: the warp-local (WL), all-digits-at-once (ALLD),
+// key-ahead (EARLY) variant with NOTHING left on the critical path from HBM:
+// besides the extension tiles, the digit's own rows (pass-through rows of d)
+// go into that digit's (otherwise unused) tile buffer with the same cp.async
+// group, and the fold rows d0 / d1 of the merged HMult go into tile buffers as
+// soon as the row pass of an earlier digit has released them -- so every
+// load of an item is in flight while the butterflies of the previous digit
+// run (round 1 loaded own rows and fold rows with plain global loads right
+// before use: long-scoreboard 1.87 per issue).  Shared memory is unchanged
+// (3 tile buffers + the row tile's twiddles per CTA).
+template <int MINB>
+__global__ void __launch_bounds__(kKT, MINB) k_row_keymult_pf(KeyMultLaunch a, const uint2* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
+  uint2* tws = reinterpret_cast<uint2*>(smraw + 3 * kKBuf * 4);
+  const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15;
+  const int warp = tid >> 5, lane = tid & 31;
+  constexpr int kTiles = kR / kRRows;
+  const int rows = a.level + a.alpha, B = a.batch, D = a.D;
+  const uint32_t LA = (uint32_t)(a.L + a.alpha);
+  const int items = rows * kTiles * B;  // (row i, tile, b), b fastest
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
+  // this warp's two rows of a [8][256] row tile -> buffer (rpos layout), one cp.async each 16 B
+  auto stage = [&](uint32_t* buf, const uint32_t* g) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int e = lane + 32 * m, rr = 2 * warp + (e >> 6), c = (e & 63) * 4;
+      cp16(buf + rr * kRowStride + rpos(c), g + rr * kR + c);
+    }
+  };
+  // cp.async.wait_group with a runtime count (<= 4 groups in flight)
+  auto wait_groups = [](int pending) {
+    if (pending >= 4) cp_wait<4>();
+    else if (pending == 3) cp_wait<3>();
+    else if (pending == 2) cp_wait<2>();
+    else if (pending == 1) cp_wait<1>();
+    else cp_wait<0>();
+  };
+  int cur_key = -1;
+  for (int it = i0; it < i1; ++it) {
+    const int b = it % B, key = it / B, tile = key % kTiles, i = key / kTiles;
+    const int g = i < a.level ? i : a.L + (i - a.level);
+    const PrimeDev P = a.primes[g];
+    const uint32_t q = P.q, q2 = P.q2, q4 = 2 * P.q2;
+    const bool fold = a.fold && i < a.level;
+    __syncwarp();  // the warp is done with the previous item's buffers
+    if (key != cur_key) {
+      const uint2* T = tw2 + ((size_t)g * kR + tile * kRRows) * kR;
+      for (int e = lane; e < kR; e += 32) cp16(&tws[2 * warp * kR + 2 * e], &T[2 * warp * kR + 2 * e]);
+      cp_commit();
+      cur_key = key;
+    }
+    const size_t tofs = (size_t)tile * kRRows * kR;
+    int committed = 0;  // groups committed for this item: digit k = group k, then the fold groups
+    for (int k = 0; k < D; ++k) {
+      const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+      const uint32_t* gsrc = (i >= lo && i < hi) ? a.d + b * a.d_bs + (size_t)i * kN + tofs
+                                                 : a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + tofs;
+      stage(sbuf + k * kKBuf, gsrc);
+      cp_commit();
+      ++committed;
+    }
+    // fold halves: into the buffers no digit uses (D < 3), else into the
+    // buffer of digit 0 / 1 once its row pass has finished with it
+    int fb0 = 0, fb1 = 0, nf = 0;  // buffers holding fold halves 0 / 1, halves issued
+    const uint32_t* fsrc0 = a.fold + b * a.fold_bs + (size_t)i * kN + tofs;
+    const uint32_t* fsrc1 = a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + tofs;
+    auto issue_fold = [&](int buf) {
+      if (nf == 0) fb0 = buf;
+      else fb1 = buf;
+      stage(sbuf + buf * kKBuf, nf == 0 ? fsrc0 : fsrc1);
+      cp_commit();
+      ++committed;
+      ++nf;
+    };
+    if (fold)
+      for (int f = D; f < 3 && nf < 2; ++f) issue_fold(f);
+    const int r = tile * kRRows + rho;
+    const uint2* W = tws + rho * kR;
+    uint64_t s0[16], s1[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s0[j] = s1[j] = 0;
+    const size_t rofs = (size_t)r * kR + 16 * tau;  // this thread's 16 coefficients after the row pass
+    for (int k = 0; k < D; ++k) {
+      const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+      uint4 kb[4], ka[4];
+      {
+        const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
+        const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          kb[m] = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
+          ka[m] = __ldg(reinterpret_cast<const uint4*>(ea + 4 * m));
+        }
+      }
+      wait_groups(committed - (k + 1));
+      __syncwarp();
+      uint32_t* line = sbuf + k * kKBuf + rho * kRowStride;
+      uint32_t v[16];
+      if (i >= lo && i < hi) {  // the digit's own row (ModUp pass-through), already in evaluation form
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const uint4 x = *reinterpret_cast<const uint4*>(line + rpos(16 * tau) + 4 * m);
+          v[4 * m] = x.x;
+          v[4 * m + 1] = x.y;
+          v[4 * m + 2] = x.z;
+          v[4 * m + 3] = x.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = line[rpos(tau + 16 * j)];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int d = 8 >> t;
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = W[(1 << t) - 1 + blk];
+            if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) line[rpos(tau + 16 * j)] = v[j];
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const uint4 x = *reinterpret_cast<const uint4*>(line + rpos(16 * tau) + 4 * m);
+          v[4 * m] = x.x;
+          v[4 * m + 1] = x.y;
+          v[4 * m + 2] = x.z;
+          v[4 * m + 3] = x.w;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int d = 8 >> t;
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = W[16 + ((1 << t) - 1 + blk) * 16 + tau];
+            if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = canon8(v[j], q, q2, q4);
+      }
+      if (fold && nf < 2 && k < 2) {  // buffer k is free now: the next fold half goes there
+        __syncwarp();
+        issue_fold(k);
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        s0[4 * m] = mac_wide(s0[4 * m], v[4 * m], kb[m].x);
+        s0[4 * m + 1] = mac_wide(s0[4 * m + 1], v[4 * m + 1], kb[m].y);
+        s0[4 * m + 2] = mac_wide(s0[4 * m + 2], v[4 * m + 2], kb[m].z);
+        s0[4 * m + 3] = mac_wide(s0[4 * m + 3], v[4 * m + 3], kb[m].w);
+        s1[4 * m] = mac_wide(s1[4 * m], v[4 * m], ka[m].x);
+        s1[4 * m + 1] = mac_wide(s1[4 * m + 1], v[4 * m + 1], ka[m].y);
+        s1[4 * m + 2] = mac_wide(s1[4 * m + 2], v[4 * m + 2], ka[m].z);
+        s1[4 * m + 3] = mac_wide(s1[4 * m + 3], v[4 * m + 3], ka[m].w);
+      }
+    }
+    if (fold) {  // merged HMult: v += P * d0 / d1 (ckks.cpp:831-842)
+      const uint32_t pm = a.p_mont[i];
+      wait_groups(0);
+      __syncwarp();
+      const uint32_t* l0 = sbuf + fb0 * kKBuf + rho * kRowStride + rpos(16 * tau);
+      const uint32_t* l1 = sbuf + fb1 * kKBuf + rho * kRowStride + rpos(16 * tau);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const uint4 x0 = *reinterpret_cast<const uint4*>(l0 + 4 * m);
+        const uint4 x1 = *reinterpret_cast<const uint4*>(l1 + 4 * m);
+        s0[4 * m] = mac_wide(s0[4 * m], x0.x, pm);
+        s0[4 * m + 1] = mac_wide(s0[4 * m + 1], x0.y, pm);
+        s0[4 * m + 2] = mac_wide(s0[4 * m + 2], x0.z, pm);
+        s0[4 * m + 3] = mac_wide(s0[4 * m + 3], x0.w, pm);
+        s1[4 * m] = mac_wide(s1[4 * m], x1.x, pm);
+        s1[4 * m + 1] = mac_wide(s1[4 * m + 1], x1.y, pm);
+        s1[4 * m + 2] = mac_wide(s1[4 * m + 2], x1.z, pm);
+        s1[4 * m + 3] = mac_wide(s1[4 * m + 3], x1.w, pm);
+      }
+    }
+    uint32_t* o0 = a.v + b * a.v_bs + (size_t)i * kN + rofs;
+    uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv_neg), q)));
+      stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv_neg), q)));
+    }
+  }
+  cp_wait<0>();
+}
+
 }  // namespace
 
 // CK32_KM selects the k_row_keymult variant for A/B runs: 0 = key halves
@@ -1030,6 +1231,21 @@ static void launch_km(const KeyMultLaunch& a, const uint2* tw2, int items, cudaS
   k_row_keymult<EARLY, MINB, ALLD, WL><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
 }
 
+template <int MINB>
+static void launch_km_pf(const KeyMultLaunch& a, const uint2* tw2, int items, cudaStream_t st) {
+  static int grid = 0;
+  constexpr int smem = kKSmem + kKBuf * 4;
+  if (!grid) {
+    cudaFuncSetAttribute(k_row_keymult_pf<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult_pf<MINB>, kKT, smem);
+    grid = sms * std::max(1, per);
+  }
+  k_row_keymult_pf<MINB><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
+}
+
 void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
   static int ver = -1;
   if (ver < 0) {
@@ -1037,6 +1253,10 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
     ver = e ? std::atoi(e) : 0;
   }
   const int items = (a.level + a.alpha) * (kR / kRRows) * a.batch;
+  if (ver == 5 && a.D <= 3) {
+    launch_km_pf<4>(a, tw2, items, st);
+    return;
+  }
   if (ver == 1)
     launch_km<true, 3>(a, tw2, items, st);
   else if (ver == 2)

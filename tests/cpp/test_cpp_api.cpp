@@ -165,9 +165,7 @@ int main(int argc, char** argv) {
     ctx.set_stream(nullptr);
     check(ck_stream_destroy(ctx.raw(), st));
   }
-  {  // hoisted_rotate_accumulate with one plaintext, rotation 1 ==
-     // mod_down of (key_mult -> automorphism -> * pt) accumulated, checked against
-     // the identity pt = R (Montgomery one): sum = hrot(x, 1)
+  {  // hoisted_rotate_accumulate with the Montgomery one R mod q as plaintext
     const uint32_t rows = level + p.alpha;
     std::vector<uint32_t> one((size_t)rows * p.n);
     for (uint32_t i = 0; i < rows; ++i) {
@@ -176,8 +174,12 @@ int main(int argc, char** argv) {
     }
     Plaintext pt1{DeviceBuffer(ctx.raw(), one.size()), Scale::two_pow(0), level, p.alpha};
     pt1.data.upload(one.data(), one.size());
+    Ciphertext id = hoisted_rotate_accumulate(ctx, x, {0}, {&pt1}, {nullptr});  // r = 0: pt * ct, no key switch
+    if (id.data.download() != x.data.download()) throw std::runtime_error("hoisted accumulate(r = 0, pt = 1) != ct");
+    // r = 1 (ModDown after the automorphism: equal to hrot only up to the BConv error, so the
+    // Python side compares it with the oracle's hoisted_rotate_accumulate)
     Ciphertext acc = hoisted_rotate_accumulate(ctx, x, {1}, {&pt1}, {&rot});
-    if (acc.data.download() != r.data.download()) throw std::runtime_error("hoisted accumulate(pt = 1) != hrot");
+    write_file(dir + "/out_acc.bin", acc.data.download());
   }
   {  // kernel level: NTT round trip on the host row mirror, automorphism group law, ew identities
     Polynomial c{DeviceBuffer(ctx.raw(), (size_t)3 * p.n), 2, 1, Domain::Coefficient, false};
@@ -210,8 +212,12 @@ int main(int argc, char** argv) {
     Ciphertext ys = make_ciphertext(ctx, level, Scale::rational(0, {(1u << 31) + 1u}, {}));
     check(ck_memcpy_d2d(ctx.raw(), xs.data.data(), x.data.data(), ctw * 4, nullptr));
     check(ck_memcpy_d2d(ctx.raw(), ys.data.data(), y.data.data(), ctw * 4, nullptr));
-    ys.scale = Scale::rational(-41, {(1u << 31) + 1u, (1u << 30) + 1u, 2u}, {(1u << 30) + 1u});  // equal
+    ys.scale = Scale::rational(-1, {(1u << 31) + 1u, (1u << 30) + 1u, 2u}, {(1u << 30) + 1u});  // equal
     (void)hadd(ctx, xs, ys);
+    xs.scale = Scale::two_pow(50);
+    ys.scale = Scale::rational(0, {25u, 13u, 41u, 61u, 101u, 1201u, 1321u, 63901u}, {});  // 2^50 + 1: 2^-50 relative
+    (void)hadd(ctx, xs, ys);
+    xs.scale = ys.scale = Scale::rational(0, {(1u << 31) + 1u}, {});
     ys.scale = Scale::rational(0, {(1u << 31) + 2u}, {});  // 2^-31 relative: beyond 2^-40
     try {
       hadd(ctx, xs, ys);

@@ -508,6 +508,12 @@ def test_cpp_mirror_drop_in(tmp_path):
     rb, ra = O.hrot(level, xb, xa, 1, evk)
     got = np.fromfile(tmp_path / "out_hrot.bin", dtype="<u4").reshape(2, level, n)
     np.testing.assert_array_equal(got, np.stack([canon(O, rb, level), canon(O, ra, level)]))
+    # the mirror's hoisted_rotate_accumulate (pt = Montgomery one, P-extended, r = 1)
+    g = O.gidx(level, a)
+    one = np.repeat(np.array([(1 << 32) % int(q) for q in O.primes[g]], np.int64)[:, None], n, 1)
+    ab, aa = O.hoisted_accumulate(level, xb, xa, [1], [one], [evk])
+    got = np.fromfile(tmp_path / "out_acc.bin", dtype="<u4").reshape(2, level, n)
+    np.testing.assert_array_equal(got, np.stack([canon(O, ab, level), canon(O, aa, level)]))
 
 
 def test_cpp_mirror_keys_with_std_mt19937_64(tmp_path):

@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+timeout 1700 python -m pytest tests -q -m gpu 2>&1 | tail -8
+timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -5 gpurun_out/bench_default.err
+python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/bench_default.json').read().strip().splitlines()[-1])
+for k in ['value','bit_exact','roofline','e2e','config4_limb_n131072','config5_helr','cpu_baseline']:
+    print(k, json.dumps(d.get(k))[:600])
+PY
