@@ -214,8 +214,8 @@ int main(int argc, char** argv) {
     check(ck_memcpy_d2d(ctx.raw(), ys.data.data(), y.data.data(), ctw * 4, nullptr));
     ys.scale = Scale::rational(-1, {(1u << 31) + 1u, (1u << 30) + 1u, 2u}, {(1u << 30) + 1u});  // equal
     (void)hadd(ctx, xs, ys);
-    xs.scale = Scale::two_pow(50);
-    ys.scale = Scale::rational(0, {25u, 13u, 41u, 61u, 101u, 1201u, 1321u, 63901u}, {});  // 2^50 + 1: 2^-50 relative
+    xs.scale = Scale::two_pow(48);
+    ys.scale = Scale::rational(0, {193u, 65537u, 22253377u}, {});  // 2^48 + 1: 2^-48 relative
     (void)hadd(ctx, xs, ys);
     xs.scale = ys.scale = Scale::rational(0, {(1u << 31) + 1u}, {});
     ys.scale = Scale::rational(0, {(1u << 31) + 2u}, {});  // 2^-31 relative: beyond 2^-40
