@@ -20,8 +20,14 @@
 // [0, 2q).  Forward: values in [0, 8q) (q < 2^29), x reduced by 4q only at
 // every other stage (`ctl`), the column pass hands [0, 8q) to the row pass
 // through HBM and the row pass canonicalises once at the end.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <stdexcept>
+#include <unordered_map>
 
 #include "ck_common.cuh"
 #include "ck_kernels.h"
@@ -41,6 +47,40 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int K>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+}
+
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers for the column pass
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(mbar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(mbar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "TMA_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TMA_WAIT_%=;\n\t}\n" ::"r"(smem_addr(mbar)),
+      "r"(parity)
+      : "memory");
+}
+// one [256 rows][32 columns] uint32 box of the 2D map (columns innermost)
+__device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* map, int col, int row, uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(smem_addr(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(smem_addr(mbar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(mbar))
+               : "memory");
 }
 
 // forward CT butterfly, Harvey lazy: x,y in [0,4q) -> [0,4q)
@@ -165,19 +205,29 @@ __device__ __forceinline__ void col_item(int it, int batch, int& job, int& b, in
 // registers: 124 -> ~96 registers, MINB CTAs per SM).
 // LOGR: log2 of the row length (8: N = 2^16 = 256 x 256; 9: N = 2^17 =
 // 256 columns of a 256 x 512 matrix, the same 256-point column transform).
-template <bool INV, bool DB, bool TWR = false, int MINB = 1, int LOGR = 8>
+// TMA (LOGR = 8, TWR, single buffer): the tile arrives with ONE
+// cp.async.bulk.tensor.2d per item (a [256][32] box of the limb matrix, one
+// 2D tensor map over the whole source allocation: rows of 256 words) plus one
+// 1D bulk copy of the 2 KB twiddle slice, completing on an mbarrier --
+// instead of 16 cp.async (and their address arithmetic) per thread.
+template <bool INV, bool DB, bool TWR = false, int MINB = 1, int LOGR = 8, bool TMA = false>
 __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
                                              uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
                                              int njobs, const PrimeDev* __restrict__ primes,
                                              const uint2* __restrict__ tw_full, const ExitConst* __restrict__ exits,
-                                             int entry) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+                                             int entry, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smraw[];
   ColBuf* buf = reinterpret_cast<ColBuf*>(smraw);
   // [2][256] twiddle ring (TWR): right after the single tile buffer (ColBuf::tw unused)
   uint2* twring = reinterpret_cast<uint2*>(smraw + (DB ? 2 * sizeof(ColBuf) : (TWR ? sizeof(ColBuf::tile) : sizeof(ColBuf))));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(twring + 512);  // TMA: one mbarrier after the ring
   const int tid = threadIdx.x, cq = tid & 7, tau = tid >> 3;
   constexpr int RS = 1 << LOGR, NT = 256 << LOGR, TILES = RS / kCCols;  // row stride, limb size, tiles per limb
   const int items = njobs * batch * TILES;
+  if (TMA) {
+    if (tid == 0) mbar_init1(mbar);
+    __syncthreads();
+  }
   // the item decoded (and its job loaded) when it is prefetched is reused
   // when it is processed
   int nb = 0, ntile = 0;
@@ -186,6 +236,18 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
     int job;
     col_item<TILES>(it, batch, job, nb, ntile);
     nJ = jobs[job];
+    if (TMA) {
+      if (tid == 0) {
+        // the CTA's generic-proxy accesses of the buffer (ordered by the
+        // caller's barrier) happen before the async-proxy writes
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const uint64_t word = INV ? nb * dst_bs + (uint64_t)nJ.dst_off * NT : nb * src_bs + (uint64_t)nJ.src_off * NT;
+        mbar_expect_tx(mbar, (uint32_t)sizeof(ColBuf::tile) + 256 * 8);
+        tma_tile(&B.tile[0], &tmap, ntile * kCCols, (int)(word / RS), mbar);
+        bulk_copy(&twring[(k & 1) * 256], tw_full + (size_t)nJ.prime * NT, 256 * 8, mbar);
+      }
+      return;
+    }
     const uint32_t* base = INV ? dst + nb * dst_bs + (size_t)nJ.dst_off * NT : src + nb * src_bs + (size_t)nJ.src_off * NT;
     if (TWR) {
       const uint32_t* g = base + ntile * kCCols;
@@ -204,14 +266,18 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
     const int nxt = it + gridDim.x;
     const int b = nb, tile = ntile;
     const RowJob J = nJ;
-    if (DB) {
-      if (nxt < items) prefetch(buf[(k + 1) & 1], nxt, k + 1);
-      cp_commit();
-      cp_wait<1>();
+    if (TMA) {
+      mbar_wait_parity(mbar, k & 1);  // item k's tile and twiddles have landed
     } else {
-      cp_wait<0>();
+      if (DB) {
+        if (nxt < items) prefetch(buf[(k + 1) & 1], nxt, k + 1);
+        cp_commit();
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
     }
-    __syncthreads();
     const PrimeDev P = primes[J.prime];
     const uint32_t q = P.q, q2 = P.q2, q4 = 2 * P.q2;
     const uint2* TW = TWR ? twring + (k & 1) * 256 : B.tw;
@@ -251,6 +317,7 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
           for (int blk = 0; blk < (1 << t); ++blk) twb[(1 << t) - 1 + blk] = B.tw[(16 << t) + (tau << t) + blk];
       }
       if (!DB) {
+        if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // my reads/writes before TMA's
         __syncthreads();
         if (nxt < items) prefetch(buf[0], nxt, k + 1);
         cp_commit();
@@ -287,6 +354,7 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
           for (int blk = 0; blk < (8 >> t); ++blk) twb[(8 >> t) - 1 + blk] = B.tw[(8 >> t) + blk];
       }
       if (!DB) {
+        if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // my reads/writes before TMA's
         __syncthreads();
         if (nxt < items) prefetch(buf[0], nxt, k + 1);
         cp_commit();
@@ -394,7 +462,10 @@ struct RowCursor {
 // COMB (forward only): drop-and-divide combine fused into the store,
 // out = (v - NTT(.)) * divisor^-1 (ckks.cpp:643-651), so the NTT output never
 // makes the extra HBM round trip through k_combine.
-template <bool INV, bool COMB = false>
+// COMB == 2: the combine's operand rows v are loaded at the start of the item
+// (into registers, their latency hidden by the 8 butterfly stages) instead of
+// right before the store (round 1: long-scoreboard 4.1 per issue there).
+template <bool INV, int COMB = 0>
 __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, const uint32_t* __restrict__ src,
                                              uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
                                              int njobs, const PrimeDev* __restrict__ primes,
@@ -463,6 +534,13 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
     uint32_t* line = line_buf + rho * kRowStride;
     uint32_t* orow = dst + b * dst_bs + (size_t)J.dst_off * kN + (size_t)r * kR;
     uint32_t v[16];
+    uint4 vvr[COMB == 2 ? 4 : 1];
+    if (COMB == 2) {  // J.dst_off = p * out_q + i; v row p * prow + i
+      const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
+      const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + (size_t)r * kR + 16 * tau;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) vvr[m] = __ldg(reinterpret_cast<const uint4*>(vr + 4 * m));
+    }
     if (!INV) {
       // phase A: c = tau + 16 j, stages 8..11 (row-shared twiddles W[0..14])
 #pragma unroll
@@ -507,7 +585,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
         const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv_neg;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          const uint4 vv = *reinterpret_cast<const uint4*>(vr + 4 * m);
+          const uint4 vv = COMB == 2 ? vvr[m] : *reinterpret_cast<const uint4*>(vr + 4 * m);
           uint4 o;
           o.x = sub_if(mont_mul(vv.x - canon8(v[4 * m], q, q2, q4) + q, di, q, qinv), q);
           o.y = sub_if(mont_mul(vv.y - canon8(v[4 * m + 1], q, q2, q4) + q, di, q, qinv), q);
@@ -573,8 +651,9 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
 
 int g_col_grid[2] = {0, 0}, g_row_grid = 0;
 bool g_col_db = false;
-int g_col_var = 2;  // CK32_COL: 0 = twiddles in registers, 1 = twiddle ring (4 CTAs/SM), 2 = ring, 5 CTAs/SM (default)
+int g_col_var = 3;  // CK32_COL: 0 = twiddles in registers, 1 = twiddle ring (4 CTAs/SM), 2 = ring, 5 CTAs/SM (cp.async), 3 = ring, 5 CTAs/SM, TMA tile loads (default)
 constexpr int kColRingSmem = (int)sizeof(ColBuf::tile) + 2 * 256 * 8;  // 36 KB (6 CTAs/SM measured no faster than 5)
+constexpr int kColTmaSmem = kColRingSmem + 16;                             // + the TMA mbarrier
 
 void init_grids() {
   if (g_row_grid) return;
@@ -596,7 +675,12 @@ void init_grids() {
   int dev = 0, sms = 148, c1 = 1, c2 = 1, r1 = 1, r2 = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (g_col_var == 1 || g_col_var == 2) {
+  cudaFuncSetAttribute(k_col<false, false, true, 5, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
+  cudaFuncSetAttribute(k_col<true, false, true, 5, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
+  if (g_col_var == 3) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, false, true, 5, 8, true>, kCT, kColTmaSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, false, true, 5, 8, true>, kCT, kColTmaSmem);
+  } else if (g_col_var == 1 || g_col_var == 2) {
     if (g_col_var == 1) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, false, true, 4>, kCT, kColRingSmem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, false, true, 4>, kCT, kColRingSmem);
@@ -618,22 +702,60 @@ void init_grids() {
   g_row_grid = sms * max(1, min(r1, r2));
 }
 
+// 2D tensor map over a limb matrix: rows of 256 uint32 starting at `base`,
+// box = [256 rows][32 columns] (one column-pass tile).  The map spans 2^31
+// rows: only boxes inside the caller's allocation are ever requested.
+// Encoded on the host once per base address (cuTensorMapEncodeTiled through
+// the runtime's driver entry point).
+const CUtensorMap& col_tensor_map(const void* base) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, CUtensorMap> cache;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(base);
+  if (it != cache.end()) return it->second;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)kR, (cuuint64_t)1 << 31};
+  const cuuint64_t strides[1] = {(cuuint64_t)kR * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kCCols, 256u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
+  if (cache.size() > 4096) cache.clear();
+  return cache.emplace(base, m).first->second;
+}
 template <bool INV>
 void launch_col(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaStream_t st) {
   const int items = a.njobs * a.batch * kCTiles;
   const int grid = min(g_col_grid[INV], items);
+  if (g_col_var == 3) {  // TMA staging (the tile source is dst for the inverse pass, as in prefetch)
+    const CUtensorMap& m = col_tensor_map(INV ? a.dst : src);
+    k_col<INV, false, true, 5, 8, true><<<grid, kCT, kColTmaSmem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch,
+                                                                       a.njobs, a.primes, a.tw, a.exits, a.entry, m);
+    return;
+  }
   if (g_col_var == 1)
     k_col<INV, false, true, 4><<<grid, kCT, kColRingSmem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
-                                                                 a.primes, a.tw, a.exits, a.entry);
+                                                                 a.primes, a.tw, a.exits, a.entry, CUtensorMap{});
   else if (g_col_var == 2)
     k_col<INV, false, true, 5><<<grid, kCT, kColRingSmem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
-                                                                 a.primes, a.tw, a.exits, a.entry);
+                                                                 a.primes, a.tw, a.exits, a.entry, CUtensorMap{});
   else if (g_col_db)
     k_col<INV, true><<<grid, kCT, 2 * sizeof(ColBuf), st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
-                                                            a.primes, a.tw, a.exits, a.entry);
+                                                            a.primes, a.tw, a.exits, a.entry, CUtensorMap{});
   else
     k_col<INV, false><<<grid, kCT, sizeof(ColBuf), st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs,
-                                                         a.primes, a.tw, a.exits, a.entry);
+                                                         a.primes, a.tw, a.exits, a.entry, CUtensorMap{});
 }
 
 // ===================================================== fused ModUp / ModDown ==
@@ -1506,7 +1628,7 @@ void launch_col9(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaS
   }
   const int items = a.njobs * a.batch * (kR5 / kCCols);
   k_col<INV, false, true, 5, 9><<<min(grid, items), kCT, kColRingSmem, st>>>(
-      a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs, a.primes, a.tw, a.exits, a.entry);
+      a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch, a.njobs, a.primes, a.tw, a.exits, a.entry, CUtensorMap{});
 }
 
 template <bool INV, int LOGR>
@@ -1549,17 +1671,32 @@ bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
   return true;
 }
 
+template <int COMB>
+static void launch_row_comb(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, int items, cudaStream_t st) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_row<false, COMB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row<false, COMB>, kRT, kRowSmem);
+    grid = sms * std::max(1, per);
+  }
+  k_row<false, COMB><<<min(grid, items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs, a.batch,
+                                                               a.njobs, a.primes, tw2, cb);
+}
+
 bool ntt256_forward_combine(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, cudaStream_t st) {
   init_grids();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_row<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmem);
-    attr = true;
+  static int early = -1;
+  if (early < 0) {
+    const char* e = std::getenv("CK32_COMB_EARLY");
+    early = e ? std::atoi(e) : 0;
   }
   const int row_items = a.njobs * (kR / kRRows) * a.batch;
   launch_col<false>(a, a.src, a.src_bs, st);
-  k_row<false, true><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs,
-                                                                        a.batch, a.njobs, a.primes, tw2, cb);
+  if (early) launch_row_comb<2>(a, tw2, cb, row_items, st);
+  else launch_row_comb<1>(a, tw2, cb, row_items, st);
   return true;
 }
 
