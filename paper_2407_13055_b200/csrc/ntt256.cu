@@ -535,6 +535,13 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
     uint32_t* orow = dst + b * dst_bs + (size_t)J.dst_off * kN + (size_t)r * kR;
     uint32_t v[16];
     uint4 vvr[COMB == 2 ? 4 : 1];
+    if (COMB == 3 && lane < 16) {  // L2 prefetch of the warp's 2 v rows (16 lines of 128 B)
+      const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
+      const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN +
+                           (size_t)(tile * kRRows + 2 * warp) * kR + lane * 32;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(vr));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + kR));
+    }
     if (COMB == 2) {  // J.dst_off = p * out_q + i; v row p * prow + i
       const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
       const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + (size_t)r * kR + 16 * tau;
@@ -922,7 +929,11 @@ constexpr int kKSmem = 2 * kKBuf * 4 + kRRows * kR * 8;
 // WL (with ALLD): every warp stages its own two rows of the tile and of the
 // twiddle tables, so the CTA never synchronises: the four warps are
 // independent pipelines (no __syncthreads in the loop).
-template <bool EARLY = false, int MINB = 1, bool ALLD = false, bool WL = false>
+// L2PF: at the item start every warp asks L2 for the lines of the rows it
+// will read with plain loads later (the digit's own rows of d and the fold
+// rows d0 / d1), so those loads hit L2 instead of going to HBM on the
+// critical path (prefetch.global.L2: no registers, no shared memory).
+template <bool EARLY = false, int MINB = 1, bool ALLD = false, bool WL = false, bool L2PF = false>
 __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, const uint2* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
@@ -986,6 +997,16 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
 #pragma unroll
     for (int j = 0; j < 16; ++j) s0[j] = s1[j] = 0;
     const size_t rofs = (size_t)r * kR + 16 * tau;  // this thread's 16 coefficients after the row pass
+    if (L2PF && i < a.level) {  // the warp's 2 rows = 16 lines of 128 B per array; lane -> one line
+      const size_t line_ofs = (size_t)(tile * kRRows + 2 * warp) * kR + (lane & 15) * 32;
+      const uint32_t* own = a.d + b * a.d_bs + (size_t)i * kN + line_ofs;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(own + (lane >> 4) * kR));
+      if (a.fold) {
+        const uint32_t* f = a.fold + b * a.fold_bs + (size_t)(lane < 16 ? i : a.level + i) * kN + line_ofs;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(f));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(f + kR));
+      }
+    }
     for (int k = 0; k < a.D; ++k) {
       const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
       uint4 kb[4], ka[4];
@@ -1338,19 +1359,20 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult_pf(KeyMultLaunch a, c
 // (default when D <= 3), 3 = the same with per-digit tile loads (4.83 TB/s),
 // 1 = per-digit loads at 3 CTAs/SM (4.20), 2 = key halves loaded after the
 // row pass (the first version, 4.77).
-template <bool EARLY, int MINB, bool ALLD = false, bool WL = false>
+template <bool EARLY, int MINB, bool ALLD = false, bool WL = false, bool L2PF = false>
 static void launch_km(const KeyMultLaunch& a, const uint2* tw2, int items, cudaStream_t st) {
   static int grid = 0;
   constexpr int smem = ALLD ? kKSmem + kKBuf * 4 : kKSmem;
   if (!grid) {
-    cudaFuncSetAttribute(k_row_keymult<EARLY, MINB, ALLD, WL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_row_keymult<EARLY, MINB, ALLD, WL, L2PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult<EARLY, MINB, ALLD, WL>, kKT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult<EARLY, MINB, ALLD, WL, L2PF>, kKT, smem);
     grid = sms * std::max(1, per);
   }
-  k_row_keymult<EARLY, MINB, ALLD, WL><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
+  k_row_keymult<EARLY, MINB, ALLD, WL, L2PF><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
 }
 
 template <int MINB>
@@ -1377,6 +1399,10 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
   const int items = (a.level + a.alpha) * (kR / kRRows) * a.batch;
   if (ver == 5 && a.D <= 3) {
     launch_km_pf<4>(a, tw2, items, st);
+    return;
+  }
+  if (ver == 6 && a.D <= 3) {
+    launch_km<true, 4, true, true, true>(a, tw2, items, st);
     return;
   }
   if (ver == 1)
@@ -1688,14 +1714,18 @@ static void launch_row_comb(const NttLaunch& a, const uint2* tw2, const CombineA
 
 bool ntt256_forward_combine(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, cudaStream_t st) {
   init_grids();
+  // CK32_COMB_EARLY: 2 = the combine operand rows are requested into L2 at
+  // the item start (default: +7-10% on this class, r2i), 1 = loaded into
+  // registers at the item start, 0 = loaded right before the store (round 1)
   static int early = -1;
   if (early < 0) {
     const char* e = std::getenv("CK32_COMB_EARLY");
-    early = e ? std::atoi(e) : 0;
+    early = e ? std::atoi(e) : 2;
   }
   const int row_items = a.njobs * (kR / kRRows) * a.batch;
   launch_col<false>(a, a.src, a.src_bs, st);
-  if (early) launch_row_comb<2>(a, tw2, cb, row_items, st);
+  if (early == 2) launch_row_comb<3>(a, tw2, cb, row_items, st);
+  else if (early) launch_row_comb<2>(a, tw2, cb, row_items, st);
   else launch_row_comb<1>(a, tw2, cb, row_items, st);
   return true;
 }

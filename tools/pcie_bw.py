@@ -29,3 +29,5 @@ def both(k):
     return f
 for k in (1, 2, 4):
     print(k, "h2d %.1f GB/s" % bw(h2d(k), 4*n), "d2h %.1f GB/s" % bw(d2h(k), 4*n))
+for k in (2, 4):
+    print(k, "h2d+d2h concurrently %.1f GB/s total" % bw(both(k), 8*n))
