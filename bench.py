@@ -145,12 +145,40 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
+        numa_local(local)
         backend = os.environ.get("CK32_DIST_BACKEND", "nccl")
+        t0 = time.perf_counter()
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        # force the communicator into existence now (NCCL creates it lazily)
+        # and say so, so a launcher can match ranks to GPUs
+        probe = torch.ones(1, device=torch.device("cuda", local) if backend == "nccl" else "cpu")
+        dist.all_reduce(probe)
+        print(f"[bench] rank {rank}/{world}: {backend} communicator up on cuda:{local} "
+              f"({torch.cuda.get_device_name(local)}, all-reduce check {int(probe.item())} == {world}) "
+              f"in {time.perf_counter() - t0:.2f} s", file=sys.stderr, flush=True)
     return world, rank, local
+
+
+def numa_local(device: int) -> None:
+    """Pin this rank's host threads to the CPUs NVML reports as local to its
+    GPU, so the pinned e2e buffers (first-touch) and the launch thread live on
+    the GPU's NUMA node.  Best effort: no NVML, no change."""
+    try:
+        import pynvml as nv
+
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(device)
+        words = nv.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        nv.nvmlShutdown()
+    except Exception:
+        pass
 
 
 def peaks():
