@@ -5,7 +5,7 @@
 // they declare -- NTT / INTT, base conversion, ModSwitch, automorphism, the
 // element-wise operations, ModUp / KeyMult / ModDown / key switching,
 // rescale, HMult, HRot, hoisting, HAdd / PAdd / PMult and the element-wise
-// part of decrypt -- as calls into the sm_100a library through its C ABI
+// part of decrypt, encode / decode -- as calls into the sm_100a library through its C ABI
 // (include/ck32_b200.h).  Linked in front of the reference's objects (whose
 // definitions of exactly these symbols are weakened, see Makefile), it turns
 // any reference caller into a GPU caller without touching the caller: the
@@ -14,8 +14,8 @@
 //
 // What stays the reference's: the data types (Polynomial with host rows,
 // BufferPool, RnsBasis, the Rational scale ledger), basis generation, table
-// construction, encode / decode and key / randomness sampling (host-side in
-// the reference too).  Every residue this backend hands back is canonical
+// construction and key / randomness sampling (host-side in the reference
+// too; their NTTs and element-wise products run here).  Every residue this backend hands back is canonical
 // in [0, q) -- the reference's correct() view of its lazy values, which every
 // reference consumer accepts; raw int32 equality with the CPU's lazy schedule
 // is not part of the contract.
@@ -24,6 +24,7 @@
 // lines); the counters (OpCounters) advance by the GPU library's counts,
 // which follow the reference's profile.
 #include <algorithm>
+#include <cmath>
 #include <complex>
 #include <cstdint>
 #include <cstring>
@@ -715,6 +716,48 @@ Ciphertext pmult(CkksContext& ctx, const Ciphertext& ct, const Plaintext& pt) {
   Ciphertext out = down_ct(g, o.u(), ctx, ct.level);
   out.scale = ct.scale * pt.scale;
   out.pending_rescale = ct.pending_rescale;
+  return out;
+}
+
+// encode (ckks.cpp:278-319): the GPU encoder replays the reference's FFT and
+// its x87 long-double scaling, so the residues are the reference's bit for bit
+Plaintext encode(CkksContext& ctx, std::span<const std::complex<double>> slots, const Rational& scale, uint32_t level,
+                 bool p_extend) {
+  const uint32_t n = ctx.params().n;
+  if (slots.size() > n / 2) throw std::invalid_argument("too many slots");
+  if (level < 1 || level > ctx.params().l) throw std::invalid_argument("level out of range");
+  if (scale <= 0 || log2_rational(scale) > 60.0) throw std::invalid_argument("scale out of the representable range");
+  Gpu& g = for_ctx(ctx);
+  const uint32_t pc = p_extend ? ctx.params().alpha : 0;
+  Dev z(g.h, std::max<size_t>(1, 4 * slots.size())), o(g.h, (size_t)(level + pc) * n);
+  if (!slots.empty()) check(ck_memcpy_h2d(g.h, z.u(), slots.data(), slots.size() * 16, nullptr));
+  check(ck_encode(g.h, reinterpret_cast<const double*>(z.u()), (uint32_t)slots.size(), log2_rational(scale), level,
+                  p_extend ? 1 : 0, o.u(), nullptr));
+  Plaintext pt;
+  pt.scale = scale;
+  pt.level = level;
+  pt.poly = down(g, o.u(), ctx.basis(), level, pc, Domain::Evaluation, true, &ctx.pool());
+  ctx.counters().ntt += level + pc;  // as the reference's encode counts it (ckks.cpp:317)
+  return pt;
+}
+
+// decode (ckks.cpp:321-362): slots within 2^-40 of the reference's (the GPU
+// rounds the centred CRT lift to double once, then scales by 2^-log2(scale))
+std::vector<std::complex<double>> decode(CkksContext& ctx, const Plaintext& pt) {
+  check_eval_mont(pt.poly, "decode");
+  const uint32_t n = ctx.params().n;
+  const double need_bits = log2_rational(pt.scale) + 40.0;  // the reference's prefix rule (ckks.cpp:326-333)
+  uint32_t c = 1;
+  double bits = std::log2((double)ctx.basis()->q_primes[0].q);
+  while (c < pt.level && bits < need_bits) bits += std::log2((double)ctx.basis()->q_primes[c++].q);
+  Gpu& g = for_ctx(ctx);
+  Dev x(g.h, (size_t)pt.level * n), z(g.h, (size_t)n / 2 * 4);
+  put_rows(g, pt.poly, 0, pt.level, x.u());
+  check(ck_decode(g.h, x.u(), pt.level, log2_rational(pt.scale), reinterpret_cast<double*>(z.u()), nullptr));
+  std::vector<std::complex<double>> out(n / 2);
+  check(ck_memcpy_d2h(g.h, out.data(), z.u(), out.size() * 16, nullptr));
+  check(ck_stream_sync(g.h, nullptr));
+  ctx.counters().intt += c;
   return out;
 }
 
