@@ -316,7 +316,20 @@ def key_switch(ctx: CkksContext, d: Polynomial, evk: EvaluationKey) -> Tuple[Pol
     return Polynomial(out[0], l), Polynomial(out[1], l)
 
 
-def hmult(ctx: CkksContext, x_in: Ciphertext, y_in: Ciphertext, relin: EvaluationKey) -> Ciphertext:
+def _out_tensor(ctx: CkksContext, shape, out: Optional[torch.Tensor]) -> torch.Tensor:
+    """The caller's output buffer (checked), or a fresh one.  Passing ``out``
+    keeps steady-state serving loops free of allocations (the caching
+    allocator's cudaMalloc synchronises the device)."""
+    if out is None:
+        return torch.empty(shape, dtype=torch.int32, device=ctx.device)
+    if tuple(out.shape) != tuple(shape) or out.dtype != torch.int32 or out.device != ctx.device:
+        raise ValueError(f"out must be an int32 tensor of shape {tuple(shape)} on {ctx.device}")
+    _ptr(out)
+    return out
+
+
+def hmult(ctx: CkksContext, x_in: Ciphertext, y_in: Ciphertext, relin: EvaluationKey,
+          out: Optional[torch.Tensor] = None) -> Ciphertext:
     """ckks.cpp:804-865 (merged ModDown+rescale unless params.lazy_rescale)."""
     if relin.kind != RELIN:
         raise ValueError("hmult needs a relinearization key")
@@ -333,7 +346,7 @@ def hmult(ctx: CkksContext, x_in: Ciphertext, y_in: Ciphertext, relin: Evaluatio
     lazy = ctx.params.lazy_rescale
     shape = list(x.data.shape)
     shape[-2] = l if lazy else l - 2
-    out = torch.empty(shape, dtype=torch.int32, device=ctx.device)
+    out = _out_tensor(ctx, shape, out)
     nat.call("ck_hmult", ctx.handle, l, x.batch, _ptr(x.data), _ptr(y.data), _ptr(relin.data), _ptr(out),
              ctx.stream())
     if lazy:
@@ -341,12 +354,13 @@ def hmult(ctx: CkksContext, x_in: Ciphertext, y_in: Ciphertext, relin: Evaluatio
     return Ciphertext(out, x.scale * y.scale / _qq(ctx, l), l - 2, False)
 
 
-def hrot(ctx: CkksContext, ct_in: Ciphertext, r: int, evk: EvaluationKey) -> Ciphertext:  # ckks.cpp:890-897
+def hrot(ctx: CkksContext, ct_in: Ciphertext, r: int, evk: EvaluationKey,
+         out: Optional[torch.Tensor] = None) -> Ciphertext:  # ckks.cpp:890-897
     ct = _flushed(ctx, ct_in)
     _check_pair(ctx, ct)
     if evk.kind != ROTATION or evk.rotation != r:
         raise ValueError("rotation key mismatch")
-    out = torch.empty_like(ct.data)
+    out = _out_tensor(ctx, ct.data.shape, out)
     nat.call("ck_hrot", ctx.handle, ct.level, ct.batch, _ptr(ct.data), int(r), _ptr(evk.data), _ptr(out),
              ctx.stream())
     return Ciphertext(out, ct.scale, ct.level, False)

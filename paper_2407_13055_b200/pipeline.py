@@ -43,8 +43,19 @@ class HostPipeline:
         self.d2h = torch.cuda.Stream(self.device)
         self.comp = [torch.cuda.Stream(self.device) for _ in range(depth)]
         self._bufs: List[List[torch.Tensor]] = [[] for _ in range(depth)]
+        self._obufs: List[List[torch.Tensor]] = [[] for _ in range(depth)]
+        self._drained = [None] * depth  # event: slot's output buffers copied to the host
         self._freed = [None] * depth   # event: slot's compute finished reading its inputs
         self._slot = 0
+
+    def _slot_outs(self, slot: int, host_out: Sequence[torch.Tensor]) -> List[torch.Tensor]:
+        bufs = self._obufs[slot]
+        want = [(self.chunk,) + tuple(h.shape[1:]) for h in host_out]
+        if len(bufs) != len(host_out) or any(tuple(b.shape) != w or b.dtype != h.dtype
+                                             for b, w, h in zip(bufs, want, host_out)):
+            bufs = [torch.empty(w, dtype=h.dtype, device=self.device) for w, h in zip(want, host_out)]
+            self._obufs[slot] = bufs
+        return bufs
 
     def _slot_bufs(self, slot: int, host_in: Sequence[torch.Tensor]) -> List[torch.Tensor]:
         bufs = self._bufs[slot]
@@ -55,12 +66,17 @@ class HostPipeline:
             self._bufs[slot] = bufs
         return bufs
 
-    def run(self, host_in: Sequence[torch.Tensor], fn: Callable[[List[torch.Tensor]], Sequence[torch.Tensor]],
-            host_out: Sequence[torch.Tensor]) -> torch.cuda.Event:
+    def run(self, host_in: Sequence[torch.Tensor], fn: Callable[..., Sequence[torch.Tensor]],
+            host_out: Sequence[torch.Tensor], outputs_in_place: bool = False) -> torch.cuda.Event:
         """Enqueue the whole batch; returns an event recorded after the last
         D2H (wait on it, or synchronise, before reading ``host_out``).  The
         caller's current stream is NOT made to wait, so back-to-back calls
-        overlap; order later work with ``stream.wait_event(returned)``."""
+        overlap; order later work with ``stream.wait_event(returned)``.
+
+        ``outputs_in_place``: ``fn(dev_inputs, dev_outputs)`` writes into
+        per-slot device output buffers the pipeline owns (e.g. through the
+        evaluator's ``out=`` arguments), so a steady-state step allocates no
+        device memory at all."""
         B = host_in[0].shape[0]
         if any(h.shape[0] != B for h in list(host_in) + list(host_out)):
             raise ValueError("host inputs and outputs must share the batch dimension")
@@ -88,16 +104,26 @@ class HostPipeline:
                 loaded = torch.cuda.Event()
                 loaded.record(self.h2d)
             s.wait_event(loaded)
+            if outputs_in_place:
+                obufs = self._slot_outs(slot, host_out)
+                if self._drained[slot] is not None:  # the slot's previous outputs reached the host
+                    s.wait_event(self._drained[slot])
             with torch.cuda.stream(s):
-                outs = fn([b[:n] for b in bufs])
+                outs = fn([b[:n] for b in bufs], [o[:n] for o in obufs]) if outputs_in_place else \
+                    fn([b[:n] for b in bufs])
                 done = torch.cuda.Event()
                 done.record(s)
             self._freed[slot] = done
             self.d2h.wait_event(done)
             with torch.cuda.stream(self.d2h):
                 for o, h in zip(outs, host_out):
-                    o.record_stream(self.d2h)  # allocated on s, read on d2h
+                    if not outputs_in_place:
+                        o.record_stream(self.d2h)  # allocated on s, read on d2h
                     h[lo:hi].copy_(o, non_blocking=True)
+                if outputs_in_place:
+                    drained = torch.cuda.Event()
+                    drained.record(self.d2h)
+                    self._drained[slot] = drained
         end = torch.cuda.Event()
         end.record(self.d2h)
         return end

@@ -386,6 +386,22 @@ def test_host_pipeline_equals_direct(chunk, depth):
     with pytest.raises(ValueError):
         pipe.run([X.data, hy], fn, [ho1, ho2])  # device tensor where a pinned host one is required
 
+    # results written into the pipeline's own per-slot buffers (the evaluator's out= arguments)
+    def fn_inplace(d, o):
+        cx = ckks.Ciphertext(d[0], s, level)
+        return (ckks.hmult(C, cx, ckks.Ciphertext(d[1], s, level), K, out=o[0]).data,
+                ckks.hrot(C, cx, 1, KR, out=o[1]).data)
+
+    ho1.zero_()
+    ho2.zero_()
+    for _ in range(3):
+        ev = pipe.run([hx, hy], fn_inplace, [ho1, ho2], outputs_in_place=True)
+    ev.synchronize()
+    np.testing.assert_array_equal(ho1.numpy().astype(np.uint32), want1)
+    np.testing.assert_array_equal(ho2.numpy().astype(np.uint32), want2)
+    with pytest.raises(ValueError):  # out= of the wrong shape
+        ckks.hmult(C, X, Y, K, out=torch.empty((B, 2, level, n), dtype=torch.int32, device="cuda"))
+
 
 def test_captured_step_replays_bit_exactly():
     """pipeline.CapturedStep: HMult + HRot captured in a CUDA graph, replayed

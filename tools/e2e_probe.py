@@ -23,19 +23,22 @@ relin = ckks.EvaluationKey(rows((D, 2), full)); rot = ckks.EvaluationKey(rows((D
 s = Fraction(1 << DB)
 hx = rows((B, 2), list(range(LV))).cpu().pin_memory(); hy = rows((B, 2), list(range(LV))).cpu().pin_memory()
 ho1 = torch.empty((B, 2, LV - 2, N), dtype=torch.int32).pin_memory(); ho2 = torch.empty((B, 2, LV, N), dtype=torch.int32).pin_memory()
-pipe = HostPipeline(dev, chunk=chunk, depth=2)
-def fn(d):
+depth = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+pipe = HostPipeline(dev, chunk=chunk, depth=depth)
+inplace = len(sys.argv) > 2 and sys.argv[2] == "inplace"
+def fn(d, o=None):
     cx = ckks.Ciphertext(d[0], s, LV)
-    return ckks.hmult(C, cx, ckks.Ciphertext(d[1], s, LV), relin).data, ckks.hrot(C, cx, 1, rot).data
+    return (ckks.hmult(C, cx, ckks.Ciphertext(d[1], s, LV), relin, out=o[0] if o else None).data,
+            ckks.hrot(C, cx, 1, rot, out=o[1] if o else None).data)
 st = torch.cuda.current_stream(dev)
-for _ in range(3): pipe.run([hx, hy], fn, [ho1, ho2])
+for _ in range(3): pipe.run([hx, hy], fn, [ho1, ho2], outputs_in_place=inplace)
 torch.cuda.synchronize()
 for rep in range(6):
     m0 = torch.cuda.memory_stats()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter(); a.record(st)
-    for _ in range(10): last = pipe.run([hx, hy], fn, [ho1, ho2])
+    for _ in range(10): last = pipe.run([hx, hy], fn, [ho1, ho2], outputs_in_place=inplace)
     st.wait_event(last); b.record(st); torch.cuda.synchronize()
     ms = a.elapsed_time(b); m1 = torch.cuda.memory_stats()
-    print(f"chunk {chunk} rep {rep}: {2 * B * 10 / (ms / 1e3):.0f} ops/s  host {1e3 * (time.perf_counter() - t0):.0f} ms  "
+    print(f"chunk {chunk} depth {depth} inplace {inplace} rep {rep}: {2 * B * 10 / (ms / 1e3):.0f} ops/s  host {1e3 * (time.perf_counter() - t0):.0f} ms  "
           f"cudaMalloc +{m1.get('num_device_alloc', 0) - m0.get('num_device_alloc', 0)} retries +{m1.get('num_alloc_retries', 0) - m0.get('num_alloc_retries', 0)}")
