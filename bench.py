@@ -715,24 +715,28 @@ def limb_measure(args, world, rank, local, graph=True):
         dist.barrier()
     ms = dp.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
     launches = C.launch_count() - l0
-    # One process driving every shard on one stream (virtual shards, or G = 1):
-    # the whole step replayed as one CUDA graph, which removes the host launch
-    # cost of the ~G x 30 small kernels per mechanism.  (Across processes the
-    # peer exchange's epochs are host-side values, so a captured step could
-    # not be replayed there.)
+    # The whole step replayed as one CUDA graph per rank, which removes the
+    # host launch cost of the ~30 small kernels per mechanism and shard: the
+    # peer exchange keeps its epochs and buffer parities in device memory, so
+    # a captured step replays across processes too.
     graph_ms = None
-    if graph and world == 1:
+    if graph and (world == 1 or args.exchange == "peer"):
         from paper_2407_13055_b200.pipeline import CapturedStep
         cap = CapturedStep(dev, step)
         for _ in range(max(args.warmup, 1)):
             cap.replay()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize(dev)
         a.record(st)
         for _ in range(args.steps):
             cap.replay()
         b.record(st)
         torch.cuda.synchronize(dev)
-        graph_ms = a.elapsed_time(b)
+        if world > 1:
+            dist.barrier()
+        graph_ms = dp.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
         del cap
     # correctness spot check against the single-device path (rank-local rows)
     if world == 1:

@@ -813,11 +813,13 @@ struct Context {
   }
 
   // ------------------------------------------------------------- launches --
+  // jobs_override: a device job table to use instead of the plan's (same
+  // count) -- the limb-sharded peer exchange selects its parity on the device
   void run_ntt(const NttPlan& pl, bool inverse, int batch, const uint32_t* src, uint64_t src_bs, uint32_t* dst,
-               uint64_t dst_bs, int entry, cudaStream_t st) {
+               uint64_t dst_bs, int entry, cudaStream_t st, const RowJob* jobs_override = nullptr) {
     if (pl.njobs == 0 || batch == 0) return;
     NttLaunch a;
-    a.jobs = pl.blob.at<RowJob>(pl.jobs_off);
+    a.jobs = jobs_override ? jobs_override : pl.blob.at<RowJob>(pl.jobs_off);
     a.njobs = pl.njobs;
     a.batch = batch;
     a.src = src;
@@ -1125,6 +1127,7 @@ struct Context {
 struct Shard {
   ~Shard() {
     if (xbuf) cudaFree(xbuf);
+    if (ctl) cudaFree(ctl);
   }
   Context* c = nullptr;
   uint32_t G = 1, s = 0, qlo = 0, qhi = 0, plo = 0, phi = 0, qmax = 0, pmax = 0;
@@ -1148,8 +1151,22 @@ struct Shard {
   uint32_t local_row(uint32_t level, uint32_t g) const { return g < c->L ? g - qlo : lq(level) + (g - c->L - plo); }
   uint32_t smax(int kind) const { return kind == 0 ? pmax : kind == 1 ? 2 : pmax + 2; }
 
+  // The phase-1 INTT jobs of the peer exchange for both buffer parities:
+  // [2][njobs], dst_off relative to the exchange buffer's base (kind 0: the
+  // ModUp send buffers, 1: the switch send buffers), so the parity can be
+  // chosen on the device (k_shard_advance) and a captured step replays.
+  std::vector<RowJob> parity_jobs(const std::vector<RowJob>& jobs, int kind) const {
+    std::vector<RowJob> out;
+    for (uint32_t par = 0; par < 2; ++par)
+      for (RowJob j : jobs) {
+        j.dst_off += kind == 0 ? par * qmax : 2 * qmax + par * 2 * (pmax + 2);
+        out.push_back(j);
+      }
+    return out;
+  }
   struct UpPlan {
     NttPlan intt, ntt;
+    size_t intt_par_off = 0;
     BconvPlan bc;
     Blob maps;
     size_t digit_off = 0, prime_off = 0, erow_off = 0;
@@ -1157,6 +1174,7 @@ struct Shard {
   };
   struct DownPlan {
     NttPlan intt, ntt;
+    size_t intt_par_off = 0;
     BconvPlan bc;
     Blob consts;  // dinv [lqo]
     uint32_t sc = 0, smax = 0, vrows = 0, lqo = 0, out_q = 0, own_sc = 0;
@@ -1220,6 +1238,7 @@ struct Shard {
     pl->intt.jobs_off = pl->intt.blob.add(ijobs);
     pl->intt.exits_off = pl->intt.blob.add(exits);
     pl->intt.njobs = (int)ijobs.size();
+    pl->intt_par_off = pl->intt.blob.add(parity_jobs(ijobs, 0));
     pl->intt.blob.upload();
     pl->ntt.jobs_off = pl->ntt.blob.add(njobs);
     pl->ntt.njobs = (int)njobs.size();
@@ -1324,6 +1343,7 @@ struct Shard {
     pl->intt.jobs_off = pl->intt.blob.add(ijobs);
     pl->intt.exits_off = pl->intt.blob.add(exits);
     pl->intt.njobs = (int)ijobs.size();
+    pl->intt_par_off = pl->intt.blob.add(parity_jobs(ijobs, 1));
     pl->intt.blob.upload();
     pl->ntt.jobs_off = pl->ntt.blob.add(njobs);
     pl->ntt.njobs = (int)njobs.size();
@@ -1366,7 +1386,14 @@ struct Shard {
   void* xbuf = nullptr;
   uint64_t up_words = 0, sw_words = 0, xbytes = 0;
   std::vector<uint64_t> peers;  // exchange base of every rank (own included)
-  uint32_t epoch[2] = {0, 0};
+  // Device-side exchange state (this rank only, not shared): the epoch of
+  // each exchange kind, and what the current epoch's buffer parity selects
+  // -- the phase-1 INTT job table and the phase-2 BConv source-row table.
+  // Every kernel of a phase takes fixed pointers, so a step that uses the
+  // peer exchange can be captured in a CUDA graph and replayed.
+  uint32_t* ctl = nullptr;      // [2] epochs
+  RowJob* jobs_cur[2] = {nullptr, nullptr};
+  uint64_t* rows_cur[2] = {nullptr, nullptr};
   Blob sig_tab;                 // [2 kinds][G] peer flag addresses for this rank
   Blob up_tab;                  // [2 parities][L] ModUp source-row addresses
   std::map<std::pair<int, uint32_t>, std::unique_ptr<Blob>> down_tab;  // [2 parities][2 sc]
@@ -1386,6 +1413,18 @@ struct Shard {
       xbytes = err_off() + 256;
       CK_CUDA(cudaMalloc(&xbuf, xbytes));
       CK_CUDA(cudaMemset(xbuf, 0, xbytes));
+      // [2] epochs | jobs_cur [qmax] + [2 (pmax + 2)] | rows_cur [L] + [2 (alpha + 2)]
+      const size_t nj0 = qmax, nj1 = 2ull * (pmax + 2), nr0 = c->L, nr1 = 2ull * (c->alpha + 2);
+      const size_t bytes = 16 + (nj0 + nj1) * sizeof(RowJob) + (nr0 + nr1) * 8 + 64;
+      CK_CUDA(cudaMalloc(&ctl, bytes));
+      CK_CUDA(cudaMemset(ctl, 0, bytes));
+      char* p = reinterpret_cast<char*>(ctl) + 16;
+      jobs_cur[0] = reinterpret_cast<RowJob*>(p);
+      jobs_cur[1] = jobs_cur[0] + nj0;
+      p += (nj0 + nj1) * sizeof(RowJob);
+      p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
+      rows_cur[0] = reinterpret_cast<uint64_t*>(p);
+      rows_cur[1] = rows_cur[0] + nr0;
     }
     if (bytes) *bytes = xbytes;
     return xbuf;
@@ -1416,11 +1455,12 @@ struct Shard {
     // written yet).  Callers barrier after set_peers, so no peer publishes
     // into this buffer before the reset has landed.
     CK_CUDA(cudaMemset(static_cast<char*>(xbuf) + flag_off(0, 0), 0, 2ull * G * 4 + 4));
+    CK_CUDA(cudaMemset(ctl, 0, 8));  // epochs restart with the peer set
     CK_CUDA(cudaDeviceSynchronize());
-    epoch[0] = epoch[1] = 0;
   }
   bool peer_mode() const { return !peers.empty(); }
-  const uint64_t* down_rows(int kind, uint32_t level, uint32_t par) {
+  // [2 parities][2 sc] source-row addresses of a drop-and-divide exchange
+  const uint64_t* down_rows(int kind, uint32_t level) {
     auto key = std::make_pair(kind, level);
     auto it = down_tab.find(key);
     if (it == down_tab.end()) {
@@ -1441,11 +1481,18 @@ struct Shard {
       b->upload();
       it = down_tab.emplace(key, std::move(b)).first;
     }
-    return it->second->at<uint64_t>(0) + (size_t)par * 2 * down_plan(kind, level).sc;
+    return it->second->at<uint64_t>(0);
   }
-  void peer_wait(int kind, cudaStream_t st) {
+  // phase 2 head: wait for every peer's flag of this kind's current (device)
+  // epoch, then select that epoch's parity of the row table into rows_cur
+  void peer_wait(int kind, const uint64_t* rows2, int nrows, cudaStream_t st) {
     if (!peer_mode()) throw InvalidArgument("no recv buffer and no peer exchange set up");
-    shard_wait(own_flags(kind), (int)G, epoch[kind], err_word(), timeout_ns, st);
+    shard_wait(own_flags(kind), (int)G, ctl + kind, err_word(), timeout_ns, rows2, rows_cur[kind], nrows, st);
+    c->launches += 1;
+  }
+  // phase 1 head: advance this kind's epoch and select the INTT job parity
+  void peer_advance(int kind, const NttPlan& intt, size_t par_off, cudaStream_t st) {
+    shard_advance(ctl + kind, intt.blob.at<RowJob>(par_off), jobs_cur[kind], intt.njobs, st);
     c->launches += 1;
   }
   uint32_t peer_error() const {
@@ -1459,10 +1506,9 @@ struct Shard {
     const UpPlan& pl = up_plan(level);
     if (!send) {
       if (!peer_mode()) throw InvalidArgument("no send buffer and no peer exchange set up");
-      const uint32_t e = ++epoch[0];
-      send = reinterpret_cast<uint32_t*>(static_cast<char*>(xbuf) + up_off(e & 1));
-      c->run_ntt(pl.intt, true, 1, d, 0, send, 0, 0, st);
-      shard_signal(sig_tab.at<uint64_t>(0), (int)G, e, st);
+      peer_advance(0, pl.intt, pl.intt_par_off, st);
+      c->run_ntt(pl.intt, true, 1, d, 0, static_cast<uint32_t*>(xbuf), 0, 0, st, jobs_cur[0]);
+      shard_signal(sig_tab.at<uint64_t>(0), (int)G, ctl + 0, st);
       c->launches += 1;
     } else {
       c->run_ntt(pl.intt, true, 1, d, 0, send, 0, 0, st);
@@ -1478,9 +1524,8 @@ struct Shard {
     const uint64_t* rows = nullptr;
     if (!recv) {  // peer exchange: wait for every rank's phase 1, read their rows in place
       if (!peer_mode()) throw InvalidArgument("no recv buffer and no peer exchange set up");
-      const uint32_t e = epoch[0];
-      peer_wait(0, st);
-      rows = up_tab.at<uint64_t>(0) + (size_t)(e & 1) * c->L;
+      peer_wait(0, up_tab.at<uint64_t>(0), (int)c->L, st);
+      rows = rows_cur[0];
     } else {
       for (uint32_t t = 0; t < G; ++t) {  // gathered blocks -> global row order
         const uint32_t cnt = lq_of(t, level);
@@ -1523,10 +1568,9 @@ struct Shard {
     const DownPlan& pl = down_plan(kind, level);
     if (!send) {
       if (!peer_mode()) throw InvalidArgument("no send buffer and no peer exchange set up");
-      const uint32_t e = ++epoch[1];
-      send = reinterpret_cast<uint32_t*>(static_cast<char*>(xbuf) + sw_off(e & 1));
-      c->run_ntt(pl.intt, true, 1, v, 0, send, 0, 0, st);
-      shard_signal(sig_tab.at<uint64_t>(0) + G, (int)G, e, st);
+      peer_advance(1, pl.intt, pl.intt_par_off, st);
+      c->run_ntt(pl.intt, true, 1, v, 0, static_cast<uint32_t*>(xbuf), 0, 0, st, jobs_cur[1]);
+      shard_signal(sig_tab.at<uint64_t>(0) + G, (int)G, ctl + 1, st);
       c->launches += 1;
     } else {
       c->run_ntt(pl.intt, true, 1, v, 0, send, 0, 0, st);
@@ -1542,9 +1586,8 @@ struct Shard {
     const uint64_t* rows = nullptr;
     if (!recv) {  // peer exchange
       if (!peer_mode()) throw InvalidArgument("no recv buffer and no peer exchange set up");
-      const uint32_t e = epoch[1];
-      peer_wait(1, st);
-      rows = down_rows(kind, level, e & 1);
+      peer_wait(1, down_rows(kind, level), (int)(2 * pl.sc), st);
+      rows = rows_cur[1];
     } else {
       uint32_t off = 0;
       for (uint32_t t = 0; t < G; ++t) {  // [G][2][smax] -> [2][sc] in gathered order
@@ -2917,7 +2960,7 @@ ck_status ck_shard_modup_keymult(ck_shard* sh, uint32_t level, const uint32_t* r
     if (!s->peer_mode()) check_ptr(recv);
     check_ptr(evk);
     if (s->up_plan(level).rows == 0) {  // nothing owned at this level (a peer rank still waits: buffer reuse)
-      if (!recv) s->peer_wait(0, S(stream));
+      if (!recv) s->peer_wait(0, s->up_tab.at<uint64_t>(0), (int)s->c->L, S(stream));
       return;
     }
     check_ptr(v);

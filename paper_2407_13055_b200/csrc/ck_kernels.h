@@ -228,11 +228,17 @@ struct ShardTailLaunch {
   const uint32_t* err = nullptr;   // peer exchange error word: when set, out is poisoned (0xFFFFFFFF)
 };
 void shard_tail(int n, int rows, const ShardTailLaunch& a, cudaStream_t st);
-// peer exchange handshake (shard.cu): signal stores `epoch` (release, system
-// scope) to the G flag words sig[0..G); wait spins (acquire, system scope)
-// until flags[t] >= epoch for every t < G, or sets *err and gives up after
-// `timeout_ns`.
-void shard_signal(const uint64_t* sig, int G, uint32_t epoch, cudaStream_t st);
-void shard_wait(const uint32_t* flags, int G, uint32_t epoch, uint32_t* err, uint64_t timeout_ns, cudaStream_t st);
+// peer exchange handshake (shard.cu): signal stores the epoch (release,
+// system scope) to the G flag words sig[0..G); wait spins (acquire, system
+// scope) until flags[t] >= epoch for every t < G, or sets *err and gives up
+// after `timeout_ns`.
+// Epochs live in device memory (*epoch): advance increments it and selects
+// the parity of the phase-1 INTT job table (jobs2 [2][njobs] -> jobs_cur);
+// wait also selects the parity of the BConv row table (rows2 [2][nrows] ->
+// rows_cur).  Nothing host-chosen per exchange: graph-capturable.
+void shard_advance(uint32_t* epoch, const RowJob* jobs2, RowJob* jobs_cur, int njobs, cudaStream_t st);
+void shard_signal(const uint64_t* sig, int G, const uint32_t* epoch, cudaStream_t st);
+void shard_wait(const uint32_t* flags, int G, const uint32_t* epoch, uint32_t* err, uint64_t timeout_ns,
+                const uint64_t* rows2, uint64_t* rows_cur, int nrows, cudaStream_t st);
 
 }  // namespace ck

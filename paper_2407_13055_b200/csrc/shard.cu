@@ -105,12 +105,24 @@ __global__ void __launch_bounds__(kST) k_shard_tail(ShardTailLaunch a, int n) {
 // BConv that reads the peers' buffers is the next kernel on the stream.  The
 // spin is bounded (globaltimer) so a missing peer reports an error instead of
 // hanging the GPU.
-__global__ void k_shard_signal(const uint64_t* __restrict__ sig, int G, uint32_t epoch) {
+// The epoch lives in device memory (advanced by k_shard_advance at the head
+// of phase 1), so no kernel of an exchange carries a host-chosen value and a
+// captured step replays correctly.
+__global__ void k_shard_advance(uint32_t* epoch, const RowJob* __restrict__ jobs2, RowJob* __restrict__ jobs_cur,
+                                int njobs) {
+  const uint32_t e = *epoch + 1;  // every thread reads the old value before thread 0 stores the new one
+  for (int t = threadIdx.x; t < njobs; t += blockDim.x) jobs_cur[t] = jobs2[(e & 1) * njobs + t];
+  __syncthreads();
+  if (threadIdx.x == 0) *epoch = e;
+}
+
+__global__ void k_shard_signal(const uint64_t* __restrict__ sig, int G, const uint32_t* __restrict__ epoch) {
   const int t = threadIdx.x;
   if (t >= G) return;
+  const uint32_t e = *epoch;
   uint32_t* p = reinterpret_cast<uint32_t*>(sig[t]);
   asm volatile("fence.sc.sys;\n" ::: "memory");
-  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(epoch) : "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(e) : "memory");
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -119,31 +131,43 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-__global__ void k_shard_wait(const uint32_t* __restrict__ flags, int G, uint32_t epoch, uint32_t* err,
-                             uint64_t timeout_ns) {
+// Phase 2 head: spin until every peer's flag reaches this rank's current
+// epoch, then copy the epoch's parity of the BConv source-row table
+// (rows2 [2][nrows]) into rows_cur, the table the BConv kernel reads.
+__global__ void k_shard_wait(const uint32_t* __restrict__ flags, int G, const uint32_t* __restrict__ epoch,
+                             uint32_t* err, uint64_t timeout_ns, const uint64_t* __restrict__ rows2,
+                             uint64_t* __restrict__ rows_cur, int nrows) {
   const int t = threadIdx.x;
-  if (t >= G) return;
-  const uint64_t t0 = globaltimer();
-  while (true) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flags + t) : "memory");
-    if ((int32_t)(v - epoch) >= 0) break;
-    if (globaltimer() - t0 > timeout_ns) {
-      atomicExch(err, 1u);
-      break;
+  const uint32_t e = *epoch;
+  if (t < G) {
+    const uint64_t t0 = globaltimer();
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flags + t) : "memory");
+      if ((int32_t)(v - e) >= 0) break;
+      if (globaltimer() - t0 > timeout_ns) {
+        atomicExch(err, 1u);
+        break;
+      }
+      __nanosleep(200);
     }
-    __nanosleep(200);
   }
+  for (int r = t; r < nrows; r += blockDim.x) rows_cur[r] = rows2[(e & 1) * nrows + r];
 }
 
 }  // namespace
 
-void shard_signal(const uint64_t* sig, int G, uint32_t epoch, cudaStream_t st) {
+void shard_advance(uint32_t* epoch, const RowJob* jobs2, RowJob* jobs_cur, int njobs, cudaStream_t st) {
+  k_shard_advance<<<1, 64, 0, st>>>(epoch, jobs2, jobs_cur, njobs);
+}
+
+void shard_signal(const uint64_t* sig, int G, const uint32_t* epoch, cudaStream_t st) {
   k_shard_signal<<<1, 32 * ((G + 31) / 32), 0, st>>>(sig, G, epoch);
 }
 
-void shard_wait(const uint32_t* flags, int G, uint32_t epoch, uint32_t* err, uint64_t timeout_ns, cudaStream_t st) {
-  k_shard_wait<<<1, 32 * ((G + 31) / 32), 0, st>>>(flags, G, epoch, err, timeout_ns);
+void shard_wait(const uint32_t* flags, int G, const uint32_t* epoch, uint32_t* err, uint64_t timeout_ns,
+                const uint64_t* rows2, uint64_t* rows_cur, int nrows, cudaStream_t st) {
+  k_shard_wait<<<1, 64, 0, st>>>(flags, G, epoch, err, timeout_ns, rows2, rows_cur, nrows);
 }
 
 void shard_key_mult(int n, const ShardKeyMultLaunch& a, cudaStream_t st) {

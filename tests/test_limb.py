@@ -355,6 +355,16 @@ def _ipc_worker(rank, world, port, q):
             out.append(ev.hrot(l, [x], 3, [k])[0].cpu().numpy())
             out.append(ev.rescale(l, [x])[0].cpu().numpy())
             out.append(ev.rescale(l, [x])[0].cpu().numpy())
+        # the same exchanges captured once per rank in a CUDA graph and replayed:
+        # the epochs and buffer parities advance on the device
+        from paper_2407_13055_b200.pipeline import CapturedStep
+
+        cap = CapturedStep(C.device, lambda: (ev.hmult(l, [x], [y], [k])[0], ev.hrot(l, [x], 3, [k])[0]))
+        for _ in range(3):
+            m, r = cap.replay()
+        torch.cuda.synchronize()
+        out.append(m.cpu().numpy())
+        out.append(r.cpu().numpy())
         torch.cuda.synchronize()
         q.put((rank, out, xch.errors()))
         dist.barrier()
@@ -369,7 +379,8 @@ def _ipc_worker(rank, world, port, q):
 def test_gpu_ipc_peer_exchange_two_processes():
     """Config 4's peer-memory exchange across processes (CUDA IPC, flags with
     system-scope release / acquire): both ranks share cuda:0 here; the same
-    code maps NVLink peers on a multi-GPU node.  Bit-exact vs the oracle."""
+    code maps NVLink peers on a multi-GPU node.  Bit-exact vs the oracle,
+    eagerly and replayed from a CUDA graph captured on each rank."""
     from pyoracle import Oracle
 
     with socket.socket() as s:
@@ -397,6 +408,6 @@ def test_gpu_ipc_peer_exchange_two_processes():
     hr = np.stack([_canon(O, ob, l), _canon(O, oa, l)])
     ob, oa = O.rescale(l, xb, xa)
     rs = np.stack([_canon(O, ob, l - 2), _canon(O, oa, l - 2)])
-    for i, want in enumerate([hm, hr, rs, rs] * 2):
+    for i, want in enumerate([hm, hr, rs, rs] * 2 + [hm, hr]):
         got = np.concatenate([parts[0][i], parts[1][i]], axis=1).astype(np.int64)
         np.testing.assert_array_equal(got, want)
