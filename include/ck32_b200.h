@@ -351,7 +351,9 @@ ck_status ck_sample_uniform(ck_rng* rng, const uint32_t* q, uint32_t rows, uint3
  * relies on each rank's phases being stream-ordered.  After a timeout the
  * phase-2 outputs are poisoned (0xFFFFFFFF, never a canonical residue) and
  * ck_shard_peer_error reports it; ck_shard_set_peers clears the flag and
- * error words (callers barrier after it). */
+ * error words (callers barrier after it).  The epochs and buffer parities
+ * are kept in device memory, so a sequence of phases captured in a CUDA graph
+ * on every rank replays correctly. */
 ck_status ck_shard_exchange_buffer(ck_shard* sh, void** base, uint64_t* bytes);
 ck_status ck_shard_set_peers(ck_shard* sh, const uint64_t* bases, uint32_t world);
 ck_status ck_shard_set_timeout(ck_shard* sh, uint64_t timeout_ns);
