@@ -1025,7 +1025,7 @@ struct Context {
                    4.0 * n * B * (pl.ntt_rows + level + 2.0 * (level + alpha)) + (fold ? 8.0 * n * level * B : 0.0) +
                        4.0 * n * 2.0 * pl.D * (level + alpha),
                    1, st);
-      row_keymult(a, d_tw2f, st);
+      row_keymult(a, d_tw2f, st, d_fwd);
     }
     launches += 2;
     counters[0] += B;

@@ -153,7 +153,9 @@ struct KeyMultLaunch {
 void key_mult(int n, const KeyMultLaunch& a, cudaStream_t st);
 // N = 2^16: forward NTT row pass of every digit's extension row fused with
 // KeyMult (ntt256.cu); `ext` holds the column-pass output.
-void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st);
+// fwd_full: the per-prime forward tables [prime][N] {w, w'} (the
+// 8-coefficient-per-thread variant reads its row twiddles from them)
+void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, const uint2* fwd_full = nullptr);
 
 // drop-and-divide combine (ckks.cpp:643-651): o = (v - o) * div_inv (Montgomery)
 void combine(int n, int rows, int npoly, int batch, const uint32_t* v, uint64_t v_ps, uint64_t v_bs, uint32_t* o,

@@ -1352,9 +1352,228 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult_pf(KeyMultLaunch a, c
   cp_wait<0>();
 }
 
+// k_row_keymult8: the fused row pass + KeyMult with 8 coefficients per
+// thread (32 threads per 256-point row, one row per warp, 4-row tiles)
+// instead of 16: 2 x 8 int64 accumulators instead of 2 x 16, so ~80
+// registers and 6 CTAs (24 warps) per SM instead of 4 (16 warps) -- the
+// kernel is latency-bound at 16 warps.  The row transform runs as 3 + 3 + 2
+// radix-2 stages with two warp-local exchanges through padded shared memory
+// (pad(c) = c + 4 (c >> 5): conflict-free for all three layouts); twiddles in
+// natural per-row order T_r[2^s - 1 + B] = F[(256 << s) + (r << s) + B]
+// (the reference's forward table, ntt.cpp:124-128), staged once per
+// (prime, row tile) and reused for every batch item.
+constexpr int kK8Rows = 4;                       // rows per CTA (one per warp)
+constexpr int kK8Stride = 288;                   // 256 + 32 padding words
+__device__ __forceinline__ int pad8(int c) { return c + 4 * (c >> 5); }
+constexpr int kK8Smem = (3 * kK8Rows * kK8Stride) * 4 + kK8Rows * 256 * 8;  // 3 digit tiles + twiddles
+
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, const uint2* __restrict__ fwd) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);                          // [3][4][288]
+  uint2* tws = reinterpret_cast<uint2*>(smraw + 3 * kK8Rows * kK8Stride * 4);   // [4][256]
+  uint2* T = tws + warp * 256;
+  constexpr int kTiles = kR / kK8Rows;
+  const int rows = a.level + a.alpha, B = a.batch;
+  const uint32_t LA = (uint32_t)(a.L + a.alpha);
+  const int items = rows * kTiles * B;  // (row i, tile, b), b fastest
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
+  const int lhi = lane >> 2, llo = lane & 3;
+  if (i0 >= i1) return;
+  // item cursor (row i, tile, b), b fastest: advanced incrementally (no
+  // divisions per item), per-(i, tile) values refreshed when b wraps
+  int b = i0 % B, tile = (i0 / B) % kTiles, i = (i0 / B) / kTiles;
+  int g = 0, r = 0;
+  PrimeDev P{};
+  uint32_t q = 0, q2 = 0, q4 = 0;
+  for (int it = i0; it < i1; ++it) {
+    __syncwarp();  // the warp is done with the previous item's buffers
+    if (it == i0 || b == 0) {  // new (row, tile): prime, and this row's 255 forward twiddles (natural order)
+      g = i < a.level ? i : a.L + (i - a.level);
+      r = tile * kK8Rows + warp;  // this warp's row of the 256 x 256 limb matrix
+      P = a.primes[g];
+      q = P.q;
+      q2 = P.q2;
+      q4 = 2 * P.q2;
+      const uint2* F = fwd + (size_t)g * kN;
+      for (int e = lane; e < 255; e += 32) {
+        const int s = 31 - __clz(e + 1), blk = e + 1 - (1 << s);
+        T[e] = __ldg(&F[(256 << s) + (r << s) + blk]);
+      }
+    }
+    // all digits' extension rows at once (one cp.async group per digit)
+    for (int k = 0; k < a.D; ++k) {
+      const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+      if (!(i >= lo && i < hi)) {
+        const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)r * kR;
+        uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int c = 4 * (lane + 32 * m);
+          cp16(line + pad8(c), gsrc + c);
+        }
+      }
+      cp_commit();
+    }
+    const size_t rofs = (size_t)r * kR + 8 * lane;  // this thread's 8 coefficients after the transform
+    if (i < a.level && (lane & 3) == 0) {  // own-digit and fold rows into L2 now (plain loads later), 1 per line
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.d + b * a.d_bs + (size_t)i * kN + rofs));
+      if (a.fold) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fold + b * a.fold_bs + (size_t)i * kN + rofs));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + rofs));
+      }
+    }
+    uint64_t s0[8], s1[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s0[j] = s1[j] = 0;
+    for (int k = 0; k < a.D; ++k) {
+      const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+      uint4 kb[2], ka[2];  // key halves first: their L2 latency hides behind the butterflies
+      {
+        const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
+        const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          kb[m] = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
+          ka[m] = __ldg(reinterpret_cast<const uint4*>(ea + 4 * m));
+        }
+      }
+      uint32_t v[8];
+      if (i >= lo && i < hi) {  // the digit's own row (ModUp pass-through), evaluation form already
+        const uint32_t* dr = a.d + b * a.d_bs + (size_t)i * kN + rofs;
+        const uint4 x0 = *reinterpret_cast<const uint4*>(dr), x1 = *reinterpret_cast<const uint4*>(dr + 4);
+        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+      } else {
+        const int pend = a.D - 1 - k;
+        if (pend >= 2) cp_wait<2>();
+        else if (pend == 1) cp_wait<1>();
+        else cp_wait<0>();
+        __syncwarp();
+        uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
+        // phase A: c = lane + 32 j, stages 0..2 (bits 7..5), row-uniform twiddles
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = line[pad8(lane + 32 * j)];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int d = 4 >> t;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = T[(1 << t) - 1 + blk];
+            if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) line[pad8(lane + 32 * j)] = v[j];
+        __syncwarp();
+        // phase B: c = 32 lhi + 4 j + llo, stages 3..5 (bits 4..2)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = line[pad8(32 * lhi + 4 * j + llo)];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int d = 4 >> t, sg = 3 + t;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = T[(1 << sg) - 1 + (lhi << t) + blk];
+            if (sg % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) line[pad8(32 * lhi + 4 * j + llo)] = v[j];
+        __syncwarp();
+        // phase C: c = 8 lane + j, stages 6, 7 (bits 1, 0)
+        {
+          const uint4 x0 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane));
+          const uint4 x1 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane + 4));
+          v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+          v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int d = 2 >> t, sg = 6 + t;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = T[(1 << sg) - 1 + (lane << (t + 1)) + blk];
+            if (sg % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = canon8(v[j], q, q2, q4);
+      }
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        s0[4 * m] = mac_wide(s0[4 * m], v[4 * m], kb[m].x);
+        s0[4 * m + 1] = mac_wide(s0[4 * m + 1], v[4 * m + 1], kb[m].y);
+        s0[4 * m + 2] = mac_wide(s0[4 * m + 2], v[4 * m + 2], kb[m].z);
+        s0[4 * m + 3] = mac_wide(s0[4 * m + 3], v[4 * m + 3], kb[m].w);
+        s1[4 * m] = mac_wide(s1[4 * m], v[4 * m], ka[m].x);
+        s1[4 * m + 1] = mac_wide(s1[4 * m + 1], v[4 * m + 1], ka[m].y);
+        s1[4 * m + 2] = mac_wide(s1[4 * m + 2], v[4 * m + 2], ka[m].z);
+        s1[4 * m + 3] = mac_wide(s1[4 * m + 3], v[4 * m + 3], ka[m].w);
+      }
+      if ((k % 6) == 5) {  // keep the sums below q 2^32 (value unchanged mod q, rescaled by R)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s0[j] = shoup_mul(mont_reduce64(s0[j], q, P.qinv_neg), P.r, P.r_sh, q);
+          s1[j] = shoup_mul(mont_reduce64(s1[j], q, P.qinv_neg), P.r, P.r_sh, q);
+        }
+      }
+    }
+    if (a.fold && i < a.level) {  // merged HMult: v += P * d0 / d1 (ckks.cpp:831-842)
+      const uint32_t pm = a.p_mont[i];
+      const uint32_t* f0 = a.fold + b * a.fold_bs + (size_t)i * kN + rofs;
+      const uint32_t* f1 = a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + rofs;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const uint4 x0 = *reinterpret_cast<const uint4*>(f0 + 4 * m);
+        const uint4 x1 = *reinterpret_cast<const uint4*>(f1 + 4 * m);
+        s0[4 * m] = mac_wide(s0[4 * m], x0.x, pm);
+        s0[4 * m + 1] = mac_wide(s0[4 * m + 1], x0.y, pm);
+        s0[4 * m + 2] = mac_wide(s0[4 * m + 2], x0.z, pm);
+        s0[4 * m + 3] = mac_wide(s0[4 * m + 3], x0.w, pm);
+        s1[4 * m] = mac_wide(s1[4 * m], x1.x, pm);
+        s1[4 * m + 1] = mac_wide(s1[4 * m + 1], x1.y, pm);
+        s1[4 * m + 2] = mac_wide(s1[4 * m + 2], x1.z, pm);
+        s1[4 * m + 3] = mac_wide(s1[4 * m + 3], x1.w, pm);
+      }
+    }
+    uint32_t* o0 = a.v + b * a.v_bs + (size_t)i * kN + rofs;
+    uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv_neg), q)));
+      stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv_neg), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv_neg), q)));
+    }
+    if (++b == B) {
+      b = 0;
+      if (++tile == kTiles) {
+        tile = 0;
+        ++i;
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
 }  // namespace
 
-// CK32_KM selects the k_row_keymult variant for A/B runs: 0 = key halves
+// CK32_KM selects the k_row_keymult variant for A/B runs: 7 = k_row_keymult8
+// (default when D <= 3), 6 = 0 + L2 prefetch of own / fold rows, 5 =
+// k_row_keymult_pf; 0 = key halves
 // loaded before the row pass, all digit tiles of an item requested at once
 // (default when D <= 3), 3 = the same with per-digit tile loads (4.83 TB/s),
 // 1 = per-digit loads at 3 CTAs/SM (4.20), 2 = key halves loaded after the
@@ -1390,11 +1609,11 @@ static void launch_km_pf(const KeyMultLaunch& a, const uint2* tw2, int items, cu
   k_row_keymult_pf<MINB><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
 }
 
-void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
+void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, const uint2* fwd_full) {
   static int ver = -1;
-  if (ver < 0) {
+  if (ver < 0) {  // default: the 8-coefficient-per-thread kernel (6 CTAs / SM; +3.5% kernel, +3% ops/s, r2r)
     const char* e = std::getenv("CK32_KM");
-    ver = e ? std::atoi(e) : 0;
+    ver = e ? std::atoi(e) : 7;
   }
   const int items = (a.level + a.alpha) * (kR / kRRows) * a.batch;
   if (ver == 5 && a.D <= 3) {
@@ -1403,6 +1622,20 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st) {
   }
   if (ver == 6 && a.D <= 3) {
     launch_km<true, 4, true, true, true>(a, tw2, items, st);
+    return;
+  }
+  if (ver == 7 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread, 6 CTAs / SM
+    static int grid = 0;
+    if (!grid) {
+      cudaFuncSetAttribute(k_row_keymult8<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK8Smem);
+      int dev = 0, sms = 148, per = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<6>, 128, kK8Smem);
+      grid = sms * std::max(1, per);
+    }
+    const int items8 = (a.level + a.alpha) * (kR / kK8Rows) * a.batch;
+    k_row_keymult8<6><<<std::min(grid, items8), 128, kK8Smem, st>>>(a, fwd_full);
     return;
   }
   if (ver == 1)
