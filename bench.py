@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=32, help="ciphertexts per GPU per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=2, help="concurrent sub-batches (CUDA streams) per GPU")
+    ap.add_argument("--split", choices=["batch", "ops"], default="batch",
+                    help="2-stream schedule: 'batch' = each stream runs HMult then HRot on half the batch; 'ops' = "
+                         "one stream runs HMult, the other HRot, each on the whole batch")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=4, help="ciphertexts per H2D/compute/D2H chunk")
     ap.add_argument("--no-cpu", action="store_true")
@@ -325,6 +328,18 @@ def main():
         start = torch.cuda.Event()
         start.record(st)
         done, outs = [], []
+        if args.split == "ops" and S_n == 2:  # HMult on one stream, HRot on the other, whole batch each
+            res = []
+            for k, s_k in enumerate(streams):
+                s_k.wait_event(start)
+                with torch.cuda.stream(s_k):
+                    res.append(ckks.hmult(C, X, Y, relin).data if k == 0 else ckks.hrot(C, X, 1, rot).data)
+                    e = torch.cuda.Event()
+                    e.record(s_k)
+                    done.append(e)
+            for e in done:
+                st.wait_event(e)
+            return [(res[0], res[1])]
         for (lo, hi), s_k in zip(subs, streams):
             s_k.wait_event(start)
             with torch.cuda.stream(s_k):
@@ -389,7 +404,7 @@ def main():
     outs = [(o1.data, o2.data) if hasattr(o1, "data") else (o1, o2) for o1, o2 in outs]
     torch.cuda.synchronize(dev)
     checked, bit_exact = [], True
-    for (lo, hi), (o1, o2) in zip(subs if S_n > 1 else [(0, B)], outs):
+    for (lo, hi), (o1, o2) in zip(subs if (S_n > 1 and args.split == "batch") else [(0, B)], outs):
         for b in sorted({lo, hi - 1}):
             X1 = ckks.Ciphertext(X.data[b:b + 1].contiguous(), s, LEVEL)
             Y1 = ckks.Ciphertext(Y.data[b:b + 1].contiguous(), s, LEVEL)
@@ -607,6 +622,7 @@ def main():
                                    f"at N=2^16, l=24, alpha=8, dnum=3 (configs[1]/[2] of BASELINE.json)",
                        "n": N_RING, "l": L, "alpha": ALPHA, "level": LEVEL, "batch_per_gpu": B,
                        "parallelism": f"dp{world} (independent ciphertexts, no collective)", "streams_per_gpu": S_n,
+                       "stream_split": args.split,
                        "l2": "inputs larger than L2 (2 x B x 12 MiB ciphertext pairs per step); keys stay L2-resident"},
             "hmult_ops_per_s": round(B * args.steps * world / (hm_ms / 1e3), 2),
             "hrot_ops_per_s": round(B * args.steps * world / (hr_ms / 1e3), 2),
