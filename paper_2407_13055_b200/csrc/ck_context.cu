@@ -330,6 +330,8 @@ struct Context {
   bool use_cluster = false;  // CK32_NTT_CLUSTER=1: single-pass 8-CTA cluster/DSMEM NTT (slower today)
   bool use_row_km = true;
   bool use_fused_combine = true;  // CK32_NO_FUSED_COMBINE=1: separate k_combine after the ModDown NTT
+  bool use_hrot_tail = false;     // CK32_FUSED_TAIL=1: HRot tail fused into the ModDown forward row pass (measured
+                                  // neutral: 16.82k vs 16.86k ops/s, profiles/r2/README.md), else k_hrot_tail
   bool use_tc = false;  // CK32_TC=1: tcgen05 split-word BConv (bit-exact; slower than the CUDA-core kernel today)  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
   int bconv_fp64 = 0;   // CK32_BCONV_FP64=1|2|3: exact BConv dot products on the FP64 pipe for all / 1 of 2 / 2 of 3 rows
   bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
@@ -499,6 +501,7 @@ struct Context {
       if (d) cudaFree(d);
     if (d_jidx) cudaFree(d_jidx);
     for (auto& kv : rot_maps) cudaFree(kv.second);
+    for (auto& kv : rot_dest) cudaFree(kv.second);
     if (d_primes) cudaFree(d_primes);
     if (d_fwd) cudaFree(d_fwd);
     if (d_inv) cudaFree(d_inv);
@@ -790,6 +793,29 @@ struct Context {
     return ref;
   }
 
+  // dest[i] of the rotation map (AutomorphismMap::dest, automorphism.cpp:40-46): the inverse of rotation_map
+  std::map<int64_t, uint32_t*> rot_dest;
+  const uint32_t* rotation_dest(int64_t r) {
+    auto it = rot_dest.find(r);
+    if (it != rot_dest.end()) return it->second;
+    const int64_t half = (int64_t)n / 2;
+    int64_t e = (-r) % half;
+    if (e < 0) e += half;
+    uint64_t g = 1;
+    const uint64_t mod = 2ull * n;
+    for (int64_t i = 0; i < e; ++i) g = g * 5 % mod;
+    std::vector<uint32_t> dest(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t bi = bit_reverse(i, logn);
+      const uint32_t phi = (uint32_t)((((2ull * bi + 1) * g) % mod - 1) / 2);
+      dest[i] = bit_reverse(phi, logn);
+    }
+    uint32_t* d = nullptr;
+    CK_CUDA(cudaMalloc(&d, n * sizeof(uint32_t)));
+    CK_CUDA(cudaMemcpy(d, dest.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    rot_dest[r] = d;
+    return d;
+  }
   const uint32_t* rotation_map(int64_t r) {  // AutomorphismMap::rotation (automorphism.cpp:11-69)
     auto it = rot_maps.find(r);
     if (it != rot_maps.end()) return it->second;
@@ -1066,6 +1092,44 @@ struct Context {
     key_mult((int)n, a, st);
     ++launches;
     counters[4] += (uint64_t)B * a.D;
+  }
+
+  // HRot's ModDown (drop_and_divide with the ModDown table, ckks.cpp:611-655)
+  // with the rest of rotate_with (ckks.cpp:875-882) fused into the forward
+  // NTT's row pass: out = phi_r((v - conv) d^-1 + (b, 0)), written straight
+  // into the output ciphertexts.  true when the fused path applies.
+  bool drop_divide_hrot(const SwitchPlan& pl, int B, const uint32_t* v, uint64_t v_bs, uint32_t* ts, uint32_t* o,
+                        const uint32_t* ct, uint64_t ct_bs, int64_t r, uint32_t* out, cudaStream_t st) {
+    if (!(logn == 16 && d_tw2f && use_ntt256 && !use_cluster && ntt_chunk_limbs >= (1 << 30) && use_fused_combine &&
+          use_hrot_tail && !fused()))
+      return false;
+    const uint64_t N = n;
+    const uint64_t ts_bs = (uint64_t)pl.npoly * pl.sc * N, o_bs = (uint64_t)pl.npoly * pl.out_q * N;
+    run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
+    run_bconv(pl.bc, B, ts, ts_bs, o, o_bs, st);
+    {
+      // NTT (8N B per row) + the tail's extra reads: v (4N B per row) and b (4N B per Q row of poly 0)
+      ProfScope ps(this, 10, 8.0 * n * pl.ntt.njobs * B + 4.0 * n * pl.out_q * pl.npoly * B + 4.0 * n * pl.out_q * B,
+                   2, st);
+      NttLaunch a = ntt_args(pl.ntt, false, B, o, o_bs, o, o_bs);
+      CombineArgs cb;
+      cb.v = v;
+      cb.v_bs = v_bs;
+      cb.prow = pl.out_q + pl.sc;
+      cb.out_q = pl.out_q;
+      cb.dinv = pl.consts.at<uint32_t>(0);
+      cb.add = ct;
+      cb.add_bs = ct_bs;
+      cb.dest = rotation_dest(r);
+      cb.out = out;
+      cb.out_bs = ct_bs;
+      ntt256_forward_hrot_tail(a, d_tw2f, cb, st);
+      launches += 2;
+    }
+    counters[3] += (uint64_t)B * pl.npoly * pl.sc;
+    counters[5] += (uint64_t)B * pl.npoly;
+    counters[2] += (uint64_t)B * pl.npoly * pl.out_q;
+    return true;
   }
 
   // drop_and_divide (ckks.cpp:611-655) for B x npoly polynomials v (out_q+sc
@@ -1804,6 +1868,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     c->use_tc = std::getenv("CK32_TC") != nullptr;
     if (const char* f = std::getenv("CK32_BCONV_FP64")) c->bconv_fp64 = std::atoi(f);
     c->use_fused_combine = std::getenv("CK32_NO_FUSED_COMBINE") == nullptr;
+    c->use_hrot_tail = std::getenv("CK32_FUSED_TAIL") != nullptr;
     c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;
     if (n == 65536) {
       // Row-pass twiddles of ntt256.cu, permuted per row in thread-consumption
@@ -1912,8 +1977,8 @@ ck_status ck_profile_read(ck_context* ctx, ck_prof_stat* out, uint32_t max_class
   return guard([&] {
     Context* c = C(ctx);
     static const char* names[] = {"ntt_fwd", "ntt_inv", "bconv", "key_mult", "tensor", "combine", "hrot_tail",
-                                  "conv_mid", "ntt_row+keymult", "ntt_fwd+combine"};
-    const uint32_t ncls = 10;
+                                  "conv_mid", "ntt_row+keymult", "ntt_fwd+combine", "ntt_fwd+rottail"};
+    const uint32_t ncls = 11;
     if (!out || !count) throw InvalidArgument("null argument");
     CK_CUDA(cudaDeviceSynchronize());
     std::vector<ck_prof_stat> st(ncls);
@@ -2530,13 +2595,13 @@ ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_
     const uint64_t ct_bs = 2ull * level * N;
     const uint32_t* a = ct + level * N;
     c->mod_up_key_mult(level, B, a, ct_bs, is, ext, rot_evk, nullptr, 0, v, st);
-    c->drop_divide(pl, B, v, v_w, ts, o, false, st);
-    {
+    if (!c->drop_divide_hrot(pl, B, v, v_w, ts, o, ct, ct_bs, r, out, st)) {
+      c->drop_divide(pl, B, v, v_w, ts, o, false, st);
       Context::ProfScope ps(c, 6, 4.0 * N * level * 7 * B, 1, st);  // v0 v1 o0 o1 b in, 2 out
       hrot_tail((int)N, (int)level, B, v, v_w, rows * N, o, o_w, level * N, ct, ct_bs, pl.consts.at<uint32_t>(0),
                 c->rotation_map(r), out, ct_bs, c->d_primes, st);
+      ++c->launches;
     }
-    ++c->launches;
     c->counters[1] += B;
     check_launch();
   });

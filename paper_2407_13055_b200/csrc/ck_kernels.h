@@ -37,8 +37,19 @@ struct CombineArgs {
   uint64_t v_bs = 0;
   uint32_t prow = 0, out_q = 1;
   const uint32_t* dinv = nullptr;  // [out_q] divisor^-1, Montgomery
+  // HRot tail (ntt256_forward_hrot_tail): + add (the ciphertext's b rows,
+  // [B][out_q][n], batch stride add_bs) on poly 0, results stored at
+  // dest[x] of the rotation into out [B][2][out_q][n] (batch stride out_bs)
+  const uint32_t* add = nullptr;
+  uint64_t add_bs = 0;
+  const uint32_t* dest = nullptr;
+  uint32_t* out = nullptr;
+  uint64_t out_bs = 0;
 };
 bool ntt256_forward_combine(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, cudaStream_t st);
+// forward NTT of the ModDown conversion with the whole HRot tail fused into
+// the row pass: combine, + b, automorphism (scattered stores within 32-blocks)
+bool ntt256_forward_hrot_tail(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, cudaStream_t st);
 // single-pass cluster/DSMEM variant (ntt_cluster.cu)
 bool ntt_cluster_available();
 void ntt_cluster_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st);

@@ -535,12 +535,17 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
     uint32_t* orow = dst + b * dst_bs + (size_t)J.dst_off * kN + (size_t)r * kR;
     uint32_t v[16];
     uint4 vvr[COMB == 2 ? 4 : 1];
-    if (COMB == 3 && lane < 16) {  // L2 prefetch of the warp's 2 v rows (16 lines of 128 B)
+    if (COMB >= 3 && lane < 16) {  // L2 prefetch of the warp's 2 v rows (16 lines of 128 B)
       const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
-      const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN +
-                           (size_t)(tile * kRRows + 2 * warp) * kR + lane * 32;
+      const size_t lofs = (size_t)(tile * kRRows + 2 * warp) * kR + lane * 32;
+      const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + lofs;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(vr));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + kR));
+      if (COMB == 4 && pi == 0) {  // HRot tail: the b rows too
+        const uint32_t* br = cb.add + b * cb.add_bs + (size_t)i * kN + lofs;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(br));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(br + kR));
+      }
     }
     if (COMB == 2) {  // J.dst_off = p * out_q + i; v row p * prow + i
       const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
@@ -586,7 +591,50 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
           else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
         }
       }
-      if (COMB) {  // J.dst_off = p * out_q + i; v row p * prow + i; prime i
+      if (COMB == 4) {
+        // HRot tail (ckks.cpp:875-882) fused: c_p = (v_p - NTT) d^-1 (+ b for
+        // p = 0) at position x = 256 r + 16 tau + m, stored at dest(x) of the
+        // rotation: the automorphism maps every aligned 32-block to one
+        // aligned 32-block (acceptance criterion 6), so the two threads of a
+        // block fill one 128 B line with their scattered stores
+        const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
+        const size_t xo = (size_t)r * kR + 16 * tau;
+        const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + xo;
+        const uint32_t* br = cb.add + b * cb.add_bs + (size_t)i * kN + xo;
+        uint32_t* orow_t = cb.out + b * cb.out_bs + ((size_t)pi * cb.out_q + i) * kN;
+        const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv_neg;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const uint4 vv = *reinterpret_cast<const uint4*>(vr + 4 * m);
+          const uint4 ds = __ldg(reinterpret_cast<const uint4*>(cb.dest + xo + 4 * m));
+          uint32_t o0 = sub_if(mont_mul(vv.x - canon8(v[4 * m], q, q2, q4) + q, di, q, qinv), q);
+          uint32_t o1 = sub_if(mont_mul(vv.y - canon8(v[4 * m + 1], q, q2, q4) + q, di, q, qinv), q);
+          uint32_t o2 = sub_if(mont_mul(vv.z - canon8(v[4 * m + 2], q, q2, q4) + q, di, q, qinv), q);
+          uint32_t o3 = sub_if(mont_mul(vv.w - canon8(v[4 * m + 3], q, q2, q4) + q, di, q, qinv), q);
+          if (pi == 0) {
+            const uint4 bb = *reinterpret_cast<const uint4*>(br + 4 * m);
+            o0 = sub_if(o0 + bb.x, q);
+            o1 = sub_if(o1 + bb.y, q);
+            o2 = sub_if(o2 + bb.z, q);
+            o3 = sub_if(o3 + bb.w, q);
+          }
+          // stage at (block, dest & 31) in this row's (now free) line buffer
+          const int x = 16 * tau + 4 * m, blk = x & ~31;
+          line[blk + (ds.x & 31)] = o0;
+          line[blk + (ds.y & 31)] = o1;
+          line[blk + (ds.z & 31)] = o2;
+          line[blk + (ds.w & 31)] = o3;
+        }
+        __syncwarp();
+        {  // whole 32-word destination blocks: lanes 2k, 2k+1 write block k's two halves
+          const int blk = (tau >> 1) * 32, half = (tau & 1) * 16;
+          const uint32_t dbase = __ldg(cb.dest + (size_t)r * kR + blk) & ~31u;
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            stg4(orow_t + dbase + half + 4 * m, *reinterpret_cast<const uint4*>(line + blk + half + 4 * m));
+        }
+        __syncwarp();  // the line buffer is refilled by the prefetch of item k + 2
+      } else if (COMB) {  // J.dst_off = p * out_q + i; v row p * prow + i; prime i
         const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
         const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + (size_t)r * kR + 16 * tau;
         const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv_neg;
@@ -1943,6 +1991,14 @@ static void launch_row_comb(const NttLaunch& a, const uint2* tw2, const CombineA
   }
   k_row<false, COMB><<<min(grid, items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs, a.batch,
                                                                a.njobs, a.primes, tw2, cb);
+}
+
+bool ntt256_forward_hrot_tail(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, cudaStream_t st) {
+  init_grids();
+  const int row_items = a.njobs * (kR / kRRows) * a.batch;
+  launch_col<false>(a, a.src, a.src_bs, st);
+  launch_row_comb<4>(a, tw2, cb, row_items, st);
+  return true;
 }
 
 bool ntt256_forward_combine(const NttLaunch& a, const uint2* tw2, const CombineArgs& cb, cudaStream_t st) {
