@@ -742,3 +742,25 @@ def test_wire_readers_reject_like_the_reference(d):
         ckks.deserialize_poly(C, bytes(big))
     with pytest.raises(ValueError):
         ckks.deserialize_evk(C, (d / "ct_u.bin").read_bytes())
+
+
+@pytest.mark.parametrize("level,r", [(24, 1), (17, -3), (8, 1 << 14), (3, 5)])
+def test_fused_hrot_tail_matches_oracle(monkeypatch, level, r):
+    """The opt-in HRot path with combine + b + automorphism fused into the
+    ModDown forward row pass (CK32_FUSED_TAIL=1, shared-memory-staged
+    32-block stores) equals the oracle, batched (B = 2)."""
+    monkeypatch.setenv("CK32_FUSED_TAIL", "1")
+    n, l, a, db, B = 1 << 16, 24, 8, 55, 2
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db))
+    O = _oracle(n, l, a, db)
+    xs, want = [], []
+    evk = O.synthetic(level, 499 + level)[4]  # one key for the batch
+    for b in range(B):
+        xb, xa = O.synthetic(level, 500 + 7 * b + level)[:2]
+        xs.append(np.stack([xb, xa]))
+        ob, oa = O.hrot(level, xb, xa, r, evk)
+        want.append(np.stack([canon(O, ob, level), canon(O, oa, level)]))
+    K = ckks.EvaluationKey(dev(evk), ckks.ROTATION, r)
+    got = host(ckks.hrot(C, ckks.Ciphertext(dev(np.stack(xs)), Fraction(1 << db), level), r, K).data)
+    np.testing.assert_array_equal(got, np.stack(want))
+    C.close()
