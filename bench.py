@@ -28,6 +28,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# enough hardware work queues that concurrently spinning peer-exchange waits of
+# virtual limb shards (one stream each) never queue behind each other
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 N_RING, L, ALPHA, DB, LEVEL = 1 << 16, 24, 8, 55, 24
 METRIC = "HMult+relin & HRot ops/s at N=2^16 (l=24, alpha=8, dnum=3)"
@@ -701,7 +704,8 @@ def limb_measure(args, world, rank, local, graph=True):
         else:
             exch = TorchExchange() if world > 1 else LocalExchange()
     lays = [s.layout for s in shards]
-    ev = LimbShardedEvaluator(shards, exch)
+    # virtual shards run side by side on their own streams, as they would on separate GPUs
+    ev = LimbShardedEvaluator(shards, exch, concurrent=bool(args.virtual_shards and world == 1))
     xs = [lay.split_ct(x, LEVEL) for lay in lays]
     ys = [lay.split_ct(y, LEVEL) for lay in lays]
     rk = [lay.split_key(relin) for lay in lays]

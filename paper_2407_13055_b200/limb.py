@@ -314,11 +314,46 @@ class LimbShardedEvaluator:
     are ``[2][lq][n]`` (see :meth:`ShardLayout.split_ct`), shard-local keys
     ``[D][2][owned Q + owned P][n]`` (:meth:`ShardLayout.split_key`)."""
 
-    def __init__(self, backends: Sequence, exchange, lazy_rescale: bool = False):
+    def __init__(self, backends: Sequence, exchange, lazy_rescale: bool = False, concurrent: bool = False):
+        """``concurrent`` (peer exchange, several shards in this process --
+        virtual shards on one GPU): every shard issues its phases on its own
+        CUDA stream, so the shards run side by side as they do on separate
+        GPUs; the only cross-shard ordering is the exchange's device flags."""
         self.backends = list(backends)
         self.x = exchange
         self.peer = bool(getattr(exchange, "peer", False))
         self.lazy_rescale = lazy_rescale
+        self.streams = None
+        if concurrent and self.peer and len(self.backends) > 1:
+            dev = self.backends[0].ctx.device
+            self.streams = [torch.cuda.Stream(dev) for _ in self.backends]
+
+    def _fork(self):
+        if self.streams:
+            cur = torch.cuda.current_stream(self.backends[0].ctx.device)
+            for s in self.streams:
+                s.wait_stream(cur)
+
+    def _join(self, outs):
+        if self.streams:
+            cur = torch.cuda.current_stream(self.backends[0].ctx.device)
+            for s in self.streams:
+                cur.wait_stream(s)
+            for o in outs:  # allocated on a shard stream, consumed on the caller's
+                if isinstance(o, torch.Tensor):
+                    o.record_stream(cur)
+        return outs
+
+    def _each(self, fn, *lists):
+        """[fn(backend, *args) for every shard], each on its own stream when concurrent."""
+        out = []
+        for k, args in enumerate(zip(self.backends, *lists)):
+            if self.streams:
+                with torch.cuda.stream(self.streams[k]):
+                    out.append(fn(*args))
+            else:
+                out.append(fn(*args))
+        return out
 
     def synchronize(self) -> None:
         """Sync point: wait for the device, then raise if a peer exchange
@@ -338,48 +373,52 @@ class LimbShardedEvaluator:
     def key_switch_v(self, level: int, ds, evks, folds=None):
         """ModUp + KeyMult (+ fold): v = [2][lq + lp] per shard (ckks.cpp:680-770)."""
         kw = {"peer": True} if self.peer else {}
-        sends = [be.modup_begin(level, d, **kw) for be, d in zip(self.backends, ds)]
+        sends = self._each(lambda be, d: be.modup_begin(level, d, **kw), ds)
         recvs = self._gather(sends)
         folds = folds or [None] * len(self.backends)
-        return [be.modup_keymult(level, r, d, e, f) for be, r, d, e, f in zip(self.backends, recvs, ds, evks, folds)]
+        return self._each(lambda be, r, d, e, f: be.modup_keymult(level, r, d, e, f), recvs, ds, evks, folds)
 
     def _switch(self, kind, level, vs, addends=None, add_mask=0, rot=None):
         kw = {"peer": True} if self.peer else {}
-        sends = [be.switch_begin(kind, level, v, **kw) for be, v in zip(self.backends, vs)]
+        sends = self._each(lambda be, v: be.switch_begin(kind, level, v, **kw), vs)
         recvs = self._gather(sends)
         addends = addends or [None] * len(self.backends)
-        return [be.switch_end(kind, level, r, v, a, add_mask, rot)
-                for be, r, v, a in zip(self.backends, recvs, vs, addends)]
+        return self._each(lambda be, r, v, a: be.switch_end(kind, level, r, v, a, add_mask, rot), recvs, vs, addends)
 
     def key_switch(self, level: int, ds, evks):
         """key_switch (ckks.cpp:778-787): [2][lq] per shard (c0, c1)."""
-        return self._switch(MOD_DOWN, level, self.key_switch_v(level, ds, evks))
+        self._fork()
+        return self._join(self._switch(MOD_DOWN, level, self.key_switch_v(level, ds, evks)))
 
     def rescale(self, level: int, cts):
         """rescale (ckks.cpp:789-802): [2][lq(level-2)] per shard."""
         if level < 4:
             raise ValueError("level exhausted")
-        return self._switch(RESCALE, level, cts)
+        self._fork()
+        return self._join(self._switch(RESCALE, level, cts))
 
     def hmult(self, level: int, xs, ys, relins):
         """hmult (ckks.cpp:804-865): merged ModDown + rescale (level - 2), or
         lazy (ModDown, then + (d0, d1), level kept) when ``lazy_rescale``."""
         if level < 4:
             raise ValueError("level exhausted")
-        t = [be.tensor(level, x, y) for be, x, y in zip(self.backends, xs, ys)]
+        self._fork()
+        t = self._each(lambda be, x, y: be.tensor(level, x, y), xs, ys)
         d01 = [a for a, _ in t]
         d2 = [b for _, b in t]
         if not self.lazy_rescale:
             vs = self.key_switch_v(level, d2, relins, folds=d01)
-            return self._switch(MERGED, level, vs)
+            return self._join(self._switch(MERGED, level, vs))
         vs = self.key_switch_v(level, d2, relins)
-        return self._switch(MOD_DOWN, level, vs, addends=d01, add_mask=3)
+        return self._join(self._switch(MOD_DOWN, level, vs, addends=d01, add_mask=3))
 
     def hrot(self, level: int, cts, r: int, evks):
         """hrot (ckks.cpp:869-897): key-switch a, c0 += b, automorphism on both."""
-        a = [ct[1].contiguous() for ct in cts]
+        self._fork()
+        a = self._each(lambda be, ct: ct[1].contiguous(), cts)
         vs = self.key_switch_v(level, a, evks)
-        return self._switch(MOD_DOWN, level, vs, addends=[ct.contiguous() for ct in cts], add_mask=1, rot=r)
+        full = self._each(lambda be, ct: ct.contiguous(), cts)
+        return self._join(self._switch(MOD_DOWN, level, vs, addends=full, add_mask=1, rot=r))
 
 
 def exchange_bytes(layout: ShardLayout, n: int, level: int, kind: int) -> int:

@@ -1,5 +1,10 @@
+import os
 import sys
 from pathlib import Path
+
+# concurrent virtual limb shards (one stream each, spin-waiting peer exchange)
+# need their streams on distinct hardware queues; set before CUDA starts
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import pytest
 

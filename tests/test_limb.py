@@ -305,7 +305,8 @@ def test_gpu_config4_n131072_matches_reference_hash(world, peer):
     shards = [ShardBackend(C, world, r) for r in range(world)]
     if peer:
         from paper_2407_13055_b200.limb import LocalPeerExchange
-        ev = LimbShardedEvaluator(shards, LocalPeerExchange(shards))
+        # the virtual shards run concurrently, one stream each (as on separate GPUs)
+        ev = LimbShardedEvaluator(shards, LocalPeerExchange(shards), concurrent=True)
     else:
         ev = LimbShardedEvaluator(shards, LocalExchange())
     lays = [s.layout for s in shards]
