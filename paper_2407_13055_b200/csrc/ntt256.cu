@@ -1415,7 +1415,9 @@ constexpr int kK8Stride = 288;                   // 256 + 32 padding words
 __device__ __forceinline__ int pad8(int c) { return c + 4 * (c >> 5); }
 constexpr int kK8Smem = (3 * kK8Rows * kK8Stride) * 4 + kK8Rows * 256 * 8;  // 3 digit tiles + twiddles
 
-template <int MINB>
+// EARLY: the key halves of digit k are loaded before its row pass (16
+// registers live across it); without, they are loaded after it (more CTAs).
+template <int MINB, bool EARLY = true>
 __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, const uint2* __restrict__ fwd) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1478,10 +1480,10 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
     for (int j = 0; j < 8; ++j) s0[j] = s1[j] = 0;
     for (int k = 0; k < a.D; ++k) {
       const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
-      uint4 kb[2], ka[2];  // key halves first: their L2 latency hides behind the butterflies
-      {
-        const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
-        const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
+      uint4 kb[2], ka[2];  // key halves (EARLY: first, their L2 latency hides behind the butterflies)
+      const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
+      const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
+      if (EARLY) {
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           kb[m] = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
@@ -1555,6 +1557,13 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = canon8(v[j], q, q2, q4);
+      }
+      if (!EARLY) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          kb[m] = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
+          ka[m] = __ldg(reinterpret_cast<const uint4*>(ea + 4 * m));
+        }
       }
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
@@ -1642,6 +1651,20 @@ static void launch_km(const KeyMultLaunch& a, const uint2* tw2, int items, cudaS
   k_row_keymult<EARLY, MINB, ALLD, WL, L2PF><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
 }
 
+template <int MINB, bool EARLY>
+static void launch_km8(const KeyMultLaunch& a, const uint2* fwd, int items, cudaStream_t st) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_row_keymult8<MINB, EARLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK8Smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<MINB, EARLY>, 128, kK8Smem);
+    grid = sms * std::max(1, per);
+  }
+  k_row_keymult8<MINB, EARLY><<<std::min(grid, items), 128, kK8Smem, st>>>(a, fwd);
+}
+
 template <int MINB>
 static void launch_km_pf(const KeyMultLaunch& a, const uint2* tw2, int items, cudaStream_t st) {
   static int grid = 0;
@@ -1672,18 +1695,12 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, cons
     launch_km<true, 4, true, true, true>(a, tw2, items, st);
     return;
   }
-  if (ver == 7 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread, 6 CTAs / SM
-    static int grid = 0;
-    if (!grid) {
-      cudaFuncSetAttribute(k_row_keymult8<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK8Smem);
-      int dev = 0, sms = 148, per = 1;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<6>, 128, kK8Smem);
-      grid = sms * std::max(1, per);
-    }
+  if ((ver == 7 || ver == 8) && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
     const int items8 = (a.level + a.alpha) * (kR / kK8Rows) * a.batch;
-    k_row_keymult8<6><<<std::min(grid, items8), 128, kK8Smem, st>>>(a, fwd_full);
+    if (ver == 7)
+      launch_km8<6, true>(a, fwd_full, items8, st);  // keys ahead of the row pass, 6 CTAs / SM
+    else
+      launch_km8<8, false>(a, fwd_full, items8, st);  // keys after it, 64 registers, 8 CTAs / SM
     return;
   }
   if (ver == 1)
