@@ -1005,12 +1005,17 @@ struct Context {
   // ModUp + KeyMult (+ fold) into v [B][2][level+alpha]. For N = 2^16 the
   // extension's forward row pass is fused into KeyMult (k_row_keymult): ext
   // only ever holds column-pass output.
-  void mod_up_key_mult(uint32_t level, int B, const uint32_t* d, uint64_t d_bs, uint32_t* is, uint32_t* ext,
-                       const uint32_t* evk, const uint32_t* fold, uint64_t fold_bs, uint32_t* v, cudaStream_t st) {
+  // pre (optional): the drop-and-divide that consumes v next; when the fused
+  // row pass + KeyMult kernel supports it, that switch's INTT pass A is done
+  // in the KeyMult epilogue (its source rows go to ts, row-transformed) and
+  // the return value is true -- the caller then runs only pass B.
+  bool mod_up_key_mult(uint32_t level, int B, const uint32_t* d, uint64_t d_bs, uint32_t* is, uint32_t* ext,
+                       const uint32_t* evk, const uint32_t* fold, uint64_t fold_bs, uint32_t* v, cudaStream_t st,
+                       const SwitchPlan* pre = nullptr, uint32_t* ts = nullptr, uint64_t ts_bs = 0) {
     if (!(logn == 16 && d_tw2f && use_ntt256 && use_row_km)) {
       mod_up(level, B, d, d_bs, is, ext, st);
       key_mult_v(level, B, ext, d, d_bs, evk, fold, fold_bs, v, st);
-      return;
+      return false;
     }
     const ModUpPlan& pl = modup_plan(level);
     const uint64_t N = n;
@@ -1040,6 +1045,20 @@ struct Context {
     a.v = v;
     a.v_bs = 2ull * (level + alpha) * n;
     a.primes = d_primes;
+    bool fused_intt = false;
+    if (pre && ts && !fused() && pre->out_q + pre->sc == level + alpha && pre->npoly == 2) {
+      KeyMultLaunch t = a;
+      t.ts = ts;
+      t.ts_bs = ts_bs;
+      t.ts_sc = (int)pre->sc;
+      t.ts_q = (int)(pre->sc - alpha);  // tail Q rows among the sources (2 merged, 0 ModDown)
+      t.src_lo = (int)(level - t.ts_q);
+      t.inv_full = d_inv;
+      if (t.ts_q >= 0 && row_keymult_fuses_intt(t)) {
+        a = t;
+        fused_intt = true;
+      }
+    }
     {
       // Per ciphertext: the row pass reads the extension rows' column-pass
       // output (4N B per row; its result never leaves the SM), KeyMult reads
@@ -1059,6 +1078,7 @@ struct Context {
     counters[5] += (uint64_t)B * pl.D;
     counters[2] += (uint64_t)B * pl.ntt_rows;
     counters[4] += (uint64_t)B * pl.D;
+    return fused_intt;
   }
 
   // key_mult (+ optional fold) into v [B][2][level+alpha]
@@ -1099,13 +1119,14 @@ struct Context {
   // NTT's row pass: out = phi_r((v - conv) d^-1 + (b, 0)), written straight
   // into the output ciphertexts.  true when the fused path applies.
   bool drop_divide_hrot(const SwitchPlan& pl, int B, const uint32_t* v, uint64_t v_bs, uint32_t* ts, uint32_t* o,
-                        const uint32_t* ct, uint64_t ct_bs, int64_t r, uint32_t* out, cudaStream_t st) {
+                        const uint32_t* ct, uint64_t ct_bs, int64_t r, uint32_t* out, cudaStream_t st,
+                        bool pre_intt = false) {
     if (!(logn == 16 && d_tw2f && use_ntt256 && !use_cluster && ntt_chunk_limbs >= (1 << 30) && use_fused_combine &&
           use_hrot_tail && !fused()))
       return false;
     const uint64_t N = n;
     const uint64_t ts_bs = (uint64_t)pl.npoly * pl.sc * N, o_bs = (uint64_t)pl.npoly * pl.out_q * N;
-    run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
+    switch_intt(pl, B, v, v_bs, ts, ts_bs, pre_intt, st);
     run_bconv(pl.bc, B, ts, ts_bs, o, o_bs, st);
     {
       // NTT (8N B per row) + the tail's extra reads: v (4N B per row) and b (4N B per Q row of poly 0)
@@ -1135,17 +1156,31 @@ struct Context {
   // drop_and_divide (ckks.cpp:611-655) for B x npoly polynomials v (out_q+sc
   // rows each, poly stride, batch stride) into o [B][npoly][out_q]; ts scratch
   // [B][npoly][sc]. If `combine_now` is false the caller fuses the combine.
+  // inverse NTT of a switch's source rows v -> ts, or, when the fused KeyMult
+  // already ran pass A into ts (pre_intt), only pass B in place on ts
+  void switch_intt(const SwitchPlan& pl, int B, const uint32_t* v, uint64_t v_bs, uint32_t* ts, uint64_t ts_bs,
+                   bool pre_intt, cudaStream_t st) {
+    if (!pre_intt) {
+      run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
+      return;
+    }
+    ProfScope ps(this, 1, 8.0 * n * pl.intt.njobs * B, 1, st);
+    ntt256_pass(3, ntt_args(pl.intt, true, B, ts, ts_bs, ts, ts_bs), d_tw2i, st);
+    launches += 1;
+  }
+
   void drop_divide(const SwitchPlan& pl, int B, const uint32_t* v, uint64_t v_bs, uint32_t* ts, uint32_t* o,
-                   bool combine_now, cudaStream_t st) {
+                   bool combine_now, cudaStream_t st, bool pre_intt = false) {
     const uint64_t N = n;
     const uint64_t prow = pl.out_q + pl.sc;
     const uint64_t ts_bs = (uint64_t)pl.npoly * pl.sc * N, o_bs = (uint64_t)pl.npoly * pl.out_q * N;
     if (fused()) {
+      if (pre_intt) throw std::logic_error("fused INTT pass A with the k_conv_mid path");
       run_convert(pl.intt, pl.cm, pl.ntt, B, v, v_bs, ts, ts_bs, o, o_bs, 4.0 * N * pl.npoly * pl.sc * B,
                   4.0 * N * pl.npoly * pl.out_q * B, st);
     } else if (combine_now && logn == 16 && d_tw2f && use_ntt256 && !use_cluster && ntt_chunk_limbs >= (1 << 30) &&
                use_fused_combine) {
-      run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
+      switch_intt(pl, B, v, v_bs, ts, ts_bs, pre_intt, st);
       run_bconv(pl.bc, B, ts, ts_bs, o, o_bs, st);
       {  // forward NTT with the combine fused into its row pass
         // NTT (8N B per row) + the combine's extra read of v (4N B per row)
@@ -1162,7 +1197,7 @@ struct Context {
       }
       combine_now = false;
     } else {
-      run_ntt(pl.intt, true, B, v, v_bs, ts, ts_bs, 0, st);
+      switch_intt(pl, B, v, v_bs, ts, ts_bs, pre_intt, st);
       run_bconv(pl.bc, B, ts, ts_bs, o, o_bs, st);
       run_ntt(pl.ntt, false, B, o, o_bs, o, o_bs, 0, st);  // BConv output already carries R
     }
@@ -2551,12 +2586,12 @@ ck_status ck_hmult(ck_context* ctx, uint32_t level, uint32_t batch, const uint32
       tensor((int)N, (int)level, B, x, y, 2ull * level * N, t01, t01_w, d2, d2_w, c->d_primes, st);
     }
     ++c->launches;
-    if (!lazy) {
-      c->mod_up_key_mult(level, B, d2, d2_w, is, ext, relin_evk, t01, t01_w, v, st);  // fold P*d0/1 fused
-      c->drop_divide(pl, B, v, v_w, ts, out, true, st);
+    if (!lazy) {  // fold P*d0/1 fused; the merged switch's INTT pass A fused into the KeyMult epilogue
+      const bool pre = c->mod_up_key_mult(level, B, d2, d2_w, is, ext, relin_evk, t01, t01_w, v, st, &pl, ts, ts_w);
+      c->drop_divide(pl, B, v, v_w, ts, out, true, st, pre);
     } else {
-      c->mod_up_key_mult(level, B, d2, d2_w, is, ext, relin_evk, nullptr, 0, v, st);
-      c->drop_divide(pl, B, v, v_w, ts, cc, true, st);
+      const bool pre = c->mod_up_key_mult(level, B, d2, d2_w, is, ext, relin_evk, nullptr, 0, v, st, &pl, ts, ts_w);
+      c->drop_divide(pl, B, v, v_w, ts, cc, true, st, pre);
       // out.b = d0 + c0, out.a = d1 + c1 (ckks.cpp:857-858)
       elementwise((int)N, (int)(2 * level), B, 0, t01, t01_w, cc, c_w, out, 2ull * level * N, nullptr,
                   c->d_primes, st, (int)level);
@@ -2594,9 +2629,9 @@ ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_
     cudaStream_t st = S(stream);
     const uint64_t ct_bs = 2ull * level * N;
     const uint32_t* a = ct + level * N;
-    c->mod_up_key_mult(level, B, a, ct_bs, is, ext, rot_evk, nullptr, 0, v, st);
-    if (!c->drop_divide_hrot(pl, B, v, v_w, ts, o, ct, ct_bs, r, out, st)) {
-      c->drop_divide(pl, B, v, v_w, ts, o, false, st);
+    const bool pre = c->mod_up_key_mult(level, B, a, ct_bs, is, ext, rot_evk, nullptr, 0, v, st, &pl, ts, ts_w);
+    if (!c->drop_divide_hrot(pl, B, v, v_w, ts, o, ct, ct_bs, r, out, st, pre)) {
+      c->drop_divide(pl, B, v, v_w, ts, o, false, st, pre);
       Context::ProfScope ps(c, 6, 4.0 * N * level * 7 * B, 1, st);  // v0 v1 o0 o1 b in, 2 out
       hrot_tail((int)N, (int)level, B, v, v_w, rows * N, o, o_w, level * N, ct, ct_bs, pl.consts.at<uint32_t>(0),
                 c->rotation_map(r), out, ct_bs, c->d_primes, st);

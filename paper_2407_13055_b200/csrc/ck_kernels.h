@@ -160,6 +160,15 @@ struct KeyMultLaunch {
   uint32_t* v = nullptr;          // [B][2][level+alpha][n]
   uint64_t v_bs = 0;
   const PrimeDev* primes = nullptr;
+  // Optional (k_row_keymult8): the following drop-and-divide's INTT pass A
+  // done in the epilogue.  Rows i >= src_lo are that switch's sources: they
+  // are written row-transformed (inverse row pass, [0, 2q)) into ts
+  // [B][2][ts_sc][n] (row ts_q + (i - level) for P rows, i - src_lo for the
+  // ts_q tail Q rows) instead of into v.  inv_full: [prime][N] inverse tables.
+  uint32_t* ts = nullptr;
+  uint64_t ts_bs = 0;
+  int src_lo = 1 << 30, ts_q = 0, ts_sc = 0;
+  const uint2* inv_full = nullptr;
 };
 void key_mult(int n, const KeyMultLaunch& a, cudaStream_t st);
 // N = 2^16: forward NTT row pass of every digit's extension row fused with
@@ -167,6 +176,8 @@ void key_mult(int n, const KeyMultLaunch& a, cudaStream_t st);
 // fwd_full: the per-prime forward tables [prime][N] {w, w'} (the
 // 8-coefficient-per-thread variant reads its row twiddles from them)
 void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, const uint2* fwd_full = nullptr);
+// whether row_keymult runs a kernel that honours KeyMultLaunch::ts (the fused INTT pass A)
+bool row_keymult_fuses_intt(const KeyMultLaunch& a);
 
 // drop-and-divide combine (ckks.cpp:643-651): o = (v - o) * div_inv (Montgomery)
 void combine(int n, int rows, int npoly, int batch, const uint32_t* v, uint64_t v_ps, uint64_t v_bs, uint32_t* o,

@@ -1413,7 +1413,7 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult_pf(KeyMultLaunch a, c
 constexpr int kK8Rows = 4;                       // rows per CTA (one per warp)
 constexpr int kK8Stride = 288;                   // 256 + 32 padding words
 __device__ __forceinline__ int pad8(int c) { return c + 4 * (c >> 5); }
-constexpr int kK8Smem = (3 * kK8Rows * kK8Stride) * 4 + kK8Rows * 256 * 8;  // 3 digit tiles + twiddles
+constexpr int kK8Smem = (3 * kK8Rows * kK8Stride) * 4 + 2 * kK8Rows * 256 * 8;  // 3 digit tiles + fwd / inv twiddles
 
 // EARLY: the key halves of digit k are loaded before its row pass (16
 // registers live across it); without, they are loaded after it (more CTAs).
@@ -1422,8 +1422,9 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
   extern __shared__ __align__(16) unsigned char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);                          // [3][4][288]
-  uint2* tws = reinterpret_cast<uint2*>(smraw + 3 * kK8Rows * kK8Stride * 4);   // [4][256]
+  uint2* tws = reinterpret_cast<uint2*>(smraw + 3 * kK8Rows * kK8Stride * 4);   // [4][256] forward, [4][256] inverse
   uint2* T = tws + warp * 256;
+  uint2* Ti = tws + (kK8Rows + warp) * 256;  // inverse row twiddles (fused INTT pass A), natural order per stage
   constexpr int kTiles = kR / kK8Rows;
   const int rows = a.level + a.alpha, B = a.batch;
   const uint32_t LA = (uint32_t)(a.L + a.alpha);
@@ -1451,6 +1452,13 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       for (int e = lane; e < 255; e += 32) {
         const int s = 31 - __clz(e + 1), blk = e + 1 - (1 << s);
         T[e] = __ldg(&F[(256 << s) + (r << s) + blk]);
+      }
+      if (a.ts && i >= a.src_lo) {  // inverse stage v of row r: I[(N >> (v+1)) + (r << (7-v)) + blk] at 256 - (256 >> v) + blk
+        const uint2* I = a.inv_full + (size_t)g * kN;
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          for (int blk = lane; blk < (128 >> v); blk += 32)
+            Ti[256 - (256 >> v) + blk] = __ldg(&I[(kN >> (v + 1)) + (r << (7 - v)) + blk]);
       }
     }
     // all digits' extension rows at once (one cp.async group per digit)
@@ -1602,18 +1610,78 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         s1[4 * m + 3] = mac_wide(s1[4 * m + 3], x1.w, pm);
       }
     }
-    uint32_t* o0 = a.v + b * a.v_bs + (size_t)i * kN + rofs;
-    uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
+    if (a.ts && i >= a.src_lo) {
+      // this row is a source of the following drop-and-divide: run its INTT
+      // pass A (the inverse row pass, GS stages v = 0..7) here and write the
+      // result where that INTT's pass B reads it (ts), not into v
+      const int tsrow = i < a.level ? i - a.src_lo : a.ts_q + (i - a.level);
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv_neg), q)));
-      stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv_neg), q)));
+      for (int pp = 0; pp < 2; ++pp) {
+        uint32_t u[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = sub_if(mont_reduce64(pp ? s1[j] : s0[j], q, P.qinv_neg), q);
+        uint32_t* line = sbuf + (pp * kK8Rows + warp) * kK8Stride;  // digit buffers 0 / 1 are free now
+        // stages v = 0, 1 on c = 8 lane + k
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int d = 1 << v;
+#pragma unroll
+          for (int p4 = 0; p4 < 4; ++p4) {
+            const int blk = p4 / d, k = blk * 2 * d + p4 % d;
+            const uint2 w = Ti[256 - (256 >> v) + (lane << (2 - v)) + blk];
+            gs(u[k], u[k + d], w.x, w.y, q, q2);
+          }
+        }
+        *reinterpret_cast<uint4*>(line + pad8(8 * lane)) = make_uint4(u[0], u[1], u[2], u[3]);
+        *reinterpret_cast<uint4*>(line + pad8(8 * lane + 4)) = make_uint4(u[4], u[5], u[6], u[7]);
+        __syncwarp();
+        // stages v = 2, 3, 4 on c = 32 lhi + 4 j + llo
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = line[pad8(32 * lhi + 4 * j + llo)];
+#pragma unroll
+        for (int v = 2; v < 5; ++v) {
+          const int d = 1 << (v - 2);
+#pragma unroll
+          for (int p4 = 0; p4 < 4; ++p4) {
+            const int blk = p4 / d, j = blk * 2 * d + p4 % d;
+            const uint2 w = Ti[256 - (256 >> v) + (lhi << (4 - v)) + blk];
+            gs(u[j], u[j + d], w.x, w.y, q, q2);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) line[pad8(32 * lhi + 4 * j + llo)] = u[j];
+        __syncwarp();
+        // stages v = 5, 6, 7 on c = lane + 32 j (row-uniform twiddles)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = line[pad8(lane + 32 * j)];
+#pragma unroll
+        for (int v = 5; v < 8; ++v) {
+          const int d = 1 << (v - 5);
+#pragma unroll
+          for (int p4 = 0; p4 < 4; ++p4) {
+            const int blk = p4 / d, j = blk * 2 * d + p4 % d;
+            const uint2 w = Ti[256 - (256 >> v) + blk];
+            gs(u[j], u[j + d], w.x, w.y, q, q2);
+          }
+        }
+        uint32_t* trow = a.ts + b * a.ts_bs + ((size_t)pp * a.ts_sc + tsrow) * kN + (size_t)r * kR;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) trow[lane + 32 * j] = u[j];
+      }
+    } else {
+      uint32_t* o0 = a.v + b * a.v_bs + (size_t)i * kN + rofs;
+      uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv_neg), q),
+                                    sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv_neg), q),
+                                    sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv_neg), q),
+                                    sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv_neg), q)));
+        stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv_neg), q),
+                                    sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv_neg), q),
+                                    sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv_neg), q),
+                                    sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv_neg), q)));
+      }
     }
     if (++b == B) {
       b = 0;
@@ -1651,6 +1719,23 @@ static void launch_km(const KeyMultLaunch& a, const uint2* tw2, int items, cudaS
   k_row_keymult<EARLY, MINB, ALLD, WL, L2PF><<<std::min(grid, items), kKT, smem, st>>>(a, tw2);
 }
 
+static int km_version() {
+  static int ver = -1;
+  if (ver < 0) {  // default: the 8-coefficient-per-thread kernel, keys after the row pass, 8 CTAs / SM (r2z:
+                  // 268 vs 277 us for KM=7 and 288 us for round 1's kernel; +1.1% / +4% ops/s)
+    const char* e = std::getenv("CK32_KM");
+    ver = e ? std::atoi(e) : 8;
+  }
+  return ver;
+}
+
+bool row_keymult_fuses_intt(const KeyMultLaunch& a) {
+  static int off = -1;
+  if (off < 0) off = std::getenv("CK32_NO_KM_INTT") != nullptr;
+  const int v = km_version();
+  return !off && (v == 7 || v == 8) && a.D <= 3;
+}
+
 template <int MINB, bool EARLY>
 static void launch_km8(const KeyMultLaunch& a, const uint2* fwd, int items, cudaStream_t st) {
   static int grid = 0;
@@ -1681,11 +1766,7 @@ static void launch_km_pf(const KeyMultLaunch& a, const uint2* tw2, int items, cu
 }
 
 void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, const uint2* fwd_full) {
-  static int ver = -1;
-  if (ver < 0) {  // default: the 8-coefficient-per-thread kernel (6 CTAs / SM; +3.5% kernel, +3% ops/s, r2r)
-    const char* e = std::getenv("CK32_KM");
-    ver = e ? std::atoi(e) : 7;
-  }
+  const int ver = km_version();
   const int items = (a.level + a.alpha) * (kR / kRRows) * a.batch;
   if (ver == 5 && a.D <= 3) {
     launch_km_pf<4>(a, tw2, items, st);
