@@ -1413,7 +1413,8 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult_pf(KeyMultLaunch a, c
 constexpr int kK8Rows = 4;                       // rows per CTA (one per warp)
 constexpr int kK8Stride = 288;                   // 256 + 32 padding words
 __device__ __forceinline__ int pad8(int c) { return c + 4 * (c >> 5); }
-constexpr int kK8Smem = (3 * kK8Rows * kK8Stride) * 4 + 2 * kK8Rows * 256 * 8;  // 3 digit tiles + fwd / inv twiddles
+constexpr int kK8SmemBase = (3 * kK8Rows * kK8Stride) * 4 + kK8Rows * 256 * 8;  // 3 digit tiles + fwd twiddles
+constexpr int kK8Smem = kK8SmemBase + kK8Rows * 256 * 8;  // + inverse twiddles (fused INTT pass A)
 
 // EARLY: the key halves of digit k are loaded before its row pass (16
 // registers live across it); without, they are loaded after it (more CTAs).
@@ -1738,16 +1739,18 @@ bool row_keymult_fuses_intt(const KeyMultLaunch& a) {
 
 template <int MINB, bool EARLY>
 static void launch_km8(const KeyMultLaunch& a, const uint2* fwd, int items, cudaStream_t st) {
-  static int grid = 0;
-  if (!grid) {
+  static int grid[2] = {0, 0};
+  const int fi = a.ts ? 1 : 0;  // the inverse twiddle region only when the INTT pass A is fused
+  const int smem = fi ? kK8Smem : kK8SmemBase;
+  if (!grid[fi]) {
     cudaFuncSetAttribute(k_row_keymult8<MINB, EARLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK8Smem);
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<MINB, EARLY>, 128, kK8Smem);
-    grid = sms * std::max(1, per);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<MINB, EARLY>, 128, smem);
+    grid[fi] = sms * std::max(1, per);
   }
-  k_row_keymult8<MINB, EARLY><<<std::min(grid, items), 128, kK8Smem, st>>>(a, fwd);
+  k_row_keymult8<MINB, EARLY><<<std::min(grid[fi], items), 128, smem, st>>>(a, fwd);
 }
 
 template <int MINB>
