@@ -1730,11 +1730,15 @@ static int km_version() {
   return ver;
 }
 
+// The switch's INTT pass A in the KeyMult epilogue (CK32_KM_INTT=1): bit-exact
+// and it removes that pass's HBM round trip, but the extra butterflies land
+// on the latency-bound KeyMult kernel -- measured neutral to slightly slower
+// (r2aa: 16.90k vs 16.96k ops/s), so opt-in.
 bool row_keymult_fuses_intt(const KeyMultLaunch& a) {
-  static int off = -1;
-  if (off < 0) off = std::getenv("CK32_NO_KM_INTT") != nullptr;
+  static int on = -1;
+  if (on < 0) on = std::getenv("CK32_KM_INTT") != nullptr;
   const int v = km_version();
-  return !off && (v == 7 || v == 8) && a.D <= 3;
+  return on && (v == 7 || v == 8) && a.D <= 3;
 }
 
 template <int MINB, bool EARLY>

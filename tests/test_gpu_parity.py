@@ -764,3 +764,42 @@ def test_fused_hrot_tail_matches_oracle(monkeypatch, level, r):
     got = host(ckks.hrot(C, ckks.Ciphertext(dev(np.stack(xs)), Fraction(1 << db), level), r, K).data)
     np.testing.assert_array_equal(got, np.stack(want))
     C.close()
+
+
+@pytest.mark.parametrize("level", [24, 13, 4])
+def test_keymult_fused_intt_pass_a_matches_oracle(monkeypatch, level):
+    """The opt-in path with the following switch's INTT pass A run in the
+    KeyMult epilogue (CK32_KM_INTT=1, read once per process: run in a fresh
+    subprocess) -- merged and lazy HMult and HRot equal the oracle."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = f'''
+import sys, numpy as np, torch
+sys.path[:0] = {[str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent.parent / "oracle")]!r}
+from fractions import Fraction
+from paper_2407_13055_b200 import ckks
+from pyoracle import Oracle
+n, l, a, db, level = 1 << 16, 24, 8, 55, {level}
+O = Oracle(n, l, a, db)
+xb, xa, yb, ya, evk = O.synthetic(level, 777 + level)
+dev = lambda v: torch.from_numpy(np.ascontiguousarray(v.astype(np.int32))).cuda()
+for lazy in (False, True):
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db, lazy_rescale=lazy))
+    x = ckks.Ciphertext(dev(np.stack([xb, xa])), Fraction(1 << db), level)
+    y = ckks.Ciphertext(dev(np.stack([yb, ya])), Fraction(1 << db), level)
+    got = ckks.hmult(C, x, y, ckks.EvaluationKey(dev(evk))).data.cpu().numpy().astype(np.uint32)
+    ob, oa = O.hmult(level, xb, xa, yb, ya, evk, lazy=lazy)
+    lo = level if lazy else level - 2
+    assert np.array_equal(got, np.stack([O.canonical(ob, O.gidx(lo)), O.canonical(oa, O.gidx(lo))])), lazy
+    if not lazy:
+        got = ckks.hrot(C, x, 3, ckks.EvaluationKey(dev(evk), ckks.ROTATION, 3)).data.cpu().numpy().astype(np.uint32)
+        ob, oa = O.hrot(level, xb, xa, 3, evk)
+        assert np.array_equal(got, np.stack([O.canonical(ob, O.gidx(level)), O.canonical(oa, O.gidx(level))]))
+    C.close()
+print("fused-intt ok")
+'''
+    env = dict(__import__("os").environ, CK32_KM_INTT="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "fused-intt ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
