@@ -1695,6 +1695,219 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
   cp_wait<0>();
 }
 
+// k_row8: the N = 2^16 row passes with 8 coefficients per thread (one
+// 256-point row per warp, 4-row tiles, 3 + 3 + 2 stages through two padded
+// warp-local exchanges -- the layout of k_row_keymult8) instead of 16: half
+// the registers and shared memory per row, so ~2x the warps per SM.
+// Forward (stages 8..15 of the NTT, lazy [0, 8q) schedule, canonical
+// output; COMB 3: the drop-and-divide combine fused, v rows requested into
+// L2 at the item start) in place on dst; inverse (stages 0..7, output
+// [0, 2q) for the column pass) src -> dst.  Twiddles come from the full
+// per-prime tables (a.tw) in natural order per row, staged once per
+// (job, row tile) and reused for the batch.
+template <bool INV, int COMB = 0>
+__global__ void __launch_bounds__(128, 8) k_row8(NttLaunch a, CombineArgs cb) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t* lines = reinterpret_cast<uint32_t*>(smraw) + warp * 2 * kK8Stride;  // this warp's 2 input buffers
+  uint2* T = reinterpret_cast<uint2*>(smraw + kK8Rows * 2 * kK8Stride * 4) + warp * 256;
+  constexpr int kTiles = kR / kK8Rows;
+  const int B = a.batch;
+  const int items = a.njobs * kTiles * B;
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
+  if (i0 >= i1) return;
+  const int lhi = lane >> 2, llo = lane & 3;
+  // cursors (job, tile, b), b fastest
+  int b = i0 % B, tile = (i0 / B) % kTiles, job = (i0 / B) / kTiles;
+  int nb = b, ntile = tile, njob = job;
+  auto advance = [&](int& bb, int& tt, int& jj) {
+    if (++bb == B) {
+      bb = 0;
+      if (++tt == kTiles) {
+        tt = 0;
+        ++jj;
+      }
+    }
+  };
+  auto in_row = [&](int bb, int tt, const RowJob& J) {
+    const int r = tt * kK8Rows + warp;
+    return INV ? a.src + bb * a.src_bs + (size_t)J.src_off * kN + (size_t)r * kR
+               : a.dst + bb * a.dst_bs + (size_t)J.dst_off * kN + (size_t)r * kR;
+  };
+  auto stage_row = [&](uint32_t* line, const uint32_t* g) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int c = 4 * (lane + 32 * m);
+      cp16(line + pad8(c), g + c);
+    }
+  };
+  RowJob J = a.jobs[job], Jn = J;
+  stage_row(lines, in_row(b, tile, J));
+  cp_commit();
+  uint32_t q = 0, q2 = 0, q4 = 0, qinv = 0, di = 0;
+  for (int it = i0, k = 0; it < i1; ++it, ++k) {
+    uint32_t* line = lines + (k & 1) * kK8Stride;
+    const int r = tile * kK8Rows + warp;
+    if (it == i0 || b == 0) {  // new (job, tile): prime and this row's 255 twiddles (natural order)
+      __syncwarp();
+      const PrimeDev P = a.primes[J.prime];
+      q = P.q;
+      q2 = P.q2;
+      q4 = 2 * P.q2;
+      qinv = P.qinv_neg;
+      const uint2* F = a.tw + (size_t)J.prime * kN;
+      if (!INV) {
+        for (int e = lane; e < 255; e += 32) {
+          const int s = 31 - __clz(e + 1), blk = e + 1 - (1 << s);
+          T[e] = __ldg(&F[(256 << s) + (r << s) + blk]);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          for (int blk = lane; blk < (128 >> v); blk += 32)
+            T[256 - (256 >> v) + blk] = __ldg(&F[(kN >> (v + 1)) + (r << (7 - v)) + blk]);
+      }
+      if (COMB) di = cb.dinv[J.dst_off - (J.dst_off / cb.out_q) * cb.out_q];
+    }
+    if (it + 1 < i1) {  // prefetch the next item's row into the other buffer
+      advance(nb, ntile, njob);
+      if (njob != job) Jn = a.jobs[njob];
+      stage_row(lines + ((k + 1) & 1) * kK8Stride, in_row(nb, ntile, Jn));
+    }
+    cp_commit();
+    if (COMB == 3) {  // the combine's v row into L2 now (plain loads at the end); one lane per 128 B line
+      const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
+      if ((lane & 3) == 0)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN +
+                                                       (size_t)r * kR + 8 * lane));
+    }
+    cp_wait<1>();
+    __syncwarp();
+    uint32_t u[8];
+    if (!INV) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[j] = line[pad8(lane + 32 * j)];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int d = 4 >> t;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = T[(1 << t) - 1 + blk];
+          if (t % 2 == 0) ctl<true>(u[j], u[j + d], w.x, w.y, q, q2, q4);
+          else ctl<false>(u[j], u[j + d], w.x, w.y, q, q2, q4);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) line[pad8(lane + 32 * j)] = u[j];
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[j] = line[pad8(32 * lhi + 4 * j + llo)];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int d = 4 >> t, sg = 3 + t;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = T[(1 << sg) - 1 + (lhi << t) + blk];
+          if (sg % 2 == 0) ctl<true>(u[j], u[j + d], w.x, w.y, q, q2, q4);
+          else ctl<false>(u[j], u[j + d], w.x, w.y, q, q2, q4);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) line[pad8(32 * lhi + 4 * j + llo)] = u[j];
+      __syncwarp();
+      {
+        const uint4 x0 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane));
+        const uint4 x1 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane + 4));
+        u[0] = x0.x; u[1] = x0.y; u[2] = x0.z; u[3] = x0.w;
+        u[4] = x1.x; u[5] = x1.y; u[6] = x1.z; u[7] = x1.w;
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int d = 2 >> t, sg = 6 + t;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          const uint2 w = T[(1 << sg) - 1 + (lane << (t + 1)) + blk];
+          if (sg % 2 == 0) ctl<true>(u[j], u[j + d], w.x, w.y, q, q2, q4);
+          else ctl<false>(u[j], u[j + d], w.x, w.y, q, q2, q4);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[j] = canon8(u[j], q, q2, q4);
+      if (COMB) {  // out = (v - NTT) d^-1 (ckks.cpp:643-651); J.dst_off = p * out_q + i
+        const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
+        const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + (size_t)r * kR + 8 * lane;
+        const uint4 v0 = *reinterpret_cast<const uint4*>(vr), v1 = *reinterpret_cast<const uint4*>(vr + 4);
+        const uint32_t vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = sub_if(mont_mul(vv[j] - u[j] + q, di, q, qinv), q);
+      }
+      uint32_t* orow = a.dst + b * a.dst_bs + (size_t)J.dst_off * kN + (size_t)r * kR + 8 * lane;
+      stg4(orow, make_uint4(u[0], u[1], u[2], u[3]));
+      stg4(orow + 4, make_uint4(u[4], u[5], u[6], u[7]));
+    } else {
+      {
+        const uint4 x0 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane));
+        const uint4 x1 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane + 4));
+        u[0] = x0.x; u[1] = x0.y; u[2] = x0.z; u[3] = x0.w;
+        u[4] = x1.x; u[5] = x1.y; u[6] = x1.z; u[7] = x1.w;
+      }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int d = 1 << v;
+#pragma unroll
+        for (int p4 = 0; p4 < 4; ++p4) {
+          const int blk = p4 / d, kk = blk * 2 * d + p4 % d;
+          const uint2 w = T[256 - (256 >> v) + (lane << (2 - v)) + blk];
+          gs(u[kk], u[kk + d], w.x, w.y, q, q2);
+        }
+      }
+      *reinterpret_cast<uint4*>(line + pad8(8 * lane)) = make_uint4(u[0], u[1], u[2], u[3]);
+      *reinterpret_cast<uint4*>(line + pad8(8 * lane + 4)) = make_uint4(u[4], u[5], u[6], u[7]);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[j] = line[pad8(32 * lhi + 4 * j + llo)];
+#pragma unroll
+      for (int v = 2; v < 5; ++v) {
+        const int d = 1 << (v - 2);
+#pragma unroll
+        for (int p4 = 0; p4 < 4; ++p4) {
+          const int blk = p4 / d, j = blk * 2 * d + p4 % d;
+          const uint2 w = T[256 - (256 >> v) + (lhi << (4 - v)) + blk];
+          gs(u[j], u[j + d], w.x, w.y, q, q2);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) line[pad8(32 * lhi + 4 * j + llo)] = u[j];
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[j] = line[pad8(lane + 32 * j)];
+#pragma unroll
+      for (int v = 5; v < 8; ++v) {
+        const int d = 1 << (v - 5);
+#pragma unroll
+        for (int p4 = 0; p4 < 4; ++p4) {
+          const int blk = p4 / d, j = blk * 2 * d + p4 % d;
+          const uint2 w = T[256 - (256 >> v) + blk];
+          gs(u[j], u[j + d], w.x, w.y, q, q2);
+        }
+      }
+      uint32_t* orow = a.dst + b * a.dst_bs + (size_t)J.dst_off * kN + (size_t)r * kR;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) orow[lane + 32 * j] = u[j];
+    }
+    __syncwarp();  // this warp's buffer k&1 is refilled by the prefetch of iteration k+1
+    b = nb;
+    tile = ntile;
+    job = njob;
+    J = Jn;
+  }
+  cp_wait<0>();
+}
+
 }  // namespace
 
 // CK32_KM selects the k_row_keymult variant for A/B runs: 7 = k_row_keymult8
@@ -1823,6 +2036,32 @@ void conv_mid(const ConvMidLaunch& a, cudaStream_t st) {
   }
 }
 
+
+// CK32_ROW8=1: the plain row passes run as k_row8 (8 coefficients per thread)
+constexpr int kRow8Smem = kK8Rows * 2 * kK8Stride * 4 + kK8Rows * 256 * 8;  // 2 input buffers + twiddles, 17 KB
+static bool use_row8() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("CK32_ROW8");
+    v = e && e[0] == '1';
+  }
+  return v == 1;
+}
+template <bool INV, int COMB>
+static void launch_row8(const NttLaunch& a, const CombineArgs& cb, cudaStream_t st) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_row8<INV, COMB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRow8Smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row8<INV, COMB>, 128, kRow8Smem);
+    grid = sms * std::max(1, per);
+  }
+  const int items = a.njobs * (kR / kK8Rows) * a.batch;
+  k_row8<INV, COMB><<<std::min(grid, items), 128, kRow8Smem, st>>>(a, cb);
+}
+
 // Individual passes (used when the fused kernels replace the other pass).
 void ntt256_pass(int which, const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
   init_grids();
@@ -1832,10 +2071,18 @@ void ntt256_pass(int which, const NttLaunch& a, const uint2* tw2, cudaStream_t s
       launch_col<false>(a, a.src, a.src_bs, st);
       break;
     case 1:  // forward row pass, in place on dst
+      if (use_row8()) {
+        launch_row8<false, 0>(a, CombineArgs{}, st);
+        break;
+      }
       k_row<false><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs,
                                                                       a.batch, a.njobs, a.primes, tw2);
       break;
     case 2:  // inverse row pass src -> dst
+      if (use_row8()) {
+        launch_row8<true, 0>(a, CombineArgs{}, st);
+        break;
+      }
       k_row<true><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.src, a.src_bs, a.dst, a.dst_bs,
                                                                      a.batch, a.njobs, a.primes, tw2);
       break;
@@ -2078,6 +2325,10 @@ bool ntt256_forward(const NttLaunch& a, const uint2* tw2, cudaStream_t st) {
   init_grids();
   const int row_items = a.njobs * (kR / kRRows) * a.batch;
   launch_col<false>(a, a.src, a.src_bs, st);
+  if (use_row8()) {
+    launch_row8<false, 0>(a, CombineArgs{}, st);
+    return true;
+  }
   k_row<false><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.dst, a.dst_bs, a.dst, a.dst_bs, a.batch,
                                                                   a.njobs, a.primes, tw2);
   return true;
@@ -2118,7 +2369,8 @@ bool ntt256_forward_combine(const NttLaunch& a, const uint2* tw2, const CombineA
   }
   const int row_items = a.njobs * (kR / kRRows) * a.batch;
   launch_col<false>(a, a.src, a.src_bs, st);
-  if (early == 2) launch_row_comb<3>(a, tw2, cb, row_items, st);
+  if (early == 2 && use_row8()) launch_row8<false, 3>(a, cb, st);
+  else if (early == 2) launch_row_comb<3>(a, tw2, cb, row_items, st);
   else if (early) launch_row_comb<2>(a, tw2, cb, row_items, st);
   else launch_row_comb<1>(a, tw2, cb, row_items, st);
   return true;
@@ -2127,8 +2379,11 @@ bool ntt256_forward_combine(const NttLaunch& a, const uint2* tw2, const CombineA
 bool ntt256_inverse(const NttLaunch& a, const uint2* tw2i, cudaStream_t st) {
   init_grids();
   const int row_items = a.njobs * (kR / kRRows) * a.batch;
-  k_row<true><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.src, a.src_bs, a.dst, a.dst_bs, a.batch,
-                                                                 a.njobs, a.primes, tw2i);
+  if (use_row8())
+    launch_row8<true, 0>(a, CombineArgs{}, st);
+  else
+    k_row<true><<<min(g_row_grid, row_items), kRT, kRowSmem, st>>>(a.jobs, a.src, a.src_bs, a.dst, a.dst_bs, a.batch,
+                                                                   a.njobs, a.primes, tw2i);
   NttLaunch b = a;
   b.entry = 0;
   launch_col<true>(b, a.dst, a.dst_bs, st);

@@ -803,3 +803,52 @@ print("fused-intt ok")
     env = dict(__import__("os").environ, CK32_KM_INTT="1")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0 and "fused-intt ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("level", [24, 7])
+def test_row8_row_passes_match_oracle(level):
+    """CK32_ROW8=1 (read once per process: fresh subprocess): the plain row
+    passes run as k_row8 (8 coefficients per thread) -- NTT round trip, the
+    INTT part-1 epilogue, HMult (merged and lazy) and HRot equal the oracle."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = f'''
+import sys, numpy as np, torch
+sys.path[:0] = {[str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent.parent / "oracle")]!r}
+from fractions import Fraction
+from paper_2407_13055_b200 import ckks
+from pyoracle import Oracle, Rng
+n, l, a, db, level = 1 << 16, 24, 8, 55, {level}
+O = Oracle(n, l, a, db)
+dev = lambda v: torch.from_numpy(np.ascontiguousarray(v.astype(np.int32))).cuda()
+C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db))
+g = O.gidx(level, 3)
+x = O.random_rows(Rng(level), g)
+p = ckks.Polynomial(dev(x), level, 3, ckks.COEFFICIENT, False)
+ckks.ntt_forward(C, p)
+f = O.ntt_fwd(x, g)
+assert np.array_equal(p.data.cpu().numpy().astype(np.uint32), O.canonical(f, g))
+ckks.intt_inverse(C, p)
+assert np.array_equal(p.data.cpu().numpy().astype(np.uint32), x.astype(np.uint32))
+C.close()
+xb, xa, yb, ya, evk = O.synthetic(level, 4242 + level)
+for lazy in (False, True):
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db, lazy_rescale=lazy))
+    xc = ckks.Ciphertext(dev(np.stack([xb, xa])), Fraction(1 << db), level)
+    yc = ckks.Ciphertext(dev(np.stack([yb, ya])), Fraction(1 << db), level)
+    got = ckks.hmult(C, xc, yc, ckks.EvaluationKey(dev(evk))).data.cpu().numpy().astype(np.uint32)
+    ob, oa = O.hmult(level, xb, xa, yb, ya, evk, lazy=lazy)
+    lo = level if lazy else level - 2
+    assert np.array_equal(got, np.stack([O.canonical(ob, O.gidx(lo)), O.canonical(oa, O.gidx(lo))])), lazy
+    if not lazy:
+        got = ckks.hrot(C, xc, 5, ckks.EvaluationKey(dev(evk), ckks.ROTATION, 5)).data.cpu().numpy().astype(np.uint32)
+        ob, oa = O.hrot(level, xb, xa, 5, evk)
+        assert np.array_equal(got, np.stack([O.canonical(ob, O.gidx(level)), O.canonical(oa, O.gidx(level))]))
+    C.close()
+print("row8 ok")
+'''
+    env = dict(__import__("os").environ, CK32_ROW8="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "row8 ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
