@@ -332,7 +332,7 @@ struct Context {
   bool use_fused_combine = true;  // CK32_NO_FUSED_COMBINE=1: separate k_combine after the ModDown NTT
   bool use_hrot_tail = false;     // CK32_FUSED_TAIL=1: HRot tail fused into the ModDown forward row pass (measured
                                   // neutral: 16.82k vs 16.86k ops/s, profiles/r2/README.md), else k_hrot_tail
-  bool use_tc = false;  // CK32_TC=1: tcgen05 split-word BConv (bit-exact; slower than the CUDA-core kernel today)  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
+  bool use_tc = true;  // tcgen05 split-word BConv (bconv_tc.cu; CK32_TC=0: the CUDA-core k_bconv)  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
   int bconv_fp64 = 0;   // CK32_BCONV_FP64=1|2|3: exact BConv dot products on the FP64 pipe for all / 1 of 2 / 2 of 3 rows
   bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
   int ntt_chunk_limbs = 1 << 30;  // limbs per pass-1/pass-2 launch pair (CK32_NTT_CHUNK; measured: no gain)
@@ -1900,8 +1900,13 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     if (const char* ch = std::getenv("CK32_NTT_CHUNK")) c->ntt_chunk_limbs = std::max(1, std::atoi(ch));
     c->use_fused = std::getenv("CK32_FUSED") != nullptr;
     c->use_row_km = std::getenv("CK32_NO_ROW_KEYMULT") == nullptr;
-    c->use_tc = std::getenv("CK32_TC") != nullptr;
     if (const char* f = std::getenv("CK32_BCONV_FP64")) c->bconv_fp64 = std::atoi(f);
+    // BConv on tcgen05 by default (whole-step A/B r2ad / r2ae: 16.95-17.01k vs
+    // 16.91-16.97k ops/s with the CUDA-core kernel: the IMAD.WIDE work moves
+    // to the tensor pipe while the other stream's NTTs hold the IMAD pipe);
+    // CK32_TC=0 selects the CUDA-core kernel, as does an FP64-pipe mode
+    const char* tc = std::getenv("CK32_TC");
+    c->use_tc = (tc ? std::atoi(tc) != 0 : true) && c->bconv_fp64 == 0;
     c->use_fused_combine = std::getenv("CK32_NO_FUSED_COMBINE") == nullptr;
     c->use_hrot_tail = std::getenv("CK32_FUSED_TAIL") != nullptr;
     c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;

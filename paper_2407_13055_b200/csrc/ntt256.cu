@@ -1418,7 +1418,10 @@ constexpr int kK8Smem = kK8SmemBase + kK8Rows * 256 * 8;  // + inverse twiddles 
 
 // EARLY: the key halves of digit k are loaded before its row pass (16
 // registers live across it); without, they are loaded after it (more CTAs).
-template <int MINB, bool EARLY = true>
+// KPF (with !EARLY): 1 = the digit's key lines are requested into L1
+// (prefetch.global.L1) before its row pass, 2 = the next digit's during this
+// digit's row pass (the first digit's at the item start).
+template <int MINB, bool EARLY = true, int KPF = 0>
 __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, const uint2* __restrict__ fwd) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1426,6 +1429,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
   uint2* tws = reinterpret_cast<uint2*>(smraw + 3 * kK8Rows * kK8Stride * 4);   // [4][256] forward, [4][256] inverse
   uint2* T = tws + warp * 256;
   uint2* Ti = tws + (kK8Rows + warp) * 256;  // inverse row twiddles (fused INTT pass A), natural order per stage
+  uint32_t* Ks = reinterpret_cast<uint32_t*>(smraw + kK8Smem) + warp * (3 * 2 * 256);  // KPF 3: key slice [D][2][256]
   constexpr int kTiles = kR / kK8Rows;
   const int rows = a.level + a.alpha, B = a.batch;
   const uint32_t LA = (uint32_t)(a.L + a.alpha);
@@ -1461,6 +1465,16 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
           for (int blk = lane; blk < (128 >> v); blk += 32)
             Ti[256 - (256 >> v) + blk] = __ldg(&I[(kN >> (v + 1)) + (r << (7 - v)) + blk]);
       }
+      if (KPF == 3) {  // this row's key slice (D digits x 2 halves x 256 words) into shared memory, reused for all b
+        for (int k = 0; k < a.D; ++k)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t* kr = a.evk + (((size_t)k * 2 + h) * LA + g) * kN + (size_t)r * kR;
+#pragma unroll
+            for (int m = 0; m < 2; ++m) cp16(Ks + (k * 2 + h) * 256 + 4 * (lane + 32 * m), kr + 4 * (lane + 32 * m));
+          }
+        cp_commit();  // older than the extension groups below: complete at the first digit's wait
+      }
     }
     // all digits' extension rows at once (one cp.async group per digit)
     for (int k = 0; k < a.D; ++k) {
@@ -1487,11 +1501,20 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
     uint64_t s0[8], s1[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) s0[j] = s1[j] = 0;
+    auto key_l1 = [&](int kk) {  // one lane per 128 B line of this thread's key coefficients
+      if ((lane & 3) == 0) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.evk + (((size_t)kk * 2 + 0) * LA + g) * kN + rofs));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.evk + (((size_t)kk * 2 + 1) * LA + g) * kN + rofs));
+      }
+    };
+    if (KPF == 2) key_l1(0);
     for (int k = 0; k < a.D; ++k) {
       const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
       uint4 kb[2], ka[2];  // key halves (EARLY: first, their L2 latency hides behind the butterflies)
       const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
       const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
+      if (KPF == 1) key_l1(k);
+      if (KPF == 2 && k + 1 < a.D) key_l1(k + 1);
       if (EARLY) {
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
@@ -1501,6 +1524,12 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       }
       uint32_t v[8];
       if (i >= lo && i < hi) {  // the digit's own row (ModUp pass-through), evaluation form already
+        if (KPF == 3 && k == 0) {  // no extension wait precedes this digit: wait for the key group here
+          if (a.D >= 3) cp_wait<2>();
+          else if (a.D == 2) cp_wait<1>();
+          else cp_wait<0>();
+          __syncwarp();
+        }
         const uint32_t* dr = a.d + b * a.d_bs + (size_t)i * kN + rofs;
         const uint4 x0 = *reinterpret_cast<const uint4*>(dr), x1 = *reinterpret_cast<const uint4*>(dr + 4);
         v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
@@ -1567,7 +1596,13 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = canon8(v[j], q, q2, q4);
       }
-      if (!EARLY) {
+      if (KPF == 3) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          kb[m] = *reinterpret_cast<const uint4*>(Ks + (k * 2 + 0) * 256 + 8 * lane + 4 * m);
+          ka[m] = *reinterpret_cast<const uint4*>(Ks + (k * 2 + 1) * 256 + 8 * lane + 4 * m);
+        }
+      } else if (!EARLY) {
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           kb[m] = __ldg(reinterpret_cast<const uint4*>(eb + 4 * m));
@@ -1951,23 +1986,23 @@ bool row_keymult_fuses_intt(const KeyMultLaunch& a) {
   static int on = -1;
   if (on < 0) on = std::getenv("CK32_KM_INTT") != nullptr;
   const int v = km_version();
-  return on && (v == 7 || v == 8) && a.D <= 3;
+  return on && v >= 7 && v <= 11 && a.D <= 3;
 }
 
-template <int MINB, bool EARLY>
+template <int MINB, bool EARLY, int KPF = 0>
 static void launch_km8(const KeyMultLaunch& a, const uint2* fwd, int items, cudaStream_t st) {
   static int grid[2] = {0, 0};
   const int fi = a.ts ? 1 : 0;  // the inverse twiddle region only when the INTT pass A is fused
-  const int smem = fi ? kK8Smem : kK8SmemBase;
+  const int smem = KPF == 3 ? kK8Smem + kK8Rows * 3 * 2 * 256 * 4 : fi ? kK8Smem : kK8SmemBase;
   if (!grid[fi]) {
-    cudaFuncSetAttribute(k_row_keymult8<MINB, EARLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK8Smem);
+    cudaFuncSetAttribute(k_row_keymult8<MINB, EARLY, KPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<MINB, EARLY>, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<MINB, EARLY, KPF>, 128, smem);
     grid[fi] = sms * std::max(1, per);
   }
-  k_row_keymult8<MINB, EARLY><<<std::min(grid[fi], items), 128, smem, st>>>(a, fwd);
+  k_row_keymult8<MINB, EARLY, KPF><<<std::min(grid[fi], items), 128, smem, st>>>(a, fwd);
 }
 
 template <int MINB>
@@ -1996,9 +2031,15 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, cons
     launch_km<true, 4, true, true, true>(a, tw2, items, st);
     return;
   }
-  if ((ver == 7 || ver == 8) && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
+  if (ver >= 7 && ver <= 11 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
     const int items8 = (a.level + a.alpha) * (kR / kK8Rows) * a.batch;
-    if (ver == 7)
+    if (ver == 11)
+      launch_km8<4, false, 3>(a, fwd_full, items8, st);  // key slice staged in shared memory per (row, tile), 4 CTAs / SM
+    else if (ver == 9)
+      launch_km8<8, false, 1>(a, fwd_full, items8, st);  // + the digit's key lines into L1 before its row pass
+    else if (ver == 10)
+      launch_km8<8, false, 2>(a, fwd_full, items8, st);  // + the next digit's key lines into L1 one digit ahead
+    else if (ver == 7)
       launch_km8<6, true>(a, fwd_full, items8, st);  // keys ahead of the row pass, 6 CTAs / SM
     else
       launch_km8<8, false>(a, fwd_full, items8, st);  // keys after it, 64 registers, 8 CTAs / SM

@@ -91,6 +91,24 @@ def test_bconv_matches_oracle(n, shape):
     np.testing.assert_array_equal(host(got), want)
 
 
+@pytest.mark.parametrize("shape", [(8, 24), (10, 22), (2, 22), (1, 3), (16, 40)])
+def test_bconv_cuda_core_matches_oracle(monkeypatch, shape):
+    """The CUDA-core BConv (k_bconv, CK32_TC=0; the tcgen05 kernel is the
+    default) equals the oracle."""
+    monkeypatch.setenv("CK32_TC", "0")
+    sc, dc = shape
+    n, l, a = 65536, 40, 16
+    C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=48))
+    O = Oracle(n, l, a, 48)
+    src_g = list(range(l - sc, l)) if sc <= 10 else [l + j for j in range(sc)]
+    dst_g = list(range(dc))
+    src = O.canonical(O.random_rows(Rng(sc * 100 + dc), np.array(src_g, np.uint32)), np.array(src_g, np.uint32))
+    got = ckks.bconv(C, dev(src), src_g, dst_g)
+    want = O.canonical(O.bconv(src.astype(np.int32), src_g, dst_g), np.array(dst_g, np.uint32))
+    np.testing.assert_array_equal(host(got), want)
+    C.close()
+
+
 @pytest.fixture
 def tc_env(monkeypatch):
     """Contexts created inside the test run BConv on the tcgen05 split-word
@@ -806,10 +824,15 @@ print("fused-intt ok")
 
 
 @pytest.mark.parametrize("level", [24, 7])
-def test_row8_row_passes_match_oracle(level):
-    """CK32_ROW8=1 (read once per process: fresh subprocess): the plain row
-    passes run as k_row8 (8 coefficients per thread) -- NTT round trip, the
-    INTT part-1 epilogue, HMult (merged and lazy) and HRot equal the oracle."""
+@pytest.mark.parametrize("variant", ["CK32_ROW8=1", "CK32_KM=7", "CK32_KM=9", "CK32_KM=10", "CK32_KM=11", "CK32_TC=0"])
+def test_variant_paths_match_oracle(level, variant):
+    """Opt-in kernel variants (env switches read once per process: a fresh
+    subprocess each) -- CK32_ROW8=1: the plain row passes as k_row8 (8
+    coefficients per thread); CK32_KM=7/9/10/11: the fused row pass + KeyMult
+    with the key ahead of the row pass / L1-prefetched / L1-prefetched one
+    digit ahead / staged in shared memory per (row, tile); CK32_TC=0: BConv
+    on the CUDA cores (k_bconv) instead of tcgen05 -- NTT round trip, HMult (merged and lazy) and HRot equal the
+    oracle."""
     import subprocess
     import sys
     from pathlib import Path
@@ -847,8 +870,9 @@ for lazy in (False, True):
         ob, oa = O.hrot(level, xb, xa, 5, evk)
         assert np.array_equal(got, np.stack([O.canonical(ob, O.gidx(level)), O.canonical(oa, O.gidx(level))]))
     C.close()
-print("row8 ok")
+print("variant ok")
 '''
-    env = dict(__import__("os").environ, CK32_ROW8="1")
+    k, v = variant.split("=")
+    env = dict(__import__("os").environ, **{k: v})
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env)
-    assert r.returncode == 0 and "row8 ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
