@@ -103,6 +103,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// wait for the outstanding tcgen05.ld's; the destination registers are tied
+// to the wait so no use of them is scheduled above it
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
 // sum_a 2^(8a) acc_a  (< 2^46) Montgomery-reduced mod q, canonical
 __device__ __forceinline__ uint32_t combine4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t q,
                                              uint32_t qinv_neg) {
@@ -239,12 +262,212 @@ __global__ void __launch_bounds__(kTT) k_bconv_tc(BconvLaunch a, BconvTc t, int 
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(NCOLS));
 }
 
+// (group, batch item, tile) item cursor, tile fastest: advanced by one per
+// item (a CTA owns a contiguous chunk), so the loop does no integer division
+struct TcCursor {
+  int tile, b, g;
+  __device__ __forceinline__ void init(int it, int tiles, int batch) {
+    tile = it % tiles;
+    const int rest = it / tiles;
+    b = rest % batch;
+    g = rest / batch;
+  }
+  __device__ __forceinline__ void next(int tiles, int batch) {
+    if (++tile == tiles) {
+      tile = 0;
+      if (++b == batch) {
+        b = 0;
+        ++g;
+      }
+    }
+  }
+};
+
+
+// k_bconv_tc2 epilogue for 8 destination rows: r = the 32 TMEM columns (4 byte
+// planes per row) of this thread's coefficient; dq = {q, q^-1}, doff = row * n
+template <bool FULL>
+__device__ __forceinline__ void tc2_store8(const uint32_t (&r)[32], const uint2* dq, const uint32_t* doff, int nv,
+                                           uint32_t* dthr) {
+  const uint4* dq4 = reinterpret_cast<const uint4*>(dq);
+  const uint4 o0 = *reinterpret_cast<const uint4*>(doff), o1 = *reinterpret_cast<const uint4*>(doff + 4);
+  const uint32_t off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+  const uint64_t base = reinterpret_cast<uint64_t>(dthr);
+#pragma unroll
+  for (int u2 = 0; u2 < 4; ++u2) {
+    const uint4 qq = dq4[u2];  // {q, q^-1} of rows 2 u2, 2 u2 + 1
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int u = 2 * u2 + e;
+      const uint32_t q = e ? qq.z : qq.x, qi = e ? qq.w : qq.y;
+      const uint32_t x = r[4 * u] + (r[4 * u + 1] << 8);      // < 2^31
+      const uint32_t y = r[4 * u + 2] + (r[4 * u + 3] << 8);  // < 2^31
+      uint32_t lo, hi;  // x + 2^16 y = sum_a 2^(8a) acc_a < 2^46
+      asm("mad.lo.cc.u32 %0, %2, 65536, %3;\n\tmadc.hi.u32 %1, %2, 65536, 0;\n" : "=r"(lo), "=r"(hi) : "r"(y), "r"(x));
+      const uint32_t v = sub_if(mont_reduce64s(lo, hi, q, qi), q);
+      uint64_t addr;  // one IMAD.WIDE.U32 per store address
+      asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(addr) : "r"(off[u]), "l"(base));
+      if (FULL || u < nv) asm volatile("st.global.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+    }
+  }
+}
+
+// k_bconv_tc2: the same GEMM with a slimmer instruction stream (the kernel
+// above is issue-bound at ~60% issue with ~800 warp instructions per item, a
+// quarter of them integer divisions decoding the item twice):
+//  * incremental item cursors (no division per item);
+//  * epilogue per output: the 4 byte planes combined into (lo, hi) with two
+//    shift-adds and one 64-bit shift-add, then the SUBTRACTIVE Montgomery
+//    reduction hi - umulhi(lo q^-1, q) (no carry term) and one min for the
+//    canonical residue -- identical canonical output;
+//  * per-group destination constants staged as {q, q^-1} pairs and 32-bit
+//    row offsets (vector loads, 8 rows at a time);
+//  * the next 8-row block's tcgen05.ld is issued before the current block is
+//    reduced (two 32-register buffers), so the TMEM load latency is hidden.
+template <int KB, int NCOLS>
+__global__ void __launch_bounds__(kTT) k_bconv_tc2(BconvLaunch a, BconvTc t, int n) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int kSbo = (KB / 16) * 128;
+  constexpr int kATile = kTT * KB;
+  const int rawStage = a.max_sc * kTT;
+  const int dcPad = (t.max_dc + 7) / 8 * 8;
+  uint32_t* raw = reinterpret_cast<uint32_t*>(smraw);              // [kNst][max_sc][128] u32
+  unsigned char* At = smraw + (size_t)kNst * rawStage * 4;         // A tile (128-B aligned)
+  unsigned char* Bt = At + kATile;                                 // B table of the current group
+  uint2* dq = reinterpret_cast<uint2*>(Bt + t.max_npad * KB);      // [dcPad] {q, q^-1}
+  uint32_t* doff = reinterpret_cast<uint32_t*>(dq + dcPad);        // [dcPad] destination row * n
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(doff + dcPad);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tiles = n / kTT;
+  const int items = a.ngroups * a.batch * tiles;
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
+  if (i0 >= i1) return;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "n"(NCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+
+  TcCursor ic;  // the next item to issue
+  ic.init(i0, tiles, a.batch);
+  int icount = i0;
+  auto issue = [&](int slot) {  // raw source tile of item `ic` into ring slot `slot`, then advance
+    if (icount < i1) {
+      const BconvGroup G = a.groups[ic.g];
+      const uint32_t* src = a.src + ic.b * a.src_bs + (size_t)G.src_off * n + (size_t)ic.tile * kTT;
+      uint32_t* dst = raw + slot * rawStage;
+      for (int e = tid; e < (int)G.sc * (kTT / 4); e += kTT) {
+        const int j = e >> 5, c = e & 31;  // kTT / 4 = 32 chunks of 16 B per source row
+        cp16(dst + j * kTT + 4 * c, src + (size_t)j * n + 4 * c);
+      }
+      ic.next(tiles, a.batch);
+      ++icount;
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < kNst - 1; ++s) issue(s);
+
+  TcCursor pc;  // the item being processed
+  pc.init(i0, tiles, a.batch);
+  int cur_g = -1, sc = 0, dc = 0, npad = 16;
+  uint32_t phase = 0;
+  for (int it = i0, k = 0; it < i1; ++it, ++k) {
+    cp_wait<kNst - 2>();
+    __syncthreads();  // raw tile k landed for all threads; iteration k-1 fully done (A, B, TMEM free)
+    issue((k + kNst - 1) % kNst);
+    const int tile = pc.tile, b = pc.b, g = pc.g;
+    pc.next(tiles, a.batch);
+    if (g != cur_g) {  // new group: its B table and destination constants
+      cur_g = g;
+      const BconvGroup G = a.groups[g];
+      sc = (int)G.sc;
+      dc = (int)G.dc;
+      npad = (4 * dc + 15) / 16 * 16;
+      const uint4* B = reinterpret_cast<const uint4*>(t.btab + t.boff[g]);
+      uint4* Bs = reinterpret_cast<uint4*>(Bt);
+      for (int e = tid; e < npad * KB / 16; e += kTT) Bs[e] = __ldg(B + e);
+      for (int i = tid; i < dcPad; i += kTT) {
+        uint2 d = make_uint2(1u, 1u);
+        uint32_t o = 0;
+        if (i < dc) {
+          const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
+          d = make_uint2(P.q, P.qinv);
+          o = a.dst_row[G.map_off + i] * (uint32_t)n;
+        }
+        dq[i] = d;
+        doff[i] = o;
+      }
+    }
+    {  // transpose: row x = tid, K chunk c holds the words src[4c .. 4c+3][x] (zero past sc)
+      const uint32_t* R = raw + (k % kNst) * rawStage;
+      uint32_t w[KB / 4];
+#pragma unroll
+      for (int j = 0; j < KB / 4; ++j) w[j] = j < sc ? R[j * kTT + tid] : 0u;
+      unsigned char* row = At + (tid >> 3) * kSbo + (tid & 7) * 16;
+#pragma unroll
+      for (int c = 0; c < KB / 16; ++c)
+        *reinterpret_cast<uint4*>(row + c * 128) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after();
+      const uint32_t idesc = idesc_u8(kTT, npad);
+      const uint32_t a0 = smem_u32(At), b0 = smem_u32(Bt);
+#pragma unroll
+      for (int kk = 0; kk < KB / 32; ++kk)
+        mma_u8(tmem, sdesc(a0 + kk * 256, 128, kSbo), sdesc(b0 + kk * 256, 128, kSbo), idesc, kk > 0);
+      mma_commit(mbar);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    fence_after();
+    uint32_t* dthr = a.dst + b * a.dst_bs + (size_t)tile * kTT + tid;
+    uint32_t r[2][32];
+    tmem_ld32_nowait(lane_addr, r[0]);
+    tmem_wait_ld(r[0]);
+#pragma unroll 1
+    for (int i8 = 0; i8 < dc; i8 += 16) {  // two 8-row blocks per trip: buffer 0, then buffer 1
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ib = i8 + 8 * h;
+        if (ib >= dc) break;
+        if (ib + 8 < dc) tmem_ld32_nowait(lane_addr + 4 * (ib + 8), r[h ^ 1]);  // next block in flight
+        if (ib + 8 <= dc)
+          tc2_store8<true>(r[h], dq + ib, doff + ib, 8, dthr);
+        else
+          tc2_store8<false>(r[h], dq + ib, doff + ib, dc - ib, dthr);
+        tmem_wait_ld(r[h ^ 1]);
+      }
+    }
+    fence_before();
+  }
+  cp_wait<0>();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(NCOLS));
+}
+
 template <int KB, int NCOLS>
 void launch_tc(const BconvLaunch& a, const BconvTc& t, int n, cudaStream_t st) {
   const int smem = kNst * a.max_sc * kTT * 4 + kTT * KB + t.max_npad * KB + ((t.max_dc + 7) / 8 * 8) * 16 + 16;
   static int grid = 0, smem_set = 0;
   if (smem > smem_set) {
     cudaFuncSetAttribute(k_bconv_tc<KB, NCOLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_bconv_tc2<KB, NCOLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     smem_set = smem;
     grid = 0;
   }
@@ -261,7 +484,10 @@ void launch_tc(const BconvLaunch& a, const BconvTc& t, int n, cudaStream_t st) {
     grid = sms * std::max(1, per);
   }
   const int items = a.ngroups * a.batch * (n / kTT);
-  k_bconv_tc<KB, NCOLS><<<std::min(grid, items), kTT, smem, st>>>(a, t, n);
+  if (t.variant == 1)
+    k_bconv_tc<KB, NCOLS><<<std::min(grid, items), kTT, smem, st>>>(a, t, n);
+  else
+    k_bconv_tc2<KB, NCOLS><<<std::min(grid, items), kTT, smem, st>>>(a, t, n);
 }
 
 }  // namespace

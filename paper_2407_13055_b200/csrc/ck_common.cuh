@@ -29,7 +29,7 @@ struct PrimeDev {
   uint32_t qinv_neg;     // -q^{-1} mod 2^32 (unsigned Montgomery)
   uint32_t r, r_sh;      // R mod q and its Shoup companion (entry x*R)
   uint32_t w1r, w1r_sh;  // psi^{N/2} * R mod q (entry-merged stage-0 twiddle)
-  uint32_t pad;
+  uint32_t qinv;         // q^{-1} mod 2^32 (subtractive Montgomery, mont_reduce64s)
 };
 
 // One row transform: source/destination row offsets (in units of N words,
@@ -63,6 +63,13 @@ __device__ __forceinline__ uint64_t mac_wide(uint64_t acc, uint32_t a, uint32_t 
   uint64_t d;
   asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(acc));
   return d;
+}
+// Subtractive Montgomery reduction of t < q*2^32 -> [0, 2q), congruent to
+// t 2^-32: with m = lo q^-1, t - m q is divisible by 2^32 with no borrow out
+// of the low word, so (t - m q) / 2^32 = hi - umulhi(m, q) in (-q, q) exactly
+// (one instruction fewer than the additive form: no carry term)
+__device__ __forceinline__ uint32_t mont_reduce64s(uint32_t lo, uint32_t hi, uint32_t q, uint32_t qinv) {
+  return hi - __umulhi(lo * qinv, q) + q;
 }
 // Montgomery reduction of a 64-bit accumulator t < q*2^32 -> [0, 2q)
 __device__ __forceinline__ uint32_t mont_reduce64(uint64_t t, uint32_t q, uint32_t qinv_neg) {

@@ -333,6 +333,7 @@ struct Context {
   bool use_hrot_tail = false;     // CK32_FUSED_TAIL=1: HRot tail fused into the ModDown forward row pass (measured
                                   // neutral: 16.82k vs 16.86k ops/s, profiles/r2/README.md), else k_hrot_tail
   bool use_tc = true;  // tcgen05 split-word BConv (bconv_tc.cu; CK32_TC=0: the CUDA-core k_bconv)  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
+  int tc_var = 2;       // tcgen05 BConv kernel: 1 = k_bconv_tc, 2 = k_bconv_tc2 (slimmer epilogue; default)
   int bconv_fp64 = 0;   // CK32_BCONV_FP64=1|2|3: exact BConv dot products on the FP64 pipe for all / 1 of 2 / 2 of 3 rows
   bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
   int ntt_chunk_limbs = 1 << 30;  // limbs per pass-1/pass-2 launch pair (CK32_NTT_CHUNK; measured: no gain)
@@ -921,6 +922,7 @@ struct Context {
       t.boff = pl.blob.at<uint32_t>(pl.tc_boff_off);
       t.max_npad = pl.tc_max_npad;
       t.max_dc = pl.tc_max_dc;
+      t.variant = tc_var;
       bconv_tc((int)n, a, t, st);
     } else {
       bconv((int)n, a, st, bconv_fp64);
@@ -1888,7 +1890,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
       P.r_sh = shoup(P.r, q);
       P.w1r = mulm(pw[n / 2], P.r, q);
       P.w1r_sh = shoup(P.w1r, q);
-      P.pad = 0;
+      P.qinv = inv32;
     }
     CK_CUDA(cudaMalloc(&c->d_primes, np * sizeof(PrimeDev)));
     CK_CUDA(cudaMemcpy(c->d_primes, c->pdev_host.data(), np * sizeof(PrimeDev), cudaMemcpyHostToDevice));
@@ -1907,6 +1909,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     // CK32_TC=0 selects the CUDA-core kernel, as does an FP64-pipe mode
     const char* tc = std::getenv("CK32_TC");
     c->use_tc = (tc ? std::atoi(tc) != 0 : true) && c->bconv_fp64 == 0;
+    c->tc_var = tc && std::atoi(tc) == 1 ? 1 : 2;  // CK32_TC=1: the first tcgen05 kernel
     c->use_fused_combine = std::getenv("CK32_NO_FUSED_COMBINE") == nullptr;
     c->use_hrot_tail = std::getenv("CK32_FUSED_TAIL") != nullptr;
     c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;

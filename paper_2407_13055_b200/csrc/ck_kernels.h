@@ -116,6 +116,7 @@ struct BconvTc {
   const unsigned char* btab = nullptr;  // per-group B tables (canonical UMMA layout)
   const uint32_t* boff = nullptr;       // byte offset of each group's table
   int max_npad = 0, max_dc = 0;
+  int variant = 2;  // 1: k_bconv_tc, 2: k_bconv_tc2 (CK32_TC, read at context creation)
 };
 bool bconv_tc_supported(int n, int max_sc, int max_dc);
 void bconv_tc(int n, const BconvLaunch& a, const BconvTc& t, cudaStream_t st);

@@ -109,11 +109,12 @@ def test_bconv_cuda_core_matches_oracle(monkeypatch, shape):
     C.close()
 
 
-@pytest.fixture
-def tc_env(monkeypatch):
+@pytest.fixture(params=["1", "2"])
+def tc_env(monkeypatch, request):
     """Contexts created inside the test run BConv on the tcgen05 split-word
-    GEMM (CK32_TC=1, read at context creation; bconv_tc.cu)."""
-    monkeypatch.setenv("CK32_TC", "1")
+    GEMM (bconv_tc.cu; CK32_TC read at context creation): 1 = k_bconv_tc,
+    2 = k_bconv_tc2 (the default)."""
+    monkeypatch.setenv("CK32_TC", request.param)
     made = []
 
     def make(n, l, a, db=55):
