@@ -363,13 +363,18 @@ __global__ void __launch_bounds__(kTT) k_bconv_tc2(BconvLaunch a, BconvTc t, int
 
   TcCursor ic;  // the next item to issue
   ic.init(i0, tiles, a.batch);
-  int icount = i0;
+  int icount = i0, ig = -1;
+  uint32_t isrc = 0, isc = 0;  // the issue group's source offset and row count (reloaded on group change)
   auto issue = [&](int slot) {  // raw source tile of item `ic` into ring slot `slot`, then advance
     if (icount < i1) {
-      const BconvGroup G = a.groups[ic.g];
-      const uint32_t* src = a.src + ic.b * a.src_bs + (size_t)G.src_off * n + (size_t)ic.tile * kTT;
+      if (ic.g != ig) {
+        ig = ic.g;
+        isrc = a.groups[ig].src_off;
+        isc = a.groups[ig].sc;
+      }
+      const uint32_t* src = a.src + ic.b * a.src_bs + (size_t)isrc * n + (size_t)ic.tile * kTT;
       uint32_t* dst = raw + slot * rawStage;
-      for (int e = tid; e < (int)G.sc * (kTT / 4); e += kTT) {
+      for (int e = tid; e < (int)isc * (kTT / 4); e += kTT) {
         const int j = e >> 5, c = e & 31;  // kTT / 4 = 32 chunks of 16 B per source row
         cp16(dst + j * kTT + 4 * c, src + (size_t)j * n + 4 * c);
       }

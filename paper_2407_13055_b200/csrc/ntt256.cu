@@ -1623,8 +1623,8 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       if ((k % 6) == 5) {  // keep the sums below q 2^32 (value unchanged mod q, rescaled by R)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          s0[j] = shoup_mul(mont_reduce64(s0[j], q, P.qinv_neg), P.r, P.r_sh, q);
-          s1[j] = shoup_mul(mont_reduce64(s1[j], q, P.qinv_neg), P.r, P.r_sh, q);
+          s0[j] = shoup_mul(mont_reduce64s((uint32_t)(s0[j]), (uint32_t)((s0[j]) >> 32), q, P.qinv), P.r, P.r_sh, q);
+          s1[j] = shoup_mul(mont_reduce64s((uint32_t)(s1[j]), (uint32_t)((s1[j]) >> 32), q, P.qinv), P.r, P.r_sh, q);
         }
       }
     }
@@ -1655,7 +1655,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       for (int pp = 0; pp < 2; ++pp) {
         uint32_t u[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) u[j] = sub_if(mont_reduce64(pp ? s1[j] : s0[j], q, P.qinv_neg), q);
+        for (int j = 0; j < 8; ++j) u[j] = sub_if(mont_reduce64s((uint32_t)(pp ? s1[j] : s0[j]), (uint32_t)((pp ? s1[j] : s0[j]) >> 32), q, P.qinv), q);
         uint32_t* line = sbuf + (pp * kK8Rows + warp) * kK8Stride;  // digit buffers 0 / 1 are free now
         // stages v = 0, 1 on c = 8 lane + k
 #pragma unroll
@@ -1709,14 +1709,14 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
-        stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv_neg), q),
-                                    sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv_neg), q),
-                                    sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv_neg), q),
-                                    sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv_neg), q)));
-        stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv_neg), q),
-                                    sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv_neg), q),
-                                    sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv_neg), q),
-                                    sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv_neg), q)));
+        stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64s((uint32_t)(s0[4 * m]), (uint32_t)((s0[4 * m]) >> 32), q, P.qinv), q),
+                                    sub_if(mont_reduce64s((uint32_t)(s0[4 * m + 1]), (uint32_t)((s0[4 * m + 1]) >> 32), q, P.qinv), q),
+                                    sub_if(mont_reduce64s((uint32_t)(s0[4 * m + 2]), (uint32_t)((s0[4 * m + 2]) >> 32), q, P.qinv), q),
+                                    sub_if(mont_reduce64s((uint32_t)(s0[4 * m + 3]), (uint32_t)((s0[4 * m + 3]) >> 32), q, P.qinv), q)));
+        stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64s((uint32_t)(s1[4 * m]), (uint32_t)((s1[4 * m]) >> 32), q, P.qinv), q),
+                                    sub_if(mont_reduce64s((uint32_t)(s1[4 * m + 1]), (uint32_t)((s1[4 * m + 1]) >> 32), q, P.qinv), q),
+                                    sub_if(mont_reduce64s((uint32_t)(s1[4 * m + 2]), (uint32_t)((s1[4 * m + 2]) >> 32), q, P.qinv), q),
+                                    sub_if(mont_reduce64s((uint32_t)(s1[4 * m + 3]), (uint32_t)((s1[4 * m + 3]) >> 32), q, P.qinv), q)));
       }
     }
     if (++b == B) {
