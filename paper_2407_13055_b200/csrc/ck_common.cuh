@@ -50,12 +50,12 @@ __device__ __forceinline__ uint32_t sub_if(uint32_t x, uint32_t m) { return min(
 __device__ __forceinline__ uint32_t canon4(uint32_t x, uint32_t q, uint32_t q2) {
   return sub_if(sub_if(x, q2), q);  // [0, 4q) -> [0, q)
 }
-// unsigned Montgomery a*b*2^-32 for a*b < q*2^32 -> [0, 2q)
-__device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t b, uint32_t q, uint32_t qinv_neg) {
+// unsigned Montgomery a*b*2^-32 for a*b < q*2^32 -> (0, 2q), subtractive
+// form (qinv = q^-1 mod 2^32; see mont_reduce64s)
+__device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t b, uint32_t q, uint32_t qinv) {
   const uint32_t lo = a * b;
   const uint32_t hi = __umulhi(a, b);
-  const uint32_t m = lo * qinv_neg;
-  return hi + __umulhi(m, q) + (lo != 0u);
+  return hi - __umulhi(lo * qinv, q) + q;
 }
 // acc + a*b with a, b < 2^32: one IMAD.WIDE.U32 (the compiler otherwise
 // sometimes widens a register-promoted operand and emits a 64x32 multiply)
@@ -71,12 +71,10 @@ __device__ __forceinline__ uint64_t mac_wide(uint64_t acc, uint32_t a, uint32_t 
 __device__ __forceinline__ uint32_t mont_reduce64s(uint32_t lo, uint32_t hi, uint32_t q, uint32_t qinv) {
   return hi - __umulhi(lo * qinv, q) + q;
 }
-// Montgomery reduction of a 64-bit accumulator t < q*2^32 -> [0, 2q)
-__device__ __forceinline__ uint32_t mont_reduce64(uint64_t t, uint32_t q, uint32_t qinv_neg) {
-  const uint32_t lo = static_cast<uint32_t>(t);
-  const uint32_t hi = static_cast<uint32_t>(t >> 32);
-  const uint32_t m = lo * qinv_neg;
-  return hi + __umulhi(m, q) + (lo != 0u);
+// Montgomery reduction of a 64-bit accumulator t < q*2^32 -> (0, 2q)
+// (subtractive form, qinv = q^-1 mod 2^32)
+__device__ __forceinline__ uint32_t mont_reduce64(uint64_t t, uint32_t q, uint32_t qinv) {
+  return mont_reduce64s(static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32), q, qinv);
 }
 
 }  // namespace ck

@@ -31,7 +31,7 @@ __device__ __forceinline__ uint32_t getc(const uint4& v, int k) {
 template <int SC>
 __global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
   __shared__ uint32_t cm[kMaxRows * SC];
-  __shared__ uint4 rc[kMaxRows];  // {q, qinv_neg, dst row, 0}
+  __shared__ uint4 rc[kMaxRows];  // {q, qinv, dst row, 0}
   const BconvGroup G = a.groups[blockIdx.y];
   for (int e = threadIdx.x; e < G.dc * SC; e += kT) {
     const int i = e / SC, j = e % SC;
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kT) k_bconv(BconvLaunch a, int n) {
   }
   for (int i = threadIdx.x; i < (int)G.dc; i += kT) {
     const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
-    rc[i] = make_uint4(P.q, P.qinv_neg, a.dst_row[G.map_off + i], 0);
+    rc[i] = make_uint4(P.q, P.qinv, a.dst_row[G.map_off + i], 0);
   }
   __syncthreads();
   const int x = (blockIdx.x * kT + threadIdx.x) * 4;
@@ -104,7 +104,7 @@ template <int SC, int MODE>
 __global__ void __launch_bounds__(kTD) k_bconv_df(BconvLaunch a, int n) {
   __shared__ uint32_t cm[kMaxRows * SC];
   __shared__ double2 cd[kMaxRows * SC];
-  __shared__ uint4 rc[kMaxRows];  // {q, qinv_neg, dst row, 0}
+  __shared__ uint4 rc[kMaxRows];  // {q, qinv, dst row, 0}
   const BconvGroup G = a.groups[blockIdx.y];
   for (int e = threadIdx.x; e < G.dc * SC; e += kTD) {
     const int i = e / SC, j = e % SC;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kTD) k_bconv_df(BconvLaunch a, int n) {
   }
   for (int i = threadIdx.x; i < (int)G.dc; i += kTD) {
     const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
-    rc[i] = make_uint4(P.q, P.qinv_neg, a.dst_row[G.map_off + i], 0);
+    rc[i] = make_uint4(P.q, P.qinv, a.dst_row[G.map_off + i], 0);
   }
   __syncthreads();
   const int x = (blockIdx.x * kTD + threadIdx.x) * 2;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kTW) k_bconv_ws(BconvLaunch a, int n) {
   }
   for (int i = threadIdx.x; i < (int)G.dc; i += kTW) {
     const PrimeDev P = a.primes[a.dst_prime[G.map_off + i]];
-    rc[i] = make_uint4(P.q, P.qinv_neg, a.dst_row[G.map_off + i], 0);
+    rc[i] = make_uint4(P.q, P.qinv, a.dst_row[G.map_off + i], 0);
   }
   __syncthreads();
   const bool fpw = threadIdx.x >= kTW / 2;
@@ -314,9 +314,9 @@ __global__ void __launch_bounds__(kT) k_tensor(int n, int level, const uint32_t*
 #define CK_T(c)                                                                              \
   {                                                                                          \
     const uint32_t bb = xb.c, ba = xa.c, cb = yb.c, ca = ya.c;                               \
-    o0.c = sub_if(mont_mul(bb, cb, P.q, P.qinv_neg), P.q);                                   \
-    o1.c = sub_if(mont_reduce64(mac_wide(mac_wide(0ull, bb, ca), ba, cb), P.q, P.qinv_neg), P.q); \
-    o2.c = sub_if(mont_mul(ba, ca, P.q, P.qinv_neg), P.q);                                   \
+    o0.c = sub_if(mont_mul(bb, cb, P.q, P.qinv), P.q);                                   \
+    o1.c = sub_if(mont_reduce64(mac_wide(mac_wide(0ull, bb, ca), ba, cb), P.q, P.qinv), P.q); \
+    o2.c = sub_if(mont_mul(ba, ca, P.q, P.qinv), P.q);                                   \
   }
   CK_T(x) CK_T(y) CK_T(z) CK_T(w)
 #undef CK_T
@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(kT) k_key_mult(KeyMultLaunch a, int n) {
   auto renorm = [&]() {  // keep the int64 sums below q*2^32 (acc value unchanged mod q, scaled back by R)
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      s0[c] = shoup_mul(mont_reduce64(s0[c], P.q, P.qinv_neg), P.r, P.r_sh, P.q);
-      s1[c] = shoup_mul(mont_reduce64(s1[c], P.q, P.qinv_neg), P.r, P.r_sh, P.q);
+      s0[c] = shoup_mul(mont_reduce64(s0[c], P.q, P.qinv), P.r, P.r_sh, P.q);
+      s1[c] = shoup_mul(mont_reduce64(s1[c], P.q, P.qinv), P.r, P.r_sh, P.q);
     }
   };
   for (int k = 0; k < a.D; ++k) {
@@ -372,14 +372,14 @@ __global__ void __launch_bounds__(kT) k_key_mult(KeyMultLaunch a, int n) {
     }
   }
   uint4 r0, r1;
-  r0.x = sub_if(mont_reduce64(s0[0], P.q, P.qinv_neg), P.q);
-  r0.y = sub_if(mont_reduce64(s0[1], P.q, P.qinv_neg), P.q);
-  r0.z = sub_if(mont_reduce64(s0[2], P.q, P.qinv_neg), P.q);
-  r0.w = sub_if(mont_reduce64(s0[3], P.q, P.qinv_neg), P.q);
-  r1.x = sub_if(mont_reduce64(s1[0], P.q, P.qinv_neg), P.q);
-  r1.y = sub_if(mont_reduce64(s1[1], P.q, P.qinv_neg), P.q);
-  r1.z = sub_if(mont_reduce64(s1[2], P.q, P.qinv_neg), P.q);
-  r1.w = sub_if(mont_reduce64(s1[3], P.q, P.qinv_neg), P.q);
+  r0.x = sub_if(mont_reduce64(s0[0], P.q, P.qinv), P.q);
+  r0.y = sub_if(mont_reduce64(s0[1], P.q, P.qinv), P.q);
+  r0.z = sub_if(mont_reduce64(s0[2], P.q, P.qinv), P.q);
+  r0.w = sub_if(mont_reduce64(s0[3], P.q, P.qinv), P.q);
+  r1.x = sub_if(mont_reduce64(s1[0], P.q, P.qinv), P.q);
+  r1.y = sub_if(mont_reduce64(s1[1], P.q, P.qinv), P.q);
+  r1.z = sub_if(mont_reduce64(s1[2], P.q, P.qinv), P.q);
+  r1.w = sub_if(mont_reduce64(s1[3], P.q, P.qinv), P.q);
   st4(a.v + b * a.v_bs + (size_t)i * n + xo, r0);
   st4(a.v + b * a.v_bs + (size_t)(rows + i) * n + xo, r1);
 }
@@ -399,10 +399,10 @@ __global__ void __launch_bounds__(kT) k_combine(int n, const uint32_t* __restric
   uint32_t* op = o + b * o_bs + p * o_ps + (size_t)i * n + xo;
   const uint4 vv = ld4(vp), ov = ld4(op);
   uint4 r;
-  r.x = sub_if(mont_mul(vv.x - ov.x + P.q, di, P.q, P.qinv_neg), P.q);
-  r.y = sub_if(mont_mul(vv.y - ov.y + P.q, di, P.q, P.qinv_neg), P.q);
-  r.z = sub_if(mont_mul(vv.z - ov.z + P.q, di, P.q, P.qinv_neg), P.q);
-  r.w = sub_if(mont_mul(vv.w - ov.w + P.q, di, P.q, P.qinv_neg), P.q);
+  r.x = sub_if(mont_mul(vv.x - ov.x + P.q, di, P.q, P.qinv), P.q);
+  r.y = sub_if(mont_mul(vv.y - ov.y + P.q, di, P.q, P.qinv), P.q);
+  r.z = sub_if(mont_mul(vv.z - ov.z + P.q, di, P.q, P.qinv), P.q);
+  r.w = sub_if(mont_mul(vv.w - ov.w + P.q, di, P.q, P.qinv), P.q);
   st4(op, r);
 }
 
@@ -422,9 +422,9 @@ __global__ void __launch_bounds__(kT) k_hrot_tail(int n, int level, const uint32
   const size_t r = (size_t)i * n + s;
   const uint32_t* vb = v + b * v_bs;
   const uint32_t* ob = o + b * o_bs;
-  uint32_t c0 = sub_if(mont_mul(vb[r] - ob[r] + P.q, di, P.q, P.qinv_neg), P.q);
+  uint32_t c0 = sub_if(mont_mul(vb[r] - ob[r] + P.q, di, P.q, P.qinv), P.q);
   c0 = sub_if(c0 + bb[b * b_bs + r], P.q);
-  const uint32_t c1 = sub_if(mont_mul(vb[v_ps + r] - ob[o_ps + r] + P.q, di, P.q, P.qinv_neg), P.q);
+  const uint32_t c1 = sub_if(mont_mul(vb[v_ps + r] - ob[o_ps + r] + P.q, di, P.q, P.qinv), P.q);
   out[b * out_bs + (size_t)i * n + j] = c0;
   out[b * out_bs + (size_t)(level + i) * n + j] = c1;
 }
@@ -448,8 +448,8 @@ __global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_
   uint4 z;
   if (op == 3) {
     const uint32_t c = rc[i];
-    z = make_uint4(sub_if(mont_mul(x.x, c, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.y, c, P.q, P.qinv_neg), P.q),
-                   sub_if(mont_mul(x.z, c, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.w, c, P.q, P.qinv_neg), P.q));
+    z = make_uint4(sub_if(mont_mul(x.x, c, P.q, P.qinv), P.q), sub_if(mont_mul(x.y, c, P.q, P.qinv), P.q),
+                   sub_if(mont_mul(x.z, c, P.q, P.qinv), P.q), sub_if(mont_mul(x.w, c, P.q, P.qinv), P.q));
     *reinterpret_cast<uint4*>(o + b * o_bs + r) = z;
     return;
   }
@@ -460,8 +460,8 @@ __global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_
     z = make_uint4(sub_if(x.x - y.x + P.q, P.q), sub_if(x.y - y.y + P.q, P.q), sub_if(x.z - y.z + P.q, P.q),
                    sub_if(x.w - y.w + P.q, P.q));
   } else {
-    z = make_uint4(sub_if(mont_mul(x.x, y.x, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.y, y.y, P.q, P.qinv_neg), P.q),
-                   sub_if(mont_mul(x.z, y.z, P.q, P.qinv_neg), P.q), sub_if(mont_mul(x.w, y.w, P.q, P.qinv_neg), P.q));
+    z = make_uint4(sub_if(mont_mul(x.x, y.x, P.q, P.qinv), P.q), sub_if(mont_mul(x.y, y.y, P.q, P.qinv), P.q),
+                   sub_if(mont_mul(x.z, y.z, P.q, P.qinv), P.q), sub_if(mont_mul(x.w, y.w, P.q, P.qinv), P.q));
   }
   *reinterpret_cast<uint4*>(o + b * o_bs + r) = z;
 }
@@ -521,14 +521,14 @@ __global__ void __launch_bounds__(kT) k_crypt(int n, int level, int op, const ui
   const size_t r = (size_t)i * n + k;
   if (op == 0) {  // x = ct [2][level], y = s
     const uint32_t cb = x[b * x_bs + r], ca = x[b * x_bs + (size_t)level * n + r];
-    out[b * out_bs + r] = sub_if(cb + sub_if(mont_mul(ca, y[r], q, P.qinv_neg), q), q);
+    out[b * out_bs + r] = sub_if(cb + sub_if(mont_mul(ca, y[r], q, P.qinv), q), q);
   } else if (op == 1) {  // x = m, y = a, z = e, w = s
-    const uint32_t as = sub_if(mont_mul(y[r], w[r], q, P.qinv_neg), q);
+    const uint32_t as = sub_if(mont_mul(y[r], w[r], q, P.qinv), q);
     out[r] = sub_if(sub_if(x[r] + z[r], q) + q - as, q);
     out[(size_t)level * n + r] = y[r];
   } else {  // x = m, y = v, z = e0, w = e1, u = pk [2][level] (b then a)
-    const uint32_t vb = sub_if(mont_mul(y[r], u[r], q, P.qinv_neg), q);
-    const uint32_t va = sub_if(mont_mul(y[r], u[(size_t)level * n + r], q, P.qinv_neg), q);
+    const uint32_t vb = sub_if(mont_mul(y[r], u[r], q, P.qinv), q);
+    const uint32_t va = sub_if(mont_mul(y[r], u[(size_t)level * n + r], q, P.qinv), q);
     out[r] = sub_if(sub_if(vb + z[r], q) + x[r], q);
     out[(size_t)level * n + r] = sub_if(va + w[r], q);
   }
@@ -548,9 +548,9 @@ __global__ void __launch_bounds__(kT) k_evk_digit(int n, const uint32_t* __restr
   const uint32_t q = P.q;
   const size_t r = (size_t)i * n + k;
   uint32_t src = s_src[r];
-  if (square) src = sub_if(mont_mul(src, src, q, P.qinv_neg), q);
-  const uint32_t sg = sub_if(mont_mul(src, gm[i], q, P.qinv_neg), q);
-  const uint32_t as = sub_if(mont_mul(a[r], s_dst[r], q, P.qinv_neg), q);
+  if (square) src = sub_if(mont_mul(src, src, q, P.qinv), q);
+  const uint32_t sg = sub_if(mont_mul(src, gm[i], q, P.qinv), q);
+  const uint32_t as = sub_if(mont_mul(a[r], s_dst[r], q, P.qinv), q);
   out[r] = sub_if(sub_if(e[r] + sg, q) + q - as, q);
 }
 
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(kT) k_addmul(int n, uint32_t* __restrict__ acc
   const uint32_t xs = x[b * x_bs + r + (src ? __ldg(&src[j]) : (uint32_t)j)];
   const uint32_t ys = y[b * y_bs + r + j];
   uint32_t* a = acc + b * acc_bs + r + j;
-  *a = sub_if(sub_if(*a + mont_mul(xs, ys, P.q, P.qinv_neg), P.q2), P.q);
+  *a = sub_if(sub_if(*a + mont_mul(xs, ys, P.q, P.qinv), P.q2), P.q);
 }
 
 inline unsigned cdiv(unsigned a, unsigned b) { return (a + b - 1) / b; }

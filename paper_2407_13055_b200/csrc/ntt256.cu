@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
         const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + xo;
         const uint32_t* br = cb.add + b * cb.add_bs + (size_t)i * kN + xo;
         uint32_t* orow_t = cb.out + b * cb.out_bs + ((size_t)pi * cb.out_q + i) * kN;
-        const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv_neg;
+        const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const uint4 vv = *reinterpret_cast<const uint4*>(vr + 4 * m);
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
       } else if (COMB) {  // J.dst_off = p * out_q + i; v row p * prow + i; prime i
         const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
         const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + (size_t)r * kR + 16 * tau;
-        const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv_neg;
+        const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const uint4 vv = COMB == 2 ? vvr[m] : *reinterpret_cast<const uint4*>(vr + 4 * m);
@@ -921,8 +921,8 @@ __global__ void __launch_bounds__(256, 1) k_conv_mid(ConvMidLaunch a) {
           a3 = mac_wide(a3, x.w, c[s]);
         }
       }
-      v[j] = make_uint4(mont_reduce64(a0, q, P.qinv_neg), mont_reduce64(a1, q, P.qinv_neg),
-                        mont_reduce64(a2, q, P.qinv_neg), mont_reduce64(a3, q, P.qinv_neg));  // [0, 2q)
+      v[j] = make_uint4(mont_reduce64(a0, q, P.qinv), mont_reduce64(a1, q, P.qinv),
+                        mont_reduce64(a2, q, P.qinv), mont_reduce64(a3, q, P.qinv));  // [0, 2q)
     }
     const uint2* tw = a.fwd_tw + (size_t)g * kN;
 #pragma unroll
@@ -1159,8 +1159,8 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
       if ((k % 6) == 5) {  // keep the sums below q 2^32 (value unchanged mod q, rescaled by R)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          s0[j] = shoup_mul(mont_reduce64(s0[j], q, P.qinv_neg), P.r, P.r_sh, q);
-          s1[j] = shoup_mul(mont_reduce64(s1[j], q, P.qinv_neg), P.r, P.r_sh, q);
+          s0[j] = shoup_mul(mont_reduce64(s0[j], q, P.qinv), P.r, P.r_sh, q);
+          s1[j] = shoup_mul(mont_reduce64(s1[j], q, P.qinv), P.r, P.r_sh, q);
         }
       }
     }
@@ -1186,14 +1186,14 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
     uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv_neg), q)));
-      stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv_neg), q)));
+      stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv), q)));
+      stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv), q)));
     }
   }
   cp_wait<0>();
@@ -1387,14 +1387,14 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult_pf(KeyMultLaunch a, c
     uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv_neg), q)));
-      stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv_neg), q),
-                                  sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv_neg), q)));
+      stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64(s0[4 * m], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 1], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 2], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s0[4 * m + 3], q, P.qinv), q)));
+      stg4(o1 + 4 * m, make_uint4(sub_if(mont_reduce64(s1[4 * m], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 1], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 2], q, P.qinv), q),
+                                  sub_if(mont_reduce64(s1[4 * m + 3], q, P.qinv), q)));
     }
   }
   cp_wait<0>();
@@ -1790,7 +1790,7 @@ __global__ void __launch_bounds__(128, 8) k_row8(NttLaunch a, CombineArgs cb) {
       q = P.q;
       q2 = P.q2;
       q4 = 2 * P.q2;
-      qinv = P.qinv_neg;
+      qinv = P.qinv;
       const uint2* F = a.tw + (size_t)J.prime * kN;
       if (!INV) {
         for (int e = lane; e < 255; e += 32) {

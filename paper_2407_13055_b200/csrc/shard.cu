@@ -35,8 +35,8 @@ __global__ void __launch_bounds__(kST) k_shard_key_mult(ShardKeyMultLaunch a, in
   auto renorm = [&]() {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      s0[c] = shoup_mul(mont_reduce64(s0[c], P.q, P.qinv_neg), P.r, P.r_sh, P.q);
-      s1[c] = shoup_mul(mont_reduce64(s1[c], P.q, P.qinv_neg), P.r, P.r_sh, P.q);
+      s0[c] = shoup_mul(mont_reduce64(s0[c], P.q, P.qinv), P.r, P.r_sh, P.q);
+      s1[c] = shoup_mul(mont_reduce64(s1[c], P.q, P.qinv), P.r, P.r_sh, P.q);
     }
   };
   for (int k = 0; k < a.D; ++k) {
@@ -66,14 +66,14 @@ __global__ void __launch_bounds__(kST) k_shard_key_mult(ShardKeyMultLaunch a, in
     }
   }
   uint4 r0, r1;
-  r0.x = sub_if(mont_reduce64(s0[0], P.q, P.qinv_neg), P.q);
-  r0.y = sub_if(mont_reduce64(s0[1], P.q, P.qinv_neg), P.q);
-  r0.z = sub_if(mont_reduce64(s0[2], P.q, P.qinv_neg), P.q);
-  r0.w = sub_if(mont_reduce64(s0[3], P.q, P.qinv_neg), P.q);
-  r1.x = sub_if(mont_reduce64(s1[0], P.q, P.qinv_neg), P.q);
-  r1.y = sub_if(mont_reduce64(s1[1], P.q, P.qinv_neg), P.q);
-  r1.z = sub_if(mont_reduce64(s1[2], P.q, P.qinv_neg), P.q);
-  r1.w = sub_if(mont_reduce64(s1[3], P.q, P.qinv_neg), P.q);
+  r0.x = sub_if(mont_reduce64(s0[0], P.q, P.qinv), P.q);
+  r0.y = sub_if(mont_reduce64(s0[1], P.q, P.qinv), P.q);
+  r0.z = sub_if(mont_reduce64(s0[2], P.q, P.qinv), P.q);
+  r0.w = sub_if(mont_reduce64(s0[3], P.q, P.qinv), P.q);
+  r1.x = sub_if(mont_reduce64(s1[0], P.q, P.qinv), P.q);
+  r1.y = sub_if(mont_reduce64(s1[1], P.q, P.qinv), P.q);
+  r1.z = sub_if(mont_reduce64(s1[2], P.q, P.qinv), P.q);
+  r1.w = sub_if(mont_reduce64(s1[3], P.q, P.qinv), P.q);
   if (a.err && *(volatile const uint32_t*)a.err) {  // a peer never arrived: poison, never silently wrong
     r0 = r1 = make_uint4(kPoison, kPoison, kPoison, kPoison);
   }
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kST) k_shard_tail(ShardTailLaunch a, int n) {
   const uint32_t s = a.src_map ? __ldg(&a.src_map[j]) : (uint32_t)j;
   const size_t e = (size_t)r * n + s;
   const uint32_t vv = a.v[(size_t)c * a.v_ps + e], oo = a.o[(size_t)c * a.o_ps + e];
-  uint32_t x = sub_if(mont_mul(vv - oo + P.q, a.dinv[r], P.q, P.qinv_neg), P.q);
+  uint32_t x = sub_if(mont_mul(vv - oo + P.q, a.dinv[r], P.q, P.qinv), P.q);
   if (a.add && (a.add_mask >> c & 1)) x = sub_if(x + a.add[(size_t)c * a.add_ps + e], P.q);
   if (a.err && *(volatile const uint32_t*)a.err) x = kPoison;  // peer exchange timed out
   a.out[(size_t)c * a.out_ps + (size_t)r * n + j] = x;
