@@ -387,6 +387,154 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
   cp_wait<0>();
 }
 
+// k_col_tma: the TMA column pass (k_col<.., TMA>) with its per-item
+// descriptors pipelined one item ahead.  In k_col the next item's RowJob is
+// loaded right before thread 0 issues its TMA (so warp 0 stalls on that
+// load in the middle of the item) and the item's PrimeDev / exit constants
+// are loaded after the tile wait (a dependent global load at every item
+// start: the R2UR / IMAD.HI long-scoreboard stalls of the source-level ncu
+// profile).  Here the next RowJob is requested at the top of the current
+// item, its PrimeDev / exit constants right after its TMA is issued, and
+// both are in registers when the item starts.  Same arithmetic, same smem.
+template <bool INV>
+__global__ void __launch_bounds__(kCT, 5) k_col_tma(const RowJob* __restrict__ jobs, uint64_t src_bs,
+                                                   uint32_t* __restrict__ dst, uint64_t dst_bs, int batch, int njobs,
+                                                   const PrimeDev* __restrict__ primes,
+                                                   const uint2* __restrict__ tw_full,
+                                                   const ExitConst* __restrict__ exits, int entry,
+                                                   const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint4* tileb = reinterpret_cast<uint4*>(smraw);                              // [256][8] uint4, 32 KB
+  uint2* twring = reinterpret_cast<uint2*>(smraw + sizeof(ColBuf::tile));     // [2][256]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(twring + 512);
+  const int tid = threadIdx.x, cq = tid & 7, tau = tid >> 3;
+  constexpr int NT = kN;
+  const int items = njobs * batch * kCTiles;
+  int it = blockIdx.x;
+  if (it >= items) return;
+  if (tid == 0) mbar_init1(mbar);
+  __syncthreads();
+  auto issue = [&](int b, int tile, const RowJob& J, int k) {  // thread 0: item's tile + twiddles -> smem
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    const uint64_t word = INV ? b * dst_bs + (uint64_t)J.dst_off * NT : b * src_bs + (uint64_t)J.src_off * NT;
+    mbar_expect_tx(mbar, (uint32_t)sizeof(ColBuf::tile) + 256 * 8);
+    tma_tile(tileb, &tmap, tile * kCCols, (int)(word / kR), mbar);
+    bulk_copy(&twring[(k & 1) * 256], tw_full + (size_t)J.prime * NT, 256 * 8, mbar);
+  };
+  int b, tile, job;
+  col_item<kCTiles>(it, batch, job, b, tile);
+  RowJob J = jobs[job];
+  PrimeDev P = primes[J.prime];
+  ExitConst ex{};
+  if (INV) ex = exits[J.epi];
+  if (tid == 0) issue(b, tile, J, 0);
+  for (int k = 0;; ++k) {
+    const int nxt = it + gridDim.x;
+    const bool more = nxt < items;
+    int nb = 0, ntile = 0, njob = 0;
+    RowJob nJ{};
+    if (more) {  // next item's descriptor: requested now, used after phase A
+      col_item<kCTiles>(nxt, batch, njob, nb, ntile);
+      nJ = jobs[njob];
+    }
+    mbar_wait_parity(mbar, k & 1);  // item k's tile and twiddles have landed
+    const uint32_t q = P.q, q2 = P.q2, q4 = 2 * P.q2;
+    const uint2* TW = twring + (k & 1) * 256;
+    uint32_t* out = dst + b * dst_bs + (size_t)J.dst_off * NT + tile * kCCols + 4 * cq;
+    uint4 v[16];
+    PrimeDev nP{};
+    ExitConst nex{};
+    if (!INV) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = tileb[(tau + 16 * j) * 8 + cq];
+      if (entry) {  // stage 0 with the entry merge x*R, y*psi^{N/2}*R (ntt.cpp:27-35)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+#define CK_E(c)                                                    \
+  {                                                                \
+    const uint32_t xx = shoup_mul(v[j].c, P.r, P.r_sh, q);         \
+    const uint32_t tt = shoup_mul(v[j + 8].c, P.w1r, P.w1r_sh, q); \
+    v[j].c = xx + tt;                                              \
+    v[j + 8].c = xx - tt + q2;                                     \
+  }
+          CK_E(x) CK_E(y) CK_E(z) CK_E(w)
+#undef CK_E
+        }
+        ct_stages16<1, 0x4>(v, [&](int t, int blk) { return TW[(1 << t) + blk]; }, q, q2, q4);
+      } else {
+        ct_stages16<0, 0x4>(v, [&](int t, int blk) { return TW[(1 << t) + blk]; }, q, q2, q4);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tileb[(tau + 16 * j) * 8 + cq] = v[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = tileb[(16 * tau + j) * 8 + cq];
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();
+      if (more) {
+        if (tid == 0) issue(nb, ntile, nJ, k + 1);
+        nP = primes[nJ.prime];
+      }
+      ct_stages16<0, 0x5>(v, [&](int t, int blk) { return TW[(16 << t) + (tau << t) + blk]; }, q, q2, q4);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) stg4(out + (16 * tau + j) * kR, v[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = tileb[(16 * tau + j) * 8 + cq];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int d = 1 << t;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          gs4(v[j], v[j + d], TW[(128 >> t) + (tau << (3 - t)) + blk], q, q2);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tileb[(16 * tau + j) * 8 + cq] = v[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = tileb[(tau + 16 * j) * 8 + cq];
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();
+      if (more) {
+        if (tid == 0) issue(nb, ntile, nJ, k + 1);
+        nP = primes[nJ.prime];
+        nex = exits[nJ.epi];
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int d = 1 << t;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int blk = p / d, j = blk * 2 * d + p % d;
+          gs4(v[j], v[j + d], TW[(8 >> t) + blk], q, q2);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // exit merge (ntt.cpp:76-84)
+#define CK_X(c)                                                            \
+  {                                                                        \
+    const uint32_t u = v[j].c + v[j + 8].c, dd = v[j].c - v[j + 8].c + q2; \
+    v[j].c = sub_if(shoup_mul(u, ex.x, ex.y, q), q);                       \
+    v[j + 8].c = sub_if(shoup_mul(dd, ex.z, ex.w, q), q);                  \
+  }
+        CK_X(x) CK_X(y) CK_X(z) CK_X(w)
+#undef CK_X
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) stg4(out + (tau + 16 * j) * kR, v[j]);
+    }
+    if (!more) break;
+    it = nxt;
+    b = nb;
+    tile = ntile;
+    J = nJ;
+    P = nP;
+    ex = nex;
+  }
+}
+
 // =============================================================== row pass ==
 // 8 rows per tile, 16 threads (half a warp) per row.  The tile's per-row
 // permuted twiddle tables (256 pairs per row) are staged in shared memory
@@ -732,7 +880,12 @@ void init_grids() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(k_col<false, false, true, 5, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
   cudaFuncSetAttribute(k_col<true, false, true, 5, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
-  if (g_col_var == 3) {
+  cudaFuncSetAttribute(k_col_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
+  cudaFuncSetAttribute(k_col_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
+  if (g_col_var == 4) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col_tma<false>, kCT, kColTmaSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col_tma<true>, kCT, kColTmaSmem);
+  } else if (g_col_var == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, false, true, 5, 8, true>, kCT, kColTmaSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, false, true, 5, 8, true>, kCT, kColTmaSmem);
   } else if (g_col_var == 1 || g_col_var == 2) {
@@ -793,6 +946,12 @@ template <bool INV>
 void launch_col(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaStream_t st) {
   const int items = a.njobs * a.batch * kCTiles;
   const int grid = min(g_col_grid[INV], items);
+  if (g_col_var == 4) {  // TMA staging, descriptors one item ahead (k_col_tma)
+    const CUtensorMap& m = col_tensor_map(INV ? a.dst : src);
+    k_col_tma<INV><<<grid, kCT, kColTmaSmem, st>>>(a.jobs, src_bs, a.dst, a.dst_bs, a.batch, a.njobs, a.primes, a.tw,
+                                                   a.exits, a.entry, m);
+    return;
+  }
   if (g_col_var == 3) {  // TMA staging (the tile source is dst for the inverse pass, as in prefetch)
     const CUtensorMap& m = col_tensor_map(INV ? a.dst : src);
     k_col<INV, false, true, 5, 8, true><<<grid, kCT, kColTmaSmem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch,
@@ -1487,12 +1646,20 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
           const int c = 4 * (lane + 32 * m);
           cp16(line + pad8(c), gsrc + c);
         }
+      } else if (KPF == 4) {  // the digit's own row (ModUp pass-through) into its otherwise unused buffer
+        const uint32_t* gsrc = a.d + b * a.d_bs + (size_t)i * kN + (size_t)r * kR;
+        uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int c = 4 * (lane + 32 * m);
+          cp16(line + pad8(c), gsrc + c);
+        }
       }
       cp_commit();
     }
     const size_t rofs = (size_t)r * kR + 8 * lane;  // this thread's 8 coefficients after the transform
     if (i < a.level && (lane & 3) == 0) {  // own-digit and fold rows into L2 now (plain loads later), 1 per line
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.d + b * a.d_bs + (size_t)i * kN + rofs));
+      if (KPF != 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.d + b * a.d_bs + (size_t)i * kN + rofs));
       if (a.fold) {
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fold + b * a.fold_bs + (size_t)i * kN + rofs));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + rofs));
@@ -1523,7 +1690,17 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         }
       }
       uint32_t v[8];
-      if (i >= lo && i < hi) {  // the digit's own row (ModUp pass-through), evaluation form already
+      if (KPF == 4 && i >= lo && i < hi) {  // own row, staged by cp.async at the item start
+        if (a.D >= 3) cp_wait<2>();
+        else if (a.D == 2) cp_wait<1>();
+        else cp_wait<0>();
+        __syncwarp();
+        const uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
+        const uint4 x0 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane));
+        const uint4 x1 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane + 4));
+        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+      } else if (i >= lo && i < hi) {  // the digit's own row (ModUp pass-through), evaluation form already
         if (KPF == 3 && k == 0) {  // no extension wait precedes this digit: wait for the key group here
           if (a.D >= 3) cp_wait<2>();
           else if (a.D == 2) cp_wait<1>();
@@ -1535,7 +1712,8 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
         v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
       } else {
-        const int pend = a.D - 1 - k;
+        // KPF 4: one post group per finished digit keeps D - 1 groups younger than this digit's
+        const int pend = KPF == 4 ? a.D - 1 : a.D - 1 - k;
         if (pend >= 2) cp_wait<2>();
         else if (pend == 1) cp_wait<1>();
         else cp_wait<0>();
@@ -1620,6 +1798,19 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         s1[4 * m + 2] = mac_wide(s1[4 * m + 2], v[4 * m + 2], ka[m].z);
         s1[4 * m + 3] = mac_wide(s1[4 * m + 3], v[4 * m + 3], ka[m].w);
       }
+      if (KPF == 4) {  // this digit's buffer is free: the fold row k (digits 0, 1 of a 3-digit key) into it
+        if (a.fold && i < a.level && k < 2 && a.D == 3) {
+          __syncwarp();
+          const uint32_t* gsrc = a.fold + b * a.fold_bs + (size_t)(k * a.level + i) * kN + (size_t)r * kR;
+          uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            const int c = 4 * (lane + 32 * m);
+            cp16(line + pad8(c), gsrc + c);
+          }
+        }
+        cp_commit();
+      }
       if ((k % 6) == 5) {  // keep the sums below q 2^32 (value unchanged mod q, rescaled by R)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -1632,6 +1823,13 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       const uint32_t pm = a.p_mont[i];
       const uint32_t* f0 = a.fold + b * a.fold_bs + (size_t)i * kN + rofs;
       const uint32_t* f1 = a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + rofs;
+      const bool staged = KPF == 4 && a.D == 3;
+      if (staged) {  // fold rows staged in digit buffers 0 / 1
+        cp_wait<0>();
+        __syncwarp();
+        f0 = sbuf + warp * kK8Stride + pad8(8 * lane);
+        f1 = sbuf + (kK8Rows + warp) * kK8Stride + pad8(8 * lane);
+      }
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const uint4 x0 = *reinterpret_cast<const uint4*>(f0 + 4 * m);
@@ -1723,6 +1921,220 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       b = 0;
       if (++tile == kTiles) {
         tile = 0;
+        ++i;
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+// k_row_keymult8b: k_row_keymult8 with the CTA's 4 warps on the SAME row r
+// of limb i for 4 consecutive batch items (warp w: b = 4 bg + w) instead of
+// 4 rows of one item.  The row's 255 forward twiddles and its key slice
+// (D digits x 2 halves x 256 words) are then shared by the warps: staged in
+// shared memory once per (i, r) -- the key with cp.async together with the
+// item's extension rows -- and read from shared memory after each digit's
+// row pass.  k_row_keymult8 loads the key halves from L2 right before the
+// MACs (64 registers leave no room to load them earlier), and that load is
+// the kernel's top stall (13% of the samples, long scoreboard, on the first
+// IMAD.WIDE of each digit); here the key crosses L2 once per 4 batch items.
+// Items (i, r, bg), bg fastest.  D <= 3; no fused INTT pass A.
+constexpr int kK8bSmem = (3 * kK8Rows * kK8Stride) * 4 + 258 * 8 + 3 * 2 * 256 * 4;
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_row_keymult8b(KeyMultLaunch a, const uint2* __restrict__ fwd) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);                         // [3][4][288] per-warp ext rows
+  // [255] row twiddles (shared), one entry past a 16-B boundary so that the
+  // 16-B cp.async chunks (odd indices 2^s - 1 + 2c) are aligned
+  uint2* T = reinterpret_cast<uint2*>(smraw + 3 * kK8Rows * kK8Stride * 4) + 1;
+  uint32_t* Ks = reinterpret_cast<uint32_t*>(T + 257);                        // [3][2][256] key slice (shared)
+  const int rows = a.level + a.alpha, B = a.batch, BG = (B + 3) >> 2;
+  const uint32_t LA = (uint32_t)(a.L + a.alpha);
+  const int items = rows * kR * BG;  // (row i, r, bg), bg fastest
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(items, i0 + chunk);
+  const int lhi = lane >> 2, llo = lane & 3;
+  if (i0 >= i1) return;
+  int bg = i0 % BG, r = (i0 / BG) % kR, i = (i0 / BG) / kR;
+  int g = 0;
+  PrimeDev P{};
+  uint32_t q = 0, q2 = 0, q4 = 0;
+  for (int it = i0; it < i1; ++it) {
+    const bool reload = it == i0 || bg == 0;
+    const int b = 4 * bg + warp;
+    const bool active = b < B;
+    if (reload) {  // new (i, r): prime, the row's twiddles and key slice
+      __syncthreads();  // every warp is done with the previous (i, r)'s T and Ks
+      g = i < a.level ? i : a.L + (i - a.level);
+      P = a.primes[g];
+      q = P.q;
+      q2 = P.q2;
+      q4 = 2 * P.q2;
+      // the row's twiddles T[2^s - 1 + blk] = F[(256 << s) + (r << s) + blk]:
+      // stage s >= 1 is 2^(s-1) aligned 16-B chunks, stage 0 one 8-B pair
+      const uint2* F = fwd + (size_t)g * kN;
+      if (tid < 127) {
+        const int sg = 32 - __clz(tid + 1), c = tid + 1 - (1 << (sg - 1));  // stage 1..7, chunk c
+        cp16(&T[(1 << sg) - 1 + 2 * c], &F[(256 << sg) + (r << sg) + 2 * c]);
+      } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&T[0]))),
+                     "l"(&F[256 + r])
+                     : "memory");
+      }
+      for (int e = tid; e < a.D * 2 * 64; e += 128) {  // D x 2 rows of 64 x 16 B
+        const int kh = e >> 6, c = 4 * (e & 63);
+        cp16(Ks + kh * 256 + c, a.evk + ((size_t)kh * LA + g) * kN + (size_t)r * kR + c);
+      }
+    }
+    cp_commit();  // the key group (empty unless reload): older than the extension groups
+    for (int k = 0; k < a.D; ++k) {
+      const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+      if (active && !(i >= lo && i < hi)) {
+        const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)r * kR;
+        uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int c = 4 * (lane + 32 * m);
+          cp16(line + pad8(c), gsrc + c);
+        }
+      }
+      cp_commit();
+    }
+    const size_t rofs = (size_t)r * kR + 8 * lane;
+    if (active && i < a.level && (lane & 3) == 0) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.d + b * a.d_bs + (size_t)i * kN + rofs));
+      if (a.fold) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fold + b * a.fold_bs + (size_t)i * kN + rofs));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + rofs));
+      }
+    }
+    if (reload) {  // the key group (oldest) has landed for every thread; T stores visible
+      if (a.D >= 3) cp_wait<3>();
+      else if (a.D == 2) cp_wait<2>();
+      else cp_wait<1>();
+      __syncthreads();
+    }
+    if (active) {
+      uint64_t s0[8], s1[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s0[j] = s1[j] = 0;
+      for (int k = 0; k < a.D; ++k) {
+        const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
+        uint32_t v[8];
+        if (i >= lo && i < hi) {  // the digit's own row (ModUp pass-through), evaluation form already
+          const uint32_t* dr = a.d + b * a.d_bs + (size_t)i * kN + rofs;
+          const uint4 x0 = *reinterpret_cast<const uint4*>(dr), x1 = *reinterpret_cast<const uint4*>(dr + 4);
+          v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+          v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+        } else {
+          const int pend = a.D - 1 - k;
+          if (pend >= 2) cp_wait<2>();
+          else if (pend == 1) cp_wait<1>();
+          else cp_wait<0>();
+          __syncwarp();
+          uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = line[pad8(lane + 32 * j)];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int d = 4 >> t;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const int blk = p / d, j = blk * 2 * d + p % d;
+              const uint2 w = T[(1 << t) - 1 + blk];
+              if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+              else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) line[pad8(lane + 32 * j)] = v[j];
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = line[pad8(32 * lhi + 4 * j + llo)];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int d = 4 >> t, sg = 3 + t;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const int blk = p / d, j = blk * 2 * d + p % d;
+              const uint2 w = T[(1 << sg) - 1 + (lhi << t) + blk];
+              if (sg % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+              else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) line[pad8(32 * lhi + 4 * j + llo)] = v[j];
+          __syncwarp();
+          {
+            const uint4 x0 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane));
+            const uint4 x1 = *reinterpret_cast<const uint4*>(line + pad8(8 * lane + 4));
+            v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+            v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+          }
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int d = 2 >> t, sg = 6 + t;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const int blk = p / d, j = blk * 2 * d + p % d;
+              const uint2 w = T[(1 << sg) - 1 + (lane << (t + 1)) + blk];
+              if (sg % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+              else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = canon8(v[j], q, q2, q4);
+        }
+        const uint4* kr = reinterpret_cast<const uint4*>(Ks + k * 512 + 8 * lane);
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const uint4 kb = kr[m], ka = kr[64 + m];  // halves 0 / 1 of digit k
+          s0[4 * m] = mac_wide(s0[4 * m], v[4 * m], kb.x);
+          s0[4 * m + 1] = mac_wide(s0[4 * m + 1], v[4 * m + 1], kb.y);
+          s0[4 * m + 2] = mac_wide(s0[4 * m + 2], v[4 * m + 2], kb.z);
+          s0[4 * m + 3] = mac_wide(s0[4 * m + 3], v[4 * m + 3], kb.w);
+          s1[4 * m] = mac_wide(s1[4 * m], v[4 * m], ka.x);
+          s1[4 * m + 1] = mac_wide(s1[4 * m + 1], v[4 * m + 1], ka.y);
+          s1[4 * m + 2] = mac_wide(s1[4 * m + 2], v[4 * m + 2], ka.z);
+          s1[4 * m + 3] = mac_wide(s1[4 * m + 3], v[4 * m + 3], ka.w);
+        }
+      }
+      if (a.fold && i < a.level) {  // merged HMult: v += P * d0 / d1 (ckks.cpp:831-842)
+        const uint32_t pm = a.p_mont[i];
+        const uint32_t* f0 = a.fold + b * a.fold_bs + (size_t)i * kN + rofs;
+        const uint32_t* f1 = a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + rofs;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const uint4 x0 = *reinterpret_cast<const uint4*>(f0 + 4 * m);
+          const uint4 x1 = *reinterpret_cast<const uint4*>(f1 + 4 * m);
+          s0[4 * m] = mac_wide(s0[4 * m], x0.x, pm);
+          s0[4 * m + 1] = mac_wide(s0[4 * m + 1], x0.y, pm);
+          s0[4 * m + 2] = mac_wide(s0[4 * m + 2], x0.z, pm);
+          s0[4 * m + 3] = mac_wide(s0[4 * m + 3], x0.w, pm);
+          s1[4 * m] = mac_wide(s1[4 * m], x1.x, pm);
+          s1[4 * m + 1] = mac_wide(s1[4 * m + 1], x1.y, pm);
+          s1[4 * m + 2] = mac_wide(s1[4 * m + 2], x1.z, pm);
+          s1[4 * m + 3] = mac_wide(s1[4 * m + 3], x1.w, pm);
+        }
+      }
+      uint32_t* o0 = a.v + b * a.v_bs + (size_t)i * kN + rofs;
+      uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+#define CK_R(s, j) sub_if(mont_reduce64s((uint32_t)(s[j]), (uint32_t)((s[j]) >> 32), q, P.qinv), q)
+        stg4(o0 + 4 * m, make_uint4(CK_R(s0, 4 * m), CK_R(s0, 4 * m + 1), CK_R(s0, 4 * m + 2), CK_R(s0, 4 * m + 3)));
+        stg4(o1 + 4 * m, make_uint4(CK_R(s1, 4 * m), CK_R(s1, 4 * m + 1), CK_R(s1, 4 * m + 2), CK_R(s1, 4 * m + 3)));
+#undef CK_R
+      }
+    } else {
+      cp_wait<0>();
+    }
+    __syncwarp();
+    if (++bg == BG) {
+      bg = 0;
+      if (++r == kR) {
+        r = 0;
         ++i;
       }
     }
@@ -2031,9 +2443,25 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, cons
     launch_km<true, 4, true, true, true>(a, tw2, items, st);
     return;
   }
-  if (ver >= 7 && ver <= 11 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
+  if (ver == 12 && a.D <= 3 && fwd_full && !a.ts && a.batch >= 4) {  // batch-shared key / twiddles
+    const int items8b = (a.level + a.alpha) * kR * ((a.batch + 3) / 4);
+    static int grid = 0;
+    if (!grid) {
+      cudaFuncSetAttribute(k_row_keymult8b<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK8bSmem);
+      int dev = 0, sms = 148, per = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8b<8>, 128, kK8bSmem);
+      grid = sms * std::max(1, per);
+    }
+    k_row_keymult8b<8><<<std::min(grid, items8b), 128, kK8bSmem, st>>>(a, fwd_full);
+    return;
+  }
+  if (ver >= 7 && ver <= 13 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
     const int items8 = (a.level + a.alpha) * (kR / kK8Rows) * a.batch;
-    if (ver == 11)
+    if (ver == 13 && !a.ts)
+      launch_km8<8, false, 4>(a, fwd_full, items8, st);  // own / fold rows through cp.async into freed digit buffers
+    else if (ver == 11)
       launch_km8<4, false, 3>(a, fwd_full, items8, st);  // key slice staged in shared memory per (row, tile), 4 CTAs / SM
     else if (ver == 9)
       launch_km8<8, false, 1>(a, fwd_full, items8, st);  // + the digit's key lines into L1 before its row pass

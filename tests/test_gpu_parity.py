@@ -366,6 +366,48 @@ def test_batched_equals_unbatched():
         np.testing.assert_array_equal(hr[b], one)
 
 
+@pytest.mark.parametrize("km", ["8", "12", "13"])
+@pytest.mark.parametrize("level,B", [(24, 6), (9, 8)])
+def test_batched_keymult_variants_equal_unbatched(km, level, B):
+    """The fused row pass + KeyMult variants at batch B >= 4 (CK32_KM=12:
+    k_row_keymult8b, four batch items per CTA sharing the row's key slice and
+    twiddles; B = 6 leaves two idle warps in the last item group): every
+    ciphertext of the batched HMult / HRot equals its B = 1 result, and the
+    first one equals the oracle (fresh subprocess: CK32_KM is read once)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = f'''
+import sys, numpy as np, torch
+sys.path[:0] = {[str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent.parent / "oracle")]!r}
+from fractions import Fraction
+from paper_2407_13055_b200 import ckks
+from pyoracle import Oracle, Rng
+n, l, a, db, level, B = 1 << 16, 24, 8, 55, {level}, {B}
+O = Oracle(n, l, a, db)
+dev = lambda v: torch.from_numpy(np.ascontiguousarray(v.astype(np.int32))).cuda()
+C = ckks.CkksContext(ckks.CkksParams(n=n, l=l, alpha=a, delta_bits=db))
+xs, ys = [], []
+for b in range(B):
+    xb, xa, yb, ya, evk = O.synthetic(level, 700 + b)
+    xs.append(np.stack([xb, xa])); ys.append(np.stack([yb, ya]))
+K = ckks.EvaluationKey(dev(evk)); KR = ckks.EvaluationKey(K.data, ckks.ROTATION, 1)
+ct = lambda v: ckks.Ciphertext(dev(v), Fraction(1 << db), level)
+hm = ckks.hmult(C, ct(np.stack(xs)), ct(np.stack(ys)), K).data.cpu().numpy().astype(np.uint32)
+hr = ckks.hrot(C, ct(np.stack(xs)), 1, KR).data.cpu().numpy().astype(np.uint32)
+for b in range(B):
+    assert np.array_equal(hm[b], ckks.hmult(C, ct(xs[b]), ct(ys[b]), K).data.cpu().numpy().astype(np.uint32)), b
+    assert np.array_equal(hr[b], ckks.hrot(C, ct(xs[b]), 1, KR).data.cpu().numpy().astype(np.uint32)), b
+ob, oa = O.hmult(level, xs[0][0], xs[0][1], ys[0][0], ys[0][1], evk)
+assert np.array_equal(hm[0], np.stack([O.canonical(ob, O.gidx(level - 2)), O.canonical(oa, O.gidx(level - 2))]))
+print("batched ok")
+'''
+    env = dict(__import__("os").environ, CK32_KM=km)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0 and "batched ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("chunk,depth", [(2, 2), (3, 3), (8, 2)])
 def test_host_pipeline_equals_direct(chunk, depth):
     """pipeline.HostPipeline (chunked H2D / compute / D2H on separate streams,
@@ -825,14 +867,17 @@ print("fused-intt ok")
 
 
 @pytest.mark.parametrize("level", [24, 7])
-@pytest.mark.parametrize("variant", ["CK32_ROW8=1", "CK32_KM=7", "CK32_KM=9", "CK32_KM=10", "CK32_KM=11", "CK32_TC=0"])
+@pytest.mark.parametrize("variant", ["CK32_ROW8=1", "CK32_KM=7", "CK32_KM=9", "CK32_KM=10", "CK32_KM=11", "CK32_TC=0",
+                                     "CK32_COL=3", "CK32_COL=4", "CK32_KM=12", "CK32_KM=13"])
 def test_variant_paths_match_oracle(level, variant):
     """Opt-in kernel variants (env switches read once per process: a fresh
     subprocess each) -- CK32_ROW8=1: the plain row passes as k_row8 (8
     coefficients per thread); CK32_KM=7/9/10/11: the fused row pass + KeyMult
     with the key ahead of the row pass / L1-prefetched / L1-prefetched one
     digit ahead / staged in shared memory per (row, tile); CK32_TC=0: BConv
-    on the CUDA cores (k_bconv) instead of tcgen05 -- NTT round trip, HMult (merged and lazy) and HRot equal the
+    on the CUDA cores (k_bconv) instead of tcgen05; CK32_COL=3/4: the TMA
+    column pass k_col / k_col_tma; CK32_KM=12: k_row_keymult8b (4 batch
+    items per CTA sharing the row's key slice and twiddles) -- NTT round trip, HMult (merged and lazy) and HRot equal the
     oracle."""
     import subprocess
     import sys
