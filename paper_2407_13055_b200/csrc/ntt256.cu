@@ -171,6 +171,58 @@ __device__ __forceinline__ void ct_stages16(uint4 (&v)[16], TWF tw, uint32_t q, 
   }
 }
 
+// One radix-2 stage over v[16] (8 butterflies, pairs at distance D, twiddle
+// index blk = p / D) with the multiplies issued in groups as in
+// ct_stages16: all IMAD.HI, then all q * hi, then the rest -- 8 independent
+// multiplies between dependent ones instead of 1 (the row passes otherwise
+// issue one Shoup multiply chain per butterfly and stall on its latency).
+// Forward CT on the lazy schedule (RED: x reduced from [0, 8q) first).
+template <int D, bool RED, class TWF>
+__device__ __forceinline__ void ct_stage8(uint32_t (&v)[16], TWF tw, uint32_t q, uint32_t q2, uint32_t q4) {
+  uint2 w[8];
+  uint32_t h[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) w[p] = tw(p / D);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int j = (p / D) * 2 * D + p % D;
+    h[p] = __umulhi(v[j + D], w[p].y);
+  }
+#pragma unroll
+  for (int p = 0; p < 8; ++p) h[p] *= q;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int j = (p / D) * 2 * D + p % D;
+    const uint32_t tt = v[j + D] * w[p].x - h[p];
+    const uint32_t xx = RED ? sub_if(v[j], q4) : v[j];
+    v[j] = xx + tt;
+    v[j + D] = xx - tt + q2;
+  }
+}
+// Inverse GS stage over v[16] (pairs at distance D), grouped the same way.
+template <int D, class TWF>
+__device__ __forceinline__ void gs_stage8(uint32_t (&v)[16], TWF tw, uint32_t q, uint32_t q2) {
+  uint2 w[8];
+  uint32_t dd[8], h[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) w[p] = tw(p / D);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int j = (p / D) * 2 * D + p % D;
+    dd[p] = v[j] - v[j + D] + q2;
+    v[j] = sub_if(v[j] + v[j + D], q2);
+  }
+#pragma unroll
+  for (int p = 0; p < 8; ++p) h[p] = __umulhi(dd[p], w[p].y);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) h[p] *= q;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int j = (p / D) * 2 * D + p % D;
+    v[j + D] = dd[p] * w[p].x - h[p];
+  }
+}
+
 // ============================================================ column pass ==
 constexpr int kCT = 128;              // threads: tau = tid>>3 (16), cq = tid&7 (8)
 constexpr int kCCols = 32;            // columns per tile
@@ -541,6 +593,10 @@ __global__ void __launch_bounds__(kCT, 5) k_col_tma(const RowJob* __restrict__ j
 // once per (job, row tile) and reused for every batch item; data tiles are
 // double-buffered with cp.async.
 constexpr int kRT = 128;
+#ifndef CK32_ROW_GROUPED
+#define CK32_ROW_GROUPED 0
+#endif
+constexpr bool kRowGrouped = CK32_ROW_GROUPED;  // k_row stages with grouped multiplies (ct_stage8 / gs_stage8): measured equal (r2ap), off
 constexpr int kRRows = kRT / 16;
 constexpr int kRowStride = 336;  // element c at c + 4*(c>>4): conflict-free for both access shapes
 __device__ __forceinline__ int rpos(int c) { return c + 4 * (c >> 4); }
@@ -705,15 +761,22 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
       // phase A: c = tau + 16 j, stages 8..11 (row-shared twiddles W[0..14])
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = line[rpos(tau + 16 * j)];
+      if (kRowGrouped) {
+        ct_stage8<8, true>(v, [&](int blk) { return W[blk]; }, q, q2, q4);
+        ct_stage8<4, false>(v, [&](int blk) { return W[1 + blk]; }, q, q2, q4);
+        ct_stage8<2, true>(v, [&](int blk) { return W[3 + blk]; }, q, q2, q4);
+        ct_stage8<1, false>(v, [&](int blk) { return W[7 + blk]; }, q, q2, q4);
+      } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int d = 8 >> t;
+        for (int t = 0; t < 4; ++t) {
+          const int d = 8 >> t;
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = W[(1 << t) - 1 + blk];
-          if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
-          else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = W[(1 << t) - 1 + blk];
+            if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          }
         }
       }
 #pragma unroll
@@ -728,15 +791,22 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
         v[4 * m + 3] = x.w;
       }
       // phase B: c = 16 tau + j, stages 12..15 (W[16 + k*16 + tau])
+      if (kRowGrouped) {
+        ct_stage8<8, true>(v, [&](int blk) { return twr[blk]; }, q, q2, q4);
+        ct_stage8<4, false>(v, [&](int blk) { return twr[1 + blk]; }, q, q2, q4);
+        ct_stage8<2, true>(v, [&](int blk) { return twr[3 + blk]; }, q, q2, q4);
+        ct_stage8<1, false>(v, [&](int blk) { return twr[7 + blk]; }, q, q2, q4);
+      } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int d = 8 >> t;
+        for (int t = 0; t < 4; ++t) {
+          const int d = 8 >> t;
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = twr[(1 << t) - 1 + blk];
-          if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
-          else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = twr[(1 << t) - 1 + blk];
+            if (t % 2 == 0) ctl<true>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+            else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
+          }
         }
       }
       if (COMB == 4) {
@@ -812,15 +882,22 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
         v[4 * m + 2] = x.z;
         v[4 * m + 3] = x.w;
       }
+      if (kRowGrouped) {
+        gs_stage8<1>(v, [&](int blk) { return twr[blk]; }, q, q2);
+        gs_stage8<2>(v, [&](int blk) { return twr[8 + blk]; }, q, q2);
+        gs_stage8<4>(v, [&](int blk) { return twr[12 + blk]; }, q, q2);
+        gs_stage8<8>(v, [&](int blk) { return twr[14 + blk]; }, q, q2);
+      } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int d = 1 << t;
-        const int off = 16 - (16 >> t);
+        for (int t = 0; t < 4; ++t) {
+          const int d = 1 << t;
+          const int off = 16 - (16 >> t);
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = twr[off + blk];
-          gs(v[j], v[j + d], w.x, w.y, q, q2);
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = twr[off + blk];
+            gs(v[j], v[j + d], w.x, w.y, q, q2);
+          }
         }
       }
 #pragma unroll
@@ -831,15 +908,22 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = line[rpos(tau + 16 * j)];
       // phase B: c = tau + 16 j, inverse stages 4..7 (row-shared W[240 + k])
+      if (kRowGrouped) {
+        gs_stage8<1>(v, [&](int blk) { return W[240 + blk]; }, q, q2);
+        gs_stage8<2>(v, [&](int blk) { return W[248 + blk]; }, q, q2);
+        gs_stage8<4>(v, [&](int blk) { return W[252 + blk]; }, q, q2);
+        gs_stage8<8>(v, [&](int blk) { return W[254 + blk]; }, q, q2);
+      } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int d = 1 << t;
-        const int off = 16 - (16 >> t);
+        for (int t = 0; t < 4; ++t) {
+          const int d = 1 << t;
+          const int off = 16 - (16 >> t);
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int blk = p / d, j = blk * 2 * d + p % d;
-          const uint2 w = W[240 + off + blk];
-          gs(v[j], v[j + d], w.x, w.y, q, q2);
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            const uint2 w = W[240 + off + blk];
+            gs(v[j], v[j + d], w.x, w.y, q, q2);
+          }
         }
       }
 #pragma unroll
