@@ -286,13 +286,22 @@ struct TcCursor {
 
 // k_bconv_tc2 epilogue for 8 destination rows: r = the 32 TMEM columns (4 byte
 // planes per row) of this thread's coefficient; dq = {q, q^-1}, doff = row * n
-template <bool FULL>
+// ROWS > 0: the 8 destination rows are consecutive rows of ROWS words (the
+// common case at N = 2^16): one address, then immediate offsets per store
+template <bool FULL, int ROWS = 0>
 __device__ __forceinline__ void tc2_store8(const uint32_t (&r)[32], const uint2* dq, const uint32_t* doff, int nv,
                                            uint32_t* dthr) {
   const uint4* dq4 = reinterpret_cast<const uint4*>(dq);
-  const uint4 o0 = *reinterpret_cast<const uint4*>(doff), o1 = *reinterpret_cast<const uint4*>(doff + 4);
-  const uint32_t off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+  uint32_t off[8];
+  if (ROWS) {
+    off[0] = doff[0];
+  } else {
+    const uint4 o0 = *reinterpret_cast<const uint4*>(doff), o1 = *reinterpret_cast<const uint4*>(doff + 4);
+    off[0] = o0.x; off[1] = o0.y; off[2] = o0.z; off[3] = o0.w;
+    off[4] = o1.x; off[5] = o1.y; off[6] = o1.z; off[7] = o1.w;
+  }
   const uint64_t base = reinterpret_cast<uint64_t>(dthr);
+  uint32_t* rbase = dthr + off[0];
 #pragma unroll
   for (int u2 = 0; u2 < 4; ++u2) {
     const uint4 qq = dq4[u2];  // {q, q^-1} of rows 2 u2, 2 u2 + 1
@@ -305,9 +314,13 @@ __device__ __forceinline__ void tc2_store8(const uint32_t (&r)[32], const uint2*
       uint32_t lo, hi;  // x + 2^16 y = sum_a 2^(8a) acc_a < 2^46
       asm("mad.lo.cc.u32 %0, %2, 65536, %3;\n\tmadc.hi.u32 %1, %2, 65536, 0;\n" : "=r"(lo), "=r"(hi) : "r"(y), "r"(x));
       const uint32_t v = sub_if(mont_reduce64s(lo, hi, q, qi), q);
-      uint64_t addr;  // one IMAD.WIDE.U32 per store address
-      asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(addr) : "r"(off[u]), "l"(base));
-      if (FULL || u < nv) asm volatile("st.global.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+      if (ROWS) {
+        if (FULL || u < nv) rbase[u * ROWS] = v;
+      } else {
+        uint64_t addr;  // one IMAD.WIDE.U32 per store address
+        asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(addr) : "r"(off[u]), "l"(base));
+        if (FULL || u < nv) asm volatile("st.global.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+      }
     }
   }
 }
@@ -336,7 +349,8 @@ __global__ void __launch_bounds__(kTT) k_bconv_tc2(BconvLaunch a, BconvTc t, int
   unsigned char* Bt = At + kATile;                                 // B table of the current group
   uint2* dq = reinterpret_cast<uint2*>(Bt + t.max_npad * KB);      // [dcPad] {q, q^-1}
   uint32_t* doff = reinterpret_cast<uint32_t*>(dq + dcPad);        // [dcPad] destination row * n
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(doff + dcPad);
+  uint32_t* dcont = doff + dcPad;                                   // [dcPad / 8] 8-row block = consecutive rows
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(doff + 2 * dcPad);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -372,12 +386,12 @@ __global__ void __launch_bounds__(kTT) k_bconv_tc2(BconvLaunch a, BconvTc t, int
         isrc = a.groups[ig].src_off;
         isc = a.groups[ig].sc;
       }
-      const uint32_t* src = a.src + ic.b * a.src_bs + (size_t)isrc * n + (size_t)ic.tile * kTT;
-      uint32_t* dst = raw + slot * rawStage;
-      for (int e = tid; e < (int)isc * (kTT / 4); e += kTT) {
-        const int j = e >> 5, c = e & 31;  // kTT / 4 = 32 chunks of 16 B per source row
-        cp16(dst + j * kTT + 4 * c, src + (size_t)j * n + 4 * c);
-      }
+      // source row j = warp + 4 m (m < 4: sc <= 16), 16-B chunk = lane (32 per 128-word row)
+      const uint32_t* src = a.src + ic.b * a.src_bs + ((size_t)isrc + warp) * n + (size_t)ic.tile * kTT + 4 * (tid & 31);
+      uint32_t* dst = raw + slot * rawStage + warp * kTT + 4 * (tid & 31);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        if (warp + 4 * m < (int)isc) cp16(dst + 4 * m * kTT, src + (size_t)(4 * m) * n);
       ic.next(tiles, a.batch);
       ++icount;
     }
@@ -416,6 +430,11 @@ __global__ void __launch_bounds__(kTT) k_bconv_tc2(BconvLaunch a, BconvTc t, int
         dq[i] = d;
         doff[i] = o;
       }
+      for (int c = tid; c < dcPad / 8; c += kTT) {  // block c: rows 8c .. 8c+7 all valid and consecutive
+        bool ok = 8 * c + 8 <= dc;
+        for (int u = 1; ok && u < 8; ++u) ok = a.dst_row[G.map_off + 8 * c + u] == a.dst_row[G.map_off + 8 * c] + u;
+        dcont[c] = ok;
+      }
     }
     {  // transpose: row x = tid, K chunk c holds the words src[4c .. 4c+3][x] (zero past sc)
       const uint32_t* R = raw + (k % kNst) * rawStage;
@@ -452,10 +471,14 @@ __global__ void __launch_bounds__(kTT) k_bconv_tc2(BconvLaunch a, BconvTc t, int
         const int ib = i8 + 8 * h;
         if (ib >= dc) break;
         if (ib + 8 < dc) tmem_ld32_nowait(lane_addr + 4 * (ib + 8), r[h ^ 1]);  // next block in flight
-        if (ib + 8 <= dc)
-          tc2_store8<true>(r[h], dq + ib, doff + ib, 8, dthr);
-        else
+        if (ib + 8 <= dc) {
+          if (n == 65536 && dcont[ib >> 3])
+            tc2_store8<true, 65536>(r[h], dq + ib, doff + ib, 8, dthr);
+          else
+            tc2_store8<true>(r[h], dq + ib, doff + ib, 8, dthr);
+        } else {
           tc2_store8<false>(r[h], dq + ib, doff + ib, dc - ib, dthr);
+        }
         tmem_wait_ld(r[h ^ 1]);
       }
     }
