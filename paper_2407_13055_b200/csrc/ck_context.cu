@@ -333,6 +333,7 @@ struct Context {
   bool use_hrot_tail = false;     // CK32_FUSED_TAIL=1: HRot tail fused into the ModDown forward row pass (measured
                                   // neutral: 16.82k vs 16.86k ops/s, profiles/r2/README.md), else k_hrot_tail
   bool use_tc = true;  // tcgen05 split-word BConv (bconv_tc.cu; CK32_TC=0: the CUDA-core k_bconv)  // CK32_NO_ROW_KEYMULT=1: separate NTT row pass and KeyMult kernels
+  bool tail_gather = false;  // CK32_TAIL_GATHER=1: the gather HRot tail (one coefficient per thread), else k_hrot_tail4
   int tc_var = 2;       // tcgen05 BConv kernel: 1 = k_bconv_tc, 2 = k_bconv_tc2 (slimmer epilogue; default)
   int bconv_fp64 = 0;   // CK32_BCONV_FP64=1|2|3: exact BConv dot products on the FP64 pipe for all / 1 of 2 / 2 of 3 rows
   bool use_fused = false;  // CK32_FUSED=1: INTT-B + BConv + NTT-1 in one kernel (k_conv_mid; slower today)
@@ -1910,6 +1911,7 @@ ck_status ck_context_create(const ck_params* params, const uint32_t* primes, int
     const char* tc = std::getenv("CK32_TC");
     c->use_tc = (tc ? std::atoi(tc) != 0 : true) && c->bconv_fp64 == 0;
     c->tc_var = tc && std::atoi(tc) == 1 ? 1 : 2;  // CK32_TC=1: the first tcgen05 kernel
+    c->tail_gather = std::getenv("CK32_TAIL_GATHER") != nullptr;
     c->use_fused_combine = std::getenv("CK32_NO_FUSED_COMBINE") == nullptr;
     c->use_hrot_tail = std::getenv("CK32_FUSED_TAIL") != nullptr;
     c->use_cluster = std::getenv("CK32_NTT_CLUSTER") != nullptr;
@@ -2642,7 +2644,7 @@ ck_status ck_hrot(ck_context* ctx, uint32_t level, uint32_t batch, const uint32_
       c->drop_divide(pl, B, v, v_w, ts, o, false, st, pre);
       Context::ProfScope ps(c, 6, 4.0 * N * level * 7 * B, 1, st);  // v0 v1 o0 o1 b in, 2 out
       hrot_tail((int)N, (int)level, B, v, v_w, rows * N, o, o_w, level * N, ct, ct_bs, pl.consts.at<uint32_t>(0),
-                c->rotation_map(r), out, ct_bs, c->d_primes, st);
+                c->rotation_map(r), out, ct_bs, c->d_primes, st, c->tail_gather ? nullptr : c->rotation_dest(r));
       ++c->launches;
     }
     c->counters[1] += B;
@@ -2884,7 +2886,8 @@ ck_status ck_hoisted_rotations(ck_context* ctx, uint32_t level, const uint32_t* 
       c->key_mult_v(level, 1, ext, a, 0, evks[i], nullptr, 0, v, st);
       c->drop_divide(pl, 1, v, 0, ts, o, false, st);
       hrot_tail((int)N, (int)level, 1, v, 0, rows * N, o, 0, level * N, ct, 0, pl.consts.at<uint32_t>(0),
-                c->rotation_map(rots[i]), dst, 0, c->d_primes, st);
+                c->rotation_map(rots[i]), dst, 0, c->d_primes, st,
+                c->tail_gather ? nullptr : c->rotation_dest(rots[i]));
       ++c->launches;
       c->counters[1] += 1;
     }

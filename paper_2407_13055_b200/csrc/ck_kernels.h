@@ -187,7 +187,8 @@ void combine(int n, int rows, int npoly, int batch, const uint32_t* v, uint64_t 
 // HRot tail (ckks.cpp:875-882): combine both halves, c0 += b, permute.
 void hrot_tail(int n, int level, int batch, const uint32_t* v, uint64_t v_bs, uint64_t v_ps, const uint32_t* o,
                uint64_t o_bs, uint64_t o_ps, const uint32_t* b, uint64_t b_bs, const uint32_t* div_inv_mont,
-               const uint32_t* src_map, uint32_t* out, uint64_t out_bs, const PrimeDev* primes, cudaStream_t st);
+               const uint32_t* src_map, uint32_t* out, uint64_t out_bs, const PrimeDev* primes, cudaStream_t st,
+               const uint32_t* dest_map = nullptr);  // dest_map: the scatter kernel (4 coefficients per thread)
 
 // element-wise (poly.cpp:146-205): op 0 add, 1 sub, 2 mul (Montgomery).
 // Row i uses prime row_prime[i] if given, else i % prime_mod (prime_mod = rows

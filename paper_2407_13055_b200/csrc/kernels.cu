@@ -429,6 +429,40 @@ __global__ void __launch_bounds__(kT) k_hrot_tail(int n, int level, const uint32
   out[b * out_bs + (size_t)(level + i) * n + j] = c1;
 }
 
+// HRot tail, scatter form: thread = 4 consecutive SOURCE coefficients x..x+3
+// (every operand read with one 16-B load: v0, o0, b, v1, o1) written to
+// out[dest[x + m]] (the automorphism maps each aligned 32-block onto one
+// aligned 32-block, so a warp's scattered 4-B stores fill whole lines in L2).
+// 6 vector loads + 8 scalar stores per 4 coefficients instead of 24 scalar
+// loads (the gather form above: one coefficient per thread).
+__global__ void __launch_bounds__(kT) k_hrot_tail4(int n, int level, const uint32_t* __restrict__ v, uint64_t v_bs,
+                                                   uint64_t v_ps, const uint32_t* __restrict__ o, uint64_t o_bs,
+                                                   uint64_t o_ps, const uint32_t* __restrict__ bb, uint64_t b_bs,
+                                                   const uint32_t* __restrict__ dinv,
+                                                   const uint32_t* __restrict__ dest, uint32_t* __restrict__ out,
+                                                   uint64_t out_bs, const PrimeDev* __restrict__ primes) {
+  const int x = (blockIdx.x * kT + threadIdx.x) * 4;
+  if (x >= n) return;
+  const int i = blockIdx.y, b = blockIdx.z;
+  const PrimeDev P = primes[i];
+  const uint32_t di = dinv[i];
+  const size_t r = (size_t)i * n + x;
+  const uint32_t* vb = v + b * v_bs + r;
+  const uint32_t* ob = o + b * o_bs + r;
+  const uint4 d4 = __ldg(reinterpret_cast<const uint4*>(dest + x));
+  const uint4 v0 = ld4(vb), o0 = ld4(ob), b0 = ld4(bb + b * b_bs + r), v1 = ld4(vb + v_ps), o1 = ld4(ob + o_ps);
+  uint32_t* out0 = out + b * out_bs + (size_t)i * n;
+  uint32_t* out1 = out + b * out_bs + (size_t)(level + i) * n;
+#define CK_T(c)                                                                                   \
+  {                                                                                               \
+    const uint32_t c0 = sub_if(mont_mul(v0.c - o0.c + P.q, di, P.q, P.qinv), P.q);                \
+    out0[d4.c] = sub_if(c0 + b0.c, P.q);                                                          \
+    out1[d4.c] = sub_if(mont_mul(v1.c - o1.c + P.q, di, P.q, P.qinv), P.q);                       \
+  }
+  CK_T(x) CK_T(y) CK_T(z) CK_T(w)
+#undef CK_T
+}
+
 // ------------------------------------------------------------ elementwise --
 // op 0 add, 1 sub, 2 Montgomery mul (poly.cpp:146-164), 3 multiply row i by
 // the canonical Montgomery constant rc[i] (ew_mul_const, poly.cpp:166-180).
@@ -659,7 +693,14 @@ void combine(int n, int rows, int npoly, int batch, const uint32_t* v, uint64_t 
 
 void hrot_tail(int n, int level, int batch, const uint32_t* v, uint64_t v_bs, uint64_t v_ps, const uint32_t* o,
                uint64_t o_bs, uint64_t o_ps, const uint32_t* b, uint64_t b_bs, const uint32_t* div_inv_mont,
-               const uint32_t* src_map, uint32_t* out, uint64_t out_bs, const PrimeDev* primes, cudaStream_t st) {
+               const uint32_t* src_map, uint32_t* out, uint64_t out_bs, const PrimeDev* primes, cudaStream_t st,
+               const uint32_t* dest_map) {
+  if (dest_map && n % 4 == 0) {
+    dim3 grid4(cdiv(n / 4, kT), level, batch);
+    k_hrot_tail4<<<grid4, kT, 0, st>>>(n, level, v, v_bs, v_ps, o, o_bs, o_ps, b, b_bs, div_inv_mont, dest_map, out,
+                                       out_bs, primes);
+    return;
+  }
   dim3 grid(cdiv(n, kT), level, batch);
   k_hrot_tail<<<grid, kT, 0, st>>>(n, level, v, v_bs, v_ps, o, o_bs, o_ps, b, b_bs, div_inv_mont, src_map, out,
                                    out_bs, primes);

@@ -868,7 +868,8 @@ print("fused-intt ok")
 
 @pytest.mark.parametrize("level", [24, 7])
 @pytest.mark.parametrize("variant", ["CK32_ROW8=1", "CK32_KM=7", "CK32_KM=9", "CK32_KM=10", "CK32_KM=11", "CK32_TC=0",
-                                     "CK32_COL=3", "CK32_COL=4", "CK32_KM=12", "CK32_KM=13"])
+                                     "CK32_COL=3", "CK32_COL=4", "CK32_KM=12", "CK32_KM=13",
+                                     "CK32_TAIL_GATHER=1"])
 def test_variant_paths_match_oracle(level, variant):
     """Opt-in kernel variants (env switches read once per process: a fresh
     subprocess each) -- CK32_ROW8=1: the plain row passes as k_row8 (8
@@ -877,7 +878,8 @@ def test_variant_paths_match_oracle(level, variant):
     digit ahead / staged in shared memory per (row, tile); CK32_TC=0: BConv
     on the CUDA cores (k_bconv) instead of tcgen05; CK32_COL=3/4: the TMA
     column pass k_col / k_col_tma; CK32_KM=12: k_row_keymult8b (4 batch
-    items per CTA sharing the row's key slice and twiddles) -- NTT round trip, HMult (merged and lazy) and HRot equal the
+    items per CTA sharing the row's key slice and twiddles); CK32_TAIL_GATHER=1:
+    the one-coefficient-per-thread gather HRot tail -- NTT round trip, HMult (merged and lazy) and HRot equal the
     oracle."""
     import subprocess
     import sys
