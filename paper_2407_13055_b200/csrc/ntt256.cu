@@ -171,6 +171,46 @@ __device__ __forceinline__ void ct_stages16(uint4 (&v)[16], TWF tw, uint32_t q, 
   }
 }
 
+// Inverse GS stages t = T0 .. T1-1 over v[16] (uint4 lanes), stage t pairing
+// rows at distance 1 << t with twiddle tw(t, blk), blk = p >> t: the
+// multiplies of each group of 16 butterflies issued as in ct_stages16 (all
+// IMAD.HI, then all q * hi, then the rest).
+template <int T0, int T1, class TWF>
+__device__ __forceinline__ void gs_stages16(uint4 (&v)[16], TWF tw, uint32_t q, uint32_t q2) {
+#pragma unroll
+  for (int t = T0; t < T1; ++t) {
+    const int d = 1 << t;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      uint32_t dd[16], h[16];
+      uint2 w[4];
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) {
+        const int p = 4 * g + pp, blk = p / d, j = blk * 2 * d + p % d;
+        w[pp] = tw(t, blk);
+        uint32_t* x = &v[j].x;
+        uint32_t* y = &v[j + d].x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          dd[4 * pp + c] = x[c] - y[c] + q2;
+          x[c] = sub_if(x[c] + y[c], q2);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) h[e] = __umulhi(dd[e], w[e >> 2].y);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) h[e] *= q;
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) {
+        const int p = 4 * g + pp, blk = p / d, j = blk * 2 * d + p % d;
+        uint32_t* y = &v[j + d].x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) y[c] = dd[4 * pp + c] * w[pp].x - h[4 * pp + c];
+      }
+    }
+  }
+}
+
 // One radix-2 stage over v[16] (8 butterflies, pairs at distance D, twiddle
 // index blk = p / D) with the multiplies issued in groups as in
 // ct_stages16: all IMAD.HI, then all q * hi, then the rest -- 8 independent
@@ -224,6 +264,10 @@ __device__ __forceinline__ void gs_stage8(uint32_t (&v)[16], TWF tw, uint32_t q,
 }
 
 // ============================================================ column pass ==
+#ifndef CK32_COL_GS_GROUPED
+#define CK32_COL_GS_GROUPED 1
+#endif
+constexpr bool kColGsGrouped = CK32_COL_GS_GROUPED;  // inverse column pass: grouped GS multiplies (gs_stages16)
 constexpr int kCT = 128;              // threads: tau = tid>>3 (16), cq = tid&7 (8)
 constexpr int kCCols = 32;            // columns per tile
 constexpr int kCTiles = kR / kCCols;  // 8 tiles per limb
@@ -384,13 +428,17 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
       // ---- inverse, stages 8..15 (r bits 0..7). phase A rows 16 tau + j.
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = B.tile[(16 * tau + j) * 8 + cq];
+      if (kColGsGrouped) {
+        gs_stages16<0, 4>(v, [&](int t, int blk) { return TW[(128 >> t) + (tau << (3 - t)) + blk]; }, q, q2);
+      } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int d = 1 << t;
+        for (int t = 0; t < 4; ++t) {
+          const int d = 1 << t;
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int blk = p / d, j = blk * 2 * d + p % d;
-          gs4(v[j], v[j + d], TW[(128 >> t) + (tau << (3 - t)) + blk], q, q2);
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            gs4(v[j], v[j + d], TW[(128 >> t) + (tau << (3 - t)) + blk], q, q2);
+          }
         }
       }
 #pragma unroll
@@ -411,13 +459,17 @@ __global__ void __launch_bounds__(kCT, MINB) k_col(const RowJob* __restrict__ jo
         if (nxt < items) prefetch(buf[0], nxt, k + 1);
         cp_commit();
       }
+      if (kColGsGrouped && TWR) {
+        gs_stages16<0, 3>(v, [&](int t, int blk) { return TW[(8 >> t) + blk]; }, q, q2);
+      } else {
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        const int d = 1 << t;
+        for (int t = 0; t < 3; ++t) {
+          const int d = 1 << t;
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int blk = p / d, j = blk * 2 * d + p % d;
-          gs4(v[j], v[j + d], TWR ? TW[(8 >> t) + blk] : twb[(8 >> t) - 1 + blk], q, q2);
+          for (int p = 0; p < 8; ++p) {
+            const int blk = p / d, j = blk * 2 * d + p % d;
+            gs4(v[j], v[j + d], TWR ? TW[(8 >> t) + blk] : twb[(8 >> t) - 1 + blk], q, q2);
+          }
         }
       }
 #pragma unroll
@@ -1688,6 +1740,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
   uint2* T = tws + warp * 256;
   uint2* Ti = tws + (kK8Rows + warp) * 256;  // inverse row twiddles (fused INTT pass A), natural order per stage
   uint32_t* Ks = reinterpret_cast<uint32_t*>(smraw + kK8Smem) + warp * (3 * 2 * 256);  // KPF 3: key slice [D][2][256]
+  uint32_t* Kd = reinterpret_cast<uint32_t*>(smraw + kK8SmemBase) + warp * (2 * 256);  // KPF 6: one digit's key [2][256]
   constexpr int kTiles = kR / kK8Rows;
   const int rows = a.level + a.alpha, B = a.batch;
   const uint32_t LA = (uint32_t)(a.L + a.alpha);
@@ -1702,7 +1755,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
   int g = 0, r = 0;
   PrimeDev P{};
   uint32_t q = 0, q2 = 0, q4 = 0;
-  for (int it = i0; it < i1; ++it) {
+  for (int it = i0, left = i1 - i0; left > 0; ++it, --left) {  // a count: no i1 live across the loop
     __syncwarp();  // the warp is done with the previous item's buffers
     if (it == i0 || b == 0) {  // new (row, tile): prime, and this row's 255 forward twiddles (natural order)
       g = i < a.level ? i : a.L + (i - a.level);
@@ -1712,9 +1765,23 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       q2 = P.q2;
       q4 = 2 * P.q2;
       const uint2* F = fwd + (size_t)g * kN;
-      for (int e = lane; e < 255; e += 32) {
-        const int s = 31 - __clz(e + 1), blk = e + 1 - (1 << s);
-        T[e] = __ldg(&F[(256 << s) + (r << s) + blk]);
+      if (KPF == 6 || KPF == 0) {  // asynchronously (one group, older than the item's extension groups)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = lane + 32 * u;
+          if (e < 255) {
+            const int s = 31 - __clz(e + 1), blk = e + 1 - (1 << s);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&T[e]))),
+                         "l"(&F[(256 << s) + (r << s) + blk])
+                         : "memory");
+          }
+        }
+        cp_commit();
+      } else {
+        for (int e = lane; e < 255; e += 32) {
+          const int s = 31 - __clz(e + 1), blk = e + 1 - (1 << s);
+          T[e] = __ldg(&F[(256 << s) + (r << s) + blk]);
+        }
       }
       if (a.ts && i >= a.src_lo) {  // inverse stage v of row r: I[(N >> (v+1)) + (r << (7-v)) + blk] at 256 - (256 >> v) + blk
         const uint2* I = a.inv_full + (size_t)g * kN;
@@ -1734,8 +1801,19 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         cp_commit();  // older than the extension groups below: complete at the first digit's wait
       }
     }
-    // all digits' extension rows at once (one cp.async group per digit)
-    for (int k = 0; k < a.D; ++k) {
+    // the next item of this CTA's chunk (b fastest): KPF 5 requests its
+    // extension rows digit by digit as soon as this item's digit buffer is free
+    int nb5 = b + 1, ntile5 = tile, ni5 = i;
+    if (nb5 == B) {
+      nb5 = 0;
+      if (++ntile5 == kTiles) {
+        ntile5 = 0;
+        ++ni5;
+      }
+    }
+    const bool next5 = KPF == 5 && left > 1;
+    // all digits' extension rows at once (one cp.async group per digit); KPF 5: the first item only
+    for (int k = 0; k < a.D && (KPF != 5 || it == i0); ++k) {
       const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
       if (!(i >= lo && i < hi)) {
         const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)r * kR;
@@ -1781,6 +1859,16 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
       if (KPF == 1) key_l1(k);
       if (KPF == 2 && k + 1 < a.D) key_l1(k + 1);
+      if (KPF == 6) {  // this digit's key slice (2 halves x 256 words) by cp.async: lands during the row pass
+        __syncwarp();  // every lane has read the previous digit's slice
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t* kr = a.evk + (((size_t)k * 2 + h) * LA + g) * kN + (size_t)r * kR;
+#pragma unroll
+          for (int m = 0; m < 2; ++m) cp16(Kd + h * 256 + 4 * (lane + 32 * m), kr + 4 * (lane + 32 * m));
+        }
+        cp_commit();
+      }
       if (EARLY) {
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
@@ -1811,9 +1899,13 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
         v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
       } else {
-        // KPF 4: one post group per finished digit keeps D - 1 groups younger than this digit's
-        const int pend = KPF == 4 ? a.D - 1 : a.D - 1 - k;
-        if (pend >= 2) cp_wait<2>();
+        // KPF 4: one post group per finished digit keeps D - 1 groups younger than this digit's;
+        // KPF 5: this item's later digits + the next item's earlier ones, D - 1 as well
+        // KPF 6: digit 0 waits behind the later digits' groups and its key group; the later
+        // digits' extension groups completed at the previous digit's key wait (only its key is younger)
+        const int pend = (KPF == 4 || KPF == 5) ? a.D - 1 : KPF == 6 ? (k == 0 ? a.D : 1) : a.D - 1 - k;
+        if (pend >= 3) cp_wait<3>();
+        else if (pend == 2) cp_wait<2>();
         else if (pend == 1) cp_wait<1>();
         else cp_wait<0>();
         __syncwarp();
@@ -1873,7 +1965,29 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = canon8(v[j], q, q2, q4);
       }
-      if (KPF == 3) {
+      if (KPF == 5) {  // digit buffer k is free: the next item's digit-k extension row into it
+        if (next5 && !(ni5 >= lo && ni5 < hi)) {
+          __syncwarp();
+          const uint32_t* gsrc =
+              a.ext + nb5 * a.ext_bs + ((size_t)k * rows + ni5) * kN + (size_t)(ntile5 * kK8Rows + warp) * kR;
+          uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            const int c = 4 * (lane + 32 * m);
+            cp16(line + pad8(c), gsrc + c);
+          }
+        }
+        cp_commit();  // one group per (item, digit), empty for own rows / past the chunk
+      }
+      if (KPF == 6) {
+        cp_wait<0>();
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          kb[m] = *reinterpret_cast<const uint4*>(Kd + 8 * lane + 4 * m);
+          ka[m] = *reinterpret_cast<const uint4*>(Kd + 256 + 8 * lane + 4 * m);
+        }
+      } else if (KPF == 3) {
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           kb[m] = *reinterpret_cast<const uint4*>(Ks + (k * 2 + 0) * 256 + 8 * lane + 4 * m);
@@ -2504,7 +2618,10 @@ template <int MINB, bool EARLY, int KPF = 0>
 static void launch_km8(const KeyMultLaunch& a, const uint2* fwd, int items, cudaStream_t st) {
   static int grid[2] = {0, 0};
   const int fi = a.ts ? 1 : 0;  // the inverse twiddle region only when the INTT pass A is fused
-  const int smem = KPF == 3 ? kK8Smem + kK8Rows * 3 * 2 * 256 * 4 : fi ? kK8Smem : kK8SmemBase;
+  const int smem = KPF == 3 ? kK8Smem + kK8Rows * 3 * 2 * 256 * 4
+                   : KPF == 6 ? kK8SmemBase + kK8Rows * 2 * 256 * 4
+                   : fi       ? kK8Smem
+                              : kK8SmemBase;
   if (!grid[fi]) {
     cudaFuncSetAttribute(k_row_keymult8<MINB, EARLY, KPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int dev = 0, sms = 148, per = 1;
@@ -2556,10 +2673,14 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, cons
     k_row_keymult8b<8><<<std::min(grid, items8b), 128, kK8bSmem, st>>>(a, fwd_full);
     return;
   }
-  if (ver >= 7 && ver <= 13 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
+  if (ver >= 7 && ver <= 15 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
     const int items8 = (a.level + a.alpha) * (kR / kK8Rows) * a.batch;
     if (ver == 13 && !a.ts)
       launch_km8<8, false, 4>(a, fwd_full, items8, st);  // own / fold rows through cp.async into freed digit buffers
+    else if (ver == 14 && !a.ts)
+      launch_km8<8, false, 5>(a, fwd_full, items8, st);  // next item's extension rows into each freed digit buffer
+    else if (ver == 15 && !a.ts)
+      launch_km8<7, false, 6>(a, fwd_full, items8, st);  // per-digit key slice + row twiddles by cp.async, 7 CTAs / SM
     else if (ver == 11)
       launch_km8<4, false, 3>(a, fwd_full, items8, st);  // key slice staged in shared memory per (row, tile), 4 CTAs / SM
     else if (ver == 9)
