@@ -150,8 +150,8 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    numa_local(local)  # also at N = 1: the e2e leg's pinned buffers are first-touched on the GPU's NUMA node
     if world > 1:
-        numa_local(local)
         backend = os.environ.get("CK32_DIST_BACKEND", "nccl")
         t0 = time.perf_counter()
         if backend == "nccl":
@@ -182,6 +182,7 @@ def numa_local(device: int) -> None:
         cpus &= set(range(os.cpu_count()))
         if cpus:
             os.sched_setaffinity(0, cpus)
+            print(f"[bench] cuda:{device}: host threads pinned to {len(cpus)} NUMA-local CPUs", file=sys.stderr)
         nv.nvmlShutdown()
     except Exception:
         pass
@@ -506,6 +507,34 @@ def main():
                "path": "ckks.hmult / ckks.hrot (C ABI) on ciphertexts copied from pinned host memory; results copied "
                        "back each step (pipeline.HostPipeline: chunks of %d, H2D / compute / D2H on separate "
                        "streams, results written into per-slot device buffers: no allocation per step)" % pipe.chunk}
+        # the link's own ceiling for this step: the same H2D and D2H bytes copied concurrently
+        # (two streams, nothing else running), best of 3 -- e2e / ceiling says how close the
+        # pipeline gets to PCIe, the bound of the end-to-end number
+        din = [torch.empty_like(hx, device=dev), torch.empty_like(hy, device=dev)]
+        dout = [torch.empty_like(ho1, device=dev), torch.empty_like(ho2, device=dev)]
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        best = None
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            a.record(st)
+            s_in.wait_event(a)
+            s_out.wait_event(a)
+            with torch.cuda.stream(s_in):
+                for d_, h_ in zip(din, (hx, hy)):
+                    d_.copy_(h_, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                for h_, d_ in zip((ho1, ho2), dout):
+                    h_.copy_(d_, non_blocking=True)
+            st.wait_stream(s_in)
+            st.wait_stream(s_out)
+            b.record(st)
+            torch.cuda.synchronize(dev)
+            best = a.elapsed_time(b) if best is None else min(best, a.elapsed_time(b))
+        ceil_ops = 2 * Be / (best / 1e3)
+        e2e["pcie_ceiling"] = {"copy_only_ms_per_step": round(best, 3),
+                               "bidirectional_GBps": round((e2e["h2d_bytes_per_step"] + e2e["d2h_bytes_per_step"]) / (best * 1e6), 1),
+                               "ops_per_s": round(ceil_ops, 1), "frac": round(e2e["value"] / world / ceil_ops, 3)}
+        del din, dout
 
     # ---- single-ciphertext serving (B = 1): eager C-ABI calls vs one CUDA graph replay
     small = None

@@ -83,6 +83,20 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
+// ALU-pinned adds.  ptxas issues about half of the butterflies' two-input
+// adds (x + t) as IMAD.IADD on the fmaheavy pipe -- the pipe that bounds the
+// NTT (IMAD.HI = 4 cycles, IMAD = 2 per warp instruction) -- while the ALU
+// pipe has slack.  min(a + b, bound) with a runtime bound the sum never
+// reaches is the same value and compiles to ONE VIADDMNMX, which only the
+// ALU pipe executes.  Measured neutral (r2s4: k_row<0, 3> -4%, the step
+// unchanged: ptxas moves other work onto IMAD.MOV instead), so off by default.
+#ifndef CK32_ALU_ADD
+#define CK32_ALU_ADD 0
+#endif
+__device__ __forceinline__ uint32_t add_alu(uint32_t a, uint32_t b, uint32_t bound) {
+  return CK32_ALU_ADD ? min(a + b, bound) : a + b;
+}
+
 // forward CT butterfly, Harvey lazy: x,y in [0,4q) -> [0,4q)
 __device__ __forceinline__ void ct(uint32_t& x, uint32_t& y, uint32_t w, uint32_t wp, uint32_t q, uint32_t q2) {
   const uint32_t xx = sub_if(x, q2);
@@ -99,7 +113,7 @@ __device__ __forceinline__ void ctl(uint32_t& x, uint32_t& y, uint32_t w, uint32
                                     uint32_t q4) {
   const uint32_t xx = RED ? sub_if(x, q4) : x;
   const uint32_t t = shoup_mul(y, w, wp, q);
-  x = xx + t;
+  x = add_alu(xx, t, 2 * q4);  // < 8q
   y = xx - t + q2;
 }
 __device__ __forceinline__ uint32_t canon8(uint32_t x, uint32_t q, uint32_t q2, uint32_t q4) {
@@ -107,7 +121,7 @@ __device__ __forceinline__ uint32_t canon8(uint32_t x, uint32_t q, uint32_t q2, 
 }
 // inverse GS butterfly: x,y in [0,2q) -> [0,2q)
 __device__ __forceinline__ void gs(uint32_t& x, uint32_t& y, uint32_t w, uint32_t wp, uint32_t q, uint32_t q2) {
-  const uint32_t u = sub_if(x + y, q2);
+  const uint32_t u = sub_if(add_alu(x, y, 2 * q2), q2);  // x + y < 4q
   y = shoup_mul(x - y + q2, w, wp, q);
   x = u;
 }
@@ -163,7 +177,7 @@ __device__ __forceinline__ void ct_stages16(uint4 (&v)[16], TWF tw, uint32_t q, 
         for (int c = 0; c < 4; ++c) {
           const uint32_t tt = y[c] * ww - h[4 * pp + c];  // shoup_mul: [0, 2q)
           const uint32_t xx = ((RED >> t) & 1u) ? sub_if(x[c], q4) : x[c];
-          x[c] = xx + tt;
+          x[c] = add_alu(xx, tt, 2 * q4);  // < 8q
           y[c] = xx - tt + q2;
         }
       }
@@ -193,7 +207,7 @@ __device__ __forceinline__ void gs_stages16(uint4 (&v)[16], TWF tw, uint32_t q, 
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           dd[4 * pp + c] = x[c] - y[c] + q2;
-          x[c] = sub_if(x[c] + y[c], q2);
+          x[c] = sub_if(add_alu(x[c], y[c], 2 * q2), q2);
         }
       }
 #pragma unroll
@@ -235,7 +249,7 @@ __device__ __forceinline__ void ct_stage8(uint32_t (&v)[16], TWF tw, uint32_t q,
     const int j = (p / D) * 2 * D + p % D;
     const uint32_t tt = v[j + D] * w[p].x - h[p];
     const uint32_t xx = RED ? sub_if(v[j], q4) : v[j];
-    v[j] = xx + tt;
+    v[j] = add_alu(xx, tt, 2 * q4);  // < 8q
     v[j + D] = xx - tt + q2;
   }
 }
@@ -250,7 +264,7 @@ __device__ __forceinline__ void gs_stage8(uint32_t (&v)[16], TWF tw, uint32_t q,
   for (int p = 0; p < 8; ++p) {
     const int j = (p / D) * 2 * D + p % D;
     dd[p] = v[j] - v[j + D] + q2;
-    v[j] = sub_if(v[j] + v[j + D], q2);
+    v[j] = sub_if(add_alu(v[j], v[j + D], 2 * q2), q2);
   }
 #pragma unroll
   for (int p = 0; p < 8; ++p) h[p] = __umulhi(dd[p], w[p].y);
@@ -1030,11 +1044,16 @@ void init_grids() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(k_col<false, false, true, 5, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
   cudaFuncSetAttribute(k_col<true, false, true, 5, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
+  cudaFuncSetAttribute(k_col<false, false, true, 6, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
+  cudaFuncSetAttribute(k_col<true, false, true, 6, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
   cudaFuncSetAttribute(k_col_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
   cudaFuncSetAttribute(k_col_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColTmaSmem);
   if (g_col_var == 4) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col_tma<false>, kCT, kColTmaSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col_tma<true>, kCT, kColTmaSmem);
+  } else if (g_col_var == 5) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, false, true, 6, 8, true>, kCT, kColTmaSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, false, true, 6, 8, true>, kCT, kColTmaSmem);
   } else if (g_col_var == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c1, k_col<false, false, true, 5, 8, true>, kCT, kColTmaSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, k_col<true, false, true, 5, 8, true>, kCT, kColTmaSmem);
@@ -1101,6 +1120,12 @@ void launch_col(const NttLaunch& a, const uint32_t* src, uint64_t src_bs, cudaSt
     static const int dbg = std::getenv("CK32_COL_DBG") ? std::atoi(std::getenv("CK32_COL_DBG")) : 0;
     k_col_tma<INV><<<grid, kCT, kColTmaSmem, st>>>(a.jobs, src_bs, a.dst, a.dst_bs, a.batch, a.njobs, a.primes, a.tw,
                                                    a.exits, a.entry, m, dbg);
+    return;
+  }
+  if (g_col_var == 5) {  // TMA staging at 6 CTAs / SM (register-capped)
+    const CUtensorMap& m = col_tensor_map(INV ? a.dst : src);
+    k_col<INV, false, true, 6, 8, true><<<grid, kCT, kColTmaSmem, st>>>(a.jobs, src, src_bs, a.dst, a.dst_bs, a.batch,
+                                                                       a.njobs, a.primes, a.tw, a.exits, a.entry, m);
     return;
   }
   if (g_col_var == 3) {  // TMA staging (the tile source is dst for the inverse pass, as in prefetch)

@@ -868,7 +868,7 @@ print("fused-intt ok")
 
 @pytest.mark.parametrize("level", [24, 7])
 @pytest.mark.parametrize("variant", ["CK32_ROW8=1", "CK32_KM=7", "CK32_KM=9", "CK32_KM=10", "CK32_KM=11", "CK32_TC=0",
-                                     "CK32_COL=3", "CK32_COL=4", "CK32_KM=12", "CK32_KM=13", "CK32_KM=14", "CK32_KM=15",
+                                     "CK32_COL=3", "CK32_COL=4", "CK32_COL=5", "CK32_KM=12", "CK32_KM=13", "CK32_KM=14", "CK32_KM=15",
                                      "CK32_TAIL_GATHER=1"])
 def test_variant_paths_match_oracle(level, variant):
     """Opt-in kernel variants (env switches read once per process: a fresh
