@@ -146,39 +146,61 @@ __device__ __forceinline__ void gs4(uint4& x, uint4& y, uint2 w, uint32_t q, uin
 // dependent ones instead of 4 (the `wait` stall of the per-butterfly order).
 // RED: bit t set = stage t reduces x from [0, 8q) to [0, 4q) first (lazy
 // schedule of `ctl`); clear = x is used as is.
+#ifndef CK32_CT_PLAIN
+#define CK32_CT_PLAIN 0
+#endif
 template <int T0, unsigned RED, class TWF>
 __device__ __forceinline__ void ct_stages16(uint4 (&v)[16], TWF tw, uint32_t q, uint32_t q2, uint32_t q4) {
+  if constexpr (CK32_CT_PLAIN != 0) {  // per-butterfly order (the round-1 skeleton's): measured 3% slower (r2s4)
 #pragma unroll
-  for (int t = T0; t < 4; ++t) {
-    const int d = 8 >> t;
-    uint2 w[8];
+    for (int t = T0; t < 4; ++t) {
+      const int d = 8 >> t;
 #pragma unroll
-    for (int blk = 0; blk < (1 << t); ++blk) w[blk] = tw(t, blk);
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      uint32_t h[16];
-#pragma unroll
-      for (int pp = 0; pp < 4; ++pp) {
-        const int p = 4 * g + pp, blk = p / d, j = blk * 2 * d + p % d;
-        h[4 * pp + 0] = __umulhi(v[j + d].x, w[blk].y);
-        h[4 * pp + 1] = __umulhi(v[j + d].y, w[blk].y);
-        h[4 * pp + 2] = __umulhi(v[j + d].z, w[blk].y);
-        h[4 * pp + 3] = __umulhi(v[j + d].w, w[blk].y);
-      }
-#pragma unroll
-      for (int e = 0; e < 16; ++e) h[e] *= q;
-#pragma unroll
-      for (int pp = 0; pp < 4; ++pp) {
-        const int p = 4 * g + pp, blk = p / d, j = blk * 2 * d + p % d;
-        const uint32_t ww = w[blk].x;
-        uint32_t* y = &v[j + d].x;
+      for (int p = 0; p < 8; ++p) {
+        const int blk = p / d, j = blk * 2 * d + p % d;
+        const uint2 w = tw(t, blk);
         uint32_t* x = &v[j].x;
+        uint32_t* y = &v[j + d].x;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const uint32_t tt = y[c] * ww - h[4 * pp + c];  // shoup_mul: [0, 2q)
-          const uint32_t xx = ((RED >> t) & 1u) ? sub_if(x[c], q4) : x[c];
-          x[c] = add_alu(xx, tt, 2 * q4);  // < 8q
-          y[c] = xx - tt + q2;
+          if ((RED >> t) & 1u) ctl<true>(x[c], y[c], w.x, w.y, q, q2, q4);
+          else ctl<false>(x[c], y[c], w.x, w.y, q, q2, q4);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int t = T0; t < 4; ++t) {
+      const int d = 8 >> t;
+      uint2 w[8];
+#pragma unroll
+      for (int blk = 0; blk < (1 << t); ++blk) w[blk] = tw(t, blk);
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        uint32_t h[16];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+          const int p = 4 * g + pp, blk = p / d, j = blk * 2 * d + p % d;
+          h[4 * pp + 0] = __umulhi(v[j + d].x, w[blk].y);
+          h[4 * pp + 1] = __umulhi(v[j + d].y, w[blk].y);
+          h[4 * pp + 2] = __umulhi(v[j + d].z, w[blk].y);
+          h[4 * pp + 3] = __umulhi(v[j + d].w, w[blk].y);
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) h[e] *= q;
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+          const int p = 4 * g + pp, blk = p / d, j = blk * 2 * d + p % d;
+          const uint32_t ww = w[blk].x;
+          uint32_t* y = &v[j + d].x;
+          uint32_t* x = &v[j].x;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t tt = y[c] * ww - h[4 * pp + c];  // shoup_mul: [0, 2q)
+            const uint32_t xx = ((RED >> t) & 1u) ? sub_if(x[c], q4) : x[c];
+            x[c] = add_alu(xx, tt, 2 * q4);  // < 8q
+            y[c] = xx - tt + q2;
+          }
         }
       }
     }
