@@ -509,6 +509,8 @@ void launch_tc(const BconvLaunch& a, const BconvTc& t, int n, cudaStream_t st) {
     // limits are smem / registers / threads and the 512 TMEM columns per SM
     per = std::max(per, std::min(227 * 1024 / (smem + 1024), 2048 / kTT));
     per = std::min(per, 512 / NCOLS);
+    if (const char* e = std::getenv("CK32_BCONV_CTAS"))  // cap (A/B of the 2-stream overlap)
+      if (std::atoi(e) > 0) per = std::min(per, std::atoi(e));
     grid = sms * std::max(1, per);
   }
   const int items = a.ngroups * a.batch * (n / kTT);

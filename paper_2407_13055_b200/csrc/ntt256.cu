@@ -1039,6 +1039,11 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
 }
 
 int g_col_grid[2] = {0, 0}, g_row_grid = 0;
+int env_cap(const char* name) {  // a positive integer from the environment, else "no cap"
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : 0;
+  return v > 0 ? v : 1 << 20;
+}
 bool g_col_db = false;
 int g_col_var = 3;  // CK32_COL: 0 = twiddles in registers, 1 = twiddle ring (4 CTAs/SM), 2 = ring, 5 CTAs/SM (cp.async), 3 = ring, 5 CTAs/SM, TMA tile loads (default)
 constexpr int kColRingSmem = (int)sizeof(ColBuf::tile) + 2 * 256 * 8;  // 36 KB (6 CTAs/SM measured no faster than 5)
@@ -1096,9 +1101,12 @@ void init_grids() {
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, k_row<false>, kRT, kRowSmem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, k_row<true>, kRT, kRowSmem);
-  g_col_grid[0] = sms * max(1, c1);
-  g_col_grid[1] = sms * max(1, c2);
-  g_row_grid = sms * max(1, min(r1, r2));
+  // CK32_COL_CTAS / CK32_ROW_CTAS: cap the persistent grids' CTAs per SM (A/B
+  // of leaving SM room for the other stream's kernels)
+  const int ccap = env_cap("CK32_COL_CTAS"), rcap = env_cap("CK32_ROW_CTAS");
+  g_col_grid[0] = sms * max(1, min(c1, ccap));
+  g_col_grid[1] = sms * max(1, min(c2, ccap));
+  g_row_grid = sms * max(1, min(min(r1, r2), rcap));
 }
 
 // 2D tensor map over a limb matrix: rows of 256 uint32 starting at `base`,
@@ -2675,7 +2683,7 @@ static void launch_km8(const KeyMultLaunch& a, const uint2* fwd, int items, cuda
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<MINB, EARLY, KPF>, 128, smem);
-    grid[fi] = sms * std::max(1, per);
+    grid[fi] = sms * std::max(1, std::min(per, env_cap("CK32_KM_CTAS")));
   }
   k_row_keymult8<MINB, EARLY, KPF><<<std::min(grid[fi], items), 128, smem, st>>>(a, fwd);
 }
