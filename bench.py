@@ -618,6 +618,7 @@ def main():
     if world == 1 and not args.no_extra:
         import copy
 
+        extra["config1_ntt_roundtrip"] = ntt_roundtrip(C, dev, st, clk)
         C.close()
         torch.cuda.empty_cache()
         c4 = {}
@@ -680,6 +681,55 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def ntt_roundtrip(C, dev, st, clk, rows: int = 3072, reps: int = 5):
+    """BASELINE config 1's NTT/INTT round trip through the C ABI
+    (ck_ntt_forward / ck_intt_inverse, ntt.hpp:90-91): `rows` limbs of
+    N = 2^16 cycling over the 32 primes (3072 x 256 KiB = 768 MiB, larger
+    than L2), forward then inverse, each timed with CUDA events on the
+    library's (current) stream over `reps` repetitions; the round trip must
+    return the input residues exactly."""
+    import numpy as np
+    import torch
+    from paper_2407_13055_b200 import _native as nat
+
+    g = np.array([i % (L + ALPHA) for i in range(rows)], np.uint32)
+    q = torch.tensor(C.primes[g].astype(np.int64), device=dev)
+    x0 = (torch.randint(0, 1 << 62, (rows, N_RING), device=dev, dtype=torch.int64) % q[:, None]).to(torch.int32)
+    x = x0.clone()
+    garr = nat.u32_array(g)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fwd = lambda: nat.call("ck_ntt_forward", C.handle, x.data_ptr(), rows, garr, C.stream())  # noqa: E731
+    inv = lambda: nat.call("ck_intt_inverse", C.handle, x.data_ptr(), rows, garr, None, C.stream())  # noqa: E731
+    fwd()
+    inv()
+    exact = bool(torch.equal(x, x0))
+    out = {}
+    peak, kind = peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = clk.summary().get("sm_mhz") or 1965.0
+    # reps forward transforms, then reps inverse ones: the inverse is exact on
+    # canonical residues, so x ends where it started
+    for name, fn in (("fwd", fwd), ("inv", inv)):
+        torch.cuda.synchronize(dev)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / reps
+        gbs = rows * 8 * N_RING / (ms * 1e6)
+        bfly = rows * 16 * (N_RING // 2) / (ms * 1e-3) / (sms * mhz * 1e6)
+        out[name] = {"ms": round(ms, 4), "ns_per_limb": round(ms * 1e6 / rows, 1), "GBps": round(gbs, 1),
+                     "frac": round(gbs / peak, 4), "butterflies_per_clk_per_sm": round(bfly, 2)}
+    exact = exact and bool(torch.equal(x, x0))
+    del x, x0
+    torch.cuda.empty_cache()
+    return dict(out, roundtrip_exact=exact, limbs=rows, peak_GBps=peak, peak_kind=kind,
+                bytes_per_limb=8 * N_RING,
+                workload="BASELINE config 1 NTT/INTT round trip: %d limbs of N=2^16 over the 32 primes "
+                         "(768 MiB, larger than L2), C ABI ck_ntt_forward / ck_intt_inverse, %d reps each" % (rows, reps))
 
 
 def run_limb(args):
