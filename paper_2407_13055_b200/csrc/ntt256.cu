@@ -805,6 +805,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
   // A), kept in registers across the batch items of one (job, row tile)
   uint2 twr[15];
   uint32_t q = 0, q2 = 0, q4 = 0;
+  uint32_t di_c = 0, qinv_c = 0;  // COMB: the job's divisor inverse and q^-1, loaded with the job (not at the store)
   for (int it = i0, k = 0; it < i1; ++it, ++k) {
     uint32_t* line_buf = sbuf + (k & 1) * kRowBufWords;
     const int b = c.b, tile = c.tile;
@@ -832,6 +833,10 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
       q = P.q;
       q2 = P.q2;
       q4 = 2 * P.q2;
+      if (COMB) {
+        qinv_c = P.qinv;
+        di_c = cb.dinv[J.dst_off % cb.out_q];
+      }
     }
     if (reload) {
 #pragma unroll
@@ -922,7 +927,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
         const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + xo;
         const uint32_t* br = cb.add + b * cb.add_bs + (size_t)i * kN + xo;
         uint32_t* orow_t = cb.out + b * cb.out_bs + ((size_t)pi * cb.out_q + i) * kN;
-        const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv;
+        const uint32_t di = di_c, qinv = qinv_c;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const uint4 vv = *reinterpret_cast<const uint4*>(vr + 4 * m);
@@ -957,7 +962,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
       } else if (COMB) {  // J.dst_off = p * out_q + i; v row p * prow + i; prime i
         const uint32_t pi = J.dst_off / cb.out_q, i = J.dst_off - pi * cb.out_q;
         const uint32_t* vr = cb.v + b * cb.v_bs + ((size_t)pi * cb.prow + i) * kN + (size_t)r * kR + 16 * tau;
-        const uint32_t di = cb.dinv[i], qinv = primes[J.prime].qinv;
+        const uint32_t di = di_c, qinv = qinv_c;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const uint4 vv = COMB == 2 ? vvr[m] : *reinterpret_cast<const uint4*>(vr + 4 * m);
