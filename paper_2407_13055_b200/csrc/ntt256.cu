@@ -1791,7 +1791,7 @@ constexpr int kK8Smem = kK8SmemBase + kK8Rows * 256 * 8;  // + inverse twiddles 
 // KPF (with !EARLY): 1 = the digit's key lines are requested into L1
 // (prefetch.global.L1) before its row pass, 2 = the next digit's during this
 // digit's row pass (the first digit's at the item start).
-template <int MINB, bool EARLY = true, int KPF = 0>
+template <int MINB, bool EARLY = true, int KPF = 0, int DD = 0>
 __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, const uint2* __restrict__ fwd) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1802,6 +1802,8 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
   uint32_t* Ks = reinterpret_cast<uint32_t*>(smraw + kK8Smem) + warp * (3 * 2 * 256);  // KPF 3: key slice [D][2][256]
   uint32_t* Kd = reinterpret_cast<uint32_t*>(smraw + kK8SmemBase) + warp * (2 * 256);  // KPF 6: one digit's key [2][256]
   constexpr int kTiles = kR / kK8Rows;
+  // KPF 7 (the MACs after all digits' row passes) is instantiated per digit count
+  const int Dn = (KPF == 7 && DD > 0) ? DD : a.D;
   const int rows = a.level + a.alpha, B = a.batch;
   const uint32_t LA = (uint32_t)(a.L + a.alpha);
   const int items = rows * kTiles * B;  // (row i, tile, b), b fastest
@@ -1825,7 +1827,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       q2 = P.q2;
       q4 = 2 * P.q2;
       const uint2* F = fwd + (size_t)g * kN;
-      if (KPF == 6 || KPF == 0) {  // asynchronously (one group, older than the item's extension groups)
+      if (KPF == 6 || KPF == 0 || KPF == 7) {  // asynchronously (one group, older than the item's extension groups)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int e = lane + 32 * u;
@@ -1851,7 +1853,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
             Ti[256 - (256 >> v) + blk] = __ldg(&I[(kN >> (v + 1)) + (r << (7 - v)) + blk]);
       }
       if (KPF == 3) {  // this row's key slice (D digits x 2 halves x 256 words) into shared memory, reused for all b
-        for (int k = 0; k < a.D; ++k)
+        for (int k = 0; k < Dn; ++k)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t* kr = a.evk + (((size_t)k * 2 + h) * LA + g) * kN + (size_t)r * kR;
@@ -1873,7 +1875,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
     }
     const bool next5 = KPF == 5 && left > 1;
     // all digits' extension rows at once (one cp.async group per digit); KPF 5: the first item only
-    for (int k = 0; k < a.D && (KPF != 5 || it == i0); ++k) {
+    for (int k = 0; k < Dn && (KPF != 5 || it == i0); ++k) {
       const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
       if (!(i >= lo && i < hi)) {
         const uint32_t* gsrc = a.ext + b * a.ext_bs + ((size_t)k * rows + i) * kN + (size_t)r * kR;
@@ -1912,13 +1914,15 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       }
     };
     if (KPF == 2) key_l1(0);
-    for (int k = 0; k < a.D; ++k) {
+    uint32_t vd[KPF == 7 ? 3 : 1][8];  // KPF 7: every digit's row-pass output, multiplied after the loop
+#pragma unroll(KPF == 7 ? 3 : 1)
+    for (int k = 0; k < Dn; ++k) {
       const int lo = k * a.alpha, hi = min((k + 1) * a.alpha, a.level);
       uint4 kb[2], ka[2];  // key halves (EARLY: first, their L2 latency hides behind the butterflies)
       const uint32_t* eb = a.evk + (((size_t)k * 2 + 0) * LA + g) * kN + rofs;
       const uint32_t* ea = a.evk + (((size_t)k * 2 + 1) * LA + g) * kN + rofs;
       if (KPF == 1) key_l1(k);
-      if (KPF == 2 && k + 1 < a.D) key_l1(k + 1);
+      if (KPF == 2 && k + 1 < Dn) key_l1(k + 1);
       if (KPF == 6) {  // this digit's key slice (2 halves x 256 words) by cp.async: lands during the row pass
         __syncwarp();  // every lane has read the previous digit's slice
 #pragma unroll
@@ -1938,8 +1942,8 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
       }
       uint32_t v[8];
       if (KPF == 4 && i >= lo && i < hi) {  // own row, staged by cp.async at the item start
-        if (a.D >= 3) cp_wait<2>();
-        else if (a.D == 2) cp_wait<1>();
+        if (Dn >= 3) cp_wait<2>();
+        else if (Dn == 2) cp_wait<1>();
         else cp_wait<0>();
         __syncwarp();
         const uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
@@ -1949,8 +1953,8 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
       } else if (i >= lo && i < hi) {  // the digit's own row (ModUp pass-through), evaluation form already
         if (KPF == 3 && k == 0) {  // no extension wait precedes this digit: wait for the key group here
-          if (a.D >= 3) cp_wait<2>();
-          else if (a.D == 2) cp_wait<1>();
+          if (Dn >= 3) cp_wait<2>();
+          else if (Dn == 2) cp_wait<1>();
           else cp_wait<0>();
           __syncwarp();
         }
@@ -1963,7 +1967,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         // KPF 5: this item's later digits + the next item's earlier ones, D - 1 as well
         // KPF 6: digit 0 waits behind the later digits' groups and its key group; the later
         // digits' extension groups completed at the previous digit's key wait (only its key is younger)
-        const int pend = (KPF == 4 || KPF == 5) ? a.D - 1 : KPF == 6 ? (k == 0 ? a.D : 1) : a.D - 1 - k;
+        const int pend = (KPF == 4 || KPF == 5) ? Dn - 1 : KPF == 6 ? (k == 0 ? Dn : 1) : Dn - 1 - k;
         if (pend >= 3) cp_wait<3>();
         else if (pend == 2) cp_wait<2>();
         else if (pend == 1) cp_wait<1>();
@@ -2025,6 +2029,11 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = canon8(v[j], q, q2, q4);
       }
+      if constexpr (KPF == 7) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vd[k][j] = v[j];
+        continue;
+      }
       if (KPF == 5) {  // digit buffer k is free: the next item's digit-k extension row into it
         if (next5 && !(ni5 >= lo && ni5 < hi)) {
           __syncwarp();
@@ -2072,7 +2081,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         s1[4 * m + 3] = mac_wide(s1[4 * m + 3], v[4 * m + 3], ka[m].w);
       }
       if (KPF == 4) {  // this digit's buffer is free: the fold row k (digits 0, 1 of a 3-digit key) into it
-        if (a.fold && i < a.level && k < 2 && a.D == 3) {
+        if (a.fold && i < a.level && k < 2 && Dn == 3) {
           __syncwarp();
           const uint32_t* gsrc = a.fold + b * a.fold_bs + (size_t)(k * a.level + i) * kN + (size_t)r * kR;
           uint32_t* line = sbuf + (k * kK8Rows + warp) * kK8Stride;
@@ -2092,11 +2101,42 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
         }
       }
     }
+    if constexpr (KPF == 7) {
+      // the key MACs of all digits at once: per output, DD products (+ the
+      // fold) summed in one expression -- IMAD.WIDE per product and 3-input
+      // adds with carry, instead of a split IMAD.WIDE + IADD3 + IADD3.X per
+      // loop-carried MAC -- then reduced and stored; one exposed key-load
+      // latency per item instead of one per digit
+      const bool fold = a.fold && i < a.level;
+      const uint32_t pm = fold ? a.p_mont[i] : 0u;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // key half b (-> v0), then a (-> v1): 12 key registers live at a time
+        uint32_t* o = a.v + b * a.v_bs + (size_t)(h * rows + i) * kN + rofs;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          uint4 kh[3];
+#pragma unroll
+          for (int k = 0; k < DD; ++k)
+            kh[k] = __ldg(reinterpret_cast<const uint4*>(a.evk + (((size_t)k * 2 + h) * LA + g) * kN + rofs + 4 * m));
+          uint4 f = make_uint4(0, 0, 0, 0);
+          if (fold) f = *reinterpret_cast<const uint4*>(a.fold + b * a.fold_bs + (size_t)(h * a.level + i) * kN + rofs + 4 * m);
+          uint32_t rr[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint64_t t = (uint64_t)(&f.x)[c] * pm;
+#pragma unroll
+            for (int k = 0; k < DD; ++k) t += (uint64_t)vd[k][4 * m + c] * (&kh[k].x)[c];
+            rr[c] = sub_if(mont_reduce64s((uint32_t)t, (uint32_t)(t >> 32), q, P.qinv), q);
+          }
+          stg4(o + 4 * m, make_uint4(rr[0], rr[1], rr[2], rr[3]));
+        }
+      }
+    } else {
     if (a.fold && i < a.level) {  // merged HMult: v += P * d0 / d1 (ckks.cpp:831-842)
       const uint32_t pm = a.p_mont[i];
       const uint32_t* f0 = a.fold + b * a.fold_bs + (size_t)i * kN + rofs;
       const uint32_t* f1 = a.fold + b * a.fold_bs + (size_t)(a.level + i) * kN + rofs;
-      const bool staged = KPF == 4 && a.D == 3;
+      const bool staged = KPF == 4 && Dn == 3;
       if (staged) {  // fold rows staged in digit buffers 0 / 1
         cp_wait<0>();
         __syncwarp();
@@ -2190,6 +2230,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
                                     sub_if(mont_reduce64s((uint32_t)(s1[4 * m + 3]), (uint32_t)((s1[4 * m + 3]) >> 32), q, P.qinv), q)));
       }
     }
+    }  // KPF != 7
     if (++b == B) {
       b = 0;
       if (++tile == kTiles) {
@@ -2674,7 +2715,7 @@ bool row_keymult_fuses_intt(const KeyMultLaunch& a) {
   return on && v >= 7 && v <= 11 && a.D <= 3;
 }
 
-template <int MINB, bool EARLY, int KPF = 0>
+template <int MINB, bool EARLY, int KPF = 0, int DD = 0>
 static void launch_km8(const KeyMultLaunch& a, const uint2* fwd, int items, cudaStream_t st) {
   static int grid[2] = {0, 0};
   const int fi = a.ts ? 1 : 0;  // the inverse twiddle region only when the INTT pass A is fused
@@ -2683,14 +2724,14 @@ static void launch_km8(const KeyMultLaunch& a, const uint2* fwd, int items, cuda
                    : fi       ? kK8Smem
                               : kK8SmemBase;
   if (!grid[fi]) {
-    cudaFuncSetAttribute(k_row_keymult8<MINB, EARLY, KPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_row_keymult8<MINB, EARLY, KPF, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<MINB, EARLY, KPF>, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_row_keymult8<MINB, EARLY, KPF, DD>, 128, smem);
     grid[fi] = sms * std::max(1, std::min(per, env_cap("CK32_KM_CTAS")));
   }
-  k_row_keymult8<MINB, EARLY, KPF><<<std::min(grid[fi], items), 128, smem, st>>>(a, fwd);
+  k_row_keymult8<MINB, EARLY, KPF, DD><<<std::min(grid[fi], items), 128, smem, st>>>(a, fwd);
 }
 
 template <int MINB>
@@ -2733,7 +2774,7 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, cons
     k_row_keymult8b<8><<<std::min(grid, items8b), 128, kK8bSmem, st>>>(a, fwd_full);
     return;
   }
-  if (ver >= 7 && ver <= 15 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
+  if (ver >= 7 && ver <= 16 && a.D <= 3 && fwd_full) {  // 8 coefficients per thread
     const int items8 = (a.level + a.alpha) * (kR / kK8Rows) * a.batch;
     if (ver == 13 && !a.ts)
       launch_km8<8, false, 4>(a, fwd_full, items8, st);  // own / fold rows through cp.async into freed digit buffers
@@ -2741,6 +2782,14 @@ void row_keymult(const KeyMultLaunch& a, const uint2* tw2, cudaStream_t st, cons
       launch_km8<8, false, 5>(a, fwd_full, items8, st);  // next item's extension rows into each freed digit buffer
     else if (ver == 15 && !a.ts)
       launch_km8<7, false, 6>(a, fwd_full, items8, st);  // per-digit key slice + row twiddles by cp.async, 7 CTAs / SM
+    else if (ver == 16 && !a.ts) {  // the MACs after all digits' row passes (per digit count)
+      if (a.D == 3)
+        launch_km8<8, false, 7, 3>(a, fwd_full, items8, st);
+      else if (a.D == 2)
+        launch_km8<8, false, 7, 2>(a, fwd_full, items8, st);
+      else
+        launch_km8<8, false, 7, 1>(a, fwd_full, items8, st);
+    }
     else if (ver == 11)
       launch_km8<4, false, 3>(a, fwd_full, items8, st);  // key slice staged in shared memory per (row, tile), 4 CTAs / SM
     else if (ver == 9)

@@ -366,7 +366,7 @@ def test_batched_equals_unbatched():
         np.testing.assert_array_equal(hr[b], one)
 
 
-@pytest.mark.parametrize("km", ["8", "12", "13", "14", "15"])
+@pytest.mark.parametrize("km", ["8", "12", "13", "14", "15", "16"])
 @pytest.mark.parametrize("level,B", [(24, 6), (9, 8)])
 def test_batched_keymult_variants_equal_unbatched(km, level, B):
     """The fused row pass + KeyMult variants at batch B >= 4 (CK32_KM=12:
@@ -868,7 +868,7 @@ print("fused-intt ok")
 
 @pytest.mark.parametrize("level", [24, 7])
 @pytest.mark.parametrize("variant", ["CK32_ROW8=1", "CK32_KM=7", "CK32_KM=9", "CK32_KM=10", "CK32_KM=11", "CK32_TC=0",
-                                     "CK32_COL=3", "CK32_COL=4", "CK32_COL=5", "CK32_KM=12", "CK32_KM=13", "CK32_KM=14", "CK32_KM=15",
+                                     "CK32_COL=3", "CK32_COL=4", "CK32_COL=5", "CK32_KM=12", "CK32_KM=13", "CK32_KM=14", "CK32_KM=15", "CK32_KM=16",
                                      "CK32_TAIL_GATHER=1"])
 def test_variant_paths_match_oracle(level, variant):
     """Opt-in kernel variants (env switches read once per process: a fresh
