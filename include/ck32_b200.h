@@ -195,11 +195,20 @@ ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, do
  * lift uses the minimal prime prefix covering scale_log2 + 40 bits (as the
  * reference), multi-precision, up to 16 primes.  Precision contract: the
  * reference rounds Rational(v) / scale to double once; here the centred lift
- * is rounded to double and multiplied by 2^-scale_log2, so slots agree with
- * the reference's within 2^-40 (not bit for bit) at every scale
- * (tests/test_gpu_encode.py). */
+ * is rounded to double and multiplied by 2^-scale_log2: bit-identical to the
+ * reference at power-of-two scales, within 2^-40 otherwise -- use
+ * ck_decode_rational for bit-identical slots at every scale. */
 ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2, double* slots_dev,
                     ck_stream stream);
+/* decode with the scale as the exact rational num / den (32-bit limbs,
+ * little endian, at most 8 words each, num > 0; scale_log2 as above selects
+ * the prime prefix): every coefficient is the correctly rounded double of
+ * Rational(v) / scale, as the reference computes it (ckks.cpp:353), so the
+ * slots are bit-identical to the reference's decode at every scale
+ * (tests/test_gpu_encode.py).  CK_ERR_ARG for more than 8 words or num = 0. */
+ck_status ck_decode_rational(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2,
+                             const uint32_t* scale_num, uint32_t num_words, const uint32_t* scale_den,
+                             uint32_t den_words, double* slots_dev, ck_stream stream);
 
 /* Element-wise parts of decrypt / encrypt (ckks.cpp:497-553).  All operands
  * are evaluation-domain Montgomery rows (canonical); the randomness of

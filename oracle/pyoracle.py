@@ -298,6 +298,8 @@ class Reference:
                                                            ctypes.c_uint32, ctypes.c_int, _u32p, ctypes.c_size_t]
         lib.ref_decode.argtypes = [ctypes.c_uint32] * 4 + [_u32p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
                                                            _f64p]
+        lib.ref_decode_big.argtypes = [ctypes.c_uint32] * 4 + [_u32p, ctypes.c_uint32, _u32p, ctypes.c_uint32, _u32p,
+                                                               ctypes.c_uint32, _f64p]
         self.lib = lib
 
     def _check(self, rc):
@@ -347,8 +349,20 @@ class Reference:
     def decode(self, n, l, alpha, db, rows, level, num, den):
         """reference decode (ckks.cpp:321-362) of canonical evaluation-domain rows"""
         out = np.zeros(n, np.float64)
-        self._check(self.lib.ref_decode(n, l, alpha, db, np.ascontiguousarray(rows[:level], np.uint32), level,
-                                        num, den, out))
+        if num < 1 << 64 and den < 1 << 64:
+            self._check(self.lib.ref_decode(n, l, alpha, db, np.ascontiguousarray(rows[:level], np.uint32), level,
+                                            num, den, out))
+        else:  # multi-word scale (what chains of rescales produce)
+            def limbs(x):
+                w = []
+                while True:
+                    w.append(x & 0xFFFFFFFF)
+                    x >>= 32
+                    if not x:
+                        return np.array(w, np.uint32)
+            wn, wd = limbs(num), limbs(den)
+            self._check(self.lib.ref_decode_big(n, l, alpha, db, np.ascontiguousarray(rows[:level], np.uint32), level,
+                                                wn, len(wn), wd, len(wd), out))
         return out[0::2] + 1j * out[1::2]
 
     def mechanism_bench(self, op, n, l, alpha, db, level, reps, warmup, seed=42):

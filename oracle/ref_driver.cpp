@@ -369,7 +369,38 @@ int ref_encode(uint32_t n, uint32_t l, uint32_t alpha, uint32_t db, const double
 }
 
 // decode (ckks.cpp:321-362) of plaintext rows given as canonical residues
-// (evaluation domain, Montgomery); writes n/2 complex slots.
+// (evaluation domain, Montgomery); writes n/2 complex slots.  The scale is
+// num / den given as little-endian 32-bit limbs (ref_decode: 64-bit values).
+static BigInt from_limbs(const uint32_t* w, uint32_t nw) {
+  BigInt x = 0;
+  for (uint32_t i = nw; i-- > 0;) {
+    x <<= 32;
+    x += BigInt(w[i]);
+  }
+  return x;
+}
+int ref_decode_big(uint32_t n, uint32_t l, uint32_t alpha, uint32_t db, const uint32_t* rows, uint32_t level,
+                   const uint32_t* num, uint32_t nnum, const uint32_t* den, uint32_t nden, double* out) {
+  try {
+    CkksContext ctx(make_params(n, l, alpha, db, false));
+    Plaintext pt;
+    pt.scale = Rational(from_limbs(num, nnum)) / Rational(from_limbs(den, nden));
+    pt.level = level;
+    pt.poly = Polynomial(ctx.basis(), level, 0, Domain::Evaluation, true, &ctx.pool());
+    for (uint32_t i = 0; i < level; ++i)
+      for (uint32_t k = 0; k < n; ++k) pt.poly.row(i)[k] = static_cast<int32_t>(rows[static_cast<size_t>(i) * n + k]);
+    const auto z = decode(ctx, pt);
+    for (uint32_t t = 0; t < n / 2; ++t) {
+      out[2 * t] = z[t].real();
+      out[2 * t + 1] = z[t].imag();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 int ref_decode(uint32_t n, uint32_t l, uint32_t alpha, uint32_t db, const uint32_t* rows, uint32_t level,
                uint64_t num, uint64_t den, double* out) {
   try {

@@ -80,6 +80,7 @@ _SIGS = {
                                      ctypes.POINTER(_vp), _vp, _vp],
     "ck_encode": [_vp, _vp, _u32, ctypes.c_double, _u32, ctypes.c_int, _vp, _vp],
     "ck_decode": [_vp, _vp, _u32, ctypes.c_double, _vp, _vp],
+    "ck_decode_rational": [_vp, _vp, _u32, ctypes.c_double, _vp, _u32, _vp, _u32, _vp, _vp],
     "ck_decrypt": [_vp, _u32, _u32, _vp, _vp, _vp, _vp],
     "ck_encrypt_sk": [_vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp],
     "ck_encrypt_pk": [_vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -449,12 +449,29 @@ def encode(ctx: CkksContext, slots, scale: Fraction, level: int, p_extend: bool 
     return Plaintext(Polynomial(out, level, ctx.params.alpha if p_extend else 0), Fraction(scale), level)
 
 
+def _limbs32(x: int) -> list:
+    """little-endian 32-bit words of a non-negative integer (at least one)"""
+    out = []
+    while True:
+        out.append(x & 0xFFFFFFFF)
+        x >>= 32
+        if not x:
+            return out
+
+
 def decode(ctx: CkksContext, pt: Plaintext) -> np.ndarray:
     """decode (ckks.cpp:321-362) on the GPU -> n/2 complex slots (numpy)."""
     _check_eval_mont(pt.poly, "decode")
     out = torch.empty(ctx.n, dtype=torch.float64, device=ctx.device)
-    nat.call("ck_decode", ctx.handle, _ptr(pt.poly.data), pt.level, ctypes.c_double(log2_rational(pt.scale)),
-             _ptr(out), ctx.stream())
+    sc = Fraction(pt.scale)
+    num, den = _limbs32(sc.numerator), _limbs32(sc.denominator)
+    if len(num) <= 8 and len(den) <= 8:  # the exact rational: slots bit-identical to the reference's
+        nat.call("ck_decode_rational", ctx.handle, _ptr(pt.poly.data), pt.level,
+                 ctypes.c_double(log2_rational(pt.scale)), nat.u32_array(num), len(num), nat.u32_array(den), len(den),
+                 _ptr(out), ctx.stream())
+    else:
+        nat.call("ck_decode", ctx.handle, _ptr(pt.poly.data), pt.level, ctypes.c_double(log2_rational(pt.scale)),
+                 _ptr(out), ctx.stream())
     h = out.cpu().numpy()
     return h[0::2] + 1j * h[1::2]
 

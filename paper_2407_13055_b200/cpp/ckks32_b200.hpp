@@ -440,7 +440,19 @@ inline std::vector<std::complex<double>> decode(CkksContext& ctx, const Plaintex
   check(ck_malloc(ctx.raw(), (size_t)n / 2 * 16, &dz));
   std::vector<std::complex<double>> out(n / 2);
   try {
-    check(ck_decode(ctx.raw(), pt.data.data(), pt.level, scale_log2(pt.scale), static_cast<double*>(dz), ctx.stream()));
+    // the exact rational scale: slots bit-identical to the reference's decode (ckks.cpp:353)
+    detail::BigU num, den;
+    for (uint32_t f : pt.scale.num) num.mul(f);
+    for (uint32_t f : pt.scale.den) den.mul(f);
+    if (pt.scale.pow2 >= 0) num.shl(pt.scale.pow2);
+    else den.shl(-pt.scale.pow2);
+    if (num.w.size() <= 8 && den.w.size() <= 8)
+      check(ck_decode_rational(ctx.raw(), pt.data.data(), pt.level, scale_log2(pt.scale), num.w.data(),
+                               (uint32_t)num.w.size(), den.w.data(), (uint32_t)den.w.size(), static_cast<double*>(dz),
+                               ctx.stream()));
+    else
+      check(ck_decode(ctx.raw(), pt.data.data(), pt.level, scale_log2(pt.scale), static_cast<double*>(dz),
+                      ctx.stream()));
     check(ck_memcpy_d2h(ctx.raw(), out.data(), dz, out.size() * 16, ctx.stream()));
     check(ck_stream_sync(ctx.raw(), ctx.stream()));
   } catch (...) {

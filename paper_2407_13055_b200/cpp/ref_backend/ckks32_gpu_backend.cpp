@@ -741,8 +741,8 @@ Plaintext encode(CkksContext& ctx, std::span<const std::complex<double>> slots, 
   return pt;
 }
 
-// decode (ckks.cpp:321-362): slots within 2^-40 of the reference's (the GPU
-// rounds the centred CRT lift to double once, then scales by 2^-log2(scale))
+// decode (ckks.cpp:321-362): the exact rational scale goes to the GPU, which
+// rounds Rational(v) / scale to double once, as the reference: bit-identical slots
 std::vector<std::complex<double>> decode(CkksContext& ctx, const Plaintext& pt) {
   check_eval_mont(pt.poly, "decode");
   const uint32_t n = ctx.params().n;
@@ -753,7 +753,16 @@ std::vector<std::complex<double>> decode(CkksContext& ctx, const Plaintext& pt) 
   Gpu& g = for_ctx(ctx);
   Dev x(g.h, (size_t)pt.level * n), z(g.h, (size_t)n / 2 * 4);
   put_rows(g, pt.poly, 0, pt.level, x.u());
-  check(ck_decode(g.h, x.u(), pt.level, log2_rational(pt.scale), reinterpret_cast<double*>(z.u()), nullptr));
+  {  // the exact rational scale (the shim's limbs): slots bit-identical to the reference's
+    const BigInt sn = boost::multiprecision::numerator(pt.scale), sd = boost::multiprecision::denominator(pt.scale);
+    const auto& nl = sn.limbs();
+    const auto& dl = sd.limbs();
+    if (!nl.empty() && !dl.empty() && nl.size() <= 8 && dl.size() <= 8)
+      check(ck_decode_rational(g.h, x.u(), pt.level, log2_rational(pt.scale), nl.data(), (uint32_t)nl.size(), dl.data(),
+                               (uint32_t)dl.size(), reinterpret_cast<double*>(z.u()), nullptr));
+    else
+      check(ck_decode(g.h, x.u(), pt.level, log2_rational(pt.scale), reinterpret_cast<double*>(z.u()), nullptr));
+  }
   std::vector<std::complex<double>> out(n / 2);
   check(ck_memcpy_d2h(g.h, out.data(), z.u(), out.size() * 16, nullptr));
   check(ck_stream_sync(g.h, nullptr));

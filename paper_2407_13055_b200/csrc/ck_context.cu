@@ -2734,8 +2734,36 @@ ck_status ck_encode(ck_context* ctx, const double* slots_dev, uint32_t count, do
   return ck_ntt_forward(ctx, out_dev, (uint32_t)g.size(), g.data(), stream);
 }
 
+static ck_status decode_impl(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2,
+                             const RatScale& rs, double* slots_dev, ck_stream stream);
+
 ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2, double* slots_dev,
                     ck_stream stream) {
+  return decode_impl(ctx, pt_dev, level, scale_log2, RatScale{}, slots_dev, stream);
+}
+
+ck_status ck_decode_rational(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2,
+                             const uint32_t* scale_num, uint32_t num_words, const uint32_t* scale_den,
+                             uint32_t den_words, double* slots_dev, ck_stream stream) {
+  RatScale rs;
+  const ck_status st = guard([&] {
+    check_ptr(scale_num);
+    check_ptr(scale_den);
+    if (num_words == 0 || den_words == 0 || num_words > (uint32_t)kMaxRat || den_words > (uint32_t)kMaxRat)
+      throw InvalidArgument("decode: scale numerator / denominator must have 1..8 32-bit words");
+    bool nz = false, dz = false;
+    for (uint32_t i = 0; i < num_words; ++i) nz |= (rs.num[i] = scale_num[i]) != 0;
+    for (uint32_t i = 0; i < den_words; ++i) dz |= (rs.den[i] = scale_den[i]) != 0;
+    if (!nz || !dz) throw InvalidArgument("decode: scale must be a positive rational");
+    rs.nnum = (int)num_words;
+    rs.nden = (int)den_words;
+  });
+  if (st != CK_OK) return st;
+  return decode_impl(ctx, pt_dev, level, scale_log2, rs, slots_dev, stream);
+}
+
+static ck_status decode_impl(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, double scale_log2,
+                             const RatScale& rs, double* slots_dev, ck_stream stream) {
   return guard([&] {
     CK_RANGE("ck_decode");
     Context* c = C(ctx);
@@ -2761,7 +2789,7 @@ ck_status ck_decode(ck_context* ctx, const uint32_t* pt_dev, uint32_t level, dou
     for (uint32_t i = 0; i < cnt; ++i) g[i] = i;
     const ck_status si = ck_intt_inverse(ctx, rows, cnt, g.data(), nullptr, stream);
     if (si != CK_OK) throw std::runtime_error(ck_last_error());
-    dec_crt((int)N, rows, c->crt_const(cnt), c->d_twist_dec, std::exp2(-scale_log2), a, st);
+    dec_crt((int)N, rows, c->crt_const(cnt), c->d_twist_dec, std::exp2(-scale_log2), a, st, rs);
     fft_pow2_dev((int)c->logn, a, a + N, c->d_fft_fwd, st);
     dec_gather((int)N, a + N, c->d_jidx, reinterpret_cast<double2*>(slots_dev), st);
     c->launches += 3 + (c->logn > 12 ? c->logn - 12 : 0);

@@ -138,8 +138,16 @@ void enc_scatter(int n, const double2* slots, int count, const uint32_t* jidx, d
 // scale = scale_mant * 2^scale_exp: the reference's long double scale (64-bit significand)
 void enc_round(int n, const double2* a, const double2* twist, unsigned long long scale_mant, int scale_exp, int rows,
                const uint32_t* row_q, uint32_t* out, cudaStream_t st);
+// decode's scale as an exact rational num / den (32-bit limbs, little endian):
+// the coefficient is then the correctly rounded double of v * den / num, as
+// the reference's static_cast<double>(Rational(v) / scale) (ckks.cpp:353)
+constexpr int kMaxRat = 8;
+struct RatScale {
+  uint32_t num[kMaxRat] = {}, den[kMaxRat] = {};
+  int nnum = 0, nden = 0;  // 0 words: use inv_scale (power-of-two scales are exact either way)
+};
 void dec_crt(int n, const uint32_t* rows, const CrtConst* cc_dev, const double2* twist, double inv_scale, double2* a,
-             cudaStream_t st);
+             cudaStream_t st, const RatScale& rs = RatScale{});
 void dec_gather(int n, const double2* a, const uint32_t* jidx, double2* out, cudaStream_t st);
 
 // tensor product of two ciphertexts (ckks.cpp:818-821): d0 = b b', d1 = b a' + a b', d2 = a a'

@@ -153,9 +153,134 @@ __device__ __forceinline__ double limbs_to_double(const uint32_t* v, int nl) {
   return ldexp(__ull2double_rn(w), lo);
 }
 
+// ---- correctly rounded |v| * den / num (the reference's
+// static_cast<double>(Rational(v) / scale), ckks.cpp:353, with the round-to-
+// nearest-even conversion of the oracle's Boost shim)
+constexpr int kMaxA = kMaxCrt + 1 + kMaxRat + 1;
+
+__device__ __forceinline__ int bitlen_w(const uint32_t* x, int n) {
+  for (int i = n - 1; i >= 0; --i)
+    if (x[i]) return 32 * i + 32 - __clz(x[i]);
+  return 0;
+}
+
+// q = floor(u / v), returns whether the remainder is nonzero; u has nu words
+// (destroyed), v has nv >= 1 words with v[nv-1] != 0, the quotient fits in 64
+// bits (Knuth, TAOCP 4.3.1 algorithm D, 32-bit digits)
+__device__ uint64_t divmod_small_q(uint32_t* u, int nu, const uint32_t* v, int nv, bool& rem_nz) {
+  uint64_t q = 0;
+  if (nv == 1) {
+    uint64_t r = 0;
+    for (int j = nu - 1; j >= 0; --j) {
+      const uint64_t t = (r << 32) | u[j];
+      const uint64_t d = t / v[0];
+      r = t - d * v[0];
+      if (j < 2) q |= d << (32 * j);
+    }
+    rem_nz = r != 0;
+    return q;
+  }
+  const int sh = __clz(v[nv - 1]);
+  uint32_t vn[kMaxRat], un[kMaxA + 1];
+  for (int i = nv - 1; i > 0; --i) vn[i] = (v[i] << sh) | (sh ? (uint32_t)((uint64_t)v[i - 1] >> (32 - sh)) : 0u);
+  vn[0] = v[0] << sh;
+  un[nu] = sh ? (uint32_t)((uint64_t)u[nu - 1] >> (32 - sh)) : 0u;
+  for (int i = nu - 1; i > 0; --i) un[i] = (u[i] << sh) | (sh ? (uint32_t)((uint64_t)u[i - 1] >> (32 - sh)) : 0u);
+  un[0] = u[0] << sh;
+  for (int j = nu - nv; j >= 0; --j) {
+    const uint64_t top = ((uint64_t)un[j + nv] << 32) | un[j + nv - 1];
+    uint64_t qhat = top / vn[nv - 1], rhat = top - qhat * vn[nv - 1];
+    while (qhat >> 32 || qhat * vn[nv - 2] > ((rhat << 32) | un[j + nv - 2])) {
+      --qhat;
+      rhat += vn[nv - 1];
+      if (rhat >> 32) break;
+    }
+    int64_t borrow = 0;
+    uint64_t carry = 0;
+    for (int i = 0; i < nv; ++i) {
+      const uint64_t p = qhat * vn[i] + carry;
+      carry = p >> 32;
+      const int64_t t = (int64_t)un[i + j] - (int64_t)(uint32_t)p - borrow;
+      un[i + j] = (uint32_t)t;
+      borrow = t < 0;
+    }
+    const int64_t t = (int64_t)un[j + nv] - (int64_t)carry - borrow;
+    un[j + nv] = (uint32_t)t;
+    if (t < 0) {  // qhat one too large: add back
+      --qhat;
+      uint64_t c = 0;
+      for (int i = 0; i < nv; ++i) {
+        const uint64_t s2 = (uint64_t)un[i + j] + vn[i] + c;
+        un[i + j] = (uint32_t)s2;
+        c = s2 >> 32;
+      }
+      un[j + nv] += (uint32_t)c;
+    }
+    if (j < 2) q |= qhat << (32 * j);
+  }
+  rem_nz = false;
+  for (int i = 0; i < nv; ++i) rem_nz |= un[i] != 0;
+  return q;
+}
+
+__device__ double rat_to_double(const uint32_t* acc, int nl, const RatScale& rs) {
+  uint32_t A[kMaxA];
+  const int na = nl + rs.nden;
+  for (int i = 0; i < na; ++i) A[i] = 0;
+  for (int i = 0; i < nl; ++i) {  // A = |v| * den
+    uint64_t carry = 0;
+    for (int j = 0; j < rs.nden; ++j) {
+      const uint64_t t = (uint64_t)acc[i] * rs.den[j] + A[i + j] + carry;
+      A[i + j] = (uint32_t)t;
+      carry = t >> 32;
+    }
+    A[i + rs.nden] = (uint32_t)carry;
+  }
+  const int nb = bitlen_w(A, na);
+  if (nb == 0) return 0.0;
+  const int db = bitlen_w(rs.num, rs.nnum);
+  const int shift = 55 - (nb - db);  // the quotient gets 55 or 56 significant bits
+  uint32_t U[kMaxA + 2];
+  bool sticky = false;
+  int nu;
+  if (shift >= 0) {  // U = A << shift
+    const int ws = shift >> 5, bs = shift & 31;
+    nu = (nb + shift + 31) >> 5;
+    for (int i = 0; i < nu; ++i) {
+      const int src = i - ws;
+      const uint32_t hi = (src >= 0 && src < na) ? A[src] : 0u;
+      const uint32_t lo = (src - 1 >= 0 && src - 1 < na) ? A[src - 1] : 0u;
+      U[i] = bs ? (hi << bs) | (lo >> (32 - bs)) : hi;
+    }
+  } else {  // U = A >> k, sticky = the bits shifted out (floor(floor(A / 2^k) / num) = floor(A / (num 2^k)))
+    const int k = -shift, ws = k >> 5, bs = k & 31;
+    for (int i = 0; i < ws && i < na; ++i) sticky |= A[i] != 0;
+    if (bs && ws < na) sticky |= (A[ws] & ((1u << bs) - 1)) != 0;
+    nu = (nb - k + 31) >> 5;
+    for (int i = 0; i < nu; ++i) {
+      const int src = i + ws;
+      const uint32_t lo = src < na ? A[src] : 0u;
+      const uint32_t hi = src + 1 < na ? A[src + 1] : 0u;
+      U[i] = bs ? (lo >> bs) | (hi << (32 - bs)) : lo;
+    }
+  }
+  int nv = rs.nnum;
+  while (nv > 1 && rs.num[nv - 1] == 0) --nv;
+  // U has db + 55 bits, so nu >= nv always (the quotient has 55 or 56 bits)
+  bool rnz = false;
+  const uint64_t qv = divmod_small_q(U, nu, rs.num, nv, rnz);
+  sticky |= rnz;
+  const int extra = (64 - __clzll(qv)) - 53;  // 2 or 3
+  uint64_t mant = qv >> extra;
+  const uint64_t rem = qv & ((1ull << extra) - 1), half = 1ull << (extra - 1);
+  if (rem > half || (rem == half && (sticky || (mant & 1)))) ++mant;
+  return ldexp((double)mant, extra - shift);
+}
+
 // CRT lift (multi-precision), centred, / scale, twisted: a_k = coeff (cos, sin)(pi k / n)
 __global__ void k_dec_crt(int n, const uint32_t* __restrict__ rows, const CrtConst* __restrict__ ccp,
-                          const double2* __restrict__ twist, double inv_scale, double2* __restrict__ a) {
+                          const double2* __restrict__ twist, double inv_scale, double2* __restrict__ a,
+                          const __grid_constant__ RatScale rs) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const CrtConst& cc = *ccp;
@@ -216,9 +341,15 @@ __global__ void k_dec_crt(int n, const uint32_t* __restrict__ rows, const CrtCon
       borrow = s < 0;
     }
   }
-  double coeff = limbs_to_double(acc, nl);
-  if (neg) coeff = -coeff;
-  coeff = __dmul_rn(coeff, inv_scale);
+  double coeff;
+  if (rs.nnum > 0) {  // one correctly rounded division by the exact rational scale
+    coeff = rat_to_double(acc, nl, rs);
+    if (neg) coeff = -coeff;
+  } else {  // |v| rounded once, times 2^-log2(scale): exact for power-of-two scales
+    coeff = limbs_to_double(acc, nl);
+    if (neg) coeff = -coeff;
+    coeff = __dmul_rn(coeff, inv_scale);
+  }
   const double2 tw = twist[k];
   a[k] = make_double2(__dmul_rn(coeff, tw.x), __dmul_rn(coeff, tw.y));
 }
@@ -256,8 +387,8 @@ void enc_round(int n, const double2* a, const double2* twist, unsigned long long
 }
 
 void dec_crt(int n, const uint32_t* rows, const CrtConst* cc_dev, const double2* twist, double inv_scale, double2* a,
-             cudaStream_t st) {
-  k_dec_crt<<<cdiv(n, 128), 128, 0, st>>>(n, rows, cc_dev, twist, inv_scale, a);
+             cudaStream_t st, const RatScale& rs) {
+  k_dec_crt<<<cdiv(n, 128), 128, 0, st>>>(n, rows, cc_dev, twist, inv_scale, a, rs);
 }
 
 void dec_gather(int n, const double2* a, const uint32_t* jidx, double2* out, cudaStream_t st) {

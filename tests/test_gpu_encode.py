@@ -4,8 +4,10 @@ reference itself (oracle/_ref, built read-only from /root/reference).
 * encode at any scale: plaintext residues bit-identical to the reference
   (the FFT replays the reference's operation order and twiddles, the final
   scaling replays its 80-bit long double rounding);
-* decode: slots within 2^-40 of the reference's decode of the same plaintext
-  (floating-point output; the only freedom is the Rational->double rounding);
+* decode: slots bit-identical to the reference's decode of the same plaintext
+  at every scale (ck_decode_rational: Rational(v) / scale rounded to double
+  once on the GPU, as ckks.cpp:353); the scale_log2-only entry point
+  ck_decode is bit-identical at power-of-two scales and within 2^-40 otherwise;
 * round trip and the reference's argument errors."""
 from __future__ import annotations
 
@@ -78,8 +80,7 @@ def test_decode_matches_reference(ref, n, l, a, level):
     pt = ckks.Plaintext(ckks.Polynomial(torch.from_numpy(rows.astype(np.int64).astype(np.int32)).cuda(), level, 0),
                         Fraction(1 << 55), level)
     got = ckks.decode(C, pt)
-    err = np.abs(got - want).max()
-    assert err <= 2.0 ** -40, err
+    np.testing.assert_array_equal(got, want)  # bit for bit
     assert np.abs(got - z).max() < 2.0 ** -30
 
 
@@ -106,10 +107,10 @@ def test_encode_errors_mirror_reference():
 def test_decode_matches_reference_at_non_power_of_two_scale(ref, num, den):
     """decode at scales that are not powers of two (what a rescale leaves,
     Delta^2 / (q q')): the reference divides the exact CRT value by the exact
-    Rational scale and rounds once (ckks.cpp:345-353); the GPU multiplies the
-    double-rounded value by 2^-log2(scale), so agreement is to 2^-40 here,
-    not bit for bit (at power-of-two scales the two coincide up to the same
-    bound, test_decode_matches_reference)."""
+    Rational scale and rounds once (ckks.cpp:345-353); so does the GPU
+    (ck_decode_rational: multi-precision v * den / num, 55-bit quotient,
+    round to nearest even with a sticky bit) -- bit for bit.  The legacy
+    ck_decode (scale_log2 only: double-rounded) stays within 2^-40."""
     n, l, a, level = 65536, 24, 8, 24
     C = ctx_for(n, l, a)
     z = unit_slots(n // 2, 31 + num % 101)
@@ -118,4 +119,31 @@ def test_decode_matches_reference_at_non_power_of_two_scale(ref, num, den):
     pt = ckks.Plaintext(ckks.Polynomial(torch.from_numpy(rows.astype(np.int64).astype(np.int32)).cuda(), level, 0),
                         Fraction(num, den), level)
     got = ckks.decode(C, pt)
-    assert np.abs(got - want).max() <= 2.0 ** -40
+    np.testing.assert_array_equal(got, want)  # bit for bit
+    # the scale_log2-only entry point: one more rounding, within 2^-40
+    import ctypes
+    from paper_2407_13055_b200 import _native as nat
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    nat.call("ck_decode", C.handle, pt.poly.data.data_ptr(), level, ctypes.c_double(ckks.log2_rational(pt.scale)),
+             out.data_ptr(), C.stream())
+    h = out.cpu().numpy()
+    assert np.abs((h[0::2] + 1j * h[1::2]) - want).max() <= 2.0 ** -40
+
+
+@pytest.mark.parametrize("level,num,den", [
+    (24, 1 << 110, 268369921 * 268238849),          # Delta^2 / (q q') after one rescale (prime-like den)
+    (22, (1 << 55) * 3 * 5 * 7 * 11 * 13, 1 << 40),  # den a power of two, odd numerator
+    (9, 2 ** 64 + 13, 2 ** 96 + 1),                  # multi-word numerator and denominator
+    (4, 1 << 20, 1),                                 # small scale, few primes in the prefix
+])
+def test_decode_bit_exact_at_rescaled_and_multiword_scales(ref, level, num, den):
+    """Exact decode over scales a chain of rescales produces (multi-word
+    numerators / denominators), against the reference on the same rows."""
+    n, l, a = 65536, 24, 8
+    C = ctx_for(n, l, a)
+    rng = np.random.default_rng(level + den % 97)
+    rows = np.stack([rng.integers(0, int(C.primes[i]), n, dtype=np.int64) for i in range(level)]).astype(np.uint32)
+    want = ref.decode(n, l, a, 55, rows, level, num, den)
+    pt = ckks.Plaintext(ckks.Polynomial(torch.from_numpy(rows.astype(np.int64).astype(np.int32)).cuda(), level, 0),
+                        Fraction(num, den), level)
+    np.testing.assert_array_equal(ckks.decode(C, pt), want)
