@@ -122,13 +122,21 @@ ck_status ck_automorphism_galois(ck_context* ctx, const uint32_t* in_dev, uint32
 /* ew_add / ew_sub / ew_mul (op 0 / 1 / 2, poly.cpp:121-164) over a polynomial
  * of q_rows Q-prefix rows then p_rows P rows (P-extended operands as the
  * reference accepts them); out may alias a or b (ew_add_inplace /
- * ew_sub_inplace, poly.cpp:182-205). */
+ * ew_sub_inplace, poly.cpp:182-205).  Ops 4 / 5 / 6: the same in the
+ * reference's raw representation -- int32 values in (-q, q) as its
+ * Polynomial rows hold them, its narrow() and signed Montgomery reduction,
+ * bit for bit (for callers that compare raw rows; every other entry point
+ * takes and returns canonical residues). */
 ck_status ck_ew_binary(ck_context* ctx, int op, const uint32_t* a, const uint32_t* b, uint32_t* out, uint32_t q_rows,
                        uint32_t p_rows, ck_stream stream);
 /* ew_mul_const (poly.hpp:127-128): row i times consts_mont[i] (host array of
  * q_rows + p_rows canonical Montgomery constants); out may alias a. */
 ck_status ck_ew_mul_const(ck_context* ctx, const uint32_t* a, const uint32_t* consts_mont, uint32_t* out,
                           uint32_t q_rows, uint32_t p_rows, ck_stream stream);
+/* ew_mul_const in the reference's raw representation (as ops 4-6 above;
+ * the constants are taken as the reference reads them, unreduced). */
+ck_status ck_ew_mul_const_raw(ck_context* ctx, const uint32_t* a, const uint32_t* consts_mont, uint32_t* out,
+                              uint32_t q_rows, uint32_t p_rows, ck_stream stream);
 /* bconv_part2 (bconv.cpp:96-174) with the caller's BConvTable::c (centred
  * Montgomery constants, [dst_count][src_count], bconv.hpp:20-22) instead of
  * the library's own table: src canonical (coefficient domain) rows. */

@@ -426,18 +426,30 @@ void apply_automorphism_inplace(Polynomial& p, const AutomorphismMap& map) {
 
 // element-wise (poly.cpp:121-205)
 namespace {
+// The element-wise ops keep the reference's raw representation (ops 4-6 of
+// ck_ew_binary: its signed lazy int32 values and formulas, bit for bit), so
+// callers that compare raw rows (test_poly.cpp:41, :112) see what the CPU
+// code would have produced.
+Dev up_raw(const Gpu& g, const Polynomial& p) {
+  Dev d(g.h, (size_t)p.rows() * p.n());
+  if (p.rows()) {
+    check(ck_memcpy_h2d(g.h, d.u(), p.row(0), (size_t)p.rows() * p.n() * 4, nullptr));
+    check(ck_stream_sync(g.h, nullptr));
+  }
+  return d;
+}
 Polynomial ew(int op, const Polynomial& a, const Polynomial& b, BufferPool* pool, bool mont_out) {
   check_binary(a, b);
   Gpu& g = for_basis(*a.basis());
-  Dev x = up(g, a), y = up(g, b);
-  check(ck_ew_binary(g.h, op, x.u(), y.u(), x.u(), a.q_count(), a.p_count(), nullptr));
+  Dev x = up_raw(g, a), y = up_raw(g, b);
+  check(ck_ew_binary(g.h, op + 4, x.u(), y.u(), x.u(), a.q_count(), a.p_count(), nullptr));
   return down(g, x.u(), a.basis(), a.q_count(), a.p_count(), a.domain(), mont_out, pool);
 }
 void ew_inplace(int op, Polynomial& a, const Polynomial& b) {
   check_binary(a, b);
   Gpu& g = for_basis(*a.basis());
-  Dev x = up(g, a), y = up(g, b);
-  check(ck_ew_binary(g.h, op, x.u(), y.u(), x.u(), a.q_count(), a.p_count(), nullptr));
+  Dev x = up_raw(g, a), y = up_raw(g, b);
+  check(ck_ew_binary(g.h, op + 4, x.u(), y.u(), x.u(), a.q_count(), a.p_count(), nullptr));
   get_rows(g, x.u(), a, 0, a.rows());
 }
 }  // namespace
@@ -451,8 +463,8 @@ Polynomial ew_mul(const Polynomial& a, const Polynomial& b, BufferPool* pool) {
 Polynomial ew_mul_const(const Polynomial& a, std::span<const uint32_t> consts_mont, BufferPool* pool) {
   if (consts_mont.size() != a.rows()) throw std::invalid_argument("constant count mismatch");
   Gpu& g = for_basis(*a.basis());
-  Dev x = up(g, a);
-  check(ck_ew_mul_const(g.h, x.u(), consts_mont.data(), x.u(), a.q_count(), a.p_count(), nullptr));
+  Dev x = up_raw(g, a);
+  check(ck_ew_mul_const_raw(g.h, x.u(), consts_mont.data(), x.u(), a.q_count(), a.p_count(), nullptr));
   return down(g, x.u(), a.basis(), a.q_count(), a.p_count(), a.domain(), a.mont(), pool);
 }
 void ew_add_inplace(Polynomial& a, const Polynomial& b) { ew_inplace(0, a, b); }

@@ -2345,7 +2345,8 @@ ck_status ck_ew_binary(ck_context* ctx, int op, const uint32_t* a, const uint32_
     check_ptr(a);
     check_ptr(b);
     check_ptr(out);
-    if (op < 0 || op > 2) throw InvalidArgument("element-wise op must be 0 (add), 1 (sub) or 2 (mul)");
+    if (op < 0 || op > 6 || op == 3)
+      throw InvalidArgument("element-wise op must be 0 (add), 1 (sub), 2 (mul) or 4 / 5 / 6 (raw add / sub / mul)");
     elementwise((int)c->n, (int)(q_rows + p_rows), 1, op, a, 0, b, 0, out, 0, c->poly_row_primes(q_rows, p_rows),
                 c->d_primes, S(stream));
     ++c->launches;
@@ -2353,8 +2354,18 @@ ck_status ck_ew_binary(ck_context* ctx, int op, const uint32_t* a, const uint32_
   });
 }
 
+static ck_status ew_mul_const_impl(ck_context* ctx, const uint32_t* a, const uint32_t* consts_mont, uint32_t* out,
+                                   uint32_t q_rows, uint32_t p_rows, ck_stream stream, bool raw);
 ck_status ck_ew_mul_const(ck_context* ctx, const uint32_t* a, const uint32_t* consts_mont, uint32_t* out,
                           uint32_t q_rows, uint32_t p_rows, ck_stream stream) {
+  return ew_mul_const_impl(ctx, a, consts_mont, out, q_rows, p_rows, stream, false);
+}
+ck_status ck_ew_mul_const_raw(ck_context* ctx, const uint32_t* a, const uint32_t* consts_mont, uint32_t* out,
+                              uint32_t q_rows, uint32_t p_rows, ck_stream stream) {
+  return ew_mul_const_impl(ctx, a, consts_mont, out, q_rows, p_rows, stream, true);
+}
+static ck_status ew_mul_const_impl(ck_context* ctx, const uint32_t* a, const uint32_t* consts_mont, uint32_t* out,
+                                   uint32_t q_rows, uint32_t p_rows, ck_stream stream, bool raw) {
   return guard([&] {
     CK_RANGE("ck_ew_mul_const");
     Context* c = C(ctx);
@@ -2366,12 +2377,12 @@ ck_status ck_ew_mul_const(ck_context* ctx, const uint32_t* a, const uint32_t* co
     std::vector<uint32_t> k(rows);
     for (uint32_t i = 0; i < rows; ++i) {
       const uint32_t q = c->q(i < q_rows ? i : c->L + (i - q_rows));
-      k[i] = consts_mont[i] % q;  // canonical, poly.hpp:121-122
+      k[i] = raw ? consts_mont[i] : consts_mont[i] % q;  // canonical, poly.hpp:121-122 (raw: as the reference reads it)
     }
     uint32_t* d = nullptr;  // stream-ordered: safe for concurrent calls on other streams
     CK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), rows * 4, S(stream)));
     CK_CUDA(cudaMemcpyAsync(d, k.data(), rows * 4, cudaMemcpyHostToDevice, S(stream)));
-    elementwise((int)c->n, (int)rows, 1, 3, a, 0, a, 0, out, 0, rp, c->d_primes, S(stream), 0, d);
+    elementwise((int)c->n, (int)rows, 1, raw ? 7 : 3, a, 0, a, 0, out, 0, rp, c->d_primes, S(stream), 0, d);
     CK_CUDA(cudaFreeAsync(d, S(stream)));  // (a pageable-source copy has staged k before returning)
     ++c->launches;
     check_launch();

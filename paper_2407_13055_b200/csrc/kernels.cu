@@ -465,7 +465,9 @@ __global__ void __launch_bounds__(kT) k_hrot_tail4(int n, int level, const uint3
 
 // ------------------------------------------------------------ elementwise --
 // op 0 add, 1 sub, 2 Montgomery mul (poly.cpp:146-164), 3 multiply row i by
-// the canonical Montgomery constant rc[i] (ew_mul_const, poly.cpp:166-180).
+// the canonical Montgomery constant rc[i] (ew_mul_const, poly.cpp:166-180);
+// ops 4 / 5 / 6 / 7: the same four in the reference's raw representation
+// (signed lazy int32 in (-q, q): narrow() and signed Montgomery, bit for bit).
 // o may alias a or b (ew_add_inplace / ew_sub_inplace, poly.cpp:182-205):
 // every thread reads its 4 words of each operand before writing them.
 __global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_t* a, uint64_t a_bs,
@@ -480,6 +482,34 @@ __global__ void __launch_bounds__(kT) k_elementwise(int n, int op, const uint32_
   const size_t r = (size_t)i * n + xo;
   const uint4 x = *reinterpret_cast<const uint4*>(a + b * a_bs + r);
   uint4 z;
+  if (op >= 4) {  // raw: the reference's signed lazy int32 formulas (poly.cpp:121-180, modarith.hpp:20-36)
+    const int32_t q = (int32_t)P.q;
+    auto narrow = [&](int64_t v) -> uint32_t {
+      if (v >= q) v -= q;
+      else if (v <= -q) v += q;
+      return (uint32_t)(int32_t)v;
+    };
+    auto mred = [&](int64_t v) -> uint32_t {  // signed Montgomery, (-q, q)
+      const int32_t hi = (int32_t)(v >> 32), t = (int32_t)((uint32_t)v * P.qinv);
+      return (uint32_t)(hi - (int32_t)(((int64_t)t * q) >> 32));
+    };
+    const int32_t* xs = reinterpret_cast<const int32_t*>(&x);
+    uint32_t* zs = reinterpret_cast<uint32_t*>(&z);
+    if (op == 7) {
+      const int32_t c = (int32_t)rc[i];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) zs[e] = mred((int64_t)xs[e] * c);
+    } else {
+      const uint4 y = *reinterpret_cast<const uint4*>(bp + b * b_bs + r);
+      const int32_t* ys = reinterpret_cast<const int32_t*>(&y);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        zs[e] = op == 4 ? narrow((int64_t)xs[e] + ys[e]) : op == 5 ? narrow((int64_t)xs[e] - ys[e])
+                                                                   : mred((int64_t)xs[e] * ys[e]);
+    }
+    *reinterpret_cast<uint4*>(o + b * o_bs + r) = z;
+    return;
+  }
   if (op == 3) {
     const uint32_t c = rc[i];
     z = make_uint4(sub_if(mont_mul(x.x, c, P.q, P.qinv), P.q), sub_if(mont_mul(x.y, c, P.q, P.qinv), P.q),

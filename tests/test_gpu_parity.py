@@ -924,3 +924,44 @@ print("variant ok")
     env = dict(__import__("os").environ, **{k: v})
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("level,p_rows", [(8, 0), (5, 3)])
+def test_ew_raw_representation_matches_reference_formulas(level, p_rows):
+    """ck_ew_binary ops 4 / 5 / 6 and ck_ew_mul_const_raw: the reference's
+    raw signed lazy int32 arithmetic (poly.cpp:121-180: narrow() after the
+    add / sub, signed Montgomery mont_mul, modarith.hpp:20-36) bit for bit on
+    values in (-q, q), restated here in numpy."""
+    import ctypes
+    from paper_2407_13055_b200 import _native as nat
+
+    n, l, a = 1024, 8, 3
+    C = ctx_for(n, l, a, 55)
+    rows = list(range(level)) + [l + j for j in range(p_rows)]
+    q = np.array([int(C.primes[g]) for g in rows], np.int64)[:, None]
+    rng = np.random.default_rng(level * 7 + p_rows)
+    x = rng.integers(-q + 1, q, (len(rows), n))
+    y = rng.integers(-q + 1, q, (len(rows), n))
+    qinv = np.array([pow(int(v), -1, 1 << 32) for v in q[:, 0]], np.int64)[:, None]
+
+    def narrow(v):
+        return np.where(v >= q, v - q, np.where(v <= -q, v + q, v))
+
+    def mred(v):  # modarith.hpp:20-29 on int64 numpy values
+        hi = v >> 32
+        t = ((v & 0xFFFFFFFF) * qinv) & 0xFFFFFFFF
+        t = np.where(t >= 1 << 31, t - (1 << 32), t)
+        return hi - ((t * q) >> 32)
+
+    dx = torch.from_numpy(x.astype(np.int32)).cuda()
+    dy = torch.from_numpy(y.astype(np.int32)).cuda()
+    for op, want in ((4, narrow(x + y)), (5, narrow(x - y)), (6, mred(x * y))):
+        out = torch.empty_like(dx)
+        nat.call("ck_ew_binary", C.handle, op, dx.data_ptr(), dy.data_ptr(), out.data_ptr(), level, p_rows, C.stream())
+        np.testing.assert_array_equal(out.cpu().numpy().astype(np.int64), want, err_msg=f"op {op}")
+    consts = rng.integers(0, 1 << 31, len(rows))
+    out = torch.empty_like(dx)
+    nat.call("ck_ew_mul_const_raw", C.handle, dx.data_ptr(), nat.u32_array(consts), out.data_ptr(), level, p_rows,
+             C.stream())
+    c32 = np.where(consts >= 1 << 31, consts - (1 << 32), consts)[:, None]
+    np.testing.assert_array_equal(out.cpu().numpy().astype(np.int64), mred(x * c32))

@@ -11,13 +11,17 @@ are weakened), so every hot-path call a reference caller makes runs on the
 GPU.  The binaries are built in the build container (they need the
 reference headers) and travel to the GPU box under _lib/ref_gpu.
 
-Expected differences, and only these: four unit cases compare RAW int32
-residues of the GPU's output with the CPU's lazy signed representation
-(ew_add(p, 0) == p, the CPU pipeline vs GPU sequential ops, the serial CPU
-NTT vs the plan, the bench's plan-vs-serial check).  The GPU returns the
+Expected differences, and only these: two unit cases compare the RAW int32
+output of the GPU NTT with the CPU's serial transform in its lazy signed
+representation (test_ntt.cpp:203/227 "all valid plans are bit-identical",
+test_bench.cpp:88 the bench's plan-vs-serial check).  The GPU returns the
 canonical [0, q) representative of the same residue (every correct()-based
-check of those values passes); raw int32 equality with the CPU's schedule is
-outside the parity contract.  Acceptance criterion 10
+check of those values passes); raw int32 equality with the CPU's NTT
+schedule is outside the parity contract.  The element-wise
+ops (ew_add / ew_sub / ew_mul / ew_mul_const) run in the reference's raw
+representation (ck_ew_binary ops 4-6, ck_ew_mul_const_raw), so
+test_poly.cpp:41 (ew_add(p, 0) == p) and :112 (the CPU pipeline vs the
+GPU's sequential ops) pass bit for bit.  Acceptance criterion 10
 drives the reference's bench CLI, which needs CLI11 (absent, out of scope).
 """
 from __future__ import annotations
@@ -35,12 +39,10 @@ BIN = Path(__file__).resolve().parent.parent / "paper_2407_13055_b200" / "_lib" 
 
 # raw-int32 comparisons against the CPU's lazy representation (see module doc)
 RAW_CASES = {
-    "ew_add/ew_sub identities",                                            # test_poly.cpp:41
-    "fused pipeline equals sequential stages bit-exactly",                 # test_poly.cpp:112
     "all valid plans are bit-identical, including OT and serial reference",  # test_ntt.cpp:203,227
     "bench: ntt-compare times plan and serial reference",                  # test_bench.cpp:88
 }
-RAW_LINES = {"test_poly.cpp:41", "test_poly.cpp:112", "test_ntt.cpp:203", "test_ntt.cpp:227", "test_bench.cpp:88"}
+RAW_LINES = {"test_ntt.cpp:203", "test_ntt.cpp:227", "test_bench.cpp:88"}
 
 
 def _run(exe, *args, timeout):
