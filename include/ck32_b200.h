@@ -99,6 +99,18 @@ ck_status ck_ntt_forward(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, con
  * or NULL. */
 ck_status ck_intt_inverse(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
                           const uint32_t* epilogue_mont, ck_stream stream);
+/* The reference's NTT / INTT in its RAW representation (ntt.cpp:15-96):
+ * int32 rows as its Polynomial holds them (signed lazy values), its signed
+ * Montgomery butterflies, (-2q, 2q) narrowing, forward entry merge and
+ * tightened last stage, inverse exit constants (+ epilogue, canonical) --
+ * butterfly for butterfly, so the rows equal the reference's
+ * forward_row_serial / inverse_row_serial (and every NttPlan of it).  A
+ * compatibility mode for callers that compare raw rows: one launch per
+ * stage, untuned; the entry points above are the fast path. */
+ck_status ck_ntt_forward_raw(ck_context* ctx, int32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
+                             ck_stream stream);
+ck_status ck_intt_inverse_raw(ck_context* ctx, int32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
+                              const uint32_t* epilogue_mont, ck_stream stream);
 /* make_bconv_table + bconv_part2 (bconv.cpp:13-46, 96-174): src is src_count
  * contiguous canonical rows (coefficient domain), dst dst_count rows. */
 ck_status ck_bconv(ck_context* ctx, const uint32_t* src_dev, uint32_t src_count, const uint32_t* src_gidx,

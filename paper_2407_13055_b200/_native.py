@@ -62,6 +62,8 @@ _SIGS = {
     "ck_ew_binary": [_vp, ctypes.c_int, _vp, _vp, _vp, _u32, _u32, _vp],
     "ck_ew_mul_const": [_vp, _vp, _u32p, _vp, _u32, _u32, _vp],
     "ck_ew_mul_const_raw": [_vp, _vp, _u32p, _vp, _u32, _u32, _vp],
+    "ck_ntt_forward_raw": [_vp, _vp, _u32, _u32p, _vp],
+    "ck_intt_inverse_raw": [_vp, _vp, _u32, _u32p, _u32p, _vp],
     "ck_bconv_table": [_vp, _vp, _u32, _u32p, _vp, _u32, _u32p, ctypes.POINTER(ctypes.c_int32), _vp],
     "ck_ew_add": [_vp, _vp, _vp, _vp, _u32, _vp],
     "ck_ew_sub": [_vp, _vp, _vp, _vp, _u32, _vp],

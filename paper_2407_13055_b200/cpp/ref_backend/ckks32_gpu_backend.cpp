@@ -152,6 +152,18 @@ Dev up(const Gpu& g, const Polynomial& p) {
   put_rows(g, p, 0, p.rows(), d.u());
   return d;
 }
+// The element-wise ops keep the reference's raw representation (ops 4-6 of
+// ck_ew_binary: its signed lazy int32 values and formulas, bit for bit), so
+// callers that compare raw rows (test_poly.cpp:41, :112) see what the CPU
+// code would have produced.
+Dev up_raw(const Gpu& g, const Polynomial& p) {
+  Dev d(g.h, (size_t)p.rows() * p.n());
+  if (p.rows()) {
+    check(ck_memcpy_h2d(g.h, d.u(), p.row(0), (size_t)p.rows() * p.n() * 4, nullptr));
+    check(ck_stream_sync(g.h, nullptr));
+  }
+  return d;
+}
 // device rows -> p (rows are contiguous in the pool buffer)
 void get_rows(const Gpu& g, const uint32_t* src, Polynomial& p, uint32_t first, uint32_t count) {
   if (!count) return;
@@ -279,40 +291,35 @@ using namespace ck32gpu;
 // ============================================================ kernel level ==
 // NttPlan::forward_row / inverse_row (ntt.hpp:71-73): one row through the GPU.
 void NttPlan::forward_row(int32_t* row, uint32_t gidx) const {
-  const auto& basis = *tables().basis;
-  Gpu& g = for_basis(basis);
+  // the reference's raw representation end to end (ck_ntt_forward_raw: its
+  // signed lazy butterflies, bit for bit -- test_ntt.cpp:203-227 compares
+  // raw rows with forward_row_serial)
+  Gpu& g = for_basis(*tables().basis);
   Dev d(g.h, g.n);
-  std::vector<uint32_t> t(g.n);
-  const uint32_t q = basis.prime(gidx).q;
-  for (uint32_t j = 0; j < g.n; ++j) t[j] = canon(row[j], q);
-  check(ck_memcpy_h2d(g.h, d.u(), t.data(), g.n * 4, nullptr));
-  check(ck_ntt_forward(g.h, d.u(), 1, &gidx, nullptr));
+  check(ck_memcpy_h2d(g.h, d.u(), row, g.n * 4, nullptr));
+  check(ck_ntt_forward_raw(g.h, reinterpret_cast<int32_t*>(d.u()), 1, &gidx, nullptr));
   check(ck_memcpy_d2h(g.h, row, d.u(), g.n * 4, nullptr));
   check(ck_stream_sync(g.h, nullptr));
 }
 
 void NttPlan::inverse_row(int32_t* row, uint32_t gidx, const uint32_t* epilogue_mont) const {
-  const auto& basis = *tables().basis;
-  Gpu& g = for_basis(basis);
+  Gpu& g = for_basis(*tables().basis);
   Dev d(g.h, g.n);
-  std::vector<uint32_t> t(g.n);
-  const uint32_t q = basis.prime(gidx).q;
-  for (uint32_t j = 0; j < g.n; ++j) t[j] = canon(row[j], q);
-  check(ck_memcpy_h2d(g.h, d.u(), t.data(), g.n * 4, nullptr));
-  check(ck_intt_inverse(g.h, d.u(), 1, &gidx, epilogue_mont, nullptr));
+  check(ck_memcpy_h2d(g.h, d.u(), row, g.n * 4, nullptr));
+  check(ck_intt_inverse_raw(g.h, reinterpret_cast<int32_t*>(d.u()), 1, &gidx, epilogue_mont, nullptr));
   check(ck_memcpy_d2h(g.h, row, d.u(), g.n * 4, nullptr));
   check(ck_stream_sync(g.h, nullptr));
 }
 
-// ntt_forward / intt_inverse (ntt.cpp:288-312): whole polynomial, one launch
+// ntt_forward / intt_inverse (ntt.cpp:288-312): whole polynomial, raw representation
 void ntt_forward(Polynomial& p, const NttPlan& plan) {
   if (p.domain() != Domain::Coefficient) throw std::invalid_argument("ntt_forward expects coefficient domain");
   if (p.mont()) throw std::invalid_argument("ntt_forward expects plain form (entry merge)");
   Gpu& g = for_basis(*plan.tables().basis);
-  Dev d = up(g, p);
+  Dev d = up_raw(g, p);
   std::vector<uint32_t> gi(p.rows());
   for (uint32_t i = 0; i < p.rows(); ++i) gi[i] = p.global_prime_index(i);
-  check(ck_ntt_forward(g.h, d.u(), p.rows(), gi.data(), nullptr));
+  check(ck_ntt_forward_raw(g.h, reinterpret_cast<int32_t*>(d.u()), p.rows(), gi.data(), nullptr));
   get_rows(g, d.u(), p, 0, p.rows());
   p.set_domain(Domain::Evaluation);
   p.set_mont(true);
@@ -322,10 +329,10 @@ void intt_inverse(Polynomial& p, const NttPlan& plan) {
   if (p.domain() != Domain::Evaluation) throw std::invalid_argument("intt_inverse expects evaluation domain");
   if (!p.mont()) throw std::invalid_argument("intt_inverse expects Montgomery form");
   Gpu& g = for_basis(*plan.tables().basis);
-  Dev d = up(g, p);
+  Dev d = up_raw(g, p);
   std::vector<uint32_t> gi(p.rows());
   for (uint32_t i = 0; i < p.rows(); ++i) gi[i] = p.global_prime_index(i);
-  check(ck_intt_inverse(g.h, d.u(), p.rows(), gi.data(), nullptr, nullptr));
+  check(ck_intt_inverse_raw(g.h, reinterpret_cast<int32_t*>(d.u()), p.rows(), gi.data(), nullptr, nullptr));
   get_rows(g, d.u(), p, 0, p.rows());
   p.set_domain(Domain::Coefficient);
   p.set_mont(false);
@@ -426,18 +433,6 @@ void apply_automorphism_inplace(Polynomial& p, const AutomorphismMap& map) {
 
 // element-wise (poly.cpp:121-205)
 namespace {
-// The element-wise ops keep the reference's raw representation (ops 4-6 of
-// ck_ew_binary: its signed lazy int32 values and formulas, bit for bit), so
-// callers that compare raw rows (test_poly.cpp:41, :112) see what the CPU
-// code would have produced.
-Dev up_raw(const Gpu& g, const Polynomial& p) {
-  Dev d(g.h, (size_t)p.rows() * p.n());
-  if (p.rows()) {
-    check(ck_memcpy_h2d(g.h, d.u(), p.row(0), (size_t)p.rows() * p.n() * 4, nullptr));
-    check(ck_stream_sync(g.h, nullptr));
-  }
-  return d;
-}
 Polynomial ew(int op, const Polynomial& a, const Polynomial& b, BufferPool* pool, bool mont_out) {
   check_binary(a, b);
   Gpu& g = for_basis(*a.basis());

@@ -458,6 +458,28 @@ struct Context {
     up(td, d_twist_dec);
     up(jidx, d_jidx);
   }
+  // NttPrimeTable constants of every prime for the raw-representation NTT
+  // (ntt.cpp:124-131: r2 = 2^64, fwd1_r2 = psi^{n/2} R^2, exit_x = n^-1,
+  // exit_y = psi^{-n/2} n^-1), uploaded on first use
+  Blob raw_consts;
+  bool raw_ready = false;
+  const RawNttConst* raw_const() {
+    if (!raw_ready) {
+      std::vector<RawNttConst> v(primes.size());
+      for (size_t g = 0; g < primes.size(); ++g) {
+        const uint32_t qq = primes[g], R = r_mod(qq), r2 = mulm(R, R, qq);
+        const uint32_t ph = (uint32_t)pow_mod(psi[g], n / 2, qq), ninv = invm(n % qq, qq);
+        v[g].r2 = (int32_t)r2;
+        v[g].fwd1_r2 = (int32_t)mulm(ph, r2, qq);
+        v[g].exit_x = (int32_t)ninv;
+        v[g].exit_y = (int32_t)mulm(invm(ph, qq), ninv, qq);
+      }
+      raw_consts.add(v);
+      raw_consts.upload();
+      raw_ready = true;
+    }
+    return raw_consts.at<RawNttConst>(0);
+  }
   // CRT constants of the first cnt primes (multi-precision, ckks.cpp:337-346),
   // uploaded once per prefix length
   const CrtConst* crt_const(uint32_t cnt) {
@@ -2184,6 +2206,51 @@ ck_status ck_ntt_forward(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, con
     check_launch();
     c->counters[2] += rows;
   });
+}
+
+static ck_status ntt_raw_impl(ck_context* ctx, int32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
+                              const uint32_t* epilogue_mont, int inverse, ck_stream stream) {
+  return guard([&] {
+    CK_RANGE("ck_ntt_raw");
+    Context* c = C(ctx);
+    check_ptr(rows_dev);
+    if (!gidx && rows) throw InvalidArgument("null prime index list");
+    if (!rows) return;
+    std::vector<uint16_t> g16(rows);
+    std::vector<uint32_t> epi(epilogue_mont ? rows : 0);
+    for (uint32_t i = 0; i < rows; ++i) {
+      if (gidx[i] >= c->primes.size()) throw InvalidArgument("prime index out of range");
+      g16[i] = (uint16_t)gidx[i];
+      if (epilogue_mont) epi[i] = epilogue_mont[i];
+    }
+    const RawNttConst* rc = c->raw_const();
+    cudaStream_t st = S(stream);
+    char* tmp = nullptr;  // stream-ordered: the per-call prime / epilogue lists
+    const size_t bytes = rows * 2 + 16 + epi.size() * 4;
+    CK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), bytes, st));
+    CK_CUDA(cudaMemcpyAsync(tmp, g16.data(), rows * 2, cudaMemcpyHostToDevice, st));
+    uint32_t* depi = nullptr;
+    if (!epi.empty()) {
+      depi = reinterpret_cast<uint32_t*>(tmp + ((rows * 2 + 15) & ~size_t(15)));
+      CK_CUDA(cudaMemcpyAsync(depi, epi.data(), epi.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    ntt_raw((int)c->n, (int)c->logn, (int)rows, inverse, rows_dev, reinterpret_cast<const uint16_t*>(tmp), c->d_primes,
+            rc, inverse ? c->d_inv : c->d_fwd, depi, st);
+    CK_CUDA(cudaStreamSynchronize(st));  // the host lists are staged from pageable memory
+    CK_CUDA(cudaFreeAsync(tmp, st));
+    c->launches += c->logn;
+    c->counters[inverse ? 3 : 2] += rows;
+    check_launch();
+  });
+}
+
+ck_status ck_ntt_forward_raw(ck_context* ctx, int32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
+                             ck_stream stream) {
+  return ntt_raw_impl(ctx, rows_dev, rows, gidx, nullptr, 0, stream);
+}
+ck_status ck_intt_inverse_raw(ck_context* ctx, int32_t* rows_dev, uint32_t rows, const uint32_t* gidx,
+                              const uint32_t* epilogue_mont, ck_stream stream) {
+  return ntt_raw_impl(ctx, rows_dev, rows, gidx, epilogue_mont, 1, stream);
 }
 
 ck_status ck_intt_inverse(ck_context* ctx, uint32_t* rows_dev, uint32_t rows, const uint32_t* gidx,

@@ -138,6 +138,14 @@ void enc_scatter(int n, const double2* slots, int count, const uint32_t* jidx, d
 // scale = scale_mant * 2^scale_exp: the reference's long double scale (64-bit significand)
 void enc_round(int n, const double2* a, const double2* twist, unsigned long long scale_mant, int scale_exp, int rows,
                const uint32_t* row_q, uint32_t* out, cudaStream_t st);
+// the reference's NTT in its raw representation (ntt_raw.cu): per-prime
+// constants of its NttPrimeTable (ntt.cpp:124-131) as signed int32
+struct RawNttConst {
+  int32_t r2 = 0, fwd1_r2 = 0, exit_x = 0, exit_y = 0;
+};
+void ntt_raw(int n, int logn, int rows, int inverse, int32_t* d, const uint16_t* gidx, const PrimeDev* primes,
+             const RawNttConst* rc, const uint2* tw, const uint32_t* epi, cudaStream_t st);
+
 // decode's scale as an exact rational num / den (32-bit limbs, little endian):
 // the coefficient is then the correctly rounded double of v * den / num, as
 // the reference's static_cast<double>(Rational(v) / scale) (ckks.cpp:353)

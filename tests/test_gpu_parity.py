@@ -965,3 +965,86 @@ def test_ew_raw_representation_matches_reference_formulas(level, p_rows):
              C.stream())
     c32 = np.where(consts >= 1 << 31, consts - (1 << 32), consts)[:, None]
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.int64), mred(x * c32))
+
+
+@pytest.mark.parametrize("n,level", [(64, 3), (1024, 8)])
+def test_ntt_raw_representation_matches_reference_serial(n, level):
+    """ck_ntt_forward_raw / ck_intt_inverse_raw: the reference's serial NTT in
+    its raw signed lazy representation (ntt.cpp:15-96, forward_row_serial /
+    inverse_row_serial), restated here in numpy stage by stage with the
+    reference's table (ntt.cpp:100-135) -- equal int32 for int32, and the
+    inverse with an epilogue constant canonical."""
+    from paper_2407_13055_b200 import _native as nat
+
+    C = ctx_for(n, 8, 3, 55)
+    logn = n.bit_length() - 1
+    g = list(range(level))
+    rng = np.random.default_rng(n + level)
+
+    def brev(i):
+        return int(format(i, f"0{logn}b")[::-1], 2)
+
+    def mred(v, q, m):  # modarith.hpp:20-29, int64 numpy
+        hi = v >> 32
+        t = ((v & 0xFFFFFFFF) * m) & 0xFFFFFFFF
+        t = np.where(t >= 1 << 31, t - (1 << 32), t)
+        return hi - ((t * q) >> 32)
+
+    def narrow(v, b):
+        return np.where(v >= b, v - b, np.where(v <= -b, v + b, v))
+
+    def find_root_2n(q):  # modarith.cpp:30-40: first g >= 2 whose cofactor power has order 2n
+        cof = (q - 1) // (2 * n)
+        for gg in range(2, q):
+            cand = pow(gg, cof, q)
+            if pow(cand, n, q) == q - 1:
+                return cand
+
+    x0 = np.stack([rng.integers(-int(C.primes[i]) + 1, int(C.primes[i]), n) for i in g]).astype(np.int64)
+    want_f, want_i = [], []
+    epi = [int(rng.integers(1, int(C.primes[i]))) for i in g]
+    for r, gi in enumerate(g):
+        q = int(C.primes[gi]); m = pow(q, -1, 1 << 32); R = (1 << 32) % q; r2 = R * R % q
+        psi = find_root_2n(q)
+        pw = [pow(psi, k, q) for k in range(n)]
+        pwi = [pow(psi, -k, q) for k in range(n)]
+        fwd = [0] + [pw[brev(i)] * R % q for i in range(1, n)]
+        inv = [0] + [pwi[brev(i)] * R % q for i in range(1, n)]
+        fwd1_r2 = pw[n // 2] * R % q * R % q
+        ninv = pow(n, -1, q)
+        exit_x, exit_y = ninv, pwi[n // 2] * ninv % q
+        a = x0[r].copy()
+        for s in range(logn):  # fwd_stages, one stage at a time (forward_row_serial)
+            mm, t = 1 << s, n >> (s + 1)
+            for gg in range(mm):
+                w = fwd1_r2 if s == 0 else fwd[mm + gg]
+                xs = a[2 * gg * t:2 * gg * t + t].copy()
+                ys = mred(a[2 * gg * t + t:2 * gg * t + 2 * t] * w, q, m)
+                if s == 0:
+                    xs = mred(xs * r2, q, m)
+                u, v = narrow(xs + ys, 2 * q), narrow(xs - ys, 2 * q)
+                if s == logn - 1:
+                    u, v = narrow(u, q), narrow(v, q)
+                a[2 * gg * t:2 * gg * t + t], a[2 * gg * t + t:2 * gg * t + 2 * t] = u, v
+        want_f.append(a.copy())
+        for s in range(logn):  # inv_stages (inverse_row_serial) with the epilogue
+            mm, t = n >> (1 + s), 1 << s
+            for gg in range(mm):
+                xs = a[2 * gg * t:2 * gg * t + t].copy()
+                ys = a[2 * gg * t + t:2 * gg * t + 2 * t].copy()
+                u, v2 = xs + ys, xs - ys
+                if mm == 1:
+                    a0, a1 = mred(u * exit_x, q, m), mred(v2 * exit_y, q, m)
+                    a0, a1 = mred(a0 * epi[r], q, m), mred(a1 * epi[r], q, m)
+                    a0, a1 = np.where(a0 < 0, a0 + q, a0), np.where(a1 < 0, a1 + q, a1)
+                    a[2 * gg * t:2 * gg * t + t], a[2 * gg * t + t:2 * gg * t + 2 * t] = a0, a1
+                else:
+                    a[2 * gg * t:2 * gg * t + t] = narrow(u, 2 * q)
+                    a[2 * gg * t + t:2 * gg * t + 2 * t] = mred(v2 * inv[mm + gg], q, m)
+        want_i.append(a.copy())
+    d = torch.from_numpy(x0.astype(np.int32)).cuda()
+    garr = nat.u32_array(g)
+    nat.call("ck_ntt_forward_raw", C.handle, d.data_ptr(), level, garr, C.stream())
+    np.testing.assert_array_equal(d.cpu().numpy().astype(np.int64), np.stack(want_f))
+    nat.call("ck_intt_inverse_raw", C.handle, d.data_ptr(), level, garr, nat.u32_array(epi), C.stream())
+    np.testing.assert_array_equal(d.cpu().numpy().astype(np.int64), np.stack(want_i))
