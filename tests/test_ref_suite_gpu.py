@@ -19,7 +19,8 @@ raw representation (ck_ew_binary ops 4-6, ck_ew_mul_const_raw,
 ck_ntt_forward_raw / ck_intt_inverse_raw: its signed lazy formulas, bit for
 bit), while the mechanisms (mod_up ... hrot) run the canonical fast path.
 Acceptance criterion 10
-drives the reference's bench CLI, which needs CLI11 (absent, out of scope).
+drives the reference's bench CLI, built here against the same backend with a
+CLI11 subset shim (oracle/shim/CLI11.hpp).
 """
 from __future__ import annotations
 
@@ -59,8 +60,14 @@ def test_reference_unit_suite_on_the_gpu():
 
 
 def test_reference_acceptance_criteria_on_the_gpu():
-    r = _run(BIN / "acceptance_gpu", "/nonexistent-bench-cli", timeout=1500)
+    """acceptance_main.cpp, all 10 criteria; criterion 10 drives the
+    reference's own benchmark CLI (tools/bench_main.cpp, built against the GPU
+    backend with the CLI11 subset of oracle/shim): NTT and BConv design-space
+    sweeps whose every point is validated bit-exact against the default plan."""
+    cli = BIN / "ckks32_bench_gpu"
+    if not cli.exists():
+        pytest.skip("ckks32_bench_gpu not built (needs /root/reference at build time)")
+    r = _run(BIN / "acceptance_gpu", str(cli), timeout=1500)
     res = dict((int(i), st) for st, i in re.findall(r"^\[(PASS|FAIL)\]\s+(\d+)\.", r.stdout, re.M))
     assert set(res) == set(range(1, 11)), r.stdout[-3000:] + r.stderr[-3000:]
-    assert all(res[i] == "PASS" for i in range(1, 10)), r.stdout
-    assert res[10] == "FAIL"  # the reference's bench CLI (CLI11) is not built
+    assert all(res[i] == "PASS" for i in range(1, 11)), r.stdout[-4000:] + r.stderr[-2000:]
