@@ -43,9 +43,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=32, help="ciphertexts per GPU per step")
+    ap.add_argument("--batch", type=int, default=48, help="ciphertexts per GPU per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--streams", type=int, default=2, help="concurrent sub-batches (CUDA streams) per GPU")
+    ap.add_argument("--streams", type=int, default=3, help="concurrent sub-batches (CUDA streams) per GPU")
     ap.add_argument("--split", choices=["batch", "ops"], default="batch",
                     help="2-stream schedule: 'batch' = each stream runs HMult then HRot on half the batch; 'ops' = "
                          "one stream runs HMult, the other HRot, each on the whole batch")
