@@ -37,7 +37,7 @@ constexpr int phase_start(int k, int p) {
 
 template <int K1, int K2>
 struct Shape {
-  static constexpr int N1 = 1 << K1, N2 = 1 << K2, LOGN = K1 + K2;
+  static constexpr int N1 = 1 << K1, N2 = 1 << K2;
   static constexpr int N = N1 * N2;
   static constexpr int TC = cmax(1, cmin(N2, kTile / N1));  // columns per pass-1 tile
   static constexpr int TCP = TC + (TC >= 16 ? 1 : 0);        // padded smem row stride

@@ -311,7 +311,6 @@ struct ColBuf {
   uint4 tile[256 * (kCCols / 4)];  // [row][quad], 32 KB
   uint2 tw[256];                   // the prime's first 256 twiddle pairs
 };
-constexpr int kColSmem = 2 * sizeof(ColBuf);
 
 __device__ __forceinline__ void col_prefetch(ColBuf& B, const uint32_t* g, const uint2* tw) {
   // 256 rows x 128 B + 2 KB of twiddles, 16 B per cp.async
@@ -618,8 +617,8 @@ __global__ void __launch_bounds__(kCT, 5) k_col_tma(const RowJob* __restrict__ j
         nP = primes[nJ.prime];
       }
       ct_stages16<0, 0x5>(v, [&](int t, int blk) { return TW[(16 << t) + (tau << t) + blk]; }, q, q2, q4);
-#pragma unroll
       if (!(dbg & 1)) {
+#pragma unroll
         for (int j = 0; j < 16; ++j) stg4(out + (16 * tau + j) * kR, v[j]);
       } else {  // keep the result live without a store
         uint32_t acc = 0;
@@ -670,8 +669,8 @@ __global__ void __launch_bounds__(kCT, 5) k_col_tma(const RowJob* __restrict__ j
         CK_X(x) CK_X(y) CK_X(z) CK_X(w)
 #undef CK_X
       }
-#pragma unroll
       if (!(dbg & 1)) {
+#pragma unroll
         for (int j = 0; j < 16; ++j) stg4(out + (tau + 16 * j) * kR, v[j]);
       } else {
         uint32_t acc = 0;
@@ -704,16 +703,6 @@ constexpr int kRowStride = 336;  // element c at c + 4*(c>>4): conflict-free for
 __device__ __forceinline__ int rpos(int c) { return c + 4 * (c >> 4); }
 constexpr int kRowBufWords = kRRows * kRowStride;
 constexpr int kRowSmem = 2 * kRowBufWords * 4 + kRRows * kR * 8;
-
-__device__ __forceinline__ void row_prefetch(uint32_t* buf, const uint32_t* g) {
-  // kRRows rows x 256 words contiguous, 16 B per cp.async
-#pragma unroll
-  for (int k = 0; k < kRRows * 64 / kRT; ++k) {
-    const int e = threadIdx.x + k * kRT;
-    const int r = e >> 6, c = (e & 63) * 4;
-    cp16(buf + r * kRowStride + rpos(c), g + r * kR + c);
-  }
-}
 
 // the two rows (2 warp, 2 warp + 1) of a kRRows x 256 tile that warp `warp` owns
 __device__ __forceinline__ void row_prefetch_warp(uint32_t* buf, const uint32_t* g, int warp, int lane) {
@@ -776,7 +765,7 @@ __global__ void __launch_bounds__(kRT) k_row(const RowJob* __restrict__ jobs, co
                                              uint64_t src_bs, uint32_t* __restrict__ dst, uint64_t dst_bs, int batch,
                                              int njobs, const PrimeDev* __restrict__ primes,
                                              const uint2* __restrict__ tw2, CombineArgs cb = CombineArgs{}) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
   uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * kRowBufWords * 4);  // [kRRows][256]
   const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15;
@@ -1202,7 +1191,7 @@ __device__ __forceinline__ int msw(int r) { return r ^ ((r >> 4) & 3); }
 
 template <int SC>
 __global__ void __launch_bounds__(256, 1) k_conv_mid(ConvMidLaunch a) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   uint4* srct = reinterpret_cast<uint4*>(smraw);                 // [SC][256][2]
   uint4* stg = srct + SC * 512 + (threadIdx.x >> 5) * 512;       // per-warp [256][2]
   const ConvMidGroup G = a.groups[blockIdx.y];
@@ -1353,7 +1342,7 @@ constexpr int kKSmem = 2 * kKBuf * 4 + kRRows * kR * 8;
 // critical path (prefetch.global.L2: no registers, no shared memory).
 template <bool EARLY = false, int MINB = 1, bool ALLD = false, bool WL = false, bool L2PF = false>
 __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, const uint2* __restrict__ tw2) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
   uint2* tws = reinterpret_cast<uint2*>(smraw + (ALLD ? 3 : 2) * kKBuf * 4);
   const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15;
@@ -1581,7 +1570,7 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult(KeyMultLaunch a, cons
 // (3 tile buffers + the row tile's twiddles per CTA).
 template <int MINB>
 __global__ void __launch_bounds__(kKT, MINB) k_row_keymult_pf(KeyMultLaunch a, const uint2* __restrict__ tw2) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
   uint2* tws = reinterpret_cast<uint2*>(smraw + 3 * kKBuf * 4);
   const int tid = threadIdx.x, rho = tid >> 4, tau = tid & 15;
@@ -1793,7 +1782,7 @@ constexpr int kK8Smem = kK8SmemBase + kK8Rows * 256 * 8;  // + inverse twiddles 
 // digit's row pass (the first digit's at the item start).
 template <int MINB, bool EARLY = true, int KPF = 0, int DD = 0>
 __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, const uint2* __restrict__ fwd) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);                          // [3][4][288]
   uint2* tws = reinterpret_cast<uint2*>(smraw + 3 * kK8Rows * kK8Stride * 4);   // [4][256] forward, [4][256] inverse
@@ -2256,7 +2245,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
 constexpr int kK8bSmem = (3 * kK8Rows * kK8Stride) * 4 + 258 * 8 + 3 * 2 * 256 * 4;
 template <int MINB>
 __global__ void __launch_bounds__(128, MINB) k_row_keymult8b(KeyMultLaunch a, const uint2* __restrict__ fwd) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);                         // [3][4][288] per-warp ext rows
   // [255] row twiddles (shared), one entry past a 16-B boundary so that the
@@ -2468,7 +2457,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8b(KeyMultLaunch a, co
 // (job, row tile) and reused for the batch.
 template <bool INV, int COMB = 0>
 __global__ void __launch_bounds__(128, 8) k_row8(NttLaunch a, CombineArgs cb) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t* lines = reinterpret_cast<uint32_t*>(smraw) + warp * 2 * kK8Stride;  // this warp's 2 input buffers
   uint2* T = reinterpret_cast<uint2*>(smraw + kK8Rows * 2 * kK8Stride * 4) + warp * 256;
@@ -2925,7 +2914,7 @@ __global__ void __launch_bounds__(kRT) k_rowx(const RowJob* __restrict__ jobs, c
                                               int njobs, const PrimeDev* __restrict__ primes,
                                               const uint2* __restrict__ tw2) {
   using G = RowX<LOGR>;
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(smraw);
   uint2* tws = reinterpret_cast<uint2*>(smraw + 2 * G::BUF * 4);  // [RPC][R]
   const int tid = threadIdx.x, rho = tid / G::TPR, tau = tid % G::TPR, warp = tid >> 5, lane = tid & 31;
