@@ -591,7 +591,7 @@ def main():
     # ---- config 2: HRot over every level (batch B) and a batch sweep at four levels
     sweep = grid = None
     if not args.no_sweep:
-        Xbig = X.data.repeat(max(1, 128 // B), 1, 1, 1) if B < 128 else X.data  # up to B = 128
+        Xbig = X.data.repeat(-(-128 // B), 1, 1, 1)[:max(128, B)] if B < 128 else X.data  # up to B = 128
 
         def hrot_rate(Bs, lv, reps=3):
             Xl = ckks.Ciphertext(Xbig[:Bs, :, :lv].contiguous(), s, lv)
