@@ -45,6 +45,12 @@ def test_device_line_contract():
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert "int_pipe" in d["roofline_ntt"]
+    assert d["bit_exact"] is True
+    pc = e["pcie_ceiling"]  # the box's own link ceiling for this step's bytes
+    assert pc["copy_only_ms_per_step"] > 0 and 0 < pc["frac"] <= 1.1
+    nt = d["config1_ntt_roundtrip"]  # config 1's NTT / INTT round trip through the C ABI
+    assert nt["roundtrip_exact"] is True and nt["fwd"]["GBps"] > 0 and nt["inv"]["GBps"] > 0
+    assert {"config4_limb_n131072", "config5_helr"} <= set(d)
 
 
 def _row_keymult_bytes(n, level, alpha, batch, fold):
