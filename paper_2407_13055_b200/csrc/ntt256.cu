@@ -1769,6 +1769,10 @@ __global__ void __launch_bounds__(kKT, MINB) k_row_keymult_pf(KeyMultLaunch a, c
 // natural per-row order T_r[2^s - 1 + B] = F[(256 << s) + (r << s) + B]
 // (the reference's forward table, ntt.cpp:124-128), staged once per
 // (prime, row tile) and reused for every batch item.
+#ifndef CK32_KM_LAZY
+#define CK32_KM_LAZY 1
+#endif
+constexpr bool kKmLazy = CK32_KM_LAZY;  // keymult8 (KPF 0): MAC inputs in [0, 8q), one canonicalisation of the output
 constexpr int kK8Rows = 4;                       // rows per CTA (one per warp)
 constexpr int kK8Stride = 288;                   // 256 + 32 padding words
 __device__ __forceinline__ int pad8(int c) { return c + 4 * (c >> 5); }
@@ -1793,6 +1797,7 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
   constexpr int kTiles = kR / kK8Rows;
   // KPF 7 (the MACs after all digits' row passes) is instantiated per digit count
   const int Dn = (KPF == 7 && DD > 0) ? DD : a.D;
+  constexpr bool LAZY = KPF == 0 && kKmLazy;  // the default variant (D <= 3 by construction of keymult8's dispatch)
   const int rows = a.level + a.alpha, B = a.batch;
   const uint32_t LA = (uint32_t)(a.L + a.alpha);
   const int items = rows * kTiles * B;  // (row i, tile, b), b fastest
@@ -2015,8 +2020,13 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
             else ctl<false>(v[j], v[j + d], w.x, w.y, q, q2, q4);
           }
         }
+        // LAZY: v stays in [0, 8q) for the MACs (the D <= 3 products + fold sum
+        // below 25 q^2, so the Montgomery reduction lands in (0, 4.2 q) and the
+        // output is canonicalised once instead of every digit's input)
+        if (!LAZY || a.ts) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = canon8(v[j], q, q2, q4);
+          for (int j = 0; j < 8; ++j) v[j] = canon8(v[j], q, q2, q4);
+        }
       }
       if constexpr (KPF == 7) {
 #pragma unroll
@@ -2207,6 +2217,19 @@ __global__ void __launch_bounds__(128, MINB) k_row_keymult8(KeyMultLaunch a, con
     } else {
       uint32_t* o0 = a.v + b * a.v_bs + (size_t)i * kN + rofs;
       uint32_t* o1 = a.v + b * a.v_bs + (size_t)(rows + i) * kN + rofs;
+      if (LAZY) {  // (0, 4.2 q) -> [0, q)
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          uint32_t r0[4], r1[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            r0[c] = canon8(mont_reduce64s((uint32_t)s0[4 * m + c], (uint32_t)(s0[4 * m + c] >> 32), q, P.qinv), q, q2, q4);
+            r1[c] = canon8(mont_reduce64s((uint32_t)s1[4 * m + c], (uint32_t)(s1[4 * m + c] >> 32), q, P.qinv), q, q2, q4);
+          }
+          stg4(o0 + 4 * m, make_uint4(r0[0], r0[1], r0[2], r0[3]));
+          stg4(o1 + 4 * m, make_uint4(r1[0], r1[1], r1[2], r1[3]));
+        }
+      } else
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         stg4(o0 + 4 * m, make_uint4(sub_if(mont_reduce64s((uint32_t)(s0[4 * m]), (uint32_t)((s0[4 * m]) >> 32), q, P.qinv), q),
