@@ -38,6 +38,10 @@ namespace {
 
 constexpr int kTT = 128;   // threads = coefficients per tile (UMMA M)
 constexpr int kNst = 4;    // raw-tile ring depth
+#ifndef CK32_TC2_FAST3
+#define CK32_TC2_FAST3 1
+#endif
+constexpr bool kTc2Fast3 = CK32_TC2_FAST3;  // k_bconv_tc2: straight-line epilogue for 24 consecutive-row destinations
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -464,6 +468,21 @@ __global__ void __launch_bounds__(kTT) k_bconv_tc2(BconvLaunch a, BconvTc t, int
     uint32_t r[2][32];
     tmem_ld32_nowait(lane_addr, r[0]);
     tmem_wait_ld(r[0]);
+    if (kTc2Fast3 && dc > 16 && dc <= 24 && n == 65536 && dcont[0] && dcont[1]) {
+      // the common shapes (ModUp digits / ModDown at level 24: 24 destination rows,
+      // the merged HMult drop-and-divide: 22) as three straight-line 8-row blocks,
+      // the first two runs of consecutive rows: no per-block branches
+      tmem_ld32_nowait(lane_addr + 32, r[1]);
+      tc2_store8<true, 65536>(r[0], dq, doff, 8, dthr);
+      tmem_wait_ld(r[1]);
+      tmem_ld32_nowait(lane_addr + 64, r[0]);
+      tc2_store8<true, 65536>(r[1], dq + 8, doff + 8, 8, dthr);
+      tmem_wait_ld(r[0]);
+      if (dc == 24 && dcont[2])
+        tc2_store8<true, 65536>(r[0], dq + 16, doff + 16, 8, dthr);
+      else
+        tc2_store8<false>(r[0], dq + 16, doff + 16, dc - 16, dthr);
+    } else
 #pragma unroll 1
     for (int i8 = 0; i8 < dc; i8 += 16) {  // two 8-row blocks per trip: buffer 0, then buffer 1
 #pragma unroll
