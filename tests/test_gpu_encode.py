@@ -147,3 +147,28 @@ def test_decode_bit_exact_at_rescaled_and_multiword_scales(ref, level, num, den)
     pt = ckks.Plaintext(ckks.Polynomial(torch.from_numpy(rows.astype(np.int64).astype(np.int32)).cuda(), level, 0),
                         Fraction(num, den), level)
     np.testing.assert_array_equal(ckks.decode(C, pt), want)
+
+
+def test_decode_rational_argument_errors():
+    """ck_decode_rational rejects a zero numerator / denominator and more than
+    8 words per side (CK_ERR_ARG -> ValueError, as the reference's decode
+    throws std::invalid_argument for a bad scale)."""
+    import ctypes
+    from paper_2407_13055_b200 import _native as nat
+
+    n, l, a, level = 1024, 8, 3, 4
+    C = ctx_for(n, l, a)
+    rows = torch.zeros((level, n), dtype=torch.int32, device="cuda")
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+
+    def call(num, den):
+        nat.call("ck_decode_rational", C.handle, rows.data_ptr(), level, ctypes.c_double(40.0), nat.u32_array(num),
+                 len(num), nat.u32_array(den), len(den), out.data_ptr(), C.stream())
+
+    call([1 << 20], [1])  # valid
+    with pytest.raises(ValueError):
+        call([0], [1])
+    with pytest.raises(ValueError):
+        call([1], [0, 0])
+    with pytest.raises(ValueError):
+        call([1] * 9, [1])
