@@ -1048,3 +1048,20 @@ def test_ntt_raw_representation_matches_reference_serial(n, level):
     np.testing.assert_array_equal(d.cpu().numpy().astype(np.int64), np.stack(want_f))
     nat.call("ck_intt_inverse_raw", C.handle, d.data_ptr(), level, garr, nat.u32_array(epi), C.stream())
     np.testing.assert_array_equal(d.cpu().numpy().astype(np.int64), np.stack(want_i))
+
+
+def test_raw_entry_points_argument_errors():
+    """The raw-representation entry points validate like the rest of the ABI:
+    a prime index past the basis, a null prime list with rows, and an
+    element-wise op code outside 0-2 / 4-6 raise ValueError."""
+    from paper_2407_13055_b200 import _native as nat
+
+    C = ctx_for(1024, 8, 3, 55)
+    d = torch.zeros((2, 1024), dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        nat.call("ck_ntt_forward_raw", C.handle, d.data_ptr(), 2, nat.u32_array([0, 99]), C.stream())
+    with pytest.raises(ValueError):
+        nat.call("ck_intt_inverse_raw", C.handle, d.data_ptr(), 2, None, None, C.stream())
+    for op in (3, 7, -1):
+        with pytest.raises(ValueError):
+            nat.call("ck_ew_binary", C.handle, op, d.data_ptr(), d.data_ptr(), d.data_ptr(), 2, 0, C.stream())
